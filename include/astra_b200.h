@@ -1,0 +1,185 @@
+/*
+ * astra_b200.h — C-ABI of the B200-native ASTRA classifier hot path.
+ *
+ * The reference (xcmix, pure Python/NumPy) has no FFI for this path: its
+ * boundary is the Python call surface listed in SURVEY.md §8(b). Each entry
+ * point below replaces the numeric core of one of those Python functions;
+ * the Python mirror in paper_2409_20156_b200/ binds them with ctypes and
+ * keeps the reference signatures, argument meanings and error classes.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers owned by the caller, row-major,
+ *     unless stated otherwise. `stream` is a cudaStream_t passed as void*
+ *     (NULL = legacy default stream). Calls are stream-ordered and never
+ *     synchronise the host, except the *_sync helpers.
+ *   - Status codes mirror xcmix.errors (errors.py:10-21), which the reference
+ *     CLI maps to exit codes 2/3/4 (cli.py:91-105):
+ *       0 ok, 2 ConfigError, 3 DataError, 4 NumericalError, 5 CUDA failure.
+ *     astra_last_error() returns the message of the last failing call on the
+ *     calling host thread.
+ *   - Label ids are int32 (L < 2^31, which covers the 120M-label config).
+ *   - "Key" = packed uint64 ordering used by every top-k in this library:
+ *       key = (monotone_u32(score + 0.0f) << 32) | (0xFFFFFFFF - label_id)
+ *     so the larger key is the higher score, ties toward the lower id — the
+ *     reference's deterministic order (anns.py:103-109, anns.py:112-133).
+ *     Key 0 marks an empty slot.
+ */
+#ifndef ASTRA_B200_H
+#define ASTRA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASTRA_OK 0
+#define ASTRA_ERR_CONFIG 2    /* xcmix.errors.ConfigError    */
+#define ASTRA_ERR_DATA 3      /* xcmix.errors.DataError      */
+#define ASTRA_ERR_NUMERICAL 4 /* xcmix.errors.NumericalError */
+#define ASTRA_ERR_CUDA 5      /* CUDA runtime failure        */
+
+/* Slot origin codes, loss.py:27-30; IMP is the importance-sampled extension. */
+#define ASTRA_ORIGIN_POS 0
+#define ASTRA_ORIGIN_HARD 1
+#define ASTRA_ORIGIN_RAND 2
+#define ASTRA_ORIGIN_PAD 3
+#define ASTRA_ORIGIN_IMP 4
+
+/* Refresh score modes. */
+#define ASTRA_REFRESH_FP32_EXACT 0  /* SIMT fmaf, fixed k order: bit-exact ids    */
+#define ASTRA_REFRESH_BF16 1        /* tcgen05 bf16 GEMM + top-k epilogue         */
+#define ASTRA_REFRESH_BF16_RERANK 2 /* bf16 top-k' then fp32-exact re-rank to k   */
+
+/* Classifier storage / optimizer. */
+#define ASTRA_W_FP32 0
+#define ASTRA_W_BF16 1
+#define ASTRA_OPT_SGD 0  /* classifiers.py:75-82: w <- w - lr*(g + wd*w)            */
+#define ASTRA_OPT_ADAM 1 /* lazy sparse Adam (torch.optim.SparseAdam semantics)    */
+
+/* Device status words written by astra_slate_step (int32[ASTRA_STATUS_WORDS]). */
+#define ASTRA_STATUS_WORDS 4
+#define ASTRA_STATUS_NONFINITE_GRAD 0     /* a touched row's gradient is non-finite */
+#define ASTRA_STATUS_NONFINITE_GRAD_EMB 1 /* grad_emb is non-finite                  */
+#define ASTRA_STATUS_BOUND_UNSAFE 2       /* overflow bound tripped -> checked path  */
+#define ASTRA_STATUS_ID_RANGE 3           /* an id fell outside [0, n_labels_total)  */
+
+const char* astra_version(void);
+const char* astra_last_error(void);
+/* Fills SM count and compute capability of the current device. */
+int astra_device_info(int* sm_count, int* cc_major, int* cc_minor);
+/* Number of kernels this library launched on the calling process (all threads). */
+uint64_t astra_launch_count(void);
+
+/* fp32 -> bf16 (round-to-nearest-even), n elements. Used for W/query snapshots. */
+int astra_f32_to_bf16(const float* src, uint16_t* dst, int64_t n, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Shortlist refresh — replaces the exact branch of
+ *   retrieve_hard_negatives(index, embeddings, positives, k_h)   anns.py:233-256
+ * including the positive mask (anns.py:254-255) and _batched_topk
+ * (anns.py:112-133). Per query: the k largest scores over the label shard
+ * [label_offset, label_offset + n_labels) excluding the query's positives,
+ * descending, ties toward the lower id. Scores never reach HBM.
+ *
+ *   queries_f32   nq x d   fp32 (FP32_EXACT, BF16_RERANK; may be NULL for BF16
+ *                          if queries_bf16 is given)
+ *   queries_bf16  nq x d   bf16 bits, or NULL (converted into the workspace)
+ *   labels_f32    n_labels x d fp32 snapshot (FP32_EXACT, BF16_RERANK)
+ *   labels_bf16   n_labels x d bf16 snapshot (BF16, BF16_RERANK)
+ *   pos_indptr    nq+1 int64, pos_ids int32 GLOBAL ids sorted ascending per row
+ *   out_keys      nq x k packed keys (input of astra_topk_merge), or NULL
+ *   out_ids       nq x k int32 global ids, or NULL
+ *   out_scores    nq x k fp32 scores (fp32-exact in modes 0/2), or NULL
+ * A query with fewer than k admissible labels in the shard is padded with
+ * key 0 / id -1 / score -inf (the cross-shard merge then fills it).
+ * Constraints: 1 <= k <= 2048; BF16 modes need d % 64 == 0.
+ * ------------------------------------------------------------------------ */
+size_t astra_refresh_workspace_size(int64_t nq, int64_t n_labels, int d, int k, int mode);
+int astra_refresh_topk(const float* queries_f32, const uint16_t* queries_bf16, int64_t nq, int d,
+                       const float* labels_f32, const uint16_t* labels_bf16, int64_t n_labels,
+                       int64_t label_offset, const int64_t* pos_indptr, const int32_t* pos_ids,
+                       int k, int mode, uint64_t* out_keys, int32_t* out_ids, float* out_scores,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* Merge n_parts partial top-k lists per query (layout [n_parts][nq][k_in],
+ * e.g. an all-gather over label shards) into the global top-k_out. Exact:
+ * the result equals a single-shard refresh over the union of the shards. */
+int astra_topk_merge(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in, int k_out,
+                     uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Negative-mixture sampler — replaces _assemble_batch_slates
+ * (trainer.py:262-318) / assemble_slate (sampler.py:146-186) with a
+ * counter-based Philox4x32-10 stream keyed by (seed, epoch, step, row, slot).
+ * Slot layout per row (S = k_p + k_h + k_i + k_r):
+ *   [0, k_p)            positives: uniform k_p-subset in random order; rows with
+ *                       fewer positives are padded by uniform non-positive labels
+ *                       (trainer.py:273-290). origin POS / PAD, y = 1 / 0.
+ *   [k_p, +k_h)         hard: hard[b, 0:k_h] verbatim (trainer.py:295-298), y = 0.
+ *   [.., +k_i)          importance (extension): draws from cand[b, 0:n_c] with
+ *                       probabilities cand_q; weight 1/(k_i q); origin IMP.
+ *   [.., +k_r)          uniform with replacement over [L] \ C, C = hard (+cand),
+ *                       rank->id map over sorted C (trainer.py:300-306),
+ *                       weight (L-|C|)/k_r (trainer.py:315-317),
+ *                       y = id in positives (trainer.py:309).
+ * Outputs are B x S (ids int32, y int8, origin int8, weights fp32).
+ * hard rows must hold distinct ids; cand rows distinct and disjoint from hard.
+ * ------------------------------------------------------------------------ */
+int astra_sample_slates(uint64_t seed, uint32_t epoch, uint32_t step, const int64_t* rows, int B,
+                        const int64_t* pos_indptr, const int32_t* pos_ids, const int32_t* hard,
+                        int hard_stride, int k_h, const int32_t* cand, const float* cand_q,
+                        int cand_stride, int n_c, int k_i, int64_t n_labels, int k_p, int k_r,
+                        int32_t* ids, int8_t* y, int8_t* origin, float* weights, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Sampled BCE forward/backward fused with the sparse row update — replaces
+ * the classifier half of _batch_forward_backward (trainer.py:366-394) and
+ * apply_classifier_updates_arrays (classifiers.py:75-82).
+ *   emb        B x d fp32  embeddings AFTER dropout (emb_used, trainer.py:343-348)
+ *   keep       B x d fp32  dropout keep scale or NULL (grad_emb *= keep, :383-384)
+ *   ids/y      B x S       slates (global ids)
+ *   origin     origin_row_stride = 0: one S-vector shared by every row (the
+ *              reference's row-0 origin, trainer.py:313); = S: per-row origin
+ *   weights    weights_row_stride = 0 (S-vector) or S (per-row)
+ *   factors_in B x S fp32 or NULL: if given, skip the score/factor stage and
+ *              use these d(loss)/d(score) factors (parity tests feed the
+ *              reference's factors to check the update bit-for-bit)
+ *   W          n_labels_local x d (fp32 or bf16); slots whose id falls outside
+ *              [label_offset, label_offset + n_labels_local) belong to another
+ *              shard and are skipped (label-range sharding)
+ *   adam_m/v   n_labels_local x d fp32 (ASTRA_OPT_ADAM) or NULL
+ *   grad_emb   B x d fp32 out (partial over this shard's slots)
+ *   loss_out   1 fp64 out: sum of this shard's slate loss terms (fp64)
+ *   status     int32[ASTRA_STATUS_WORDS] out (zeroed by the call)
+ * Semantics: every id present in the slate is updated once (dead/pad slots
+ * included, so they receive weight decay), gradients sum duplicates in
+ * ascending flat (b*S+s) order, W is updated only if every touched row's
+ * gradient and grad_emb are finite (the reference raises before writing).
+ * ------------------------------------------------------------------------ */
+size_t astra_step_workspace_size(int B, int S, int d, int64_t n_labels_local);
+int astra_slate_step(const float* emb, const float* keep, const int32_t* ids, const int8_t* y,
+                     const int8_t* origin, int64_t origin_row_stride, const float* weights,
+                     int64_t weights_row_stride, const float* factors_in, int B, int S, int d,
+                     void* W, int w_dtype, float* adam_m, float* adam_v, int optimizer,
+                     int64_t n_labels_local, int64_t label_offset, float lr, float weight_decay,
+                     float adam_beta1, float adam_beta2, float adam_eps, int64_t adam_step,
+                     float* grad_emb, double* loss_out, int32_t* status, float* factors_out,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* apply_classifier_updates_arrays(bank, ids, grads, lr, wd)  classifiers.py:75-82
+ * ids (U, unique, local row index) and grads (U x d) on device. Raises
+ * NumericalError semantics: nothing is written if any gradient is
+ * non-finite (status[0] = 1, return 0 — the caller syncs and raises). */
+int astra_apply_updates(void* W, int w_dtype, int64_t n_labels, int d, const int64_t* ids,
+                        const float* grads, int64_t U, float lr, float weight_decay,
+                        int32_t* status, void* stream);
+
+/* Synchronous helper: cudaStreamSynchronize + error mapping. */
+int astra_stream_sync(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASTRA_B200_H */
