@@ -1,0 +1,141 @@
+// capi.cu — the extern "C" boundary (include/astra_b200.h) and host helpers.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <atomic>
+
+#include "common.cuh"
+#include "topk.cuh"
+
+namespace astra {
+
+static thread_local char g_err[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return ASTRA_OK;
+  return set_error(ASTRA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int num_sms() {
+  static thread_local int dev_cached = -1, sms_cached = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != dev_cached) {
+    cudaDeviceGetAttribute(&sms_cached, cudaDevAttrMultiProcessorCount, dev);
+    dev_cached = dev;
+    if (sms_cached <= 0) sms_cached = 148;
+  }
+  return sms_cached;
+}
+
+// defined in the kernel translation units
+int f32_to_bf16(const float*, uint16_t*, int64_t, cudaStream_t);
+size_t refresh_workspace_size(int64_t, int64_t, int, int, int);
+int refresh_topk(const float*, const uint16_t*, int64_t, int, const float*, const uint16_t*, int64_t, int64_t,
+                 const int64_t*, const int32_t*, int, int, uint64_t*, int32_t*, float*, void*, size_t, cudaStream_t);
+int topk_merge(const uint64_t*, int64_t, int, int, int, uint64_t*, int32_t*, float*, uint64_t*, cudaStream_t);
+int sample_slates(uint64_t, uint32_t, uint32_t, const int64_t*, int, const int64_t*, const int32_t*, const int32_t*,
+                  int, int, const int32_t*, const float*, int, int, int, int64_t, int, int, int32_t*, int8_t*,
+                  int8_t*, float*, cudaStream_t);
+size_t step_workspace_size(int, int, int, int64_t);
+int slate_step(const float*, const float*, const int32_t*, const int8_t*, const int8_t*, int64_t, const float*,
+               int64_t, const float*, int, int, int, void*, int, float*, float*, int, int64_t, int64_t, float, float,
+               float, float, float, int64_t, float*, double*, int32_t*, float*, void*, size_t, cudaStream_t);
+int apply_updates(void*, int, int64_t, int, const int64_t*, const float*, int64_t, float, float, int32_t*,
+                  cudaStream_t);
+
+}  // namespace astra
+
+using namespace astra;
+
+static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+const char* astra_version(void) { return "astra-b200 0.1 (sm_100a)"; }
+const char* astra_last_error(void) { return g_err; }
+uint64_t astra_launch_count(void) { return g_launches.load(); }
+
+int astra_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  ASTRA_TRY(check_cuda(cudaGetDevice(&dev), "cudaGetDevice"));
+  if (sm_count) ASTRA_TRY(check_cuda(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev), "attr"));
+  if (cc_major) ASTRA_TRY(check_cuda(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev), "attr"));
+  if (cc_minor) ASTRA_TRY(check_cuda(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev), "attr"));
+  return ASTRA_OK;
+}
+
+int astra_f32_to_bf16(const float* src, uint16_t* dst, int64_t n, void* stream) {
+  return f32_to_bf16(src, dst, n, S(stream));
+}
+
+size_t astra_refresh_workspace_size(int64_t nq, int64_t n_labels, int d, int k, int mode) {
+  return refresh_workspace_size(nq, n_labels, d, k, mode);
+}
+
+int astra_refresh_topk(const float* queries_f32, const uint16_t* queries_bf16, int64_t nq, int d,
+                       const float* labels_f32, const uint16_t* labels_bf16, int64_t n_labels, int64_t label_offset,
+                       const int64_t* pos_indptr, const int32_t* pos_ids, int k, int mode, uint64_t* out_keys,
+                       int32_t* out_ids, float* out_scores, void* workspace, size_t workspace_bytes, void* stream) {
+  return refresh_topk(queries_f32, queries_bf16, nq, d, labels_f32, labels_bf16, n_labels, label_offset, pos_indptr,
+                      pos_ids, k, mode, out_keys, out_ids, out_scores, workspace, workspace_bytes, S(stream));
+}
+
+size_t astra_merge_workspace_size(int64_t nq, int k_out) {
+  return static_cast<size_t>(nq) * topk_cap(k_out) * sizeof(uint64_t);
+}
+
+int astra_topk_merge(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in, int k_out, uint64_t* out_keys,
+                     int32_t* out_ids, float* out_scores, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_parts < 1 || k_in < 1 || k_out < 1 || k_out > 2048) return set_error(ASTRA_ERR_CONFIG, "merge: bad sizes");
+  if (!workspace || workspace_bytes < astra_merge_workspace_size(nq, k_out))
+    return set_error(ASTRA_ERR_CONFIG, "merge workspace too small");
+  return topk_merge(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores,
+                    static_cast<uint64_t*>(workspace), S(stream));
+}
+
+int astra_sample_slates(uint64_t seed, uint32_t epoch, uint32_t step, const int64_t* rows, int B,
+                        const int64_t* pos_indptr, const int32_t* pos_ids, const int32_t* hard, int hard_stride,
+                        int k_h, const int32_t* cand, const float* cand_q, int cand_stride, int n_c, int k_i,
+                        int64_t n_labels, int k_p, int k_r, int32_t* ids, int8_t* y, int8_t* origin, float* weights,
+                        void* stream) {
+  return sample_slates(seed, epoch, step, rows, B, pos_indptr, pos_ids, hard, hard_stride, k_h, cand, cand_q,
+                       cand_stride, n_c, k_i, n_labels, k_p, k_r, ids, y, origin, weights, S(stream));
+}
+
+size_t astra_step_workspace_size(int B, int S_, int d, int64_t n_labels_local) {
+  return step_workspace_size(B, S_, d, n_labels_local);
+}
+
+int astra_slate_step(const float* emb, const float* keep, const int32_t* ids, const int8_t* y, const int8_t* origin,
+                     int64_t origin_row_stride, const float* weights, int64_t weights_row_stride,
+                     const float* factors_in, int B, int S_, int d, void* W, int w_dtype, float* adam_m,
+                     float* adam_v, int optimizer, int64_t n_labels_local, int64_t label_offset, float lr,
+                     float weight_decay, float adam_beta1, float adam_beta2, float adam_eps, int64_t adam_step,
+                     float* grad_emb, double* loss_out, int32_t* status, float* factors_out, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  return slate_step(emb, keep, ids, y, origin, origin_row_stride, weights, weights_row_stride, factors_in, B, S_, d,
+                    W, w_dtype, adam_m, adam_v, optimizer, n_labels_local, label_offset, lr, weight_decay,
+                    adam_beta1, adam_beta2, adam_eps, adam_step, grad_emb, loss_out, status, factors_out, workspace,
+                    workspace_bytes, S(stream));
+}
+
+int astra_apply_updates(void* W, int w_dtype, int64_t n_labels, int d, const int64_t* ids, const float* grads,
+                        int64_t U, float lr, float weight_decay, int32_t* status, void* stream) {
+  return apply_updates(W, w_dtype, n_labels, d, ids, grads, U, lr, weight_decay, status, S(stream));
+}
+
+int astra_stream_sync(void* stream) { return check_cuda(cudaStreamSynchronize(S(stream)), "stream sync"); }
+
+}  // extern "C"

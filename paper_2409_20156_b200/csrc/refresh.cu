@@ -1,0 +1,380 @@
+// refresh.cu — shortlist refresh orchestration, the fp32-exact SIMT path,
+// cross-partition merge and the fp32 re-rank.
+//
+// Replaces the exact branch of retrieve_hard_negatives (anns.py:233-256):
+// scores = E @ W^T (anns.py:253), positives masked (anns.py:254-255), top-k
+// by (score desc, id asc) (anns.py:112-133). The score matrix is never
+// materialised: each CTA streams a label range for a 128-query tile and keeps
+// per-query running top-k lists (topk.cuh).
+//
+// Modes (include/astra_b200.h):
+//   FP32_EXACT  SIMT FFMA tile kernel here; every score is the sequential
+//               fmaf chain over t = 0..d-1, so ids are bit-identical to
+//               oracle_refresh_fp32.
+//   BF16        tcgen05 kernel (refresh_tc.cu), bf16 operands, fp32 accum.
+//   BF16_RERANK tcgen05 top-k' (k' = 2k) then the k' candidates are re-scored
+//               with the same sequential fmaf chain and re-ranked: equal to
+//               FP32_EXACT whenever the exact top-k lies inside the top-k'.
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "topk.cuh"
+
+namespace astra {
+
+// refresh_tc.cu
+int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb, int64_t L, int64_t label_offset,
+                      const int64_t* pos_indptr, const int32_t* pos_ids, int k, int cap, int n_parts,
+                      uint64_t* bufs, uint64_t* part_keys, cudaStream_t st);
+int refresh_tc_parts(int64_t nq, int64_t L);
+
+namespace {
+
+constexpr int kBM = 128, kBN = 128, kBK = 8;
+constexpr int kSimtThreads = 256;
+
+// ------------------------------------------------------------- fp32 SIMT
+
+struct SimtArgs {
+  const float* Q;
+  const float* W;
+  int64_t nq, L, off;
+  int d, k, cap, n_parts;
+  int64_t labels_per_part;
+  const int64_t* pos_indptr;
+  const int32_t* pos_ids;
+  uint64_t* bufs;       // [n_qtiles * n_parts * 128][cap]
+  uint64_t* part_keys;  // [n_parts][nq][k]
+};
+
+constexpr size_t kSimtSmem = sizeof(float) * (2 * kBK * kBM + 2 * kBK * kBN + kBM * (kBN + 1));
+
+__global__ void __launch_bounds__(kSimtThreads) refresh_simt_kernel(SimtArgs a) {
+  extern __shared__ __align__(16) float dsm[];
+  float(*As)[kBK][kBM] = reinterpret_cast<float(*)[kBK][kBM]>(dsm);
+  float(*Bs)[kBK][kBN] = reinterpret_cast<float(*)[kBK][kBN]>(dsm + 2 * kBK * kBM);
+  float(*sc)[kBN + 1] = reinterpret_cast<float(*)[kBN + 1]>(dsm + 2 * kBK * kBM + 2 * kBK * kBN);
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int qt = blockIdx.x, part = blockIdx.y;
+  const int64_t q0 = static_cast<int64_t>(qt) * kBM;
+  const int64_t l_begin = static_cast<int64_t>(part) * a.labels_per_part;
+  const int64_t l_end = std::min<int64_t>(a.L, l_begin + a.labels_per_part);
+
+  // epilogue lane state (threads 0..127 own query rows)
+  LaneTopK t;
+  const bool row_owner = tid < kBM;
+  const int64_t q = q0 + tid;
+  const bool active = row_owner && q < a.nq;
+  if (row_owner) {
+    uint64_t* buf = a.bufs + ((static_cast<size_t>(qt) * a.n_parts + part) * kBM + tid) * a.cap;
+    const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
+    lane_init(t, buf, a.pos_ids + p0, p1 - p0);
+  }
+
+  // loader mapping: 128 rows x 8 k per tile = 1024 floats, 4 per thread
+  const int lrow = tid >> 1, lk = (tid & 1) * 4;
+  for (int64_t lt = l_begin; lt < l_end; lt += kBN) {
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    const int nkt = (a.d + kBK - 1) / kBK;
+    auto load = [&](int kt, int buf) {
+      const int kk = kt * kBK + lk;
+      const int64_t qr = q0 + lrow, lr = lt + lrow;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kc = kk + u;
+        As[buf][lk + u][lrow] = (qr < a.nq && kc < a.d) ? a.Q[qr * a.d + kc] : 0.0f;
+        Bs[buf][lk + u][lrow] = (lr < l_end && kc < a.d) ? a.W[lr * a.d + kc] : 0.0f;
+      }
+    };
+    load(0, 0);
+    __syncthreads();
+    for (int kt = 0; kt < nkt; ++kt) {
+      const int cur = kt & 1;
+      if (kt + 1 < nkt) load(kt + 1, cur ^ 1);
+#pragma unroll
+      for (int kk = 0; kk < kBK; ++kk) {
+        float av[8], bv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) av[i] = As[cur][kk][ty * 8 + i];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bv[j] = Bs[cur][kk][tx * 8 + j];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sc[ty * 8 + i][tx * 8 + j] = acc[i][j];
+    __syncthreads();
+    if (row_owner) {
+      const int nl = static_cast<int>(std::min<int64_t>(kBN, l_end - lt));
+      for (int c0 = 0; c0 < kBN; c0 += 32) {
+        topk_reserve(t, 32, a.cap, a.k, active);
+        if (active) {
+          const int cn = std::min(32, nl - c0);
+          for (int c = 0; c < cn; ++c)
+            lane_offer(t, sc[tid][c0 + c], static_cast<uint32_t>(lt + c0 + c + a.off));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (row_owner) {
+    uint64_t* out = a.part_keys + (static_cast<size_t>(part) * a.nq + (active ? q : 0)) * a.k;
+    topk_flush(t, a.cap, a.k, active, out);
+  }
+}
+
+// ------------------------------------------------------------- merge
+
+// One thread per query: offer the n_parts partial lists (layout [part][nq][k_in])
+// and keep the best k_out. Keys already exclude positives.
+__global__ void __launch_bounds__(128) merge_kernel(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in,
+                                                    int k_out, int cap, uint64_t* bufs, uint64_t* out_keys,
+                                                    int32_t* out_ids, float* out_scores) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
+  const bool active = q < nq;
+  LaneTopK t;
+  lane_init(t, bufs + static_cast<size_t>(active ? q : 0) * cap, nullptr, 0);
+  for (int p = 0; p < n_parts; ++p) {
+    const uint64_t* src = part_keys + (static_cast<size_t>(p) * nq + (active ? q : 0)) * k_in;
+    for (int c0 = 0; c0 < k_in; c0 += 32) {
+      topk_reserve(t, 32, cap, k_out, active);
+      if (active) {
+        const int cn = std::min(32, k_in - c0);
+        for (int c = 0; c < cn; ++c) {
+          uint64_t key = src[c0 + c];
+          if (key) lane_offer_key(t, key);
+        }
+      }
+    }
+  }
+  // flush into the buffer itself (rows are private), then decode
+  topk_flush(t, cap, k_out, active, t.buf);
+  if (active) {
+    for (int j = 0; j < k_out; ++j) {
+      uint64_t key = t.buf[j];
+      if (out_keys) out_keys[q * k_out + j] = key;
+      if (out_ids) out_ids[q * k_out + j] = key ? key_id(key) : -1;
+      if (out_scores) out_scores[q * k_out + j] = key ? key_score(key) : -INFINITY;
+    }
+  }
+}
+
+// ------------------------------------------------------------- fp32 re-rank
+
+// Block per query: re-score the k' candidates with the sequential fmaf chain
+// (the FP32_EXACT order), sort the keys descending in shared memory, keep k.
+__global__ void __launch_bounds__(128) rerank_kernel(const float* Q, const float* W, int d, int64_t off,
+                                                     const uint64_t* cand, int kc, int k, uint64_t* out_keys,
+                                                     int32_t* out_ids, float* out_scores) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t q = blockIdx.x;
+  int Pn = 1;
+  while (Pn < kc) Pn <<= 1;
+  float* qs = reinterpret_cast<float*>(smem);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem + align_up(sizeof(float) * d, 16));
+  for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = Q[q * d + t];
+  __syncthreads();
+  for (int c = threadIdx.x; c < Pn; c += blockDim.x) {
+    uint64_t key = 0;
+    if (c < kc) {
+      uint64_t ck = cand[q * kc + c];
+      if (ck) {
+        const int32_t gid = key_id(ck);
+        const float* w = W + static_cast<size_t>(gid - off) * d;
+        float s = 0.0f;
+        int t = 0;
+        if ((d & 3) == 0) {
+          for (; t < d; t += 4) {
+            float4 wv = __ldg(reinterpret_cast<const float4*>(w + t));
+            s = fmaf(qs[t], wv.x, s);
+            s = fmaf(qs[t + 1], wv.y, s);
+            s = fmaf(qs[t + 2], wv.z, s);
+            s = fmaf(qs[t + 3], wv.w, s);
+          }
+        }
+        for (; t < d; ++t) s = fmaf(qs[t], w[t], s);
+        key = make_key(s, static_cast<uint32_t>(gid));
+      }
+    }
+    keys[c] = key;
+  }
+  __syncthreads();
+  for (int size = 2; size <= Pn; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < Pn; i += blockDim.x) {
+        int j = i ^ stride;
+        if (j > i) {
+          const bool desc = (i & size) == 0;
+          uint64_t x = keys[i], z = keys[j];
+          if ((x < z) == desc) {
+            keys[i] = z;
+            keys[j] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    uint64_t key = keys[j];
+    if (out_keys) out_keys[q * k + j] = key;
+    if (out_ids) out_ids[q * k + j] = key ? key_id(key) : -1;
+    if (out_scores) out_scores[q * k + j] = key ? key_score(key) : -INFINITY;
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* src, uint16_t* dst, int64_t n) {
+  const int64_t i0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * 4;
+  for (int64_t i = i0; i < n; i += stride) {
+    if (i + 4 <= n && (reinterpret_cast<uintptr_t>(src + i) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst + i) & 7) == 0) {
+      float4 v = *reinterpret_cast<const float4*>(src + i);
+      uint2 o;
+      o.x = static_cast<uint32_t>(f32_to_bf16_bits(v.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(v.y)) << 16);
+      o.y = static_cast<uint32_t>(f32_to_bf16_bits(v.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(v.w)) << 16);
+      *reinterpret_cast<uint2*>(dst + i) = o;
+    } else {
+      for (int64_t j = i; j < n && j < i + 4; ++j) dst[j] = f32_to_bf16_bits(src[j]);
+    }
+  }
+}
+
+struct RefreshWs {
+  uint16_t* qb;
+  uint64_t* bufs;
+  uint64_t* part_keys;
+  uint64_t* merge_bufs;
+  uint64_t* cand;
+};
+
+int simt_parts(int64_t nq, int64_t L) {
+  const int64_t qtiles = (nq + kBM - 1) / kBM;
+  int64_t parts = std::max<int64_t>(1, (2LL * num_sms() + qtiles - 1) / qtiles);
+  parts = std::min<int64_t>(parts, std::max<int64_t>(1, (L + kBN - 1) / kBN));
+  return static_cast<int>(parts);
+}
+
+size_t carve_refresh(void* base, size_t cap_bytes, int64_t nq, int64_t L, int d, int k, int mode, RefreshWs* w,
+                     int* n_parts_out, int* kk_out) {
+  Carve c(base, cap_bytes);
+  const int kk = mode == ASTRA_REFRESH_BF16_RERANK ? 2 * k : k;  // candidates per query before re-rank
+  const int cap = topk_cap(kk);
+  const int n_parts = mode == ASTRA_REFRESH_FP32_EXACT ? simt_parts(nq, L) : refresh_tc_parts(nq, L);
+  const int64_t qtiles = (nq + 127) / 128;
+  w->qb = mode == ASTRA_REFRESH_FP32_EXACT ? nullptr : c.take<uint16_t>(static_cast<size_t>(nq) * d);
+  w->bufs = c.take<uint64_t>(static_cast<size_t>(qtiles) * n_parts * 128 * cap);
+  w->part_keys = c.take<uint64_t>(static_cast<size_t>(n_parts) * nq * kk);
+  w->merge_bufs = c.take<uint64_t>(static_cast<size_t>(nq) * cap);
+  w->cand = mode == ASTRA_REFRESH_BF16_RERANK ? c.take<uint64_t>(static_cast<size_t>(nq) * kk) : nullptr;
+  *n_parts_out = n_parts;
+  *kk_out = kk;
+  return c.off;
+}
+
+}  // namespace
+
+int f32_to_bf16(const float* src, uint16_t* dst, int64_t n, cudaStream_t st) {
+  if (n <= 0) return ASTRA_OK;
+  const int grid = static_cast<int>(std::min<int64_t>((n / 4 + 255) / 256 + 1, 16LL * num_sms()));
+  f32_to_bf16_kernel<<<grid, 256, 0, st>>>(src, dst, n);
+  ASTRA_LAUNCHED("f32_to_bf16");
+  return ASTRA_OK;
+}
+
+size_t refresh_workspace_size(int64_t nq, int64_t L, int d, int k, int mode) {
+  RefreshWs w;
+  int np, kk;
+  return carve_refresh(nullptr, 0, nq, L, d, k, mode, &w, &np, &kk);
+}
+
+int topk_merge(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in, int k_out, uint64_t* out_keys,
+               int32_t* out_ids, float* out_scores, uint64_t* bufs, cudaStream_t st) {
+  if (nq <= 0) return ASTRA_OK;
+  const int cap = topk_cap(k_out);
+  merge_kernel<<<static_cast<unsigned>((nq + 127) / 128), 128, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, cap,
+                                                                       bufs, out_keys, out_ids, out_scores);
+  ASTRA_LAUNCHED("merge");
+  return ASTRA_OK;
+}
+
+int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, const float* wf, const uint16_t* wb,
+                 int64_t L, int64_t off, const int64_t* pos_indptr, const int32_t* pos_ids, int k, int mode,
+                 uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* ws, size_t ws_bytes,
+                 cudaStream_t st) {
+  if (k < 1 || k > 2048) return set_error(ASTRA_ERR_CONFIG, "refresh: k=%d outside [1, 2048]", k);
+  if (nq < 0 || L < 0 || d <= 0) return set_error(ASTRA_ERR_CONFIG, "refresh: bad shape");
+  if (L + off >= (int64_t(1) << 31)) return set_error(ASTRA_ERR_CONFIG, "refresh: label ids exceed int32");
+  if (mode == ASTRA_REFRESH_FP32_EXACT) {
+    if (!qf || !wf) return set_error(ASTRA_ERR_CONFIG, "FP32_EXACT needs fp32 queries and labels");
+  } else if (mode == ASTRA_REFRESH_BF16 || mode == ASTRA_REFRESH_BF16_RERANK) {
+    if (d % 64) return set_error(ASTRA_ERR_CONFIG, "bf16 refresh needs d %% 64 == 0 (d=%d)", d);
+    if (!wb) return set_error(ASTRA_ERR_CONFIG, "bf16 refresh needs the bf16 label snapshot");
+    if (!qf && !qb_in) return set_error(ASTRA_ERR_CONFIG, "bf16 refresh needs queries");
+    if (mode == ASTRA_REFRESH_BF16_RERANK && (!qf || !wf))
+      return set_error(ASTRA_ERR_CONFIG, "BF16_RERANK needs fp32 queries and labels");
+  } else {
+    return set_error(ASTRA_ERR_CONFIG, "refresh: unknown mode %d", mode);
+  }
+  RefreshWs w;
+  int n_parts, kk;
+  size_t need = carve_refresh(ws, ws_bytes, nq, L, d, k, mode, &w, &n_parts, &kk);
+  if (!ws || ws_bytes < need) return set_error(ASTRA_ERR_CONFIG, "refresh workspace too small (%zu < %zu)", ws_bytes, need);
+  if (nq == 0) return ASTRA_OK;
+  const int cap = topk_cap(kk);
+  if (mode == ASTRA_REFRESH_FP32_EXACT) {
+    SimtArgs a;
+    a.Q = qf;
+    a.W = wf;
+    a.nq = nq;
+    a.L = L;
+    a.off = off;
+    a.d = d;
+    a.k = kk;
+    a.cap = cap;
+    a.n_parts = n_parts;
+    const int64_t tiles = (L + kBN - 1) / kBN;
+    a.labels_per_part = ((tiles + n_parts - 1) / n_parts) * kBN;
+    a.pos_indptr = pos_indptr;
+    a.pos_ids = pos_ids;
+    a.bufs = w.bufs;
+    a.part_keys = w.part_keys;
+    dim3 grid(static_cast<unsigned>((nq + kBM - 1) / kBM), static_cast<unsigned>(n_parts));
+    cudaFuncSetAttribute(refresh_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSimtSmem);
+    refresh_simt_kernel<<<grid, kSimtThreads, kSimtSmem, st>>>(a);
+    ASTRA_LAUNCHED("refresh_simt");
+  } else {
+    const uint16_t* qb = qb_in;
+    if (!qb) {
+      ASTRA_TRY(f32_to_bf16(qf, w.qb, nq * d, st));
+      qb = w.qb;
+    }
+    ASTRA_TRY(launch_refresh_tc(qb, nq, d, wb, L, off, pos_indptr, pos_ids, kk, cap, n_parts, w.bufs, w.part_keys, st));
+  }
+  if (mode == ASTRA_REFRESH_BF16_RERANK) {
+    ASTRA_TRY(topk_merge(w.part_keys, nq, n_parts, kk, kk, w.cand, nullptr, nullptr, w.merge_bufs, st));
+    size_t smem = align_up(sizeof(float) * d, 16);
+    int Pn = 1;
+    while (Pn < kk) Pn <<= 1;
+    smem += sizeof(uint64_t) * Pn;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rerank_kernel<<<static_cast<unsigned>(nq), 128, smem, st>>>(qf, wf, d, off, w.cand, kk, k, out_keys, out_ids, out_scores);
+    ASTRA_LAUNCHED("rerank");
+    return ASTRA_OK;
+  }
+  return topk_merge(w.part_keys, nq, n_parts, kk, k, out_keys, out_ids, out_scores, w.merge_bufs, st);
+}
+
+}  // namespace astra

@@ -1,0 +1,345 @@
+// refresh_tc.cu — bf16 tcgen05 GEMM of queries x labels with a fused top-k
+// epilogue: the B200 shortlist refresh (replaces anns.py:253-256).
+//
+// One CTA owns a 128-query tile and sweeps a contiguous range of label tiles
+// (N = 256 labels each). Warp roles (256 threads):
+//   warp 0      TMA producer: A (128 x 64 bf16) and B (256 x 64 bf16) k-blocks,
+//               SWIZZLE_128B, into a 4-stage shared-memory ring (48 KB/stage).
+//   warp 1      MMA issuer: one elected lane issues tcgen05.mma.kind::f16
+//               (M=128, N=256, K=16) into a TMEM accumulator; tcgen05.commit
+//               releases smem stages and publishes finished accumulators.
+//   warp 2      TMEM allocator (512 columns = 2 accumulators of 256 fp32 cols).
+//   warps 4-7   epilogue: tcgen05.ld 32 columns at a time (thread = query row =
+//               TMEM lane), running top-k per query (topk.cuh). The two TMEM
+//               accumulators double-buffer the epilogue against the next MMA.
+// Scores never leave the SM; per-query partial top-k lists go to HBM once.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "topk.cuh"
+
+namespace astra {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, UMMA_K = 16, STAGES = 4;
+constexpr int A_STAGE = BM * BK * 2;  // 16 KB
+constexpr int B_STAGE = BN * BK * 2;  // 32 KB
+constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
+constexpr int TMEM_COLS = 512;
+constexpr int kThreads = 256;
+constexpr int kEpiWarp0 = 4;
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+
+// idesc for kind::f16: D=F32, A=B=BF16, both K-major, N>>3 at [17,23), M>>4 at [24,29)
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (8-row x 128 B atoms,
+// SBO = 1024 B between atoms, version 1 for sm_100).
+__device__ __forceinline__ uint64_t smem_desc(const void* p) {
+  const uint32_t a = smem_u32(p);
+  return static_cast<uint64_t>((a >> 4) & 0x3FFFu) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(2) << 61);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct TcArgs {
+  int64_t nq, L, off;
+  int d, k, cap, n_parts;
+  int64_t tiles_per_part;
+  const int64_t* pos_indptr;
+  const int32_t* pos_ids;
+  uint64_t* bufs;
+  uint64_t* part_keys;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    refresh_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, part = blockIdx.y;
+  const int64_t q0 = static_cast<int64_t>(qt) * BM;
+  const int64_t n_tiles = (a.L + BN - 1) / BN;
+  const int64_t t_begin = static_cast<int64_t>(part) * a.tiles_per_part;
+  const int64_t t_end = std::min<int64_t>(n_tiles, t_begin + a.tiles_per_part);
+  const int nkb = a.d / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = t_begin; t < t_end; ++t) {
+        const int n0 = static_cast<int>(t * BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, static_cast<int>(q0));
+          tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint64_t ad = smem_desc(sA + stage * A_STAGE);
+          const uint64_t bd = smem_desc(sB + stage * B_STAGE);
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+            // +32 B along K inside the 128 B swizzle atom = +2 in the encoded address
+            mma_bf16(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
+          }
+          mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) mma_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ---------------- epilogue: TMEM -> registers -> running top-k
+    const int row = (warp - kEpiWarp0) * 32 + lane;  // TMEM lane = query row in tile
+    const int64_t q = q0 + row;
+    const bool active = q < a.nq;
+    LaneTopK tk;
+    {
+      uint64_t* buf = a.bufs + ((static_cast<size_t>(qt) * a.n_parts + part) * BM + row) * a.cap;
+      const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
+      lane_init(tk, buf, a.pos_ids + p0, p1 - p0);
+    }
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>((warp - kEpiWarp0) * 32) << 16);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t t = t_begin; t < t_end; ++t) {
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t n0 = t * BN;
+      const int nvalid = static_cast<int>(std::min<int64_t>(BN, a.L - n0));
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        __syncwarp();
+        tmem_ld32(lane_base + static_cast<uint32_t>(acc * BN + c0), r);
+        if (c0 >= nvalid) continue;  // tile tail (uniform across the CTA)
+        // warp-level prefilter: skip the chunk if no lane can admit anything
+        float mx = __uint_as_float(r[0]);
+#pragma unroll
+        for (int j = 1; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(r[j]));
+        if (!__any_sync(0xffffffffu, active && mx >= tk.tau_s)) continue;
+        topk_reserve(tk, 32, a.cap, a.k, active);
+        if (active) {
+          const int cn = std::min(32, nvalid - c0);
+          const uint32_t g0 = static_cast<uint32_t>(n0 + c0 + a.off);
+          for (int j = 0; j < cn; ++j) lane_offer(tk, __uint_as_float(r[j]), g0 + j);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    uint64_t* out = a.part_keys + (static_cast<size_t>(part) * a.nq + (active ? q : 0)) * a.k;
+    topk_flush(tk, a.cap, a.k, active, out);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int make_map(CUtensorMap* m, const void* base, int64_t rows, int d, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return set_error(ASTRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(ASTRA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return ASTRA_OK;
+}
+
+}  // namespace
+
+int refresh_tc_parts(int64_t nq, int64_t L) {
+  const int64_t qtiles = (nq + BM - 1) / BM;
+  const int64_t n_tiles = std::max<int64_t>(1, (L + BN - 1) / BN);
+  int64_t parts = std::max<int64_t>(1, num_sms() / std::max<int64_t>(1, qtiles));
+  return static_cast<int>(std::min<int64_t>(parts, n_tiles));
+}
+
+int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb, int64_t L, int64_t label_offset,
+                      const int64_t* pos_indptr, const int32_t* pos_ids, int k, int cap, int n_parts, uint64_t* bufs,
+                      uint64_t* part_keys, cudaStream_t st) {
+  if ((reinterpret_cast<uintptr_t>(qb) & 15) || (reinterpret_cast<uintptr_t>(wb) & 15))
+    return set_error(ASTRA_ERR_CONFIG, "bf16 operands must be 16-byte aligned");
+  CUtensorMap tmA, tmB;
+  ASTRA_TRY(make_map(&tmA, qb, nq, d, BM));
+  ASTRA_TRY(make_map(&tmB, wb, std::max<int64_t>(L, 1), d, BN));
+  TcArgs a;
+  a.nq = nq;
+  a.L = L;
+  a.off = label_offset;
+  a.d = d;
+  a.k = k;
+  a.cap = cap;
+  a.n_parts = n_parts;
+  const int64_t n_tiles = (L + BN - 1) / BN;
+  a.tiles_per_part = (n_tiles + n_parts - 1) / n_parts;
+  a.pos_indptr = pos_indptr;
+  a.pos_ids = pos_ids;
+  a.bufs = bufs;
+  a.part_keys = part_keys;
+  static bool attr_set = false;
+  if (!attr_set) {
+    ASTRA_TRY(check_cuda(cudaFuncSetAttribute(refresh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(kSmemBytes)),
+                         "smem attr"));
+    attr_set = true;
+  }
+  dim3 grid(static_cast<unsigned>((nq + BM - 1) / BM), static_cast<unsigned>(n_parts));
+  refresh_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(tmA, tmB, a);
+  ASTRA_LAUNCHED("refresh_tc");
+  return ASTRA_OK;
+}
+
+}  // namespace astra

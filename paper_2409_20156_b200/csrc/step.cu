@@ -1,0 +1,871 @@
+// step.cu — sampled BCE forward/backward fused with the sparse row update.
+//
+// Replaces the classifier half of _batch_forward_backward
+// (trainer.py:366-394) and apply_classifier_updates_arrays
+// (classifiers.py:75-82). HBM-bound; the pipeline is
+//
+//   1. slot_forward   (CTA per batch row)  gather W[ids[b,s]] with 16 B vector
+//                     loads, warp-reduce dot, BCE loss terms (fp64), factors
+//                     c*(sigma-y) (trainer.py:369-380), grad_emb[b] reduced
+//                     across warps in a fixed order (trainer.py:382-384).
+//   2. finalize       fixed-order fp64 loss sum + overflow bound.
+//   3. count/scan/scatter  counting sort of the B*S slots by label
+//                     (replaces the dense L x d A^T@emb, trainer.py:390-393).
+//   4. label_update   (warp per unique label) sum f*emb in ascending b*S+s
+//                     order with separate mul/add roundings — the order scipy's
+//                     csc_matvecs uses — then the SGD/Adam row update, W read
+//                     and written once.
+// W is written only if every touched gradient and grad_emb is finite: the
+// reference raises NumericalError before writing (classifiers.py:79-80,
+// encoder.py:145-146). Step 2 proves finiteness from a bound in the common
+// case; otherwise a check pass (label_check) runs first.
+#include <limits.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace astra {
+namespace {
+
+constexpr int kFwdThreads = 256;
+constexpr int kFwdWarps = kFwdThreads / 32;
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int kUpdThreads = 256;
+constexpr double kBoundSafe = 1e37;
+
+struct FwdArgs {
+  const float* emb;
+  const float* keep;
+  const int32_t* ids;
+  const int8_t* y;
+  const int8_t* origin;
+  int64_t origin_stride;
+  const float* weights;
+  int64_t weights_stride;
+  const float* factors_in;
+  int B, S, d;
+  const void* W;
+  int64_t Lloc, off;
+  float* grad_emb;
+  float* factors;
+  double* loss_rows;
+  double* bound_rows;
+  int32_t* status;
+};
+
+__device__ __forceinline__ float expit_f32(float x) {
+  // scipy.special.expit on float32: 1 / (1 + exp(-x)) in single precision
+  return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+}
+
+__device__ __forceinline__ double softplus64(double x) {
+  // log(1 + e^x) = logaddexp(0, x) (loss.py:36-43)
+  return fmax(x, 0.0) + log1p(exp(-fabs(x)));
+}
+
+// d(loss)/d(score) and the fp64 loss term of one slot (trainer.py:369-380).
+__device__ __forceinline__ float slot_factor(const FwdArgs& a, int b, int s, float sc, double* loss_term) {
+  const int8_t o = a.origin[b * a.origin_stride + s];
+  const float yf = static_cast<float>(a.y[static_cast<size_t>(b) * a.S + s]);
+  const float w = a.weights[b * a.weights_stride + s];
+  const bool pos_slot = o == ASTRA_ORIGIN_POS;
+  const float pos_term = pos_slot ? yf : 0.0f;
+  const float neg_alive = pos_slot ? 0.0f : __fsub_rn(1.0f, yf);
+  const float sig = expit_f32(sc);
+  const float wn = __fmul_rn(w, neg_alive);
+  const double spn = softplus64(-static_cast<double>(sc));
+  *loss_term = static_cast<double>(pos_term) * spn + static_cast<double>(wn) * (spn + static_cast<double>(sc));
+  return __fadd_rn(__fmul_rn(pos_term, __fsub_rn(sig, 1.0f)), __fmul_rn(wn, sig));
+}
+
+template <bool BF16>
+__device__ __forceinline__ float4 load_w4(const void* W, size_t elem) {
+  if constexpr (BF16) {
+    uint2 u = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(W) + elem));
+    return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                       __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+  } else {
+    return __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(W) + elem));
+  }
+}
+
+// Shared tail of both forward kernels: reduce the per-warp grad_emb / loss /
+// |f| partials in warp order (deterministic) and write row b.
+__device__ void forward_tail(const FwdArgs& a, int b, float* red, double lsum, double fabs_sum, float emax) {
+  __shared__ double s_loss[kFwdWarps], s_fabs[kFwdWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  lsum = warp_sum(lsum);
+  fabs_sum = warp_sum(fabs_sum);
+  if (lane == 0) {
+    s_loss[warp] = lsum;
+    s_fabs[warp] = fabs_sum;
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int k = threadIdx.x; k < a.d; k += kFwdThreads) {
+    float g = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kFwdWarps; ++w) g += red[w * a.d + k];
+    if (a.keep) g = __fmul_rn(g, a.keep[static_cast<size_t>(b) * a.d + k]);
+    a.grad_emb[static_cast<size_t>(b) * a.d + k] = g;
+    bad |= !isfinite(g);
+  }
+  if (bad) a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] = 1;
+  if (threadIdx.x == 0) {
+    double l = 0.0, fa = 0.0;
+    for (int w = 0; w < kFwdWarps; ++w) {
+      l += s_loss[w];
+      fa += s_fabs[w];
+    }
+    a.loss_rows[b] = l;
+    a.bound_rows[b] = fa * static_cast<double>(emax);
+  }
+}
+
+// Vectorised forward: d = NV * 128, each lane owns NV float4 of the row.
+template <int NV, bool BF16>
+__global__ void __launch_bounds__(kFwdThreads) slot_forward_vec(FwdArgs a) {
+  __shared__ __align__(16) float red[kFwdWarps * NV * 128];
+  __shared__ float s_emax[kFwdWarps];
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = NV * 128;
+  float4 e[NV], g[NV];
+  float emax = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    e[i] = *reinterpret_cast<const float4*>(a.emb + static_cast<size_t>(b) * d + i * 128 + lane * 4);
+    g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    emax = fmaxf(emax, fmaxf(fmaxf(fabsf(e[i].x), fabsf(e[i].y)), fmaxf(fabsf(e[i].z), fabsf(e[i].w))));
+    if (!(isfinite(e[i].x) && isfinite(e[i].y) && isfinite(e[i].z) && isfinite(e[i].w))) emax = INFINITY;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  double lsum = 0.0, fabs_sum = 0.0;
+  const int32_t* row_ids = a.ids + static_cast<size_t>(b) * a.S;
+  // two slots in flight per warp for memory-level parallelism
+  for (int s0 = warp * 2; s0 < a.S; s0 += kFwdWarps * 2) {
+    int sl[2] = {s0, s0 + 1};
+    int64_t loc[2];
+    bool own[2];
+    float4 w[2][NV];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      own[u] = false;
+      loc[u] = 0;
+      if (sl[u] < a.S) {
+        loc[u] = static_cast<int64_t>(row_ids[sl[u]]) - a.off;
+        own[u] = loc[u] >= 0 && loc[u] < a.Lloc;
+      }
+      if (own[u]) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) w[u][i] = load_w4<BF16>(a.W, static_cast<size_t>(loc[u]) * d + i * 128 + lane * 4);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!own[u]) continue;  // warp-uniform
+      float f;
+      if (a.factors_in) {
+        f = a.factors_in[static_cast<size_t>(b) * a.S + sl[u]];
+      } else {
+        float acc = 0.0f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          acc = fmaf(w[u][i].x, e[i].x, acc);
+          acc = fmaf(w[u][i].y, e[i].y, acc);
+          acc = fmaf(w[u][i].z, e[i].z, acc);
+          acc = fmaf(w[u][i].w, e[i].w, acc);
+        }
+        acc = warp_sum(acc);
+        double lt;
+        f = slot_factor(a, b, sl[u], acc, &lt);
+        if (lane == 0) lsum += lt;
+      }
+      if (lane == 0) {
+        fabs_sum += static_cast<double>(fabsf(f));
+        if (a.factors) a.factors[static_cast<size_t>(b) * a.S + sl[u]] = f;
+      }
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        g[i].x = fmaf(f, w[u][i].x, g[i].x);
+        g[i].y = fmaf(f, w[u][i].y, g[i].y);
+        g[i].z = fmaf(f, w[u][i].z, g[i].z);
+        g[i].w = fmaf(f, w[u][i].w, g[i].w);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) *reinterpret_cast<float4*>(red + warp * d + i * 128 + lane * 4) = g[i];
+  if (lane == 0) s_emax[warp] = emax;
+  __syncthreads();
+  forward_tail(a, b, red, lsum, fabs_sum, s_emax[0]);
+}
+
+// Generic forward for any d: emb and the per-warp partials live in shared memory.
+template <bool BF16>
+__global__ void __launch_bounds__(kFwdThreads) slot_forward_generic(FwdArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  float* e = sm;                 // d
+  float* red = sm + a.d;         // kFwdWarps * d
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = a.d;
+  __shared__ float s_emax;
+  for (int k = threadIdx.x; k < d; k += kFwdThreads) e[k] = a.emb[static_cast<size_t>(b) * d + k];
+  for (int k = threadIdx.x; k < kFwdWarps * d; k += kFwdThreads) red[k] = 0.0f;
+  __syncthreads();
+  if (warp == 0) {
+    float m = 0.0f;
+    for (int k = lane; k < d; k += 32) m = isfinite(e[k]) ? fmaxf(m, fabsf(e[k])) : INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_emax = m;
+  }
+  double lsum = 0.0, fabs_sum = 0.0;
+  float* gw = red + warp * d;
+  for (int s = warp; s < a.S; s += kFwdWarps) {
+    int64_t loc = static_cast<int64_t>(a.ids[static_cast<size_t>(b) * a.S + s]) - a.off;
+    if (loc < 0 || loc >= a.Lloc) continue;
+    float f;
+    if (a.factors_in) {
+      f = a.factors_in[static_cast<size_t>(b) * a.S + s];
+    } else {
+      float acc = 0.0f;
+      for (int k = lane; k < d; k += 32) {
+        size_t el = static_cast<size_t>(loc) * d + k;
+        float wv = BF16 ? bf16_bits_to_f32(static_cast<const uint16_t*>(a.W)[el]) : static_cast<const float*>(a.W)[el];
+        acc = fmaf(wv, e[k], acc);
+      }
+      acc = warp_sum(acc);
+      double lt;
+      f = slot_factor(a, b, s, acc, &lt);
+      if (lane == 0) lsum += lt;
+    }
+    if (lane == 0) {
+      fabs_sum += static_cast<double>(fabsf(f));
+      if (a.factors) a.factors[static_cast<size_t>(b) * a.S + s] = f;
+    }
+    for (int k = lane; k < d; k += 32) {
+      size_t el = static_cast<size_t>(loc) * d + k;
+      float wv = BF16 ? bf16_bits_to_f32(static_cast<const uint16_t*>(a.W)[el]) : static_cast<const float*>(a.W)[el];
+      gw[k] = fmaf(f, wv, gw[k]);
+    }
+  }
+  __syncthreads();
+  forward_tail(a, b, red, lsum, fabs_sum, s_emax);
+}
+
+// Fixed-order fp64 sums of the per-row loss and overflow bound.
+__global__ void __launch_bounds__(1024) finalize_kernel(const double* loss_rows, const double* bound_rows, int B,
+                                                        double* loss_out, int32_t* status) {
+  __shared__ double sl[1024], sb[1024];
+  double l = 0.0, bd = 0.0;
+  for (int i = threadIdx.x; i < B; i += 1024) {
+    l += loss_rows[i];
+    bd += bound_rows[i];
+  }
+  sl[threadIdx.x] = l;
+  sb[threadIdx.x] = bd;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      sl[threadIdx.x] += sl[threadIdx.x + o];
+      sb[threadIdx.x] += sb[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *loss_out = sl[0];
+    if (!(sb[0] < kBoundSafe)) status[ASTRA_STATUS_BOUND_UNSAFE] = 1;
+  }
+}
+
+// ---------------------------------------------------------------- counting sort
+
+__global__ void count_kernel(const int32_t* ids, int64_t n, int64_t off, int64_t Lloc, uint32_t* counts,
+                             int32_t* rank, int32_t* status) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t id = ids[i];
+    if (id < 0) status[ASTRA_STATUS_ID_RANGE] = 1;
+    int64_t loc = static_cast<int64_t>(id) - off;
+    rank[i] = (loc >= 0 && loc < Lloc) ? static_cast<int32_t>(atomicAdd(counts + loc, 1u)) : -1;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* counts, int64_t Lloc,
+                                                                   uint32_t* blk_slots, uint32_t* blk_nz) {
+  __shared__ uint32_t ss[kScanThreads / 32], sn[kScanThreads / 32];
+  int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+  uint32_t s = 0, nz = 0;
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t l = base + i * kScanThreads + threadIdx.x;
+    if (l < Lloc) {
+      uint32_t c = counts[l];
+      s += c;
+      nz += c > 0;
+    }
+  }
+  s = warp_sum(s);
+  nz = warp_sum(nz);
+  if ((threadIdx.x & 31) == 0) {
+    ss[threadIdx.x >> 5] = s;
+    sn[threadIdx.x >> 5] = nz;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t a = 0, c = 0;
+    for (int w = 0; w < kScanThreads / 32; ++w) {
+      a += ss[w];
+      c += sn[w];
+    }
+    blk_slots[blockIdx.x] = a;
+    blk_nz[blockIdx.x] = c;
+  }
+}
+
+// Exclusive scan of the per-block sums (single CTA), writes U.
+__global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* blk_slots, uint32_t* blk_nz, int nb,
+                                                        uint32_t* U) {
+  __shared__ uint32_t cs[1024], cn[1024];
+  const int per = (nb + 1023) / 1024;
+  const int lo = threadIdx.x * per, hi = min(nb, lo + per);
+  uint32_t a = 0, c = 0;
+  for (int i = lo; i < hi; ++i) {
+    a += blk_slots[i];
+    c += blk_nz[i];
+  }
+  cs[threadIdx.x] = a;
+  cn[threadIdx.x] = c;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    uint32_t xa = threadIdx.x >= o ? cs[threadIdx.x - o] : 0;
+    uint32_t xc = threadIdx.x >= o ? cn[threadIdx.x - o] : 0;
+    __syncthreads();
+    cs[threadIdx.x] += xa;
+    cn[threadIdx.x] += xc;
+    __syncthreads();
+  }
+  uint32_t ra = cs[threadIdx.x] - a, rc = cn[threadIdx.x] - c;  // exclusive
+  for (int i = lo; i < hi; ++i) {
+    uint32_t va = blk_slots[i], vc = blk_nz[i];
+    blk_slots[i] = ra;
+    blk_nz[i] = rc;
+    ra += va;
+    rc += vc;
+  }
+  if (threadIdx.x == 1023) *U = cn[1023];
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* counts, int64_t Lloc,
+                                                                  const uint32_t* blk_slots,
+                                                                  const uint32_t* blk_nz, uint32_t* offsets,
+                                                                  int32_t* uniq) {
+  __shared__ uint32_t ws[kScanThreads / 32], wn[kScanThreads / 32];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + static_cast<int64_t>(threadIdx.x) * kScanItems;
+  uint32_t c[kScanItems];
+  uint32_t s = 0, nz = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t l = base + i;
+    c[i] = l < Lloc ? counts[l] : 0u;
+    s += c[i];
+    nz += c[i] > 0;
+  }
+  // block-exclusive scan of (s, nz) over threads
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t is = s, in = nz;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t xs = __shfl_up_sync(0xffffffffu, is, o), xn = __shfl_up_sync(0xffffffffu, in, o);
+    if (lane >= o) {
+      is += xs;
+      in += xn;
+    }
+  }
+  if (lane == 31) {
+    ws[warp] = is;
+    wn[warp] = in;
+  }
+  __syncthreads();
+  uint32_t ps = blk_slots[blockIdx.x], pn = blk_nz[blockIdx.x];
+  for (int w = 0; w < warp; ++w) {
+    ps += ws[w];
+    pn += wn[w];
+  }
+  ps += is - s;
+  pn += in - nz;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t l = base + i;
+    if (l < Lloc) {
+      offsets[l] = ps;
+      if (c[i]) uniq[pn++] = static_cast<int32_t>(l);
+      ps += c[i];
+    }
+  }
+}
+
+__global__ void scatter_kernel(const int32_t* ids, const int32_t* rank, int64_t n, int64_t off,
+                               const uint32_t* offsets, int32_t* perm) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t r = rank[i];
+    if (r >= 0) perm[offsets[static_cast<int64_t>(ids[i]) - off] + r] = static_cast<int32_t>(i);
+  }
+}
+
+// ---------------------------------------------------------------- label-major update
+
+struct UpdArgs {
+  const float* emb;
+  const float* factors;
+  const int32_t* uniq;
+  const uint32_t* U;
+  const uint32_t* offsets;
+  const uint32_t* counts;
+  const int32_t* perm;
+  int32_t* perm2;  // sorted segments longer than 32
+  int S, d;
+  void* W;
+  float* m;
+  float* v;
+  float lr, wd;
+  float c1, c2, eps, neg_step;  // Adam: fp32(1-b1), fp32(1-b2), eps, fp32(-lr*sqrt(bc2)/bc1)
+  int32_t* status;
+};
+
+// Sort the label's slot indices ascending. Segments <= 32 stay in a register
+// (returned); longer ones are rank-sorted into perm2.
+__device__ __forceinline__ int32_t sort_segment(const UpdArgs& a, uint32_t start, uint32_t n, int lane) {
+  if (n <= 32) {
+    int32_t v = lane < static_cast<int>(n) ? a.perm[start + lane] : INT_MAX;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        int32_t o = __shfl_xor_sync(0xffffffffu, v, stride);
+        bool up = (lane & size) == 0;
+        bool lower = (lane & stride) == 0;
+        int32_t lo = min(v, o), hi = max(v, o);
+        v = (lower == up) ? lo : hi;
+      }
+    }
+    return v;
+  }
+  for (uint32_t i = lane; i < n; i += 32) {
+    int32_t x = a.perm[start + i];
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < n; ++j) r += a.perm[start + j] < x;
+    a.perm2[start + r] = x;
+  }
+  __syncwarp();
+  return 0;
+}
+
+__device__ __forceinline__ int32_t seg_slot(const UpdArgs& a, uint32_t start, uint32_t n, int32_t reg, uint32_t j) {
+  return n <= 32 ? __shfl_sync(0xffffffffu, reg, static_cast<int>(j)) : a.perm2[start + j];
+}
+
+// One element's update: SGD (classifiers.py:82, each op rounded like NumPy)
+// or SparseAdam (torch.optim.SparseAdam op order).
+template <bool ADAM>
+__device__ __forceinline__ float upd_elem(const UpdArgs& a, float p, float g, float* mp, float* vp) {
+  if constexpr (!ADAM) {
+    return __fsub_rn(p, __fmul_rn(a.lr, __fadd_rn(g, __fmul_rn(a.wd, p))));
+  } else {
+    if (a.wd != 0.0f) g = __fadd_rn(g, __fmul_rn(a.wd, p));
+    float m0 = *mp, v0 = *vp;
+    float mu = __fmul_rn(__fsub_rn(g, m0), a.c1);
+    float vu = __fmul_rn(__fsub_rn(__fmul_rn(g, g), v0), a.c2);
+    *mp = __fadd_rn(m0, mu);
+    *vp = __fadd_rn(v0, vu);
+    float numer = __fadd_rn(mu, m0);
+    float denom = __fadd_rn(__fsqrt_rn(__fadd_rn(vu, v0)), a.eps);
+    return __fadd_rn(p, __fmul_rn(a.neg_step, __fdiv_rn(numer, denom)));
+  }
+}
+
+template <bool BF16>
+__device__ __forceinline__ float load_p(const void* W, size_t el) {
+  return BF16 ? bf16_bits_to_f32(static_cast<const uint16_t*>(W)[el]) : static_cast<const float*>(W)[el];
+}
+template <bool BF16>
+__device__ __forceinline__ void store_p(void* W, size_t el, float v) {
+  if constexpr (BF16)
+    static_cast<uint16_t*>(W)[el] = f32_to_bf16_bits(v);
+  else
+    static_cast<float*>(W)[el] = v;
+}
+
+// CHECK_ONLY: compute every gradient, flag non-finite ones, write nothing.
+template <bool BF16, bool ADAM, bool CHECK_ONLY>
+__global__ void __launch_bounds__(kUpdThreads) label_update_kernel(UpdArgs a) {
+  const int lane = threadIdx.x & 31;
+  if (CHECK_ONLY) {
+    if (!a.status[ASTRA_STATUS_BOUND_UNSAFE]) return;  // finiteness already proven
+  } else {
+    if (a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] || a.status[ASTRA_STATUS_NONFINITE_GRAD]) return;
+  }
+  const uint32_t U = *a.U;
+  const int d = a.d;
+  const uint32_t warps = gridDim.x * (kUpdThreads / 32);
+  for (uint32_t u = blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5); u < U; u += warps) {
+    const int32_t l = a.uniq[u];
+    const uint32_t start = a.offsets[l], n = a.counts[l];
+    const int32_t reg = sort_segment(a, start, n, lane);
+    bool bad = false;
+    for (int k0 = 0; k0 < d; k0 += 128) {
+      // each lane: 4 consecutive elements of this 128-wide chunk
+      const int k = k0 + lane * 4;
+      float g[4] = {0.f, 0.f, 0.f, 0.f};
+      const int nk = k < d ? min(4, d - k) : 0;
+      for (uint32_t j = 0; j < n; ++j) {
+        const int32_t slot = seg_slot(a, start, n, reg, j);
+        const float f = a.factors[slot];
+        const float* e = a.emb + static_cast<size_t>(slot / a.S) * d + k;
+        for (int t = 0; t < nk; ++t) g[t] = __fadd_rn(g[t], __fmul_rn(f, e[t]));
+      }
+      for (int t = 0; t < nk; ++t) bad |= !isfinite(g[t]);
+      if (!CHECK_ONLY) {
+        const size_t row = static_cast<size_t>(l) * d;
+        for (int t = 0; t < nk; ++t) {
+          float p = load_p<BF16>(a.W, row + k + t);
+          float np = upd_elem<ADAM>(a, p, g[t], ADAM ? a.m + row + k + t : nullptr, ADAM ? a.v + row + k + t : nullptr);
+          store_p<BF16>(a.W, row + k + t, np);
+        }
+      }
+    }
+    if (CHECK_ONLY && __any_sync(0xffffffffu, bad)) a.status[ASTRA_STATUS_NONFINITE_GRAD] = 1;
+  }
+}
+
+// Vectorised update for d % 128 == 0 (NV float4 per lane), fp32 or bf16 W.
+template <int NV, bool BF16, bool ADAM>
+__global__ void __launch_bounds__(kUpdThreads) label_update_vec(UpdArgs a) {
+  const int lane = threadIdx.x & 31;
+  if (a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] || a.status[ASTRA_STATUS_NONFINITE_GRAD]) return;
+  const uint32_t U = *a.U;
+  constexpr int d = NV * 128;
+  const uint32_t warps = gridDim.x * (kUpdThreads / 32);
+  for (uint32_t u = blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5); u < U; u += warps) {
+    const int32_t l = a.uniq[u];
+    const uint32_t start = a.offsets[l], n = a.counts[l];
+    const int32_t reg = sort_segment(a, start, n, lane);
+    const size_t row = static_cast<size_t>(l) * d;
+    // issue the row loads first; they overlap the gradient accumulation
+    float4 p[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if constexpr (BF16) {
+        uint2 q = *reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(a.W) + row + i * 128 + lane * 4);
+        p[i] = make_float4(__uint_as_float(q.x << 16), __uint_as_float(q.x & 0xFFFF0000u),
+                           __uint_as_float(q.y << 16), __uint_as_float(q.y & 0xFFFF0000u));
+      } else {
+        p[i] = *reinterpret_cast<const float4*>(static_cast<const float*>(a.W) + row + i * 128 + lane * 4);
+      }
+    }
+    float4 g[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t j = 0;
+    for (; j + 2 <= n; j += 2) {  // two occurrences' loads in flight, summed in order
+      int32_t s0 = seg_slot(a, start, n, reg, j), s1 = seg_slot(a, start, n, reg, j + 1);
+      float f0 = a.factors[s0], f1 = a.factors[s1];
+      const float* e0 = a.emb + static_cast<size_t>(s0 / a.S) * d + lane * 4;
+      const float* e1 = a.emb + static_cast<size_t>(s1 / a.S) * d + lane * 4;
+      float4 x0[NV], x1[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        x0[i] = *reinterpret_cast<const float4*>(e0 + i * 128);
+        x1[i] = *reinterpret_cast<const float4*>(e1 + i * 128);
+      }
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        g[i].x = __fadd_rn(g[i].x, __fmul_rn(f0, x0[i].x));
+        g[i].y = __fadd_rn(g[i].y, __fmul_rn(f0, x0[i].y));
+        g[i].z = __fadd_rn(g[i].z, __fmul_rn(f0, x0[i].z));
+        g[i].w = __fadd_rn(g[i].w, __fmul_rn(f0, x0[i].w));
+        g[i].x = __fadd_rn(g[i].x, __fmul_rn(f1, x1[i].x));
+        g[i].y = __fadd_rn(g[i].y, __fmul_rn(f1, x1[i].y));
+        g[i].z = __fadd_rn(g[i].z, __fmul_rn(f1, x1[i].z));
+        g[i].w = __fadd_rn(g[i].w, __fmul_rn(f1, x1[i].w));
+      }
+    }
+    if (j < n) {
+      int32_t s0 = seg_slot(a, start, n, reg, j);
+      float f0 = a.factors[s0];
+      const float* e0 = a.emb + static_cast<size_t>(s0 / a.S) * d + lane * 4;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        float4 x0 = *reinterpret_cast<const float4*>(e0 + i * 128);
+        g[i].x = __fadd_rn(g[i].x, __fmul_rn(f0, x0.x));
+        g[i].y = __fadd_rn(g[i].y, __fmul_rn(f0, x0.y));
+        g[i].z = __fadd_rn(g[i].z, __fmul_rn(f0, x0.z));
+        g[i].w = __fadd_rn(g[i].w, __fmul_rn(f0, x0.w));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const size_t el = row + i * 128 + lane * 4;
+      float4 np;
+      if constexpr (ADAM) {
+        float4 m4 = *reinterpret_cast<float4*>(a.m + el), v4 = *reinterpret_cast<float4*>(a.v + el);
+        np.x = upd_elem<true>(a, p[i].x, g[i].x, &m4.x, &v4.x);
+        np.y = upd_elem<true>(a, p[i].y, g[i].y, &m4.y, &v4.y);
+        np.z = upd_elem<true>(a, p[i].z, g[i].z, &m4.z, &v4.z);
+        np.w = upd_elem<true>(a, p[i].w, g[i].w, &m4.w, &v4.w);
+        *reinterpret_cast<float4*>(a.m + el) = m4;
+        *reinterpret_cast<float4*>(a.v + el) = v4;
+      } else {
+        np.x = upd_elem<false>(a, p[i].x, g[i].x, nullptr, nullptr);
+        np.y = upd_elem<false>(a, p[i].y, g[i].y, nullptr, nullptr);
+        np.z = upd_elem<false>(a, p[i].z, g[i].z, nullptr, nullptr);
+        np.w = upd_elem<false>(a, p[i].w, g[i].w, nullptr, nullptr);
+      }
+      if constexpr (BF16) {
+        uint2 q;
+        q.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
+        q.y = static_cast<uint32_t>(f32_to_bf16_bits(np.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.w)) << 16);
+        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(a.W) + el) = q;
+      } else {
+        *reinterpret_cast<float4*>(static_cast<float*>(a.W) + el) = np;
+      }
+    }
+  }
+}
+
+// apply_classifier_updates_arrays: explicit (ids, grads) form.
+__global__ void apply_check_kernel(const float* grads, int64_t n, int32_t* status) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    bad |= !isfinite(grads[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) status[ASTRA_STATUS_NONFINITE_GRAD] = 1;
+}
+
+template <bool BF16>
+__global__ void apply_rows_kernel(void* W, int d, const int64_t* ids, const float* grads, int64_t U, float lr,
+                                  float wd, const int32_t* status) {
+  if (status[ASTRA_STATUS_NONFINITE_GRAD]) return;
+  const int64_t n = U * d;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / d, k = i - r * d;
+    const size_t el = static_cast<size_t>(ids[r]) * d + k;
+    float p = load_p<BF16>(W, el);
+    store_p<BF16>(W, el, __fsub_rn(p, __fmul_rn(lr, __fadd_rn(grads[i], __fmul_rn(wd, p)))));
+  }
+}
+
+template <int NV, bool BF16>
+void launch_forward_vec(const FwdArgs& a, cudaStream_t st) {
+  slot_forward_vec<NV, BF16><<<a.B, kFwdThreads, 0, st>>>(a);
+}
+
+template <bool BF16, bool ADAM>
+int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
+  const int nv = a.d % 128 == 0 ? a.d / 128 : 0;
+  label_update_kernel<BF16, ADAM, true><<<max_ctas, kUpdThreads, 0, st>>>(a);
+  ASTRA_LAUNCHED("label_check");
+  switch (nv) {
+    case 1: label_update_vec<1, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
+    case 2: label_update_vec<2, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
+    case 4: label_update_vec<4, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
+    case 6: label_update_vec<6, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
+    case 8: label_update_vec<8, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
+    default: label_update_kernel<BF16, ADAM, false><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
+  }
+  ASTRA_LAUNCHED("label_update");
+  return ASTRA_OK;
+}
+
+struct StepWs {
+  float* factors;
+  int32_t* rank;
+  int32_t* perm;
+  int32_t* perm2;
+  uint32_t* counts;
+  uint32_t* offsets;
+  int32_t* uniq;
+  uint32_t* blk_slots;
+  uint32_t* blk_nz;
+  uint32_t* U;
+  double* loss_rows;
+  double* bound_rows;
+};
+
+size_t carve_step(void* base, size_t cap, int B, int S, int64_t Lloc, StepWs* w) {
+  Carve c(base, cap);
+  const int64_t n = static_cast<int64_t>(B) * S;
+  const int64_t nb = (Lloc + kScanTile - 1) / kScanTile;
+  w->factors = c.take<float>(n);
+  w->rank = c.take<int32_t>(n);
+  w->perm = c.take<int32_t>(n);
+  w->perm2 = c.take<int32_t>(n);
+  w->counts = c.take<uint32_t>(Lloc);
+  w->offsets = c.take<uint32_t>(Lloc);
+  w->uniq = c.take<int32_t>(n < Lloc ? n : Lloc);
+  w->blk_slots = c.take<uint32_t>(nb);
+  w->blk_nz = c.take<uint32_t>(nb);
+  w->U = c.take<uint32_t>(1);
+  w->loss_rows = c.take<double>(B);
+  w->bound_rows = c.take<double>(B);
+  return c.off;
+}
+
+}  // namespace
+
+size_t step_workspace_size(int B, int S, int d, int64_t Lloc) {
+  (void)d;
+  StepWs w;
+  return carve_step(nullptr, 0, B, S, Lloc, &w);
+}
+
+int slate_step(const float* emb, const float* keep, const int32_t* ids, const int8_t* y, const int8_t* origin,
+               int64_t origin_stride, const float* weights, int64_t weights_stride, const float* factors_in, int B,
+               int S, int d, void* W, int w_dtype, float* adam_m, float* adam_v, int optimizer, int64_t Lloc,
+               int64_t off, float lr, float wd, float b1, float b2, float eps, int64_t adam_step, float* grad_emb,
+               double* loss_out, int32_t* status, float* factors_out, void* workspace, size_t ws_bytes,
+               cudaStream_t st) {
+  if (B < 0 || S < 0 || d <= 0 || Lloc < 0) return set_error(ASTRA_ERR_CONFIG, "slate_step: bad shape");
+  if (Lloc >= (int64_t(1) << 31) || static_cast<int64_t>(B) * S >= (int64_t(1) << 31))
+    return set_error(ASTRA_ERR_CONFIG, "slate_step: shard too large for 32-bit slot indices");
+  if (w_dtype != ASTRA_W_FP32 && w_dtype != ASTRA_W_BF16) return set_error(ASTRA_ERR_CONFIG, "bad w_dtype");
+  if (optimizer == ASTRA_OPT_ADAM && (!adam_m || !adam_v))
+    return set_error(ASTRA_ERR_CONFIG, "Adam needs moment buffers");
+  StepWs w;
+  size_t need = carve_step(workspace, ws_bytes, B, S, Lloc, &w);
+  if (!workspace || ws_bytes < need) return set_error(ASTRA_ERR_CONFIG, "step workspace too small (%zu < %zu)", ws_bytes, need);
+  ASTRA_TRY(check_cuda(cudaMemsetAsync(status, 0, sizeof(int32_t) * ASTRA_STATUS_WORDS, st), "memset status"));
+  ASTRA_TRY(check_cuda(cudaMemsetAsync(loss_out, 0, sizeof(double), st), "memset loss"));
+  if (B == 0 || S == 0) {
+    if (B) ASTRA_TRY(check_cuda(cudaMemsetAsync(grad_emb, 0, sizeof(float) * B * d, st), "memset grad_emb"));
+    return ASTRA_OK;
+  }
+  const bool bf16 = w_dtype == ASTRA_W_BF16;
+  FwdArgs fa;
+  fa.emb = emb;
+  fa.keep = keep;
+  fa.ids = ids;
+  fa.y = y;
+  fa.origin = origin;
+  fa.origin_stride = origin_stride;
+  fa.weights = weights;
+  fa.weights_stride = weights_stride;
+  fa.factors_in = factors_in;
+  fa.B = B;
+  fa.S = S;
+  fa.d = d;
+  fa.W = W;
+  fa.Lloc = Lloc;
+  fa.off = off;
+  fa.grad_emb = grad_emb;
+  fa.factors = factors_out ? factors_out : w.factors;
+  fa.loss_rows = w.loss_rows;
+  fa.bound_rows = w.bound_rows;
+  fa.status = status;
+  const int nv = d % 128 == 0 ? d / 128 : 0;
+  const bool aligned = (reinterpret_cast<uintptr_t>(emb) % 16 == 0) && (reinterpret_cast<uintptr_t>(W) % 16 == 0);
+  if (aligned && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
+    switch (nv * 2 + (bf16 ? 1 : 0)) {
+      case 2: launch_forward_vec<1, false>(fa, st); break;
+      case 3: launch_forward_vec<1, true>(fa, st); break;
+      case 4: launch_forward_vec<2, false>(fa, st); break;
+      case 5: launch_forward_vec<2, true>(fa, st); break;
+      case 8: launch_forward_vec<4, false>(fa, st); break;
+      case 9: launch_forward_vec<4, true>(fa, st); break;
+      case 12: launch_forward_vec<6, false>(fa, st); break;
+      case 13: launch_forward_vec<6, true>(fa, st); break;
+      case 16: launch_forward_vec<8, false>(fa, st); break;
+      case 17: launch_forward_vec<8, true>(fa, st); break;
+    }
+  } else {
+    size_t smem = sizeof(float) * static_cast<size_t>(d) * (1 + kFwdWarps);
+    if (smem > 200 * 1024) return set_error(ASTRA_ERR_CONFIG, "slate_step: d=%d too large", d);
+    if (bf16) {
+      cudaFuncSetAttribute(slot_forward_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      slot_forward_generic<true><<<B, kFwdThreads, smem, st>>>(fa);
+    } else {
+      cudaFuncSetAttribute(slot_forward_generic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      slot_forward_generic<false><<<B, kFwdThreads, smem, st>>>(fa);
+    }
+  }
+  ASTRA_LAUNCHED("slot_forward");
+  finalize_kernel<<<1, 1024, 0, st>>>(w.loss_rows, w.bound_rows, B, loss_out, status);
+  ASTRA_LAUNCHED("finalize");
+
+  // counting sort of the slots by local label id
+  const int64_t n = static_cast<int64_t>(B) * S;
+  const int64_t nb = (Lloc + kScanTile - 1) / kScanTile;
+  if (Lloc == 0) return ASTRA_OK;
+  if (nb > 1024 * 1024) return set_error(ASTRA_ERR_CONFIG, "label shard too large");
+  const int sms = num_sms();
+  const int grid_n = static_cast<int>(std::min<int64_t>((n + 255) / 256, 8LL * sms));
+  ASTRA_TRY(check_cuda(cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * Lloc, st), "memset counts"));
+  count_kernel<<<grid_n, 256, 0, st>>>(ids, n, off, Lloc, w.counts, w.rank, status);
+  ASTRA_LAUNCHED("count");
+  scan_reduce_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz);
+  ASTRA_LAUNCHED("scan_reduce");
+  scan_top_kernel<<<1, 1024, 0, st>>>(w.blk_slots, w.blk_nz, static_cast<int>(nb), w.U);
+  ASTRA_LAUNCHED("scan_top");
+  scan_apply_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz, w.offsets, w.uniq);
+  ASTRA_LAUNCHED("scan_apply");
+  scatter_kernel<<<grid_n, 256, 0, st>>>(ids, w.rank, n, off, w.offsets, w.perm);
+  ASTRA_LAUNCHED("scatter");
+
+  UpdArgs ua;
+  ua.emb = emb;
+  ua.factors = fa.factors;
+  ua.uniq = w.uniq;
+  ua.U = w.U;
+  ua.offsets = w.offsets;
+  ua.counts = w.counts;
+  ua.perm = w.perm;
+  ua.perm2 = w.perm2;
+  ua.S = S;
+  ua.d = d;
+  ua.W = W;
+  ua.m = adam_m;
+  ua.v = adam_v;
+  ua.lr = lr;
+  ua.wd = wd;
+  ua.status = status;
+  ua.c1 = ua.c2 = ua.eps = ua.neg_step = 0.0f;
+  if (optimizer == ASTRA_OPT_ADAM) {
+    double bc1 = 1.0 - pow(static_cast<double>(b1), static_cast<double>(adam_step));
+    double bc2 = 1.0 - pow(static_cast<double>(b2), static_cast<double>(adam_step));
+    ua.c1 = static_cast<float>(1.0 - static_cast<double>(b1));
+    ua.c2 = static_cast<float>(1.0 - static_cast<double>(b2));
+    ua.eps = eps;
+    ua.neg_step = static_cast<float>(-(static_cast<double>(lr) * sqrt(bc2) / bc1));
+  }
+  const int upd_ctas = 16 * sms;
+  if (optimizer == ASTRA_OPT_ADAM)
+    return bf16 ? launch_update<true, true>(ua, upd_ctas, st) : launch_update<false, true>(ua, upd_ctas, st);
+  return bf16 ? launch_update<true, false>(ua, upd_ctas, st) : launch_update<false, false>(ua, upd_ctas, st);
+}
+
+int apply_updates(void* W, int w_dtype, int64_t n_labels, int d, const int64_t* ids, const float* grads, int64_t U,
+                  float lr, float wd, int32_t* status, cudaStream_t st) {
+  (void)n_labels;
+  ASTRA_TRY(check_cuda(cudaMemsetAsync(status, 0, sizeof(int32_t) * ASTRA_STATUS_WORDS, st), "memset status"));
+  if (U == 0) return ASTRA_OK;
+  const int64_t n = U * d;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 8LL * num_sms()));
+  apply_check_kernel<<<grid, 256, 0, st>>>(grads, n, status);
+  ASTRA_LAUNCHED("apply_check");
+  if (w_dtype == ASTRA_W_BF16)
+    apply_rows_kernel<true><<<grid, 256, 0, st>>>(W, d, ids, grads, U, lr, wd, status);
+  else
+    apply_rows_kernel<false><<<grid, 256, 0, st>>>(W, d, ids, grads, U, lr, wd, status);
+  ASTRA_LAUNCHED("apply_rows");
+  return ASTRA_OK;
+}
+
+}  // namespace astra

@@ -1,0 +1,230 @@
+"""Device-level operations on torch CUDA tensors — one per C-ABI entry point.
+
+PyTorch is only the plumbing here (device memory, the current stream); all
+arithmetic runs in libastra_b200.so. Every call is stream-ordered on
+torch.cuda.current_stream() and does not synchronise unless stated.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .errors import ConfigError, NumericalError
+
+REFRESH_FP32_EXACT, REFRESH_BF16, REFRESH_BF16_RERANK = 0, 1, 2
+W_FP32, W_BF16 = 0, 1
+OPT_SGD, OPT_ADAM = 0, 1
+ORIGIN_POS, ORIGIN_HARD, ORIGIN_RAND, ORIGIN_PAD, ORIGIN_IMP = 0, 1, 2, 3, 4
+STATUS_NONFINITE_GRAD, STATUS_NONFINITE_GRAD_EMB, STATUS_BOUND_UNSAFE, STATUS_ID_RANGE = 0, 1, 2, 3
+
+_MODES = {"fp32": REFRESH_FP32_EXACT, "fp32_exact": REFRESH_FP32_EXACT, "bf16": REFRESH_BF16,
+          "bf16_rerank": REFRESH_BF16_RERANK}
+
+
+def refresh_mode(mode) -> int:
+    if isinstance(mode, int):
+        return mode
+    try:
+        return _MODES[mode]
+    except KeyError:
+        raise ConfigError(f"unknown refresh mode {mode!r}") from None
+
+
+class _Workspaces:
+    """Per-device scratch buffers grown on demand (one per call site tag)."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, tag: str, nbytes: int, device) -> torch.Tensor:
+        key = (tag, torch.device(device).index)
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            self._bufs[key] = buf
+        return buf
+
+
+WORKSPACES = _Workspaces()
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _cuda(t, dtype, name):
+    if t is None:
+        return None
+    if not (t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+        raise ConfigError(f"{name}: expected a contiguous CUDA {dtype} tensor, got {t.dtype} on {t.device}")
+    return t
+
+
+def f32_to_bf16(x: torch.Tensor) -> torch.Tensor:
+    _cuda(x, torch.float32, "f32_to_bf16")
+    out = torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
+    _lib.check(_lib.load().astra_f32_to_bf16(_p(x), _p(out), x.numel(), _stream()))
+    return out
+
+
+def refresh_topk(queries, pos_indptr, pos_ids, k, mode="bf16_rerank", labels_f32=None, labels_bf16=None,
+                 label_offset=0, queries_bf16=None, n_labels=None):
+    """Top-k (keys, ids, scores) per query over a label shard, positives
+    excluded (retrieve_hard_negatives, anns.py:233-256). keys are int64 views of
+    the packed uint64 keys (for astra_topk_merge)."""
+    mode = refresh_mode(mode)
+    ref = queries if queries is not None else queries_bf16
+    nq, d = ref.shape
+    if n_labels is None:
+        n_labels = (labels_f32 if labels_f32 is not None else labels_bf16).shape[0]
+    _cuda(queries, torch.float32, "queries")
+    _cuda(labels_f32, torch.float32, "labels_f32")
+    _cuda(labels_bf16, torch.bfloat16, "labels_bf16")
+    _cuda(queries_bf16, torch.bfloat16, "queries_bf16")
+    _cuda(pos_indptr, torch.int64, "pos_indptr")
+    _cuda(pos_ids, torch.int32, "pos_ids")
+    lib = _lib.load()
+    dev = ref.device
+    ws_n = lib.astra_refresh_workspace_size(nq, n_labels, d, k, mode)
+    ws = WORKSPACES.get("refresh", ws_n, dev)
+    keys = torch.empty((nq, k), dtype=torch.int64, device=dev)
+    ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    scores = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    _lib.check(lib.astra_refresh_topk(
+        _p(queries), _p(queries_bf16), nq, d, _p(labels_f32), _p(labels_bf16), n_labels, label_offset,
+        _p(pos_indptr), _p(pos_ids), k, mode, _p(keys), _p(ids), _p(scores), _p(ws), ws.numel(), _stream()))
+    return keys, ids, scores
+
+
+def topk_merge(part_keys: torch.Tensor, k_out: int):
+    """Merge [n_parts, nq, k_in] partial key lists into the global top-k_out."""
+    _cuda(part_keys, torch.int64, "part_keys")
+    n_parts, nq, k_in = part_keys.shape
+    lib = _lib.load()
+    dev = part_keys.device
+    ws = WORKSPACES.get("merge", lib.astra_merge_workspace_size(nq, k_out), dev)
+    keys = torch.empty((nq, k_out), dtype=torch.int64, device=dev)
+    ids = torch.empty((nq, k_out), dtype=torch.int32, device=dev)
+    scores = torch.empty((nq, k_out), dtype=torch.float32, device=dev)
+    _lib.check(lib.astra_topk_merge(_p(part_keys), nq, n_parts, k_in, k_out, _p(keys), _p(ids), _p(scores), _p(ws),
+                                    ws.numel(), _stream()))
+    return keys, ids, scores
+
+
+def sample_slates(seed, epoch, step, rows, pos_indptr, pos_ids, hard, k_h, n_labels, k_p, k_r,
+                  cand=None, cand_q=None, k_i=0):
+    """Philox negative-mixture slates: (ids int32, y int8, origin int8, weights fp32), B x S."""
+    _cuda(rows, torch.int64, "rows")
+    _cuda(pos_indptr, torch.int64, "pos_indptr")
+    _cuda(pos_ids, torch.int32, "pos_ids")
+    B = rows.shape[0]
+    dev = rows.device
+    if hard is None or k_h == 0:
+        hard, k_h, hard_stride = None, 0, 1
+    else:
+        _cuda(hard, torch.int32, "hard")
+        hard_stride = hard.shape[1]
+    n_c, cand_stride = 0, 1
+    if cand is not None and k_i > 0:
+        _cuda(cand, torch.int32, "cand")
+        _cuda(cand_q, torch.float32, "cand_q")
+        n_c = cand_stride = cand.shape[1]
+    else:
+        cand = cand_q = None
+        k_i = 0
+    S = k_p + k_h + k_i + k_r
+    ids = torch.empty((B, S), dtype=torch.int32, device=dev)
+    y = torch.empty((B, S), dtype=torch.int8, device=dev)
+    origin = torch.empty((B, S), dtype=torch.int8, device=dev)
+    weights = torch.empty((B, S), dtype=torch.float32, device=dev)
+    _lib.check(_lib.load().astra_sample_slates(
+        seed & 0xFFFFFFFFFFFFFFFF, epoch & 0xFFFFFFFF, step & 0xFFFFFFFF, _p(rows), B, _p(pos_indptr), _p(pos_ids),
+        _p(hard), hard_stride, k_h, _p(cand), _p(cand_q), cand_stride, n_c, k_i, n_labels, k_p, k_r,
+        _p(ids), _p(y), _p(origin), _p(weights), _stream()))
+    return ids, y, origin, weights
+
+
+class StepResult:
+    """Device outputs of one slate step; `loss`/`status` sync only when read."""
+
+    def __init__(self, loss, grad_emb, status, factors):
+        self.loss_dev = loss
+        self.grad_emb = grad_emb
+        self.status = status
+        self.factors = factors
+
+    def status_host(self):
+        return self.status.cpu().tolist()
+
+    @property
+    def loss(self) -> float:
+        return float(self.loss_dev.item())
+
+
+def slate_step(emb, ids, y, origin, weights, W, lr, weight_decay=0.0, keep=None, factors_in=None,
+               optimizer="sgd", adam_m=None, adam_v=None, adam_step=1, betas=(0.9, 0.999), eps=1e-8,
+               label_offset=0, want_factors=False) -> StepResult:
+    """Fused sampled-BCE fwd/bwd + sparse row update of W (trainer.py:366-394).
+
+    origin/weights may be S-vectors (the reference's row-0 semantics) or B x S."""
+    _cuda(emb, torch.float32, "emb")
+    _cuda(keep, torch.float32, "keep")
+    _cuda(ids, torch.int32, "ids")
+    _cuda(y, torch.int8, "y")
+    _cuda(origin, torch.int8, "origin")
+    _cuda(weights, torch.float32, "weights")
+    _cuda(factors_in, torch.float32, "factors_in")
+    if W.dtype not in (torch.float32, torch.bfloat16) or not W.is_cuda or not W.is_contiguous():
+        raise ConfigError("W must be a contiguous CUDA fp32/bf16 tensor")
+    B, S = ids.shape
+    d = emb.shape[1]
+    Lloc = W.shape[0]
+    opt = OPT_ADAM if optimizer == "adam" else OPT_SGD
+    if opt == OPT_ADAM:
+        _cuda(adam_m, torch.float32, "adam_m")
+        _cuda(adam_v, torch.float32, "adam_v")
+    o_stride = 0 if origin.dim() == 1 else S
+    w_stride = 0 if weights.dim() == 1 else S
+    lib = _lib.load()
+    dev = emb.device
+    ws = WORKSPACES.get("step", lib.astra_step_workspace_size(B, S, d, Lloc), dev)
+    grad_emb = torch.empty((B, d), dtype=torch.float32, device=dev)
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    status = torch.empty(4, dtype=torch.int32, device=dev)
+    factors = torch.empty((B, S), dtype=torch.float32, device=dev) if want_factors else None
+    _lib.check(lib.astra_slate_step(
+        _p(emb), _p(keep), _p(ids), _p(y), _p(origin), o_stride, _p(weights), w_stride, _p(factors_in), B, S, d,
+        _p(W), W_BF16 if W.dtype == torch.bfloat16 else W_FP32, _p(adam_m), _p(adam_v), opt, Lloc, label_offset,
+        float(lr), float(weight_decay), float(betas[0]), float(betas[1]), float(eps), int(adam_step),
+        _p(grad_emb), _p(loss), _p(status), _p(factors), _p(ws), ws.numel(), _stream()))
+    return StepResult(loss, grad_emb, status, factors)
+
+
+def raise_for_step_status(status) -> None:
+    """Host check of a step's status words (syncs). Mirrors the reference's
+    NumericalError raises (classifiers.py:79-80, encoder.py:145-146)."""
+    s = status.cpu().tolist() if torch.is_tensor(status) else list(status)
+    if s[STATUS_NONFINITE_GRAD_EMB]:
+        raise NumericalError("non-finite upstream gradients")
+    if s[STATUS_NONFINITE_GRAD]:
+        raise NumericalError("non-finite classifier gradient")
+
+
+def apply_updates(W, ids, grads, lr, weight_decay=0.0):
+    """apply_classifier_updates_arrays on device (classifiers.py:75-82); syncs
+    to raise NumericalError without writing when a gradient is non-finite."""
+    _cuda(ids, torch.int64, "ids")
+    _cuda(grads, torch.float32, "grads")
+    status = torch.zeros(4, dtype=torch.int32, device=W.device)
+    _lib.check(_lib.load().astra_apply_updates(
+        _p(W), W_BF16 if W.dtype == torch.bfloat16 else W_FP32, W.shape[0], W.shape[1], _p(ids), _p(grads),
+        ids.shape[0], float(lr), float(weight_decay), _p(status), _stream()))
+    if status[STATUS_NONFINITE_GRAD].item():
+        raise NumericalError("non-finite classifier gradient")

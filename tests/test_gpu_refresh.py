@@ -1,0 +1,130 @@
+"""GPU parity of the shortlist refresh (anns.py:233-256) through the C-ABI.
+
+FP32_EXACT ids/keys must equal the C oracle bit-for-bit; BF16_RERANK must
+equal FP32_EXACT; plain BF16 must reach the recall bar against fp32.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from gpu_util import csr, dev, random_positives, u64
+from oracle import c_oracle as co
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(E, W, positives, k, mode, offset=0):
+    from paper_2409_20156_b200 import ops
+
+    ip, pid = csr(positives)
+    Wd = dev(W)
+    keys, ids, scores = ops.refresh_topk(
+        dev(E), dev(ip), dev(pid), k, mode, labels_f32=Wd, labels_bf16=ops.f32_to_bf16(Wd) if mode != "fp32" else None,
+        label_offset=offset)
+    torch.cuda.synchronize()
+    return u64(keys), ids.cpu().numpy(), scores.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["refresh_random.npz", "refresh_ties.npz"])
+def test_fp32_exact_matches_oracle_on_golden(cuda_lib, name):
+    g = golden(name)
+    ip, pid = g["pos_indptr"], g["pos_ids"]
+    positives = [pid[ip[i] : ip[i + 1]] for i in range(len(ip) - 1)]
+    k = int(g["k_h"])
+    keys, ids, _ = _run(g["E"], g["W"], positives, k, "fp32")
+    okeys, oids, _ = co.refresh_fp32(g["E"], g["W"], ip, pid, k)
+    np.testing.assert_array_equal(keys, okeys)
+    np.testing.assert_array_equal(ids, oids)
+    if name == "refresh_ties.npz":  # order-independent scores: equals the reference itself
+        np.testing.assert_array_equal(ids, g["ids"])
+
+
+@pytest.mark.parametrize("nq,L,d,k", [(130, 1000, 24, 5), (257, 5000, 64, 64), (64, 3000, 96, 300), (33, 700, 128, 600)])
+def test_fp32_exact_shapes(cuda_lib, nq, L, d, k):
+    rng = np.random.default_rng(nq + L)
+    W = rng.standard_normal((L, d)).astype(np.float32)
+    E = rng.standard_normal((nq, d)).astype(np.float32)
+    positives = random_positives(rng, nq, L, 0, 6)
+    keys, ids, scores = _run(E, W, positives, k, "fp32")
+    okeys, oids, oscores = co.refresh_fp32(E, W, *csr(positives), k)
+    np.testing.assert_array_equal(keys, okeys)
+    np.testing.assert_array_equal(ids, oids)
+    np.testing.assert_array_equal(scores, oscores)
+
+
+def test_known_answers(cuda_lib):
+    W = np.array([[0.0, 1.0], [1.0, 0.0], [1.0, 0.0], [0.5, 0.0]], np.float32)
+    _, ids, _ = _run(np.array([[1.0, 0.0]], np.float32), W, [np.zeros(0, np.int32)], 3, "fp32")
+    assert ids[0].tolist() == [1, 2, 3]  # test_anns.py:30-33
+    W = np.random.default_rng(1).standard_normal((20, 4)).astype(np.float32)
+    _, ids, _ = _run(np.zeros((1, 4), np.float32), W, [np.zeros(0, np.int32)], 5, "fp32")
+    assert ids[0].tolist() == [0, 1, 2, 3, 4]  # test_anns.py:46-50
+
+
+def test_shard_merge_equals_single_shard(cuda_lib):
+    from paper_2409_20156_b200 import ops
+
+    rng = np.random.default_rng(3)
+    L, d, nq, k = 6000, 64, 200, 40
+    W = rng.standard_normal((L, d)).astype(np.float32)
+    E = rng.standard_normal((nq, d)).astype(np.float32)
+    positives = random_positives(rng, nq, L, 0, 8)
+    full_keys, full_ids, _ = _run(E, W, positives, k, "fp32")
+    bounds = [0, 1700, 4100, L]
+    parts = []
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        keys, _, _ = _run(E, W[lo:hi], positives, k, "fp32", offset=lo)
+        parts.append(keys)
+    part_keys = dev(np.stack(parts).view(np.int64))
+    mk, mids, _ = ops.topk_merge(part_keys, k)
+    np.testing.assert_array_equal(u64(mk), full_keys)
+    np.testing.assert_array_equal(mids.cpu().numpy(), full_ids)
+
+
+@pytest.mark.parametrize("nq,L,d,k", [(256, 20000, 128, 32), (300, 9000, 768, 64), (1, 5000, 64, 8)])
+def test_bf16_recall_and_rerank(cuda_lib, nq, L, d, k):
+    rng = np.random.default_rng(7)
+    W = rng.uniform(-1 / np.sqrt(d), 1 / np.sqrt(d), size=(L, d)).astype(np.float32)
+    E = rng.standard_normal((nq, d)).astype(np.float32)
+    positives = random_positives(rng, nq, L, 0, 5)
+    _, exact_ids, _ = _run(E, W, positives, k, "fp32")
+    _, bf_ids, bf_scores = _run(E, W, positives, k, "bf16")
+    recall = np.mean([len(set(a) & set(b)) / k for a, b in zip(bf_ids.tolist(), exact_ids.tolist())])
+    assert recall >= 0.98, recall
+    # bf16 scores are close to the fp32 scores of the same labels
+    full = co.scores_fp32(E, W)
+    ref = np.take_along_axis(full, bf_ids.astype(np.int64), axis=1)
+    assert np.abs(bf_scores - ref).max() < 0.05 * np.abs(full).max()
+    for i, p in enumerate(positives):
+        assert not set(bf_ids[i].tolist()) & set(p.tolist())
+        assert len(set(bf_ids[i].tolist())) == k
+    _, rr_ids, rr_scores = _run(E, W, positives, k, "bf16_rerank")
+    np.testing.assert_array_equal(rr_ids, exact_ids)  # north star: recall@k >= 0.999 in bf16 mode
+
+
+def test_bf16_rerank_label_offset_and_tail(cuda_lib):
+    rng = np.random.default_rng(9)
+    L, d, nq, k = 1000 + 37, 64, 130, 16  # label tail inside a 256-wide tile, query tail
+    W = rng.standard_normal((L, d)).astype(np.float32)
+    E = rng.standard_normal((nq, d)).astype(np.float32)
+    positives = [p + 5000 for p in random_positives(rng, nq, L, 0, 4)]
+    _, exact_ids, _ = _run(E, W, positives, k, "fp32", offset=5000)
+    _, rr_ids, _ = _run(E, W, positives, k, "bf16_rerank", offset=5000)
+    np.testing.assert_array_equal(rr_ids, exact_ids)
+    assert rr_ids.min() >= 5000 and rr_ids.max() < 5000 + L
+
+
+def test_config_errors(cuda_lib):
+    from paper_2409_20156_b200 import ops
+    from paper_2409_20156_b200.errors import ConfigError
+
+    E = torch.zeros((4, 48), device="cuda")
+    W = torch.zeros((10, 48), device="cuda")
+    ip = torch.zeros(5, dtype=torch.int64, device="cuda")
+    pid = torch.zeros(0, dtype=torch.int32, device="cuda")
+    with pytest.raises(ConfigError):
+        ops.refresh_topk(E, ip, pid, 3, "bf16", labels_bf16=W.to(torch.bfloat16))  # d % 64
+    with pytest.raises(ConfigError):
+        ops.refresh_topk(E, ip, pid, 0, "fp32", labels_f32=W)

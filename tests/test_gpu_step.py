@@ -1,0 +1,243 @@
+"""GPU parity of the sampled-loss step + sparse update (trainer.py:366-394,
+classifiers.py:75-82) through the C-ABI.
+
+Tolerance (north star): loss / grad_emb / W' within 1e-5 relative for fp32
+with an absolute floor of 1e-6 * max|ref| (near-zero entries
+make a pure relative bound meaningless); 2e-2 relative for bf16 W.
+Untouched rows must be bit-identical; with the reference's own factors fed in
+(factors_in) the update itself must be bit-identical.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from gpu_util import dev
+from oracle import xcmix_port as port
+
+pytestmark = pytest.mark.gpu
+
+
+def close(a, b, rtol=1e-5, floor=1e-6):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    atol = floor * max(np.abs(b).max(), 1e-30)
+    bad = np.abs(a - b) > atol + rtol * np.abs(b)
+    assert not bad.any(), f"{bad.sum()} / {bad.size} outside tolerance; max abs diff {np.abs(a - b).max():.3e}"
+
+
+def _step(g, p, factors_in=None):
+    from paper_2409_20156_b200 import ops
+
+    W = dev(g[p + "W_before"])
+    emb = g[p + "emb"]
+    keep = g[p + "keep"] if g[p + "keep"].size else None
+    emb_used = emb * keep if keep is not None else emb
+    res = ops.slate_step(
+        dev(emb_used), dev(g[p + "ids"].astype(np.int32)), dev(g[p + "y"]), dev(g[p + "origin"]), dev(g[p + "weights"]),
+        W, float(g[p + "lr"]), float(g["wd"]), keep=None if keep is None else dev(keep),
+        factors_in=None if factors_in is None else dev(factors_in))
+    torch.cuda.synchronize()
+    return res, W.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["step_c1_parity.npz", "step_dropout.npz"])
+def test_step_matches_reference_golden(cuda_lib, name):
+    g = golden(name)
+    L = int(g["L"])
+    for t in range(int(g["n_steps"])):
+        p = f"s{t}_"
+        res, W = _step(g, p)
+        assert res.status_host() == [0, 0, 0, 0]
+        assert abs(res.loss - float(g[p + "loss"])) <= 1e-5 * abs(float(g[p + "loss"]))
+        close(res.grad_emb.cpu().numpy(), g[p + "grad_emb"])
+        uids = g[p + "uids"]
+        close(W[uids], g[p + "W_after_touched"])
+        untouched = np.ones(L, bool)
+        untouched[uids] = False
+        np.testing.assert_array_equal(W[untouched], g[p + "W_before"][untouched])
+
+
+@pytest.mark.parametrize("name", ["step_c1_parity.npz", "step_dropout.npz"])
+def test_update_bitexact_given_reference_factors(cuda_lib, name):
+    g = golden(name)
+    for t in range(int(g["n_steps"])):
+        p = f"s{t}_"
+        emb = g[p + "emb"]
+        keep = g[p + "keep"] if g[p + "keep"].size else None
+        emb_used = emb * keep if keep is not None else emb
+        scores = np.einsum("bsd,bd->bs", g[p + "W_before"][g[p + "ids"]], emb_used)
+        _, factors = port.slate_factors(scores, g[p + "y"], g[p + "origin"], g[p + "weights"])
+        _, W = _step(g, p, factors_in=factors)
+        np.testing.assert_array_equal(W[g[p + "uids"]], g[p + "W_after_touched"])
+
+
+def _random_step(L, d, B, S, seed, n_hot=0):
+    rng = np.random.default_rng(seed)
+    W = rng.uniform(-1 / np.sqrt(d), 1 / np.sqrt(d), size=(L, d)).astype(np.float32)
+    emb = rng.standard_normal((B, d)).astype(np.float32)
+    ids = rng.integers(0, L, size=(B, S)).astype(np.int64)
+    if n_hot:  # a few labels shared by many rows (long segments in the sort)
+        ids[:, :n_hot] = rng.integers(0, 4, size=(B, n_hot))
+    y = (rng.random((B, S)) < 0.05).astype(np.int8)
+    origin = np.full(S, port.ORIGIN_RAND, np.int8)
+    origin[:4] = port.ORIGIN_POS
+    origin[4:20] = port.ORIGIN_HARD
+    weights = np.ones(S, np.float32)
+    weights[origin == port.ORIGIN_RAND] = np.float32((L - 16) / (S - 20))
+    return W, emb, ids, y, origin, weights
+
+
+@pytest.mark.parametrize("L,d,B,S,n_hot", [(100_000, 768, 48, 584, 0), (3000, 64, 256, 52, 8), (5000, 100, 40, 30, 3),
+                                           (2000, 128, 96, 70, 40)])
+def test_step_vs_oracle_shapes(cuda_lib, L, d, B, S, n_hot):
+    from paper_2409_20156_b200 import ops
+
+    W, emb, ids, y, origin, weights = _random_step(L, d, B, S, L + d, n_hot)
+    Wd = dev(W)
+    res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wd, 0.3, 1e-3)
+    Wref = W.copy()
+    loss, grad_emb, _, uids = port.slate_step(Wref, emb, None, ids, y, origin, weights, 0.3, 1e-3)
+    torch.cuda.synchronize()
+    assert res.status_host() == [0, 0, 0, 0]
+    assert abs(res.loss - loss) <= 1e-5 * abs(loss)
+    close(res.grad_emb.cpu().numpy(), grad_emb)
+    Wg = Wd.cpu().numpy()
+    close(Wg[uids], Wref[uids])
+    mask = np.ones(L, bool)
+    mask[uids] = False
+    np.testing.assert_array_equal(Wg[mask], W[mask])
+
+
+def test_per_row_origin_and_weights(cuda_lib):
+    """B x S origin/weights (the fixed-semantics / importance path) vs oracle."""
+    from paper_2409_20156_b200 import ops
+
+    W, emb, ids, y, origin, weights = _random_step(4000, 128, 32, 40, 5)
+    rng = np.random.default_rng(1)
+    origin2 = np.tile(origin, (32, 1))
+    origin2[rng.random(origin2.shape) < 0.1] = port.ORIGIN_PAD
+    weights2 = rng.uniform(0.5, 50, size=(32, 40)).astype(np.float32)
+    Wd = dev(W)
+    res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin2), dev(weights2), Wd, 0.1, 0.0)
+    Wref = W.copy()
+    loss, grad_emb, _, uids = port.slate_step(Wref, emb, None, ids, y, origin2, weights2, 0.1, 0.0)
+    assert abs(res.loss - loss) <= 1e-5 * abs(loss)
+    close(res.grad_emb.cpu().numpy(), grad_emb)
+    close(Wd.cpu().numpy()[uids], Wref[uids])
+
+
+def test_label_sharded_step_equals_single(cuda_lib):
+    from paper_2409_20156_b200 import ops
+
+    L = 6000
+    W, emb, ids, y, origin, weights = _random_step(L, 256, 64, 60, 11, n_hot=5)
+    full = dev(W)
+    r_full = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), full, 0.2, 1e-3)
+    cut = 2500
+    shards = [dev(W[:cut]), dev(W[cut:])]
+    rs = [ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), s, 0.2, 1e-3,
+                         label_offset=o) for s, o in zip(shards, [0, cut])]
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(np.concatenate([s.cpu().numpy() for s in shards]), full.cpu().numpy())
+    assert abs(sum(r.loss for r in rs) - r_full.loss) <= 1e-9 * abs(r_full.loss)
+    close(sum(r.grad_emb.cpu().numpy().astype(np.float64) for r in rs), r_full.grad_emb.cpu().numpy())
+
+
+def test_adam_matches_torch_sparse_adam(cuda_lib):
+    from paper_2409_20156_b200 import ops
+
+    L, d = 3000, 128
+    W, emb, ids, y, origin, weights = _random_step(L, d, 32, 40, 21, n_hot=3)
+    Wd = dev(W)
+    m = torch.zeros_like(Wd)
+    v = torch.zeros_like(Wd)
+    param = torch.nn.Parameter(torch.from_numpy(W.copy()))
+    opt = torch.optim.SparseAdam([param], lr=0.01, betas=(0.9, 0.999), eps=1e-8)
+    rng = np.random.default_rng(0)
+    for step in (1, 2, 3):
+        factors = rng.standard_normal(ids.shape).astype(np.float32)
+        uids, grads = port.per_label_gradient(ids, factors, emb, L)
+        param.grad = torch.sparse_coo_tensor(torch.from_numpy(uids)[None], torch.from_numpy(grads), (L, d))
+        opt.step()
+        ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wd, 0.01, 0.0,
+                       factors_in=dev(factors), optimizer="adam", adam_m=m, adam_v=v, adam_step=step)
+        torch.cuda.synchronize()
+        got = Wd.cpu().numpy()
+        ref = param.detach().numpy()
+        close(got, ref, rtol=1e-6, floor=1e-7)
+        assert (got == ref).mean() > 0.99  # same op order as SparseAdam: (almost) all bits equal
+
+
+def test_bf16_weights_sgd(cuda_lib):
+    from paper_2409_20156_b200 import ops
+
+    L, d = 8000, 256
+    W, emb, ids, y, origin, weights = _random_step(L, d, 32, 50, 31)
+    Wb = dev(W).to(torch.bfloat16)
+    W32 = Wb.float().cpu().numpy()
+    res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wb, 0.05, 1e-3)
+    Wref = W32.copy()
+    loss, grad_emb, _, uids = port.slate_step(Wref, emb, None, ids, y, origin, weights, 0.05, 1e-3)
+    assert abs(res.loss - loss) <= 2e-2 * abs(loss)
+    close(res.grad_emb.cpu().numpy(), grad_emb, rtol=2e-2, floor=1e-3)
+    close(Wb.float().cpu().numpy()[uids], Wref[uids], rtol=2e-2, floor=1e-3)
+
+
+def test_nonfinite_grad_emb_blocks_update(cuda_lib):
+    from paper_2409_20156_b200 import ops
+    from paper_2409_20156_b200.errors import NumericalError
+
+    W, emb, ids, y, origin, weights = _random_step(2000, 128, 16, 30, 41)
+    emb[3, 7] = np.nan
+    Wd = dev(W)
+    res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wd, 0.1, 1e-3)
+    np.testing.assert_array_equal(Wd.cpu().numpy(), W)
+    with pytest.raises(NumericalError):
+        ops.raise_for_step_status(res.status)
+
+
+def test_nonfinite_row_blocks_update(cuda_lib):
+    from paper_2409_20156_b200 import ops
+    from paper_2409_20156_b200.errors import NumericalError
+
+    W, emb, ids, y, origin, weights = _random_step(2000, 128, 16, 30, 43)
+    W[ids[5, 9]] = np.inf
+    Wd = dev(W)
+    res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wd, 0.1, 1e-3)
+    st = res.status_host()
+    assert st[2] == 1  # overflow bound tripped -> checked path
+    np.testing.assert_array_equal(Wd.cpu().numpy(), W)
+    with pytest.raises(NumericalError):
+        ops.raise_for_step_status(st)
+
+
+def test_huge_but_finite_takes_checked_path(cuda_lib):
+    from paper_2409_20156_b200 import ops
+
+    W, emb, ids, y, origin, weights = _random_step(2000, 128, 8, 30, 47)
+    emb *= np.float32(1e35)
+    Wd = dev(W)
+    res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wd, 1e-3, 0.0)
+    st = res.status_host()
+    Wref = W.copy()
+    _, _, _, uids = port.slate_step(Wref, emb, None, ids, y, origin, weights, 1e-3, 0.0)
+    assert st[2] == 1 and st[0] == 0 and st[1] == 0
+    close(Wd.cpu().numpy()[uids], Wref[uids], rtol=1e-4)
+
+
+def test_apply_updates_golden_bitexact(cuda_lib):
+    from paper_2409_20156_b200 import ops
+    from paper_2409_20156_b200.errors import NumericalError
+
+    g = golden("update.npz")
+    W = dev(g["W_before"])
+    ops.apply_updates(W, dev(g["ids"]), dev(g["grads"]), float(g["lr"]), float(g["wd"]))
+    np.testing.assert_array_equal(W.cpu().numpy(), g["W_after"])
+    bad = g["grads"].copy()
+    bad[3, 2] = np.nan
+    W2 = dev(g["W_before"])
+    with pytest.raises(NumericalError):
+        ops.apply_updates(W2, dev(g["ids"]), dev(bad), 0.3, 0.01)
+    np.testing.assert_array_equal(W2.cpu().numpy(), g["W_before"])
