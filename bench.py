@@ -1,0 +1,374 @@
+"""Benchmark of the full ASTRA classifier step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step = one pass of the hot path over one batch of B=1024 query rows per GPU
+at the LF-AmazonTitles-1.3M shape (BASELINE.json configs[3]: L=1,305,265,
+d=768): shortlist refresh of the batch's queries against the whole label set
+(bf16 tcgen05 GEMM + fused top-k + fp32 re-rank, k_h=64), Philox slates
+(k_p=8, k_h=64, k_r=512 -> S=584), fused sampled-BCE fwd/bwd + SGD update of
+the fp32 W. This is the composite "train samples/s (shortlist+loss+update)"
+with every training row refreshed once per epoch (tau_r = 1, the most
+refresh-heavy schedule); refresh-only MIPS q/s and step-only samples/s are
+reported beside it. Multi-GPU: W label-sharded, per-GPU batch fixed (weak
+scaling), NCCL all-gather / reduce-scatter as in paper_2409_20156_b200/shard.py.
+
+--impl reference times the reference's own CPU algorithm (oracle/xcmix_port.py,
+a bit-pinned restatement of xcmix — /root/reference is absent on the GPU box)
+on the host cores with the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# C4 = LF-AmazonTitles-1.3M shape, slate from SURVEY.md §8
+CFG = dict(workload="LF-AmazonTitles-1.3M shape, synthetic", L=1_305_265, d=768, N=2_248_619, B=1024,
+           k_p=8, k_h=64, k_r=512, labels_per_point=38, tau_r=1, lr=0.05, wd=1e-4)
+METRIC = "ASTRA train samples/s (shortlist+loss+update)"
+UNIT = "samples/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ data
+def make_batches(rng, n_batches, B, L, lpp, N, rank, world):
+    """Synthetic batches: global row ids, positives (labels_per_point distinct
+    uniform labels per row, sorted), embeddings N(0,1) fp32."""
+    out = []
+    for t in range(n_batches):
+        rows = ((t * world + rank) * B + np.arange(B, dtype=np.int64)) % N
+        pos = np.sort(rng.integers(0, L, size=(B, lpp)), axis=1)
+        # distinct per row: collisions are rare at L=1.3M; drop duplicates
+        indptr = np.zeros(B + 1, np.int64)
+        flat = []
+        for b in range(B):
+            u = np.unique(pos[b])
+            flat.append(u)
+            indptr[b + 1] = indptr[b] + len(u)
+        ids = np.concatenate(flat).astype(np.int32)
+        emb = rng.standard_normal((B, CFG["d"]), dtype=np.float32)
+        out.append(dict(rows=rows, indptr=indptr, pos=ids, emb=emb))
+    return out
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_20156_b200 import _lib, ops
+    from paper_2409_20156_b200.engine import ClassifierEngine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L, d, B = CFG["L"], CFG["d"], CFG["B"]
+    k_p, k_h, k_r = CFG["k_p"], CFG["k_h"], CFG["k_r"]
+    S = k_p + k_h + k_r
+    hbm, tf_burst, tf_sus, peak_kind = peaks()
+
+    eng = ClassifierEngine(L, d, k_p=k_p, k_h=k_h, k_r=k_r, seed=0, refresh_mode="bf16_rerank")
+    eng.snapshot(epoch=0)
+    L_loc = eng.hi - eng.lo
+    rng = np.random.default_rng(1000 + rank)
+    n_b = args.warmup + args.steps
+    host = make_batches(rng, n_b, B, L, CFG["labels_per_point"], CFG["N"], rank, world)
+    dev = []
+    for hb in host:
+        dev.append({k: torch.from_numpy(v).cuda() for k, v in hb.items()})
+    # the stale hard-negative cache rows of each batch: one refresh per batch up front
+    for db in dev:
+        db["hard"], _ = eng.refresh(db["emb"], db["indptr"], db["pos"], k_h)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_b)]
+    ids_keep = []
+
+    def one(t, timed):
+        db = dev[t]
+        e = ev[t]
+        e[0].record(stream)
+        new_ids, _ = eng.refresh(db["emb"], db["indptr"], db["pos"], k_h)
+        e[1].record(stream)
+        slates = eng.sample(db["rows"], db["indptr"], db["pos"], db["hard"], epoch=1, step=t)
+        e[2].record(stream)
+        loss, grad_emb, status = eng.step(db["emb"], slates, CFG["lr"], CFG["wd"])
+        e[3].record(stream)
+        if timed:
+            ids_keep.append(slates[0])
+        return loss, status
+
+    for t in range(args.warmup):
+        one(t, False)
+    torch.cuda.synchronize()
+    eng.comm.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for t in range(args.warmup, n_b):
+        loss, status = one(t, True)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    eng.comm.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = _lib.launch_count() - launches0
+    ops.raise_for_step_status(status)
+    ms_local = t_start.elapsed_time(t_end)
+    ms_t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_total = float(ms_t.item())
+    timed = range(args.warmup, n_b)
+    ph = {k: 0.0 for k in ("refresh", "sample", "step")}
+    for t in timed:
+        e = ev[t]
+        ph["refresh"] += e[0].elapsed_time(e[1])
+        ph["sample"] += e[1].elapsed_time(e[2])
+        ph["step"] += e[2].elapsed_time(e[3])
+    K = args.steps
+    ms_step = ms_total / K
+    value = B * world * K / (ms_total / 1e3)
+
+    # dominant kernel: the refresh (tcgen05 GEMM + fused top-k [+ merge/re-rank])
+    q_per_refresh = B * world  # every shard scores all gathered queries
+    flops = 2.0 * L_loc * d * q_per_refresh
+    t_ref = ph["refresh"] / K / 1e3
+    achieved_tf = flops / t_ref / 1e12
+    # step roofline: BASELINE.md bytes formula (U unique rows, fp32 SGD: read+write)
+    U = [int(torch.unique(ids[(ids >= eng.lo) & (ids < eng.hi)]).numel()) for ids in ids_keep]
+    U_mean = sum(U) / len(U)
+    step_bytes = U_mean * d * (2 * 4) + 2 * B * world * d * 4 + B * world * S * 5
+    t_step = ph["step"] / K / 1e3
+    step_gbs = step_bytes / t_step / 1e9
+
+    # end-to-end: the public API with HOST buffers (pinned), copies inside the timed region
+    pinned = []
+    for hb, db in zip(host, dev):
+        pinned.append({k: torch.from_numpy(v).pin_memory() for k, v in hb.items()} | {"hard": db["hard"].cpu().pin_memory()})
+    outs = None
+    for t in range(args.warmup):
+        p = pinned[t]
+        outs, _ = eng.train_step_host(p["emb"], p["rows"], p["indptr"], p["pos"], p["hard"], 1, t, CFG["lr"], CFG["wd"], out=outs)
+    torch.cuda.synchronize()
+    eng.comm.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h2d = d2h = 0
+    for t in range(args.warmup, n_b):
+        p = pinned[t]
+        outs, _ = eng.train_step_host(p["emb"], p["rows"], p["indptr"], p["pos"], p["hard"], 1, t, CFG["lr"], CFG["wd"], out=outs)
+        h2d = sum(x.numel() * x.element_size() for x in (p["emb"], p["rows"], p["indptr"], p["pos"], p["hard"]))
+        d2h = sum(x.numel() * x.element_size() for x in outs[:2]) - 8 + outs[2].numel() * outs[2].element_size()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = B * world * K / (float(e2e_ms.item()) / 1e3)
+
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32 W/step, bf16 tensor-core refresh + fp32 re-rank", "data": "synthetic",
+        "config": {"workload": CFG["workload"], "n_labels": L, "dim": d, "batch_per_gpu": B, "global_batch": B * world,
+                   "k_p": k_p, "k_h": k_h, "k_r": k_r, "slate": S, "labels_per_point": CFG["labels_per_point"],
+                   "tau_r": CFG["tau_r"], "refresh_mode": "bf16_rerank", "optimizer": "sgd+wd",
+                   "parallelism": f"label-shard{world}", "l2": "inputs larger than L2 (W fp32 4.0 GB + snapshots 6 GB)"},
+        "phases_ms_per_step": {k: round(v / K, 4) for k, v in ph.items()},
+        "refresh_mips_qps": round(B * world / t_ref, 1),
+        "step_only_samples_per_s": round(B * world / (t_step + ph["sample"] / K / 1e3), 1),
+        "composite_tau_r5_samples_per_s": round(B * world / (t_step + ph["sample"] / K / 1e3 + t_ref / 5), 1),
+        "roofline": {"bound": "tensor", "kernel": "refresh (tcgen05 GEMM + fused top-k + merge + re-rank)",
+                     "achieved": round(achieved_tf, 2), "peak": tf_sus, "unit": "TFLOP/s",
+                     "frac": round(achieved_tf / tf_sus, 4), "traffic": None,
+                     "algorithmic": f"2*L_shard*d*Q = {flops:.3e} flop per launch", "peak_kind": f"{peak_kind} sustained"},
+        "roofline_step": {"bound": "hbm", "kernel": "step (gather/loss/grad + counting sort + fused SGD row update)",
+                          "achieved": round(step_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(step_gbs / hbm, 4),
+                          "algorithmic": f"U*d*8 + 2*B*d*4 + B*S*5 = {step_bytes:.3e} B (U={U_mean:.0f})",
+                          "peak_kind": peak_kind},
+        "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ CPU arm
+def cpu_workload(rng, q_sample):
+    """Host data for the CPU path: W (L x d fp32), one batch of B rows."""
+    L, d, B = CFG["L"], CFG["d"], CFG["B"]
+    W = rng.random((L, d), dtype=np.float32)
+    W *= np.float32(2.0 / np.sqrt(d))
+    W -= np.float32(1.0 / np.sqrt(d))
+    emb = rng.standard_normal((B, d), dtype=np.float32)
+    positives = [np.unique(rng.integers(0, L, size=CFG["labels_per_point"])).astype(np.int32) for _ in range(B)]
+    return W, emb, positives
+
+
+def time_reference_cpu(W, emb, positives, rng, q_sample, seed):
+    """One bounded sample of the reference CPU path: refresh of q_sample
+    queries + one full-batch classifier step. Returns (t_refresh, t_step)."""
+    from oracle import xcmix_port as port
+
+    L = W.shape[0]
+    B = emb.shape[0]
+    t0 = time.perf_counter()
+    hard = port.retrieve_hard_negatives(W, emb[:q_sample], positives[:q_sample], CFG["k_h"], chunk=q_sample)
+    t_ref = time.perf_counter() - t0
+    hard_all = np.concatenate([hard] * (B // q_sample + 1))[:B].astype(np.int64)
+    pos_padded, n_pos = port.pad_positives(positives)
+    t0 = time.perf_counter()
+    srng = np.random.default_rng(seed)
+    ids, y, origin, weights = port.assemble_batch_slates(pos_padded, n_pos, np.arange(B), L, CFG["k_p"], CFG["k_r"], srng, hard_all)
+    port.slate_step(W, emb, None, ids, y, origin, weights, CFG["lr"], CFG["wd"])
+    t_step = time.perf_counter() - t0
+    return t_ref, t_step
+
+
+def cpu_baseline(args):
+    rng = np.random.default_rng(7)
+    q = args.cpu_queries
+    W, emb, positives = cpu_workload(rng, q)
+    t_ref, t_step = time_reference_cpu(W, emb, positives, rng, q, 1)
+    B = CFG["B"]
+    per_sample = t_step / B + t_ref / q / CFG["tau_r"]
+    return {"value": round(1.0 / per_sample, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"1 step of B={B} (S=584) + refresh of {q} queries vs L={CFG['L']}, numpy/scipy/OpenBLAS, "
+                      f"threads={os.environ.get('OMP_NUM_THREADS', 'all')}",
+            "step_s": round(t_step, 3), "refresh_qps": round(q / t_ref, 2)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rng = np.random.default_rng(7)
+    q = args.cpu_queries
+    W, emb, positives = cpu_workload(rng, q)
+    B = CFG["B"]
+    for t in range(args.warmup):
+        time_reference_cpu(W, emb, positives, rng, q, 100 + t)
+    tot = 0.0
+    for t in range(args.steps):
+        t_ref, t_step = time_reference_cpu(W, emb, positives, rng, q, 200 + t)
+        tot += t_step + t_ref * (B / q) / CFG["tau_r"]
+    value = B * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (numpy)",
+            "data": "synthetic",
+            "config": {"workload": CFG["workload"], "n_labels": CFG["L"], "dim": CFG["d"], "batch_per_gpu": B,
+                       "k_p": CFG["k_p"], "k_h": CFG["k_h"], "k_r": CFG["k_r"], "slate": CFG["k_p"] + CFG["k_h"] + CFG["k_r"],
+                       "tau_r": CFG["tau_r"]},
+            "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"per step: 1 classifier step of B={B} + refresh of {q} queries scaled to B"},
+            "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-queries", type=int, default=128)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

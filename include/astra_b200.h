@@ -155,6 +155,9 @@ int astra_sample_slates(uint64_t seed, uint32_t epoch, uint32_t step, const int6
  *   grad_emb   B x d fp32 out (partial over this shard's slots)
  *   loss_out   1 fp64 out: sum of this shard's slate loss terms (fp64)
  *   status     int32[ASTRA_STATUS_WORDS] out (zeroed by the call)
+ *   lr, weight_decay, betas, eps are host doubles: SGD rounds lr/wd to fp32
+ *   like np.float32(lr) (classifiers.py:82); Adam derives its step size in
+ *   double like torch.optim.SparseAdam.
  * Semantics: every id present in the slate is updated once (dead/pad slots
  * included, so they receive weight decay), gradients sum duplicates in
  * ascending flat (b*S+s) order, W is updated only if every touched row's
@@ -165,8 +168,8 @@ int astra_slate_step(const float* emb, const float* keep, const int32_t* ids, co
                      const int8_t* origin, int64_t origin_row_stride, const float* weights,
                      int64_t weights_row_stride, const float* factors_in, int B, int S, int d,
                      void* W, int w_dtype, float* adam_m, float* adam_v, int optimizer,
-                     int64_t n_labels_local, int64_t label_offset, float lr, float weight_decay,
-                     float adam_beta1, float adam_beta2, float adam_eps, int64_t adam_step,
+                     int64_t n_labels_local, int64_t label_offset, double lr, double weight_decay,
+                     double adam_beta1, double adam_beta2, double adam_eps, int64_t adam_step,
                      float* grad_emb, double* loss_out, int32_t* status, float* factors_out,
                      void* workspace, size_t workspace_bytes, void* stream);
 

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "libastra_b200.so")
 _lib = None
 _lock = threading.Lock()
 
-p, i32, i64, u32, u64, f32, sz = C.c_void_p, C.c_int, C.c_int64, C.c_uint32, C.c_uint64, C.c_float, C.c_size_t
+p, i32, i64, u32, u64, f32, f64, sz = C.c_void_p, C.c_int, C.c_int64, C.c_uint32, C.c_uint64, C.c_float, C.c_double, C.c_size_t
 
 _SIGS = {
     "astra_version": ([], C.c_char_p),
@@ -32,7 +32,7 @@ _SIGS = {
     "astra_topk_merge": ([p, i64, i32, i32, i32, p, p, p, p, sz, p], i32),
     "astra_sample_slates": ([u64, u32, u32, p, i32, p, p, p, i32, i32, p, p, i32, i32, i32, i64, i32, i32, p, p, p, p, p], i32),
     "astra_step_workspace_size": ([i32, i32, i32, i64], sz),
-    "astra_slate_step": ([p, p, p, p, p, i64, p, i64, p, i32, i32, i32, p, i32, p, p, i32, i64, i64, f32, f32, f32, f32, f32,
+    "astra_slate_step": ([p, p, p, p, p, i64, p, i64, p, i32, i32, i32, p, i32, p, p, i32, i64, i64, f64, f64, f64, f64, f64,
                           i64, p, p, p, p, p, sz, p], i32),
     "astra_apply_updates": ([p, i32, i64, i32, p, p, i64, f32, f32, p, p], i32),
     "astra_stream_sync": ([p], i32),

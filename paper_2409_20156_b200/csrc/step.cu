@@ -730,7 +730,7 @@ size_t step_workspace_size(int B, int S, int d, int64_t Lloc) {
 int slate_step(const float* emb, const float* keep, const int32_t* ids, const int8_t* y, const int8_t* origin,
                int64_t origin_stride, const float* weights, int64_t weights_stride, const float* factors_in, int B,
                int S, int d, void* W, int w_dtype, float* adam_m, float* adam_v, int optimizer, int64_t Lloc,
-               int64_t off, float lr, float wd, float b1, float b2, float eps, int64_t adam_step, float* grad_emb,
+               int64_t off, double lr, double wd, double b1, double b2, double eps, int64_t adam_step, float* grad_emb,
                double* loss_out, int32_t* status, float* factors_out, void* workspace, size_t ws_bytes,
                cudaStream_t st) {
   if (B < 0 || S < 0 || d <= 0 || Lloc < 0) return set_error(ASTRA_ERR_CONFIG, "slate_step: bad shape");
@@ -833,17 +833,18 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
   ua.W = W;
   ua.m = adam_m;
   ua.v = adam_v;
-  ua.lr = lr;
-  ua.wd = wd;
+  ua.lr = static_cast<float>(lr);  // np.float32(lr), classifiers.py:82
+  ua.wd = static_cast<float>(wd);
   ua.status = status;
   ua.c1 = ua.c2 = ua.eps = ua.neg_step = 0.0f;
   if (optimizer == ASTRA_OPT_ADAM) {
-    double bc1 = 1.0 - pow(static_cast<double>(b1), static_cast<double>(adam_step));
-    double bc2 = 1.0 - pow(static_cast<double>(b2), static_cast<double>(adam_step));
-    ua.c1 = static_cast<float>(1.0 - static_cast<double>(b1));
-    ua.c2 = static_cast<float>(1.0 - static_cast<double>(b2));
-    ua.eps = eps;
-    ua.neg_step = static_cast<float>(-(static_cast<double>(lr) * sqrt(bc2) / bc1));
+    // torch.optim.SparseAdam: scalars in double, rounded to fp32 when applied
+    double bc1 = 1.0 - pow(b1, static_cast<double>(adam_step));
+    double bc2 = 1.0 - pow(b2, static_cast<double>(adam_step));
+    ua.c1 = static_cast<float>(1.0 - b1);
+    ua.c2 = static_cast<float>(1.0 - b2);
+    ua.eps = static_cast<float>(eps);
+    ua.neg_step = static_cast<float>(-(lr * sqrt(bc2) / bc1));
   }
   const int upd_ctas = 16 * sms;
   if (optimizer == ASTRA_OPT_ADAM)

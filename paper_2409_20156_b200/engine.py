@@ -1,0 +1,173 @@
+"""Device-resident ASTRA classifier state and the full classifier step.
+
+`ClassifierEngine` owns one label shard of W (+ optimizer state) on one GPU
+and runs the hot path of SURVEY.md §8:
+
+  snapshot()  build_exact (anns.py:99): an immutable fp32 copy of W plus its
+              bf16 copy for the tensor-core refresh; non-finite -> NumericalError.
+  refresh()   retrieve_hard_negatives (anns.py:233-256) over every shard:
+              local fused GEMM + top-k, all-gather of partial keys, exact merge.
+  sample()    _assemble_batch_slates (trainer.py:262-318) via Philox.
+  step()      classifier half of _batch_forward_backward (trainer.py:366-394):
+              fused loss fwd/bwd + sparse SGD/Adam update of the local shard,
+              grad_emb reduce-scattered back to the rows' owners.
+  train_step_host()  the end-to-end call with HOST buffers (pinned H2D of the
+              step's inputs, D2H of grad_emb / loss / refreshed ids).
+
+All device work goes through `backend` (default: the CUDA C-ABI ops module).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import ops as cuda_ops
+from .errors import ConfigError, NumericalError
+from .shard import Comm, gather_csr, shard_range
+
+
+def init_uniform_scaled(rows: int, dim: int, seed: int, device) -> torch.Tensor:
+    """uniform(-1/sqrt(d), 1/sqrt(d)) like init_classifiers (classifiers.py:37-40),
+    drawn on the device (torch generator, not NumPy's PCG64 stream)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    bound = 1.0 / math.sqrt(dim)
+    w = torch.empty((rows, dim), dtype=torch.float32, device=device)
+    w.uniform_(-bound, bound, generator=g)
+    return w
+
+
+class ClassifierEngine:
+    def __init__(self, n_labels: int, dim: int, *, k_p: int, k_h: int, k_r: int, k_i: int = 0,
+                 weights=None, w_dtype=torch.float32, optimizer: str = "sgd", betas=(0.9, 0.999), eps=1e-8,
+                 refresh_mode: str = "bf16_rerank", seed: int = 0, device=None, group=None, backend=None):
+        if optimizer not in ("sgd", "adam"):
+            raise ConfigError(f"unknown optimizer {optimizer!r}")
+        if k_p < 1 or k_h < 0 or k_r < 0 or k_i < 0:
+            raise ConfigError("need k_p >= 1, k_h >= 0, k_r >= 0, k_i >= 0")
+        self.ops = backend if backend is not None else cuda_ops
+        self.comm = Comm(group)
+        self.device = torch.device(device if device is not None else ("cuda" if torch.cuda.is_available() else "cpu"))
+        self.n_labels, self.dim = int(n_labels), int(dim)
+        self.lo, self.hi = shard_range(self.n_labels, self.comm.rank, self.comm.world)
+        self.k_p, self.k_h, self.k_r, self.k_i = k_p, k_h, k_r, k_i
+        self.seed = seed
+        self.refresh_mode = refresh_mode
+        self.optimizer = optimizer
+        self.betas, self.eps = betas, eps
+        if weights is None:
+            W = init_uniform_scaled(self.hi - self.lo, dim, seed + 1 + 7919 * self.comm.rank, self.device)
+        else:
+            W = torch.as_tensor(weights)[self.lo : self.hi].to(self.device, torch.float32)
+        self.W = W.to(w_dtype).contiguous()
+        self.m = self.v = None
+        if optimizer == "adam":
+            self.m = torch.zeros((self.hi - self.lo, dim), dtype=torch.float32, device=self.device)
+            self.v = torch.zeros_like(self.m)
+        self.adam_step = 0
+        self.snap_f32 = self.snap_bf16 = None
+        self.snapshot_epoch = -1
+
+    # ------------------------------------------------------------ snapshot
+    def snapshot(self, epoch: int = 0, check_finite: bool = True) -> None:
+        """Immutable copy of the shard for the refresh (anns.py:90-100)."""
+        if check_finite and not bool(torch.isfinite(self.W).all()):
+            raise NumericalError("non-finite vectors in index build")
+        self.snap_f32 = self.W.float().clone() if self.W.dtype != torch.float32 else self.W.clone()
+        self.snap_bf16 = self.ops.f32_to_bf16(self.snap_f32) if self.refresh_mode != "fp32" else None
+        self.snapshot_epoch = epoch
+
+    # ------------------------------------------------------------ refresh
+    def refresh(self, queries: torch.Tensor, pos_indptr: torch.Tensor, pos_ids: torch.Tensor, k: int,
+                mode: str | None = None):
+        """Global top-k (ids, scores) for this rank's queries over ALL shards,
+        positives excluded. Collective when world_size > 1."""
+        if self.snap_f32 is None:
+            raise ConfigError("refresh before snapshot()")
+        mode = mode or self.refresh_mode
+        B = queries.shape[0]
+        q_all = self.comm.all_gather(queries)
+        ip_all, pid_all = gather_csr(self.comm, pos_indptr, pos_ids)
+        keys, ids, scores = self.ops.refresh_topk(
+            q_all, ip_all, pid_all, k, mode, labels_f32=self.snap_f32, labels_bf16=self.snap_bf16, label_offset=self.lo)
+        if self.comm.world == 1:
+            return ids, scores
+        parts = self.comm.all_gather_stack(keys)  # [world, world*B, k]
+        mine = parts[:, self.comm.rank * B : (self.comm.rank + 1) * B].contiguous()
+        _, ids, scores = self.ops.topk_merge(mine, k)
+        return ids, scores
+
+    # ------------------------------------------------------------ sampler
+    def sample(self, rows, pos_indptr, pos_ids, hard, epoch: int, step: int, k_h: int | None = None,
+               k_r: int | None = None, cand=None, cand_q=None):
+        """Slates for this rank's rows (Philox), all-gathered to every shard."""
+        k_h = self.k_h if k_h is None else k_h
+        k_r = self.k_r if k_r is None else k_r
+        ids, y, origin, weights = self.ops.sample_slates(
+            self.seed, epoch, step, rows, pos_indptr, pos_ids, hard, k_h, self.n_labels, self.k_p, k_r,
+            cand=cand, cand_q=cand_q, k_i=self.k_i if cand is not None else 0)
+        if self.comm.world > 1:
+            ids, y, origin, weights = (self.comm.all_gather(t) for t in (ids, y, origin, weights))
+        return ids, y, origin, weights
+
+    # ------------------------------------------------------------ step
+    def step(self, emb: torch.Tensor, slates, lr: float, weight_decay: float, keep=None, factors_in=None):
+        """Fused sampled-BCE step on this shard. Returns (loss_dev fp64[1],
+        grad_emb of this rank's rows, status int32[4]). No host sync."""
+        ids, y, origin, weights = slates
+        emb_all = self.comm.all_gather(emb)
+        keep_all = self.comm.all_gather(keep) if keep is not None else None
+        if self.optimizer == "adam":
+            self.adam_step += 1
+        res = self.ops.slate_step(
+            emb_all, ids, y, origin, weights, self.W, lr, weight_decay, keep=keep_all, factors_in=factors_in,
+            optimizer=self.optimizer, adam_m=self.m, adam_v=self.v, adam_step=max(self.adam_step, 1),
+            betas=self.betas, eps=self.eps, label_offset=self.lo)
+        grad_emb = self.comm.reduce_scatter(res.grad_emb)
+        loss = self.comm.all_reduce(res.loss_dev)
+        status = self.comm.all_reduce(res.status)
+        return loss, grad_emb, status
+
+    # ------------------------------------------------------------ full step
+    def train_step(self, emb, rows, pos_indptr, pos_ids, hard, epoch, step, lr, weight_decay, k_refresh=None,
+                   keep=None):
+        """One full classifier step on device-resident inputs: refresh of the
+        batch's queries (new hard negatives for a later epoch), slates from the
+        current (stale) hard cache rows, fused loss/update."""
+        new_ids, _ = self.refresh(emb, pos_indptr, pos_ids, k_refresh or self.k_h)
+        slates = self.sample(rows, pos_indptr, pos_ids, hard, epoch, step)
+        loss, grad_emb, status = self.step(emb, slates, lr, weight_decay, keep=keep)
+        return loss, grad_emb, status, new_ids
+
+    def train_step_host(self, emb_h, rows_h, pos_indptr_h, pos_ids_h, hard_h, epoch, step, lr, weight_decay,
+                        out=None):
+        """End-to-end call with HOST buffers: H2D of the step's inputs (pinned
+        memory, non_blocking), the device step, D2H of grad_emb, the loss and the
+        refreshed hard ids. Returns host tensors (grad_emb, loss, new_ids)."""
+        dev = self.device
+        emb = emb_h.to(dev, non_blocking=True)
+        rows = rows_h.to(dev, non_blocking=True)
+        ip = pos_indptr_h.to(dev, non_blocking=True)
+        pid = pos_ids_h.to(dev, non_blocking=True)
+        hard = hard_h.to(dev, non_blocking=True) if hard_h is not None else None
+        loss, grad_emb, status, new_ids = self.train_step(emb, rows, ip, pid, hard, epoch, step, lr, weight_decay)
+        if out is None:
+            out = (torch.empty(grad_emb.shape, dtype=grad_emb.dtype, pin_memory=True),
+                   torch.empty(2, dtype=torch.float64, pin_memory=True),
+                   torch.empty(new_ids.shape, dtype=new_ids.dtype, pin_memory=True))
+        out[0].copy_(grad_emb, non_blocking=True)
+        out[1][:1].copy_(loss, non_blocking=True)
+        out[2].copy_(new_ids, non_blocking=True)
+        return out, status
+
+    # ------------------------------------------------------------ host views
+    def weights_host(self) -> np.ndarray:
+        """This shard's W as fp32 NumPy (for eval / checkpoint boundaries)."""
+        return self.W.float().cpu().numpy()
+
+
+def h2d_bytes(*tensors) -> int:
+    return int(sum(t.numel() * t.element_size() for t in tensors if t is not None))
