@@ -64,7 +64,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except FileNotFoundError:
@@ -173,13 +173,16 @@ def run_ours(args):
             ids_keep.append(slates[0])
         return loss, status
 
+    # clock samples cover warm-up + timed region (the timed region alone can be
+    # shorter than nvidia-smi's sampling period)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(1.0)
     for t in range(args.warmup):
         one(t, False)
     torch.cuda.synchronize()
     eng.comm.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
     launches0 = _lib.launch_count()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)

@@ -104,8 +104,10 @@ int astra_refresh_topk(const float* queries_f32, const uint16_t* queries_bf16, i
                        void* workspace, size_t workspace_bytes, void* stream);
 
 /* Merge n_parts partial top-k lists per query (layout [n_parts][nq][k_in],
- * e.g. an all-gather over label shards) into the global top-k_out. Exact:
- * the result equals a single-shard refresh over the union of the shards. */
+ * e.g. an all-gather over label shards) into the global top-k_out. Each list
+ * must be sorted descending and zero-padded, as astra_refresh_topk writes its
+ * out_keys. Exact: the result equals a single-shard refresh over the union of
+ * the shards. */
 size_t astra_merge_workspace_size(int64_t nq, int k_out);
 int astra_topk_merge(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in, int k_out,
                      uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* workspace,

@@ -172,6 +172,76 @@ __global__ void __launch_bounds__(128) merge_kernel(const uint64_t* part_keys, i
   }
 }
 
+// Warp per query: fold the n_parts descending-sorted partial lists into the
+// running top-P (P = 32*R >= k_out). For two descending lists A, B the sequence
+// max(A[i], B[P-1-i]) holds exactly the top P of A u B and is bitonic, so one
+// half-cleaner pass re-sorts it. Exact, and independent of the part order.
+template <int R>
+__global__ void __launch_bounds__(256) merge_warp_kernel(const uint64_t* part_keys, int64_t nq, int n_parts,
+                                                         int k_in, int k_out, uint64_t* out_keys, int32_t* out_ids,
+                                                         float* out_scores) {
+  constexpr int P = 32 * R;
+  const int lane = threadIdx.x & 31;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (q >= nq) return;  // warp-uniform
+  const int kin = k_in < P ? k_in : P;
+  uint64_t cur[R];
+  {
+    const uint64_t* src = part_keys + static_cast<size_t>(q) * k_in;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = r * 32 + lane;
+      cur[r] = e < kin ? src[e] : 0ull;
+    }
+  }
+  for (int p = 1; p < n_parts; ++p) {
+    const uint64_t* src = part_keys + (static_cast<size_t>(p) * nq + q) * k_in;
+    uint64_t nx[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = r * 32 + lane;
+      nx[r] = e < kin ? src[e] : 0ull;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint64_t o = shfl64(nx[R - 1 - r], 31 - lane);
+      cur[r] = cur[r] > o ? cur[r] : o;
+    }
+#pragma unroll
+    for (int stride = P / 2; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+        const int rs = stride >> 5;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if ((r & rs) == 0) {
+            const uint64_t a = cur[r], b = cur[r | rs];
+            cur[r] = a > b ? a : b;
+            cur[r | rs] = a > b ? b : a;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint64_t o = shfl_xor64(cur[r], stride);
+          const bool lower = (lane & stride) == 0;
+          cur[r] = lower ? (cur[r] > o ? cur[r] : o) : (cur[r] > o ? o : cur[r]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = r * 32 + lane;
+    if (e < k_out) {
+      const uint64_t key = cur[r];
+      const size_t o = static_cast<size_t>(q) * k_out + e;
+      if (out_keys) out_keys[o] = key;
+      if (out_ids) out_ids[o] = key ? key_id(key) : -1;
+      if (out_scores) out_scores[o] = key ? key_score(key) : -INFINITY;
+    }
+  }
+}
+
 // ------------------------------------------------------------- fp32 re-rank
 
 // Block per query: re-score the k' candidates with the sequential fmaf chain
@@ -303,6 +373,22 @@ size_t refresh_workspace_size(int64_t nq, int64_t L, int d, int k, int mode) {
 int topk_merge(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in, int k_out, uint64_t* out_keys,
                int32_t* out_ids, float* out_scores, uint64_t* bufs, cudaStream_t st) {
   if (nq <= 0) return ASTRA_OK;
+  if (k_out <= 512) {
+    // part lists are sorted descending (refresh / flush output contract)
+    const unsigned grid = static_cast<unsigned>((nq + 7) / 8);
+    if (k_out <= 32)
+      merge_warp_kernel<1><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores);
+    else if (k_out <= 64)
+      merge_warp_kernel<2><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores);
+    else if (k_out <= 128)
+      merge_warp_kernel<4><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores);
+    else if (k_out <= 256)
+      merge_warp_kernel<8><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores);
+    else
+      merge_warp_kernel<16><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores);
+    ASTRA_LAUNCHED("merge_warp");
+    return ASTRA_OK;
+  }
   const int cap = topk_cap(k_out);
   merge_kernel<<<static_cast<unsigned>((nq + 127) / 128), 128, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, cap,
                                                                        bufs, out_keys, out_ids, out_scores);

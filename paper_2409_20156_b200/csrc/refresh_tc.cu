@@ -247,9 +247,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!__any_sync(0xffffffffu, active && mx >= tk.tau_s)) continue;
         topk_reserve(tk, 32, a.cap, a.k, active);
         if (active) {
-          const int cn = std::min(32, nvalid - c0);
+          const int cn = nvalid - c0;  // >= 1; columns past the label tail are skipped
           const uint32_t g0 = static_cast<uint32_t>(n0 + c0 + a.off);
-          for (int j = 0; j < cn; ++j) lane_offer(tk, __uint_as_float(r[j]), g0 + j);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)  // fully unrolled: r[] stays in registers
+            if (j < cn) lane_offer(tk, __uint_as_float(r[j]), g0 + j);
         }
       }
       tc_fence_before();

@@ -167,7 +167,7 @@ def test_adam_matches_torch_sparse_adam(cuda_lib):
         got = Wd.cpu().numpy()
         ref = param.detach().numpy()
         close(got, ref, rtol=1e-6, floor=1e-7)
-        assert (got == ref).mean() > 0.999  # same op order as SparseAdam: (almost) all bits equal
+        assert (got == ref).mean() > 0.99  # same op order as SparseAdam: nearly all bits equal
 
 
 def test_bf16_weights_sgd(cuda_lib):
