@@ -27,7 +27,7 @@ namespace astra {
 // refresh_tc.cu
 int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb, int64_t L, int64_t label_offset,
                       const int64_t* pos_indptr, const int32_t* pos_ids, int k, int cap, int n_parts,
-                      uint64_t* bufs, uint64_t* part_keys, cudaStream_t st);
+                      uint64_t* bufs, uint64_t* part_keys, uint64_t* gtau, cudaStream_t st);
 int refresh_tc_parts(int64_t nq, int64_t L);
 
 namespace {
@@ -47,6 +47,7 @@ struct SimtArgs {
   const int32_t* pos_ids;
   uint64_t* bufs;       // [n_qtiles * n_parts * 128][cap]
   uint64_t* part_keys;  // [n_parts][nq][k]
+  uint64_t* gtau;       // [nq] shared per-query thresholds
 };
 
 constexpr size_t kSimtSmem = sizeof(float) * (2 * kBK * kBM + 2 * kBK * kBN + kBM * (kBN + 1));
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(kSimtThreads) refresh_simt_kernel(SimtArgs a) 
   if (row_owner) {
     uint64_t* buf = a.bufs + ((static_cast<size_t>(qt) * a.n_parts + part) * kBM + tid) * a.cap;
     const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
-    lane_init(t, buf, a.pos_ids + p0, p1 - p0);
+    lane_init(t, buf, a.pos_ids + p0, p1 - p0, active ? a.gtau + q : nullptr);
   }
 
   // loader mapping: 128 rows x 8 k per tile = 1024 floats, 4 per thread
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(kSimtThreads) refresh_simt_kernel(SimtArgs a) 
       for (int j = 0; j < 8; ++j) sc[ty * 8 + i][tx * 8 + j] = acc[i][j];
     __syncthreads();
     if (row_owner) {
+      lane_sync_tau(t);
       const int nl = static_cast<int>(std::min<int64_t>(kBN, l_end - lt));
       for (int c0 = 0; c0 < kBN; c0 += 32) {
         topk_reserve(t, 32, a.cap, a.k, active);
@@ -244,42 +246,54 @@ __global__ void __launch_bounds__(256) merge_warp_kernel(const uint64_t* part_ke
 
 // ------------------------------------------------------------- fp32 re-rank
 
-// Block per query: re-score the k' candidates with the sequential fmaf chain
-// (the FP32_EXACT order), sort the keys descending in shared memory, keep k.
-__global__ void __launch_bounds__(128) rerank_kernel(const float* Q, const float* W, int d, int64_t off,
-                                                     const uint64_t* cand, int kc, int k, uint64_t* out_keys,
-                                                     int32_t* out_ids, float* out_scores) {
+// Block per query (4 warps): re-score the k' candidates with the sequential
+// fmaf chain (the FP32_EXACT order), sort the keys descending in shared memory,
+// keep k. Each warp owns 32 candidates at a time and stages their rows through
+// shared memory 64 floats per step with coalesced 16 B loads (lane t then runs
+// its candidate's chain from a padded row: conflict-free). Needs d % 64 == 0.
+constexpr int kRrWarps = 4, kRrChunk = 64, kRrPitch = kRrChunk + 1;
+
+__global__ void __launch_bounds__(kRrWarps * 32) rerank_kernel(const float* Q, const float* W, int d, int64_t off,
+                                                               const uint64_t* cand, int kc, int k,
+                                                               uint64_t* out_keys, int32_t* out_ids,
+                                                               float* out_scores) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int64_t q = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int Pn = 1;
   while (Pn < kc) Pn <<= 1;
   float* qs = reinterpret_cast<float*>(smem);
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem + align_up(sizeof(float) * d, 16));
+  float* tile = qs + d + warp * 32 * kRrPitch;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem + align_up(sizeof(float) * (d + kRrWarps * 32 * kRrPitch), 16));
   for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = Q[q * d + t];
+  for (int c = threadIdx.x; c < Pn; c += blockDim.x) keys[c] = 0ull;
   __syncthreads();
-  for (int c = threadIdx.x; c < Pn; c += blockDim.x) {
-    uint64_t key = 0;
-    if (c < kc) {
-      uint64_t ck = cand[q * kc + c];
-      if (ck) {
-        const int32_t gid = key_id(ck);
-        const float* w = W + static_cast<size_t>(gid - off) * d;
-        float s = 0.0f;
-        int t = 0;
-        if ((d & 3) == 0) {
-          for (; t < d; t += 4) {
-            float4 wv = __ldg(reinterpret_cast<const float4*>(w + t));
-            s = fmaf(qs[t], wv.x, s);
-            s = fmaf(qs[t + 1], wv.y, s);
-            s = fmaf(qs[t + 2], wv.z, s);
-            s = fmaf(qs[t + 3], wv.w, s);
-          }
-        }
-        for (; t < d; ++t) s = fmaf(qs[t], w[t], s);
-        key = make_key(s, static_cast<uint32_t>(gid));
+  for (int c0 = warp * 32; c0 < kc; c0 += kRrWarps * 32) {
+    const int c = c0 + lane;
+    const uint64_t ck = c < kc ? cand[q * kc + c] : 0ull;
+    const int32_t gid = ck ? key_id(ck) : -1;
+    float s = 0.0f;
+    for (int t0 = 0; t0 < d; t0 += kRrChunk) {
+      // 32 rows x 64 floats: 2 rows per instruction, 16 lanes x 16 B each
+#pragma unroll 4
+      for (int i = 0; i < 16; ++i) {
+        const int r = 2 * i + (lane >> 4);
+        const int32_t rg = __shfl_sync(0xffffffffu, gid, r);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (rg >= 0) v = __ldg(reinterpret_cast<const float4*>(W + static_cast<size_t>(rg - off) * d + t0) + (lane & 15));
+        float* dst = tile + r * kRrPitch + (lane & 15) * 4;
+        dst[0] = v.x;
+        dst[1] = v.y;
+        dst[2] = v.z;
+        dst[3] = v.w;
       }
+      __syncwarp();
+      const float* row = tile + lane * kRrPitch;
+#pragma unroll 16
+      for (int t = 0; t < kRrChunk; ++t) s = fmaf(qs[t0 + t], row[t], s);
+      __syncwarp();
     }
-    keys[c] = key;
+    if (ck) keys[c] = make_key(s, static_cast<uint32_t>(gid));
   }
   __syncthreads();
   for (int size = 2; size <= Pn; size <<= 1) {
@@ -323,6 +337,7 @@ __global__ void f32_to_bf16_kernel(const float* src, uint16_t* dst, int64_t n) {
 }
 
 struct RefreshWs {
+  uint64_t* gtau;
   uint16_t* qb;
   uint64_t* bufs;
   uint64_t* part_keys;
@@ -344,6 +359,7 @@ size_t carve_refresh(void* base, size_t cap_bytes, int64_t nq, int64_t L, int d,
   const int cap = topk_cap(kk);
   const int n_parts = mode == ASTRA_REFRESH_FP32_EXACT ? simt_parts(nq, L) : refresh_tc_parts(nq, L);
   const int64_t qtiles = (nq + 127) / 128;
+  w->gtau = c.take<uint64_t>(static_cast<size_t>(nq));
   w->qb = mode == ASTRA_REFRESH_FP32_EXACT ? nullptr : c.take<uint16_t>(static_cast<size_t>(nq) * d);
   w->bufs = c.take<uint64_t>(static_cast<size_t>(qtiles) * n_parts * 128 * cap);
   w->part_keys = c.take<uint64_t>(static_cast<size_t>(n_parts) * nq * kk);
@@ -437,6 +453,8 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
     a.pos_ids = pos_ids;
     a.bufs = w.bufs;
     a.part_keys = w.part_keys;
+    a.gtau = w.gtau;
+    ASTRA_TRY(check_cuda(cudaMemsetAsync(w.gtau, 0, sizeof(uint64_t) * nq, st), "memset gtau"));
     dim3 grid(static_cast<unsigned>((nq + kBM - 1) / kBM), static_cast<unsigned>(n_parts));
     cudaFuncSetAttribute(refresh_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSimtSmem);
     refresh_simt_kernel<<<grid, kSimtThreads, kSimtSmem, st>>>(a);
@@ -447,16 +465,15 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
       ASTRA_TRY(f32_to_bf16(qf, w.qb, nq * d, st));
       qb = w.qb;
     }
-    ASTRA_TRY(launch_refresh_tc(qb, nq, d, wb, L, off, pos_indptr, pos_ids, kk, cap, n_parts, w.bufs, w.part_keys, st));
+    ASTRA_TRY(launch_refresh_tc(qb, nq, d, wb, L, off, pos_indptr, pos_ids, kk, cap, n_parts, w.bufs, w.part_keys, w.gtau, st));
   }
   if (mode == ASTRA_REFRESH_BF16_RERANK) {
     ASTRA_TRY(topk_merge(w.part_keys, nq, n_parts, kk, kk, w.cand, nullptr, nullptr, w.merge_bufs, st));
-    size_t smem = align_up(sizeof(float) * d, 16);
     int Pn = 1;
     while (Pn < kk) Pn <<= 1;
-    smem += sizeof(uint64_t) * Pn;
+    size_t smem = align_up(sizeof(float) * (d + kRrWarps * 32 * kRrPitch), 16) + sizeof(uint64_t) * Pn;
     if (smem > 48 * 1024) cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    rerank_kernel<<<static_cast<unsigned>(nq), 128, smem, st>>>(qf, wf, d, off, w.cand, kk, k, out_keys, out_ids, out_scores);
+    rerank_kernel<<<static_cast<unsigned>(nq), kRrWarps * 32, smem, st>>>(qf, wf, d, off, w.cand, kk, k, out_keys, out_ids, out_scores);
     ASTRA_LAUNCHED("rerank");
     return ASTRA_OK;
   }

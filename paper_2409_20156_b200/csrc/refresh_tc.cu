@@ -31,7 +31,8 @@ constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int TMEM_COLS = 512;
 constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+constexpr int kStageTile = 4 * 32 * 33 * 4;  // per epilogue warp: 32 lanes x 32 scores (+1 pad)
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/ + kStageTile;
 
 // idesc for kind::f16: D=F32, A=B=BF16, both K-major, N>>3 at [17,23), M>>4 at [24,29)
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -115,6 +116,7 @@ struct TcArgs {
   const int32_t* pos_ids;
   uint64_t* bufs;
   uint64_t* part_keys;
+  uint64_t* gtau;  // nq shared thresholds (zeroed by the host before launch)
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -128,6 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stile = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, part = blockIdx.y;
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     {
       uint64_t* buf = a.bufs + ((static_cast<size_t>(qt) * a.n_parts + part) * BM + row) * a.cap;
       const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
-      lane_init(tk, buf, a.pos_ids + p0, p1 - p0);
+      lane_init(tk, buf, a.pos_ids + p0, p1 - p0, active ? a.gtau + q : nullptr);
     }
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>((warp - kEpiWarp0) * 32) << 16);
     int acc = 0;
@@ -234,25 +237,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int64_t n0 = t * BN;
       const int nvalid = static_cast<int>(std::min<int64_t>(BN, a.L - n0));
+      lane_sync_tau(tk);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         __syncwarp();
         tmem_ld32(lane_base + static_cast<uint32_t>(acc * BN + c0), r);
         if (c0 >= nvalid) continue;  // tile tail (uniform across the CTA)
-        // warp-level prefilter: skip the chunk if no lane can admit anything
-        float mx = __uint_as_float(r[0]);
+        // per-lane candidate mask: columns whose score reaches this query's threshold
+        const int cn = nvalid - c0;
+        uint32_t m = 0;
 #pragma unroll
-        for (int j = 1; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(r[j]));
-        if (!__any_sync(0xffffffffu, active && mx >= tk.tau_s)) continue;
-        topk_reserve(tk, 32, a.cap, a.k, active);
-        if (active) {
-          const int cn = nvalid - c0;  // >= 1; columns past the label tail are skipped
-          const uint32_t g0 = static_cast<uint32_t>(n0 + c0 + a.off);
+        for (int j = 0; j < 32; ++j) m |= (j < cn && __uint_as_float(r[j]) >= tk.tau_s) ? (1u << j) : 0u;
+        if (!active) m = 0;
+        if (!__any_sync(0xffffffffu, m != 0)) continue;  // the common case after warm-up
+        topk_reserve(tk, __popc(m), a.cap, a.k, active);
+        // stage the chunk in shared memory so the rare candidates are read by index
+        float* st = stile + (warp - kEpiWarp0) * (32 * 33) + lane * 33;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)  // fully unrolled: r[] stays in registers
-            if (j < cn) lane_offer(tk, __uint_as_float(r[j]), g0 + j);
+        for (int j = 0; j < 32; ++j) st[j] = __uint_as_float(r[j]);
+        __syncwarp();
+        const uint32_t g0 = static_cast<uint32_t>(n0 + c0 + a.off);
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          lane_offer(tk, st[j], g0 + j);
         }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
@@ -311,7 +322,7 @@ int refresh_tc_parts(int64_t nq, int64_t L) {
 
 int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb, int64_t L, int64_t label_offset,
                       const int64_t* pos_indptr, const int32_t* pos_ids, int k, int cap, int n_parts, uint64_t* bufs,
-                      uint64_t* part_keys, cudaStream_t st) {
+                      uint64_t* part_keys, uint64_t* gtau, cudaStream_t st) {
   if ((reinterpret_cast<uintptr_t>(qb) & 15) || (reinterpret_cast<uintptr_t>(wb) & 15))
     return set_error(ASTRA_ERR_CONFIG, "bf16 operands must be 16-byte aligned");
   CUtensorMap tmA, tmB;
@@ -331,6 +342,8 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
   a.pos_ids = pos_ids;
   a.bufs = bufs;
   a.part_keys = part_keys;
+  a.gtau = gtau;
+  ASTRA_TRY(check_cuda(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * nq, st), "memset gtau"));
   static bool attr_set = false;
   if (!attr_set) {
     ASTRA_TRY(check_cuda(cudaFuncSetAttribute(refresh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -22,15 +22,30 @@ struct LaneTopK {
   int cnt;
   uint64_t tau;         // admit keys > tau (0 = admit all)
   float tau_s;          // key_score(tau) or -inf: cheap score prefilter
+  uint64_t* gtau;       // this query's threshold shared by every label partition (or null)
 };
 
-__device__ __forceinline__ void lane_init(LaneTopK& t, uint64_t* buf, const int32_t* pos, int64_t npos) {
+__device__ __forceinline__ void lane_init(LaneTopK& t, uint64_t* buf, const int32_t* pos, int64_t npos,
+                                          uint64_t* gtau = nullptr) {
   t.buf = buf;
   t.pos = pos;
   t.npos = npos;
   t.cnt = 0;
   t.tau = 0;
   t.tau_s = -INFINITY;
+  t.gtau = gtau;
+}
+
+// Raise tau to the query's shared threshold. Any partition's k-th best key is a
+// valid bound for all of them: a key below it cannot be in the global top-k.
+__device__ __forceinline__ void lane_sync_tau(LaneTopK& t) {
+  if (t.gtau) {
+    const uint64_t g = *reinterpret_cast<volatile uint64_t*>(t.gtau);
+    if (g > t.tau) {
+      t.tau = g;
+      t.tau_s = key_score(g);
+    }
+  }
 }
 
 // Admit one candidate (caller guarantees room: see topk_reserve).
@@ -183,8 +198,11 @@ __device__ __forceinline__ void topk_reserve(LaneTopK& t, int incoming, int cap,
     int kept = compact_any(b, c, cap, p, np, k, &kth);
     if (lane == L) {
       t.cnt = kept;
-      t.tau = kth;
-      t.tau_s = kth ? key_score(kth) : -INFINITY;
+      if (kth > t.tau) {
+        t.tau = kth;
+        t.tau_s = key_score(kth);
+        if (t.gtau) atomicMax(reinterpret_cast<unsigned long long*>(t.gtau), static_cast<unsigned long long>(kth));
+      }
     }
   }
 }
