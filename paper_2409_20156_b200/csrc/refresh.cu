@@ -29,6 +29,7 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
                       const int64_t* pos_indptr, const int32_t* pos_ids, int k, int cap, int n_parts,
                       uint64_t* bufs, uint64_t* part_keys, uint64_t* gtau, cudaStream_t st);
 int refresh_tc_parts(int64_t nq, int64_t L);
+int refresh_tc_lists_per_part();
 
 namespace {
 
@@ -353,19 +354,21 @@ int simt_parts(int64_t nq, int64_t L) {
 }
 
 size_t carve_refresh(void* base, size_t cap_bytes, int64_t nq, int64_t L, int d, int k, int mode, RefreshWs* w,
-                     int* n_parts_out, int* kk_out) {
+                     int* n_parts_out, int* n_lists_out, int* kk_out) {
   Carve c(base, cap_bytes);
   const int kk = mode == ASTRA_REFRESH_BF16_RERANK ? 2 * k : k;  // candidates per query before re-rank
   const int cap = topk_cap(kk);
   const int n_parts = mode == ASTRA_REFRESH_FP32_EXACT ? simt_parts(nq, L) : refresh_tc_parts(nq, L);
+  const int n_lists = mode == ASTRA_REFRESH_FP32_EXACT ? n_parts : n_parts * refresh_tc_lists_per_part();
   const int64_t qtiles = (nq + 127) / 128;
   w->gtau = c.take<uint64_t>(static_cast<size_t>(nq));
   w->qb = mode == ASTRA_REFRESH_FP32_EXACT ? nullptr : c.take<uint16_t>(static_cast<size_t>(nq) * d);
-  w->bufs = c.take<uint64_t>(static_cast<size_t>(qtiles) * n_parts * 128 * cap);
-  w->part_keys = c.take<uint64_t>(static_cast<size_t>(n_parts) * nq * kk);
+  w->bufs = c.take<uint64_t>(static_cast<size_t>(qtiles) * n_lists * 128 * cap);
+  w->part_keys = c.take<uint64_t>(static_cast<size_t>(n_lists) * nq * kk);
   w->merge_bufs = c.take<uint64_t>(static_cast<size_t>(nq) * cap);
   w->cand = mode == ASTRA_REFRESH_BF16_RERANK ? c.take<uint64_t>(static_cast<size_t>(nq) * kk) : nullptr;
   *n_parts_out = n_parts;
+  *n_lists_out = n_lists;
   *kk_out = kk;
   return c.off;
 }
@@ -382,8 +385,8 @@ int f32_to_bf16(const float* src, uint16_t* dst, int64_t n, cudaStream_t st) {
 
 size_t refresh_workspace_size(int64_t nq, int64_t L, int d, int k, int mode) {
   RefreshWs w;
-  int np, kk;
-  return carve_refresh(nullptr, 0, nq, L, d, k, mode, &w, &np, &kk);
+  int np, nl, kk;
+  return carve_refresh(nullptr, 0, nq, L, d, k, mode, &w, &np, &nl, &kk);
 }
 
 int topk_merge(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in, int k_out, uint64_t* out_keys,
@@ -431,8 +434,8 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
     return set_error(ASTRA_ERR_CONFIG, "refresh: unknown mode %d", mode);
   }
   RefreshWs w;
-  int n_parts, kk;
-  size_t need = carve_refresh(ws, ws_bytes, nq, L, d, k, mode, &w, &n_parts, &kk);
+  int n_parts, n_lists, kk;
+  size_t need = carve_refresh(ws, ws_bytes, nq, L, d, k, mode, &w, &n_parts, &n_lists, &kk);
   if (!ws || ws_bytes < need) return set_error(ASTRA_ERR_CONFIG, "refresh workspace too small (%zu < %zu)", ws_bytes, need);
   if (nq == 0) return ASTRA_OK;
   const int cap = topk_cap(kk);
@@ -468,7 +471,7 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
     ASTRA_TRY(launch_refresh_tc(qb, nq, d, wb, L, off, pos_indptr, pos_ids, kk, cap, n_parts, w.bufs, w.part_keys, w.gtau, st));
   }
   if (mode == ASTRA_REFRESH_BF16_RERANK) {
-    ASTRA_TRY(topk_merge(w.part_keys, nq, n_parts, kk, kk, w.cand, nullptr, nullptr, w.merge_bufs, st));
+    ASTRA_TRY(topk_merge(w.part_keys, nq, n_lists, kk, kk, w.cand, nullptr, nullptr, w.merge_bufs, st));
     int Pn = 1;
     while (Pn < kk) Pn <<= 1;
     size_t smem = align_up(sizeof(float) * (d + kRrWarps * 32 * kRrPitch), 16) + sizeof(uint64_t) * Pn;
@@ -477,7 +480,7 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
     ASTRA_LAUNCHED("rerank");
     return ASTRA_OK;
   }
-  return topk_merge(w.part_keys, nq, n_parts, kk, k, out_keys, out_ids, out_scores, w.merge_bufs, st);
+  return topk_merge(w.part_keys, nq, n_lists, kk, k, out_keys, out_ids, out_scores, w.merge_bufs, st);
 }
 
 }  // namespace astra

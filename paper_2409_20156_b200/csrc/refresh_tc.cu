@@ -29,10 +29,11 @@ constexpr int A_STAGE = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int TMEM_COLS = 512;
-constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
-constexpr int kStageTile = 4 * 32 * 33 * 4;  // per epilogue warp: 32 lanes x 32 scores (+1 pad)
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/ + kStageTile;
+constexpr int kEpiSplit = 2;                            // epilogue warps per TMEM lane quadrant
+constexpr int kEpiWarps = 4 * kEpiSplit;                // each owns (32 query rows) x (BN / kEpiSplit columns)
+constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);  // 384
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
 
 // idesc for kind::f16: D=F32, A=B=BF16, both K-major, N>>3 at [17,23), M>>4 at [24,29)
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -108,6 +109,33 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Issue one 32-column TMEM load without waiting (pair with tmem_wait()).
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// r[j] for a run-time j without local memory: a 5-level select tree.
+__device__ __forceinline__ uint32_t pick32(const uint32_t* r, int j) {
+  uint32_t a[16], b[8], c[4], d[2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = (j & 16) ? r[i + 16] : r[i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) b[i] = (j & 8) ? a[i + 8] : a[i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = (j & 4) ? b[i + 4] : b[i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) d[i] = (j & 2) ? c[i + 2] : c[i];
+  return (j & 1) ? d[1] : d[0];
+}
+
 struct TcArgs {
   int64_t nq, L, off;
   int d, k, cap, n_parts;
@@ -130,7 +158,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* stile = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, part = blockIdx.y;
@@ -149,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -220,16 +247,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= kEpiWarp0) {
     // ---------------- epilogue: TMEM -> registers -> running top-k
-    const int row = (warp - kEpiWarp0) * 32 + lane;  // TMEM lane = query row in tile
+    // warp e = warp - 4 reads TMEM lanes 32*(e%4).. (its lane quadrant, = warp % 4)
+    // and columns [half*BN/2, (half+1)*BN/2) of every accumulator.
+    const int e = warp - kEpiWarp0, quad = e & 3, half = e >> 2;
+    const int row = quad * 32 + lane;  // TMEM lane = query row in tile
     const int64_t q = q0 + row;
     const bool active = q < a.nq;
+    const int list = part * kEpiSplit + half;  // independent partial list per column half
     LaneTopK tk;
     {
-      uint64_t* buf = a.bufs + ((static_cast<size_t>(qt) * a.n_parts + part) * BM + row) * a.cap;
+      uint64_t* buf = a.bufs + ((static_cast<size_t>(qt) * a.n_parts * kEpiSplit + list) * BM + row) * a.cap;
       const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
       lane_init(tk, buf, a.pos_ids + p0, p1 - p0, active ? a.gtau + q : nullptr);
     }
-    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>((warp - kEpiWarp0) * 32) << 16);
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+    constexpr int kCols = BN / kEpiSplit;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t t = t_begin; t < t_end; ++t) {
@@ -239,31 +271,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nvalid = static_cast<int>(std::min<int64_t>(BN, a.L - n0));
       lane_sync_tau(tk);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
+      for (int c0 = half * kCols; c0 < (half + 1) * kCols; c0 += 64) {
+        uint32_t r[64];
         __syncwarp();
-        tmem_ld32(lane_base + static_cast<uint32_t>(acc * BN + c0), r);
-        if (c0 >= nvalid) continue;  // tile tail (uniform across the CTA)
-        // per-lane candidate mask: columns whose score reaches this query's threshold
-        const int cn = nvalid - c0;
-        uint32_t m = 0;
+        tmem_ld32_nowait(lane_base + static_cast<uint32_t>(acc * BN + c0), r);
+        tmem_ld32_nowait(lane_base + static_cast<uint32_t>(acc * BN + c0 + 32), r + 32);
+        tmem_wait();
+        const int cn = nvalid - c0;  // valid columns in this 64-wide chunk (may exceed 64)
+        if (cn <= 0) continue;       // tile tail (uniform across the CTA)
+        float mx = -INFINITY;
+        if (cn >= 64) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) m |= (j < cn && __uint_as_float(r[j]) >= tk.tau_s) ? (1u << j) : 0u;
-        if (!active) m = 0;
-        if (!__any_sync(0xffffffffu, m != 0)) continue;  // the common case after warm-up
-        topk_reserve(tk, __popc(m), a.cap, a.k, active);
-        // stage the chunk in shared memory so the rare candidates are read by index
-        float* st = stile + (warp - kEpiWarp0) * (32 * 33) + lane * 33;
+          for (int j = 0; j < 64; ++j) mx = fmaxf(mx, __uint_as_float(r[j]));
+        } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) st[j] = __uint_as_float(r[j]);
-        __syncwarp();
-        const uint32_t g0 = static_cast<uint32_t>(n0 + c0 + a.off);
-        while (m) {
-          const int j = __ffs(m) - 1;
-          m &= m - 1;
-          lane_offer(tk, st[j], g0 + j);
+          for (int j = 0; j < 64; ++j)
+            if (j < cn) mx = fmaxf(mx, __uint_as_float(r[j]));
         }
-        __syncwarp();
+        if (!__any_sync(0xffffffffu, active && mx >= tk.tau_s)) continue;  // the common case
+        uint32_t m0 = 0, m1 = 0;
+        if (active) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            m0 |= (j < cn && __uint_as_float(r[j]) >= tk.tau_s) ? (1u << j) : 0u;
+            m1 |= (j + 32 < cn && __uint_as_float(r[j + 32]) >= tk.tau_s) ? (1u << j) : 0u;
+          }
+        }
+        topk_reserve(tk, __popc(m0) + __popc(m1), a.cap, a.k, active);
+        const uint32_t g0 = static_cast<uint32_t>(n0 + c0 + a.off);
+        while (m0) {
+          const int j = __ffs(m0) - 1;
+          m0 &= m0 - 1;
+          lane_offer(tk, __uint_as_float(pick32(r, j)), g0 + j);
+        }
+        while (m1) {
+          const int j = __ffs(m1) - 1;
+          m1 &= m1 - 1;
+          lane_offer(tk, __uint_as_float(pick32(r + 32, j)), g0 + 32 + j);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -273,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
-    uint64_t* out = a.part_keys + (static_cast<size_t>(part) * a.nq + (active ? q : 0)) * a.k;
+    uint64_t* out = a.part_keys + (static_cast<size_t>(list) * a.nq + (active ? q : 0)) * a.k;
     topk_flush(tk, a.cap, a.k, active, out);
   }
 
@@ -312,6 +357,8 @@ int make_map(CUtensorMap* m, const void* base, int64_t rows, int d, int box_rows
 }
 
 }  // namespace
+
+int refresh_tc_lists_per_part() { return kEpiSplit; }
 
 int refresh_tc_parts(int64_t nq, int64_t L) {
   const int64_t qtiles = (nq + BM - 1) / BM;
