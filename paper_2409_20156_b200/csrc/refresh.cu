@@ -26,10 +26,10 @@ namespace astra {
 
 // refresh_tc.cu
 int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb, int64_t L, int64_t label_offset,
-                      const int64_t* pos_indptr, const int32_t* pos_ids, int k, int cap, int n_parts,
-                      uint64_t* bufs, uint64_t* part_keys, uint64_t* gtau, cudaStream_t st);
-int refresh_tc_parts(int64_t nq, int64_t L);
-int refresh_tc_lists_per_part();
+                      const int64_t* pos_indptr, const int32_t* pos_ids, int k, int cap, uint64_t* bufs,
+                      uint64_t* part_keys, uint64_t* gtau, cudaStream_t st);
+void refresh_tc_layout(int64_t nq, int64_t L, int* n_ctas, int* n_lists);
+int refresh_tc_split();
 
 namespace {
 
@@ -358,12 +358,20 @@ size_t carve_refresh(void* base, size_t cap_bytes, int64_t nq, int64_t L, int d,
   Carve c(base, cap_bytes);
   const int kk = mode == ASTRA_REFRESH_BF16_RERANK ? 2 * k : k;  // candidates per query before re-rank
   const int cap = topk_cap(kk);
-  const int n_parts = mode == ASTRA_REFRESH_FP32_EXACT ? simt_parts(nq, L) : refresh_tc_parts(nq, L);
-  const int n_lists = mode == ASTRA_REFRESH_FP32_EXACT ? n_parts : n_parts * refresh_tc_lists_per_part();
-  const int64_t qtiles = (nq + 127) / 128;
+  int n_parts, n_lists;
+  size_t n_bufs;  // per-lane candidate buffers
+  if (mode == ASTRA_REFRESH_FP32_EXACT) {
+    n_parts = n_lists = simt_parts(nq, L);
+    n_bufs = static_cast<size_t>((nq + 127) / 128) * n_parts * 128;
+  } else {
+    int n_ctas;
+    refresh_tc_layout(nq, L, &n_ctas, &n_lists);
+    n_parts = n_lists;
+    n_bufs = static_cast<size_t>(n_ctas) * refresh_tc_split() * 128;
+  }
   w->gtau = c.take<uint64_t>(static_cast<size_t>(nq));
   w->qb = mode == ASTRA_REFRESH_FP32_EXACT ? nullptr : c.take<uint16_t>(static_cast<size_t>(nq) * d);
-  w->bufs = c.take<uint64_t>(static_cast<size_t>(qtiles) * n_lists * 128 * cap);
+  w->bufs = c.take<uint64_t>(n_bufs * cap);
   w->part_keys = c.take<uint64_t>(static_cast<size_t>(n_lists) * nq * kk);
   w->merge_bufs = c.take<uint64_t>(static_cast<size_t>(nq) * cap);
   w->cand = mode == ASTRA_REFRESH_BF16_RERANK ? c.take<uint64_t>(static_cast<size_t>(nq) * kk) : nullptr;
@@ -468,7 +476,7 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
       ASTRA_TRY(f32_to_bf16(qf, w.qb, nq * d, st));
       qb = w.qb;
     }
-    ASTRA_TRY(launch_refresh_tc(qb, nq, d, wb, L, off, pos_indptr, pos_ids, kk, cap, n_parts, w.bufs, w.part_keys, w.gtau, st));
+    ASTRA_TRY(launch_refresh_tc(qb, nq, d, wb, L, off, pos_indptr, pos_ids, kk, cap, w.bufs, w.part_keys, w.gtau, st));
   }
   if (mode == ASTRA_REFRESH_BF16_RERANK) {
     ASTRA_TRY(topk_merge(w.part_keys, nq, n_lists, kk, kk, w.cand, nullptr, nullptr, w.merge_bufs, st));

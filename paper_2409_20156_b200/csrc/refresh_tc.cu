@@ -97,18 +97,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
 // Issue one 32-column TMEM load without waiting (pair with tmem_wait()).
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
   asm volatile(
@@ -138,14 +126,36 @@ __device__ __forceinline__ uint32_t pick32(const uint32_t* r, int j) {
 
 struct TcArgs {
   int64_t nq, L, off;
-  int d, k, cap, n_parts;
-  int64_t tiles_per_part;
+  int d, k, cap;
+  int64_t n_lt, total;  // label tiles per query tile; n_qt * n_lt work units
   const int64_t* pos_indptr;
   const int32_t* pos_ids;
   uint64_t* bufs;
   uint64_t* part_keys;
   uint64_t* gtau;  // nq shared thresholds (zeroed by the host before launch)
 };
+
+// Static "stream-K" schedule: the n_qt x n_lt (query tile, label tile) units
+// are linearised query-tile-major and cut into gridDim.x equal contiguous
+// ranges, so every CTA gets the same number of MMA tiles for any batch size.
+// A range covers one or a few (query tile, label-tile run) segments; the lane
+// state restarts at each segment and the segment's partial list goes to slot
+// (cta - first cta of that query tile).
+struct Seg {
+  int64_t qt, lt0, lt1;
+  int slot;
+};
+
+__device__ __forceinline__ bool next_seg(int64_t& u, int64_t u1, const TcArgs& a, Seg& s) {
+  if (u >= u1) return false;
+  s.qt = u / a.n_lt;
+  s.lt0 = u - s.qt * a.n_lt;
+  const int64_t end = std::min<int64_t>(u1, (s.qt + 1) * a.n_lt);
+  s.lt1 = s.lt0 + (end - u);
+  s.slot = static_cast<int>(blockIdx.x - (s.qt * a.n_lt * gridDim.x) / a.total);
+  u = end;
+  return true;
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     refresh_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
@@ -160,11 +170,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, part = blockIdx.y;
-  const int64_t q0 = static_cast<int64_t>(qt) * BM;
-  const int64_t n_tiles = (a.L + BN - 1) / BN;
-  const int64_t t_begin = static_cast<int64_t>(part) * a.tiles_per_part;
-  const int64_t t_end = std::min<int64_t>(n_tiles, t_begin + a.tiles_per_part);
+  const int64_t u_begin = (static_cast<int64_t>(blockIdx.x) * a.total + gridDim.x - 1) / gridDim.x;
+  const int64_t u_end = (static_cast<int64_t>(blockIdx.x + 1) * a.total + gridDim.x - 1) / gridDim.x;
   const int nkb = a.d / BK;
 
   if (warp == 0 && lane == 0) {
@@ -195,16 +202,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = t_begin; t < t_end; ++t) {
-        const int n0 = static_cast<int>(t * BN);
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, static_cast<int>(q0));
-          tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+      int64_t u = u_begin;
+      Seg sg;
+      while (next_seg(u, u_end, a, sg)) {
+        const int q0 = static_cast<int>(sg.qt * BM);
+        for (int64_t t = sg.lt0; t < sg.lt1; ++t) {
+          const int n0 = static_cast<int>(t * BN);
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], STAGE_BYTES);
+            tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, q0);
+            tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -215,7 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t t = t_begin; t < t_end; ++t) {
+    const int64_t n_units = u_end - u_begin;  // MMA tiles of this CTA, in schedule order
+    for (int64_t t = 0; t < n_units; ++t) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -251,75 +264,79 @@ __global__ void __launch_bounds__(kThreads, 1)
     // and columns [half*BN/2, (half+1)*BN/2) of every accumulator.
     const int e = warp - kEpiWarp0, quad = e & 3, half = e >> 2;
     const int row = quad * 32 + lane;  // TMEM lane = query row in tile
-    const int64_t q = q0 + row;
-    const bool active = q < a.nq;
-    const int list = part * kEpiSplit + half;  // independent partial list per column half
-    LaneTopK tk;
-    {
-      uint64_t* buf = a.bufs + ((static_cast<size_t>(qt) * a.n_parts * kEpiSplit + list) * BM + row) * a.cap;
-      const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
-      lane_init(tk, buf, a.pos_ids + p0, p1 - p0, active ? a.gtau + q : nullptr);
-    }
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+    uint64_t* buf = a.bufs + ((static_cast<size_t>(blockIdx.x) * kEpiSplit + half) * BM + row) * a.cap;
     constexpr int kCols = BN / kEpiSplit;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t t = t_begin; t < t_end; ++t) {
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const int64_t n0 = t * BN;
-      const int nvalid = static_cast<int>(std::min<int64_t>(BN, a.L - n0));
-      lane_sync_tau(tk);
+    int64_t u = u_begin;
+    Seg sg;
+    while (next_seg(u, u_end, a, sg)) {
+      const int64_t q = sg.qt * BM + row;
+      const bool active = q < a.nq;
+      LaneTopK tk;
+      {
+        const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
+        lane_init(tk, buf, a.pos_ids + p0, p1 - p0, active ? a.gtau + q : nullptr);
+      }
+      for (int64_t t = sg.lt0; t < sg.lt1; ++t) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const int64_t n0 = t * BN;
+        const int nvalid = static_cast<int>(std::min<int64_t>(BN, a.L - n0));
+        lane_sync_tau(tk);
 #pragma unroll 1
-      for (int c0 = half * kCols; c0 < (half + 1) * kCols; c0 += 64) {
-        uint32_t r[64];
-        __syncwarp();
-        tmem_ld32_nowait(lane_base + static_cast<uint32_t>(acc * BN + c0), r);
-        tmem_ld32_nowait(lane_base + static_cast<uint32_t>(acc * BN + c0 + 32), r + 32);
-        tmem_wait();
-        const int cn = nvalid - c0;  // valid columns in this 64-wide chunk (may exceed 64)
-        if (cn <= 0) continue;       // tile tail (uniform across the CTA)
-        float mx = -INFINITY;
-        if (cn >= 64) {
+        for (int c0 = half * kCols; c0 < (half + 1) * kCols; c0 += 64) {
+          uint32_t r[64];
+          __syncwarp();
+          tmem_ld32_nowait(lane_base + static_cast<uint32_t>(acc * BN + c0), r);
+          tmem_ld32_nowait(lane_base + static_cast<uint32_t>(acc * BN + c0 + 32), r + 32);
+          tmem_wait();
+          const int cn = nvalid - c0;  // valid columns in this 64-wide chunk (may exceed 64)
+          if (cn <= 0) continue;       // tile tail (uniform across the CTA)
+          float mx = -INFINITY;
+          if (cn >= 64) {
 #pragma unroll
-          for (int j = 0; j < 64; ++j) mx = fmaxf(mx, __uint_as_float(r[j]));
-        } else {
+            for (int j = 0; j < 64; ++j) mx = fmaxf(mx, __uint_as_float(r[j]));
+          } else {
 #pragma unroll
-          for (int j = 0; j < 64; ++j)
-            if (j < cn) mx = fmaxf(mx, __uint_as_float(r[j]));
-        }
-        if (!__any_sync(0xffffffffu, active && mx >= tk.tau_s)) continue;  // the common case
-        uint32_t m0 = 0, m1 = 0;
-        if (active) {
+            for (int j = 0; j < 64; ++j)
+              if (j < cn) mx = fmaxf(mx, __uint_as_float(r[j]));
+          }
+          if (!__any_sync(0xffffffffu, active && mx >= tk.tau_s)) continue;  // the common case
+          uint32_t m0 = 0, m1 = 0;
+          if (active) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            m0 |= (j < cn && __uint_as_float(r[j]) >= tk.tau_s) ? (1u << j) : 0u;
-            m1 |= (j + 32 < cn && __uint_as_float(r[j + 32]) >= tk.tau_s) ? (1u << j) : 0u;
+            for (int j = 0; j < 32; ++j) {
+              m0 |= (j < cn && __uint_as_float(r[j]) >= tk.tau_s) ? (1u << j) : 0u;
+              m1 |= (j + 32 < cn && __uint_as_float(r[j + 32]) >= tk.tau_s) ? (1u << j) : 0u;
+            }
+          }
+          topk_reserve(tk, __popc(m0) + __popc(m1), a.cap, a.k, active);
+          const uint32_t g0 = static_cast<uint32_t>(n0 + c0 + a.off);
+          while (m0) {
+            const int j = __ffs(m0) - 1;
+            m0 &= m0 - 1;
+            lane_offer(tk, __uint_as_float(pick32(r, j)), g0 + j);
+          }
+          while (m1) {
+            const int j = __ffs(m1) - 1;
+            m1 &= m1 - 1;
+            lane_offer(tk, __uint_as_float(pick32(r + 32, j)), g0 + 32 + j);
           }
         }
-        topk_reserve(tk, __popc(m0) + __popc(m1), a.cap, a.k, active);
-        const uint32_t g0 = static_cast<uint32_t>(n0 + c0 + a.off);
-        while (m0) {
-          const int j = __ffs(m0) - 1;
-          m0 &= m0 - 1;
-          lane_offer(tk, __uint_as_float(pick32(r, j)), g0 + j);
-        }
-        while (m1) {
-          const int j = __ffs(m1) - 1;
-          m1 &= m1 - 1;
-          lane_offer(tk, __uint_as_float(pick32(r + 32, j)), g0 + 32 + j);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
+      const int list = sg.slot * kEpiSplit + half;
+      uint64_t* out = a.part_keys + (static_cast<size_t>(list) * a.nq + (active ? q : 0)) * a.k;
+      topk_flush(tk, a.cap, a.k, active, out);
     }
-    uint64_t* out = a.part_keys + (static_cast<size_t>(list) * a.nq + (active ? q : 0)) * a.k;
-    topk_flush(tk, a.cap, a.k, active, out);
   }
 
   tc_fence_before();
@@ -358,23 +375,36 @@ int make_map(CUtensorMap* m, const void* base, int64_t rows, int d, int box_rows
 
 }  // namespace
 
-int refresh_tc_lists_per_part() { return kEpiSplit; }
+int refresh_tc_split() { return kEpiSplit; }
 
-int refresh_tc_parts(int64_t nq, int64_t L) {
-  const int64_t qtiles = (nq + BM - 1) / BM;
-  const int64_t n_tiles = std::max<int64_t>(1, (L + BN - 1) / BN);
-  int64_t parts = std::max<int64_t>(1, num_sms() / std::max<int64_t>(1, qtiles));
-  return static_cast<int>(std::min<int64_t>(parts, n_tiles));
+// Grid size and number of partial lists per query for a refresh of nq queries
+// over L labels (see next_seg).
+void refresh_tc_layout(int64_t nq, int64_t L, int* n_ctas, int* n_lists) {
+  const int64_t n_qt = std::max<int64_t>(1, (nq + BM - 1) / BM);
+  const int64_t n_lt = std::max<int64_t>(1, (L + BN - 1) / BN);
+  const int64_t total = n_qt * n_lt;
+  const int64_t G = std::min<int64_t>(num_sms(), total);
+  int64_t slots = 1;
+  for (int64_t qt = 0; qt < n_qt; ++qt) {
+    const int64_t c0 = (qt * n_lt * G) / total;
+    const int64_t c1 = ((qt + 1) * n_lt - 1) * G / total;
+    slots = std::max<int64_t>(slots, c1 - c0 + 1);
+  }
+  *n_ctas = static_cast<int>(G);
+  *n_lists = static_cast<int>(slots) * kEpiSplit;
 }
 
 int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb, int64_t L, int64_t label_offset,
-                      const int64_t* pos_indptr, const int32_t* pos_ids, int k, int cap, int n_parts, uint64_t* bufs,
+                      const int64_t* pos_indptr, const int32_t* pos_ids, int k, int cap, uint64_t* bufs,
                       uint64_t* part_keys, uint64_t* gtau, cudaStream_t st) {
   if ((reinterpret_cast<uintptr_t>(qb) & 15) || (reinterpret_cast<uintptr_t>(wb) & 15))
     return set_error(ASTRA_ERR_CONFIG, "bf16 operands must be 16-byte aligned");
+  if (L <= 0) return ASTRA_OK;
+  int G, n_lists;
+  refresh_tc_layout(nq, L, &G, &n_lists);
   CUtensorMap tmA, tmB;
   ASTRA_TRY(make_map(&tmA, qb, nq, d, BM));
-  ASTRA_TRY(make_map(&tmB, wb, std::max<int64_t>(L, 1), d, BN));
+  ASTRA_TRY(make_map(&tmB, wb, L, d, BN));
   TcArgs a;
   a.nq = nq;
   a.L = L;
@@ -382,15 +412,16 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
   a.d = d;
   a.k = k;
   a.cap = cap;
-  a.n_parts = n_parts;
-  const int64_t n_tiles = (L + BN - 1) / BN;
-  a.tiles_per_part = (n_tiles + n_parts - 1) / n_parts;
+  a.n_lt = (L + BN - 1) / BN;
+  a.total = ((nq + BM - 1) / BM) * a.n_lt;
   a.pos_indptr = pos_indptr;
   a.pos_ids = pos_ids;
   a.bufs = bufs;
   a.part_keys = part_keys;
   a.gtau = gtau;
   ASTRA_TRY(check_cuda(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * nq, st), "memset gtau"));
+  // slots a query tile does not use stay empty (key 0) for the merge
+  ASTRA_TRY(check_cuda(cudaMemsetAsync(part_keys, 0, sizeof(uint64_t) * n_lists * nq * k, st), "memset part keys"));
   static bool attr_set = false;
   if (!attr_set) {
     ASTRA_TRY(check_cuda(cudaFuncSetAttribute(refresh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -398,8 +429,7 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
                          "smem attr"));
     attr_set = true;
   }
-  dim3 grid(static_cast<unsigned>((nq + BM - 1) / BM), static_cast<unsigned>(n_parts));
-  refresh_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(tmA, tmB, a);
+  refresh_tc_kernel<<<G, kThreads, kSmemBytes, st>>>(tmA, tmB, a);
   ASTRA_LAUNCHED("refresh_tc");
   return ASTRA_OK;
 }
