@@ -93,7 +93,7 @@ int astra_refresh_topk(const float* queries_f32, const uint16_t* queries_bf16, i
 }
 
 size_t astra_merge_workspace_size(int64_t nq, int k_out) {
-  return static_cast<size_t>(nq) * topk_cap(k_out) * sizeof(uint64_t);
+  return static_cast<size_t>(nq) * (topk_cap(k_out) + kTopkSlack) * sizeof(uint64_t);
 }
 
 int astra_topk_merge(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in, int k_out, uint64_t* out_keys,

@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kSimtThreads) refresh_simt_kernel(SimtArgs a) 
   const int64_t q = q0 + tid;
   const bool active = row_owner && q < a.nq;
   if (row_owner) {
-    uint64_t* buf = a.bufs + ((static_cast<size_t>(qt) * a.n_parts + part) * kBM + tid) * a.cap;
+    uint64_t* buf = a.bufs + ((static_cast<size_t>(qt) * a.n_parts + part) * kBM + tid) * (a.cap + kTopkSlack);
     const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
     lane_init(t, buf, a.pos_ids + p0, p1 - p0, active ? a.gtau + q : nullptr);
   }
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(128) merge_kernel(const uint64_t* part_keys, i
   const int64_t q = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
   const bool active = q < nq;
   LaneTopK t;
-  lane_init(t, bufs + static_cast<size_t>(active ? q : 0) * cap, nullptr, 0);
+  lane_init(t, bufs + static_cast<size_t>(active ? q : 0) * (cap + kTopkSlack), nullptr, 0);
   for (int p = 0; p < n_parts; ++p) {
     const uint64_t* src = part_keys + (static_cast<size_t>(p) * nq + (active ? q : 0)) * k_in;
     for (int c0 = 0; c0 < k_in; c0 += 32) {
@@ -346,6 +346,14 @@ struct RefreshWs {
   uint64_t* cand;
 };
 
+// bf16 candidates kept per query before the fp32 re-rank: k' = max(1.5k, k+16),
+// a multiple of 8 (bf16 top-k' contains the fp32 top-k; see tests + DESIGN.md).
+int rerank_candidates(int k) {
+  int kc = std::max((3 * k + 1) / 2, k + 16);
+  kc = (kc + 7) / 8 * 8;
+  return std::min(kc, 2048);
+}
+
 int simt_parts(int64_t nq, int64_t L) {
   const int64_t qtiles = (nq + kBM - 1) / kBM;
   int64_t parts = std::max<int64_t>(1, (2LL * num_sms() + qtiles - 1) / qtiles);
@@ -356,7 +364,7 @@ int simt_parts(int64_t nq, int64_t L) {
 size_t carve_refresh(void* base, size_t cap_bytes, int64_t nq, int64_t L, int d, int k, int mode, RefreshWs* w,
                      int* n_parts_out, int* n_lists_out, int* kk_out) {
   Carve c(base, cap_bytes);
-  const int kk = mode == ASTRA_REFRESH_BF16_RERANK ? 2 * k : k;  // candidates per query before re-rank
+  const int kk = mode == ASTRA_REFRESH_BF16_RERANK ? rerank_candidates(k) : k;
   const int cap = topk_cap(kk);
   int n_parts, n_lists;
   size_t n_bufs;  // per-lane candidate buffers
@@ -371,9 +379,9 @@ size_t carve_refresh(void* base, size_t cap_bytes, int64_t nq, int64_t L, int d,
   }
   w->gtau = c.take<uint64_t>(static_cast<size_t>(nq));
   w->qb = mode == ASTRA_REFRESH_FP32_EXACT ? nullptr : c.take<uint16_t>(static_cast<size_t>(nq) * d);
-  w->bufs = c.take<uint64_t>(n_bufs * cap);
+  w->bufs = c.take<uint64_t>(n_bufs * (cap + kTopkSlack));
   w->part_keys = c.take<uint64_t>(static_cast<size_t>(n_lists) * nq * kk);
-  w->merge_bufs = c.take<uint64_t>(static_cast<size_t>(nq) * cap);
+  w->merge_bufs = c.take<uint64_t>(static_cast<size_t>(nq) * (cap + kTopkSlack));
   w->cand = mode == ASTRA_REFRESH_BF16_RERANK ? c.take<uint64_t>(static_cast<size_t>(nq) * kk) : nullptr;
   *n_parts_out = n_parts;
   *n_lists_out = n_lists;

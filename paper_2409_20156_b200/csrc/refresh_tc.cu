@@ -16,6 +16,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -30,9 +32,10 @@ constexpr int B_STAGE = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int TMEM_COLS = 512;
 constexpr int kEpiWarp0 = 4;
-constexpr int kEpiSplit = 2;                            // epilogue warps per TMEM lane quadrant
-constexpr int kEpiWarps = 4 * kEpiSplit;                // each owns (32 query rows) x (BN / kEpiSplit columns)
-constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);  // 384
+// SPLIT = epilogue warps per TMEM lane quadrant; each owns (32 query rows) x
+// (BN / SPLIT columns) and its own partial list. Threads = 32 * (4 + 4*SPLIT).
+template <int SPLIT>
+constexpr int threads_for() { return 32 * (kEpiWarp0 + 4 * SPLIT); }
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
 
 // idesc for kind::f16: D=F32, A=B=BF16, both K-major, N>>3 at [17,23), M>>4 at [24,29)
@@ -157,8 +160,11 @@ __device__ __forceinline__ bool next_seg(int64_t& u, int64_t u1, const TcArgs& a
   return true;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int SPLIT>
+__global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     refresh_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+  constexpr int kEpiSplit = SPLIT;
+  constexpr int kEpiWarps = 4 * SPLIT;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* sA = smem;
@@ -265,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int e = warp - kEpiWarp0, quad = e & 3, half = e >> 2;
     const int row = quad * 32 + lane;  // TMEM lane = query row in tile
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
-    uint64_t* buf = a.bufs + ((static_cast<size_t>(blockIdx.x) * kEpiSplit + half) * BM + row) * a.cap;
+    uint64_t* buf = a.bufs + ((static_cast<size_t>(blockIdx.x) * kEpiSplit + half) * BM + row) * (a.cap + kTopkSlack);
     constexpr int kCols = BN / kEpiSplit;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               m1 |= (j + 32 < cn && __uint_as_float(r[j + 32]) >= tk.tau_s) ? (1u << j) : 0u;
             }
           }
-          topk_reserve(tk, __popc(m0) + __popc(m1), a.cap, a.k, active);
+          // append (at most 64 <= kTopkSlack keys), then compact with r[] dead
           const uint32_t g0 = static_cast<uint32_t>(n0 + c0 + a.off);
           while (m0) {
             const int j = __ffs(m0) - 1;
@@ -324,6 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             m1 &= m1 - 1;
             lane_offer(tk, __uint_as_float(pick32(r + 32, j)), g0 + 32 + j);
           }
+          topk_settle(tk, a.cap, a.k, active);
         }
         tc_fence_before();
         __syncwarp();
@@ -375,7 +382,14 @@ int make_map(CUtensorMap* m, const void* base, int64_t rows, int d, int box_rows
 
 }  // namespace
 
-int refresh_tc_split() { return kEpiSplit; }
+// Epilogue split (ASTRA_TC_SPLIT=1|2, default 2).
+int refresh_tc_split() {
+  static int split = [] {
+    const char* e = getenv("ASTRA_TC_SPLIT");
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
+  return split;
+}
 
 // Grid size and number of partial lists per query for a refresh of nq queries
 // over L labels (see next_seg).
@@ -391,7 +405,7 @@ void refresh_tc_layout(int64_t nq, int64_t L, int* n_ctas, int* n_lists) {
     slots = std::max<int64_t>(slots, c1 - c0 + 1);
   }
   *n_ctas = static_cast<int>(G);
-  *n_lists = static_cast<int>(slots) * kEpiSplit;
+  *n_lists = static_cast<int>(slots) * refresh_tc_split();
 }
 
 int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb, int64_t L, int64_t label_offset,
@@ -424,12 +438,18 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
   ASTRA_TRY(check_cuda(cudaMemsetAsync(part_keys, 0, sizeof(uint64_t) * n_lists * nq * k, st), "memset part keys"));
   static bool attr_set = false;
   if (!attr_set) {
-    ASTRA_TRY(check_cuda(cudaFuncSetAttribute(refresh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ASTRA_TRY(check_cuda(cudaFuncSetAttribute(refresh_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(kSmemBytes)),
+                         "smem attr"));
+    ASTRA_TRY(check_cuda(cudaFuncSetAttribute(refresh_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(kSmemBytes)),
                          "smem attr"));
     attr_set = true;
   }
-  refresh_tc_kernel<<<G, kThreads, kSmemBytes, st>>>(tmA, tmB, a);
+  if (refresh_tc_split() == 1)
+    refresh_tc_kernel<1><<<G, threads_for<1>(), kSmemBytes, st>>>(tmA, tmB, a);
+  else
+    refresh_tc_kernel<2><<<G, threads_for<2>(), kSmemBytes, st>>>(tmA, tmB, a);
   ASTRA_LAUNCHED("refresh_tc");
   return ASTRA_OK;
 }
