@@ -2,16 +2,18 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step = one pass of the hot path over one batch of B=1024 query rows per GPU
-at the LF-AmazonTitles-1.3M shape (BASELINE.json configs[3]: L=1,305,265,
-d=768): shortlist refresh of the batch's queries against the whole label set
-(bf16 tcgen05 GEMM + fused top-k + fp32 re-rank, k_h=64), Philox slates
-(k_p=8, k_h=64, k_r=512 -> S=584), fused sampled-BCE fwd/bwd + SGD update of
-the fp32 W. This is the composite "train samples/s (shortlist+loss+update)"
-with every training row refreshed once per epoch (tau_r = 1, the most
-refresh-heavy schedule); refresh-only MIPS q/s and step-only samples/s are
-reported beside it. Multi-GPU: W label-sharded, per-GPU batch fixed (weak
-scaling), NCCL all-gather / reduce-scatter as in paper_2409_20156_b200/shard.py.
+A step = one pass of the hot path over one batch of 8192 query rows per GPU at
+the LF-AmazonTitles-1.3M shape (BASELINE.json configs[3]: L=1,305,265, d=768):
+the shortlist refresh of the batch's 8192 queries against the whole label set
+(bf16 tcgen05 GEMM + fused top-k + fp32 re-rank, k_h=64; the reference refreshes
+all N rows in one batched call, anns.py:253) and the training of the same rows
+as 8 SGD minibatches of B=1024: Philox slates (k_p=8, k_h=64, k_r=512 -> S=584)
++ fused sampled-BCE fwd/bwd + SGD update of the fp32 W. This is the composite
+"train samples/s (shortlist+loss+update)" with every training row refreshed
+once per epoch (tau_r = 1, the most refresh-heavy schedule); refresh-only MIPS
+q/s and step-only samples/s are reported beside it. Multi-GPU: W label-sharded,
+per-GPU batch fixed (weak scaling), NCCL all-gather / reduce-scatter as in
+paper_2409_20156_b200/shard.py.
 
 --impl reference times the reference's own CPU algorithm (oracle/xcmix_port.py,
 a bit-pinned restatement of xcmix — /root/reference is absent on the GPU box)
@@ -36,7 +38,7 @@ sys.path.insert(0, ROOT)
 
 # C4 = LF-AmazonTitles-1.3M shape, slate from SURVEY.md §8
 CFG = dict(workload="LF-AmazonTitles-1.3M shape, synthetic", L=1_305_265, d=768, N=2_248_619, B=1024,
-           k_p=8, k_h=64, k_r=512, labels_per_point=38, tau_r=1, lr=0.05, wd=1e-4)
+           minibatches=8, k_p=8, k_h=64, k_r=512, labels_per_point=38, tau_r=1, lr=0.05, wd=1e-4)
 METRIC = "ASTRA train samples/s (shortlist+loss+update)"
 UNIT = "samples/s"
 
@@ -102,12 +104,12 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ data
-def make_batches(rng, n_batches, B, L, lpp, N, rank, world):
-    """Synthetic batches: global row ids, positives (labels_per_point distinct
-    uniform labels per row, sorted), embeddings N(0,1) fp32."""
+def make_batches(rng, n_batches, B, L, lpp, N, slot, n_slots):
+    """Synthetic minibatches: global row ids, positives (labels_per_point
+    distinct uniform labels per row, sorted), embeddings N(0,1) fp32."""
     out = []
     for t in range(n_batches):
-        rows = ((t * world + rank) * B + np.arange(B, dtype=np.int64)) % N
+        rows = ((slot * n_batches + t) * B + np.arange(B, dtype=np.int64)) % N
         pos = np.sort(rng.integers(0, L, size=(B, lpp)), axis=1)
         # distinct per row: collisions are rare at L=1.3M; drop duplicates
         indptr = np.zeros(B + 1, np.int64)
@@ -136,41 +138,52 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    L, d, B = CFG["L"], CFG["d"], CFG["B"]
+    L, d, B, M = CFG["L"], CFG["d"], CFG["B"], CFG["minibatches"]
     k_p, k_h, k_r = CFG["k_p"], CFG["k_h"], CFG["k_r"]
     S = k_p + k_h + k_r
+    R = B * M  # rows per step per GPU (refresh chunk)
     hbm, tf_burst, tf_sus, peak_kind = peaks()
 
     eng = ClassifierEngine(L, d, k_p=k_p, k_h=k_h, k_r=k_r, seed=0, refresh_mode="bf16_rerank")
     eng.snapshot(epoch=0)
     L_loc = eng.hi - eng.lo
     rng = np.random.default_rng(1000 + rank)
-    n_b = args.warmup + args.steps
-    host = make_batches(rng, n_b, B, L, CFG["labels_per_point"], CFG["N"], rank, world)
+    n_steps = args.warmup + args.steps
+    # host data: per step M minibatches (rows, positives CSR, embeddings)
+    host = [make_batches(rng, M, B, L, CFG["labels_per_point"], CFG["N"], rank + t * world, world * n_steps)
+            for t in range(n_steps)]
     dev = []
-    for hb in host:
-        dev.append({k: torch.from_numpy(v).cuda() for k, v in hb.items()})
-    # the stale hard-negative cache rows of each batch: one refresh per batch up front
-    for db in dev:
-        db["hard"], _ = eng.refresh(db["emb"], db["indptr"], db["pos"], k_h)
+    for mbs in host:
+        mb_dev = [{k: torch.from_numpy(v).cuda() for k, v in hb.items()} for hb in mbs]
+        ip = np.concatenate([[0]] + [hb["indptr"][1:] + sum(int(x["indptr"][-1]) for x in mbs[:i])
+                                     for i, hb in enumerate(mbs)]).astype(np.int64)
+        chunk = {"emb": torch.from_numpy(np.concatenate([hb["emb"] for hb in mbs])).cuda(),
+                 "indptr": torch.from_numpy(ip).cuda(),
+                 "pos": torch.from_numpy(np.concatenate([hb["pos"] for hb in mbs])).cuda()}
+        dev.append({"mbs": mb_dev, "chunk": chunk})
+    # the stale hard-negative cache rows of each minibatch: one refresh per chunk up front
+    for st in dev:
+        hard, _ = eng.refresh(st["chunk"]["emb"], st["chunk"]["indptr"], st["chunk"]["pos"], k_h)
+        for i, m in enumerate(st["mbs"]):
+            m["hard"] = hard[i * B : (i + 1) * B].contiguous()
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_b)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * M + 2)] for _ in range(n_steps)]
     ids_keep = []
 
     def one(t, timed):
-        db = dev[t]
-        e = ev[t]
+        st, e = dev[t], ev[t]
         e[0].record(stream)
-        new_ids, _ = eng.refresh(db["emb"], db["indptr"], db["pos"], k_h)
+        eng.refresh(st["chunk"]["emb"], st["chunk"]["indptr"], st["chunk"]["pos"], k_h)
         e[1].record(stream)
-        slates = eng.sample(db["rows"], db["indptr"], db["pos"], db["hard"], epoch=1, step=t)
-        e[2].record(stream)
-        loss, grad_emb, status = eng.step(db["emb"], slates, CFG["lr"], CFG["wd"])
-        e[3].record(stream)
-        if timed:
-            ids_keep.append(slates[0])
+        for i, m in enumerate(st["mbs"]):
+            slates = eng.sample(m["rows"], m["indptr"], m["pos"], m["hard"], epoch=1, step=t * M + i)
+            e[2 + 2 * i].record(stream)
+            loss, grad_emb, status = eng.step(m["emb"], slates, CFG["lr"], CFG["wd"])
+            e[3 + 2 * i].record(stream)
+            if timed and i == 0:
+                ids_keep.append(slates[0])
         return loss, status
 
     # clock samples cover warm-up + timed region (the timed region alone can be
@@ -187,7 +200,7 @@ def run_ours(args):
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
-    for t in range(args.warmup, n_b):
+    for t in range(args.warmup, n_steps):
         loss, status = one(t, True)
     t_end.record(stream)
     torch.cuda.synchronize()
@@ -196,24 +209,22 @@ def run_ours(args):
     clk = clocks.stop()
     launches = _lib.launch_count() - launches0
     ops.raise_for_step_status(status)
-    ms_local = t_start.elapsed_time(t_end)
-    ms_t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    ms_t = torch.tensor([t_start.elapsed_time(t_end)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_total = float(ms_t.item())
-    timed = range(args.warmup, n_b)
-    ph = {k: 0.0 for k in ("refresh", "sample", "step")}
-    for t in timed:
+    K = args.steps
+    ph = {"refresh": 0.0, "sample": 0.0, "step": 0.0}
+    for t in range(args.warmup, n_steps):
         e = ev[t]
         ph["refresh"] += e[0].elapsed_time(e[1])
-        ph["sample"] += e[1].elapsed_time(e[2])
-        ph["step"] += e[2].elapsed_time(e[3])
-    K = args.steps
-    ms_step = ms_total / K
-    value = B * world * K / (ms_total / 1e3)
+        for i in range(M):
+            ph["sample"] += (e[1] if i == 0 else e[1 + 2 * i]).elapsed_time(e[2 + 2 * i])
+            ph["step"] += e[2 + 2 * i].elapsed_time(e[3 + 2 * i])
+    value = R * world * K / (ms_total / 1e3)
 
     # dominant kernel: the refresh (tcgen05 GEMM + fused top-k [+ merge/re-rank])
-    q_per_refresh = B * world  # every shard scores all gathered queries
+    q_per_refresh = R * world  # every shard scores all gathered queries
     flops = 2.0 * L_loc * d * q_per_refresh
     t_ref = ph["refresh"] / K / 1e3
     achieved_tf = flops / t_ref / 1e12
@@ -221,52 +232,68 @@ def run_ours(args):
     U = [int(torch.unique(ids[(ids >= eng.lo) & (ids < eng.hi)]).numel()) for ids in ids_keep]
     U_mean = sum(U) / len(U)
     step_bytes = U_mean * d * (2 * 4) + 2 * B * world * d * 4 + B * world * S * 5
-    t_step = ph["step"] / K / 1e3
+    t_step = ph["step"] / (K * M) / 1e3
+    t_samp = ph["sample"] / (K * M) / 1e3
     step_gbs = step_bytes / t_step / 1e9
 
     # end-to-end: the public API with HOST buffers (pinned), copies inside the timed region
     pinned = []
-    for hb, db in zip(host, dev):
-        pinned.append({k: torch.from_numpy(v).pin_memory() for k, v in hb.items()} | {"hard": db["hard"].cpu().pin_memory()})
-    outs = None
-    for t in range(args.warmup):
+    for t in range(n_steps):
+        mbs = [{k: torch.from_numpy(v).pin_memory() for k, v in hb.items()} for hb in host[t]]
+        for m, md in zip(mbs, dev[t]["mbs"]):
+            m["hard"] = md["hard"].cpu().pin_memory()
+        ch = {k: v.cpu().pin_memory() for k, v in dev[t]["chunk"].items()}
+        pinned.append({"mbs": mbs, "chunk": ch})
+    outs = [None] * M
+    rout = None
+
+    def one_host(t):
+        nonlocal rout
         p = pinned[t]
-        outs, _ = eng.train_step_host(p["emb"], p["rows"], p["indptr"], p["pos"], p["hard"], 1, t, CFG["lr"], CFG["wd"], out=outs)
+        rout = eng.refresh_host(p["chunk"]["emb"], p["chunk"]["indptr"], p["chunk"]["pos"], k_h, out=rout)
+        for i, m in enumerate(p["mbs"]):
+            outs[i], _ = eng.train_step_host(m["emb"], m["rows"], m["indptr"], m["pos"], m["hard"], 1, t * M + i,
+                                             CFG["lr"], CFG["wd"], out=outs[i])
+
+    for t in range(args.warmup):
+        one_host(t)
     torch.cuda.synchronize()
     eng.comm.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    h2d = d2h = 0
-    for t in range(args.warmup, n_b):
-        p = pinned[t]
-        outs, _ = eng.train_step_host(p["emb"], p["rows"], p["indptr"], p["pos"], p["hard"], 1, t, CFG["lr"], CFG["wd"], out=outs)
-        h2d = sum(x.numel() * x.element_size() for x in (p["emb"], p["rows"], p["indptr"], p["pos"], p["hard"]))
-        d2h = sum(x.numel() * x.element_size() for x in outs[:2]) - 8 + outs[2].numel() * outs[2].element_size()
+    for t in range(args.warmup, n_steps):
+        one_host(t)
     e1.record(stream)
     torch.cuda.synchronize()
+    nbytes = lambda ts: sum(x.numel() * x.element_size() for x in ts)  # noqa: E731
+    p = pinned[-1]
+    h2d = nbytes(p["chunk"].values()) + sum(nbytes((m["emb"], m["rows"], m["indptr"], m["pos"], m["hard"])) for m in p["mbs"])
+    d2h = nbytes([rout]) + sum(nbytes(o) for o in outs)
     e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = B * world * K / (float(e2e_ms.item()) / 1e3)
+    e2e_value = R * world * K / (float(e2e_ms.item()) / 1e3)
 
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": round(ms_total / K, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "fp32 W/step, bf16 tensor-core refresh + fp32 re-rank", "data": "synthetic",
-        "config": {"workload": CFG["workload"], "n_labels": L, "dim": d, "batch_per_gpu": B, "global_batch": B * world,
-                   "k_p": k_p, "k_h": k_h, "k_r": k_r, "slate": S, "labels_per_point": CFG["labels_per_point"],
-                   "tau_r": CFG["tau_r"], "refresh_mode": "bf16_rerank", "optimizer": "sgd+wd",
+        "config": {"workload": CFG["workload"], "n_labels": L, "dim": d, "rows_per_step_per_gpu": R,
+                   "minibatch": B, "minibatches_per_step": M, "global_batch": B * world, "k_p": k_p, "k_h": k_h,
+                   "k_r": k_r, "slate": S, "labels_per_point": CFG["labels_per_point"], "tau_r": CFG["tau_r"],
+                   "refresh_chunk": R * world, "refresh_mode": "bf16_rerank", "optimizer": "sgd+wd",
                    "parallelism": f"label-shard{world}", "l2": "inputs larger than L2 (W fp32 4.0 GB + snapshots 6 GB)"},
         "phases_ms_per_step": {k: round(v / K, 4) for k, v in ph.items()},
-        "refresh_mips_qps": round(B * world / t_ref, 1),
-        "step_only_samples_per_s": round(B * world / (t_step + ph["sample"] / K / 1e3), 1),
-        "composite_tau_r5_samples_per_s": round(B * world / (t_step + ph["sample"] / K / 1e3 + t_ref / 5), 1),
+        "refresh_mips_qps": round(q_per_refresh / t_ref, 1),
+        "step_only_samples_per_s": round(B * world / (t_step + t_samp), 1),
+        "composite_tau_r5_samples_per_s": round(R * world / (M * (t_step + t_samp) + t_ref / 5), 1),
         "roofline": {"bound": "tensor", "kernel": "refresh (tcgen05 GEMM + fused top-k + merge + re-rank)",
                      "achieved": round(achieved_tf, 2), "peak": tf_sus, "unit": "TFLOP/s",
                      "frac": round(achieved_tf / tf_sus, 4), "traffic": None,
-                     "algorithmic": f"2*L_shard*d*Q = {flops:.3e} flop per launch", "peak_kind": f"{peak_kind} sustained"},
-        "roofline_step": {"bound": "hbm", "kernel": "step (gather/loss/grad + counting sort + fused SGD row update)",
+                     "algorithmic": f"2*L_shard*d*Q = {flops:.3e} flop per launch (Q={q_per_refresh})",
+                     "peak_kind": f"{peak_kind} sustained"},
+        "roofline_step": {"bound": "hbm", "kernel": "minibatch step (gather/loss/grad + counting sort + fused SGD row update)",
                           "achieved": round(step_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(step_gbs / hbm, 4),
                           "algorithmic": f"U*d*8 + 2*B*d*4 + B*S*5 = {step_bytes:.3e} B (U={U_mean:.0f})",
                           "peak_kind": peak_kind},

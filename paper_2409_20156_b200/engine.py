@@ -131,36 +131,39 @@ class ClassifierEngine:
         status = self.comm.all_reduce(res.status)
         return loss, grad_emb, status
 
-    # ------------------------------------------------------------ full step
-    def train_step(self, emb, rows, pos_indptr, pos_ids, hard, epoch, step, lr, weight_decay, k_refresh=None,
-                   keep=None):
-        """One full classifier step on device-resident inputs: refresh of the
-        batch's queries (new hard negatives for a later epoch), slates from the
-        current (stale) hard cache rows, fused loss/update."""
-        new_ids, _ = self.refresh(emb, pos_indptr, pos_ids, k_refresh or self.k_h)
-        slates = self.sample(rows, pos_indptr, pos_ids, hard, epoch, step)
-        loss, grad_emb, status = self.step(emb, slates, lr, weight_decay, keep=keep)
-        return loss, grad_emb, status, new_ids
+    # ------------------------------------------------------------ host API
+    def refresh_host(self, queries_h, pos_indptr_h, pos_ids_h, k: int | None = None, out=None):
+        """retrieve_hard_negatives for a chunk of queries given in HOST (pinned)
+        memory: H2D of the queries and positives, refresh, D2H of the ids."""
+        dev = self.device
+        q = queries_h.to(dev, non_blocking=True)
+        ip = pos_indptr_h.to(dev, non_blocking=True)
+        pid = pos_ids_h.to(dev, non_blocking=True)
+        ids, _ = self.refresh(q, ip, pid, k or self.k_h)
+        if out is None:
+            out = torch.empty(ids.shape, dtype=ids.dtype, pin_memory=True)
+        out.copy_(ids, non_blocking=True)
+        return out
 
     def train_step_host(self, emb_h, rows_h, pos_indptr_h, pos_ids_h, hard_h, epoch, step, lr, weight_decay,
                         out=None):
-        """End-to-end call with HOST buffers: H2D of the step's inputs (pinned
-        memory, non_blocking), the device step, D2H of grad_emb, the loss and the
-        refreshed hard ids. Returns host tensors (grad_emb, loss, new_ids)."""
+        """One training minibatch with HOST inputs: H2D (pinned, non_blocking)
+        of embeddings / rows / positives / hard-cache rows, Philox slates, fused
+        loss + update, D2H of grad_emb and the loss. Returns
+        ((grad_emb_h, loss_h), status_dev)."""
         dev = self.device
         emb = emb_h.to(dev, non_blocking=True)
         rows = rows_h.to(dev, non_blocking=True)
         ip = pos_indptr_h.to(dev, non_blocking=True)
         pid = pos_ids_h.to(dev, non_blocking=True)
         hard = hard_h.to(dev, non_blocking=True) if hard_h is not None else None
-        loss, grad_emb, status, new_ids = self.train_step(emb, rows, ip, pid, hard, epoch, step, lr, weight_decay)
+        slates = self.sample(rows, ip, pid, hard, epoch, step)
+        loss, grad_emb, status = self.step(emb, slates, lr, weight_decay)
         if out is None:
             out = (torch.empty(grad_emb.shape, dtype=grad_emb.dtype, pin_memory=True),
-                   torch.empty(2, dtype=torch.float64, pin_memory=True),
-                   torch.empty(new_ids.shape, dtype=new_ids.dtype, pin_memory=True))
+                   torch.empty(1, dtype=torch.float64, pin_memory=True))
         out[0].copy_(grad_emb, non_blocking=True)
-        out[1][:1].copy_(loss, non_blocking=True)
-        out[2].copy_(new_ids, non_blocking=True)
+        out[1].copy_(loss, non_blocking=True)
         return out, status
 
     # ------------------------------------------------------------ host views
