@@ -1,0 +1,136 @@
+"""Drop-in for the exact shortlist refresh of xcmix.anns.
+
+Same names, signatures, return types and error classes as the reference:
+  build_exact(vectors, snapshot_epoch=0) -> AnnsIndex            anns.py:99-100
+  retrieve_hard_negatives(index, embeddings, positives, k_h,
+                          query_beam=128) -> NegativeCache        anns.py:233-268
+The exact branch (anns.py:252-256: E @ W^T, positive mask, _batched_topk) runs
+on the GPU (libastra_b200: tcgen05 GEMM + fused top-k, or the fp32-exact SIMT
+kernel). The approximate graph index (anns.py:136-208) is outside the B200
+path: retrieve_hard_negatives raises ConfigError for it unless install()
+recorded the reference implementation to hand it back to.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _backend
+from .errors import ConfigError, NumericalError
+
+try:  # reuse the caller's types when running under the reference package
+    from xcmix.anns import AnnsIndex, NegativeCache
+except ImportError:
+
+    @dataclass
+    class AnnsIndex:
+        kind: str
+        vectors: np.ndarray
+        snapshot_epoch: int = 0
+        graph: list | None = None
+        entry_point: int = 0
+
+        @property
+        def size(self) -> int:
+            return self.vectors.shape[0]
+
+    @dataclass
+    class NegativeCache:
+        ids: np.ndarray
+        built_from_epoch: int
+
+        @property
+        def n_queries(self) -> int:
+            return self.ids.shape[0]
+
+        @property
+        def k_h(self) -> int:
+            return self.ids.shape[1]
+
+
+# set by install(): the reference implementation for non-exact indexes
+_approx_impl = None
+QUERY_CHUNK = 1 << 16
+
+
+def _check_vectors(vectors) -> np.ndarray:
+    """Contiguous fp32 copy, nonempty 2-D, finite (anns.py:90-96)."""
+    vectors = np.ascontiguousarray(vectors, dtype=np.float32)
+    if vectors.ndim != 2 or vectors.shape[0] < 1:
+        raise ConfigError("index needs a nonempty M x d matrix")
+    if not np.isfinite(vectors).all():
+        raise NumericalError("non-finite vectors in index build")
+    return vectors.copy()
+
+
+def build_exact(vectors, snapshot_epoch: int = 0) -> AnnsIndex:
+    return AnnsIndex(kind="exact", vectors=_check_vectors(vectors), snapshot_epoch=snapshot_epoch)
+
+
+def refresh_mode_for(d: int, n_labels: int) -> str:
+    """fp32-exact unless the tensor-core path applies (ASTRA_REFRESH_MODE overrides)."""
+    mode = os.environ.get("ASTRA_REFRESH_MODE", "auto")
+    if mode != "auto":
+        return mode
+    return "bf16_rerank" if d % 64 == 0 and n_labels >= 4096 else "fp32"
+
+
+def _device_snapshot(index: AnnsIndex, mode: str):
+    """fp32 (+ bf16) device copies of the immutable index, cached on the index."""
+    ops = _backend.get()
+    dev = _backend.device()
+    snap = getattr(index, "_astra_snapshot", None)
+    if snap is None or snap[0] is not index.vectors or snap[1] != dev:
+        w32 = torch.from_numpy(np.ascontiguousarray(index.vectors, dtype=np.float32)).to(dev)
+        snap = [index.vectors, dev, w32, None]
+        index._astra_snapshot = snap
+    if mode != "fp32" and snap[3] is None:
+        snap[3] = ops.f32_to_bf16(snap[2])
+    return snap[2], snap[3]
+
+
+def positives_csr(positives, rows=None):
+    """(indptr int64, ids int32) of per-query positive id arrays, sorted per row."""
+    if rows is not None:
+        positives = [positives[i] for i in rows]
+    lens = np.fromiter((len(p) for p in positives), dtype=np.int64, count=len(positives))
+    indptr = np.zeros(len(positives) + 1, dtype=np.int64)
+    np.cumsum(lens, out=indptr[1:])
+    ids = (np.concatenate([np.sort(np.asarray(p, dtype=np.int64)) for p in positives]).astype(np.int32)
+           if indptr[-1] else np.zeros(0, dtype=np.int32))
+    return indptr, ids
+
+
+def retrieve_hard_negatives(index, embeddings, positives, k_h: int, query_beam: int = 128,
+                            mode: str | None = None) -> NegativeCache:
+    """Per query: top (k_h + |positives|), drop the positives, keep k_h
+    (anns.py:233-268), ids int32, descending score, ties to the lower id."""
+    N = embeddings.shape[0]
+    if k_h == 0:
+        return NegativeCache(np.empty((N, 0), dtype=np.int32), index.snapshot_epoch)
+    max_pos = max((len(p) for p in positives), default=0)
+    if k_h + max_pos > index.size:
+        raise ConfigError("k_h plus the positive count exceeds the label count")
+    if index.kind != "exact":
+        if _approx_impl is None:
+            raise ConfigError(f"index kind {index.kind!r} is not served by the B200 refresh")
+        return _approx_impl(index, embeddings, positives, k_h, query_beam)
+    ops = _backend.get()
+    L, d = index.vectors.shape
+    mode = mode or refresh_mode_for(d, L)
+    w32, wbf = _device_snapshot(index, mode)
+    dev = w32.device
+    E = np.ascontiguousarray(embeddings, dtype=np.float32)
+    out = np.empty((N, k_h), dtype=np.int32)
+    for lo in range(0, N, QUERY_CHUNK):
+        hi = min(N, lo + QUERY_CHUNK)
+        indptr, ids = positives_csr(positives[lo:hi])
+        _, top, _ = ops.refresh_topk(
+            torch.from_numpy(E[lo:hi]).to(dev), torch.from_numpy(indptr).to(dev), torch.from_numpy(ids).to(dev),
+            k_h, mode, labels_f32=w32, labels_bf16=wbf)
+        out[lo:hi] = top.cpu().numpy()
+    return NegativeCache(out, index.snapshot_epoch)

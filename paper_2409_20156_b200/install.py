@@ -1,0 +1,55 @@
+"""Bind the B200 path into a running reference (xcmix) process.
+
+Rebinds the module globals the reference resolves at call time (SURVEY.md
+§8(b)):
+  xcmix.anns.retrieve_hard_negatives           <- anns.retrieve_hard_negatives
+        (trainer.py:453 and sampler.py:203 call it through the module)
+  xcmix.trainer._batch_forward_backward        <- trainer._batch_forward_backward
+        (resolved by train_epoch, trainer.py:487)
+  xcmix.trainer._assemble_batch_slates         <- trainer._assemble_batch_slates
+        (slates="philox"; slates="reference" keeps the reference's PCG64 slates
+        so the GPU step can be compared bit-for-bit on identical indices)
+  xcmix.trainer/classifiers.apply_classifier_updates_arrays <- classifiers.*
+        (trainer.py:27 imported the name, classifiers.py:71 uses the global)
+Code that imported a name before install() (`from xcmix.anns import f`) keeps
+the old object: install first (e.g. from a pytest plugin / conftest).
+"""
+
+from __future__ import annotations
+
+from . import _backend, anns, classifiers, trainer
+
+_saved: dict = {}
+
+
+def install(backend=None, slates: str = "philox") -> None:
+    import xcmix.anns as xa
+    import xcmix.classifiers as xc
+    import xcmix.trainer as xt
+
+    if slates not in ("philox", "reference"):
+        raise ValueError("slates must be 'philox' or 'reference'")
+    if backend is not None:
+        _backend.set_backend(backend)
+    if not _saved:
+        _saved.update({
+            (xa, "retrieve_hard_negatives"): xa.retrieve_hard_negatives,
+            (xt, "_batch_forward_backward"): xt._batch_forward_backward,
+            (xt, "_assemble_batch_slates"): xt._assemble_batch_slates,
+            (xt, "apply_classifier_updates_arrays"): xt.apply_classifier_updates_arrays,
+            (xc, "apply_classifier_updates_arrays"): xc.apply_classifier_updates_arrays,
+        })
+    anns._approx_impl = _saved[(xa, "retrieve_hard_negatives")]
+    xa.retrieve_hard_negatives = anns.retrieve_hard_negatives
+    xt._batch_forward_backward = trainer._batch_forward_backward
+    xt._assemble_batch_slates = (trainer._assemble_batch_slates if slates == "philox"
+                                 else _saved[(xt, "_assemble_batch_slates")])
+    xt.apply_classifier_updates_arrays = classifiers.apply_classifier_updates_arrays
+    xc.apply_classifier_updates_arrays = classifiers.apply_classifier_updates_arrays
+
+
+def uninstall() -> None:
+    for (mod, name), fn in _saved.items():
+        setattr(mod, name, fn)
+    _saved.clear()
+    anns._approx_impl = None

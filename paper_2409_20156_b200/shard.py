@@ -33,14 +33,21 @@ class Comm:
         self.enabled = dist.is_available() and dist.is_initialized()
         self.world = dist.get_world_size(group) if self.enabled else 1
         self.rank = dist.get_rank(group) if self.enabled else 0
+        # NCCL has the fused tensor collectives; gloo (CPU tests) gets the list forms
+        self.nccl = self.enabled and dist.get_backend(group) == "nccl"
 
     def all_gather(self, t: torch.Tensor) -> torch.Tensor:
         """Concatenate equal-shaped tensors of all ranks along dim 0."""
         if self.world == 1:
             return t
-        out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
-        return out
+        t = t.contiguous()
+        if self.nccl:
+            out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(out, t, group=self.group)
+            return out
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(parts, t, group=self.group)
+        return torch.cat(parts)
 
     def all_gather_stack(self, t: torch.Tensor) -> torch.Tensor:
         """[world, *t.shape] stack of every rank's tensor."""
@@ -62,9 +69,15 @@ class Comm:
         """Sum over ranks, then keep this rank's dim-0 slice."""
         if self.world == 1:
             return t
-        out = torch.empty((t.shape[0] // self.world,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        dist.reduce_scatter_tensor(out, t.contiguous(), group=self.group)
-        return out
+        t = t.contiguous()
+        if self.nccl:
+            out = torch.empty((t.shape[0] // self.world,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            dist.reduce_scatter_tensor(out, t, group=self.group)
+            return out
+        full = t.clone()
+        dist.all_reduce(full, group=self.group)
+        n = t.shape[0] // self.world
+        return full[self.rank * n : (self.rank + 1) * n].contiguous()
 
     def all_reduce(self, t: torch.Tensor) -> torch.Tensor:
         if self.world > 1:

@@ -1,0 +1,120 @@
+"""A CPU stand-in for paper_2409_20156_b200.ops built on the ORACLE — test
+infrastructure only.
+
+It lets the host-side logic (the reference-facing mirror, install(), the
+label-sharded engine and its collectives) run in the build container without
+a GPU, e.g. under gloo with world_size 2, or underneath the reference's own
+test-suite. It is injected explicitly (install(backend=...) /
+ClassifierEngine(backend=...)); the product never selects it.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from oracle import c_oracle as co
+from oracle import xcmix_port as port
+from paper_2409_20156_b200.errors import ConfigError, NumericalError
+from paper_2409_20156_b200.ops import StepResult, raise_for_step_status  # noqa: F401  (pure host helpers)
+
+DEVICE = "cpu"
+
+
+def _np(t):
+    return None if t is None else t.detach().cpu().numpy()
+
+
+def f32_to_bf16(x):
+    return x.to(torch.bfloat16)
+
+
+def refresh_topk(queries, pos_indptr, pos_ids, k, mode="fp32", labels_f32=None, labels_bf16=None, label_offset=0,
+                 queries_bf16=None, n_labels=None):
+    if k < 1:
+        raise ConfigError("refresh: k must be >= 1")
+    keys, ids, scores = co.refresh_fp32(_np(queries), _np(labels_f32), _np(pos_indptr), _np(pos_ids), k, label_offset)
+    return (torch.from_numpy(keys.view(np.int64)), torch.from_numpy(ids), torch.from_numpy(scores))
+
+
+def topk_merge(part_keys, k_out):
+    pk = _np(part_keys).view(np.uint64)
+    n_parts, nq, k_in = pk.shape
+    allk = np.sort(pk.transpose(1, 0, 2).reshape(nq, n_parts * k_in), axis=1)[:, ::-1][:, :k_out]
+    allk = np.ascontiguousarray(allk)
+    ids = np.where(allk > 0, co.key_to_id(allk), -1).astype(np.int32)
+    scores = np.where(allk > 0, co.key_to_score(allk), -np.inf).astype(np.float32)
+    return torch.from_numpy(allk.view(np.int64)), torch.from_numpy(ids), torch.from_numpy(scores)
+
+
+def sample_slates(seed, epoch, step, rows, pos_indptr, pos_ids, hard, k_h, n_labels, k_p, k_r, cand=None,
+                  cand_q=None, k_i=0):
+    try:
+        out = co.sample_slates(seed, epoch, step, _np(rows), _np(pos_indptr), _np(pos_ids), _np(hard), k_h, n_labels,
+                               k_p, k_r, cand=_np(cand), cand_q=_np(cand_q), k_i=k_i)
+    except ValueError as e:
+        raise ConfigError(str(e)) from None
+    return tuple(torch.from_numpy(a) for a in out)
+
+
+def slate_step(emb, ids, y, origin, weights, W, lr, weight_decay=0.0, keep=None, factors_in=None, optimizer="sgd",
+               adam_m=None, adam_v=None, adam_step=1, betas=(0.9, 0.999), eps=1e-8, label_offset=0,
+               want_factors=False):
+    """The reference arithmetic (oracle/xcmix_port.py) restricted to this
+    shard's label range [label_offset, label_offset + W.shape[0])."""
+    if optimizer != "sgd":
+        raise ConfigError("oracle backend: SGD only")
+    E = _np(emb)
+    I = _np(ids).astype(np.int64)
+    Y = _np(y)
+    O = _np(origin)
+    Wt = _np(W).astype(np.float32, copy=False)
+    Wn = W.detach().numpy()  # in-place view
+    L_loc = Wn.shape[0]
+    B, S = I.shape
+    own = (I >= label_offset) & (I < label_offset + L_loc)
+    loc = np.where(own, I - label_offset, 0)
+    rows_w = Wt[loc]
+    if factors_in is None:
+        scores = np.einsum("bsd,bd->bs", rows_w, E)
+        terms_ok = own
+        O2 = O if O.ndim == 2 else np.broadcast_to(O, (B, S))
+        W2 = _np(weights) if _np(weights).ndim == 2 else np.broadcast_to(_np(weights), (B, S))
+        _, factors = port.slate_factors(scores, Y, O2, W2)
+        pos_slot = O2 == port.ORIGIN_POS
+        yf = Y.astype(np.float32)
+        sp_neg = port.softplus64(-scores)
+        lt = (yf * pos_slot) * sp_neg + (W2 * ((1.0 - yf) * (~pos_slot))) * (sp_neg + scores)
+        loss = float(lt[terms_ok].sum())
+    else:
+        factors = _np(factors_in)
+        loss = float("nan")
+    factors = np.where(own, factors, np.float32(0)).astype(np.float32)
+    grad_emb = np.einsum("bs,bsd->bd", factors, rows_w * own[:, :, None])
+    if keep is not None:
+        grad_emb = grad_emb * _np(keep)
+    status = np.zeros(4, np.int32)
+    if not np.isfinite(grad_emb).all():
+        status[1] = 1
+    owned_flat = own.ravel()
+    A = sp.csr_matrix((factors.ravel()[owned_flat], loc.ravel()[owned_flat],
+                       np.concatenate([[0], np.cumsum(own.sum(axis=1))])), shape=(B, L_loc))
+    full = A.T @ E
+    uids = np.unique(loc.ravel()[owned_flat])
+    grads = np.asarray(full[uids], dtype=np.float32)
+    if not np.isfinite(grads).all():
+        status[0] = 1
+    if not status.any() and len(uids):
+        rows = Wn[uids]
+        Wn[uids] = rows - np.float32(lr) * (grads + np.float32(weight_decay) * rows)
+    return StepResult(torch.tensor([loss], dtype=torch.float64), torch.from_numpy(np.ascontiguousarray(grad_emb, np.float32)),
+                      torch.from_numpy(status), torch.from_numpy(factors) if want_factors else None)
+
+
+def apply_updates(W, ids, grads, lr, weight_decay=0.0):
+    Wn = W.detach().numpy()
+    try:
+        port.apply_classifier_updates_arrays(Wn, _np(ids), _np(grads), lr, weight_decay)
+    except port.OracleNumericalError as e:
+        raise NumericalError(str(e)) from None
