@@ -2,12 +2,12 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step = one pass of the hot path over one batch of 8192 query rows per GPU at
+A step = one pass of the hot path over one batch of 9216 query rows per GPU at
 the LF-AmazonTitles-1.3M shape (BASELINE.json configs[3]: L=1,305,265, d=768):
-the shortlist refresh of the batch's 8192 queries against the whole label set
+the shortlist refresh of the batch's 9216 queries against the whole label set
 (bf16 tcgen05 GEMM + fused top-k + fp32 re-rank, k_h=64; the reference refreshes
 all N rows in one batched call, anns.py:253) and the training of the same rows
-as 8 SGD minibatches of B=1024: Philox slates (k_p=8, k_h=64, k_r=512 -> S=584)
+as 9 SGD minibatches of B=1024: Philox slates (k_p=8, k_h=64, k_r=512 -> S=584)
 + fused sampled-BCE fwd/bwd + SGD update of the fp32 W. This is the composite
 "train samples/s (shortlist+loss+update)" with every training row refreshed
 once per epoch (tau_r = 1, the most refresh-heavy schedule); refresh-only MIPS
@@ -38,7 +38,7 @@ sys.path.insert(0, ROOT)
 
 # C4 = LF-AmazonTitles-1.3M shape, slate from SURVEY.md §8
 CFG = dict(workload="LF-AmazonTitles-1.3M shape, synthetic", L=1_305_265, d=768, N=2_248_619, B=1024,
-           minibatches=8, k_p=8, k_h=64, k_r=512, labels_per_point=38, tau_r=1, lr=0.05, wd=1e-4)
+           minibatches=9, k_p=8, k_h=64, k_r=512, labels_per_point=38, tau_r=1, lr=0.05, wd=1e-4)
 METRIC = "ASTRA train samples/s (shortlist+loss+update)"
 UNIT = "samples/s"
 

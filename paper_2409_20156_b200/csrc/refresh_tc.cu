@@ -130,7 +130,7 @@ __device__ __forceinline__ uint32_t pick32(const uint32_t* r, int j) {
 struct TcArgs {
   int64_t nq, L, off;
   int d, k, cap;
-  int64_t n_lt, total;  // label tiles per query tile; n_qt * n_lt work units
+  int64_t n_lt, tiles_per_part;  // label tiles; label tiles per part
   const int64_t* pos_indptr;
   const int32_t* pos_ids;
   uint64_t* bufs;
@@ -138,25 +138,23 @@ struct TcArgs {
   uint64_t* gtau;  // nq shared thresholds (zeroed by the host before launch)
 };
 
-// Static "stream-K" schedule: the n_qt x n_lt (query tile, label tile) units
-// are linearised query-tile-major and cut into gridDim.x equal contiguous
-// ranges, so every CTA gets the same number of MMA tiles for any batch size.
-// A range covers one or a few (query tile, label-tile run) segments; the lane
-// state restarts at each segment and the segment's partial list goes to slot
-// (cta - first cta of that query tile).
+// Schedule: grid (query tile, label part). Each CTA sweeps one contiguous
+// label range for one 128-query tile; all CTAs of a part stream the same W
+// tiles at about the same time, so W comes from DRAM ~once per part and the
+// other query tiles hit L2. Lists per query = n_parts * SPLIT.
 struct Seg {
   int64_t qt, lt0, lt1;
   int slot;
 };
 
 __device__ __forceinline__ bool next_seg(int64_t& u, int64_t u1, const TcArgs& a, Seg& s) {
-  if (u >= u1) return false;
-  s.qt = u / a.n_lt;
-  s.lt0 = u - s.qt * a.n_lt;
-  const int64_t end = std::min<int64_t>(u1, (s.qt + 1) * a.n_lt);
-  s.lt1 = s.lt0 + (end - u);
-  s.slot = static_cast<int>(blockIdx.x - (s.qt * a.n_lt * gridDim.x) / a.total);
-  u = end;
+  if (u > u1) return false;  // exactly one (possibly empty) segment per CTA: empty ones flush zeros
+  (void)a;
+  s.qt = blockIdx.x;
+  s.lt0 = u;
+  s.lt1 = u1;
+  s.slot = blockIdx.y;
+  u = u1 + 1;
   return true;
 }
 
@@ -176,8 +174,8 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t u_begin = (static_cast<int64_t>(blockIdx.x) * a.total + gridDim.x - 1) / gridDim.x;
-  const int64_t u_end = (static_cast<int64_t>(blockIdx.x + 1) * a.total + gridDim.x - 1) / gridDim.x;
+  const int64_t u_begin = std::min<int64_t>(a.n_lt, static_cast<int64_t>(blockIdx.y) * a.tiles_per_part);
+  const int64_t u_end = std::min<int64_t>(a.n_lt, u_begin + a.tiles_per_part);
   const int nkb = a.d / BK;
 
   if (warp == 0 && lane == 0) {
@@ -271,7 +269,8 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     const int e = warp - kEpiWarp0, quad = e & 3, half = e >> 2;
     const int row = quad * 32 + lane;  // TMEM lane = query row in tile
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
-    uint64_t* buf = a.bufs + ((static_cast<size_t>(blockIdx.x) * kEpiSplit + half) * BM + row) * (a.cap + kTopkSlack);
+    uint64_t* buf = a.bufs + ((static_cast<size_t>(blockIdx.x * gridDim.y + blockIdx.y) * kEpiSplit + half) * BM + row) *
+                             (a.cap + kTopkSlack);
     constexpr int kCols = BN / kEpiSplit;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -391,21 +390,13 @@ int refresh_tc_split() {
   return split;
 }
 
-// Grid size and number of partial lists per query for a refresh of nq queries
-// over L labels (see next_seg).
+// Number of CTAs and of partial lists per query for nq queries over L labels.
 void refresh_tc_layout(int64_t nq, int64_t L, int* n_ctas, int* n_lists) {
   const int64_t n_qt = std::max<int64_t>(1, (nq + BM - 1) / BM);
   const int64_t n_lt = std::max<int64_t>(1, (L + BN - 1) / BN);
-  const int64_t total = n_qt * n_lt;
-  const int64_t G = std::min<int64_t>(num_sms(), total);
-  int64_t slots = 1;
-  for (int64_t qt = 0; qt < n_qt; ++qt) {
-    const int64_t c0 = (qt * n_lt * G) / total;
-    const int64_t c1 = ((qt + 1) * n_lt - 1) * G / total;
-    slots = std::max<int64_t>(slots, c1 - c0 + 1);
-  }
-  *n_ctas = static_cast<int>(G);
-  *n_lists = static_cast<int>(slots) * refresh_tc_split();
+  const int64_t parts = std::min<int64_t>(n_lt, std::max<int64_t>(1, num_sms() / n_qt));
+  *n_ctas = static_cast<int>(n_qt * parts);
+  *n_lists = static_cast<int>(parts) * refresh_tc_split();
 }
 
 int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb, int64_t L, int64_t label_offset,
@@ -416,6 +407,7 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
   if (L <= 0) return ASTRA_OK;
   int G, n_lists;
   refresh_tc_layout(nq, L, &G, &n_lists);
+  const int n_parts = n_lists / refresh_tc_split();
   CUtensorMap tmA, tmB;
   ASTRA_TRY(make_map(&tmA, qb, nq, d, BM));
   ASTRA_TRY(make_map(&tmB, wb, L, d, BN));
@@ -427,15 +419,13 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
   a.k = k;
   a.cap = cap;
   a.n_lt = (L + BN - 1) / BN;
-  a.total = ((nq + BM - 1) / BM) * a.n_lt;
+  a.tiles_per_part = (a.n_lt + n_parts - 1) / n_parts;
   a.pos_indptr = pos_indptr;
   a.pos_ids = pos_ids;
   a.bufs = bufs;
   a.part_keys = part_keys;
   a.gtau = gtau;
   ASTRA_TRY(check_cuda(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * nq, st), "memset gtau"));
-  // slots a query tile does not use stay empty (key 0) for the merge
-  ASTRA_TRY(check_cuda(cudaMemsetAsync(part_keys, 0, sizeof(uint64_t) * n_lists * nq * k, st), "memset part keys"));
   static bool attr_set = false;
   if (!attr_set) {
     ASTRA_TRY(check_cuda(cudaFuncSetAttribute(refresh_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -446,10 +436,12 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
                          "smem attr"));
     attr_set = true;
   }
+  const dim3 grid(static_cast<unsigned>((nq + BM - 1) / BM), static_cast<unsigned>(n_parts));
+  (void)G;
   if (refresh_tc_split() == 1)
-    refresh_tc_kernel<1><<<G, threads_for<1>(), kSmemBytes, st>>>(tmA, tmB, a);
+    refresh_tc_kernel<1><<<grid, threads_for<1>(), kSmemBytes, st>>>(tmA, tmB, a);
   else
-    refresh_tc_kernel<2><<<G, threads_for<2>(), kSmemBytes, st>>>(tmA, tmB, a);
+    refresh_tc_kernel<2><<<grid, threads_for<2>(), kSmemBytes, st>>>(tmA, tmB, a);
   ASTRA_LAUNCHED("refresh_tc");
   return ASTRA_OK;
 }

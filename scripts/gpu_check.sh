@@ -11,7 +11,7 @@ if [ "${NCU:-1}" = "1" ]; then
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_bench.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:refresh_tc_kernel -s 2 -c 1 \
     -o gpurun_out/prof_refresh_tc python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_tc.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"label_update_vec|slot_forward_vec" -s 4 -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"label_update_vec|slot_forward_vec|rerank_kernel|merge_warp" -s 8 -c 4 \
     -o gpurun_out/prof_step python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_step.log 2>&1
 fi
 tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
