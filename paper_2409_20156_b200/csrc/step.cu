@@ -128,7 +128,7 @@ __device__ void forward_tail(const FwdArgs& a, int b, float* red, double lsum, d
 
 // Vectorised forward: d = NV * 128, each lane owns NV float4 of the row.
 template <int NV, bool BF16>
-__global__ void __launch_bounds__(kFwdThreads) slot_forward_vec(FwdArgs a) {
+__global__ void __launch_bounds__(kFwdThreads, 1) slot_forward_vec(FwdArgs a) {
   __shared__ __align__(16) float red[kFwdWarps * NV * 128];
   __shared__ float s_emax[kFwdWarps];
   const int b = blockIdx.x;
@@ -147,18 +147,19 @@ __global__ void __launch_bounds__(kFwdThreads) slot_forward_vec(FwdArgs a) {
   for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
   double lsum = 0.0, fabs_sum = 0.0;
   const int32_t* row_ids = a.ids + static_cast<size_t>(b) * a.S;
-  // two slots in flight per warp for memory-level parallelism
-  for (int s0 = warp * 2; s0 < a.S; s0 += kFwdWarps * 2) {
-    int sl[2] = {s0, s0 + 1};
-    int64_t loc[2];
-    bool own[2];
-    float4 w[2][NV];
+  // UNR slots in flight per warp for memory-level parallelism (HBM latency x BW per SM)
+  constexpr int UNR = NV <= 2 ? 8 : (NV <= 4 ? 6 : 4);
+  for (int s0 = warp * UNR; s0 < a.S; s0 += kFwdWarps * UNR) {
+    int64_t loc[UNR];
+    bool own[UNR];
+    float4 w[UNR][NV];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < UNR; ++u) {
+      const int sl = s0 + u;
       own[u] = false;
       loc[u] = 0;
-      if (sl[u] < a.S) {
-        loc[u] = static_cast<int64_t>(row_ids[sl[u]]) - a.off;
+      if (sl < a.S) {
+        loc[u] = static_cast<int64_t>(row_ids[sl]) - a.off;
         own[u] = loc[u] >= 0 && loc[u] < a.Lloc;
       }
       if (own[u]) {
@@ -167,11 +168,12 @@ __global__ void __launch_bounds__(kFwdThreads) slot_forward_vec(FwdArgs a) {
       }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < UNR; ++u) {
       if (!own[u]) continue;  // warp-uniform
+      const int sl = s0 + u;
       float f;
       if (a.factors_in) {
-        f = a.factors_in[static_cast<size_t>(b) * a.S + sl[u]];
+        f = a.factors_in[static_cast<size_t>(b) * a.S + sl];
       } else {
         float acc = 0.0f;
 #pragma unroll
@@ -183,12 +185,12 @@ __global__ void __launch_bounds__(kFwdThreads) slot_forward_vec(FwdArgs a) {
         }
         acc = warp_sum(acc);
         double lt;
-        f = slot_factor(a, b, sl[u], acc, &lt);
+        f = slot_factor(a, b, sl, acc, &lt);
         if (lane == 0) lsum += lt;
       }
       if (lane == 0) {
         fabs_sum += static_cast<double>(fabsf(f));
-        if (a.factors) a.factors[static_cast<size_t>(b) * a.S + sl[u]] = f;
+        if (a.factors) a.factors[static_cast<size_t>(b) * a.S + sl] = f;
       }
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
