@@ -76,6 +76,27 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// Multicast variant: the box lands at the same smem offset in every CTA of
+// `mask` and completes tx bytes on the mbarrier at the same offset in each.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // K-major SWIZZLE_128B shared-memory matrix descriptor (8-row x 128 B atoms,
 // SBO = 1024 B between atoms, version 1 for sm_100).
 __device__ __forceinline__ uint64_t smem_desc(const void* p) {
@@ -95,6 +116,16 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+
+// Arrive on `bar` (same smem offset) in every CTA of `mask` once this thread's
+// prior tcgen05.mma ops complete: releases a multicast-filled stage cluster-wide.
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -158,11 +189,17 @@ __device__ __forceinline__ bool next_seg(int64_t& u, int64_t u1, const TcArgs& a
   return true;
 }
 
-template <int SPLIT>
+// CL = cluster size along query tiles: the CL CTAs of a cluster sweep the same
+// label tiles; each loads 1/CL of every W tile and multicasts it to all of them,
+// so W leaves L2 once per cluster and the cluster moves in lockstep.
+template <int SPLIT, int CL>
 __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     refresh_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
   constexpr int kEpiSplit = SPLIT;
   constexpr int kEpiWarps = 4 * SPLIT;
+  constexpr uint16_t kMask = static_cast<uint16_t>((1u << CL) - 1);
+  constexpr int B_SLICE = B_STAGE / CL;  // bytes of W tile rows loaded by each cluster rank
+  const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* sA = smem;
@@ -183,7 +220,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // every cluster CTA's MMA must release the stage
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -197,7 +234,10 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync_all();  // peers' barriers are initialised before any multicast targets them
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -214,9 +254,13 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
           const int n0 = static_cast<int>(t * BN);
           for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], STAGE_BYTES);
+            mbar_expect_tx(&full[stage], STAGE_BYTES);  // own A + all CL slices of the W tile
             tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, q0);
-            tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
+            if (CL == 1)
+              tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
+            else
+              tma_load_2d_mc(sB + stage * B_STAGE + crank * B_SLICE, &tmB, &full[stage], kb * BK,
+                             n0 + static_cast<int>(crank) * (BN / CL), kMask);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -247,7 +291,10 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
             // +32 B along K inside the 128 B swizzle atom = +2 in the encoded address
             mma_bf16(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
           }
-          mma_commit(&empty[stage]);
+          if (CL == 1)
+            mma_commit(&empty[stage]);
+          else
+            mma_commit_mc(&empty[stage], kMask);
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -346,7 +393,10 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync_all();  // no CTA leaves while peers may still signal its barriers
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
@@ -379,7 +429,47 @@ int make_map(CUtensorMap* m, const void* base, int64_t rows, int d, int box_rows
   return ASTRA_OK;
 }
 
+template <int SPLIT, int CL>
+int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const TcArgs& a, dim3 grid, cudaStream_t st) {
+  static bool attr_set = false;
+  auto kern = refresh_tc_kernel<SPLIT, CL>;
+  if (!attr_set) {
+    ASTRA_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(kSmemBytes)),
+                         "smem attr"));
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads_for<SPLIT>());
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ASTRA_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a), "launch refresh_tc"));
+  ASTRA_LAUNCHED("refresh_tc");
+  return ASTRA_OK;
+}
+
 }  // namespace
+
+// Cluster size along query tiles (ASTRA_TC_CLUSTER=1|2|4, default 2), reduced
+// for batches with few query tiles.
+int refresh_tc_cluster(int64_t n_qt) {
+  static int cl = [] {
+    const char* e = getenv("ASTRA_TC_CLUSTER");
+    const int v = e ? atoi(e) : 2;
+    return (v == 1 || v == 2 || v == 4) ? v : 2;
+  }();
+  int c = cl;
+  while (c > 1 && n_qt < c) c >>= 1;
+  return c;
+}
 
 // Epilogue split (ASTRA_TC_SPLIT=1|2, default 1: measured faster, fewer partial lists).
 int refresh_tc_split() {
@@ -392,7 +482,9 @@ int refresh_tc_split() {
 
 // Number of CTAs and of partial lists per query for nq queries over L labels.
 void refresh_tc_layout(int64_t nq, int64_t L, int* n_ctas, int* n_lists) {
-  const int64_t n_qt = std::max<int64_t>(1, (nq + BM - 1) / BM);
+  int64_t n_qt = std::max<int64_t>(1, (nq + BM - 1) / BM);
+  const int cl = refresh_tc_cluster(n_qt);
+  n_qt = (n_qt + cl - 1) / cl * cl;  // whole clusters (padding tiles hold no queries)
   const int64_t n_lt = std::max<int64_t>(1, (L + BN - 1) / BN);
   const int64_t parts = std::min<int64_t>(n_lt, std::max<int64_t>(1, num_sms() / n_qt));
   *n_ctas = static_cast<int>(n_qt * parts);
@@ -408,9 +500,10 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
   int G, n_lists;
   refresh_tc_layout(nq, L, &G, &n_lists);
   const int n_parts = n_lists / refresh_tc_split();
+  const int cl = refresh_tc_cluster((nq + BM - 1) / BM);
   CUtensorMap tmA, tmB;
   ASTRA_TRY(make_map(&tmA, qb, nq, d, BM));
-  ASTRA_TRY(make_map(&tmB, wb, L, d, BN));
+  ASTRA_TRY(make_map(&tmB, wb, L, d, BN / cl));
   TcArgs a;
   a.nq = nq;
   a.L = L;
@@ -426,24 +519,14 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
   a.part_keys = part_keys;
   a.gtau = gtau;
   ASTRA_TRY(check_cuda(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * nq, st), "memset gtau"));
-  static bool attr_set = false;
-  if (!attr_set) {
-    ASTRA_TRY(check_cuda(cudaFuncSetAttribute(refresh_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(kSmemBytes)),
-                         "smem attr"));
-    ASTRA_TRY(check_cuda(cudaFuncSetAttribute(refresh_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(kSmemBytes)),
-                         "smem attr"));
-    attr_set = true;
-  }
-  const dim3 grid(static_cast<unsigned>((nq + BM - 1) / BM), static_cast<unsigned>(n_parts));
-  (void)G;
-  if (refresh_tc_split() == 1)
-    refresh_tc_kernel<1><<<grid, threads_for<1>(), kSmemBytes, st>>>(tmA, tmB, a);
-  else
-    refresh_tc_kernel<2><<<grid, threads_for<2>(), kSmemBytes, st>>>(tmA, tmB, a);
-  ASTRA_LAUNCHED("refresh_tc");
-  return ASTRA_OK;
+  const dim3 grid(static_cast<unsigned>(G / n_parts), static_cast<unsigned>(n_parts));
+  const int split = refresh_tc_split();
+  if (split == 1 && cl == 1) return launch_variant<1, 1>(tmA, tmB, a, grid, st);
+  if (split == 1 && cl == 2) return launch_variant<1, 2>(tmA, tmB, a, grid, st);
+  if (split == 1 && cl == 4) return launch_variant<1, 4>(tmA, tmB, a, grid, st);
+  if (split == 2 && cl == 1) return launch_variant<2, 1>(tmA, tmB, a, grid, st);
+  if (split == 2 && cl == 2) return launch_variant<2, 2>(tmA, tmB, a, grid, st);
+  return launch_variant<2, 4>(tmA, tmB, a, grid, st);
 }
 
 }  // namespace astra
