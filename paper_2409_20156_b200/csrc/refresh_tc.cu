@@ -167,6 +167,7 @@ struct TcArgs {
   uint64_t* bufs;
   uint64_t* part_keys;
   uint64_t* gtau;  // nq shared thresholds (zeroed by the host before launch)
+  int debug_no_topk;  // ASTRA_TC_DEBUG_NO_TOPK=1: skip selection (pipeline-rate measurement only)
 };
 
 // Schedule: grid (query tile, label part). Each CTA sweeps one contiguous
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
           tmem_ld32_nowait(lane_base + static_cast<uint32_t>(acc * BN + c0 + 32), r + 32);
           tmem_wait();
           const int cn = nvalid - c0;  // valid columns in this 64-wide chunk (may exceed 64)
-          if (cn <= 0) continue;       // tile tail (uniform across the CTA)
+          if (cn <= 0 || a.debug_no_topk) continue;  // tile tail (uniform across the CTA)
           float mx = -INFINITY;
           if (cn >= 64) {
 #pragma unroll
@@ -518,6 +519,7 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
   a.bufs = bufs;
   a.part_keys = part_keys;
   a.gtau = gtau;
+  a.debug_no_topk = getenv("ASTRA_TC_DEBUG_NO_TOPK") != nullptr;
   ASTRA_TRY(check_cuda(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * nq, st), "memset gtau"));
   const dim3 grid(static_cast<unsigned>(G / n_parts), static_cast<unsigned>(n_parts));
   const int split = refresh_tc_split();
