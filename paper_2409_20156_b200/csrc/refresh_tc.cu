@@ -16,6 +16,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -53,9 +54,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done;
   do {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep until the phase flips
         : "memory");
   } while (!done);
 }
@@ -168,6 +169,7 @@ struct TcArgs {
   uint64_t* part_keys;
   uint64_t* gtau;  // nq shared thresholds (zeroed by the host before launch)
   int debug_no_topk;  // ASTRA_TC_DEBUG_NO_TOPK=1: skip selection (pipeline-rate measurement only)
+  unsigned long long* dbg;  // ASTRA_TC_DEBUG_COUNTERS=1: [slow chunks, candidates, compactions, chunks]
 };
 
 // Schedule: grid (query tile, label part). Each CTA sweeps one contiguous
@@ -188,6 +190,45 @@ __device__ __forceinline__ bool next_seg(int64_t& u, int64_t u1, const TcArgs& a
   s.slot = blockIdx.y;
   u = u1 + 1;
   return true;
+}
+
+// Scan one 32-column chunk of scores held in registers: a warp vote on the
+// per-lane maxima skips the chunk unless some query can admit a candidate;
+// candidates are appended (r[] indexed through a select tree, no local memory)
+// and over-full buffers compacted once r[] is dead.
+template <class Args>
+__device__ __forceinline__ void scan_chunk(LaneTopK& tk, const uint32_t* r, int cn, uint32_t g0, bool active,
+                                           const Args& a) {
+  if (cn <= 0 || a.debug_no_topk) return;  // tile tail (uniform across the CTA)
+  float t16[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float x0 = (j < cn) ? __uint_as_float(r[j]) : -INFINITY;
+    const float x1 = (j + 16 < cn) ? __uint_as_float(r[j + 16]) : -INFINITY;
+    t16[j] = fmaxf(x0, x1);
+  }
+#pragma unroll
+  for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+    for (int j = 0; j < w; ++j) t16[j] = fmaxf(t16[j], t16[j + w]);
+  if (a.dbg && (threadIdx.x & 31) == 0) atomicAdd(a.dbg + 3, 1ull);
+  if (!__any_sync(0xffffffffu, active && t16[0] >= tk.tau_s)) return;  // the common case
+  if (a.dbg && (threadIdx.x & 31) == 0) atomicAdd(a.dbg + 0, 1ull);
+  uint32_t m = 0;
+  if (active) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) m |= (j < cn && __uint_as_float(r[j]) >= tk.tau_s) ? (1u << j) : 0u;
+  }
+  while (m) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    lane_offer(tk, __uint_as_float(pick32(r, j)), g0 + j);
+  }
+  if (a.dbg) {
+    const unsigned need = __ballot_sync(0xffffffffu, active && (tk.cnt - tk.nsorted) > a.cap / 2);
+    if ((threadIdx.x & 31) == 0) atomicAdd(a.dbg + 2, static_cast<unsigned long long>(__popc(need)));
+  }
+  topk_settle(tk, a.cap, a.k, active);
 }
 
 // CL = cluster size along query tiles: the CL CTAs of a cluster sweep the same
@@ -332,52 +373,39 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
         const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
         lane_init(tk, buf, a.pos_ids + p0, p1 - p0, active ? a.gtau + q : nullptr);
       }
+      uint64_t g_pref = 0;  // shared threshold prefetched one tile ahead
       for (int64_t t = sg.lt0; t < sg.lt1; ++t) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const int64_t n0 = t * BN;
         const int nvalid = static_cast<int>(std::min<int64_t>(BN, a.L - n0));
-        lane_sync_tau(tk);
+        // shared threshold: apply the value fetched during the previous tile, fetch the next
+        if (tk.gtau) {
+          if (g_pref > tk.tau) {
+            tk.tau = g_pref;
+            tk.tau_s = key_score(g_pref);
+          }
+          g_pref = *reinterpret_cast<volatile uint64_t*>(tk.gtau);
+        }
+        // 32-column chunks, the next chunk's TMEM load in flight while this one is scanned
+        const uint32_t tbase = lane_base + static_cast<uint32_t>(acc * BN + half * kCols);
+        const int col0 = half * kCols;
+        uint32_t ra[32], rb[32];
+        __syncwarp();
+        tmem_ld32_nowait(tbase, ra);
+        tmem_wait();
 #pragma unroll 1
-        for (int c0 = half * kCols; c0 < (half + 1) * kCols; c0 += 64) {
-          uint32_t r[64];
+        for (int c = 0; c < kCols; c += 64) {
           __syncwarp();
-          tmem_ld32_nowait(lane_base + static_cast<uint32_t>(acc * BN + c0), r);
-          tmem_ld32_nowait(lane_base + static_cast<uint32_t>(acc * BN + c0 + 32), r + 32);
+          tmem_ld32_nowait(tbase + c + 32, rb);
+          scan_chunk(tk, ra, nvalid - (col0 + c), static_cast<uint32_t>(n0 + col0 + c + a.off), active, a);
+          __syncwarp();
           tmem_wait();
-          const int cn = nvalid - c0;  // valid columns in this 64-wide chunk (may exceed 64)
-          if (cn <= 0 || a.debug_no_topk) continue;  // tile tail (uniform across the CTA)
-          float mx = -INFINITY;
-          if (cn >= 64) {
-#pragma unroll
-            for (int j = 0; j < 64; ++j) mx = fmaxf(mx, __uint_as_float(r[j]));
-          } else {
-#pragma unroll
-            for (int j = 0; j < 64; ++j)
-              if (j < cn) mx = fmaxf(mx, __uint_as_float(r[j]));
-          }
-          if (!__any_sync(0xffffffffu, active && mx >= tk.tau_s)) continue;  // the common case
-          uint32_t m0 = 0, m1 = 0;
-          if (active) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              m0 |= (j < cn && __uint_as_float(r[j]) >= tk.tau_s) ? (1u << j) : 0u;
-              m1 |= (j + 32 < cn && __uint_as_float(r[j + 32]) >= tk.tau_s) ? (1u << j) : 0u;
-            }
-          }
-          // append (at most 64 <= kTopkSlack keys), then compact with r[] dead
-          const uint32_t g0 = static_cast<uint32_t>(n0 + c0 + a.off);
-          while (m0) {
-            const int j = __ffs(m0) - 1;
-            m0 &= m0 - 1;
-            lane_offer(tk, __uint_as_float(pick32(r, j)), g0 + j);
-          }
-          while (m1) {
-            const int j = __ffs(m1) - 1;
-            m1 &= m1 - 1;
-            lane_offer(tk, __uint_as_float(pick32(r + 32, j)), g0 + 32 + j);
-          }
-          topk_settle(tk, a.cap, a.k, active);
+          __syncwarp();
+          if (c + 64 < kCols) tmem_ld32_nowait(tbase + c + 64, ra);
+          scan_chunk(tk, rb, nvalid - (col0 + c + 32), static_cast<uint32_t>(n0 + col0 + c + 32 + a.off), active, a);
+          __syncwarp();
+          tmem_wait();
         }
         tc_fence_before();
         __syncwarp();
@@ -520,9 +548,24 @@ int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
   a.part_keys = part_keys;
   a.gtau = gtau;
   a.debug_no_topk = getenv("ASTRA_TC_DEBUG_NO_TOPK") != nullptr;
+  static unsigned long long* dbg_buf = nullptr;
+  const bool counters = getenv("ASTRA_TC_DEBUG_COUNTERS") != nullptr;
+  if (counters && !dbg_buf) cudaMalloc(&dbg_buf, 4 * sizeof(unsigned long long));
+  a.dbg = counters ? dbg_buf : nullptr;
+  if (counters) cudaMemsetAsync(dbg_buf, 0, 4 * sizeof(unsigned long long), st);
   ASTRA_TRY(check_cuda(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * nq, st), "memset gtau"));
   const dim3 grid(static_cast<unsigned>(G / n_parts), static_cast<unsigned>(n_parts));
   const int split = refresh_tc_split();
+  if (counters) {
+    int rc = split == 1 ? (cl == 2 ? launch_variant<1, 2>(tmA, tmB, a, grid, st) : launch_variant<1, 1>(tmA, tmB, a, grid, st))
+                        : launch_variant<2, 1>(tmA, tmB, a, grid, st);
+    unsigned long long h[4];
+    cudaMemcpyAsync(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[refresh_tc] nq=%lld k=%d slow_chunks=%llu/%llu (%.3f) cnt_sum_at_settle=%llu compactions=%llu\n",
+            (long long)nq, k, h[0], h[3], h[3] ? double(h[0]) / h[3] : 0.0, h[1], h[2]);
+    return rc;
+  }
   if (split == 1 && cl == 1) return launch_variant<1, 1>(tmA, tmB, a, grid, st);
   if (split == 1 && cl == 2) return launch_variant<1, 2>(tmA, tmB, a, grid, st);
   if (split == 1 && cl == 4) return launch_variant<1, 4>(tmA, tmB, a, grid, st);

@@ -209,10 +209,12 @@ __device__ inline int compact_mem(uint64_t* buf, int cnt, int cap, const int32_t
   return valid < k ? valid : k;
 }
 
-// Capacity for a given k: 2P, P = next power of two >= max(k, 32).
+// Capacity for a given k: 2P, P = next power of two >= max(k + 32, 64): the
+// sorted prefix (<= k) plus a newcomer region of P (compaction every ~P-k..P
+// admissions; larger P = fewer, slightly longer compactions).
 __host__ __device__ inline int topk_cap(int k) {
-  int p = 32;
-  while (p < k) p <<= 1;
+  int p = 64;
+  while (p < k + 32) p <<= 1;
   return 2 * p;
 }
 
