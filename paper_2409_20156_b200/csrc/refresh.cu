@@ -20,16 +20,11 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "refresh_tc.cuh"
 #include "topk.cuh"
 
 namespace astra {
 
-// refresh_tc.cu
-int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb, int64_t L, int64_t label_offset,
-                      const int64_t* pos_indptr, const int32_t* pos_ids, int k, int cap, uint64_t* bufs,
-                      uint64_t* part_keys, uint64_t* gtau, cudaStream_t st);
-void refresh_tc_layout(int64_t nq, int64_t L, int* n_ctas, int* n_lists);
-int refresh_tc_split();
 
 namespace {
 
@@ -182,11 +177,12 @@ __global__ void __launch_bounds__(128) merge_kernel(const uint64_t* part_keys, i
 template <int R>
 __global__ void __launch_bounds__(256) merge_warp_kernel(const uint64_t* part_keys, int64_t nq, int n_parts,
                                                          int k_in, int k_out, uint64_t* out_keys, int32_t* out_ids,
-                                                         float* out_scores) {
+                                                         float* out_scores, const int32_t* only) {
   constexpr int P = 32 * R;
   const int lane = threadIdx.x & 31;
   const int64_t q = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (q >= nq) return;  // warp-uniform
+  if (only && !only[q]) return;
   const int kin = k_in < P ? k_in : P;
   uint64_t cur[R];
   {
@@ -337,13 +333,149 @@ __global__ void f32_to_bf16_kernel(const float* src, uint16_t* dst, int64_t n) {
   }
 }
 
+// ------------------------------------------------------------- select (two-pass refresh)
+
+// Warp per query: the j-th largest of the query's 64-label group maxima
+// (orderable bits, gmax [nq][n_groups]) by an MSB-first radix select. Each of
+// the top-j group maxima is a distinct label, so at least j sampled labels
+// score >= it: tau_keys[q] = (T << 32) admits every key with score >= T.
+__global__ void __launch_bounds__(256) tau_select_kernel(const uint32_t* gmax, int64_t nq, int n_groups, int j,
+                                                         uint64_t* tau_keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (q >= nq) return;  // warp-uniform
+  const uint32_t* v = gmax + static_cast<size_t>(q) * n_groups;
+  uint32_t T = 0;
+  if (n_groups >= j) {
+    for (int b = 31; b >= 0; --b) {
+      const uint32_t c = T | (1u << b);
+      int n = 0;
+      for (int i = lane; i < n_groups; i += 32) n += __ldg(v + i) >= c;
+      if (warp_sum(n) >= j) T = c;
+    }
+  }
+  if (lane == 0) tau_keys[q] = static_cast<uint64_t>(T) << 32;
+}
+
+// Warp per query: gather the FIXED-mode candidate lists of the query's label
+// parts, drop the query's positives (anns.py:254-255) and keep the top k in
+// (score desc, id asc) order: a radix select of the k-th largest score over
+// the candidates, then a bitonic sort of the (usually exactly k) keys at or
+// above it. The result is exact whenever at least k non-positive candidates
+// exist and no list overflowed (every key of the true top-k is >= the k-th
+// candidate >= the threshold, hence a candidate); otherwise the query is
+// flagged for the exact running-top-k fallback.
+constexpr int kSelWarps = 4, kSelSmall = 256;
+
+__global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* cand, const int32_t* cand_cnt,
+                                                                int n_parts, int cand_cap, int64_t nq,
+                                                                const int64_t* pos_indptr, const int32_t* pos_ids,
+                                                                int k, int sel_max, uint64_t* out_keys,
+                                                                int32_t* out_ids, float* out_scores, int32_t* flags) {
+  extern __shared__ __align__(16) uint64_t sel_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * kSelWarps + warp;
+  if (q >= nq) return;  // warp-uniform
+  uint64_t* S = sel_smem + static_cast<size_t>(warp) * (sel_max + kSelSmall);
+  uint64_t* R = S + sel_max;
+  int total = 0;
+  bool overflow = false;
+  for (int p = 0; p < n_parts; ++p) {
+    const int c = cand_cnt[static_cast<size_t>(p) * nq + q];
+    overflow |= c > cand_cap;
+    total += c < cand_cap ? c : cand_cap;
+  }
+  bool fail = overflow || total > sel_max;
+  if (!fail) {
+    const int64_t p0 = pos_indptr[q], np = pos_indptr[q + 1] - p0;
+    int o = 0, valid = 0;
+    for (int p = 0; p < n_parts; ++p) {
+      const int c = min(cand_cnt[static_cast<size_t>(p) * nq + q], cand_cap);
+      const uint64_t* src = cand + (static_cast<size_t>(p) * nq + q) * cand_cap;
+      for (int e = lane; e < c; e += 32) {
+        uint64_t v = src[e];
+        if (np > 0 && sorted_contains(pos_ids + p0, np, key_id(v))) v = 0ull;
+        S[o + e] = v;
+        valid += v != 0ull;
+      }
+      o += c;
+    }
+    fail = warp_sum(valid) < k;
+  }
+  if (lane == 0) flags[q] = fail ? 1 : 0;
+  if (fail) return;
+  __syncwarp();
+  // k-th largest score bits T: count(score >= T) >= k > count(score >= T + 1)
+  uint32_t T = 0;
+  for (int b = 31; b >= 0; --b) {
+    const uint32_t c = T | (1u << b);
+    int n = 0;
+    for (int i = lane; i < total; i += 32) {
+      const uint64_t v = S[i];
+      n += v != 0ull && static_cast<uint32_t>(v >> 32) >= c;
+    }
+    if (warp_sum(n) >= k) T = c;
+  }
+  // warp-aggregated compaction of the keys with score >= T (k plus score ties)
+  int nr = 0;
+  for (int i0 = 0; i0 < total; i0 += 32) {
+    const int i = i0 + lane;
+    const uint64_t v = i < total ? S[i] : 0ull;
+    const bool take = v != 0ull && static_cast<uint32_t>(v >> 32) >= T;
+    const unsigned b = __ballot_sync(0xffffffffu, take);
+    const int at = nr + __popc(b & ((1u << lane) - 1u));
+    if (take && at < kSelSmall) R[at] = v;
+    nr += __popc(b);
+  }
+  uint64_t* X = R;
+  int n = nr;
+  if (nr > kSelSmall) {  // pathological score ties: sort everything
+    X = S;
+    n = total;
+  }
+  int Pn = 1;
+  while (Pn < n) Pn <<= 1;
+  for (int e = n + lane; e < Pn; e += 32) X[e] = 0ull;
+  __syncwarp();
+  for (int size = 2; size <= Pn; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < (Pn >> 1); i += 32) {
+        const int x = 2 * stride * (i / stride) + (i & (stride - 1));
+        const int y = x + stride;
+        const bool desc = (x & size) == 0;
+        const uint64_t va = X[x], vb = X[y];
+        if ((va < vb) == desc) {
+          X[x] = vb;
+          X[y] = va;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  for (int jj = lane; jj < k; jj += 32) {
+    const uint64_t key = X[jj];
+    const size_t o = static_cast<size_t>(q) * k + jj;
+    if (out_keys) out_keys[o] = key;
+    if (out_ids) out_ids[o] = key_id(key);
+    if (out_scores) out_scores[o] = key_score(key);
+  }
+}
+
+// ------------------------------------------------------------- workspace
+
 struct RefreshWs {
   uint64_t* gtau;
   uint16_t* qb;
   uint64_t* bufs;
   uint64_t* part_keys;
   uint64_t* merge_bufs;
-  uint64_t* cand;
+  uint64_t* rr_cand;    // BF16_RERANK: bf16 top-k' per query before the fp32 re-rank
+  // two-pass (sample / threshold / select / verify)
+  uint32_t* gmax;       // [nq][n_groups] group maxima of the label sample
+  uint64_t* tau_keys;   // [nq] per-query threshold
+  uint64_t* cand;       // [n_parts][nq][cand_cap]
+  int32_t* cand_cnt;    // [n_parts][nq]
+  int32_t* flags;       // [nq] 1 = select could not prove exactness -> fallback
 };
 
 // bf16 candidates kept per query before the fp32 re-rank: k' = max(1.5k, k+16),
@@ -361,32 +493,133 @@ int simt_parts(int64_t nq, int64_t L) {
   return static_cast<int>(parts);
 }
 
+// Two-pass refresh plan. The exact running top-k spends most of its time in
+// data-dependent compaction bursts that stall the tensor pipe (the MMA waits
+// for the slowest of four epilogue warps). The two-pass plan removes them:
+//  1. sample: every kSampleStride-th label tile (~1/16 of the flops) writes
+//     its 64-label group maxima; the j-th largest of them, t_q, is a score
+//     at least j sampled labels reach, so about j*16 labels overall; j is
+//     chosen so that P(fewer than k keys >= t_q) is ~5 sigma small for
+//     i.i.d. scores;
+//  2. threshold: the full fused GEMM appends every key >= t_q (FIXED mode:
+//     a compare per score, no compaction);
+//  3. select: exact top-k of each query's candidates, or a flag when fewer
+//     than k non-positive candidates exist (or a list overflowed);
+//  4. verify: the exact running top-k only for the query tiles holding a
+//     flagged query (CTAs of other tiles exit at once).
+// The result equals the running top-k for every query, whatever the data.
+struct TwoPass {
+  bool on = false;
+  int64_t stride = 16;
+  int j = 0;            // sample depth
+  int n_groups = 0;     // 64-label groups in the sample
+  int cand_cap = 0;     // per (query, part) candidate capacity
+  int sel_max = 0;      // per-query select capacity (power of two)
+};
+
+constexpr int64_t kSampleStride = 16;
+constexpr int kSelMax = 4096;
+
+TwoPass plan_two_pass(int64_t nq, int64_t L, int kk, int n_parts) {
+  TwoPass t;
+  const int force = [] {
+    const char* e = getenv("ASTRA_REFRESH_TWO_PASS");  // 0 = never, 1 = whenever feasible
+    return e ? atoi(e) : -1;
+  }();
+  const int64_t n_tiles = (L + kTcTileLabels - 1) / kTcTileLabels;
+  if (force == 0 || kk > 512) return t;
+  if (n_tiles < kSampleStride * (force == 1 ? 1 : 32)) return t;  // small label sets: running top-k
+  const double z = 5.0, m = static_cast<double>(kk) / kSampleStride;
+  int j = static_cast<int>(std::ceil(std::pow(z / 2 + std::sqrt(z * z / 4 + m), 2.0)));
+  const int64_t n_lt_s = (n_tiles + kSampleStride - 1) / kSampleStride;
+  j = static_cast<int>(std::min<int64_t>(j, n_lt_s * 4 / 2));  // at most half the sample's 64-label groups
+  if (j < 1) return t;
+  const double mean_per_part = static_cast<double>(j) * kSampleStride / n_parts;
+  int cap = static_cast<int>(3.0 * mean_per_part + 64.0);
+  cap = (cap + 31) / 32 * 32;
+  if (static_cast<int64_t>(cap) * n_parts > kSelMax) {
+    if (force != 1) return t;  // many parts (small batches): running top-k
+    cap = std::max(32, kSelMax / n_parts / 32 * 32);
+  }
+  t.on = true;
+  t.stride = kSampleStride;
+  t.j = j;
+  t.n_groups = static_cast<int>(n_lt_s * 4);
+  t.cand_cap = cap;
+  int sm = 1;
+  while (sm < cap * n_parts) sm <<= 1;
+  t.sel_max = std::min(sm, kSelMax);
+  return t;
+}
+
 size_t carve_refresh(void* base, size_t cap_bytes, int64_t nq, int64_t L, int d, int k, int mode, RefreshWs* w,
-                     int* n_parts_out, int* n_lists_out, int* kk_out) {
+                     int* n_parts_out, int* kk_out, TwoPass* tp) {
   Carve c(base, cap_bytes);
   const int kk = mode == ASTRA_REFRESH_BF16_RERANK ? rerank_candidates(k) : k;
   const int cap = topk_cap(kk);
-  int n_parts, n_lists;
+  int n_parts;
   size_t n_bufs;  // per-lane candidate buffers
+  size_t buf_words;
+  size_t pk_words;
+  *tp = TwoPass();
   if (mode == ASTRA_REFRESH_FP32_EXACT) {
-    n_parts = n_lists = simt_parts(nq, L);
+    n_parts = simt_parts(nq, L);
     n_bufs = static_cast<size_t>((nq + 127) / 128) * n_parts * 128;
+    buf_words = n_bufs * (cap + kTopkSlack);
+    pk_words = static_cast<size_t>(n_parts) * nq * kk;
   } else {
     int n_ctas;
-    refresh_tc_layout(nq, L, &n_ctas, &n_lists);
-    n_parts = n_lists;
-    n_bufs = static_cast<size_t>(n_ctas) * refresh_tc_split() * 128;
+    refresh_tc_layout(nq, (L + kTcTileLabels - 1) / kTcTileLabels, &n_ctas, &n_parts);
+    buf_words = static_cast<size_t>(n_ctas) * 128 * (cap + kTopkSlack);
+    pk_words = static_cast<size_t>(n_parts) * nq * kk;
+    *tp = plan_two_pass(nq, L, kk, n_parts);
   }
   w->gtau = c.take<uint64_t>(static_cast<size_t>(nq));
   w->qb = mode == ASTRA_REFRESH_FP32_EXACT ? nullptr : c.take<uint16_t>(static_cast<size_t>(nq) * d);
-  w->bufs = c.take<uint64_t>(n_bufs * (cap + kTopkSlack));
-  w->part_keys = c.take<uint64_t>(static_cast<size_t>(n_lists) * nq * kk);
+  w->bufs = c.take<uint64_t>(buf_words);
+  w->part_keys = c.take<uint64_t>(pk_words);
   w->merge_bufs = c.take<uint64_t>(static_cast<size_t>(nq) * (cap + kTopkSlack));
-  w->cand = mode == ASTRA_REFRESH_BF16_RERANK ? c.take<uint64_t>(static_cast<size_t>(nq) * kk) : nullptr;
+  w->rr_cand = mode == ASTRA_REFRESH_BF16_RERANK ? c.take<uint64_t>(static_cast<size_t>(nq) * kk) : nullptr;
+  w->gmax = nullptr;
+  w->tau_keys = w->cand = nullptr;
+  w->cand_cnt = w->flags = nullptr;
+  if (tp->on) {
+    w->gmax = c.take<uint32_t>(static_cast<size_t>(nq) * tp->n_groups);
+    w->tau_keys = c.take<uint64_t>(static_cast<size_t>(nq));
+    w->cand = c.take<uint64_t>(static_cast<size_t>(n_parts) * nq * tp->cand_cap);
+    w->cand_cnt = c.take<int32_t>(static_cast<size_t>(n_parts) * nq);
+    w->flags = c.take<int32_t>(static_cast<size_t>(nq));
+  }
   *n_parts_out = n_parts;
-  *n_lists_out = n_lists;
   *kk_out = kk;
   return c.off;
+}
+
+int topk_merge_only(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in, int k_out, uint64_t* out_keys,
+                    int32_t* out_ids, float* out_scores, uint64_t* bufs, const int32_t* only, cudaStream_t st) {
+  if (nq <= 0) return ASTRA_OK;
+  if (k_out <= 512) {
+    // part lists are sorted descending (refresh / flush output contract)
+    const unsigned grid = static_cast<unsigned>((nq + 7) / 8);
+    if (k_out <= 32)
+      merge_warp_kernel<1><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores, only);
+    else if (k_out <= 64)
+      merge_warp_kernel<2><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores, only);
+    else if (k_out <= 128)
+      merge_warp_kernel<4><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores, only);
+    else if (k_out <= 256)
+      merge_warp_kernel<8><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores, only);
+    else
+      merge_warp_kernel<16><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores, only);
+    ASTRA_LAUNCHED("merge_warp");
+    return ASTRA_OK;
+  }
+  if (only) return set_error(ASTRA_ERR_CONFIG, "merge: k_out > 512 with a query subset is not supported");
+  const int cap = topk_cap(k_out);
+  merge_kernel<<<static_cast<unsigned>((nq + 127) / 128), 128, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, cap,
+                                                                       bufs, out_keys, out_ids, out_scores);
+  ASTRA_LAUNCHED("merge");
+  return ASTRA_OK;
 }
 
 }  // namespace
@@ -401,34 +634,14 @@ int f32_to_bf16(const float* src, uint16_t* dst, int64_t n, cudaStream_t st) {
 
 size_t refresh_workspace_size(int64_t nq, int64_t L, int d, int k, int mode) {
   RefreshWs w;
-  int np, nl, kk;
-  return carve_refresh(nullptr, 0, nq, L, d, k, mode, &w, &np, &nl, &kk);
+  int np, kk;
+  TwoPass tp;
+  return carve_refresh(nullptr, 0, nq, L, d, k, mode, &w, &np, &kk, &tp);
 }
 
 int topk_merge(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in, int k_out, uint64_t* out_keys,
                int32_t* out_ids, float* out_scores, uint64_t* bufs, cudaStream_t st) {
-  if (nq <= 0) return ASTRA_OK;
-  if (k_out <= 512) {
-    // part lists are sorted descending (refresh / flush output contract)
-    const unsigned grid = static_cast<unsigned>((nq + 7) / 8);
-    if (k_out <= 32)
-      merge_warp_kernel<1><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores);
-    else if (k_out <= 64)
-      merge_warp_kernel<2><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores);
-    else if (k_out <= 128)
-      merge_warp_kernel<4><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores);
-    else if (k_out <= 256)
-      merge_warp_kernel<8><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores);
-    else
-      merge_warp_kernel<16><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores);
-    ASTRA_LAUNCHED("merge_warp");
-    return ASTRA_OK;
-  }
-  const int cap = topk_cap(k_out);
-  merge_kernel<<<static_cast<unsigned>((nq + 127) / 128), 128, 0, st>>>(part_keys, nq, n_parts, k_in, k_out, cap,
-                                                                       bufs, out_keys, out_ids, out_scores);
-  ASTRA_LAUNCHED("merge");
-  return ASTRA_OK;
+  return topk_merge_only(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores, bufs, nullptr, st);
 }
 
 int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, const float* wf, const uint16_t* wb,
@@ -450,11 +663,17 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
     return set_error(ASTRA_ERR_CONFIG, "refresh: unknown mode %d", mode);
   }
   RefreshWs w;
-  int n_parts, n_lists, kk;
-  size_t need = carve_refresh(ws, ws_bytes, nq, L, d, k, mode, &w, &n_parts, &n_lists, &kk);
+  int n_parts, kk;
+  TwoPass tp;
+  size_t need = carve_refresh(ws, ws_bytes, nq, L, d, k, mode, &w, &n_parts, &kk, &tp);
   if (!ws || ws_bytes < need) return set_error(ASTRA_ERR_CONFIG, "refresh workspace too small (%zu < %zu)", ws_bytes, need);
   if (nq == 0) return ASTRA_OK;
   const int cap = topk_cap(kk);
+  // where the bf16 / fp32 top-kk lands: the re-rank input, or the caller's outputs
+  const bool rerank = mode == ASTRA_REFRESH_BF16_RERANK;
+  uint64_t* o_keys = rerank ? w.rr_cand : out_keys;
+  int32_t* o_ids = rerank ? nullptr : out_ids;
+  float* o_scores = rerank ? nullptr : out_scores;
   if (mode == ASTRA_REFRESH_FP32_EXACT) {
     SimtArgs a;
     a.Q = qf;
@@ -478,25 +697,72 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
     cudaFuncSetAttribute(refresh_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSimtSmem);
     refresh_simt_kernel<<<grid, kSimtThreads, kSimtSmem, st>>>(a);
     ASTRA_LAUNCHED("refresh_simt");
+    ASTRA_TRY(topk_merge(w.part_keys, nq, n_parts, kk, kk, o_keys, o_ids, o_scores, w.merge_bufs, st));
   } else {
     const uint16_t* qb = qb_in;
     if (!qb) {
       ASTRA_TRY(f32_to_bf16(qf, w.qb, nq * d, st));
       qb = w.qb;
     }
-    ASTRA_TRY(launch_refresh_tc(qb, nq, d, wb, L, off, pos_indptr, pos_ids, kk, cap, w.bufs, w.part_keys, w.gtau, st));
+    TcLaunch p;
+    p.qb = qb;
+    p.nq = nq;
+    p.d = d;
+    p.wb = wb;
+    p.L = L;
+    p.off = off;
+    p.pos_indptr = pos_indptr;
+    p.pos_ids = pos_ids;
+    p.bufs = w.bufs;
+    p.part_keys = w.part_keys;
+    p.gtau = w.gtau;
+    if (tp.on) {
+      // 1. sample pass: group maxima of every stride-th label tile, threshold
+      TcLaunch s = p;
+      s.tile_stride = tp.stride;
+      s.gmax = w.gmax;
+      ASTRA_TRY(launch_refresh_tc(s, st));
+      tau_select_kernel<<<static_cast<unsigned>((nq + 7) / 8), 256, 0, st>>>(w.gmax, nq, tp.n_groups, tp.j, w.tau_keys);
+      ASTRA_LAUNCHED("tau_select");
+      // 2. threshold pass over every label
+      TcLaunch f = p;
+      f.tau_in = w.tau_keys;
+      f.tau_stride = 1;
+      f.cand = w.cand;
+      f.cand_cnt = w.cand_cnt;
+      f.cand_cap = tp.cand_cap;
+      ASTRA_TRY(launch_refresh_tc(f, st));
+      // 3. select
+      const size_t smem = sizeof(uint64_t) * (tp.sel_max + kSelSmall) * kSelWarps;
+      cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      select_kernel<<<static_cast<unsigned>((nq + kSelWarps - 1) / kSelWarps), kSelWarps * 32, smem, st>>>(
+          w.cand, w.cand_cnt, n_parts, tp.cand_cap, nq, pos_indptr, pos_ids, kk, tp.sel_max, o_keys, o_ids, o_scores,
+          w.flags);
+      ASTRA_LAUNCHED("select");
+      // 4. verify: exact running top-k for the flagged query tiles only
+      TcLaunch v = p;
+      v.k = kk;
+      v.cap = cap;
+      v.only_flagged = w.flags;
+      ASTRA_TRY(launch_refresh_tc(v, st));
+      ASTRA_TRY(topk_merge_only(w.part_keys, nq, n_parts, kk, kk, o_keys, o_ids, o_scores, w.merge_bufs, w.flags, st));
+    } else {
+      p.k = kk;
+      p.cap = cap;
+      ASTRA_TRY(launch_refresh_tc(p, st));
+      ASTRA_TRY(topk_merge(w.part_keys, nq, n_parts, kk, kk, o_keys, o_ids, o_scores, w.merge_bufs, st));
+    }
   }
-  if (mode == ASTRA_REFRESH_BF16_RERANK) {
-    ASTRA_TRY(topk_merge(w.part_keys, nq, n_lists, kk, kk, w.cand, nullptr, nullptr, w.merge_bufs, st));
+  if (rerank) {
     int Pn = 1;
     while (Pn < kk) Pn <<= 1;
     size_t smem = align_up(sizeof(float) * (d + kRrWarps * 32 * kRrPitch), 16) + sizeof(uint64_t) * Pn;
     if (smem > 48 * 1024) cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    rerank_kernel<<<static_cast<unsigned>(nq), kRrWarps * 32, smem, st>>>(qf, wf, d, off, w.cand, kk, k, out_keys, out_ids, out_scores);
+    rerank_kernel<<<static_cast<unsigned>(nq), kRrWarps * 32, smem, st>>>(qf, wf, d, off, w.rr_cand, kk, k, out_keys,
+                                                                           out_ids, out_scores);
     ASTRA_LAUNCHED("rerank");
-    return ASTRA_OK;
   }
-  return topk_merge(w.part_keys, nq, n_lists, kk, k, out_keys, out_ids, out_scores, w.merge_bufs, st);
+  return ASTRA_OK;
 }
 
 }  // namespace astra

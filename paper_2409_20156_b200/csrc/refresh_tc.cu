@@ -4,15 +4,22 @@
 // One CTA owns a 128-query tile and sweeps a contiguous range of label tiles
 // (N = 256 labels each). Warp roles (256 threads):
 //   warp 0      TMA producer: A (128 x 64 bf16) and B (256 x 64 bf16) k-blocks,
-//               SWIZZLE_128B, into a 4-stage shared-memory ring (48 KB/stage).
+//               SWIZZLE_128B, into a 4-stage shared-memory ring (48 KB/stage);
+//               with a cluster of CL query tiles each CTA loads 1/CL of every
+//               W tile and multicasts it to the cluster.
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma.kind::f16
 //               (M=128, N=256, K=16) into a TMEM accumulator; tcgen05.commit
 //               releases smem stages and publishes finished accumulators.
 //   warp 2      TMEM allocator (512 columns = 2 accumulators of 256 fp32 cols).
-//   warps 4-7   epilogue: tcgen05.ld 32 columns at a time (thread = query row =
-//               TMEM lane), running top-k per query (topk.cuh). The two TMEM
-//               accumulators double-buffer the epilogue against the next MMA.
-// Scores never leave the SM; per-query partial top-k lists go to HBM once.
+//   warps 4-7   epilogue: tcgen05.ld 64 columns per step (thread = query row =
+//               TMEM lane), one warp vote per step, then either
+//                 RUNNING  exact running top-k per query (topk.cuh), or
+//                 FIXED    append every key >= a per-query threshold to a
+//                          candidate list (no compaction, no bursts), or
+//                 GMAX     write the maximum of every 64-label group (the
+//                          sample pass: a threshold source).
+// Scores never leave the SM. refresh.cu composes the two modes into the
+// sample / threshold / select / verify pipeline (see the comment there).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -22,22 +29,22 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "refresh_tc.cuh"
 #include "topk.cuh"
 
 namespace astra {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, UMMA_K = 16, STAGES = 4;
+constexpr int BM = 128, BN = kTcTileLabels, BK = 64, UMMA_K = 16, STAGES = 4;
 constexpr int A_STAGE = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int TMEM_COLS = 512;
-constexpr int kEpiWarp0 = 4;
-// SPLIT = epilogue warps per TMEM lane quadrant; each owns (32 query rows) x
-// (BN / SPLIT columns) and its own partial list. Threads = 32 * (4 + 4*SPLIT).
-template <int SPLIT>
-constexpr int threads_for() { return 32 * (kEpiWarp0 + 4 * SPLIT); }
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+constexpr int kEpiWarp0 = 4, kEpiWarps = 4;
+constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
+constexpr size_t kBarrierBytes = 256;
+// + one 256 B score-staging row per epilogue thread (slow path of scan64)
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + STAGES * STAGE_BYTES + kBarrierBytes + kEpiWarps * 32 * 256;
 
 // idesc for kind::f16: D=F32, A=B=BF16, both K-major, N>>3 at [17,23), M>>4 at [24,29)
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -145,102 +152,151 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// r[j] for a run-time j without local memory: a 5-level select tree.
-__device__ __forceinline__ uint32_t pick32(const uint32_t* r, int j) {
-  uint32_t a[16], b[8], c[4], d[2];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) a[i] = (j & 16) ? r[i + 16] : r[i];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) b[i] = (j & 8) ? a[i + 8] : a[i];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) c[i] = (j & 4) ? b[i + 4] : b[i];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) d[i] = (j & 2) ? c[i + 2] : c[i];
-  return (j & 1) ? d[1] : d[0];
-}
-
 struct TcArgs {
   int64_t nq, L, off;
   int d, k, cap;
-  int64_t n_lt, tiles_per_part;  // label tiles; label tiles per part
+  int64_t n_lt, tiles_per_part, tile_stride;  // swept label tiles, per part, stride between them
   const int64_t* pos_indptr;
   const int32_t* pos_ids;
-  uint64_t* bufs;
-  uint64_t* part_keys;
-  uint64_t* gtau;  // nq shared thresholds (zeroed by the host before launch)
+  uint64_t* bufs;       // RUNNING: per-lane buffers
+  uint64_t* part_keys;  // RUNNING: [n_parts][nq][k]
+  uint64_t* gtau;       // RUNNING: nq shared thresholds (zeroed by the host before launch)
+  const uint64_t* tau_in;  // FIXED: threshold of query q = tau_in[q * tau_stride]
+  int tau_stride;
+  uint64_t* cand;          // FIXED: [n_parts][nq][cand_cap]
+  int32_t* cand_cnt;       // FIXED: [n_parts][nq]
+  int cand_cap;
+  uint32_t* gmax;          // GMAX: [nq][n_lt * 4] orderable bits of the 64-label group maxima
+  const int32_t* only_flagged;
   int debug_no_topk;  // ASTRA_TC_DEBUG_NO_TOPK=1: skip selection (pipeline-rate measurement only)
-  unsigned long long* dbg;  // ASTRA_TC_DEBUG_COUNTERS=1: [slow chunks, candidates, compactions, chunks]
+  // ASTRA_TC_DEBUG_COUNTERS=1: [slow steps, -, compactions, steps, then clock64 cycle sums:
+  // 4 epi tfull wait, 5 epi fast path, 6 epi slow path, 7 epi settle, 8 epi total,
+  // 9 mma tempty wait, 10 mma full wait, 11 mma total]
+  unsigned long long* dbg;
 };
 
-// Schedule: grid (query tile, label part). Each CTA sweeps one contiguous
-// label range for one 128-query tile; all CTAs of a part stream the same W
-// tiles at about the same time, so W comes from DRAM ~once per part and the
-// other query tiles hit L2. Lists per query = n_parts * SPLIT.
-struct Seg {
-  int64_t qt, lt0, lt1;
-  int slot;
+enum { kRunning = 0, kFixed = 1, kGmax = 2 };
+
+struct EpiProf {
+  long long fast = 0, slow = 0, settle = 0;
 };
 
-__device__ __forceinline__ bool next_seg(int64_t& u, int64_t u1, const TcArgs& a, Seg& s) {
-  if (u > u1) return false;  // exactly one (possibly empty) segment per CTA: empty ones flush zeros
-  (void)a;
-  s.qt = blockIdx.x;
-  s.lt0 = u;
-  s.lt1 = u1;
-  s.slot = blockIdx.y;
-  u = u1 + 1;
-  return true;
+// Admit one score (RUNNING: key > tau into the lane buffer, room guaranteed by
+// topk_settle; FIXED: key >= tau into the candidate list, counting past the
+// capacity — overflow is detected by the select pass).
+template <bool FIXED>
+__device__ __forceinline__ void admit(LaneTopK& tk, float s, uint32_t gid, int cand_cap) {
+  if (s >= tk.tau_s) {
+    if constexpr (FIXED) {
+      const uint64_t key = make_key(s, gid);
+      if (key >= tk.tau) {
+        if (tk.cnt < cand_cap) tk.buf[tk.cnt] = key;
+        ++tk.cnt;
+      }
+    } else {
+      lane_offer(tk, s, gid);
+    }
+  }
 }
 
-// Scan one 32-column chunk of scores held in registers: a warp vote on the
-// per-lane maxima skips the chunk unless some query can admit a candidate;
-// candidates are appended (r[] indexed through a select tree, no local memory)
-// and over-full buffers compacted once r[] is dead.
-template <class Args>
-__device__ __forceinline__ void scan_chunk(LaneTopK& tk, const uint32_t* r, int cn, uint32_t g0, bool active,
-                                           const Args& a) {
-  if (cn <= 0 || a.debug_no_topk) return;  // tile tail (uniform across the CTA)
-  float t16[16];
+// Scan 64 columns held in registers (ra = columns 0-31, rb = 32-63 of the
+// step). Fast path: an FMNMX3 max tree over the 64 scores and ONE warp vote;
+// the warp skips the step unless some query can admit a candidate. Slow path:
+// the tree level with 8 maxima (group g = columns g + 8i) picks the groups to
+// inspect; the step is staged in the lane's 256 B shared-memory row with group
+// g's 8 scores in 16 B chunks 2g, 2g+1 (chunk c stored at c ^ (lane & 7):
+// conflict-free STS.128), so a flagged group costs two LDS.128 and 8 compares.
+// The tile-tail guards exist only in the !FULL instance.
+template <bool FULL, bool FIXED, class Args>
+__device__ __forceinline__ void scan64(LaneTopK& tk, const uint32_t* ra, const uint32_t* rb, int cn, uint32_t g0,
+                                       bool active, const Args& a, float* stage, EpiProf& pf) {
+  if (!FULL && cn <= 0) return;  // tile tail (uniform across the CTA)
+  if (a.debug_no_topk) return;
+  const long long c0 = a.dbg ? clock64() : 0;
+  auto val = [&](int col) -> float {  // score of column col (compile-time) of the step, -inf past the tail
+    const float v = __uint_as_float(col < 32 ? ra[col] : rb[col - 32]);
+    return (FULL || col < cn) ? v : -INFINITY;
+  };
+  float t[32];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const float x0 = (j < cn) ? __uint_as_float(r[j]) : -INFINITY;
-    const float x1 = (j + 16 < cn) ? __uint_as_float(r[j + 16]) : -INFINITY;
-    t16[j] = fmaxf(x0, x1);
-  }
+  for (int j = 0; j < 32; ++j) t[j] = fmaxf(val(j), val(j + 32));
 #pragma unroll
-  for (int w = 8; w > 0; w >>= 1)
+  for (int j = 0; j < 16; ++j) t[j] = fmaxf(t[j], t[j + 16]);
+  float grp[8];  // grp[g] = max of columns g + 8i, i < 8
 #pragma unroll
-    for (int j = 0; j < w; ++j) t16[j] = fmaxf(t16[j], t16[j + w]);
+  for (int j = 0; j < 8; ++j) grp[j] = fmaxf(t[j], t[j + 8]);
+  const float m = fmaxf(fmaxf(fmaxf(grp[0], grp[1]), fmaxf(grp[2], grp[3])),
+                        fmaxf(fmaxf(grp[4], grp[5]), fmaxf(grp[6], grp[7])));
+  const bool want = active && m >= tk.tau_s;
+  const bool any = __any_sync(0xffffffffu, want);
   if (a.dbg && (threadIdx.x & 31) == 0) atomicAdd(a.dbg + 3, 1ull);
-  if (!__any_sync(0xffffffffu, active && t16[0] >= tk.tau_s)) return;  // the common case
+  const long long c1 = a.dbg ? clock64() : 0;
+  if (a.dbg) pf.fast += c1 - c0;
+  if (!any) return;
   if (a.dbg && (threadIdx.x & 31) == 0) atomicAdd(a.dbg + 0, 1ull);
-  uint32_t m = 0;
-  if (active) {
+  const int sw = threadIdx.x & 7;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) m |= (j < cn && __uint_as_float(r[j]) >= tk.tau_s) ? (1u << j) : 0u;
+  for (int g = 0; g < 8; ++g) {
+    *reinterpret_cast<float4*>(stage + (((2 * g) ^ sw) << 2)) = make_float4(val(g), val(g + 8), val(g + 16), val(g + 24));
+    *reinterpret_cast<float4*>(stage + (((2 * g + 1) ^ sw) << 2)) =
+        make_float4(val(g + 32), val(g + 40), val(g + 48), val(g + 56));
   }
-  while (m) {
-    const int j = __ffs(m) - 1;
-    m &= m - 1;
-    lane_offer(tk, __uint_as_float(pick32(r, j)), g0 + j);
+  uint32_t gm = 0;
+  if (want) {
+#pragma unroll
+    for (int g = 0; g < 8; ++g) gm |= grp[g] >= tk.tau_s ? (1u << g) : 0u;
   }
-  if (a.dbg) {
-    const unsigned need = __ballot_sync(0xffffffffu, active && (tk.cnt - tk.nsorted) > a.cap / 2);
-    if ((threadIdx.x & 31) == 0) atomicAdd(a.dbg + 2, static_cast<unsigned long long>(__popc(need)));
+  while (gm) {
+    const int g = __ffs(gm) - 1;
+    gm &= gm - 1;
+    const float4 x = *reinterpret_cast<const float4*>(stage + (((2 * g) ^ sw) << 2));
+    const float4 y = *reinterpret_cast<const float4*>(stage + (((2 * g + 1) ^ sw) << 2));
+    const uint32_t gg = g0 + g;
+    admit<FIXED>(tk, x.x, gg, a.cand_cap);
+    admit<FIXED>(tk, x.y, gg + 8, a.cand_cap);
+    admit<FIXED>(tk, x.z, gg + 16, a.cand_cap);
+    admit<FIXED>(tk, x.w, gg + 24, a.cand_cap);
+    admit<FIXED>(tk, y.x, gg + 32, a.cand_cap);
+    admit<FIXED>(tk, y.y, gg + 40, a.cand_cap);
+    admit<FIXED>(tk, y.z, gg + 48, a.cand_cap);
+    admit<FIXED>(tk, y.w, gg + 56, a.cand_cap);
   }
-  topk_settle(tk, a.cap, a.k, active);
+  __syncwarp();
+  if constexpr (!FIXED) {
+    long long c2 = 0;
+    if (a.dbg) {
+      const unsigned need = __ballot_sync(0xffffffffu, active && (tk.cnt - tk.nsorted) > a.cap / 2);
+      if ((threadIdx.x & 31) == 0) atomicAdd(a.dbg + 2, static_cast<unsigned long long>(__popc(need)));
+      c2 = clock64();
+      pf.slow += c2 - c1;
+    }
+    topk_settle(tk, a.cap, a.k, active);  // <= 64 appends per lane since the last settle (kTopkSlack)
+    if (a.dbg) pf.settle += clock64() - c2;
+  } else {
+    if (a.dbg) pf.slow += clock64() - c1;
+  }
 }
 
-// CL = cluster size along query tiles: the CL CTAs of a cluster sweep the same
-// label tiles; each loads 1/CL of every W tile and multicasts it to all of them,
-// so W leaves L2 once per cluster and the cluster moves in lockstep.
-template <int SPLIT, int CL>
-__global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
+// Grid (query tile, label part): each CTA sweeps one contiguous range of the
+// swept label tiles for one 128-query tile; all CTAs of a part stream the same
+// W tiles at about the same time, so W comes from DRAM ~once per part and the
+// other query tiles hit L2. CL = cluster size along query tiles: the CL CTAs
+// of a cluster sweep the same label tiles; each loads 1/CL of every W tile and
+// multicasts it to all of them.
+template <int CL, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
     refresh_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
-  constexpr int kEpiSplit = SPLIT;
-  constexpr int kEpiWarps = 4 * SPLIT;
   constexpr uint16_t kMask = static_cast<uint16_t>((1u << CL) - 1);
   constexpr int B_SLICE = B_STAGE / CL;  // bytes of W tile rows loaded by each cluster rank
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (a.only_flagged) {
+    // verification fallback: the whole cluster leaves unless one of its queries is flagged
+    const int64_t q0 = static_cast<int64_t>(blockIdx.x / CL) * CL * BM;
+    int f = 0;
+    for (int i = threadIdx.x; i < CL * BM; i += kThreads)
+      if (q0 + i < a.nq && a.only_flagged[q0 + i]) f = 1;
+    if (!__syncthreads_or(f)) return;
+  }
   const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -251,8 +307,8 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stage_base = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + kBarrierBytes);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t u_begin = std::min<int64_t>(a.n_lt, static_cast<int64_t>(blockIdx.y) * a.tiles_per_part);
   const int64_t u_end = std::min<int64_t>(a.n_lt, u_begin + a.tiles_per_part);
   const int nkb = a.d / BK;
@@ -288,25 +344,21 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int64_t u = u_begin;
-      Seg sg;
-      while (next_seg(u, u_end, a, sg)) {
-        const int q0 = static_cast<int>(sg.qt * BM);
-        for (int64_t t = sg.lt0; t < sg.lt1; ++t) {
-          const int n0 = static_cast<int>(t * BN);
-          for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], STAGE_BYTES);  // own A + all CL slices of the W tile
-            tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, q0);
-            if (CL == 1)
-              tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
-            else
-              tma_load_2d_mc(sB + stage * B_STAGE + crank * B_SLICE, &tmB, &full[stage], kb * BK,
-                             n0 + static_cast<int>(crank) * (BN / CL), kMask);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
+      const int q0 = static_cast<int>(blockIdx.x * BM);
+      for (int64_t t = u_begin; t < u_end; ++t) {
+        const int n0 = static_cast<int>(t * a.tile_stride * BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], STAGE_BYTES);  // own A + all CL slices of the W tile
+          tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, q0);
+          if (CL == 1)
+            tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
+          else
+            tma_load_2d_mc(sB + stage * B_STAGE + crank * B_SLICE, &tmB, &full[stage], kb * BK,
+                           n0 + static_cast<int>(crank) * (BN / CL), kMask);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
@@ -317,13 +369,18 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    const int64_t n_units = u_end - u_begin;  // MMA tiles of this CTA, in schedule order
-    for (int64_t t = 0; t < n_units; ++t) {
+    long long p_te = 0, p_full = 0;
+    const long long p_t0 = a.dbg ? clock64() : 0;
+    for (int64_t t = u_begin; t < u_end; ++t) {
+      long long w0 = a.dbg ? clock64() : 0;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
+      if (a.dbg) p_te += clock64() - w0;
       tc_fence_after();
       const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * BN);
       for (int kb = 0; kb < nkb; ++kb) {
+        w0 = a.dbg ? clock64() : 0;
         mbar_wait(&full[stage], phase);
+        if (a.dbg) p_full += clock64() - w0;
         tc_fence_after();
         if (lane == 0) {
           const uint64_t ad = smem_desc(sA + stage * A_STAGE);
@@ -351,34 +408,54 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
         acc_phase ^= 1;
       }
     }
+    if (a.dbg && lane == 0) {
+      atomicAdd(a.dbg + 9, static_cast<unsigned long long>(p_te));
+      atomicAdd(a.dbg + 10, static_cast<unsigned long long>(p_full));
+      atomicAdd(a.dbg + 11, static_cast<unsigned long long>(clock64() - p_t0));
+    }
   } else if (warp >= kEpiWarp0) {
-    // ---------------- epilogue: TMEM -> registers -> running top-k
-    // warp e = warp - 4 reads TMEM lanes 32*(e%4).. (its lane quadrant, = warp % 4)
-    // and columns [half*BN/2, (half+1)*BN/2) of every accumulator.
-    const int e = warp - kEpiWarp0, quad = e & 3, half = e >> 2;
-    const int row = quad * 32 + lane;  // TMEM lane = query row in tile
-    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
-    uint64_t* buf = a.bufs + ((static_cast<size_t>(blockIdx.x * gridDim.y + blockIdx.y) * kEpiSplit + half) * BM + row) *
-                             (a.cap + kTopkSlack);
-    constexpr int kCols = BN / kEpiSplit;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    int64_t u = u_begin;
-    Seg sg;
-    while (next_seg(u, u_end, a, sg)) {
-      const int64_t q = sg.qt * BM + row;
-      const bool active = q < a.nq;
-      LaneTopK tk;
-      {
-        const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
+    // ---------------- epilogue: TMEM -> registers -> per-query selection
+    // warp e = warp - 4 reads TMEM lanes 32*e.. (its lane quadrant, = warp % 4)
+    const int e = warp - kEpiWarp0;
+    const int row = e * 32 + lane;  // TMEM lane = query row in tile
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(e * 32) << 16);
+    float* stage = stage_base + (e * 32 + lane) * 64;
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * BM + row;
+    const bool active = q < a.nq;
+    const int list = blockIdx.y;
+    LaneTopK tk;
+    {
+      const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
+      if constexpr (MODE == kGmax) {
+        lane_init(tk, nullptr, nullptr, 0);
+        (void)p0;
+        (void)p1;
+      } else if constexpr (MODE == kFixed) {
+        lane_init(tk, a.cand + (static_cast<size_t>(list) * a.nq + (active ? q : 0)) * a.cand_cap, nullptr, 0);
+        tk.tau = active ? a.tau_in[static_cast<size_t>(q) * a.tau_stride] : ~0ull;
+        tk.tau_s = tk.tau ? key_score(tk.tau) : -INFINITY;
+        (void)p0;
+        (void)p1;
+      } else {
+        uint64_t* buf = a.bufs + (static_cast<size_t>(blockIdx.x * gridDim.y + blockIdx.y) * BM + row) *
+                                     (a.cap + kTopkSlack);
         lane_init(tk, buf, a.pos_ids + p0, p1 - p0, active ? a.gtau + q : nullptr);
       }
-      uint64_t g_pref = 0;  // shared threshold prefetched one tile ahead
-      for (int64_t t = sg.lt0; t < sg.lt1; ++t) {
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-        const int64_t n0 = t * BN;
-        const int nvalid = static_cast<int>(std::min<int64_t>(BN, a.L - n0));
+    }
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    EpiProf pf;
+    long long p_wait = 0;
+    const long long p_t0 = a.dbg ? clock64() : 0;
+    uint64_t g_pref = 0;  // RUNNING: shared threshold prefetched one tile ahead
+    for (int64_t t = u_begin; t < u_end; ++t) {
+      const long long w0 = a.dbg ? clock64() : 0;
+      mbar_wait(&tfull[acc], acc_phase);
+      if (a.dbg) p_wait += clock64() - w0;
+      tc_fence_after();
+      const int64_t n0 = t * a.tile_stride * BN;
+      const int nvalid = static_cast<int>(std::min<int64_t>(BN, a.L - n0));
+      if constexpr (MODE == kRunning) {
         // shared threshold: apply the value fetched during the previous tile, fetch the next
         if (tk.gtau) {
           if (g_pref > tk.tau) {
@@ -387,37 +464,66 @@ __global__ void __launch_bounds__(threads_for<SPLIT>(), 1)
           }
           g_pref = *reinterpret_cast<volatile uint64_t*>(tk.gtau);
         }
-        // 32-column chunks, the next chunk's TMEM load in flight while this one is scanned
-        const uint32_t tbase = lane_base + static_cast<uint32_t>(acc * BN + half * kCols);
-        const int col0 = half * kCols;
-        uint32_t ra[32], rb[32];
-        __syncwarp();
-        tmem_ld32_nowait(tbase, ra);
-        tmem_wait();
-#pragma unroll 1
-        for (int c = 0; c < kCols; c += 64) {
+      }
+      // 64-column steps: two 32-column TMEM loads, one wait, one vote
+      const uint32_t tbase = lane_base + static_cast<uint32_t>(acc * BN);
+      const bool full_tile = nvalid == BN;
+      if constexpr (MODE == kGmax) {
+        uint32_t gm[4];
+#pragma unroll
+        for (int c = 0; c < BN; c += 64) {
+          uint32_t ra[32], rb[32];
           __syncwarp();
+          tmem_ld32_nowait(tbase + c, ra);
           tmem_ld32_nowait(tbase + c + 32, rb);
-          scan_chunk(tk, ra, nvalid - (col0 + c), static_cast<uint32_t>(n0 + col0 + c + a.off), active, a);
-          __syncwarp();
           tmem_wait();
-          __syncwarp();
-          if (c + 64 < kCols) tmem_ld32_nowait(tbase + c + 64, ra);
-          scan_chunk(tk, rb, nvalid - (col0 + c + 32), static_cast<uint32_t>(n0 + col0 + c + 32 + a.off), active, a);
-          __syncwarp();
-          tmem_wait();
+          float m = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float x0 = (full_tile || c + j < nvalid) ? __uint_as_float(ra[j]) : -INFINITY;
+            const float x1 = (full_tile || c + j + 32 < nvalid) ? __uint_as_float(rb[j]) : -INFINITY;
+            m = fmaxf(m, fmaxf(x0, x1));
+          }
+          gm[c / 64] = ord_bits(__float_as_uint(__fadd_rn(m, 0.0f)));  // -inf: empty group, below every score
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
+        if (active)
+          *reinterpret_cast<uint4*>(a.gmax + static_cast<size_t>(q) * (a.n_lt * 4) + t * 4) =
+              make_uint4(gm[0], gm[1], gm[2], gm[3]);
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 64) {
+          uint32_t ra[32], rb[32];
+          __syncwarp();
+          tmem_ld32_nowait(tbase + c, ra);
+          tmem_ld32_nowait(tbase + c + 32, rb);
+          tmem_wait();
+          const uint32_t g0 = static_cast<uint32_t>(n0 + c + a.off);
+          if (full_tile)
+            scan64<true, MODE == kFixed>(tk, ra, rb, 64, g0, active, a, stage, pf);
+          else
+            scan64<false, MODE == kFixed>(tk, ra, rb, nvalid - c, g0, active, a, stage, pf);
         }
       }
-      const int list = sg.slot * kEpiSplit + half;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if constexpr (MODE == kFixed) {
+      if (active) a.cand_cnt[static_cast<size_t>(list) * a.nq + q] = tk.cnt;
+    } else if constexpr (MODE == kRunning) {
       uint64_t* out = a.part_keys + (static_cast<size_t>(list) * a.nq + (active ? q : 0)) * a.k;
       topk_flush(tk, a.cap, a.k, active, out);
+    }
+    if (a.dbg && lane == 0) {
+      atomicAdd(a.dbg + 4, static_cast<unsigned long long>(p_wait));
+      atomicAdd(a.dbg + 5, static_cast<unsigned long long>(pf.fast));
+      atomicAdd(a.dbg + 6, static_cast<unsigned long long>(pf.slow));
+      atomicAdd(a.dbg + 7, static_cast<unsigned long long>(pf.settle));
+      atomicAdd(a.dbg + 8, static_cast<unsigned long long>(clock64() - p_t0));
     }
   }
 
@@ -458,10 +564,10 @@ int make_map(CUtensorMap* m, const void* base, int64_t rows, int d, int box_rows
   return ASTRA_OK;
 }
 
-template <int SPLIT, int CL>
+template <int CL, int MODE>
 int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const TcArgs& a, dim3 grid, cudaStream_t st) {
   static bool attr_set = false;
-  auto kern = refresh_tc_kernel<SPLIT, CL>;
+  auto kern = refresh_tc_kernel<CL, MODE>;
   if (!attr_set) {
     ASTRA_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(kSmemBytes)),
@@ -470,7 +576,7 @@ int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const TcArgs&
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(threads_for<SPLIT>());
+  cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -485,93 +591,93 @@ int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const TcArgs&
   return ASTRA_OK;
 }
 
-}  // namespace
-
-// Cluster size along query tiles (ASTRA_TC_CLUSTER=1|2|4, default 2), reduced
-// for batches with few query tiles.
+// Cluster size along query tiles (ASTRA_TC_CLUSTER=1|2, default 2), reduced
+// for batches with a single query tile.
 int refresh_tc_cluster(int64_t n_qt) {
   static int cl = [] {
     const char* e = getenv("ASTRA_TC_CLUSTER");
-    const int v = e ? atoi(e) : 2;
-    return (v == 1 || v == 2 || v == 4) ? v : 2;
+    return (e && atoi(e) == 1) ? 1 : 2;
   }();
-  int c = cl;
-  while (c > 1 && n_qt < c) c >>= 1;
-  return c;
+  return n_qt < cl ? 1 : cl;
 }
 
-// Epilogue split (ASTRA_TC_SPLIT=1|2, default 1: measured faster, fewer partial lists).
-int refresh_tc_split() {
-  static int split = [] {
-    const char* e = getenv("ASTRA_TC_SPLIT");
-    return (e && atoi(e) == 2) ? 2 : 1;
-  }();
-  return split;
-}
+}  // namespace
 
-// Number of CTAs and of partial lists per query for nq queries over L labels.
-void refresh_tc_layout(int64_t nq, int64_t L, int* n_ctas, int* n_lists) {
+void refresh_tc_layout(int64_t nq, int64_t n_tiles, int* n_ctas, int* n_parts) {
   int64_t n_qt = std::max<int64_t>(1, (nq + BM - 1) / BM);
   const int cl = refresh_tc_cluster(n_qt);
   n_qt = (n_qt + cl - 1) / cl * cl;  // whole clusters (padding tiles hold no queries)
-  const int64_t n_lt = std::max<int64_t>(1, (L + BN - 1) / BN);
-  const int64_t parts = std::min<int64_t>(n_lt, std::max<int64_t>(1, num_sms() / n_qt));
+  n_tiles = std::max<int64_t>(1, n_tiles);
+  const int64_t parts = std::min<int64_t>(n_tiles, std::max<int64_t>(1, num_sms() / n_qt));
   *n_ctas = static_cast<int>(n_qt * parts);
-  *n_lists = static_cast<int>(parts) * refresh_tc_split();
+  *n_parts = static_cast<int>(parts);
 }
 
-int launch_refresh_tc(const uint16_t* qb, int64_t nq, int d, const uint16_t* wb, int64_t L, int64_t label_offset,
-                      const int64_t* pos_indptr, const int32_t* pos_ids, int k, int cap, uint64_t* bufs,
-                      uint64_t* part_keys, uint64_t* gtau, cudaStream_t st) {
-  if ((reinterpret_cast<uintptr_t>(qb) & 15) || (reinterpret_cast<uintptr_t>(wb) & 15))
+int launch_refresh_tc(const TcLaunch& p, cudaStream_t st) {
+  if ((reinterpret_cast<uintptr_t>(p.qb) & 15) || (reinterpret_cast<uintptr_t>(p.wb) & 15))
     return set_error(ASTRA_ERR_CONFIG, "bf16 operands must be 16-byte aligned");
-  if (L <= 0) return ASTRA_OK;
-  int G, n_lists;
-  refresh_tc_layout(nq, L, &G, &n_lists);
-  const int n_parts = n_lists / refresh_tc_split();
-  const int cl = refresh_tc_cluster((nq + BM - 1) / BM);
+  if (p.L <= 0 || p.nq <= 0) return ASTRA_OK;
+  const int64_t n_tiles_all = (p.L + BN - 1) / BN;
+  const int64_t n_lt = (n_tiles_all + p.tile_stride - 1) / p.tile_stride;
+  int G, n_parts;
+  refresh_tc_layout(p.nq, n_lt, &G, &n_parts);
+  const int cl = refresh_tc_cluster((p.nq + BM - 1) / BM);
   CUtensorMap tmA, tmB;
-  ASTRA_TRY(make_map(&tmA, qb, nq, d, BM));
-  ASTRA_TRY(make_map(&tmB, wb, L, d, BN / cl));
+  ASTRA_TRY(make_map(&tmA, p.qb, p.nq, p.d, BM));
+  ASTRA_TRY(make_map(&tmB, p.wb, p.L, p.d, BN / cl));
   TcArgs a;
-  a.nq = nq;
-  a.L = L;
-  a.off = label_offset;
-  a.d = d;
-  a.k = k;
-  a.cap = cap;
-  a.n_lt = (L + BN - 1) / BN;
-  a.tiles_per_part = (a.n_lt + n_parts - 1) / n_parts;
-  a.pos_indptr = pos_indptr;
-  a.pos_ids = pos_ids;
-  a.bufs = bufs;
-  a.part_keys = part_keys;
-  a.gtau = gtau;
+  a.nq = p.nq;
+  a.L = p.L;
+  a.off = p.off;
+  a.d = p.d;
+  a.k = p.k;
+  a.cap = p.cap;
+  a.n_lt = n_lt;
+  a.tiles_per_part = (n_lt + n_parts - 1) / n_parts;
+  a.tile_stride = p.tile_stride;
+  a.pos_indptr = p.pos_indptr;
+  a.pos_ids = p.pos_ids;
+  a.bufs = p.bufs;
+  a.part_keys = p.part_keys;
+  a.gtau = p.gtau;
+  a.tau_in = p.tau_in;
+  a.tau_stride = p.tau_stride;
+  a.cand = p.cand;
+  a.cand_cnt = p.cand_cnt;
+  a.cand_cap = p.cand_cap;
+  a.only_flagged = p.only_flagged;
+  a.gmax = p.gmax;
+  const int mode = p.gmax ? kGmax : (p.tau_in ? kFixed : kRunning);
   a.debug_no_topk = getenv("ASTRA_TC_DEBUG_NO_TOPK") != nullptr;
   static unsigned long long* dbg_buf = nullptr;
   const bool counters = getenv("ASTRA_TC_DEBUG_COUNTERS") != nullptr;
-  if (counters && !dbg_buf) cudaMalloc(&dbg_buf, 4 * sizeof(unsigned long long));
+  if (counters && !dbg_buf) cudaMalloc(&dbg_buf, 12 * sizeof(unsigned long long));
   a.dbg = counters ? dbg_buf : nullptr;
-  if (counters) cudaMemsetAsync(dbg_buf, 0, 4 * sizeof(unsigned long long), st);
-  ASTRA_TRY(check_cuda(cudaMemsetAsync(gtau, 0, sizeof(uint64_t) * nq, st), "memset gtau"));
+  if (counters) cudaMemsetAsync(dbg_buf, 0, 12 * sizeof(unsigned long long), st);
+  if (mode == kRunning) ASTRA_TRY(check_cuda(cudaMemsetAsync(p.gtau, 0, sizeof(uint64_t) * p.nq, st), "memset gtau"));
   const dim3 grid(static_cast<unsigned>(G / n_parts), static_cast<unsigned>(n_parts));
-  const int split = refresh_tc_split();
-  if (counters) {
-    int rc = split == 1 ? (cl == 2 ? launch_variant<1, 2>(tmA, tmB, a, grid, st) : launch_variant<1, 1>(tmA, tmB, a, grid, st))
-                        : launch_variant<2, 1>(tmA, tmB, a, grid, st);
-    unsigned long long h[4];
+  int rc;
+  if (mode == kFixed)
+    rc = cl == 2 ? launch_variant<2, kFixed>(tmA, tmB, a, grid, st) : launch_variant<1, kFixed>(tmA, tmB, a, grid, st);
+  else if (mode == kGmax)
+    rc = cl == 2 ? launch_variant<2, kGmax>(tmA, tmB, a, grid, st) : launch_variant<1, kGmax>(tmA, tmB, a, grid, st);
+  else
+    rc = cl == 2 ? launch_variant<2, kRunning>(tmA, tmB, a, grid, st) : launch_variant<1, kRunning>(tmA, tmB, a, grid, st);
+  if (counters && rc == ASTRA_OK) {
+    unsigned long long h[12];
     cudaMemcpyAsync(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    fprintf(stderr, "[refresh_tc] nq=%lld k=%d slow_chunks=%llu/%llu (%.3f) cnt_sum_at_settle=%llu compactions=%llu\n",
-            (long long)nq, k, h[0], h[3], h[3] ? double(h[0]) / h[3] : 0.0, h[1], h[2]);
-    return rc;
+    const double ew = static_cast<double>(G) * kEpiWarps, mw = G;
+    fprintf(stderr, "[refresh_tc %s] nq=%lld k=%d stride=%lld slow_steps=%llu/%llu (%.3f) compactions=%llu\n",
+            mode == kFixed ? "fixed" : (mode == kGmax ? "gmax" : "running"), (long long)p.nq, p.k, (long long)p.tile_stride, h[0], h[3],
+            h[3] ? double(h[0]) / h[3] : 0.0, h[2]);
+    fprintf(stderr,
+            "[refresh_tc] per epilogue warp Mcycles: total %.2f tfull-wait %.2f fast %.2f slow %.2f settle %.2f | "
+            "per MMA warp: total %.2f tempty-wait %.2f full-wait %.2f\n",
+            h[8] / ew / 1e6, h[4] / ew / 1e6, h[5] / ew / 1e6, h[6] / ew / 1e6, h[7] / ew / 1e6, h[11] / mw / 1e6,
+            h[9] / mw / 1e6, h[10] / mw / 1e6);
   }
-  if (split == 1 && cl == 1) return launch_variant<1, 1>(tmA, tmB, a, grid, st);
-  if (split == 1 && cl == 2) return launch_variant<1, 2>(tmA, tmB, a, grid, st);
-  if (split == 1 && cl == 4) return launch_variant<1, 4>(tmA, tmB, a, grid, st);
-  if (split == 2 && cl == 1) return launch_variant<2, 1>(tmA, tmB, a, grid, st);
-  if (split == 2 && cl == 2) return launch_variant<2, 2>(tmA, tmB, a, grid, st);
-  return launch_variant<2, 4>(tmA, tmB, a, grid, st);
+  return rc;
 }
 
 }  // namespace astra

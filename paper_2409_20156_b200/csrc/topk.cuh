@@ -135,6 +135,39 @@ __device__ __forceinline__ void bitonic_sort_desc(uint64_t (&x)[R], int lane) {
   }
 }
 
+// Zero the keys of x[] whose id is one of the query's positives (the mask of
+// anns.py:254-255). Up to 64 positives are held in two registers per lane and
+// broadcast: one parallel load instead of a dependent binary search in global
+// memory per key (which made compaction latency-bound).
+template <int R>
+__device__ __forceinline__ void drop_positives(uint64_t (&x)[R], const int32_t* pos, int64_t npos, int lane) {
+  if (npos <= 0) return;
+  if (npos <= 64) {
+    const int32_t p0 = lane < npos ? pos[lane] : -1;
+    const int32_t p1 = lane + 32 < npos ? pos[lane + 32] : -1;
+    int32_t id[R];
+    bool hit[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      id[r] = x[r] ? key_id(x[r]) : -2;
+      hit[r] = false;
+    }
+    const int n = static_cast<int>(npos);
+    for (int i = 0; i < n; ++i) {
+      const int32_t pv = __shfl_sync(0xffffffffu, i < 32 ? p0 : p1, i & 31);
+#pragma unroll
+      for (int r = 0; r < R; ++r) hit[r] |= id[r] == pv;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (hit[r]) x[r] = 0ull;
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (x[r] && sorted_contains(pos, npos, key_id(x[r]))) x[r] = 0ull;
+  }
+}
+
 // Warp-cooperative compaction of one lane's buffer (P = 32*R): newcomers
 // buf[ns, cnt) lose positives and are sorted; merged with the sorted prefix
 // buf[0, ns) into the best k at buf[0, kept). Returns kept; *kth = k-th key
@@ -147,11 +180,10 @@ __device__ int compact_regs(uint64_t* buf, int ns, int cnt, const int32_t* pos, 
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int e = r * 32 + lane;
-    uint64_t v = ns + e < cnt ? buf[ns + e] : 0ull;
-    if (v && npos && sorted_contains(pos, npos, key_id(v))) v = 0ull;
-    nw[r] = v;
+    nw[r] = ns + e < cnt ? buf[ns + e] : 0ull;
     old[r] = e < ns ? buf[e] : 0ull;
   }
+  drop_positives<R>(nw, pos, npos, lane);
   bitonic_sort_desc<R>(nw, lane);
   // top P of (old u new): max(old[i], new[P-1-i]) is bitonic; clean it
 #pragma unroll
@@ -232,16 +264,18 @@ __device__ __forceinline__ int compact_any(uint64_t* buf, int ns, int cnt, int c
   }
 }
 
-// Compact lane L's buffer (all 32 lanes participate). Newcomers beyond P are
-// merged in further rounds (topk_settle lets up to kTopkSlack extra keys in).
-__device__ __forceinline__ void compact_lane(LaneTopK& t, int L, int cap, int k) {
+struct CompactResult {
+  uint64_t kth;  // new k-th best key (0 if fewer than k valid keys)
+  int kept;      // sorted prefix length after the compaction
+};
+
+// Out-of-line body of compact_lane: the bitonic networks are large, and
+// inlining them at every call site bloats the epilogue loops far past the
+// instruction cache (the fast path must stay a few hundred instructions).
+static __device__ __noinline__ CompactResult compact_lane_impl(uint64_t* b, const int32_t* p, int64_t np, int c, int ns,
+                                                        int cap, int k) {
   const int lane = threadIdx.x & 31;
   const int P = cap / 2;
-  uint64_t* b = reinterpret_cast<uint64_t*>(shfl64(reinterpret_cast<uint64_t>(t.buf), L));
-  const int32_t* p = reinterpret_cast<const int32_t*>(shfl64(reinterpret_cast<uint64_t>(t.pos), L));
-  const int64_t np = static_cast<int64_t>(shfl64(static_cast<uint64_t>(t.npos), L));
-  int c = __shfl_sync(0xffffffffu, t.cnt, L);
-  int ns = __shfl_sync(0xffffffffu, t.nsorted, L);
   uint64_t kth = 0;
   int kept;
   while (true) {
@@ -261,12 +295,25 @@ __device__ __forceinline__ void compact_lane(LaneTopK& t, int L, int cap, int k)
     ns = kept;
     c = kept + rest;
   }
+  return CompactResult{kth, kept};
+}
+
+// Compact lane L's buffer (all 32 lanes participate). Newcomers beyond P are
+// merged in further rounds (topk_settle lets up to kTopkSlack extra keys in).
+__device__ __forceinline__ void compact_lane(LaneTopK& t, int L, int cap, int k) {
+  const int lane = threadIdx.x & 31;
+  uint64_t* b = reinterpret_cast<uint64_t*>(shfl64(reinterpret_cast<uint64_t>(t.buf), L));
+  const int32_t* p = reinterpret_cast<const int32_t*>(shfl64(reinterpret_cast<uint64_t>(t.pos), L));
+  const int64_t np = static_cast<int64_t>(shfl64(static_cast<uint64_t>(t.npos), L));
+  const int c = __shfl_sync(0xffffffffu, t.cnt, L);
+  const int ns = __shfl_sync(0xffffffffu, t.nsorted, L);
+  const CompactResult r = compact_lane_impl(b, p, np, c, ns, cap, k);
   if (lane == L) {
-    t.cnt = t.nsorted = kept;
-    if (kth > t.tau) {
-      t.tau = kth;
-      t.tau_s = key_score(kth);
-      if (t.gtau) atomicMax(reinterpret_cast<unsigned long long*>(t.gtau), static_cast<unsigned long long>(kth));
+    t.cnt = t.nsorted = r.kept;
+    if (r.kth > t.tau) {
+      t.tau = r.kth;
+      t.tau_s = key_score(r.kth);
+      if (t.gtau) atomicMax(reinterpret_cast<unsigned long long*>(t.gtau), static_cast<unsigned long long>(r.kth));
     }
   }
 }

@@ -128,3 +128,51 @@ def test_config_errors(cuda_lib):
         ops.refresh_topk(E, ip, pid, 3, "bf16", labels_bf16=W.to(torch.bfloat16))  # d % 64
     with pytest.raises(ConfigError):
         ops.refresh_topk(E, ip, pid, 0, "fp32", labels_f32=W)
+
+
+def _with_two_pass(flag, fn):
+    import os
+
+    old = os.environ.get("ASTRA_REFRESH_TWO_PASS")
+    os.environ["ASTRA_REFRESH_TWO_PASS"] = flag
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ["ASTRA_REFRESH_TWO_PASS"]
+        else:
+            os.environ["ASTRA_REFRESH_TWO_PASS"] = old
+
+
+@pytest.mark.parametrize("mode,k", [("bf16", 32), ("bf16", 96), ("bf16_rerank", 64)])
+@pytest.mark.parametrize("nq", [700, 2100])
+def test_two_pass_equals_running_topk(cuda_lib, mode, k, nq):
+    """sample -> threshold -> select -> verify must return exactly the keys of
+    the single-pass running top-k (same bf16 scores), positives excluded."""
+    rng = np.random.default_rng(k + nq)
+    L, d = 70_000 + 129, 128  # 274 label tiles (tail inside a tile), 18 sample tiles
+    W = rng.uniform(-1 / np.sqrt(d), 1 / np.sqrt(d), size=(L, d)).astype(np.float32)
+    E = rng.standard_normal((nq, d)).astype(np.float32)
+    positives = [p + 11 for p in random_positives(rng, nq, L, 0, 12)]  # global ids (label_offset 11)
+    run_keys, run_ids, _ = _with_two_pass("0", lambda: _run(E, W, positives, k, mode, offset=11))
+    tp_keys, tp_ids, _ = _with_two_pass("1", lambda: _run(E, W, positives, k, mode, offset=11))
+    np.testing.assert_array_equal(tp_keys, run_keys)
+    np.testing.assert_array_equal(tp_ids, run_ids)
+    for i, p in enumerate(positives):
+        assert not set(tp_ids[i].tolist()) & set(p.tolist())
+
+
+def test_two_pass_fallback_on_adversarial_sample(cuda_lib):
+    """Labels of the sampled tiles score far higher than the rest, so the
+    sample threshold admits fewer than k candidates for most queries: the
+    verification fallback must still give the exact result."""
+    rng = np.random.default_rng(5)
+    L, d, nq, k = 256 * 40, 64, 300, 48
+    W = rng.uniform(-0.1, 0.1, size=(L, d)).astype(np.float32)
+    E = np.abs(rng.standard_normal((nq, d))).astype(np.float32)
+    for t in range(0, L // 256, 16):  # the sampled tiles (stride 16)
+        W[t * 256 : (t + 1) * 256] = np.abs(W[t * 256 : (t + 1) * 256]) + 0.5
+    positives = random_positives(rng, nq, L, 0, 3)
+    run_keys, _, _ = _with_two_pass("0", lambda: _run(E, W, positives, k, "bf16"))
+    tp_keys, _, _ = _with_two_pass("1", lambda: _run(E, W, positives, k, "bf16"))
+    np.testing.assert_array_equal(tp_keys, run_keys)
