@@ -21,10 +21,12 @@
 // case; otherwise a check pass (label_check) runs first.
 #include <limits.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace astra {
 namespace {
@@ -80,6 +82,29 @@ __device__ __forceinline__ float slot_factor(const FwdArgs& a, int b, int s, flo
   const double spn = softplus64(-static_cast<double>(sc));
   *loss_term = static_cast<double>(pos_term) * spn + static_cast<double>(wn) * (spn + static_cast<double>(sc));
   return __fadd_rn(__fmul_rn(pos_term, __fsub_rn(sig, 1.0f)), __fmul_rn(wn, sig));
+}
+
+// slot_factor split in two for the TMA kernel: the factor (needed at once by
+// every lane), and the fp64 loss term, evaluated later lane-parallel for 32
+// slots at a time (one softplus per lane instead of one per slot per lane).
+__device__ __forceinline__ float slot_factor_only(const FwdArgs& a, int b, int s, float sc, float* pos_term_out,
+                                                  float* wn_out) {
+  const int8_t o = a.origin[b * a.origin_stride + s];
+  const float yf = static_cast<float>(a.y[static_cast<size_t>(b) * a.S + s]);
+  const float w = a.weights[b * a.weights_stride + s];
+  const bool pos_slot = o == ASTRA_ORIGIN_POS;
+  const float pos_term = pos_slot ? yf : 0.0f;
+  const float neg_alive = pos_slot ? 0.0f : __fsub_rn(1.0f, yf);
+  const float sig = expit_f32(sc);
+  const float wn = __fmul_rn(w, neg_alive);
+  *pos_term_out = pos_term;
+  *wn_out = wn;
+  return __fadd_rn(__fmul_rn(pos_term, __fsub_rn(sig, 1.0f)), __fmul_rn(wn, sig));
+}
+
+__device__ __forceinline__ double slot_loss(float sc, float pos_term, float wn) {
+  const double spn = softplus64(-static_cast<double>(sc));
+  return static_cast<double>(pos_term) * spn + static_cast<double>(wn) * (spn + static_cast<double>(sc));
 }
 
 template <bool BF16>
@@ -206,6 +231,187 @@ __global__ void __launch_bounds__(kFwdThreads, 1) slot_forward_vec(FwdArgs a) {
   if (lane == 0) s_emax[warp] = emax;
   __syncthreads();
   forward_tail(a, b, red, lsum, fabs_sum, s_emax[0]);
+}
+
+// TMA-fed forward (the default for d % 128 == 0): CTA per batch row; one
+// producer lane streams the row's owned W rows into a shared-memory ring with
+// 1-D bulk copies (cp.async.bulk + mbarrier transaction counts), so each CTA
+// keeps RING rows (48 KB) in flight with no register cost; four consumer warps
+// take ring slots round-robin (warp w: owned slots w, w+4, ...), compute the
+// dot with the embedding held in registers, the BCE/factor algebra, and
+// accumulate f * w_row. The per-warp partials are reduced in warp order
+// (deterministic). Replaces the register-pipelined gather (2-3x the HBM rate).
+constexpr int kTmaConsumers = 4;
+constexpr int kTmaThreads = 32 * (kTmaConsumers + 1);
+
+template <bool BF16>
+constexpr int tma_ring() { return BF16 ? 32 : 16; }
+
+template <int NV, bool BF16>
+constexpr size_t tma_fwd_smem(int S) {
+  return static_cast<size_t>(tma_ring<BF16>()) * NV * 128 * (BF16 ? 2 : 4) + 2 * 8 * tma_ring<BF16>() +
+         static_cast<size_t>(S) * 4 + 64;
+}
+
+template <int NV, bool BF16>
+__global__ void __launch_bounds__(kTmaThreads, 3) slot_forward_tma(FwdArgs a) {
+  constexpr int d = NV * 128;
+  constexpr int RING = tma_ring<BF16>();
+  constexpr uint32_t ROWB = d * (BF16 ? 2 : 4);
+  extern __shared__ __align__(128) unsigned char fsm[];
+  unsigned char* ring = fsm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(fsm + RING * ROWB);
+  uint64_t* empty = full + RING;
+  int32_t* own = reinterpret_cast<int32_t*>(empty + RING);
+  __shared__ int s_nown;
+  __shared__ double s_loss[kTmaConsumers], s_fabs[kTmaConsumers];
+  __shared__ float s_emax[kTmaConsumers];
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t* row_ids = a.ids + static_cast<size_t>(b) * a.S;
+  if (warp == 0) {
+    // owned slots of this row, in slot order (label-sharded W: others are skipped)
+    int n = 0;
+    for (int s0 = 0; s0 < a.S; s0 += 32) {
+      const int sl = s0 + lane;
+      bool o = false;
+      if (sl < a.S) {
+        const int64_t loc = static_cast<int64_t>(row_ids[sl]) - a.off;
+        o = loc >= 0 && loc < a.Lloc;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, o);
+      if (o) own[n + __popc(m & ((1u << lane) - 1u))] = sl;
+      n += __popc(m);
+    }
+    if (lane == 0) {
+      s_nown = n;
+      for (int r = 0; r < RING; ++r) {
+        mbar_init(&full[r], 1);
+        mbar_init(&empty[r], 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+  __syncthreads();
+  const int n_own = s_nown;
+  if (warp == kTmaConsumers) {
+    // ---------------- producer
+    if (lane == 0) {
+      const unsigned char* Wb = static_cast<const unsigned char*>(a.W);
+      for (int i = 0; i < n_own; ++i) {
+        const int r = i % RING;
+        mbar_wait(&empty[r], ((i / RING) & 1) ^ 1);
+        mbar_expect_tx(&full[r], ROWB);
+        const int64_t loc = static_cast<int64_t>(row_ids[own[i]]) - a.off;
+        bulk_g2s(ring + r * ROWB, Wb + static_cast<size_t>(loc) * ROWB, ROWB, &full[r]);
+      }
+    }
+  } else {
+    // ---------------- consumers
+    float4 e[NV], g[NV];
+    float emax = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      e[i] = *reinterpret_cast<const float4*>(a.emb + static_cast<size_t>(b) * d + i * 128 + lane * 4);
+      g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      emax = fmaxf(emax, fmaxf(fmaxf(fabsf(e[i].x), fabsf(e[i].y)), fmaxf(fabsf(e[i].z), fabsf(e[i].w))));
+      if (!(isfinite(e[i].x) && isfinite(e[i].y) && isfinite(e[i].z) && isfinite(e[i].w))) emax = INFINITY;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    double lsum = 0.0, fabs_sum = 0.0;
+    float pend_sc = 0.0f, pend_pt = 0.0f, pend_wn = 0.0f;  // lane c holds the c-th pending loss term
+    int c_pend = 0;
+    for (int i = warp; i < n_own; i += kTmaConsumers) {
+      const int r = i % RING;
+      const int sl = own[i];
+      const float fin = a.factors_in ? a.factors_in[static_cast<size_t>(b) * a.S + sl] : 0.0f;
+      mbar_wait(&full[r], (i / RING) & 1);
+      float4 w[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        if constexpr (BF16) {
+          const uint2 u = *reinterpret_cast<const uint2*>(ring + r * ROWB + (j * 128 + lane * 4) * 2);
+          w[j] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                             __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+        } else {
+          w[j] = *reinterpret_cast<const float4*>(ring + r * ROWB + (j * 128 + lane * 4) * 4);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[r]);  // the row is in registers: release the slot
+      float f;
+      if (a.factors_in) {
+        f = fin;
+      } else {
+        float acc = 0.0f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          acc = fmaf(w[j].x, e[j].x, acc);
+          acc = fmaf(w[j].y, e[j].y, acc);
+          acc = fmaf(w[j].z, e[j].z, acc);
+          acc = fmaf(w[j].w, e[j].w, acc);
+        }
+        acc = warp_sum(acc);
+        float pt, wn;
+        f = slot_factor_only(a, b, sl, acc, &pt, &wn);
+        if (lane == c_pend) {
+          pend_sc = acc;
+          pend_pt = pt;
+          pend_wn = wn;
+        }
+        if (++c_pend == 32) {
+          lsum += slot_loss(pend_sc, pend_pt, pend_wn);
+          c_pend = 0;
+        }
+      }
+      if (lane == 0) {
+        fabs_sum += static_cast<double>(fabsf(f));
+        if (a.factors) a.factors[static_cast<size_t>(b) * a.S + sl] = f;
+      }
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        g[j].x = fmaf(f, w[j].x, g[j].x);
+        g[j].y = fmaf(f, w[j].y, g[j].y);
+        g[j].z = fmaf(f, w[j].z, g[j].z);
+        g[j].w = fmaf(f, w[j].w, g[j].w);
+      }
+    }
+    if (lane < c_pend) lsum += slot_loss(pend_sc, pend_pt, pend_wn);
+    lsum = warp_sum(lsum);
+    fabs_sum = warp_sum(fabs_sum);
+    if (lane == 0) {
+      s_loss[warp] = lsum;
+      s_fabs[warp] = fabs_sum;
+      s_emax[warp] = emax;
+    }
+    __syncthreads();  // (1) every ring row consumed: the ring is reused for the partials
+    float* red = reinterpret_cast<float*>(ring);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) *reinterpret_cast<float4*>(red + warp * d + j * 128 + lane * 4) = g[j];
+  }
+  if (warp == kTmaConsumers) __syncthreads();  // (1), producer side (bar.sync counts threads, not call sites)
+  __syncthreads();                             // (2) partials written
+  const float* red = reinterpret_cast<const float*>(ring);
+  bool bad = false;
+  for (int k = threadIdx.x; k < d; k += kTmaThreads) {
+    float gk = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kTmaConsumers; ++w) gk += red[w * d + k];
+    if (a.keep) gk = __fmul_rn(gk, a.keep[static_cast<size_t>(b) * d + k]);
+    a.grad_emb[static_cast<size_t>(b) * d + k] = gk;
+    bad |= !isfinite(gk);
+  }
+  if (bad) a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] = 1;
+  if (threadIdx.x == 0) {
+    double l = 0.0, fa = 0.0;
+    for (int w = 0; w < kTmaConsumers; ++w) {
+      l += s_loss[w];
+      fa += s_fabs[w];
+    }
+    a.loss_rows[b] = l;
+    a.bound_rows[b] = fa * static_cast<double>(s_emax[0]);
+  }
 }
 
 // Generic forward for any d: emb and the per-warp partials live in shared memory.
@@ -667,7 +873,18 @@ __global__ void apply_rows_kernel(void* W, int d, const int64_t* ids, const floa
 
 template <int NV, bool BF16>
 void launch_forward_vec(const FwdArgs& a, cudaStream_t st) {
-  slot_forward_vec<NV, BF16><<<a.B, kFwdThreads, 0, st>>>(a);
+  static const bool legacy = getenv("ASTRA_STEP_LEGACY_FWD") != nullptr;  // register-pipelined gather
+  const size_t smem = tma_fwd_smem<NV, BF16>(a.S);
+  if (!legacy && smem <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(slot_forward_tma<NV, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    slot_forward_tma<NV, BF16><<<a.B, kTmaThreads, smem, st>>>(a);
+  } else {
+    slot_forward_vec<NV, BF16><<<a.B, kFwdThreads, 0, st>>>(a);
+  }
 }
 
 template <bool BF16, bool ADAM>

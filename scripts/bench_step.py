@@ -1,0 +1,49 @@
+"""Step microbenchmark at the bench shape (L=1.3M, d=768, B=1024, S=584): ms per
+minibatch of Philox slates + fused loss/update, and its HBM roofline."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2409_20156_b200.engine import ClassifierEngine  # noqa: E402
+
+L, d, B, k_p, k_h, k_r = 1_305_265, 768, 1024, 8, 64, 512
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+eng = ClassifierEngine(L, d, k_p=k_p, k_h=k_h, k_r=k_r, seed=0)
+g = torch.Generator(device="cuda")
+g.manual_seed(1)
+mbs = []
+for t in range(4):
+    rows = torch.arange(t * B, (t + 1) * B, device="cuda", dtype=torch.int64)
+    pos = torch.randint(0, L, (B, 38), device="cuda", generator=g).sort(1).values.to(torch.int32)
+    ip = torch.arange(0, B * 38 + 1, 38, device="cuda", dtype=torch.int64)
+    hard = torch.randint(0, L, (B, k_h), device="cuda", generator=g).to(torch.int32)
+    emb = torch.randn((B, d), device="cuda", generator=g)
+    mbs.append((rows, ip, pos.reshape(-1).contiguous(), hard, emb))
+
+
+def one(i):
+    rows, ip, pid, hard, emb = mbs[i % 4]
+    sl = eng.sample(rows, ip, pid, hard, epoch=1, step=i)
+    return eng.step(emb, sl, 0.05, 1e-4), sl
+
+
+for i in range(3):
+    one(i)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+import time  # noqa: E402
+
+e0.record()
+h0 = time.perf_counter()
+for i in range(n):
+    _, sl = one(i)
+h1 = time.perf_counter()
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / n
+print(f"host {1e3 * (h1 - h0) / n:.3f} ms/minibatch (python + launches, no sync)")
+U = int(torch.unique(sl[0]).numel())
+byts = U * d * 8 + 2 * B * d * 4 + B * (k_p + k_h + k_r) * 5
+print(f"step {ms:.3f} ms/minibatch  U={U}  {byts / ms / 1e6:.0f} GB/s algorithmic ({byts / 1e9:.2f} GB)")

@@ -10,8 +10,11 @@ def launches(path, top=15):
     hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     h = rows[hdr]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = defaultdict(lambda: [0, 0.0])
     for r in rows[hdr + 1:]:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue
         try:
             v = float(r[vi].replace(",", ""))
         except (ValueError, IndexError):
