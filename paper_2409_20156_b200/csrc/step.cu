@@ -848,6 +848,129 @@ __global__ void __launch_bounds__(kUpdThreads) label_update_vec(UpdArgs a) {
   }
 }
 
+// TMA-fed SGD update (the default for d % 128 == 0): each CTA owns a
+// contiguous chunk of the sorted unique-label list; one producer lane streams
+// the chunk's W rows into a shared-memory ring with bulk copies while four
+// consumer warps (warp w: the chunk's labels w, w+4, ...) sum the label's
+// gradient from the L2-resident embeddings (same ascending-slot order and
+// roundings as label_update_vec), then take the row from the ring, apply the
+// update and store it. W is read and written once per touched row.
+template <int NV, bool BF16>
+__global__ void __launch_bounds__(kTmaThreads, 3) label_update_tma(UpdArgs a) {
+  constexpr int d = NV * 128;
+  constexpr int RING = tma_ring<BF16>();
+  constexpr uint32_t ROWB = d * (BF16 ? 2 : 4);
+  extern __shared__ __align__(128) unsigned char usm[];
+  unsigned char* ring = usm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(usm + RING * ROWB);
+  uint64_t* empty = full + RING;
+  if (a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] || a.status[ASTRA_STATUS_NONFINITE_GRAD]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t U = *a.U;
+  const uint32_t chunk = (U + gridDim.x - 1) / gridDim.x;
+  const uint32_t u0 = min(U, blockIdx.x * chunk), u1 = min(U, u0 + chunk);
+  const int n_mine = static_cast<int>(u1 - u0);
+  if (n_mine == 0) return;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < RING; ++r) {
+      mbar_init(&full[r], 1);
+      mbar_init(&empty[r], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kTmaConsumers) {
+    if (lane == 0) {
+      const unsigned char* Wb = static_cast<const unsigned char*>(a.W);
+      for (int i = 0; i < n_mine; ++i) {
+        const int r = i % RING;
+        mbar_wait(&empty[r], ((i / RING) & 1) ^ 1);
+        mbar_expect_tx(&full[r], ROWB);
+        bulk_g2s(ring + r * ROWB, Wb + static_cast<size_t>(a.uniq[u0 + i]) * ROWB, ROWB, &full[r]);
+      }
+    }
+    return;
+  }
+  for (int i = warp; i < n_mine; i += kTmaConsumers) {
+    const int r = i % RING;
+    const int32_t l = a.uniq[u0 + i];
+    const uint32_t start = a.offsets[l], n = a.counts[l];
+    const int32_t reg = sort_segment(a, start, n, lane);
+    float4 g[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) g[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t j = 0;
+    for (; j + 2 <= n; j += 2) {  // two occurrences' loads in flight, summed in order
+      const int32_t s0 = seg_slot(a, start, n, reg, j), s1 = seg_slot(a, start, n, reg, j + 1);
+      const float f0 = a.factors[s0], f1 = a.factors[s1];
+      const float* e0 = a.emb + static_cast<size_t>(s0 / a.S) * d + lane * 4;
+      const float* e1 = a.emb + static_cast<size_t>(s1 / a.S) * d + lane * 4;
+      float4 x0[NV], x1[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        x0[q] = *reinterpret_cast<const float4*>(e0 + q * 128);
+        x1[q] = *reinterpret_cast<const float4*>(e1 + q * 128);
+      }
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        g[q].x = __fadd_rn(g[q].x, __fmul_rn(f0, x0[q].x));
+        g[q].y = __fadd_rn(g[q].y, __fmul_rn(f0, x0[q].y));
+        g[q].z = __fadd_rn(g[q].z, __fmul_rn(f0, x0[q].z));
+        g[q].w = __fadd_rn(g[q].w, __fmul_rn(f0, x0[q].w));
+        g[q].x = __fadd_rn(g[q].x, __fmul_rn(f1, x1[q].x));
+        g[q].y = __fadd_rn(g[q].y, __fmul_rn(f1, x1[q].y));
+        g[q].z = __fadd_rn(g[q].z, __fmul_rn(f1, x1[q].z));
+        g[q].w = __fadd_rn(g[q].w, __fmul_rn(f1, x1[q].w));
+      }
+    }
+    if (j < n) {
+      const int32_t s0 = seg_slot(a, start, n, reg, j);
+      const float f0 = a.factors[s0];
+      const float* e0 = a.emb + static_cast<size_t>(s0 / a.S) * d + lane * 4;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const float4 x0 = *reinterpret_cast<const float4*>(e0 + q * 128);
+        g[q].x = __fadd_rn(g[q].x, __fmul_rn(f0, x0.x));
+        g[q].y = __fadd_rn(g[q].y, __fmul_rn(f0, x0.y));
+        g[q].z = __fadd_rn(g[q].z, __fmul_rn(f0, x0.z));
+        g[q].w = __fadd_rn(g[q].w, __fmul_rn(f0, x0.w));
+      }
+    }
+    mbar_wait(&full[r], (i / RING) & 1);
+    float4 p[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      if constexpr (BF16) {
+        const uint2 u = *reinterpret_cast<const uint2*>(ring + r * ROWB + (q * 128 + lane * 4) * 2);
+        p[q] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                           __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+      } else {
+        p[q] = *reinterpret_cast<const float4*>(ring + r * ROWB + (q * 128 + lane * 4) * 4);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[r]);
+    const size_t row = static_cast<size_t>(l) * d;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      float4 np;
+      np.x = upd_elem<false>(a, p[q].x, g[q].x, nullptr, nullptr);
+      np.y = upd_elem<false>(a, p[q].y, g[q].y, nullptr, nullptr);
+      np.z = upd_elem<false>(a, p[q].z, g[q].z, nullptr, nullptr);
+      np.w = upd_elem<false>(a, p[q].w, g[q].w, nullptr, nullptr);
+      const size_t el = row + q * 128 + lane * 4;
+      if constexpr (BF16) {
+        uint2 o;
+        o.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
+        o.y = static_cast<uint32_t>(f32_to_bf16_bits(np.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.w)) << 16);
+        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(a.W) + el) = o;
+      } else {
+        *reinterpret_cast<float4*>(static_cast<float*>(a.W) + el) = np;
+      }
+    }
+  }
+}
+
 // apply_classifier_updates_arrays: explicit (ids, grads) form.
 __global__ void apply_check_kernel(const float* grads, int64_t n, int32_t* status) {
   bool bad = false;
@@ -887,11 +1010,35 @@ void launch_forward_vec(const FwdArgs& a, cudaStream_t st) {
   }
 }
 
+template <int NV, bool BF16>
+void launch_upd_tma(const UpdArgs& a, int grid, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(label_update_tma<NV, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  label_update_tma<NV, BF16><<<grid, kTmaThreads, smem, st>>>(a);
+}
+
 template <bool BF16, bool ADAM>
 int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
   const int nv = a.d % 128 == 0 ? a.d / 128 : 0;
   label_update_kernel<BF16, ADAM, true><<<max_ctas, kUpdThreads, 0, st>>>(a);
   ASTRA_LAUNCHED("label_check");
+  static const bool legacy = getenv("ASTRA_STEP_LEGACY_UPD") != nullptr;
+  if (!ADAM && !legacy && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
+    const int grid = 3 * num_sms();
+    const size_t smem = static_cast<size_t>(tma_ring<BF16>()) * a.d * (BF16 ? 2 : 4) + 2 * 8 * tma_ring<BF16>();
+    switch (nv) {
+      case 1: launch_upd_tma<1, BF16>(a, grid, smem, st); break;
+      case 2: launch_upd_tma<2, BF16>(a, grid, smem, st); break;
+      case 4: launch_upd_tma<4, BF16>(a, grid, smem, st); break;
+      case 6: launch_upd_tma<6, BF16>(a, grid, smem, st); break;
+      case 8: launch_upd_tma<8, BF16>(a, grid, smem, st); break;
+    }
+    ASTRA_LAUNCHED("label_update_tma");
+    return ASTRA_OK;
+  }
   switch (nv) {
     case 1: label_update_vec<1, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
     case 2: label_update_vec<2, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
