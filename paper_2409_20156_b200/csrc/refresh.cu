@@ -16,10 +16,12 @@
 //               with the same sequential fmaf chain and re-ranked: equal to
 //               FP32_EXACT whenever the exact top-k lies inside the top-k'.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
 #include "common.cuh"
+#include "ptx.cuh"
 #include "refresh_tc.cuh"
 #include "topk.cuh"
 
@@ -315,6 +317,122 @@ __global__ void __launch_bounds__(kRrWarps * 32) rerank_kernel(const float* Q, c
     if (out_ids) out_ids[q * k + j] = key ? key_id(key) : -1;
     if (out_scores) out_scores[q * k + j] = key ? key_score(key) : -INFINITY;
   }
+}
+
+// TMA-fed re-rank (kc <= 128): CTA per query, a producer warp whose lanes
+// bulk-copy their candidate's fp32 row, ch floats at a time, into a 2-stage
+// ring (32 rows x ch floats, pitch 4 words mod 32: conflict-free LDS.128), and
+// a consumer warp whose lane t runs candidate t's sequential fmaf chain over
+// t = 0..d-1 (the FP32_EXACT order) across the chunks. Keys are sorted in
+// registers (warp bitonic) and the best k written. 3 CTAs per SM keep ~200 KB
+// of rows in flight per SM; the old kernel stalled on each 64-float chunk.
+constexpr int kRtRing = 2;
+
+__host__ __device__ inline int rerank_chunk(int d) { return d % 256 == 0 ? 256 : 64; }
+
+template <int R>
+__global__ void __launch_bounds__(64) rerank_tma_kernel(const float* Q, const float* W, int d, int64_t off,
+                                                        const uint64_t* cand, int kc, int k, uint64_t* out_keys,
+                                                        int32_t* out_ids, float* out_scores) {
+  extern __shared__ __align__(128) unsigned char rsm[];
+  const int ch = rerank_chunk(d);
+  const int pitch = ch * 4 + 16;
+  const int stage_bytes = 32 * pitch;
+  unsigned char* ring = rsm;
+  float* qs = reinterpret_cast<float*>(rsm + kRtRing * stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(qs + d);
+  uint64_t* empty = full + kRtRing;
+  const int64_t q = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = d / ch;
+  const int n_units = (kc + 31) / 32;
+  for (int t = threadIdx.x; t < d; t += 64) qs[t] = Q[q * d + t];
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < kRtRing; ++r) {
+      mbar_init(&full[r], 1);
+      mbar_init(&empty[r], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // ---------------- producer: lane t copies candidate u*32+t's row chunks
+    for (int u = 0; u < n_units; ++u) {
+      const int c = u * 32 + lane;
+      const uint64_t key = c < kc ? cand[q * kc + c] : 0ull;
+      const int32_t gid = key ? key_id(key) : -1;
+      const uint32_t nbytes = __popc(__ballot_sync(0xffffffffu, gid >= 0)) * ch * 4;
+      for (int h = 0; h < nch; ++h) {
+        const int i = u * nch + h, st = i % kRtRing;
+        mbar_wait(&empty[st], ((i / kRtRing) & 1) ^ 1);
+        if (lane == 0) mbar_expect_tx(&full[st], nbytes);
+        __syncwarp();
+        if (gid >= 0)
+          bulk_g2s(ring + st * stage_bytes + lane * pitch, W + static_cast<size_t>(gid - off) * d + h * ch, ch * 4,
+                   &full[st]);
+      }
+    }
+    return;
+  }
+  // ---------------- consumer
+  uint64_t keys[R];
+#pragma unroll
+  for (int u = 0; u < R; ++u) keys[u] = 0ull;
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    if (u < n_units) {
+      const int c = u * 32 + lane;
+      const uint64_t key = c < kc ? cand[q * kc + c] : 0ull;
+      const int32_t gid = key ? key_id(key) : -1;
+      float s = 0.0f;
+      for (int h = 0; h < nch; ++h) {
+        const int i = u * nch + h, st = i % kRtRing;
+        mbar_wait(&full[st], (i / kRtRing) & 1);
+        const float* row = reinterpret_cast<const float*>(ring + st * stage_bytes + lane * pitch);
+        const float* qh = qs + h * ch;
+#pragma unroll 8
+        for (int t = 0; t < ch; t += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(row + t);
+          const float4 x = *reinterpret_cast<const float4*>(qh + t);
+          s = fmaf(x.x, v.x, s);
+          s = fmaf(x.y, v.y, s);
+          s = fmaf(x.z, v.z, s);
+          s = fmaf(x.w, v.w, s);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+      keys[u] = gid >= 0 ? make_key(s, static_cast<uint32_t>(gid)) : 0ull;
+    }
+  }
+  bitonic_sort_desc<R>(keys, lane);
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const int e = u * 32 + lane;
+    if (e < k) {
+      const uint64_t key = keys[u];
+      const size_t o = static_cast<size_t>(q) * k + e;
+      if (out_keys) out_keys[o] = key;
+      if (out_ids) out_ids[o] = key ? key_id(key) : -1;
+      if (out_scores) out_scores[o] = key ? key_score(key) : -INFINITY;
+    }
+  }
+}
+
+template <int R>
+int launch_rerank_tma(const float* qf, const float* wf, int d, int64_t off, const uint64_t* cand, int64_t nq, int kc,
+                      int k, uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st) {
+  const int ch = rerank_chunk(d);
+  const size_t smem = static_cast<size_t>(kRtRing) * 32 * (ch * 4 + 16) + sizeof(float) * d + 16 * kRtRing;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rerank_tma_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  rerank_tma_kernel<R><<<static_cast<unsigned>(nq), 64, smem, st>>>(qf, wf, d, off, cand, kc, k, out_keys, out_ids,
+                                                                    out_scores);
+  ASTRA_LAUNCHED("rerank_tma");
+  return ASTRA_OK;
 }
 
 __global__ void f32_to_bf16_kernel(const float* src, uint16_t* dst, int64_t n) {
@@ -752,6 +870,13 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
       ASTRA_TRY(launch_refresh_tc(p, st));
       ASTRA_TRY(topk_merge(w.part_keys, nq, n_parts, kk, kk, o_keys, o_ids, o_scores, w.merge_bufs, st));
     }
+  }
+  static const bool legacy_rr = getenv("ASTRA_RERANK_LEGACY") != nullptr;
+  if (rerank && !legacy_rr && kk <= 128 && d % 64 == 0 &&
+      (reinterpret_cast<uintptr_t>(wf) & 15) == 0) {
+    if (kk <= 32) return launch_rerank_tma<1>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+    if (kk <= 64) return launch_rerank_tma<2>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+    return launch_rerank_tma<4>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
   }
   if (rerank) {
     int Pn = 1;
