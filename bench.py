@@ -103,6 +103,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of each timed
+    kernel, from the committed `ncu --set full` summary (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(p)).items() if not k.startswith("_")}
+    except (OSError, ValueError, KeyError):
+        return {}
+
+
 # ------------------------------------------------------------------ data
 def make_batches(rng, n_batches, B, L, lpp, N, slot, n_slots):
     """Synthetic minibatches: global row ids, positives (labels_per_point
@@ -197,6 +207,9 @@ def run_ours(args):
     eng.comm.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
+    for name in ("refresh_gemm", "slot_forward", "label_update"):
+        _lib.kernel_timing(name)  # drop warm-up records
+    _lib.kernel_timing_enable(True)
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
@@ -208,6 +221,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     clk = clocks.stop()
     launches = _lib.launch_count() - launches0
+    _lib.kernel_timing_enable(False)
+    kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "slot_forward", "label_update")}
     ops.raise_for_step_status(status)
     ms_t = torch.tensor([t_start.elapsed_time(t_end)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -223,11 +238,15 @@ def run_ours(args):
             ph["step"] += e[2 + 2 * i].elapsed_time(e[3 + 2 * i])
     value = R * world * K / (ms_total / 1e3)
 
-    # dominant kernel: the refresh (tcgen05 GEMM + fused top-k [+ merge/re-rank])
+    # dominant kernel: the refresh GEMM pass (tcgen05 bf16 GEMM of the queries
+    # against every label with the fused candidate epilogue), timed live with
+    # CUDA events on its stream around each launch (astra_kernel_timing)
     q_per_refresh = R * world  # every shard scores all gathered queries
     flops = 2.0 * L_loc * d * q_per_refresh
+    gemm_ms, gemm_n = kt["refresh_gemm"]
+    t_gemm = gemm_ms / max(gemm_n, 1) / 1e3
+    achieved_tf = flops / t_gemm / 1e12
     t_ref = ph["refresh"] / K / 1e3
-    achieved_tf = flops / t_ref / 1e12
     # step roofline: BASELINE.md bytes formula (U unique rows, fp32 SGD: read+write)
     U = [int(torch.unique(ids[(ids >= eng.lo) & (ids < eng.hi)]).numel()) for ids in ids_keep]
     U_mean = sum(U) / len(U)
@@ -235,7 +254,12 @@ def run_ours(args):
     t_step = ph["step"] / (K * M) / 1e3
     t_samp = ph["sample"] / (K * M) / 1e3
     step_gbs = step_bytes / t_step / 1e9
-
+    # per-kernel HBM rates of the step (algorithmic bytes per launch / live event time)
+    fwd_ms, fwd_n = kt["slot_forward"]
+    upd_ms, upd_n = kt["label_update"]
+    fwd_bytes = B * world * S * d * 4 + B * world * d * 4 * 2  # gathered rows + emb + grad_emb
+    upd_bytes = U_mean * d * 4 * 2  # each touched row read + written once (emb rows come from L2)
+    traffic = _ncu_traffic()
     # end-to-end: the public API with HOST buffers (pinned), copies inside the timed region
     pinned = []
     for t in range(n_steps):
@@ -288,15 +312,26 @@ def run_ours(args):
         "refresh_mips_qps": round(q_per_refresh / t_ref, 1),
         "step_only_samples_per_s": round(B * world / (t_step + t_samp), 1),
         "composite_tau_r5_samples_per_s": round(R * world / (M * (t_step + t_samp) + t_ref / 5), 1),
-        "roofline": {"bound": "tensor", "kernel": "refresh (tcgen05 GEMM + fused top-k + merge + re-rank)",
+        "roofline": {"bound": "tensor", "kernel": "refresh_tc_kernel threshold pass (tcgen05 bf16 GEMM + fused candidate epilogue)",
                      "achieved": round(achieved_tf, 2), "peak": tf_sus, "unit": "TFLOP/s",
-                     "frac": round(achieved_tf / tf_sus, 4), "traffic": None,
+                     "frac": round(achieved_tf / tf_sus, 4), "traffic": traffic.get("refresh_gemm"),
                      "algorithmic": f"2*L_shard*d*Q = {flops:.3e} flop per launch (Q={q_per_refresh})",
-                     "peak_kind": f"{peak_kind} sustained"},
+                     "launch_ms": round(t_gemm * 1e3, 4), "launches": gemm_n,
+                     "share_of_refresh": round(t_gemm / t_ref, 4),
+                     "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)"},
         "roofline_step": {"bound": "hbm", "kernel": "minibatch step (gather/loss/grad + counting sort + fused SGD row update)",
                           "achieved": round(step_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(step_gbs / hbm, 4),
                           "algorithmic": f"U*d*8 + 2*B*d*4 + B*S*5 = {step_bytes:.3e} B (U={U_mean:.0f})",
-                          "peak_kind": peak_kind},
+                          "peak_kind": peak_kind,
+                          "kernels": {
+                              "slot_forward": {"launch_ms": round(fwd_ms / max(fwd_n, 1), 4),
+                                               "achieved_gbs": round(fwd_bytes / (fwd_ms / max(fwd_n, 1) / 1e3) / 1e9, 1),
+                                               "algorithmic_bytes": int(fwd_bytes),
+                                               "traffic": traffic.get("slot_forward")},
+                              "label_update": {"launch_ms": round(upd_ms / max(upd_n, 1), 4),
+                                               "achieved_gbs": round(upd_bytes / (upd_ms / max(upd_n, 1) / 1e3) / 1e9, 1),
+                                               "algorithmic_bytes": int(upd_bytes),
+                                               "traffic": traffic.get("label_update")}}},
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
         "clocks": clk,

@@ -72,6 +72,16 @@ int astra_device_info(int* sm_count, int* cc_major, int* cc_minor);
 /* Number of kernels this library launched on the calling process (all threads). */
 uint64_t astra_launch_count(void);
 
+/* Live kernel timing (bench.py's roofline). While enabled, the library records
+ * a CUDA event pair on the launching stream around each launch of the named
+ * kernels: "refresh_gemm" (the fused tcgen05 GEMM + selection pass that scores
+ * every label: the threshold pass, or the single running-top-k pass),
+ * "slot_forward" and "label_update" (the step). astra_kernel_timing syncs the
+ * pairs recorded under `name`, returns their summed milliseconds and count,
+ * and clears them. Not a reference interface (measurement only). */
+void astra_kernel_timing_enable(int on);
+int astra_kernel_timing(const char* name, double* total_ms, int64_t* count);
+
 /* fp32 -> bf16 (round-to-nearest-even), n elements. Used for W/query snapshots. */
 int astra_f32_to_bf16(const float* src, uint16_t* dst, int64_t n, void* stream);
 

@@ -25,6 +25,8 @@ _SIGS = {
     "astra_last_error": ([], C.c_char_p),
     "astra_device_info": ([p, p, p], i32),
     "astra_launch_count": ([], u64),
+    "astra_kernel_timing_enable": ([i32], None),
+    "astra_kernel_timing": ([C.c_char_p, p, p], i32),
     "astra_f32_to_bf16": ([p, p, i64, p], i32),
     "astra_refresh_workspace_size": ([i64, i64, i32, i32, i32], sz),
     "astra_refresh_topk": ([p, p, i64, i32, p, p, i64, i64, p, p, i32, i32, p, p, p, p, sz, p], i32),
@@ -66,3 +68,14 @@ def check(rc: int) -> None:
 
 def launch_count() -> int:
     return int(load().astra_launch_count())
+
+
+def kernel_timing_enable(on: bool = True) -> None:
+    load().astra_kernel_timing_enable(1 if on else 0)
+
+
+def kernel_timing(name: str):
+    """(total_ms, launches) of the named kernel since the last read (syncs its events)."""
+    ms, n = C.c_double(0.0), C.c_int64(0)
+    check(load().astra_kernel_timing(name.encode(), C.byref(ms), C.byref(n)))
+    return ms.value, n.value

@@ -3,6 +3,11 @@
 #include <stdio.h>
 
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "topk.cuh"
@@ -26,6 +31,17 @@ int check_cuda(cudaError_t e, const char* what) {
 }
 
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static std::atomic<bool> g_kt_on{false};
+static std::mutex g_kt_mu;
+static std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> g_kt;
+
+bool kernel_timing_on() { return g_kt_on.load(std::memory_order_relaxed); }
+
+void kernel_timing_push(const char* name, cudaEvent_t e0, cudaEvent_t e1) {
+  std::lock_guard<std::mutex> lk(g_kt_mu);
+  g_kt[name].emplace_back(e0, e1);
+}
 
 int num_sms() {
   static thread_local int dev_cached = -1, sms_cached = 0;
@@ -66,6 +82,29 @@ extern "C" {
 const char* astra_version(void) { return "astra-b200 0.1 (sm_100a)"; }
 const char* astra_last_error(void) { return g_err; }
 uint64_t astra_launch_count(void) { return g_launches.load(); }
+
+void astra_kernel_timing_enable(int on) { g_kt_on.store(on != 0); }
+
+int astra_kernel_timing(const char* name, double* total_ms, int64_t* count) {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  {
+    std::lock_guard<std::mutex> lk(g_kt_mu);
+    auto it = g_kt.find(name);
+    if (it != g_kt.end()) ev.swap(it->second);
+  }
+  double tot = 0.0;
+  for (auto& p : ev) {
+    ASTRA_TRY(check_cuda(cudaEventSynchronize(p.second), "kernel timing sync"));
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, p.first, p.second);
+    tot += ms;
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  if (total_ms) *total_ms = tot;
+  if (count) *count = static_cast<int64_t>(ev.size());
+  return ASTRA_OK;
+}
 
 int astra_device_info(int* sm_count, int* cc_major, int* cc_minor) {
   int dev = 0;

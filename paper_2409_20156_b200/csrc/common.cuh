@@ -21,6 +21,30 @@ int check_cuda(cudaError_t e, const char* what);
 void count_launch(uint64_t n = 1);
 int num_sms();
 
+// Live kernel timing (astra_kernel_timing_enable / astra_kernel_timing): when
+// enabled, a KernelTimer scope records CUDA events on the launching stream
+// around the launches it encloses and files the pair under `name`.
+bool kernel_timing_on();
+void kernel_timing_push(const char* name, cudaEvent_t e0, cudaEvent_t e1);
+struct KernelTimer {
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  KernelTimer(const char* n, cudaStream_t s) : name(n), st(s) {
+    if (kernel_timing_on()) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, st);
+    }
+  }
+  ~KernelTimer() {
+    if (e0) {
+      cudaEventRecord(e1, st);
+      kernel_timing_push(name, e0, e1);
+    }
+  }
+};
+
 #define ASTRA_TRY(expr)            \
   do {                             \
     int _rc = (expr);              \

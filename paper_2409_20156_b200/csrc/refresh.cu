@@ -16,6 +16,7 @@
 //               with the same sequential fmaf chain and re-ranked: equal to
 //               FP32_EXACT whenever the exact top-k lies inside the top-k'.
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -762,6 +763,41 @@ int topk_merge(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in, int
   return topk_merge_only(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores, bufs, nullptr, st);
 }
 
+// ASTRA_PROFILE_REFRESH=1: CUDA events between the pipeline stages of each
+// refresh call, printed after a sync (diagnostics only; changes timing).
+struct StageProf {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[12];
+  const char* name[12];
+  int n = 0;
+  explicit StageProf(cudaStream_t s) : st(s) {
+    static const bool env = getenv("ASTRA_PROFILE_REFRESH") != nullptr;
+    on = env;
+    if (on) mark("start");
+  }
+  void mark(const char* what) {
+    if (!on || n >= 12) return;
+    cudaEventCreate(&ev[n]);
+    cudaEventRecord(ev[n], st);
+    name[n++] = what;
+  }
+  ~StageProf() {
+    if (!on) return;
+    cudaEventSynchronize(ev[n - 1]);
+    fprintf(stderr, "[refresh stages]");
+    for (int i = 1; i < n; ++i) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      fprintf(stderr, " %s=%.3f", name[i], ms);
+    }
+    float tot = 0.0f;
+    cudaEventElapsedTime(&tot, ev[0], ev[n - 1]);
+    fprintf(stderr, " total=%.3f ms\n", tot);
+    for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+  }
+};
+
 int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, const float* wf, const uint16_t* wb,
                  int64_t L, int64_t off, const int64_t* pos_indptr, const int32_t* pos_ids, int k, int mode,
                  uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* ws, size_t ws_bytes,
@@ -786,6 +822,7 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
   size_t need = carve_refresh(ws, ws_bytes, nq, L, d, k, mode, &w, &n_parts, &kk, &tp);
   if (!ws || ws_bytes < need) return set_error(ASTRA_ERR_CONFIG, "refresh workspace too small (%zu < %zu)", ws_bytes, need);
   if (nq == 0) return ASTRA_OK;
+  StageProf prof(st);
   const int cap = topk_cap(kk);
   // where the bf16 / fp32 top-kk lands: the re-rank input, or the caller's outputs
   const bool rerank = mode == ASTRA_REFRESH_BF16_RERANK;
@@ -839,7 +876,9 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
       TcLaunch s = p;
       s.tile_stride = tp.stride;
       s.gmax = w.gmax;
+      prof.mark("to_bf16");
       ASTRA_TRY(launch_refresh_tc(s, st));
+      prof.mark("sample");
       tau_select_kernel<<<static_cast<unsigned>((nq + 7) / 8), 256, 0, st>>>(w.gmax, nq, tp.n_groups, tp.j, w.tau_keys);
       ASTRA_LAUNCHED("tau_select");
       // 2. threshold pass over every label
@@ -849,7 +888,12 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
       f.cand = w.cand;
       f.cand_cnt = w.cand_cnt;
       f.cand_cap = tp.cand_cap;
-      ASTRA_TRY(launch_refresh_tc(f, st));
+      prof.mark("tau_select");
+      {
+        KernelTimer kt("refresh_gemm", st);
+        ASTRA_TRY(launch_refresh_tc(f, st));
+      }
+      prof.mark("threshold");
       // 3. select
       const size_t smem = sizeof(uint64_t) * (tp.sel_max + kSelSmall) * kSelWarps;
       cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -862,21 +906,32 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
       v.k = kk;
       v.cap = cap;
       v.only_flagged = w.flags;
+      prof.mark("select");
       ASTRA_TRY(launch_refresh_tc(v, st));
       ASTRA_TRY(topk_merge_only(w.part_keys, nq, n_parts, kk, kk, o_keys, o_ids, o_scores, w.merge_bufs, w.flags, st));
+      prof.mark("verify");
     } else {
       p.k = kk;
       p.cap = cap;
-      ASTRA_TRY(launch_refresh_tc(p, st));
+      {
+        KernelTimer kt("refresh_gemm", st);
+        ASTRA_TRY(launch_refresh_tc(p, st));
+      }
       ASTRA_TRY(topk_merge(w.part_keys, nq, n_parts, kk, kk, o_keys, o_ids, o_scores, w.merge_bufs, st));
     }
   }
   static const bool legacy_rr = getenv("ASTRA_RERANK_LEGACY") != nullptr;
   if (rerank && !legacy_rr && kk <= 128 && d % 64 == 0 &&
       (reinterpret_cast<uintptr_t>(wf) & 15) == 0) {
-    if (kk <= 32) return launch_rerank_tma<1>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
-    if (kk <= 64) return launch_rerank_tma<2>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
-    return launch_rerank_tma<4>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+    int rc;
+    if (kk <= 32)
+      rc = launch_rerank_tma<1>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+    else if (kk <= 64)
+      rc = launch_rerank_tma<2>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+    else
+      rc = launch_rerank_tma<4>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+    prof.mark("rerank");
+    return rc;
   }
   if (rerank) {
     int Pn = 1;

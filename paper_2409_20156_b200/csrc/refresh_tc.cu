@@ -209,16 +209,21 @@ __device__ __forceinline__ void scan64(LaneTopK& tk, const uint32_t* ra, const u
   if (!any) return;
   if (a.dbg && (threadIdx.x & 31) == 0) atomicAdd(a.dbg + 0, 1ull);
   const int sw = threadIdx.x & 7;
-#pragma unroll
-  for (int g = 0; g < 8; ++g) {
-    *reinterpret_cast<float4*>(stage + (((2 * g) ^ sw) << 2)) = make_float4(val(g), val(g + 8), val(g + 16), val(g + 24));
-    *reinterpret_cast<float4*>(stage + (((2 * g + 1) ^ sw) << 2)) =
-        make_float4(val(g + 32), val(g + 40), val(g + 48), val(g + 56));
-  }
   uint32_t gm = 0;
   if (want) {
 #pragma unroll
     for (int g = 0; g < 8; ++g) gm |= grp[g] >= tk.tau_s ? (1u << g) : 0u;
+  }
+  // stage only the flagged groups (predicated stores: shared-memory traffic
+  // proportional to the lanes that have candidates)
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    if (gm & (1u << g)) {
+      *reinterpret_cast<float4*>(stage + (((2 * g) ^ sw) << 2)) =
+          make_float4(val(g), val(g + 8), val(g + 16), val(g + 24));
+      *reinterpret_cast<float4*>(stage + (((2 * g + 1) ^ sw) << 2)) =
+          make_float4(val(g + 32), val(g + 40), val(g + 48), val(g + 56));
+    }
   }
   while (gm) {
     const int g = __ffs(gm) - 1;

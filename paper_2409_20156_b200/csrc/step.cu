@@ -1138,31 +1138,34 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
   fa.status = status;
   const int nv = d % 128 == 0 ? d / 128 : 0;
   const bool aligned = (reinterpret_cast<uintptr_t>(emb) % 16 == 0) && (reinterpret_cast<uintptr_t>(W) % 16 == 0);
-  if (aligned && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
-    switch (nv * 2 + (bf16 ? 1 : 0)) {
-      case 2: launch_forward_vec<1, false>(fa, st); break;
-      case 3: launch_forward_vec<1, true>(fa, st); break;
-      case 4: launch_forward_vec<2, false>(fa, st); break;
-      case 5: launch_forward_vec<2, true>(fa, st); break;
-      case 8: launch_forward_vec<4, false>(fa, st); break;
-      case 9: launch_forward_vec<4, true>(fa, st); break;
-      case 12: launch_forward_vec<6, false>(fa, st); break;
-      case 13: launch_forward_vec<6, true>(fa, st); break;
-      case 16: launch_forward_vec<8, false>(fa, st); break;
-      case 17: launch_forward_vec<8, true>(fa, st); break;
-    }
-  } else {
-    size_t smem = sizeof(float) * static_cast<size_t>(d) * (1 + kFwdWarps);
-    if (smem > 200 * 1024) return set_error(ASTRA_ERR_CONFIG, "slate_step: d=%d too large", d);
-    if (bf16) {
-      cudaFuncSetAttribute(slot_forward_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      slot_forward_generic<true><<<B, kFwdThreads, smem, st>>>(fa);
+  {
+    KernelTimer kt_fwd("slot_forward", st);
+    if (aligned && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
+      switch (nv * 2 + (bf16 ? 1 : 0)) {
+        case 2: launch_forward_vec<1, false>(fa, st); break;
+        case 3: launch_forward_vec<1, true>(fa, st); break;
+        case 4: launch_forward_vec<2, false>(fa, st); break;
+        case 5: launch_forward_vec<2, true>(fa, st); break;
+        case 8: launch_forward_vec<4, false>(fa, st); break;
+        case 9: launch_forward_vec<4, true>(fa, st); break;
+        case 12: launch_forward_vec<6, false>(fa, st); break;
+        case 13: launch_forward_vec<6, true>(fa, st); break;
+        case 16: launch_forward_vec<8, false>(fa, st); break;
+        case 17: launch_forward_vec<8, true>(fa, st); break;
+      }
     } else {
-      cudaFuncSetAttribute(slot_forward_generic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      slot_forward_generic<false><<<B, kFwdThreads, smem, st>>>(fa);
+      size_t smem = sizeof(float) * static_cast<size_t>(d) * (1 + kFwdWarps);
+      if (smem > 200 * 1024) return set_error(ASTRA_ERR_CONFIG, "slate_step: d=%d too large", d);
+      if (bf16) {
+        cudaFuncSetAttribute(slot_forward_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        slot_forward_generic<true><<<B, kFwdThreads, smem, st>>>(fa);
+      } else {
+        cudaFuncSetAttribute(slot_forward_generic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        slot_forward_generic<false><<<B, kFwdThreads, smem, st>>>(fa);
+      }
     }
+    ASTRA_LAUNCHED("slot_forward");
   }
-  ASTRA_LAUNCHED("slot_forward");
   finalize_kernel<<<1, 1024, 0, st>>>(w.loss_rows, w.bound_rows, B, loss_out, status);
   ASTRA_LAUNCHED("finalize");
 
@@ -1213,6 +1216,7 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     ua.neg_step = static_cast<float>(-(lr * sqrt(bc2) / bc1));
   }
   const int upd_ctas = 16 * sms;
+  KernelTimer kt_upd("label_update", st);
   if (optimizer == ASTRA_OPT_ADAM)
     return bf16 ? launch_update<true, true>(ua, upd_ctas, st) : launch_update<false, true>(ua, upd_ctas, st);
   return bf16 ? launch_update<true, false>(ua, upd_ctas, st) : launch_update<false, false>(ua, upd_ctas, st);

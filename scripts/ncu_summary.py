@@ -32,7 +32,11 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__registers_per_thread",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum", "sm__cycles_elapsed.avg",
-        "launch__shared_mem_per_block_dynamic", "l1tex__t_bytes.sum"]
+        "launch__shared_mem_per_block_dynamic", "l1tex__t_bytes.sum", "sm__cycles_elapsed.avg.per_second",
+        "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__memory_throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum", "dram__bytes_read.sum.per_second",
+        "dram__bytes_write.sum.per_second"]
 
 
 def raw(rep):
@@ -46,6 +50,10 @@ def raw(rep):
             if w in h:
                 i = h.index(w)
                 out.append(f"  {w:70s} {r[i]:>16s} {units[i]}")
+        stalls = sorted(((k, r[j]) for j, k in enumerate(h) if k.startswith("smsp__pcsamp_warps_issue_stalled_")
+                         and not k.endswith("_not_issued") and r[j] not in ("", "0")),
+                        key=lambda x: -float(x[1].replace(",", "")))[:8]
+        out.append("  top stall reasons (pc samples): " + ", ".join(f"{k[33:]}={v}" for k, v in stalls))
     return "\n".join(out)
 
 
