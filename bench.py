@@ -182,11 +182,22 @@ def run_ours(args):
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * M + 2)] for _ in range(n_steps)]
     ids_keep = []
 
+    # the refresh of the step's rows runs on a side stream concurrently with the
+    # training minibatches (its output is the NEXT epoch's stale cache, as the
+    # reference's background _RefreshJob thread, trainer.py:198-214), confined
+    # to an SM budget so the HBM-bound step keeps the remaining SMs
+    overlap = args.refresh_sms > 0
+    rstream = torch.cuda.Stream() if overlap else stream
+    if overlap:
+        _lib.set_refresh_sm_budget(args.refresh_sms)
+
     def one(t, timed):
         st, e = dev[t], ev[t]
         e[0].record(stream)
-        eng.refresh(st["chunk"]["emb"], st["chunk"]["indptr"], st["chunk"]["pos"], k_h)
-        e[1].record(stream)
+        rstream.wait_stream(stream)
+        with torch.cuda.stream(rstream):
+            eng.refresh(st["chunk"]["emb"], st["chunk"]["indptr"], st["chunk"]["pos"], k_h)
+            e[1].record(rstream)
         for i, m in enumerate(st["mbs"]):
             slates = eng.sample(m["rows"], m["indptr"], m["pos"], m["hard"], epoch=1, step=t * M + i)
             e[2 + 2 * i].record(stream)
@@ -194,6 +205,7 @@ def run_ours(args):
             e[3 + 2 * i].record(stream)
             if timed and i == 0:
                 ids_keep.append(slates[0])
+        stream.wait_stream(rstream)
         return loss, status
 
     # clock samples cover warm-up + timed region (the timed region alone can be
@@ -234,7 +246,7 @@ def run_ours(args):
         e = ev[t]
         ph["refresh"] += e[0].elapsed_time(e[1])
         for i in range(M):
-            ph["sample"] += (e[1] if i == 0 else e[1 + 2 * i]).elapsed_time(e[2 + 2 * i])
+            ph["sample"] += (e[1 if not overlap else 0] if i == 0 else e[1 + 2 * i]).elapsed_time(e[2 + 2 * i])
             ph["step"] += e[2 + 2 * i].elapsed_time(e[3 + 2 * i])
     value = R * world * K / (ms_total / 1e3)
 
@@ -274,10 +286,13 @@ def run_ours(args):
     def one_host(t):
         nonlocal rout
         p = pinned[t]
-        rout = eng.refresh_host(p["chunk"]["emb"], p["chunk"]["indptr"], p["chunk"]["pos"], k_h, out=rout)
+        rstream.wait_stream(stream)
+        with torch.cuda.stream(rstream):
+            rout = eng.refresh_host(p["chunk"]["emb"], p["chunk"]["indptr"], p["chunk"]["pos"], k_h, out=rout)
         for i, m in enumerate(p["mbs"]):
             outs[i], _ = eng.train_step_host(m["emb"], m["rows"], m["indptr"], m["pos"], m["hard"], 1, t * M + i,
                                              CFG["lr"], CFG["wd"], out=outs[i])
+        stream.wait_stream(rstream)
 
     for t in range(args.warmup):
         one_host(t)
@@ -307,6 +322,7 @@ def run_ours(args):
                    "minibatch": B, "minibatches_per_step": M, "global_batch": B * world, "k_p": k_p, "k_h": k_h,
                    "k_r": k_r, "slate": S, "labels_per_point": CFG["labels_per_point"], "tau_r": CFG["tau_r"],
                    "refresh_chunk": R * world, "refresh_mode": "bf16_rerank", "optimizer": "sgd+wd",
+                   "refresh_overlap": overlap, "refresh_sms": args.refresh_sms if overlap else None,
                    "parallelism": f"label-shard{world}", "l2": "inputs larger than L2 (W fp32 4.0 GB + snapshots 6 GB)"},
         "phases_ms_per_step": {k: round(v / K, 4) for k, v in ph.items()},
         "refresh_mips_qps": round(q_per_refresh / t_ref, 1),
@@ -426,6 +442,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=128)
+    ap.add_argument("--refresh-sms", type=int, default=0,
+                    help="SM budget of the refresh running concurrently with training on a side stream (0 = serial)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -80,6 +80,13 @@ uint64_t astra_launch_count(void);
  * pairs recorded under `name`, returns their summed milliseconds and count,
  * and clears them. Not a reference interface (measurement only). */
 void astra_kernel_timing_enable(int on);
+
+/* Cap the number of SMs the refresh GEMM kernels occupy (0 = all SMs; the
+ * default). The kernels are persistent (one CTA per SM of the budget), so a
+ * refresh issued on a side stream leaves the other SMs to the training step
+ * running concurrently on the main stream — the B200 form of the reference's
+ * background refresh thread (trainer.py:198-214). Process-wide setting. */
+void astra_set_refresh_sm_budget(int n_sms);
 int astra_kernel_timing(const char* name, double* total_ms, int64_t* count);
 
 /* fp32 -> bf16 (round-to-nearest-even), n elements. Used for W/query snapshots. */

@@ -27,6 +27,7 @@ _SIGS = {
     "astra_launch_count": ([], u64),
     "astra_kernel_timing_enable": ([i32], None),
     "astra_kernel_timing": ([C.c_char_p, p, p], i32),
+    "astra_set_refresh_sm_budget": ([i32], None),
     "astra_f32_to_bf16": ([p, p, i64, p], i32),
     "astra_refresh_workspace_size": ([i64, i64, i32, i32, i32], sz),
     "astra_refresh_topk": ([p, p, i64, i32, p, p, i64, i64, p, p, i32, i32, p, p, p, p, sz, p], i32),
@@ -72,6 +73,11 @@ def launch_count() -> int:
 
 def kernel_timing_enable(on: bool = True) -> None:
     load().astra_kernel_timing_enable(1 if on else 0)
+
+
+def set_refresh_sm_budget(n_sms: int) -> None:
+    """Cap the SMs the refresh GEMM occupies (0 = all)."""
+    load().astra_set_refresh_sm_budget(int(n_sms))
 
 
 def kernel_timing(name: str):

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "refresh_tc.cuh"
 #include "topk.cuh"
 
 namespace astra {
@@ -84,6 +85,8 @@ const char* astra_last_error(void) { return g_err; }
 uint64_t astra_launch_count(void) { return g_launches.load(); }
 
 void astra_kernel_timing_enable(int on) { g_kt_on.store(on != 0); }
+
+void astra_set_refresh_sm_budget(int n_sms) { set_refresh_sm_budget(n_sms); }
 
 int astra_kernel_timing(const char* name, double* total_ms, int64_t* count) {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;

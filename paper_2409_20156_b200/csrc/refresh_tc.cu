@@ -27,6 +27,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -43,7 +44,8 @@ constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int TMEM_COLS = 512;
 constexpr int kEpiWarp0 = 4, kEpiWarps = 4;
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
-constexpr size_t kBarrierBytes = 256;
+constexpr size_t kBarrierBytes = 1024;  // mbarriers, TMEM address, only_flagged bitmap
+constexpr int kQtBits = 6144;           // query-tile clusters covered by the bitmap
 // + one 256 B score-staging row per epilogue thread (slow path of scan64)
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + STAGES * STAGE_BYTES + kBarrierBytes + kEpiWarps * 32 * 256;
 
@@ -130,6 +132,8 @@ struct TcArgs {
   int64_t nq, L, off;
   int d, k, cap;
   int64_t n_lt, tiles_per_part, tile_stride;  // swept label tiles, per part, stride between them
+  int64_t n_qt_cl;                            // query-tile clusters (CL query tiles each)
+  int n_parts;                                // label parts (= partial lists per query)
   const int64_t* pos_indptr;
   const int32_t* pos_ids;
   uint64_t* bufs;       // RUNNING: per-lane buffers
@@ -256,27 +260,47 @@ __device__ __forceinline__ void scan64(LaneTopK& tk, const uint32_t* ra, const u
   }
 }
 
-// Grid (query tile, label part): each CTA sweeps one contiguous range of the
-// swept label tiles for one 128-query tile; all CTAs of a part stream the same
-// W tiles at about the same time, so W comes from DRAM ~once per part and the
-// other query tiles hit L2. CL = cluster size along query tiles: the CL CTAs
-// of a cluster sweep the same label tiles; each loads 1/CL of every W tile and
-// multicasts it to all of them.
+// One work unit = (cluster of CL query tiles, label part): the CL CTAs of a
+// cluster sweep the same contiguous range of swept label tiles; each loads
+// 1/CL of every W tile and multicasts it to all of them. Clusters are
+// persistent: cluster c takes units c, c + n_clusters, ... (unit uc = part *
+// n_qt_cl + query-tile cluster), so the grid can be sized to an SM budget and
+// the query tiles of a part stream the same W tiles at about the same time (W
+// comes from DRAM ~once per part; the other query tiles hit L2).
+struct Unit {
+  int64_t qt;      // this CTA's query tile
+  int part;        // label part = the query's partial list index
+  int64_t t0, t1;  // swept label tiles [t0, t1)
+};
+
+template <int CL>
+__device__ __forceinline__ Unit unit_of(const TcArgs& a, int64_t uc, uint32_t crank) {
+  Unit u;
+  const int64_t qc = uc % a.n_qt_cl;
+  u.part = static_cast<int>(uc / a.n_qt_cl);
+  u.qt = qc * CL + crank;
+  u.t0 = std::min<int64_t>(a.n_lt, static_cast<int64_t>(u.part) * a.tiles_per_part);
+  u.t1 = std::min<int64_t>(a.n_lt, u.t0 + a.tiles_per_part);
+  return u;
+}
+
+// only_flagged: 1 bit per query-tile cluster in shared memory (all roles skip
+// the same units); clusters beyond the bitmap are always active.
+__device__ __forceinline__ bool unit_active(const uint32_t* qbits, int64_t n_qt_cl, int64_t uc) {
+  if (!qbits) return true;
+  const int64_t qc = uc % n_qt_cl;
+  if (qc >= kQtBits) return true;
+  return (qbits[qc >> 5] >> (qc & 31)) & 1u;
+}
+
 template <int CL, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     refresh_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
   constexpr uint16_t kMask = static_cast<uint16_t>((1u << CL) - 1);
   constexpr int B_SLICE = B_STAGE / CL;  // bytes of W tile rows loaded by each cluster rank
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (a.only_flagged) {
-    // verification fallback: the whole cluster leaves unless one of its queries is flagged
-    const int64_t q0 = static_cast<int64_t>(blockIdx.x / CL) * CL * BM;
-    int f = 0;
-    for (int i = threadIdx.x; i < CL * BM; i += kThreads)
-      if (q0 + i < a.nq && a.only_flagged[q0 + i]) f = 1;
-    if (!__syncthreads_or(f)) return;
-  }
   const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
+  const int64_t cluster = blockIdx.x / CL, n_clusters = gridDim.x / CL;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* sA = smem;
@@ -286,12 +310,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* qbits_s = tmem_holder + 8;  // kQtBits bits
   float* stage_base = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + kBarrierBytes);
-
-  const int64_t u_begin = std::min<int64_t>(a.n_lt, static_cast<int64_t>(blockIdx.y) * a.tiles_per_part);
-  const int64_t u_end = std::min<int64_t>(a.n_lt, u_begin + a.tiles_per_part);
   const int nkb = a.d / BK;
+  const int64_t n_units = a.n_qt_cl * a.n_parts;
 
+  const uint32_t* qbits = nullptr;
+  if (a.only_flagged) {
+    // verification fallback: which query-tile clusters hold a flagged query
+    for (int i = threadIdx.x; i < kQtBits / 32; i += kThreads) qbits_s[i] = 0u;
+    __syncthreads();
+    const int64_t nq_bits = std::min<int64_t>(a.nq, static_cast<int64_t>(kQtBits) * CL * BM);
+    for (int64_t q = threadIdx.x; q < nq_bits; q += kThreads)
+      if (a.only_flagged[q]) {
+        const int64_t qc = q / (CL * BM);
+        atomicOr(&qbits_s[qc >> 5], 1u << (qc & 31));
+      }
+    qbits = qbits_s;
+  }
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -323,21 +359,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const int q0 = static_cast<int>(blockIdx.x * BM);
-      for (int64_t t = u_begin; t < u_end; ++t) {
-        const int n0 = static_cast<int>(t * a.tile_stride * BN);
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], STAGE_BYTES);  // own A + all CL slices of the W tile
-          tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, q0);
-          if (CL == 1)
-            tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
-          else
-            tma_load_2d_mc(sB + stage * B_STAGE + crank * B_SLICE, &tmB, &full[stage], kb * BK,
-                           n0 + static_cast<int>(crank) * (BN / CL), kMask);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+      for (int64_t uc = cluster; uc < n_units; uc += n_clusters) {
+        if (!unit_active(qbits, a.n_qt_cl, uc)) continue;
+        const Unit un = unit_of<CL>(a, uc, crank);
+        const int q0 = static_cast<int>(un.qt * BM);
+        for (int64_t t = un.t0; t < un.t1; ++t) {
+          const int n0 = static_cast<int>(t * a.tile_stride * BN);
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], STAGE_BYTES);  // own A + all CL slices of the W tile
+            tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, q0);
+            if (CL == 1)
+              tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
+            else
+              tma_load_2d_mc(sB + stage * B_STAGE + crank * B_SLICE, &tmB, &full[stage], kb * BK,
+                             n0 + static_cast<int>(crank) * (BN / CL), kMask);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -350,41 +390,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     long long p_te = 0, p_full = 0;
     const long long p_t0 = a.dbg ? clock64() : 0;
-    for (int64_t t = u_begin; t < u_end; ++t) {
-      long long w0 = a.dbg ? clock64() : 0;
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      if (a.dbg) p_te += clock64() - w0;
-      tc_fence_after();
-      const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * BN);
-      for (int kb = 0; kb < nkb; ++kb) {
-        w0 = a.dbg ? clock64() : 0;
-        mbar_wait(&full[stage], phase);
-        if (a.dbg) p_full += clock64() - w0;
+    for (int64_t uc = cluster; uc < n_units; uc += n_clusters) {
+      if (!unit_active(qbits, a.n_qt_cl, uc)) continue;
+      const Unit un = unit_of<CL>(a, uc, crank);
+      for (int64_t t = un.t0; t < un.t1; ++t) {
+        long long w0 = a.dbg ? clock64() : 0;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        if (a.dbg) p_te += clock64() - w0;
         tc_fence_after();
-        if (lane == 0) {
-          const uint64_t ad = smem_desc(sA + stage * A_STAGE);
-          const uint64_t bd = smem_desc(sB + stage * B_STAGE);
+        const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          w0 = a.dbg ? clock64() : 0;
+          mbar_wait(&full[stage], phase);
+          if (a.dbg) p_full += clock64() - w0;
+          tc_fence_after();
+          if (lane == 0) {
+            const uint64_t ad = smem_desc(sA + stage * A_STAGE);
+            const uint64_t bd = smem_desc(sB + stage * B_STAGE);
 #pragma unroll
-          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-            // +32 B along K inside the 128 B swizzle atom = +2 in the encoded address
-            mma_bf16(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
+            for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+              // +32 B along K inside the 128 B swizzle atom = +2 in the encoded address
+              mma_bf16(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
+            }
+            if (CL == 1)
+              mma_commit(&empty[stage]);
+            else
+              mma_commit_mc(&empty[stage], kMask);
           }
-          if (CL == 1)
-            mma_commit(&empty[stage]);
-          else
-            mma_commit_mc(&empty[stage], kMask);
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
+        if (lane == 0) mma_commit(&tfull[acc]);
         __syncwarp();
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
         }
-      }
-      if (lane == 0) mma_commit(&tfull[acc]);
-      __syncwarp();
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
       }
     }
     if (a.dbg && lane == 0) {
@@ -399,103 +443,101 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = e * 32 + lane;  // TMEM lane = query row in tile
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(e * 32) << 16);
     float* stage = stage_base + (e * 32 + lane) * 64;
-    const int64_t q = static_cast<int64_t>(blockIdx.x) * BM + row;
-    const bool active = q < a.nq;
-    const int list = blockIdx.y;
-    LaneTopK tk;
-    {
-      const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
-      if constexpr (MODE == kGmax) {
-        lane_init(tk, nullptr, nullptr, 0);
-        (void)p0;
-        (void)p1;
-      } else if constexpr (MODE == kFixed) {
-        lane_init(tk, a.cand + (static_cast<size_t>(list) * a.nq + (active ? q : 0)) * a.cand_cap, nullptr, 0);
-        tk.tau = active ? a.tau_in[static_cast<size_t>(q) * a.tau_stride] : ~0ull;
-        tk.tau_s = tk.tau ? key_score(tk.tau) : -INFINITY;
-        (void)p0;
-        (void)p1;
-      } else {
-        uint64_t* buf = a.bufs + (static_cast<size_t>(blockIdx.x * gridDim.y + blockIdx.y) * BM + row) *
-                                     (a.cap + kTopkSlack);
-        lane_init(tk, buf, a.pos_ids + p0, p1 - p0, active ? a.gtau + q : nullptr);
-      }
-    }
+    uint64_t* const run_buf = a.bufs ? a.bufs + (static_cast<size_t>(blockIdx.x) * BM + row) * (a.cap + kTopkSlack)
+                                     : nullptr;
     int acc = 0;
     uint32_t acc_phase = 0;
     EpiProf pf;
     long long p_wait = 0;
     const long long p_t0 = a.dbg ? clock64() : 0;
-    uint64_t g_pref = 0;  // RUNNING: shared threshold prefetched one tile ahead
-    for (int64_t t = u_begin; t < u_end; ++t) {
-      const long long w0 = a.dbg ? clock64() : 0;
-      mbar_wait(&tfull[acc], acc_phase);
-      if (a.dbg) p_wait += clock64() - w0;
-      tc_fence_after();
-      const int64_t n0 = t * a.tile_stride * BN;
-      const int nvalid = static_cast<int>(std::min<int64_t>(BN, a.L - n0));
-      if constexpr (MODE == kRunning) {
-        // shared threshold: apply the value fetched during the previous tile, fetch the next
-        if (tk.gtau) {
-          if (g_pref > tk.tau) {
-            tk.tau = g_pref;
-            tk.tau_s = key_score(g_pref);
-          }
-          g_pref = *reinterpret_cast<volatile uint64_t*>(tk.gtau);
-        }
-      }
-      // 64-column steps: two 32-column TMEM loads, one wait, one vote
-      const uint32_t tbase = lane_base + static_cast<uint32_t>(acc * BN);
-      const bool full_tile = nvalid == BN;
+    for (int64_t uc = cluster; uc < n_units; uc += n_clusters) {
+      if (!unit_active(qbits, a.n_qt_cl, uc)) continue;
+      const Unit un = unit_of<CL>(a, uc, crank);
+      const int64_t q = un.qt * BM + row;
+      const bool active = q < a.nq;
+      const int list = un.part;
+      LaneTopK tk;
       if constexpr (MODE == kGmax) {
-        uint32_t gm[4];
-#pragma unroll
-        for (int c = 0; c < BN; c += 64) {
-          uint32_t ra[32], rb[32];
-          __syncwarp();
-          tmem_ld32_nowait(tbase + c, ra);
-          tmem_ld32_nowait(tbase + c + 32, rb);
-          tmem_wait();
-          float m = -INFINITY;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float x0 = (full_tile || c + j < nvalid) ? __uint_as_float(ra[j]) : -INFINITY;
-            const float x1 = (full_tile || c + j + 32 < nvalid) ? __uint_as_float(rb[j]) : -INFINITY;
-            m = fmaxf(m, fmaxf(x0, x1));
-          }
-          gm[c / 64] = ord_bits(__float_as_uint(__fadd_rn(m, 0.0f)));  // -inf: empty group, below every score
-        }
-        if (active)
-          *reinterpret_cast<uint4*>(a.gmax + static_cast<size_t>(q) * (a.n_lt * 4) + t * 4) =
-              make_uint4(gm[0], gm[1], gm[2], gm[3]);
+        lane_init(tk, nullptr, nullptr, 0);
+      } else if constexpr (MODE == kFixed) {
+        lane_init(tk, a.cand + (static_cast<size_t>(list) * a.nq + (active ? q : 0)) * a.cand_cap, nullptr, 0);
+        tk.tau = active ? a.tau_in[static_cast<size_t>(q) * a.tau_stride] : ~0ull;
+        tk.tau_s = tk.tau ? key_score(tk.tau) : -INFINITY;
       } else {
+        const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
+        lane_init(tk, run_buf, a.pos_ids + p0, p1 - p0, active ? a.gtau + q : nullptr);
+      }
+      uint64_t g_pref = 0;  // RUNNING: shared threshold prefetched one tile ahead
+      for (int64_t t = un.t0; t < un.t1; ++t) {
+        const long long w0 = a.dbg ? clock64() : 0;
+        mbar_wait(&tfull[acc], acc_phase);
+        if (a.dbg) p_wait += clock64() - w0;
+        tc_fence_after();
+        const int64_t n0 = t * a.tile_stride * BN;
+        const int nvalid = static_cast<int>(std::min<int64_t>(BN, a.L - n0));
+        if constexpr (MODE == kRunning) {
+          // shared threshold: apply the value fetched during the previous tile, fetch the next
+          if (tk.gtau) {
+            if (g_pref > tk.tau) {
+              tk.tau = g_pref;
+              tk.tau_s = key_score(g_pref);
+            }
+            g_pref = *reinterpret_cast<volatile uint64_t*>(tk.gtau);
+          }
+        }
+        // 64-column steps: two 32-column TMEM loads, one wait, one vote
+        const uint32_t tbase = lane_base + static_cast<uint32_t>(acc * BN);
+        const bool full_tile = nvalid == BN;
+        if constexpr (MODE == kGmax) {
+          uint32_t gm[4];
+#pragma unroll
+          for (int c = 0; c < BN; c += 64) {
+            uint32_t ra[32], rb[32];
+            __syncwarp();
+            tmem_ld32_nowait(tbase + c, ra);
+            tmem_ld32_nowait(tbase + c + 32, rb);
+            tmem_wait();
+            float m = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float x0 = (full_tile || c + j < nvalid) ? __uint_as_float(ra[j]) : -INFINITY;
+              const float x1 = (full_tile || c + j + 32 < nvalid) ? __uint_as_float(rb[j]) : -INFINITY;
+              m = fmaxf(m, fmaxf(x0, x1));
+            }
+            gm[c / 64] = ord_bits(__float_as_uint(__fadd_rn(m, 0.0f)));  // -inf: empty group, below every score
+          }
+          if (active)
+            *reinterpret_cast<uint4*>(a.gmax + static_cast<size_t>(q) * (a.n_lt * 4) + t * 4) =
+                make_uint4(gm[0], gm[1], gm[2], gm[3]);
+        } else {
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 64) {
-          uint32_t ra[32], rb[32];
-          __syncwarp();
-          tmem_ld32_nowait(tbase + c, ra);
-          tmem_ld32_nowait(tbase + c + 32, rb);
-          tmem_wait();
-          const uint32_t g0 = static_cast<uint32_t>(n0 + c + a.off);
-          if (full_tile)
-            scan64<true, MODE == kFixed>(tk, ra, rb, 64, g0, active, a, stage, pf);
-          else
-            scan64<false, MODE == kFixed>(tk, ra, rb, nvalid - c, g0, active, a, stage, pf);
+          for (int c = 0; c < BN; c += 64) {
+            uint32_t ra[32], rb[32];
+            __syncwarp();
+            tmem_ld32_nowait(tbase + c, ra);
+            tmem_ld32_nowait(tbase + c + 32, rb);
+            tmem_wait();
+            const uint32_t g0 = static_cast<uint32_t>(n0 + c + a.off);
+            if (full_tile)
+              scan64<true, MODE == kFixed>(tk, ra, rb, 64, g0, active, a, stage, pf);
+            else
+              scan64<false, MODE == kFixed>(tk, ra, rb, nvalid - c, g0, active, a, stage, pf);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
+      if constexpr (MODE == kFixed) {
+        if (active) a.cand_cnt[static_cast<size_t>(list) * a.nq + q] = tk.cnt;
+      } else if constexpr (MODE == kRunning) {
+        uint64_t* out = a.part_keys + (static_cast<size_t>(list) * a.nq + (active ? q : 0)) * a.k;
+        topk_flush(tk, a.cap, a.k, active, out);
       }
-    }
-    if constexpr (MODE == kFixed) {
-      if (active) a.cand_cnt[static_cast<size_t>(list) * a.nq + q] = tk.cnt;
-    } else if constexpr (MODE == kRunning) {
-      uint64_t* out = a.part_keys + (static_cast<size_t>(list) * a.nq + (active ? q : 0)) * a.k;
-      topk_flush(tk, a.cap, a.k, active, out);
     }
     if (a.dbg && lane == 0) {
       atomicAdd(a.dbg + 4, static_cast<unsigned long long>(p_wait));
@@ -582,14 +624,37 @@ int refresh_tc_cluster(int64_t n_qt) {
 
 }  // namespace
 
+static std::atomic<int> g_refresh_sm_budget{0};
+
+void set_refresh_sm_budget(int n_sms) { g_refresh_sm_budget.store(n_sms > 0 ? n_sms : 0); }
+
+// Persistent grid: at most one CTA per SM of the budget (astra_set_refresh_sm_budget,
+// default every SM); the fewest label parts whose (query-tile cluster, part)
+// units keep >= 93% of the budget's clusters busy over whole rounds.
 void refresh_tc_layout(int64_t nq, int64_t n_tiles, int* n_ctas, int* n_parts) {
-  int64_t n_qt = std::max<int64_t>(1, (nq + BM - 1) / BM);
+  const int64_t n_qt = std::max<int64_t>(1, (nq + BM - 1) / BM);
   const int cl = refresh_tc_cluster(n_qt);
-  n_qt = (n_qt + cl - 1) / cl * cl;  // whole clusters (padding tiles hold no queries)
+  const int64_t n_qt_cl = (n_qt + cl - 1) / cl;
   n_tiles = std::max<int64_t>(1, n_tiles);
-  const int64_t parts = std::min<int64_t>(n_tiles, std::max<int64_t>(1, num_sms() / n_qt));
-  *n_ctas = static_cast<int>(n_qt * parts);
-  *n_parts = static_cast<int>(parts);
+  int budget = num_sms();
+  const int b = g_refresh_sm_budget.load();
+  if (b > 0) budget = std::min(budget, b);
+  const int64_t n_cl_max = std::max(1, budget / cl);
+  int64_t best_p = 1;
+  double best_eff = -1.0;
+  for (int64_t p = 1; p <= std::min<int64_t>(n_tiles, 64); ++p) {
+    const int64_t units = n_qt_cl * p;
+    const int64_t n_cl = std::min(n_cl_max, units);
+    const int64_t rounds = (units + n_cl - 1) / n_cl;
+    const double eff = static_cast<double>(units) / static_cast<double>(rounds * n_cl_max);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best_p = p;
+    }
+    if (best_eff >= 0.93) break;  // fewest parts that fill the budget: fewer lists, more L2 reuse of W
+  }
+  *n_ctas = static_cast<int>(std::min(n_cl_max, n_qt_cl * best_p) * cl);
+  *n_parts = static_cast<int>(best_p);
 }
 
 int launch_refresh_tc(const TcLaunch& p, cudaStream_t st) {
@@ -614,6 +679,8 @@ int launch_refresh_tc(const TcLaunch& p, cudaStream_t st) {
   a.n_lt = n_lt;
   a.tiles_per_part = (n_lt + n_parts - 1) / n_parts;
   a.tile_stride = p.tile_stride;
+  a.n_qt_cl = ((p.nq + BM - 1) / BM + cl - 1) / cl;
+  a.n_parts = n_parts;
   a.pos_indptr = p.pos_indptr;
   a.pos_ids = p.pos_ids;
   a.bufs = p.bufs;
@@ -634,7 +701,7 @@ int launch_refresh_tc(const TcLaunch& p, cudaStream_t st) {
   a.dbg = counters ? dbg_buf : nullptr;
   if (counters) cudaMemsetAsync(dbg_buf, 0, 12 * sizeof(unsigned long long), st);
   if (mode == kRunning) ASTRA_TRY(check_cuda(cudaMemsetAsync(p.gtau, 0, sizeof(uint64_t) * p.nq, st), "memset gtau"));
-  const dim3 grid(static_cast<unsigned>(G / n_parts), static_cast<unsigned>(n_parts));
+  const dim3 grid(static_cast<unsigned>(G));
   int rc;
   if (mode == kFixed)
     rc = cl == 2 ? launch_variant<2, kFixed>(tmA, tmB, a, grid, st) : launch_variant<1, kFixed>(tmA, tmB, a, grid, st);

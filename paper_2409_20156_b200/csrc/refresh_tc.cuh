@@ -45,5 +45,8 @@ constexpr int kTcTileLabels = 256;
 int launch_refresh_tc(const TcLaunch& p, cudaStream_t st);
 // CTAs and per-query lists (= label parts) for nq queries over n_tiles label tiles.
 void refresh_tc_layout(int64_t nq, int64_t n_tiles, int* n_ctas, int* n_parts);
+// Cap on the SMs the refresh GEMM occupies (0 = all), so that a refresh on a
+// side stream leaves SMs to the training step (astra_set_refresh_sm_budget).
+void set_refresh_sm_budget(int n_sms);
 
 }  // namespace astra

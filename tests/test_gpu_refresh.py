@@ -176,3 +176,24 @@ def test_two_pass_fallback_on_adversarial_sample(cuda_lib):
     run_keys, _, _ = _with_two_pass("0", lambda: _run(E, W, positives, k, "bf16"))
     tp_keys, _, _ = _with_two_pass("1", lambda: _run(E, W, positives, k, "bf16"))
     np.testing.assert_array_equal(tp_keys, run_keys)
+
+
+@pytest.mark.parametrize("budget", [52, 17])
+def test_sm_budget_same_result(cuda_lib, budget):
+    """A refresh confined to an SM budget (persistent clusters looping over
+    more (query tile, label part) units) returns exactly the same keys."""
+    from paper_2409_20156_b200 import _lib
+
+    rng = np.random.default_rng(budget)
+    L, d, nq, k = 70_000, 128, 1500, 48
+    W = rng.uniform(-1 / np.sqrt(d), 1 / np.sqrt(d), size=(L, d)).astype(np.float32)
+    E = rng.standard_normal((nq, d)).astype(np.float32)
+    positives = random_positives(rng, nq, L, 0, 6)
+    for flag in ("0", "1"):
+        full_keys, _, _ = _with_two_pass(flag, lambda: _run(E, W, positives, k, "bf16"))
+        _lib.set_refresh_sm_budget(budget)
+        try:
+            b_keys, _, _ = _with_two_pass(flag, lambda: _run(E, W, positives, k, "bf16"))
+        finally:
+            _lib.set_refresh_sm_budget(0)
+        np.testing.assert_array_equal(b_keys, full_keys)
