@@ -4,6 +4,9 @@ Same names, signatures, return types and error classes as the reference:
   build_exact(vectors, snapshot_epoch=0) -> AnnsIndex            anns.py:99-100
   retrieve_hard_negatives(index, embeddings, positives, k_h,
                           query_beam=128) -> NegativeCache        anns.py:233-268
+  query_topk(index, query, k, query_beam=128) -> ScoredLabels     anns.py:211-230
+plus query_topk_batch(index, queries, k) -> (ids, scores), the batched form
+the exact MIPS kernel is built for (evaluation / UpToDateHard).
 The exact branch (anns.py:252-256: E @ W^T, positive mask, _batched_topk) runs
 on the GPU (libastra_b200: tcgen05 GEMM + fused top-k, or the fp32-exact SIMT
 kernel). The approximate graph index (anns.py:136-208) is outside the B200
@@ -52,8 +55,19 @@ except ImportError:
             return self.ids.shape[1]
 
 
-# set by install(): the reference implementation for non-exact indexes
+try:
+    from xcmix.classifiers import ScoredLabels
+except ImportError:
+
+    @dataclass
+    class ScoredLabels:
+        label_ids: np.ndarray
+        scores: np.ndarray
+
+
+# set by install(): the reference implementations for non-exact indexes
 _approx_impl = None
+_approx_query_impl = None
 QUERY_CHUNK = 1 << 16
 
 
@@ -134,3 +148,43 @@ def retrieve_hard_negatives(index, embeddings, positives, k_h: int, query_beam: 
             k_h, mode, labels_f32=w32, labels_bf16=wbf)
         out[lo:hi] = top.cpu().numpy()
     return NegativeCache(out, index.snapshot_epoch)
+
+
+def query_topk_batch(index, queries, k: int, mode: str | None = None):
+    """Exact top-k (ids int64, scores float64) of every query row against the
+    index, descending, ties toward the lower id, no exclusions: the same fused
+    refresh kernel with empty positive lists. fp32-exact (sequential fmaf) by
+    default, so ids follow the reference's float64 ranking up to fp32 ties."""
+    if index.kind != "exact":
+        raise ConfigError("query_topk_batch serves exact indexes")
+    if k > index.size:
+        raise ConfigError(f"k={k} exceeds index size {index.size}")
+    ops = _backend.get()
+    L, d = index.vectors.shape
+    mode = mode or os.environ.get("ASTRA_QUERY_MODE", "fp32")
+    w32, wbf = _device_snapshot(index, mode)
+    dev = w32.device
+    Q = np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32)
+    N = Q.shape[0]
+    ids = np.empty((N, k), dtype=np.int64)
+    scores = np.empty((N, k), dtype=np.float64)
+    for lo in range(0, N, QUERY_CHUNK):
+        hi = min(N, lo + QUERY_CHUNK)
+        indptr = torch.zeros(hi - lo + 1, dtype=torch.int64, device=dev)
+        pid = torch.zeros(0, dtype=torch.int32, device=dev)
+        _, top, sc = ops.refresh_topk(torch.from_numpy(Q[lo:hi]).to(dev), indptr, pid, k, mode, labels_f32=w32,
+                                      labels_bf16=wbf)
+        ids[lo:hi] = top.cpu().numpy()
+        scores[lo:hi] = sc.cpu().numpy()
+    return ids, scores
+
+
+def query_topk(index, query, k: int, query_beam: int = 128):
+    """Top-k ids by inner product for one query (anns.py:211-230); exact
+    indexes on the GPU, graph indexes through the reference implementation."""
+    if index.kind != "exact":
+        if _approx_query_impl is None:
+            raise ConfigError(f"index kind {index.kind!r} is not served by the B200 path")
+        return _approx_query_impl(index, query, k, query_beam)
+    ids, scores = query_topk_batch(index, np.asarray(query, dtype=np.float64)[None, :], k)
+    return ScoredLabels(ids[0], scores[0])

@@ -11,13 +11,16 @@ Rebinds the module globals the reference resolves at call time (SURVEY.md
         so the GPU step can be compared bit-for-bit on identical indices)
   xcmix.trainer/classifiers.apply_classifier_updates_arrays <- classifiers.*
         (trainer.py:27 imported the name, classifiers.py:71 uses the global)
+  xcmix.anns.query_topk                        <- anns.query_topk
+        (UpToDateHard, trainer.py:321-333; evaluation's anns mode)
+  xcmix.evaluation.predict_topk                <- evaluation.predict_topk (exact mode)
 Code that imported a name before install() (`from xcmix.anns import f`) keeps
 the old object: install first (e.g. from a pytest plugin / conftest).
 """
 
 from __future__ import annotations
 
-from . import _backend, anns, classifiers, trainer
+from . import _backend, anns, classifiers, evaluation, trainer
 
 _saved: dict = {}
 
@@ -31,8 +34,15 @@ def install(backend=None, slates: str = "philox") -> None:
         raise ValueError("slates must be 'philox' or 'reference'")
     if backend is not None:
         _backend.set_backend(backend)
+    try:
+        import xcmix.evaluation as xe
+    except ImportError:  # evaluation needs the reference's optional deps
+        xe = None
     if not _saved:
+        if xe is not None:
+            _saved[(xe, "predict_topk")] = xe.predict_topk
         _saved.update({
+            (xa, "query_topk"): xa.query_topk,
             (xa, "retrieve_hard_negatives"): xa.retrieve_hard_negatives,
             (xt, "_batch_forward_backward"): xt._batch_forward_backward,
             (xt, "_assemble_batch_slates"): xt._assemble_batch_slates,
@@ -40,7 +50,12 @@ def install(backend=None, slates: str = "philox") -> None:
             (xc, "apply_classifier_updates_arrays"): xc.apply_classifier_updates_arrays,
         })
     anns._approx_impl = _saved[(xa, "retrieve_hard_negatives")]
+    anns._approx_query_impl = _saved[(xa, "query_topk")]
     xa.retrieve_hard_negatives = anns.retrieve_hard_negatives
+    xa.query_topk = anns.query_topk
+    if xe is not None:
+        evaluation._reference_predict = _saved[(xe, "predict_topk")]
+        xe.predict_topk = evaluation.predict_topk
     xt._batch_forward_backward = trainer._batch_forward_backward
     xt._assemble_batch_slates = (trainer._assemble_batch_slates if slates == "philox"
                                  else _saved[(xt, "_assemble_batch_slates")])
@@ -53,3 +68,5 @@ def uninstall() -> None:
         setattr(mod, name, fn)
     _saved.clear()
     anns._approx_impl = None
+    anns._approx_query_impl = None
+    evaluation._reference_predict = None

@@ -16,7 +16,8 @@ import pytest
 from conftest import ROOT
 
 REF = "/root/reference/pkg"
-SUITES = ["test_anns.py", "test_classifiers.py", "test_sampler.py", "test_loss.py", "test_trainer.py", "test_encoder.py"]
+SUITES = ["test_anns.py", "test_classifiers.py", "test_sampler.py", "test_loss.py", "test_trainer.py", "test_encoder.py",
+          "test_eval.py"]
 
 
 def _run(slates, extra=()):

@@ -197,3 +197,26 @@ def test_sm_budget_same_result(cuda_lib, budget):
         finally:
             _lib.set_refresh_sm_budget(0)
         np.testing.assert_array_equal(b_keys, full_keys)
+
+
+def test_query_topk_batch_reuses_the_mips_kernel(cuda_lib):
+    """anns.query_topk / query_topk_batch (anns.py:211-230, the UpToDateHard and
+    evaluation path): fp32-exact ids equal the C oracle bit for bit, and the
+    float64 ranking of the reference on well-separated scores."""
+    from paper_2409_20156_b200 import anns
+
+    rng = np.random.default_rng(11)
+    L, d, N, k = 5000, 64, 37, 10
+    W = rng.standard_normal((L, d)).astype(np.float32)
+    Q = rng.standard_normal((N, d)).astype(np.float32)
+    index = anns.build_exact(W)
+    ids, scores = anns.query_topk_batch(index, Q, k)
+    _, oids, oscores = co.refresh_fp32(Q, W, np.zeros(N + 1, np.int64), np.zeros(0, np.int32), k)
+    np.testing.assert_array_equal(ids, oids)
+    np.testing.assert_array_equal(scores, oscores.astype(np.float64))
+    s64 = W.astype(np.float64) @ Q.astype(np.float64).T
+    for i in range(N):
+        order = np.lexsort((np.arange(L), -s64[:, i]))[:k]
+        assert ids[i].tolist() == order.tolist()
+    one = anns.query_topk(index, Q[3], k)
+    assert one.label_ids.tolist() == ids[3].tolist()
