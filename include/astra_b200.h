@@ -103,7 +103,9 @@ int astra_f32_to_bf16(const float* src, uint16_t* dst, int64_t n, void* stream);
  *   queries_f32   nq x d   fp32 (FP32_EXACT, BF16_RERANK; may be NULL for BF16
  *                          if queries_bf16 is given)
  *   queries_bf16  nq x d   bf16 bits, or NULL (converted into the workspace)
- *   labels_f32    n_labels x d fp32 snapshot (FP32_EXACT, BF16_RERANK)
+ *   labels_f32    n_labels x d fp32 snapshot (FP32_EXACT, BF16_RERANK; for
+ *                 BF16_RERANK it may be NULL: the re-rank then scores the bf16
+ *                 snapshot's values exactly — the bf16-W configuration)
  *   labels_bf16   n_labels x d bf16 snapshot (BF16, BF16_RERANK)
  *   pos_indptr    nq+1 int64, pos_ids int32 GLOBAL ids sorted ascending per row
  *   out_keys      nq x k packed keys (input of astra_topk_merge), or NULL

@@ -331,13 +331,14 @@ constexpr int kRtRing = 2;
 
 __host__ __device__ inline int rerank_chunk(int d) { return d % 256 == 0 ? 256 : 64; }
 
-template <int R>
-__global__ void __launch_bounds__(64) rerank_tma_kernel(const float* Q, const float* W, int d, int64_t off,
+template <int R, bool BF16>
+__global__ void __launch_bounds__(64) rerank_tma_kernel(const float* Q, const void* W, int d, int64_t off,
                                                         const uint64_t* cand, int kc, int k, uint64_t* out_keys,
                                                         int32_t* out_ids, float* out_scores) {
   extern __shared__ __align__(128) unsigned char rsm[];
   const int ch = rerank_chunk(d);
-  const int pitch = ch * 4 + 16;
+  constexpr int esz = BF16 ? 2 : 4;
+  const int pitch = ch * esz + 16;
   const int stage_bytes = 32 * pitch;
   unsigned char* ring = rsm;
   float* qs = reinterpret_cast<float*>(rsm + kRtRing * stage_bytes);
@@ -362,15 +363,16 @@ __global__ void __launch_bounds__(64) rerank_tma_kernel(const float* Q, const fl
       const int c = u * 32 + lane;
       const uint64_t key = c < kc ? cand[q * kc + c] : 0ull;
       const int32_t gid = key ? key_id(key) : -1;
-      const uint32_t nbytes = __popc(__ballot_sync(0xffffffffu, gid >= 0)) * ch * 4;
+      const uint32_t nbytes = __popc(__ballot_sync(0xffffffffu, gid >= 0)) * ch * esz;
       for (int h = 0; h < nch; ++h) {
         const int i = u * nch + h, st = i % kRtRing;
         mbar_wait(&empty[st], ((i / kRtRing) & 1) ^ 1);
         if (lane == 0) mbar_expect_tx(&full[st], nbytes);
         __syncwarp();
         if (gid >= 0)
-          bulk_g2s(ring + st * stage_bytes + lane * pitch, W + static_cast<size_t>(gid - off) * d + h * ch, ch * 4,
-                   &full[st]);
+          bulk_g2s(ring + st * stage_bytes + lane * pitch,
+                   static_cast<const unsigned char*>(W) + (static_cast<size_t>(gid - off) * d + h * ch) * esz,
+                   ch * esz, &full[st]);
       }
     }
     return;
@@ -389,11 +391,18 @@ __global__ void __launch_bounds__(64) rerank_tma_kernel(const float* Q, const fl
       for (int h = 0; h < nch; ++h) {
         const int i = u * nch + h, st = i % kRtRing;
         mbar_wait(&full[st], (i / kRtRing) & 1);
-        const float* row = reinterpret_cast<const float*>(ring + st * stage_bytes + lane * pitch);
+        const unsigned char* row = ring + st * stage_bytes + lane * pitch;
         const float* qh = qs + h * ch;
 #pragma unroll 8
         for (int t = 0; t < ch; t += 4) {
-          const float4 v = *reinterpret_cast<const float4*>(row + t);
+          float4 v;
+          if constexpr (BF16) {
+            const uint2 u = *reinterpret_cast<const uint2*>(row + t * 2);
+            v = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                            __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+          } else {
+            v = *reinterpret_cast<const float4*>(row + t * 4);
+          }
           const float4 x = *reinterpret_cast<const float4*>(qh + t);
           s = fmaf(x.x, v.x, s);
           s = fmaf(x.y, v.y, s);
@@ -420,18 +429,18 @@ __global__ void __launch_bounds__(64) rerank_tma_kernel(const float* Q, const fl
   }
 }
 
-template <int R>
-int launch_rerank_tma(const float* qf, const float* wf, int d, int64_t off, const uint64_t* cand, int64_t nq, int kc,
+template <int R, bool BF16>
+int launch_rerank_tma(const float* qf, const void* wl, int d, int64_t off, const uint64_t* cand, int64_t nq, int kc,
                       int k, uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st) {
   const int ch = rerank_chunk(d);
-  const size_t smem = static_cast<size_t>(kRtRing) * 32 * (ch * 4 + 16) + sizeof(float) * d + 16 * kRtRing;
+  const size_t smem = static_cast<size_t>(kRtRing) * 32 * (ch * (BF16 ? 2 : 4) + 16) + sizeof(float) * d + 16 * kRtRing;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(rerank_tma_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(rerank_tma_kernel<R, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  rerank_tma_kernel<R><<<static_cast<unsigned>(nq), 64, smem, st>>>(qf, wf, d, off, cand, kc, k, out_keys, out_ids,
-                                                                    out_scores);
+  rerank_tma_kernel<R, BF16><<<static_cast<unsigned>(nq), 64, smem, st>>>(qf, wl, d, off, cand, kc, k, out_keys,
+                                                                          out_ids, out_scores);
   ASTRA_LAUNCHED("rerank_tma");
   return ASTRA_OK;
 }
@@ -811,8 +820,7 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
     if (d % 64) return set_error(ASTRA_ERR_CONFIG, "bf16 refresh needs d %% 64 == 0 (d=%d)", d);
     if (!wb) return set_error(ASTRA_ERR_CONFIG, "bf16 refresh needs the bf16 label snapshot");
     if (!qf && !qb_in) return set_error(ASTRA_ERR_CONFIG, "bf16 refresh needs queries");
-    if (mode == ASTRA_REFRESH_BF16_RERANK && (!qf || !wf))
-      return set_error(ASTRA_ERR_CONFIG, "BF16_RERANK needs fp32 queries and labels");
+    if (mode == ASTRA_REFRESH_BF16_RERANK && !qf) return set_error(ASTRA_ERR_CONFIG, "BF16_RERANK needs fp32 queries");
   } else {
     return set_error(ASTRA_ERR_CONFIG, "refresh: unknown mode %d", mode);
   }
@@ -921,15 +929,21 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
     }
   }
   static const bool legacy_rr = getenv("ASTRA_RERANK_LEGACY") != nullptr;
-  if (rerank && !legacy_rr && kk <= 128 && d % 64 == 0 &&
-      (reinterpret_cast<uintptr_t>(wf) & 15) == 0) {
+  // the re-rank scores the fp32 snapshot, or the bf16 one when no fp32 copy is given (bf16 W)
+  const bool rr_bf16 = wf == nullptr;
+  const void* wl = rr_bf16 ? static_cast<const void*>(wb) : static_cast<const void*>(wf);
+  if (rerank && (rr_bf16 || (!legacy_rr && kk <= 128 && d % 64 == 0 && (reinterpret_cast<uintptr_t>(wf) & 15) == 0))) {
+    if (kk > 128) return set_error(ASTRA_ERR_CONFIG, "BF16_RERANK from bf16 labels needs k' <= 128 (k <= 85)");
     int rc;
     if (kk <= 32)
-      rc = launch_rerank_tma<1>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+      rc = rr_bf16 ? launch_rerank_tma<1, true>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st)
+                   : launch_rerank_tma<1, false>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
     else if (kk <= 64)
-      rc = launch_rerank_tma<2>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+      rc = rr_bf16 ? launch_rerank_tma<2, true>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st)
+                   : launch_rerank_tma<2, false>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
     else
-      rc = launch_rerank_tma<4>(qf, wf, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+      rc = rr_bf16 ? launch_rerank_tma<4, true>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st)
+                   : launch_rerank_tma<4, false>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
     prof.mark("rerank");
     return rc;
   }

@@ -855,8 +855,8 @@ __global__ void __launch_bounds__(kUpdThreads) label_update_vec(UpdArgs a) {
 // gradient from the L2-resident embeddings (same ascending-slot order and
 // roundings as label_update_vec), then take the row from the ring, apply the
 // update and store it. W is read and written once per touched row.
-template <int NV, bool BF16>
-__global__ void __launch_bounds__(kTmaThreads, 3) label_update_tma(UpdArgs a) {
+template <int NV, bool BF16, bool ADAM>
+__global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(UpdArgs a) {
   constexpr int d = NV * 128;
   constexpr int RING = tma_ring<BF16>();
   constexpr uint32_t ROWB = d * (BF16 ? 2 : 4);
@@ -896,6 +896,15 @@ __global__ void __launch_bounds__(kTmaThreads, 3) label_update_tma(UpdArgs a) {
     const int32_t l = a.uniq[u0 + i];
     const uint32_t start = a.offsets[l], n = a.counts[l];
     const int32_t reg = sort_segment(a, start, n, lane);
+    const size_t row = static_cast<size_t>(l) * d;
+    float4 m4[ADAM ? NV : 1], v4[ADAM ? NV : 1];
+    if constexpr (ADAM) {  // moment rows: loads issued before the gradient sum
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        m4[q] = *reinterpret_cast<const float4*>(a.m + row + q * 128 + lane * 4);
+        v4[q] = *reinterpret_cast<const float4*>(a.v + row + q * 128 + lane * 4);
+      }
+    }
     float4 g[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) g[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -950,15 +959,23 @@ __global__ void __launch_bounds__(kTmaThreads, 3) label_update_tma(UpdArgs a) {
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[r]);
-    const size_t row = static_cast<size_t>(l) * d;
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
       float4 np;
-      np.x = upd_elem<false>(a, p[q].x, g[q].x, nullptr, nullptr);
-      np.y = upd_elem<false>(a, p[q].y, g[q].y, nullptr, nullptr);
-      np.z = upd_elem<false>(a, p[q].z, g[q].z, nullptr, nullptr);
-      np.w = upd_elem<false>(a, p[q].w, g[q].w, nullptr, nullptr);
       const size_t el = row + q * 128 + lane * 4;
+      if constexpr (ADAM) {
+        np.x = upd_elem<true>(a, p[q].x, g[q].x, &m4[q].x, &v4[q].x);
+        np.y = upd_elem<true>(a, p[q].y, g[q].y, &m4[q].y, &v4[q].y);
+        np.z = upd_elem<true>(a, p[q].z, g[q].z, &m4[q].z, &v4[q].z);
+        np.w = upd_elem<true>(a, p[q].w, g[q].w, &m4[q].w, &v4[q].w);
+        *reinterpret_cast<float4*>(a.m + el) = m4[q];
+        *reinterpret_cast<float4*>(a.v + el) = v4[q];
+      } else {
+        np.x = upd_elem<false>(a, p[q].x, g[q].x, nullptr, nullptr);
+        np.y = upd_elem<false>(a, p[q].y, g[q].y, nullptr, nullptr);
+        np.z = upd_elem<false>(a, p[q].z, g[q].z, nullptr, nullptr);
+        np.w = upd_elem<false>(a, p[q].w, g[q].w, nullptr, nullptr);
+      }
       if constexpr (BF16) {
         uint2 o;
         o.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
@@ -1010,14 +1027,14 @@ void launch_forward_vec(const FwdArgs& a, cudaStream_t st) {
   }
 }
 
-template <int NV, bool BF16>
+template <int NV, bool BF16, bool ADAM>
 void launch_upd_tma(const UpdArgs& a, int grid, size_t smem, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(label_update_tma<NV, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(label_update_tma<NV, BF16, ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  label_update_tma<NV, BF16><<<grid, kTmaThreads, smem, st>>>(a);
+  label_update_tma<NV, BF16, ADAM><<<grid, kTmaThreads, smem, st>>>(a);
 }
 
 template <bool BF16, bool ADAM>
@@ -1026,15 +1043,15 @@ int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
   label_update_kernel<BF16, ADAM, true><<<max_ctas, kUpdThreads, 0, st>>>(a);
   ASTRA_LAUNCHED("label_check");
   static const bool legacy = getenv("ASTRA_STEP_LEGACY_UPD") != nullptr;
-  if (!ADAM && !legacy && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
-    const int grid = 3 * num_sms();
+  if (!legacy && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
+    const int grid = (ADAM ? 2 : 3) * num_sms();
     const size_t smem = static_cast<size_t>(tma_ring<BF16>()) * a.d * (BF16 ? 2 : 4) + 2 * 8 * tma_ring<BF16>();
     switch (nv) {
-      case 1: launch_upd_tma<1, BF16>(a, grid, smem, st); break;
-      case 2: launch_upd_tma<2, BF16>(a, grid, smem, st); break;
-      case 4: launch_upd_tma<4, BF16>(a, grid, smem, st); break;
-      case 6: launch_upd_tma<6, BF16>(a, grid, smem, st); break;
-      case 8: launch_upd_tma<8, BF16>(a, grid, smem, st); break;
+      case 1: launch_upd_tma<1, BF16, ADAM>(a, grid, smem, st); break;
+      case 2: launch_upd_tma<2, BF16, ADAM>(a, grid, smem, st); break;
+      case 4: launch_upd_tma<4, BF16, ADAM>(a, grid, smem, st); break;
+      case 6: launch_upd_tma<6, BF16, ADAM>(a, grid, smem, st); break;
+      case 8: launch_upd_tma<8, BF16, ADAM>(a, grid, smem, st); break;
     }
     ASTRA_LAUNCHED("label_update_tma");
     return ASTRA_OK;

@@ -76,8 +76,14 @@ class ClassifierEngine:
         """Immutable copy of the shard for the refresh (anns.py:90-100)."""
         if check_finite and not bool(torch.isfinite(self.W).all()):
             raise NumericalError("non-finite vectors in index build")
-        self.snap_f32 = self.W.float().clone() if self.W.dtype != torch.float32 else self.W.clone()
-        self.snap_bf16 = self.ops.f32_to_bf16(self.snap_f32) if self.refresh_mode != "fp32" else None
+        if self.W.dtype == torch.bfloat16 and self.refresh_mode != "fp32":
+            # bf16 W: the bf16 copy is the whole snapshot (the re-rank scores its
+            # values exactly); no fp32 copy (46 GB for a 15M-label shard)
+            self.snap_f32 = None
+            self.snap_bf16 = self.W.clone()
+        else:
+            self.snap_f32 = self.W.float().clone() if self.W.dtype != torch.float32 else self.W.clone()
+            self.snap_bf16 = self.ops.f32_to_bf16(self.snap_f32) if self.refresh_mode != "fp32" else None
         self.snapshot_epoch = epoch
 
     # ------------------------------------------------------------ refresh
@@ -85,7 +91,7 @@ class ClassifierEngine:
                 mode: str | None = None):
         """Global top-k (ids, scores) for this rank's queries over ALL shards,
         positives excluded. Collective when world_size > 1."""
-        if self.snap_f32 is None:
+        if self.snap_f32 is None and self.snap_bf16 is None:
             raise ConfigError("refresh before snapshot()")
         mode = mode or self.refresh_mode
         B = queries.shape[0]

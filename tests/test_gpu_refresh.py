@@ -220,3 +220,23 @@ def test_query_topk_batch_reuses_the_mips_kernel(cuda_lib):
         assert ids[i].tolist() == order.tolist()
     one = anns.query_topk(index, Q[3], k)
     assert one.label_ids.tolist() == ids[3].tolist()
+
+
+@pytest.mark.parametrize("k", [16, 64])
+def test_bf16_rerank_from_bf16_labels(cuda_lib, k):
+    """bf16 W (no fp32 copy): BF16_RERANK re-scores the bf16 rows exactly, so
+    the ids equal FP32_EXACT run on the bf16-rounded W."""
+    from paper_2409_20156_b200 import ops
+
+    rng = np.random.default_rng(k)
+    L, d, nq = 30_000, 256, 300
+    W = rng.uniform(-1 / np.sqrt(d), 1 / np.sqrt(d), size=(L, d)).astype(np.float32)
+    E = rng.standard_normal((nq, d)).astype(np.float32)
+    positives = random_positives(rng, nq, L, 0, 5)
+    Wb = ops.f32_to_bf16(dev(W))
+    W_rounded = Wb.float().cpu().numpy()
+    ip, pid = csr(positives)
+    keys, ids, scores = ops.refresh_topk(dev(E), dev(ip), dev(pid), k, "bf16_rerank", labels_bf16=Wb)
+    _, exact_ids, exact_scores = _run(E, W_rounded, positives, k, "fp32")
+    np.testing.assert_array_equal(ids.cpu().numpy(), exact_ids)
+    np.testing.assert_array_equal(scores.cpu().numpy(), exact_scores)
