@@ -360,6 +360,122 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------ C5 shard emulation
+C5 = dict(workload="120M-label synthetic, rank-0 shard of 8 (15M labels) emulated on one GPU", L_total=120_000_000,
+          world=8, d=768, B_global=4096, k_p=16, k_h=200, k_i=200, n_cand=400, k_r=2000, labels_per_point=10,
+          lr=1e-3, wd=0.0)
+
+
+def run_c5shard(args):
+    """BASELINE.json configs[4] as one of its 8 label shards: W (15M x 768 bf16)
+    + Adam m, v (fp32) resident on this GPU; each step = the refresh of the
+    global batch's 4096 queries against the shard (bf16 tcgen05 two-pass +
+    bf16-row re-rank, k_h=200) + Philox slates over all 120M labels (k_p=16,
+    k_h=200, k_i=200 importance, k_r=2000 -> S=2416) + the fused loss/update of
+    the slots this shard owns (~1/8). The collectives of the 8-GPU job (query /
+    embedding all-gathers, key all-gather, grad_emb reduce-scatter: ~40 MB per
+    step over NVLink) are not run; the line reports the shard's compute time."""
+    import torch
+
+    from paper_2409_20156_b200 import _lib, ops
+
+    torch.cuda.set_device(0)
+    c = C5
+    L = c["L_total"] // c["world"]
+    d, B = c["d"], c["B_global"]
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+    W = torch.empty((L, d), dtype=torch.bfloat16, device="cuda")
+    for lo in range(0, L, 1 << 20):  # chunked init (uniform(-1/sqrt(d), 1/sqrt(d)), classifiers.py:37-40)
+        hi = min(L, lo + (1 << 20))
+        W[lo:hi] = ((torch.rand((hi - lo, d), device="cuda", generator=g) * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+    m = torch.zeros((L, d), dtype=torch.float32, device="cuda")
+    v = torch.zeros_like(m)
+    snap = W.clone()
+    n_steps = args.warmup + args.steps
+    data = []
+    for t in range(n_steps):
+        rows = torch.arange(t * B, (t + 1) * B, dtype=torch.int64, device="cuda")
+        pos = torch.randint(0, c["L_total"], (B, c["labels_per_point"]), device="cuda", generator=g).sort(1).values
+        ip = torch.arange(0, B * c["labels_per_point"] + 1, c["labels_per_point"], dtype=torch.int64, device="cuda")
+        pid = pos.to(torch.int32).reshape(-1).contiguous()
+        emb = torch.randn((B, d), device="cuda", generator=g)
+        hard = torch.randint(0, c["L_total"], (B, c["k_h"]), device="cuda", generator=g).to(torch.int32)
+        cand = torch.randint(0, c["L_total"], (B, c["n_cand"]), device="cuda", generator=g).to(torch.int32)
+        cand_q = torch.full((B, c["n_cand"]), 1.0 / c["n_cand"], device="cuda")
+        data.append((rows, ip, pid, emb, hard, cand, cand_q))
+    stream = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_steps)]
+
+    def one(t):
+        rows, ip, pid, emb, hard, cand, cand_q = data[t]
+        e = ev[t]
+        e[0].record(stream)
+        ops.refresh_topk(emb, ip, pid, c["k_h"], "bf16_rerank", labels_bf16=snap)
+        e[1].record(stream)
+        sl = ops.sample_slates(0, 1, t, rows, ip, pid, hard, c["k_h"], c["L_total"], c["k_p"], c["k_r"], cand=cand,
+                               cand_q=cand_q, k_i=c["k_i"])
+        e[2].record(stream)
+        res = ops.slate_step(emb, *sl, W, c["lr"], c["wd"], optimizer="adam", adam_m=m, adam_v=v, adam_step=t + 1,
+                             label_offset=0)
+        e[3].record(stream)
+        return res, sl
+
+    for t in range(args.warmup):
+        one(t)
+    torch.cuda.synchronize()
+    for name in ("refresh_gemm", "slot_forward", "label_update"):
+        _lib.kernel_timing(name)
+    _lib.kernel_timing_enable(True)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for t in range(args.warmup, n_steps):
+        res, sl = one(t)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    _lib.kernel_timing_enable(False)
+    kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "slot_forward", "label_update")}
+    ops.raise_for_step_status(res.status)
+    K = args.steps
+    ms = t0.elapsed_time(t1) / K
+    ph = {"refresh": 0.0, "sample": 0.0, "step": 0.0}
+    for t in range(args.warmup, n_steps):
+        e = ev[t]
+        ph["refresh"] += e[0].elapsed_time(e[1]) / K
+        ph["sample"] += e[1].elapsed_time(e[2]) / K
+        ph["step"] += e[2].elapsed_time(e[3]) / K
+    ids = sl[0]
+    own = ids[(ids >= 0) & (ids < L)]
+    U = int(torch.unique(own).numel())
+    _, tf_burst, tf_sus, peak_kind = peaks()[0], peaks()[1], peaks()[2], peaks()[3]
+    hbm = peaks()[0]
+    gemm_ms, gemm_n = kt["refresh_gemm"]
+    flops = 2.0 * L * d * B
+    achieved = flops / (gemm_ms / max(gemm_n, 1) / 1e3) / 1e12
+    step_bytes = U * d * (2 * 2 + 2 * 8) + 2 * B * d * 4 + B * sl[0].shape[1] * 5
+    line = {
+        "metric": METRIC + " [C5 shard emulation]", "value": round(B / (ms / 1e3), 1), "unit": UNIT, "n_gpus": 1,
+        "emulates_n_gpus": c["world"], "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16 W + fp32 Adam state; bf16 tcgen05 refresh + re-rank on the bf16 rows", "data": "synthetic",
+        "config": {"workload": c["workload"], "n_labels_total": c["L_total"], "labels_shard": L, "dim": d,
+                   "global_batch": B, "k_p": c["k_p"], "k_h": c["k_h"], "k_i": c["k_i"], "k_r": c["k_r"],
+                   "slate": int(sl[0].shape[1]), "tau_r": 1, "optimizer": "adam", "owned_slots": int(own.numel()),
+                   "unique_rows": U},
+        "phases_ms_per_step": {k: round(v, 3) for k, v in ph.items()},
+        "refresh_mips_qps_shard": round(B / (ph["refresh"] / 1e3), 1),
+        "composite_tau_r5_samples_per_s": round(B / ((ph["sample"] + ph["step"] + ph["refresh"] / 5) / 1e3), 1),
+        "roofline": {"bound": "tensor", "kernel": "refresh_tc_kernel threshold pass", "achieved": round(achieved, 2),
+                     "peak": tf_sus, "unit": "TFLOP/s", "frac": round(achieved / tf_sus, 4),
+                     "launch_ms": round(gemm_ms / max(gemm_n, 1), 3)},
+        "roofline_step": {"bound": "hbm", "achieved": round(step_bytes / (ph["step"] / 1e3) / 1e9, 1), "peak": hbm,
+                          "unit": "GB/s", "frac": round(step_bytes / (ph["step"] / 1e3) / 1e9 / hbm, 4),
+                          "algorithmic": f"U*d*(2*2 + 2*8) + 2*B*d*4 + B*S*5 = {step_bytes:.3e} B (U={U})"},
+        "memory_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ CPU arm
 def cpu_workload(rng, q_sample):
     """Host data for the CPU path: W (L x d fp32), one batch of B rows."""
@@ -442,6 +558,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=128)
+    ap.add_argument("--config", default="c4", choices=["c4", "c5shard"],
+                    help="c4 (default, the headline line) or c5shard (120M-label config, one of 8 shards)")
     ap.add_argument("--refresh-sms", type=int, default=0,
                     help="SM budget of the refresh running concurrently with training on a side stream (0 = serial)")
     args = ap.parse_args()
@@ -449,6 +567,8 @@ def main():
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c5shard":
+        run_c5shard(args)
     else:
         run_ours(args)
 

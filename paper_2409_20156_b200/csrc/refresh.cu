@@ -20,6 +20,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(kRrWarps * 32) rerank_kernel(const float* Q, c
   }
 }
 
-// TMA-fed re-rank (kc <= 128): CTA per query, a producer warp whose lanes
+// TMA-fed re-rank (kc <= 512): CTA per query, a producer warp whose lanes
 // bulk-copy their candidate's fp32 row, ch floats at a time, into a 2-stage
 // ring (32 rows x ch floats, pitch 4 words mod 32: conflict-free LDS.128), and
 // a consumer warp whose lane t runs candidate t's sequential fmaf chain over
@@ -932,18 +933,25 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
   // the re-rank scores the fp32 snapshot, or the bf16 one when no fp32 copy is given (bf16 W)
   const bool rr_bf16 = wf == nullptr;
   const void* wl = rr_bf16 ? static_cast<const void*>(wb) : static_cast<const void*>(wf);
-  if (rerank && (rr_bf16 || (!legacy_rr && kk <= 128 && d % 64 == 0 && (reinterpret_cast<uintptr_t>(wf) & 15) == 0))) {
-    if (kk > 128) return set_error(ASTRA_ERR_CONFIG, "BF16_RERANK from bf16 labels needs k' <= 128 (k <= 85)");
+  if (rerank && (rr_bf16 || (!legacy_rr && kk <= 512 && d % 64 == 0 && (reinterpret_cast<uintptr_t>(wf) & 15) == 0))) {
+    if (kk > 512) return set_error(ASTRA_ERR_CONFIG, "BF16_RERANK from bf16 labels needs k' <= 512 (k <= 341)");
+    auto go = [&](auto r_tag) {
+      constexpr int R = decltype(r_tag)::value;
+      return rr_bf16 ? launch_rerank_tma<R, true>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st)
+                     : launch_rerank_tma<R, false>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores,
+                                                   st);
+    };
     int rc;
     if (kk <= 32)
-      rc = rr_bf16 ? launch_rerank_tma<1, true>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st)
-                   : launch_rerank_tma<1, false>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+      rc = go(std::integral_constant<int, 1>());
     else if (kk <= 64)
-      rc = rr_bf16 ? launch_rerank_tma<2, true>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st)
-                   : launch_rerank_tma<2, false>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+      rc = go(std::integral_constant<int, 2>());
+    else if (kk <= 128)
+      rc = go(std::integral_constant<int, 4>());
+    else if (kk <= 256)
+      rc = go(std::integral_constant<int, 8>());
     else
-      rc = rr_bf16 ? launch_rerank_tma<4, true>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st)
-                   : launch_rerank_tma<4, false>(qf, wl, d, off, w.rr_cand, nq, kk, k, out_keys, out_ids, out_scores, st);
+      rc = go(std::integral_constant<int, 16>());
     prof.mark("rerank");
     return rc;
   }

@@ -250,7 +250,7 @@ constexpr int tma_ring() { return BF16 ? 32 : 16; }
 template <int NV, bool BF16>
 constexpr size_t tma_fwd_smem(int S) {
   return static_cast<size_t>(tma_ring<BF16>()) * NV * 128 * (BF16 ? 2 : 4) + 2 * 8 * tma_ring<BF16>() +
-         static_cast<size_t>(S) * 4 + 64;
+         static_cast<size_t>(S) * 8 + 64;
 }
 
 template <int NV, bool BF16>
@@ -269,19 +269,29 @@ __global__ void __launch_bounds__(kTmaThreads, 3) slot_forward_tma(FwdArgs a) {
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t* row_ids = a.ids + static_cast<size_t>(b) * a.S;
+  // the row's ids -> smem with every thread (independent loads), then warp 0
+  // compacts the owned slots in slot order (label-sharded W: others are
+  // skipped): own[i] = slot, own_loc[i] = local W row, read by the producer
+  // from shared memory (a global load per issued row serialised it).
+  int32_t* own_loc = own + a.S;
+  for (int sl = threadIdx.x; sl < a.S; sl += kTmaThreads) own_loc[sl] = row_ids[sl];
+  __syncthreads();
   if (warp == 0) {
-    // owned slots of this row, in slot order (label-sharded W: others are skipped)
     int n = 0;
     for (int s0 = 0; s0 < a.S; s0 += 32) {
       const int sl = s0 + lane;
-      bool o = false;
-      if (sl < a.S) {
-        const int64_t loc = static_cast<int64_t>(row_ids[sl]) - a.off;
-        o = loc >= 0 && loc < a.Lloc;
-      }
+      int64_t loc = -1;
+      if (sl < a.S) loc = static_cast<int64_t>(own_loc[sl]) - a.off;
+      const bool o = loc >= 0 && loc < a.Lloc;
       const unsigned m = __ballot_sync(0xffffffffu, o);
-      if (o) own[n + __popc(m & ((1u << lane) - 1u))] = sl;
+      __syncwarp();  // every lane has read own_loc[s0..s0+31] before it is overwritten below
+      if (o) {
+        const int at = n + __popc(m & ((1u << lane) - 1u));
+        own[at] = sl;
+        own_loc[at] = static_cast<int32_t>(loc);
+      }
       n += __popc(m);
+      __syncwarp();
     }
     if (lane == 0) {
       s_nown = n;
@@ -302,8 +312,7 @@ __global__ void __launch_bounds__(kTmaThreads, 3) slot_forward_tma(FwdArgs a) {
         const int r = i % RING;
         mbar_wait(&empty[r], ((i / RING) & 1) ^ 1);
         mbar_expect_tx(&full[r], ROWB);
-        const int64_t loc = static_cast<int64_t>(row_ids[own[i]]) - a.off;
-        bulk_g2s(ring + r * ROWB, Wb + static_cast<size_t>(loc) * ROWB, ROWB, &full[r]);
+        bulk_g2s(ring + r * ROWB, Wb + static_cast<size_t>(own_loc[i]) * ROWB, ROWB, &full[r]);
       }
     }
   } else {
@@ -855,11 +864,22 @@ __global__ void __launch_bounds__(kUpdThreads) label_update_vec(UpdArgs a) {
 // gradient from the L2-resident embeddings (same ascending-slot order and
 // roundings as label_update_vec), then take the row from the ring, apply the
 // update and store it. W is read and written once per touched row.
+// Ring geometry of the update: one entry = the W row (+ the Adam m and v rows).
+template <int NV, bool BF16, bool ADAM>
+struct UpdRing {
+  static constexpr uint32_t WB = NV * 128 * (BF16 ? 2 : 4);
+  static constexpr uint32_t MB = ADAM ? NV * 128 * 4 : 0;
+  static constexpr uint32_t ENTRY = WB + 2 * MB;
+  static constexpr int RING = ADAM ? 8 : (BF16 ? 32 : 16);
+  static constexpr size_t smem() { return static_cast<size_t>(RING) * ENTRY + 2 * 8 * RING; }
+};
+
 template <int NV, bool BF16, bool ADAM>
 __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(UpdArgs a) {
   constexpr int d = NV * 128;
-  constexpr int RING = tma_ring<BF16>();
-  constexpr uint32_t ROWB = d * (BF16 ? 2 : 4);
+  using RG = UpdRing<NV, BF16, ADAM>;
+  constexpr int RING = RG::RING;
+  constexpr uint32_t ROWB = RG::ENTRY;
   extern __shared__ __align__(128) unsigned char usm[];
   unsigned char* ring = usm;
   uint64_t* full = reinterpret_cast<uint64_t*>(usm + RING * ROWB);
@@ -880,13 +900,25 @@ __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(Up
   }
   __syncthreads();
   if (warp == kTmaConsumers) {
-    if (lane == 0) {
-      const unsigned char* Wb = static_cast<const unsigned char*>(a.W);
-      for (int i = 0; i < n_mine; ++i) {
-        const int r = i % RING;
-        mbar_wait(&empty[r], ((i / RING) & 1) ^ 1);
-        mbar_expect_tx(&full[r], ROWB);
-        bulk_g2s(ring + r * ROWB, Wb + static_cast<size_t>(a.uniq[u0 + i]) * ROWB, ROWB, &full[r]);
+    // producer warp: 32 label ids per coalesced load, lane 0 issues the copies
+    const unsigned char* Wb = static_cast<const unsigned char*>(a.W);
+    for (int i0 = 0; i0 < n_mine; i0 += 32) {
+      const int32_t l_lane = i0 + lane < n_mine ? a.uniq[u0 + i0 + lane] : 0;
+      const int nb = min(32, n_mine - i0);
+      for (int jj = 0; jj < nb; ++jj) {
+        const size_t l = static_cast<size_t>(__shfl_sync(0xffffffffu, l_lane, jj));
+        if (lane == 0) {
+          const int i = i0 + jj, r = i % RING;
+          mbar_wait(&empty[r], ((i / RING) & 1) ^ 1);
+          mbar_expect_tx(&full[r], ROWB);
+          unsigned char* dst = ring + r * ROWB;
+          bulk_g2s(dst, Wb + l * RG::WB, RG::WB, &full[r]);
+          if constexpr (ADAM) {
+            bulk_g2s(dst + RG::WB, a.m + l * d, RG::MB, &full[r]);
+            bulk_g2s(dst + RG::WB + RG::MB, a.v + l * d, RG::MB, &full[r]);
+          }
+        }
+        __syncwarp();
       }
     }
     return;
@@ -897,14 +929,6 @@ __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(Up
     const uint32_t start = a.offsets[l], n = a.counts[l];
     const int32_t reg = sort_segment(a, start, n, lane);
     const size_t row = static_cast<size_t>(l) * d;
-    float4 m4[ADAM ? NV : 1], v4[ADAM ? NV : 1];
-    if constexpr (ADAM) {  // moment rows: loads issued before the gradient sum
-#pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        m4[q] = *reinterpret_cast<const float4*>(a.m + row + q * 128 + lane * 4);
-        v4[q] = *reinterpret_cast<const float4*>(a.v + row + q * 128 + lane * 4);
-      }
-    }
     float4 g[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) g[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -955,6 +979,14 @@ __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(Up
                            __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
       } else {
         p[q] = *reinterpret_cast<const float4*>(ring + r * ROWB + (q * 128 + lane * 4) * 4);
+      }
+    }
+    float4 m4[ADAM ? NV : 1], v4[ADAM ? NV : 1];
+    if constexpr (ADAM) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        m4[q] = *reinterpret_cast<const float4*>(ring + r * ROWB + RG::WB + (q * 128 + lane * 4) * 4);
+        v4[q] = *reinterpret_cast<const float4*>(ring + r * ROWB + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
       }
     }
     __syncwarp();
@@ -1045,7 +1077,14 @@ int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
   static const bool legacy = getenv("ASTRA_STEP_LEGACY_UPD") != nullptr;
   if (!legacy && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
     const int grid = (ADAM ? 2 : 3) * num_sms();
-    const size_t smem = static_cast<size_t>(tma_ring<BF16>()) * a.d * (BF16 ? 2 : 4) + 2 * 8 * tma_ring<BF16>();
+    size_t smem = 0;
+    switch (nv) {
+      case 1: smem = UpdRing<1, BF16, ADAM>::smem(); break;
+      case 2: smem = UpdRing<2, BF16, ADAM>::smem(); break;
+      case 4: smem = UpdRing<4, BF16, ADAM>::smem(); break;
+      case 6: smem = UpdRing<6, BF16, ADAM>::smem(); break;
+      case 8: smem = UpdRing<8, BF16, ADAM>::smem(); break;
+    }
     switch (nv) {
       case 1: launch_upd_tma<1, BF16, ADAM>(a, grid, smem, st); break;
       case 2: launch_upd_tma<2, BF16, ADAM>(a, grid, smem, st); break;
