@@ -464,25 +464,78 @@ __global__ void f32_to_bf16_kernel(const float* src, uint16_t* dst, int64_t n) {
 
 // ------------------------------------------------------------- select (two-pass refresh)
 
+// The j-th largest of n 32-bit values (j >= 1, duplicates counted) by an
+// MSB-first radix select with 8-bit digits: 4 passes over the values, each
+// building a 256-bin histogram of the values matching the prefix so far in
+// the warp's shared memory. get(i, &v) returns false for values to ignore.
+template <class Get>
+__device__ __forceinline__ uint32_t warp_kth_largest(Get get, int n, int j, uint32_t* hist, int lane) {
+  uint32_t prefix = 0, mask = 0;
+  int need = j;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int b = lane; b < 256; b += 32) hist[b] = 0u;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      uint32_t x;
+      if (get(i, x) && (x & mask) == prefix) atomicAdd(&hist[(x >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    // lane l owns bins 255-8l .. 248-8l (descending); inclusive scan from the top
+    uint32_t c[8], sum = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      c[t] = hist[255 - 8 * lane - t];
+      sum += c[t];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - sum;
+    const unsigned owner = __ballot_sync(0xffffffffu, excl < static_cast<uint32_t>(need) &&
+                                                          incl >= static_cast<uint32_t>(need));
+    int digit = 0, before = 0;
+    if (owner) {
+      const int src = __ffs(owner) - 1;
+      uint32_t cum = __shfl_sync(0xffffffffu, excl, src);
+      int dd = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t ct = __shfl_sync(0xffffffffu, c[t], src);
+        if (cum < static_cast<uint32_t>(need) && cum + ct >= static_cast<uint32_t>(need) && dd == 0) {
+          digit = 255 - 8 * src - t;
+          before = static_cast<int>(cum);
+          dd = 1;
+        }
+        cum += ct;
+      }
+    } else {
+      return 0u;  // fewer than j values
+    }
+    need -= before;
+    prefix |= static_cast<uint32_t>(digit) << shift;
+    mask |= 255u << shift;
+    __syncwarp();
+  }
+  return prefix;
+}
+
 // Warp per query: the j-th largest of the query's 64-label group maxima
 // (orderable bits, gmax [nq][n_groups]) by an MSB-first radix select. Each of
 // the top-j group maxima is a distinct label, so at least j sampled labels
 // score >= it: tau_keys[q] = (T << 32) admits every key with score >= T.
 __global__ void __launch_bounds__(256) tau_select_kernel(const uint32_t* gmax, int64_t nq, int n_groups, int j,
                                                          uint64_t* tau_keys) {
-  const int lane = threadIdx.x & 31;
-  const int64_t q = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  __shared__ uint32_t hist[8][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * 8 + warp;
   if (q >= nq) return;  // warp-uniform
   const uint32_t* v = gmax + static_cast<size_t>(q) * n_groups;
   uint32_t T = 0;
-  if (n_groups >= j) {
-    for (int b = 31; b >= 0; --b) {
-      const uint32_t c = T | (1u << b);
-      int n = 0;
-      for (int i = lane; i < n_groups; i += 32) n += __ldg(v + i) >= c;
-      if (warp_sum(n) >= j) T = c;
-    }
-  }
+  if (n_groups >= j)
+    T = warp_kth_largest([&](int i, uint32_t& x) { x = __ldg(v + i); return true; }, n_groups, j, hist[warp], lane);
   if (lane == 0) tau_keys[q] = static_cast<uint64_t>(T) << 32;
 }
 
@@ -494,7 +547,7 @@ __global__ void __launch_bounds__(256) tau_select_kernel(const uint32_t* gmax, i
 // exist and no list overflowed (every key of the true top-k is >= the k-th
 // candidate >= the threshold, hence a candidate); otherwise the query is
 // flagged for the exact running-top-k fallback.
-constexpr int kSelWarps = 4, kSelSmall = 256;
+constexpr int kSelWarps = 4, kSelSmall = 256, kSelPos = 128;
 
 __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* cand, const int32_t* cand_cnt,
                                                                 int n_parts, int cand_cap, int64_t nq,
@@ -517,13 +570,20 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
   bool fail = overflow || total > sel_max;
   if (!fail) {
     const int64_t p0 = pos_indptr[q], np = pos_indptr[q + 1] - p0;
+    // the query's positives in shared memory (binary searches there, not in L2)
+    __shared__ int32_t sel_pos[kSelWarps][kSelPos];
+    const bool pos_smem = np <= kSelPos;
+    if (pos_smem)
+      for (int e = lane; e < np; e += 32) sel_pos[warp][e] = pos_ids[p0 + e];
+    __syncwarp();
+    const int32_t* P = pos_smem ? sel_pos[warp] : pos_ids + p0;
     int o = 0, valid = 0;
     for (int p = 0; p < n_parts; ++p) {
       const int c = min(cand_cnt[static_cast<size_t>(p) * nq + q], cand_cap);
       const uint64_t* src = cand + (static_cast<size_t>(p) * nq + q) * cand_cap;
       for (int e = lane; e < c; e += 32) {
         uint64_t v = src[e];
-        if (np > 0 && sorted_contains(pos_ids + p0, np, key_id(v))) v = 0ull;
+        if (np > 0 && sorted_contains(P, np, key_id(v))) v = 0ull;
         S[o + e] = v;
         valid += v != 0ull;
       }
@@ -535,16 +595,14 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
   if (fail) return;
   __syncwarp();
   // k-th largest score bits T: count(score >= T) >= k > count(score >= T + 1)
-  uint32_t T = 0;
-  for (int b = 31; b >= 0; --b) {
-    const uint32_t c = T | (1u << b);
-    int n = 0;
-    for (int i = lane; i < total; i += 32) {
-      const uint64_t v = S[i];
-      n += v != 0ull && static_cast<uint32_t>(v >> 32) >= c;
-    }
-    if (warp_sum(n) >= k) T = c;
-  }
+  __shared__ uint32_t sel_hist[kSelWarps][256];
+  const uint32_t T = warp_kth_largest(
+      [&](int i, uint32_t& x) {
+        const uint64_t v = S[i];
+        x = static_cast<uint32_t>(v >> 32);
+        return v != 0ull;
+      },
+      total, k, sel_hist[warp], lane);
   // warp-aggregated compaction of the keys with score >= T (k plus score ties)
   int nr = 0;
   for (int i0 = 0; i0 < total; i0 += 32) {
