@@ -176,6 +176,14 @@ int astra_sample_slates(uint64_t seed, uint32_t epoch, uint32_t step, const int6
  *   grad_emb   B x d fp32 out (partial over this shard's slots)
  *   loss_out   1 fp64 out: sum of this shard's slate loss terms (fp64)
  *   status     int32[ASTRA_STATUS_WORDS] out (zeroed by the call)
+ *   factors_out B x S fp32 out (d(loss)/d(score) per slot) or NULL
+ *   w_absmax   1 fp32 in/out or NULL: a running upper bound on max|W| of this
+ *              shard, kept current by the call (every updated row folds its
+ *              new |values| in). With it, the call can prove up front that
+ *              no gradient and no grad_emb entry can overflow, and then runs
+ *              the L2-chunked fused step (gather of chunk p + update of chunk
+ *              p-1 per phase of one persistent kernel); without it, or when
+ *              the proof fails, it runs the two-pass schedule.
  *   lr, weight_decay, betas, eps are host doubles: SGD rounds lr/wd to fp32
  *   like np.float32(lr) (classifiers.py:82); Adam derives its step size in
  *   double like torch.optim.SparseAdam.
@@ -192,7 +200,7 @@ int astra_slate_step(const float* emb, const float* keep, const int32_t* ids, co
                      int64_t n_labels_local, int64_t label_offset, double lr, double weight_decay,
                      double adam_beta1, double adam_beta2, double adam_eps, int64_t adam_step,
                      float* grad_emb, double* loss_out, int32_t* status, float* factors_out,
-                     void* workspace, size_t workspace_bytes, void* stream);
+                     float* w_absmax, void* workspace, size_t workspace_bytes, void* stream);
 
 /* apply_classifier_updates_arrays(bank, ids, grads, lr, wd)  classifiers.py:75-82
  * ids (U, unique, local row index) and grads (U x d) on device. Raises

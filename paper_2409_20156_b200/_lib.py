@@ -36,7 +36,7 @@ _SIGS = {
     "astra_sample_slates": ([u64, u32, u32, p, i32, p, p, p, i32, i32, p, p, i32, i32, i32, i64, i32, i32, p, p, p, p, p], i32),
     "astra_step_workspace_size": ([i32, i32, i32, i64], sz),
     "astra_slate_step": ([p, p, p, p, p, i64, p, i64, p, i32, i32, i32, p, i32, p, p, i32, i64, i64, f64, f64, f64, f64, f64,
-                          i64, p, p, p, p, p, sz, p], i32),
+                          i64, p, p, p, p, p, p, sz, p], i32),
     "astra_apply_updates": ([p, i32, i64, i32, p, p, i64, f32, f32, p, p], i32),
     "astra_stream_sync": ([p], i32),
 }

@@ -68,7 +68,7 @@ int sample_slates(uint64_t, uint32_t, uint32_t, const int64_t*, int, const int64
 size_t step_workspace_size(int, int, int, int64_t);
 int slate_step(const float*, const float*, const int32_t*, const int8_t*, const int8_t*, int64_t, const float*,
                int64_t, const float*, int, int, int, void*, int, float*, float*, int, int64_t, int64_t, double, double,
-               double, double, double, int64_t, float*, double*, int32_t*, float*, void*, size_t, cudaStream_t);
+               double, double, double, int64_t, float*, double*, int32_t*, float*, float*, void*, size_t, cudaStream_t);
 int apply_updates(void*, int, int64_t, int, const int64_t*, const float*, int64_t, float, float, int32_t*,
                   cudaStream_t);
 
@@ -165,12 +165,12 @@ int astra_slate_step(const float* emb, const float* keep, const int32_t* ids, co
                      const float* factors_in, int B, int S_, int d, void* W, int w_dtype, float* adam_m,
                      float* adam_v, int optimizer, int64_t n_labels_local, int64_t label_offset, double lr,
                      double weight_decay, double adam_beta1, double adam_beta2, double adam_eps, int64_t adam_step,
-                     float* grad_emb, double* loss_out, int32_t* status, float* factors_out, void* workspace,
-                     size_t workspace_bytes, void* stream) {
+                     float* grad_emb, double* loss_out, int32_t* status, float* factors_out, float* w_absmax,
+                     void* workspace, size_t workspace_bytes, void* stream) {
   return slate_step(emb, keep, ids, y, origin, origin_row_stride, weights, weights_row_stride, factors_in, B, S_, d,
                     W, w_dtype, adam_m, adam_v, optimizer, n_labels_local, label_offset, lr, weight_decay,
-                    adam_beta1, adam_beta2, adam_eps, adam_step, grad_emb, loss_out, status, factors_out, workspace,
-                    workspace_bytes, S(stream));
+                    adam_beta1, adam_beta2, adam_eps, adam_step, grad_emb, loss_out, status, factors_out, w_absmax,
+                    workspace, workspace_bytes, S(stream));
 }
 
 int astra_apply_updates(void* W, int w_dtype, int64_t n_labels, int d, const int64_t* ids, const float* grads,

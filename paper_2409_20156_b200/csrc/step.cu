@@ -21,6 +21,8 @@
 // case; otherwise a check pass (label_check) runs first.
 #include <limits.h>
 #include <math.h>
+
+#include <cmath>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -655,7 +657,20 @@ struct UpdArgs {
   float lr, wd;
   float c1, c2, eps, neg_step;  // Adam: fp32(1-b1), fp32(1-b2), eps, fp32(-lr*sqrt(bc2)/bc1)
   int32_t* status;
+  float* w_absmax;  // running max|W| bound kept current by every update kernel (or null)
 };
+
+// Fold a warp's max |new W| into the running bound (non-negative floats order as bits).
+__device__ __forceinline__ void push_wmax(const UpdArgs& a, float wmax, int lane) {
+  if (!a.w_absmax) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+  if (lane == 0 && wmax > 0.0f) atomicMax(reinterpret_cast<unsigned*>(a.w_absmax), __float_as_uint(wmax));
+}
+
+__device__ __forceinline__ float absmax4(float4 v) {
+  return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+}
 
 // Sort the label's slot indices ascending. Segments <= 32 stay in a register
 // (returned); longer ones are rank-sorted into perm2.
@@ -770,6 +785,7 @@ __global__ void __launch_bounds__(kUpdThreads) label_update_vec(UpdArgs a) {
   const uint32_t U = *a.U;
   constexpr int d = NV * 128;
   const uint32_t warps = gridDim.x * (kUpdThreads / 32);
+  float wmax = 0.0f;
   for (uint32_t u = blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5); u < U; u += warps) {
     const int32_t l = a.uniq[u];
     const uint32_t start = a.offsets[l], n = a.counts[l];
@@ -853,8 +869,10 @@ __global__ void __launch_bounds__(kUpdThreads) label_update_vec(UpdArgs a) {
       } else {
         *reinterpret_cast<float4*>(static_cast<float*>(a.W) + el) = np;
       }
+      wmax = fmaxf(wmax, absmax4(np));
     }
   }
+  push_wmax(a, wmax, lane);
 }
 
 // TMA-fed SGD update (the default for d % 128 == 0): each CTA owns a
@@ -923,6 +941,7 @@ __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(Up
     }
     return;
   }
+  float wmax = 0.0f;
   for (int i = warp; i < n_mine; i += kTmaConsumers) {
     const int r = i % RING;
     const int32_t l = a.uniq[u0 + i];
@@ -1016,8 +1035,444 @@ __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(Up
       } else {
         *reinterpret_cast<float4*>(static_cast<float*>(a.W) + el) = np;
       }
+      wmax = fmaxf(wmax, absmax4(np));  // (bf16: the bound holds for the rounded value too)
     }
   }
+  push_wmax(a, wmax, lane);
+}
+
+// ================================================================ fused step
+// One persistent cooperative kernel per minibatch that keeps the rows it
+// gathers L2-resident until they are updated: the label range is cut into C
+// chunks whose touched rows (~24 MB) fit in L2 with room to spare, and phase p
+// runs the forward (gather, scores, factors, loss, grad_emb) of every slot whose
+// label lies in chunk p AND the update of chunk p-1 (rows gathered in the
+// previous phase: L2 hits), separated by grid barriers. DRAM then sees each
+// touched row read once and written once, the formula's minimum.
+//
+// Determinism is unchanged: a warp owns one batch row and accumulates its
+// grad_emb in registers over (chunk asc, slot asc); labels sum their gradient
+// in ascending b*S+s order as label_update does.
+// Finiteness (classifiers.py:79-80, encoder.py:145-146: nothing is written when
+// a gradient is non-finite) is proven up front from bounds: with
+// S_f = sum over owned slots of (1 + |weight|) >= sum |factor|, every label
+// gradient is <= S_f * max|emb| and every grad_emb entry <= S_f * max|W|
+// (max|W| a running bound kept by the caller, updated here). Without the proof
+// (or without the bound) the same kernel runs the two-pass schedule: all
+// forwards, a check of every gradient, then the updates.
+
+constexpr int kFusedWarps = 8;
+constexpr int kFusedThreads = 32 * kFusedWarps;
+constexpr int kMaxChunks = 127;
+constexpr double kFusedSafe = 1e30;
+
+struct FusedArgs {
+  FwdArgs f;
+  UpdArgs u;
+  int C;
+  int64_t Lc;
+  const uint32_t* uc;        // [C+1] bounds of chunk c in uniq
+  const int32_t* row_slots;  // [B][S] owned slots of row b, by (chunk, slot)
+  const int32_t* row_locs;   // [B][S] their local W rows
+  const int32_t* row_cofs;   // [B][C+1] offsets into row_slots
+  float* w_absmax;           // running max|W| bound (in/out) or null
+  unsigned* bar;             // grid barrier counter (zeroed before launch)
+  double* sf_acc;            // sum over owned slots of (1 + |weight|)
+  unsigned* emax_acc;        // max|emb| (float bits; +inf if non-finite)
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Forward of row b's owned slots [j0, j1) of row_slots (UNR rows in flight).
+template <int NV, bool BF16>
+__device__ __forceinline__ void fused_fwd(const FusedArgs& A, int b, int j0, int j1, const float4 (&e)[NV],
+                                          float4 (&g)[NV], double& lsum, double& fabs_sum, float& pend_sc,
+                                          float& pend_pt, float& pend_wn, int& c_pend, int lane) {
+  const FwdArgs& a = A.f;
+  constexpr int d = NV * 128;
+  constexpr int UNR = NV <= 4 ? 8 : 4;
+  const int32_t* rs = A.row_slots + static_cast<size_t>(b) * a.S;
+  const int32_t* rl = A.row_locs + static_cast<size_t>(b) * a.S;
+  for (int j = j0; j < j1; j += UNR) {
+    int sl[UNR];
+    float4 w[UNR][NV];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      sl[u] = j + u < j1 ? rs[j + u] : -1;
+      if (sl[u] >= 0) {
+        const int64_t loc = rl[j + u];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) w[u][i] = load_w4<BF16>(a.W, static_cast<size_t>(loc) * d + i * 128 + lane * 4);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (sl[u] < 0) continue;  // warp-uniform
+      float acc = 0.0f;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        acc = fmaf(w[u][i].x, e[i].x, acc);
+        acc = fmaf(w[u][i].y, e[i].y, acc);
+        acc = fmaf(w[u][i].z, e[i].z, acc);
+        acc = fmaf(w[u][i].w, e[i].w, acc);
+      }
+      acc = warp_sum(acc);
+      float pt, wn;
+      const float f = slot_factor_only(a, b, sl[u], acc, &pt, &wn);
+      if (lane == c_pend) {
+        pend_sc = acc;
+        pend_pt = pt;
+        pend_wn = wn;
+      }
+      if (++c_pend == 32) {
+        lsum += slot_loss(pend_sc, pend_pt, pend_wn);
+        c_pend = 0;
+      }
+      if (lane == 0) {
+        __stcg(a.factors + static_cast<size_t>(b) * a.S + sl[u], f);
+        fabs_sum += static_cast<double>(fabsf(f));
+      }
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        g[i].x = fmaf(f, w[u][i].x, g[i].x);
+        g[i].y = fmaf(f, w[u][i].y, g[i].y);
+        g[i].z = fmaf(f, w[u][i].z, g[i].z);
+        g[i].w = fmaf(f, w[u][i].w, g[i].w);
+      }
+    }
+  }
+}
+
+// Gradient of unique label index uq (ascending b*S+s order, separate roundings
+// as label_update), then (unless CHECK) the SGD / Adam update of its row.
+// Returns false if a gradient entry is non-finite. wmax tracks max|W new|.
+template <int NV, bool BF16, bool ADAM, bool CHECK>
+__device__ __forceinline__ bool fused_upd(const UpdArgs& a, uint32_t uq, float& wmax, int lane) {
+  constexpr int d = NV * 128;
+  const int32_t l = a.uniq[uq];
+  const uint32_t start = a.offsets[l], n = a.counts[l];
+  const int32_t reg = sort_segment(a, start, n, lane);
+  const size_t row = static_cast<size_t>(l) * d;
+  float4 p[NV];
+  if constexpr (!CHECK) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if constexpr (BF16) {
+        const uint2 q = __ldcg(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(a.W) + row + i * 128 + lane * 4));
+        p[i] = make_float4(__uint_as_float(q.x << 16), __uint_as_float(q.x & 0xFFFF0000u),
+                           __uint_as_float(q.y << 16), __uint_as_float(q.y & 0xFFFF0000u));
+      } else {
+        p[i] = __ldcg(reinterpret_cast<const float4*>(static_cast<const float*>(a.W) + row + i * 128 + lane * 4));
+      }
+    }
+  }
+  float4 g[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t j = 0; j < n; ++j) {
+    const int32_t s0 = seg_slot(a, start, n, reg, j);
+    const float f0 = __ldcg(a.factors + s0);
+    const float* e0 = a.emb + static_cast<size_t>(s0 / a.S) * d + lane * 4;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float4 x0 = *reinterpret_cast<const float4*>(e0 + i * 128);
+      g[i].x = __fadd_rn(g[i].x, __fmul_rn(f0, x0.x));
+      g[i].y = __fadd_rn(g[i].y, __fmul_rn(f0, x0.y));
+      g[i].z = __fadd_rn(g[i].z, __fmul_rn(f0, x0.z));
+      g[i].w = __fadd_rn(g[i].w, __fmul_rn(f0, x0.w));
+    }
+  }
+  if constexpr (CHECK) {
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) bad |= !(isfinite(g[i].x) && isfinite(g[i].y) && isfinite(g[i].z) && isfinite(g[i].w));
+    return !__any_sync(0xffffffffu, bad);
+  } else {
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const size_t el = row + i * 128 + lane * 4;
+    float4 np;
+    if constexpr (ADAM) {
+      float4 m4 = *reinterpret_cast<float4*>(a.m + el), v4 = *reinterpret_cast<float4*>(a.v + el);
+      np.x = upd_elem<true>(a, p[i].x, g[i].x, &m4.x, &v4.x);
+      np.y = upd_elem<true>(a, p[i].y, g[i].y, &m4.y, &v4.y);
+      np.z = upd_elem<true>(a, p[i].z, g[i].z, &m4.z, &v4.z);
+      np.w = upd_elem<true>(a, p[i].w, g[i].w, &m4.w, &v4.w);
+      *reinterpret_cast<float4*>(a.m + el) = m4;
+      *reinterpret_cast<float4*>(a.v + el) = v4;
+    } else {
+      np.x = upd_elem<false>(a, p[i].x, g[i].x, nullptr, nullptr);
+      np.y = upd_elem<false>(a, p[i].y, g[i].y, nullptr, nullptr);
+      np.z = upd_elem<false>(a, p[i].z, g[i].z, nullptr, nullptr);
+      np.w = upd_elem<false>(a, p[i].w, g[i].w, nullptr, nullptr);
+    }
+    if constexpr (BF16) {
+      uint2 q;
+      q.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
+      q.y = static_cast<uint32_t>(f32_to_bf16_bits(np.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.w)) << 16);
+      *reinterpret_cast<uint2*>(static_cast<uint16_t*>(a.W) + el) = q;
+      np = make_float4(bf16_bits_to_f32(static_cast<uint16_t>(q.x)), bf16_bits_to_f32(static_cast<uint16_t>(q.x >> 16)),
+                       bf16_bits_to_f32(static_cast<uint16_t>(q.y)), bf16_bits_to_f32(static_cast<uint16_t>(q.y >> 16)));
+    } else {
+      *reinterpret_cast<float4*>(static_cast<float*>(a.W) + el) = np;
+    }
+    wmax = fmaxf(wmax, fmaxf(fmaxf(fabsf(np.x), fabsf(np.y)), fmaxf(fabsf(np.z), fabsf(np.w))));
+  }
+  return true;
+  }
+}
+
+template <int NV, bool BF16, bool ADAM>
+__global__ void __launch_bounds__(kFusedThreads, 1) step_fused_kernel(FusedArgs A) {
+  const FwdArgs& a = A.f;
+  constexpr int d = NV * 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t NW = static_cast<int64_t>(gridDim.x) * kFusedWarps;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kFusedWarps + warp;
+  const int b = static_cast<int>(gw);
+  const bool has_row = gw < a.B;
+  unsigned gen = 0;
+  __shared__ double s_sf[kFusedWarps];
+  __shared__ float s_em[kFusedWarps];
+
+  // ---- phase 0: the finiteness bounds
+  float4 e[NV];
+  float emax = 0.0f;
+  double sf = 0.0;
+  if (has_row) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      e[i] = *reinterpret_cast<const float4*>(a.emb + static_cast<size_t>(b) * d + i * 128 + lane * 4);
+      emax = fmaxf(emax, fmaxf(fmaxf(fabsf(e[i].x), fabsf(e[i].y)), fmaxf(fabsf(e[i].z), fabsf(e[i].w))));
+      if (!(isfinite(e[i].x) && isfinite(e[i].y) && isfinite(e[i].z) && isfinite(e[i].w))) emax = INFINITY;
+    }
+    const int j1 = A.row_cofs[static_cast<size_t>(b) * (A.C + 1) + A.C];
+    const int32_t* rs = A.row_slots + static_cast<size_t>(b) * a.S;
+    for (int j = lane; j < j1; j += 32) {
+      const float wt = a.weights[b * a.weights_stride + rs[j]];
+      sf += 1.0 + (isfinite(wt) ? fabs(static_cast<double>(wt)) : INFINITY);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  const float row_emax = emax;
+  sf = warp_sum(sf);
+  if (lane == 0) {
+    s_sf[warp] = sf;
+    s_em[warp] = emax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    float m = 0.0f;
+    for (int w = 0; w < kFusedWarps; ++w) {
+      t += s_sf[w];
+      m = fmaxf(m, s_em[w]);
+    }
+    atomicAdd(A.sf_acc, t);
+    atomicMax(A.emax_acc, __float_as_uint(m));  // non-negative floats order as their bits
+  }
+  grid_barrier(A.bar, ++gen * gridDim.x);
+  const double SF = *reinterpret_cast<volatile double*>(A.sf_acc);
+  const float EM = __uint_as_float(*reinterpret_cast<volatile unsigned*>(A.emax_acc));
+  const float WM = A.w_absmax ? *reinterpret_cast<volatile float*>(A.w_absmax) : INFINITY;
+  const bool safe = isfinite(SF) && isfinite(EM) && isfinite(WM) && SF * static_cast<double>(EM) < kFusedSafe &&
+                    SF * static_cast<double>(WM) < kFusedSafe;
+
+  float4 g[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  double lsum = 0.0, fabs_sum = 0.0;
+  float pend_sc = 0.0f, pend_pt = 0.0f, pend_wn = 0.0f;
+  int c_pend = 0;
+  float wmax = 0.0f;
+  const int32_t* cofs = A.row_cofs + static_cast<size_t>(b) * (A.C + 1);
+
+  if (safe) {
+    // ---- interleaved schedule: forward of chunk p with the update of chunk p-1
+    for (int p = 0; p <= A.C; ++p) {
+      if (p < A.C && has_row) fused_fwd<NV, BF16>(A, b, cofs[p], cofs[p + 1], e, g, lsum, fabs_sum, pend_sc, pend_pt,
+                                                  pend_wn, c_pend, lane);
+      if (p >= 1) {
+        const uint32_t u0 = A.uc[p - 1], u1 = A.uc[p];
+        for (int64_t uq = u0 + gw; uq < u1; uq += NW) fused_upd<NV, BF16, ADAM, false>(A.u, static_cast<uint32_t>(uq), wmax, lane);
+      }
+      if (p < A.C) grid_barrier(A.bar, ++gen * gridDim.x);
+    }
+  } else {
+    // ---- two-pass schedule: every forward, then a check of every gradient, then the updates
+    if (has_row)
+      fused_fwd<NV, BF16>(A, b, cofs[0], cofs[A.C], e, g, lsum, fabs_sum, pend_sc, pend_pt, pend_wn, c_pend, lane);
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) bad |= !(isfinite(g[i].x) && isfinite(g[i].y) && isfinite(g[i].z) && isfinite(g[i].w));
+    if (has_row && __any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.status + ASTRA_STATUS_NONFINITE_GRAD_EMB, 1);
+    grid_barrier(A.bar, ++gen * gridDim.x);
+    const uint32_t U = *A.u.U;
+    bool ok = true;
+    for (int64_t uq = gw; uq < U; uq += NW) ok &= fused_upd<NV, BF16, ADAM, true>(A.u, static_cast<uint32_t>(uq), wmax, lane);
+    if (!ok && lane == 0) atomicExch(a.status + ASTRA_STATUS_NONFINITE_GRAD, 1);
+    grid_barrier(A.bar, ++gen * gridDim.x);
+    const bool go = *reinterpret_cast<volatile int32_t*>(a.status + ASTRA_STATUS_NONFINITE_GRAD) == 0 &&
+                    *reinterpret_cast<volatile int32_t*>(a.status + ASTRA_STATUS_NONFINITE_GRAD_EMB) == 0;
+    if (go)
+      for (int64_t uq = gw; uq < U; uq += NW) fused_upd<NV, BF16, ADAM, false>(A.u, static_cast<uint32_t>(uq), wmax, lane);
+  }
+
+  // ---- per-row outputs (grad_emb in a fixed order: this warp's registers)
+  if (has_row) {
+    if (lane < c_pend) lsum += slot_loss(pend_sc, pend_pt, pend_wn);
+    lsum = warp_sum(lsum);
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      float4 gi = g[i];
+      const size_t el = static_cast<size_t>(b) * d + i * 128 + lane * 4;
+      if (a.keep) {
+        const float4 k4 = *reinterpret_cast<const float4*>(a.keep + el);
+        gi = make_float4(__fmul_rn(gi.x, k4.x), __fmul_rn(gi.y, k4.y), __fmul_rn(gi.z, k4.z), __fmul_rn(gi.w, k4.w));
+      }
+      *reinterpret_cast<float4*>(a.grad_emb + el) = gi;
+      bad |= !(isfinite(gi.x) && isfinite(gi.y) && isfinite(gi.z) && isfinite(gi.w));
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] = 1;
+    if (lane == 0) {
+      a.loss_rows[b] = lsum;
+      a.bound_rows[b] = fabs_sum * static_cast<double>(row_emax);  // the legacy overflow bound (status word 2)
+    }
+  }
+  if (A.w_absmax) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    if (lane == 0 && wmax > 0.0f) atomicMax(reinterpret_cast<unsigned*>(A.w_absmax), __float_as_uint(wmax));
+  }
+}
+
+// Chunk c's [first, last) positions in the sorted unique-label list.
+__global__ void chunk_bounds_kernel(const int32_t* uniq, const uint32_t* U, int64_t Lc, int C, uint32_t* uc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > C) return;
+  const int64_t key = static_cast<int64_t>(c) * Lc;
+  uint32_t lo = 0, hi = *U;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (static_cast<int64_t>(uniq[mid]) < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  uc[c] = lo;
+}
+
+// Warp per row: the row's owned slots bucketed by label chunk, stable in slot order.
+__global__ void __launch_bounds__(256) row_bucket_kernel(const int32_t* ids, int B, int S, int64_t off, int64_t Lloc,
+                                                         int64_t Lc, int C, int32_t* row_slots, int32_t* row_locs,
+                                                         int32_t* row_cofs) {
+  __shared__ int cnt[8][kMaxChunks + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 8 + warp;
+  if (b >= B) return;
+  int* cn = cnt[warp];
+  for (int c = lane; c <= C; c += 32) cn[c] = 0;
+  __syncwarp();
+  const int32_t* rid = ids + static_cast<size_t>(b) * S;
+  for (int s = lane; s < S; s += 32) {
+    const int64_t loc = static_cast<int64_t>(rid[s]) - off;
+    if (loc >= 0 && loc < Lloc) atomicAdd(&cn[loc / Lc], 1);
+  }
+  __syncwarp();
+  if (lane == 0) {  // exclusive scan (C <= 127)
+    int acc = 0;
+    for (int c = 0; c <= C; ++c) {
+      const int t = cn[c];
+      cn[c] = acc;
+      acc += t;
+    }
+  }
+  __syncwarp();
+  for (int c = lane; c <= C; c += 32) row_cofs[static_cast<size_t>(b) * (C + 1) + c] = cn[c];
+  __syncwarp();
+  for (int s0 = 0; s0 < S; s0 += 32) {
+    const int s = s0 + lane;
+    int c = -1;
+    if (s < S) {
+      const int64_t loc = static_cast<int64_t>(rid[s]) - off;
+      if (loc >= 0 && loc < Lloc) c = static_cast<int>(loc / Lc);
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, c);
+    if (c >= 0) {
+      const size_t at = static_cast<size_t>(b) * S + cn[c] + __popc(grp & ((1u << lane) - 1u));
+      row_slots[at] = s;
+      row_locs[at] = static_cast<int32_t>(static_cast<int64_t>(rid[s]) - off);
+    }
+    __syncwarp();
+    if (c >= 0 && lane == __ffs(grp) - 1) cn[c] += __popc(grp);
+    __syncwarp();
+  }
+}
+
+template <int NV, bool BF16, bool ADAM>
+int launch_fused(const FusedArgs& A, cudaStream_t st) {
+  static int grid = 0;
+  auto kern = step_fused_kernel<NV, BF16, ADAM>;
+  if (!grid) {
+    int per_sm = 0;
+    ASTRA_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFusedThreads, 0), "occupancy"));
+    grid = std::max(1, per_sm) * num_sms();
+  }
+  if (static_cast<int64_t>(grid) * kFusedWarps < A.f.B) return ASTRA_ERR_CONFIG;  // caller falls back
+  FusedArgs a = A;
+  void* args[] = {&a};
+  ASTRA_TRY(check_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kFusedThreads), args,
+                                                   0, st),
+                       "launch step_fused"));
+  ASTRA_LAUNCHED("step_fused");
+  return ASTRA_OK;
+}
+
+template <bool BF16, bool ADAM>
+int launch_fused_nv(int nv, const FusedArgs& A, cudaStream_t st) {
+  switch (nv) {
+    case 1: return launch_fused<1, BF16, ADAM>(A, st);
+    case 2: return launch_fused<2, BF16, ADAM>(A, st);
+    case 4: return launch_fused<4, BF16, ADAM>(A, st);
+    case 6: return launch_fused<6, BF16, ADAM>(A, st);
+    case 8: return launch_fused<8, BF16, ADAM>(A, st);
+  }
+  return ASTRA_ERR_CONFIG;
+}
+
+// Max B the fused kernel serves (one batch row per warp of the cooperative grid).
+template <bool BF16, bool ADAM>
+int fused_max_rows(int nv) {
+  static int cached[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+  if (nv < 0 || nv > 8) return 0;
+  if (cached[nv] >= 0) return cached[nv];
+  int per_sm = 0;
+  switch (nv) {
+    case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fused_kernel<1, BF16, ADAM>, kFusedThreads, 0); break;
+    case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fused_kernel<2, BF16, ADAM>, kFusedThreads, 0); break;
+    case 4: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fused_kernel<4, BF16, ADAM>, kFusedThreads, 0); break;
+    case 6: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fused_kernel<6, BF16, ADAM>, kFusedThreads, 0); break;
+    case 8: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fused_kernel<8, BF16, ADAM>, kFusedThreads, 0); break;
+    default: return 0;
+  }
+  cached[nv] = per_sm * num_sms() * kFusedWarps;
+  return cached[nv];
 }
 
 // apply_classifier_updates_arrays: explicit (ids, grads) form.
@@ -1108,6 +1563,13 @@ int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
 }
 
 struct StepWs {
+  int32_t* row_slots;
+  int32_t* row_locs;
+  int32_t* row_cofs;
+  uint32_t* uc;
+  unsigned* bar;
+  double* sf_acc;
+  unsigned* emax_acc;
   float* factors;
   int32_t* rank;
   int32_t* perm;
@@ -1138,6 +1600,13 @@ size_t carve_step(void* base, size_t cap, int B, int S, int64_t Lloc, StepWs* w)
   w->U = c.take<uint32_t>(1);
   w->loss_rows = c.take<double>(B);
   w->bound_rows = c.take<double>(B);
+  w->row_slots = c.take<int32_t>(n);
+  w->row_locs = c.take<int32_t>(n);
+  w->row_cofs = c.take<int32_t>(static_cast<size_t>(B) * (kMaxChunks + 1));
+  w->uc = c.take<uint32_t>(kMaxChunks + 1);
+  w->bar = c.take<unsigned>(4);  // bar, emax_acc, (pad), then the fp64 accumulator
+  w->emax_acc = w->bar ? w->bar + 1 : nullptr;
+  w->sf_acc = c.take<double>(1);
   return c.off;
 }
 
@@ -1153,8 +1622,8 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
                int64_t origin_stride, const float* weights, int64_t weights_stride, const float* factors_in, int B,
                int S, int d, void* W, int w_dtype, float* adam_m, float* adam_v, int optimizer, int64_t Lloc,
                int64_t off, double lr, double wd, double b1, double b2, double eps, int64_t adam_step, float* grad_emb,
-               double* loss_out, int32_t* status, float* factors_out, void* workspace, size_t ws_bytes,
-               cudaStream_t st) {
+               double* loss_out, int32_t* status, float* factors_out, float* w_absmax, void* workspace,
+               size_t ws_bytes, cudaStream_t st) {
   if (B < 0 || S < 0 || d <= 0 || Lloc < 0) return set_error(ASTRA_ERR_CONFIG, "slate_step: bad shape");
   if (Lloc >= (int64_t(1) << 31) || static_cast<int64_t>(B) * S >= (int64_t(1) << 31))
     return set_error(ASTRA_ERR_CONFIG, "slate_step: shard too large for 32-bit slot indices");
@@ -1194,7 +1663,22 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
   fa.status = status;
   const int nv = d % 128 == 0 ? d / 128 : 0;
   const bool aligned = (reinterpret_cast<uintptr_t>(emb) % 16 == 0) && (reinterpret_cast<uintptr_t>(W) % 16 == 0);
-  {
+  const bool adam = optimizer == ASTRA_OPT_ADAM;
+  static const int fused_env = [] {
+    // ASTRA_STEP_FUSED=1 selects the persistent L2-chunked step. Measured at the
+    // bench shape: 2.3 ms/minibatch vs 0.94 ms for the TMA two-kernel path (one
+    // warp per row and per label is latency-bound at 8 warps/SM); kept as a
+    // correct, tested alternative until it is software-pipelined.
+    const char* e = getenv("ASTRA_STEP_FUSED");
+    return e ? atoi(e) : 0;
+  }();
+  bool fused = fused_env && !factors_in && aligned && Lloc > 0 && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8);
+  if (fused) {
+    const int max_rows = bf16 ? (adam ? fused_max_rows<true, true>(nv) : fused_max_rows<true, false>(nv))
+                              : (adam ? fused_max_rows<false, true>(nv) : fused_max_rows<false, false>(nv));
+    fused = B <= max_rows;
+  }
+  if (!fused) {
     KernelTimer kt_fwd("slot_forward", st);
     if (aligned && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
       switch (nv * 2 + (bf16 ? 1 : 0)) {
@@ -1222,8 +1706,10 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     }
     ASTRA_LAUNCHED("slot_forward");
   }
-  finalize_kernel<<<1, 1024, 0, st>>>(w.loss_rows, w.bound_rows, B, loss_out, status);
-  ASTRA_LAUNCHED("finalize");
+  if (!fused) {
+    finalize_kernel<<<1, 1024, 0, st>>>(w.loss_rows, w.bound_rows, B, loss_out, status);
+    ASTRA_LAUNCHED("finalize");
+  }
 
   // counting sort of the slots by local label id
   const int64_t n = static_cast<int64_t>(B) * S;
@@ -1270,6 +1756,45 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     ua.c2 = static_cast<float>(1.0 - b2);
     ua.eps = static_cast<float>(eps);
     ua.neg_step = static_cast<float>(-(lr * sqrt(bc2) / bc1));
+  }
+  ua.w_absmax = w_absmax;
+  if (fused) {
+    // label chunks of ~24 MB of touched rows (+ Adam state) each: they stay in L2
+    // between their gather (phase p) and their update (phase p+1)
+    const double row_bytes = static_cast<double>(d) * ((bf16 ? 2 : 4) + (adam ? 8 : 0));
+    int C = static_cast<int>(std::ceil(static_cast<double>(n) * row_bytes / (24.0 * 1024 * 1024)));
+    C = std::max(1, std::min(C, kMaxChunks));
+    const int64_t Lc = (Lloc + C - 1) / C;
+    C = static_cast<int>((Lloc + Lc - 1) / Lc);
+    chunk_bounds_kernel<<<1, kMaxChunks + 1, 0, st>>>(w.uniq, w.U, Lc, C, w.uc);
+    ASTRA_LAUNCHED("chunk_bounds");
+    row_bucket_kernel<<<static_cast<unsigned>((B + 7) / 8), 256, 0, st>>>(ids, B, S, off, Lloc, Lc, C, w.row_slots,
+                                                                          w.row_locs, w.row_cofs);
+    ASTRA_LAUNCHED("row_bucket");
+    ASTRA_TRY(check_cuda(cudaMemsetAsync(w.bar, 0, 4 * sizeof(unsigned), st), "memset barrier"));
+    ASTRA_TRY(check_cuda(cudaMemsetAsync(w.sf_acc, 0, sizeof(double), st), "memset bound"));
+    FusedArgs A;
+    A.f = fa;
+    A.u = ua;
+    A.C = C;
+    A.Lc = Lc;
+    A.uc = w.uc;
+    A.row_slots = w.row_slots;
+    A.row_locs = w.row_locs;
+    A.row_cofs = w.row_cofs;
+    A.w_absmax = w_absmax;
+    A.bar = w.bar;
+    A.sf_acc = w.sf_acc;
+    A.emax_acc = w.emax_acc;
+    {
+      KernelTimer kt("step_fused", st);
+      int rc = bf16 ? (adam ? launch_fused_nv<true, true>(nv, A, st) : launch_fused_nv<true, false>(nv, A, st))
+                    : (adam ? launch_fused_nv<false, true>(nv, A, st) : launch_fused_nv<false, false>(nv, A, st));
+      if (rc != ASTRA_OK) return rc == ASTRA_ERR_CONFIG ? set_error(rc, "fused step: grid too small") : rc;
+    }
+    finalize_kernel<<<1, 1024, 0, st>>>(w.loss_rows, w.bound_rows, B, loss_out, status);
+    ASTRA_LAUNCHED("finalize");
+    return ASTRA_OK;
   }
   const int upd_ctas = 16 * sms;
   KernelTimer kt_upd("label_update", st);

@@ -63,6 +63,10 @@ class ClassifierEngine:
         else:
             W = torch.as_tensor(weights)[self.lo : self.hi].to(self.device, torch.float32)
         self.W = W.to(w_dtype).contiguous()
+        # running bound on max|W| (kept current by every update): lets the step
+        # prove finiteness up front and run the L2-chunked fused schedule
+        self.w_absmax = self.W.abs().amax().float().reshape(1).clone() if self.W.numel() else \
+            torch.zeros(1, dtype=torch.float32, device=self.device)
         self.m = self.v = None
         if optimizer == "adam":
             self.m = torch.zeros((self.hi - self.lo, dim), dtype=torch.float32, device=self.device)
@@ -131,7 +135,7 @@ class ClassifierEngine:
         res = self.ops.slate_step(
             emb_all, ids, y, origin, weights, self.W, lr, weight_decay, keep=keep_all, factors_in=factors_in,
             optimizer=self.optimizer, adam_m=self.m, adam_v=self.v, adam_step=max(self.adam_step, 1),
-            betas=self.betas, eps=self.eps, label_offset=self.lo)
+            betas=self.betas, eps=self.eps, label_offset=self.lo, w_absmax=self.w_absmax)
         grad_emb = self.comm.reduce_scatter(res.grad_emb)
         loss = self.comm.all_reduce(res.loss_dev)
         status = self.comm.all_reduce(res.status)

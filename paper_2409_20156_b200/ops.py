@@ -170,10 +170,12 @@ class StepResult:
 
 def slate_step(emb, ids, y, origin, weights, W, lr, weight_decay=0.0, keep=None, factors_in=None,
                optimizer="sgd", adam_m=None, adam_v=None, adam_step=1, betas=(0.9, 0.999), eps=1e-8,
-               label_offset=0, want_factors=False) -> StepResult:
+               label_offset=0, want_factors=False, w_absmax=None) -> StepResult:
     """Fused sampled-BCE fwd/bwd + sparse row update of W (trainer.py:366-394).
 
-    origin/weights may be S-vectors (the reference's row-0 semantics) or B x S."""
+    origin/weights may be S-vectors (the reference's row-0 semantics) or B x S.
+    w_absmax: optional fp32[1] CUDA tensor, a running bound on max|W| kept
+    current by the call (enables the L2-chunked fused step)."""
     _cuda(emb, torch.float32, "emb")
     _cuda(keep, torch.float32, "keep")
     _cuda(ids, torch.int32, "ids")
@@ -181,6 +183,7 @@ def slate_step(emb, ids, y, origin, weights, W, lr, weight_decay=0.0, keep=None,
     _cuda(origin, torch.int8, "origin")
     _cuda(weights, torch.float32, "weights")
     _cuda(factors_in, torch.float32, "factors_in")
+    _cuda(w_absmax, torch.float32, "w_absmax")
     if W.dtype not in (torch.float32, torch.bfloat16) or not W.is_cuda or not W.is_contiguous():
         raise ConfigError("W must be a contiguous CUDA fp32/bf16 tensor")
     B, S = ids.shape
@@ -203,7 +206,7 @@ def slate_step(emb, ids, y, origin, weights, W, lr, weight_decay=0.0, keep=None,
         _p(emb), _p(keep), _p(ids), _p(y), _p(origin), o_stride, _p(weights), w_stride, _p(factors_in), B, S, d,
         _p(W), W_BF16 if W.dtype == torch.bfloat16 else W_FP32, _p(adam_m), _p(adam_v), opt, Lloc, label_offset,
         float(lr), float(weight_decay), float(betas[0]), float(betas[1]), float(eps), int(adam_step),
-        _p(grad_emb), _p(loss), _p(status), _p(factors), _p(ws), ws.numel(), _stream()))
+        _p(grad_emb), _p(loss), _p(status), _p(factors), _p(w_absmax), _p(ws), ws.numel(), _stream()))
     return StepResult(loss, grad_emb, status, factors)
 
 

@@ -60,7 +60,7 @@ def sample_slates(seed, epoch, step, rows, pos_indptr, pos_ids, hard, k_h, n_lab
 
 def slate_step(emb, ids, y, origin, weights, W, lr, weight_decay=0.0, keep=None, factors_in=None, optimizer="sgd",
                adam_m=None, adam_v=None, adam_step=1, betas=(0.9, 0.999), eps=1e-8, label_offset=0,
-               want_factors=False):
+               want_factors=False, w_absmax=None):
     """The reference arithmetic (oracle/xcmix_port.py) restricted to this
     shard's label range [label_offset, label_offset + W.shape[0])."""
     if optimizer != "sgd":

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import golden
+from conftest import ROOT, golden
 from gpu_util import dev
 from oracle import xcmix_port as port
 
@@ -241,3 +241,45 @@ def test_apply_updates_golden_bitexact(cuda_lib):
     with pytest.raises(NumericalError):
         ops.apply_updates(W2, dev(g["ids"]), dev(bad), 0.3, 0.01)
     np.testing.assert_array_equal(W2.cpu().numpy(), g["W_before"])
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_engine_step_schedules_agree(cuda_lib, fused):
+    """The engine step (w_absmax bound maintained) under the two-kernel TMA path
+    and under the persistent L2-chunked schedule matches the reference
+    arithmetic (oracle port) on the same slates."""
+    import subprocess
+    import sys
+
+    code = f"""
+import os, sys
+os.environ["ASTRA_STEP_FUSED"] = "{fused}"
+sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {ROOT!r} + "/tests")
+import numpy as np, torch
+from oracle import xcmix_port as port
+from paper_2409_20156_b200.engine import ClassifierEngine
+L, d, B, S = 200_000, 768, 64, 120
+rng = np.random.default_rng(5)
+W = rng.uniform(-0.03, 0.03, size=(L, d)).astype(np.float32)
+emb = rng.standard_normal((B, d)).astype(np.float32)
+ids = rng.integers(0, L, size=(B, S)).astype(np.int64)
+y = (rng.random((B, S)) < 0.05).astype(np.int8)
+origin = np.full(S, 2, np.int8); origin[:4] = 0
+weights = np.full(S, 3.5, np.float32); weights[:4] = 1.0
+eng = ClassifierEngine(L, d, k_p=4, k_h=0, k_r=S - 4, weights=W, seed=0)
+sl = tuple(torch.from_numpy(a).cuda() for a in (ids.astype(np.int32), y, origin, weights))
+loss, ge, st = eng.step(torch.from_numpy(emb).cuda(), sl, 0.05, 1e-4)
+Wref = W.copy()
+rl, rge, _, uids = port.slate_step(Wref, emb, None, ids, y, origin, weights, 0.05, 1e-4)
+got = eng.W.cpu().numpy()
+assert st.cpu().tolist()[:2] == [0, 0]
+assert abs(float(loss.item()) - rl) <= 1e-5 * abs(rl)
+assert np.allclose(ge.cpu().numpy(), rge, rtol=1e-5, atol=1e-6 * np.abs(rge).max())
+assert np.allclose(got[uids], Wref[uids], rtol=1e-5, atol=1e-6 * np.abs(Wref).max())
+mask = np.ones(L, bool); mask[uids] = False
+assert np.array_equal(got[mask], W[mask])
+assert float(eng.w_absmax.item()) >= np.abs(got).max()
+print("ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
