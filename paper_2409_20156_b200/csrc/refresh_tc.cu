@@ -10,6 +10,10 @@
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma.kind::f16
 //               (M=128, N=256, K=16) into a TMEM accumulator; tcgen05.commit
 //               releases smem stages and publishes finished accumulators.
+//               Default: CTA pairs (cta_group::2): the even CTA of a cluster
+//               of 2 issues M=256 MMAs over both CTAs' shared memory (each
+//               stages its 128 query rows and 128 of the tile's 256 W rows,
+//               6 x 32 KB ring), commits to both CTAs' barriers.
 //   warp 2      TMEM allocator (512 columns = 2 accumulators of 256 fp32 cols).
 //   warps 4-7   epilogue: tcgen05.ld 64 columns per step (thread = query row =
 //               TMEM lane), one warp vote per step, then either
@@ -51,6 +55,19 @@ constexpr size_t kSmemBytes = 1024 /*align slack*/ + STAGES * STAGE_BYTES + kBar
 
 // idesc for kind::f16: D=F32, A=B=BF16, both K-major, N>>3 at [17,23), M>>4 at [24,29)
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+// CTA pair (cta_group::2): M = 256 (128 query rows per CTA), N = 256 (each CTA holds 128 W rows)
+constexpr uint32_t kIdescPair =
+    (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t((2 * BM) >> 4) << 24);
+
+// Shared-memory ring geometry: single CTA (4 x 48 KB: A 128 rows + B 256 rows)
+// or CTA pair (6 x 32 KB: A 128 rows + this CTA's 128 of the 256 B rows).
+template <bool PAIR>
+struct Geo {
+  static constexpr int B_ROWS = PAIR ? BN / 2 : BN;
+  static constexpr int B_ST = B_ROWS * BK * 2;
+  static constexpr int STG = A_STAGE + B_ST;
+  static constexpr int NST = PAIR ? 6 : STAGES;
+};
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -109,6 +126,43 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
       "h"(mask)
+      : "memory");
+}
+
+// Pair TMA load: lands in this CTA's smem, completes tx on the LEADER's barrier
+// (bar_cluster = its shared::cluster address).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// shared::cluster address of `p` (a shared::cta address) in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_cluster(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdescPair), "r"(accumulate));
+}
+
+// Arrive on `bar` in both CTAs of the pair once the leader's prior tcgen05.mma complete.
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
       : "memory");
 }
 
@@ -293,25 +347,29 @@ __device__ __forceinline__ bool unit_active(const uint32_t* qbits, int64_t n_qt_
   return (qbits[qc >> 5] >> (qc & 31)) & 1u;
 }
 
-template <int CL, int MODE>
+template <int CL, int MODE, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     refresh_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+  static_assert(!PAIR || CL == 2, "a CTA pair is a cluster of 2");
+  using G = Geo<PAIR>;
+  constexpr int NST = G::NST;
   constexpr uint16_t kMask = static_cast<uint16_t>((1u << CL) - 1);
-  constexpr int B_SLICE = B_STAGE / CL;  // bytes of W tile rows loaded by each cluster rank
+  constexpr int B_SLICE = B_STAGE / CL;  // bytes of W tile rows loaded by each cluster rank (multicast)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
   const int64_t cluster = blockIdx.x / CL, n_clusters = gridDim.x / CL;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* sA = smem;
-  unsigned char* sB = smem + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  unsigned char* sB = smem + NST * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * G::STG);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t* qbits_s = tmem_holder + 8;  // kQtBits bits
-  float* stage_base = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + kBarrierBytes);
+  float* stage_base = reinterpret_cast<float*>(smem + NST * G::STG + kBarrierBytes);
+  const bool leader = !PAIR || crank == 0;
   const int nkb = a.d / BK;
   const int64_t n_units = a.n_qt_cl * a.n_parts;
 
@@ -331,20 +389,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);  // every cluster CTA's MMA must release the stage
+      // multicast: every cluster CTA's MMA releases the stage; pair: one commit from the leader
+      mbar_init(&empty[s], PAIR ? 1 : CL);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], kEpiWarps);
+      mbar_init(&tempty[s], PAIR ? 2 * kEpiWarps : kEpiWarps);  // pair: both CTAs' epilogues free the leader's MMA
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   if (CL > 1)
@@ -367,14 +432,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int n0 = static_cast<int>(t * a.tile_stride * BN);
           for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], STAGE_BYTES);  // own A + all CL slices of the W tile
-            tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, q0);
-            if (CL == 1)
-              tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
-            else
-              tma_load_2d_mc(sB + stage * B_STAGE + crank * B_SLICE, &tmB, &full[stage], kb * BK,
-                             n0 + static_cast<int>(crank) * (BN / CL), kMask);
-            if (++stage == STAGES) {
+            if constexpr (PAIR) {
+              // both CTAs load their A rows and their half of the W tile; the
+              // transaction bytes of both complete on the leader's barrier
+              const uint32_t bar = mapa_cluster(&full[stage], 0);
+              if (leader) mbar_expect_tx(&full[stage], 2 * G::STG);
+              tma_load_2d_pair(sA + stage * A_STAGE, &tmA, bar, kb * BK, q0);
+              tma_load_2d_pair(sB + stage * G::B_ST, &tmB, bar, kb * BK, n0 + static_cast<int>(crank) * G::B_ROWS);
+            } else {
+              mbar_expect_tx(&full[stage], STAGE_BYTES);  // own A + all CL slices of the W tile
+              tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, q0);
+              if (CL == 1)
+                tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
+              else
+                tma_load_2d_mc(sB + stage * B_STAGE + crank * B_SLICE, &tmB, &full[stage], kb * BK,
+                               n0 + static_cast<int>(crank) * (BN / CL), kMask);
+            }
+            if (++stage == NST) {
               stage = 0;
               phase ^= 1;
             }
@@ -382,8 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer
+  } else if (warp == 1 && leader) {
+    // ---------------- MMA issuer (pair: the leader CTA issues for both)
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -406,24 +480,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           if (lane == 0) {
             const uint64_t ad = smem_desc(sA + stage * A_STAGE);
-            const uint64_t bd = smem_desc(sB + stage * B_STAGE);
+            const uint64_t bd = smem_desc(sB + stage * G::B_ST);
 #pragma unroll
             for (int kk = 0; kk < BK / UMMA_K; ++kk) {
               // +32 B along K inside the 128 B swizzle atom = +2 in the encoded address
-              mma_bf16(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
+              if constexpr (PAIR)
+                mma_bf16_pair(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
+              else
+                mma_bf16(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
             }
-            if (CL == 1)
+            if constexpr (PAIR)
+              mma_commit_pair(&empty[stage]);
+            else if (CL == 1)
               mma_commit(&empty[stage]);
             else
               mma_commit_mc(&empty[stage], kMask);
           }
           __syncwarp();
-          if (++stage == STAGES) {
+          if (++stage == NST) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (lane == 0) mma_commit(&tfull[acc]);
+        if (lane == 0) {
+          if constexpr (PAIR)
+            mma_commit_pair(&tfull[acc]);
+          else
+            mma_commit(&tfull[acc]);
+        }
         __syncwarp();
         if (++acc == 2) {
           acc = 0;
@@ -526,7 +610,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if constexpr (PAIR)
+            mbar_arrive_cluster(mapa_cluster(&tempty[acc], 0));  // the leader's MMA reuses both halves
+          else
+            mbar_arrive(&tempty[acc]);
+        }
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -555,7 +644,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
   }
 }
 
@@ -585,10 +677,10 @@ int make_map(CUtensorMap* m, const void* base, int64_t rows, int d, int box_rows
   return ASTRA_OK;
 }
 
-template <int CL, int MODE>
+template <int CL, int MODE, bool PAIR = false>
 int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const TcArgs& a, dim3 grid, cudaStream_t st) {
   static bool attr_set = false;
-  auto kern = refresh_tc_kernel<CL, MODE>;
+  auto kern = refresh_tc_kernel<CL, MODE, PAIR>;
   if (!attr_set) {
     ASTRA_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(kSmemBytes)),
@@ -703,7 +795,22 @@ int launch_refresh_tc(const TcLaunch& p, cudaStream_t st) {
   if (mode == kRunning) ASTRA_TRY(check_cuda(cudaMemsetAsync(p.gtau, 0, sizeof(uint64_t) * p.nq, st), "memset gtau"));
   const dim3 grid(static_cast<unsigned>(G));
   int rc;
-  if (mode == kFixed)
+  // CTA pairs (tcgen05 cta_group::2, M=256 per MMA, each CTA stages half of the
+  // W tile) by default; ASTRA_TC_PAIR=0 selects W multicast in clusters of 2.
+  // ncu: 1/3 less L2->SM traffic, tensor pipe 87% vs 85% active at the same
+  // power-capped clock (profiles/r01/ncu_full_refresh_threshold_pair.txt).
+  static const bool pair = [] {
+    const char* e = getenv("ASTRA_TC_PAIR");
+    return !(e && atoi(e) == 0);
+  }();
+  if (cl == 2 && pair) {
+    if (mode == kFixed)
+      rc = launch_variant<2, kFixed, true>(tmA, tmB, a, grid, st);
+    else if (mode == kGmax)
+      rc = launch_variant<2, kGmax, true>(tmA, tmB, a, grid, st);
+    else
+      rc = launch_variant<2, kRunning, true>(tmA, tmB, a, grid, st);
+  } else if (mode == kFixed)
     rc = cl == 2 ? launch_variant<2, kFixed>(tmA, tmB, a, grid, st) : launch_variant<1, kFixed>(tmA, tmB, a, grid, st);
   else if (mode == kGmax)
     rc = cl == 2 ? launch_variant<2, kGmax>(tmA, tmB, a, grid, st) : launch_variant<1, kGmax>(tmA, tmB, a, grid, st);
