@@ -103,6 +103,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def bench_config(world: int) -> dict:
+    """The workload description shared by both arms' JSON lines."""
+    c = CFG
+    R = c["B"] * c["minibatches"]
+    return {"workload": c["workload"], "n_labels": c["L"], "dim": c["d"], "rows_per_step_per_gpu": R,
+            "minibatch": c["B"], "minibatches_per_step": c["minibatches"], "global_batch": c["B"] * world,
+            "k_p": c["k_p"], "k_h": c["k_h"], "k_r": c["k_r"], "slate": c["k_p"] + c["k_h"] + c["k_r"],
+            "labels_per_point": c["labels_per_point"], "tau_r": c["tau_r"], "refresh_chunk": R * world,
+            "refresh_mode": "bf16_rerank", "optimizer": "sgd+wd", "parallelism": f"label-shard{world}",
+            "l2": "inputs larger than L2 (W fp32 4.0 GB + snapshots 6 GB)"}
+
+
 def _ncu_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of each timed
     kernel, from the committed `ncu --set full` summary (profiles/)."""
@@ -318,12 +330,8 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": round(ms_total / K, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "fp32 W/step, bf16 tensor-core refresh + fp32 re-rank", "data": "synthetic",
-        "config": {"workload": CFG["workload"], "n_labels": L, "dim": d, "rows_per_step_per_gpu": R,
-                   "minibatch": B, "minibatches_per_step": M, "global_batch": B * world, "k_p": k_p, "k_h": k_h,
-                   "k_r": k_r, "slate": S, "labels_per_point": CFG["labels_per_point"], "tau_r": CFG["tau_r"],
-                   "refresh_chunk": R * world, "refresh_mode": "bf16_rerank", "optimizer": "sgd+wd",
-                   "refresh_overlap": overlap, "refresh_sms": args.refresh_sms if overlap else None,
-                   "parallelism": f"label-shard{world}", "l2": "inputs larger than L2 (W fp32 4.0 GB + snapshots 6 GB)"},
+        "config": dict(bench_config(world), refresh_overlap=overlap,
+                       refresh_sms=args.refresh_sms if overlap else None),
         "phases_ms_per_step": {k: round(v / K, 4) for k, v in ph.items()},
         "refresh_mips_qps": round(q_per_refresh / t_ref, 1),
         "step_only_samples_per_s": round(B * world / (t_step + t_samp), 1),
@@ -541,9 +549,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (numpy)",
             "data": "synthetic",
-            "config": {"workload": CFG["workload"], "n_labels": CFG["L"], "dim": CFG["d"], "batch_per_gpu": B,
-                       "k_p": CFG["k_p"], "k_h": CFG["k_h"], "k_r": CFG["k_r"], "slate": CFG["k_p"] + CFG["k_h"] + CFG["k_r"],
-                       "tau_r": CFG["tau_r"]},
+            "config": bench_config(world),
             "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                              "sample": f"per step: 1 classifier step of B={B} + refresh of {q} queries scaled to B"},
             "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
