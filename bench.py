@@ -305,6 +305,7 @@ def run_ours(args):
             outs[i], _ = eng.train_step_host(m["emb"], m["rows"], m["indptr"], m["pos"], m["hard"], 1, t * M + i,
                                              CFG["lr"], CFG["wd"], out=outs[i])
         stream.wait_stream(rstream)
+        eng.wait_host_outputs()  # the step's D2H results are complete when the step ends
 
     for t in range(args.warmup):
         one_host(t)

@@ -144,42 +144,126 @@ class ClassifierEngine:
     # ------------------------------------------------------------ host API
     def refresh_host(self, queries_h, pos_indptr_h, pos_ids_h, k: int | None = None, out=None):
         """retrieve_hard_negatives for a chunk of queries given in HOST (pinned)
-        memory: H2D of the queries and positives, refresh, D2H of the ids."""
-        dev = self.device
-        q = queries_h.to(dev, non_blocking=True)
-        ip = pos_indptr_h.to(dev, non_blocking=True)
-        pid = pos_ids_h.to(dev, non_blocking=True)
-        ids, _ = self.refresh(q, ip, pid, k or self.k_h)
+        memory: H2D of the queries and positives, refresh, D2H of the ids.
+        On CUDA the copies run on side streams (double-buffered staging), so
+        they overlap the previous call's compute; `wait_host_outputs()` makes
+        the current stream wait for the D2H."""
+        if self.device.type != "cuda":
+            ids, _ = self.refresh(queries_h.to(self.device), pos_indptr_h.to(self.device), pos_ids_h.to(self.device),
+                                  k or self.k_h)
+            out = torch.empty(ids.shape, dtype=ids.dtype) if out is None else out
+            out.copy_(ids)
+            return out
+        pipe = self._pipe("refresh")
+        d, slot = pipe.stage({"q": queries_h, "ip": pos_indptr_h, "pid": pos_ids_h})
+        ids, _ = self.refresh(d["q"], d["ip"], d["pid"], k or self.k_h)
+        pipe.release(slot)
         if out is None:
             out = torch.empty(ids.shape, dtype=ids.dtype, pin_memory=True)
-        out.copy_(ids, non_blocking=True)
+        pipe.fetch(ids, out)
         return out
 
     def train_step_host(self, emb_h, rows_h, pos_indptr_h, pos_ids_h, hard_h, epoch, step, lr, weight_decay,
                         out=None):
-        """One training minibatch with HOST inputs: H2D (pinned, non_blocking)
-        of embeddings / rows / positives / hard-cache rows, Philox slates, fused
-        loss + update, D2H of grad_emb and the loss. Returns
-        ((grad_emb_h, loss_h), status_dev)."""
-        dev = self.device
-        emb = emb_h.to(dev, non_blocking=True)
-        rows = rows_h.to(dev, non_blocking=True)
-        ip = pos_indptr_h.to(dev, non_blocking=True)
-        pid = pos_ids_h.to(dev, non_blocking=True)
-        hard = hard_h.to(dev, non_blocking=True) if hard_h is not None else None
-        slates = self.sample(rows, ip, pid, hard, epoch, step)
-        loss, grad_emb, status = self.step(emb, slates, lr, weight_decay)
+        """One training minibatch with HOST inputs: H2D (pinned) of embeddings /
+        rows / positives / hard-cache rows, Philox slates, fused loss + update,
+        D2H of grad_emb and the loss. On CUDA the H2D copies of call i+1 run on
+        a copy stream while call i computes (double-buffered device staging)
+        and the D2H on a third stream; `wait_host_outputs()` orders them
+        before the caller reads `out`. Returns ((grad_emb_h, loss_h), status_dev)."""
+        if self.device.type != "cuda":
+            dev = self.device
+            hard = hard_h.to(dev) if hard_h is not None else None
+            slates = self.sample(rows_h.to(dev), pos_indptr_h.to(dev), pos_ids_h.to(dev), hard, epoch, step)
+            loss, grad_emb, status = self.step(emb_h.to(dev), slates, lr, weight_decay)
+            if out is None:
+                out = (torch.empty(grad_emb.shape, dtype=grad_emb.dtype), torch.empty(1, dtype=torch.float64))
+            out[0].copy_(grad_emb)
+            out[1].copy_(loss)
+            return out, status
+        pipe = self._pipe("step")
+        d, slot = pipe.stage({"emb": emb_h, "rows": rows_h, "ip": pos_indptr_h, "pid": pos_ids_h, "hard": hard_h})
+        slates = self.sample(d["rows"], d["ip"], d["pid"], d["hard"], epoch, step)
+        loss, grad_emb, status = self.step(d["emb"], slates, lr, weight_decay)
+        pipe.release(slot)
         if out is None:
             out = (torch.empty(grad_emb.shape, dtype=grad_emb.dtype, pin_memory=True),
                    torch.empty(1, dtype=torch.float64, pin_memory=True))
-        out[0].copy_(grad_emb, non_blocking=True)
-        out[1].copy_(loss, non_blocking=True)
+        pipe.fetch(grad_emb, out[0])
+        pipe.fetch(loss, out[1])
         return out, status
+
+    def wait_host_outputs(self) -> None:
+        """Make the current stream wait for every D2H issued by the host API."""
+        for pipe in getattr(self, "_pipes", {}).values():
+            torch.cuda.current_stream().wait_stream(pipe.d2h)
+
+    def _pipe(self, name: str) -> "_HostPipe":
+        pipes = self.__dict__.setdefault("_pipes", {})
+        if name not in pipes:
+            pipes[name] = _HostPipe(self.device)
+        return pipes[name]
 
     # ------------------------------------------------------------ host views
     def weights_host(self) -> np.ndarray:
         """This shard's W as fp32 NumPy (for eval / checkpoint boundaries)."""
         return self.W.float().cpu().numpy()
+
+
+class _HostPipe:
+    """Double-buffered host->device staging on a copy stream plus a D2H stream.
+
+    stage() copies a call's pinned inputs into device slot k (after the compute
+    that last read slot k, tracked by release()) and makes the current stream
+    wait for the copy; fetch() copies a result back on the D2H stream after the
+    current stream's work. Slots are owned device buffers (never freed), so no
+    caching-allocator reuse can race the side streams."""
+
+    def __init__(self, device, n_slots: int = 2):
+        self.device = device
+        self.h2d = torch.cuda.Stream(device)
+        self.d2h = torch.cuda.Stream(device)
+        self.slots = [dict() for _ in range(n_slots)]
+        self.free = [None] * n_slots
+        self.k = 0
+
+    def stage(self, tensors: dict):
+        k = self.k
+        self.k = (k + 1) % len(self.slots)
+        bufs = self.slots[k]
+        out = {}
+        with torch.cuda.stream(self.h2d):
+            if self.free[k] is not None:
+                self.h2d.wait_event(self.free[k])
+            for name, t in tensors.items():
+                if t is None:
+                    out[name] = None
+                    continue
+                n = t.numel()
+                buf = bufs.get(name)
+                if buf is None or buf.numel() < n or buf.dtype != t.dtype:
+                    buf = torch.empty(max(n, 1), dtype=t.dtype, device=self.device)
+                    bufs[name] = buf
+                view = buf[:n].view(t.shape)
+                view.copy_(t, non_blocking=True)
+                out[name] = view
+            ready = torch.cuda.Event()
+            ready.record(self.h2d)
+        torch.cuda.current_stream().wait_event(ready)
+        return out, k
+
+    def release(self, k: int) -> None:
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.free[k] = ev
+
+    def fetch(self, dev_tensor, host_out) -> None:
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.d2h.wait_event(ev)
+        with torch.cuda.stream(self.d2h):
+            host_out.copy_(dev_tensor, non_blocking=True)
+        dev_tensor.record_stream(self.d2h)
 
 
 def h2d_bytes(*tensors) -> int:

@@ -283,3 +283,39 @@ print("ok")
 """
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_host_api_pipelined_equals_device_api(cuda_lib):
+    """ClassifierEngine.refresh_host / train_step_host (double-buffered H2D on a
+    copy stream, D2H on another) give the device API's results, call after call."""
+    from paper_2409_20156_b200.engine import ClassifierEngine
+
+    L, d, B, k_p, k_h, k_r = 50_000, 128, 96, 4, 8, 24
+    rng = np.random.default_rng(3)
+    W = rng.uniform(-0.05, 0.05, size=(L, d)).astype(np.float32)
+    a = ClassifierEngine(L, d, k_p=k_p, k_h=k_h, k_r=k_r, weights=W, seed=1)
+    b = ClassifierEngine(L, d, k_p=k_p, k_h=k_h, k_r=k_r, weights=W, seed=1)
+    a.snapshot()
+    b.snapshot()
+    host_out = []
+    for t in range(5):
+        emb = rng.standard_normal((B, d)).astype(np.float32)
+        rows = np.arange(t * B, (t + 1) * B, dtype=np.int64)
+        pos = [np.unique(rng.integers(0, L, 3)).astype(np.int32) for _ in range(B)]
+        ip = np.zeros(B + 1, np.int64)
+        ip[1:] = np.cumsum([len(p) for p in pos])
+        pid = np.concatenate(pos)
+        pin = lambda x: torch.from_numpy(x).pin_memory()  # noqa: E731
+        ids_h = a.refresh_host(pin(emb), pin(ip), pin(pid), k_h)
+        hard = torch.from_numpy(ids_h.numpy().copy()) if t == 0 else hard
+        (ge_h, loss_h), _ = a.train_step_host(pin(emb), pin(rows), pin(ip), pin(pid), hard.pin_memory(), 1, t, 0.05, 1e-4)
+        a.wait_host_outputs()
+        torch.cuda.synchronize()
+        host_out.append((ids_h.numpy().copy(), ge_h.numpy().copy(), float(loss_h.item())))
+        ids_d, _ = b.refresh(dev(emb), dev(ip), dev(pid), k_h)
+        sl = b.sample(dev(rows), dev(ip), dev(pid), hard.cuda(), 1, t)
+        loss_d, ge_d, _ = b.step(dev(emb), sl, 0.05, 1e-4)
+        np.testing.assert_array_equal(host_out[-1][0], ids_d.cpu().numpy())
+        np.testing.assert_array_equal(host_out[-1][1], ge_d.cpu().numpy())
+        assert host_out[-1][2] == float(loss_d.item())
+    np.testing.assert_array_equal(a.W.cpu().numpy(), b.W.cpu().numpy())
