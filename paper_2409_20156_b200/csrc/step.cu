@@ -104,6 +104,33 @@ __device__ __forceinline__ float slot_factor_only(const FwdArgs& a, int b, int s
   return __fadd_rn(__fmul_rn(pos_term, __fsub_rn(sig, 1.0f)), __fmul_rn(wn, sig));
 }
 
+// The slot's (origin, y, weight), loaded ahead of its W row so that these
+// L2 loads overlap the row's arrival instead of following it.
+struct SlotMeta {
+  int8_t o;
+  float yf, w;
+};
+
+__device__ __forceinline__ SlotMeta slot_meta(const FwdArgs& a, int b, int s) {
+  SlotMeta m;
+  m.o = a.origin[b * a.origin_stride + s];
+  m.yf = static_cast<float>(a.y[static_cast<size_t>(b) * a.S + s]);
+  m.w = a.weights[b * a.weights_stride + s];
+  return m;
+}
+
+// slot_factor_only from prefetched metadata (same arithmetic).
+__device__ __forceinline__ float slot_factor_meta(const SlotMeta& m, float sc, float* pos_term_out, float* wn_out) {
+  const bool pos_slot = m.o == ASTRA_ORIGIN_POS;
+  const float pos_term = pos_slot ? m.yf : 0.0f;
+  const float neg_alive = pos_slot ? 0.0f : __fsub_rn(1.0f, m.yf);
+  const float sig = expit_f32(sc);
+  const float wn = __fmul_rn(m.w, neg_alive);
+  *pos_term_out = pos_term;
+  *wn_out = wn;
+  return __fadd_rn(__fmul_rn(pos_term, __fsub_rn(sig, 1.0f)), __fmul_rn(wn, sig));
+}
+
 __device__ __forceinline__ double slot_loss(float sc, float pos_term, float wn) {
   const double spn = softplus64(-static_cast<double>(sc));
   return static_cast<double>(pos_term) * spn + static_cast<double>(wn) * (spn + static_cast<double>(sc));
@@ -337,6 +364,7 @@ __global__ void __launch_bounds__(kTmaThreads, 3) slot_forward_tma(FwdArgs a) {
       const int r = i % RING;
       const int sl = own[i];
       const float fin = a.factors_in ? a.factors_in[static_cast<size_t>(b) * a.S + sl] : 0.0f;
+      const SlotMeta meta = slot_meta(a, b, sl);
       mbar_wait(&full[r], (i / RING) & 1);
       float4 w[NV];
 #pragma unroll
@@ -365,7 +393,7 @@ __global__ void __launch_bounds__(kTmaThreads, 3) slot_forward_tma(FwdArgs a) {
         }
         acc = warp_sum(acc);
         float pt, wn;
-        f = slot_factor_only(a, b, sl, acc, &pt, &wn);
+        f = slot_factor_meta(meta, acc, &pt, &wn);
         if (lane == c_pend) {
           pend_sc = acc;
           pend_pt = pt;
@@ -1475,6 +1503,489 @@ int fused_max_rows(int nv) {
   return cached[nv];
 }
 
+// ================================================================ pipelined step
+// One cooperative kernel per minibatch, one CTA per SM, two roles per CTA that
+// work through the label chunks of the fused schedule without grid barriers:
+//   forward warps 0-3 own the CTA's batch rows (<= 8; embeddings and grad_emb
+//   partials in shared memory, row r -> warp r % 4, fixed order); chunk by
+//   chunk they gather the rows' slot rows (each warp self-feeds a private ring
+//   of bulk copies RF rows ahead, across chunk borders), compute scores,
+//   factors, loss terms and f * w_row; when the CTA finishes chunk c it bumps
+//   done[c];
+//   update warps 4-7 + producer warp 8 follow behind: for chunk c they wait
+//   for done[c] == #CTAs, then update the CTA's share of the chunk's labels as
+//   label_update_tma does (bulk-copied rows, still L2-resident from the gather).
+// DRAM sees each touched row read once (gather) and written once (update).
+// Finiteness is proven up front from bounds (as the fused schedule); without
+// the proof the update warps wait for every forward, check every gradient,
+// and only then update.
+constexpr int kPipeRows = 8;                // batch rows per CTA
+constexpr int kPipeThreads = 32 * 9;        // 4 forward + 4 update + 1 update producer
+
+template <int NV, bool BF16>
+struct PipeRing {
+  static constexpr uint32_t WB = NV * 128 * (BF16 ? 2 : 4);
+  static constexpr int RF = BF16 ? 12 : 6;  // self-fed entries per forward warp
+};
+
+struct PipeArgs {
+  FusedArgs x;
+  int rows_f;
+  unsigned* done;   // [C] CTAs whose forward finished chunk c
+  unsigned* ready;  // [0] bounds published, [1] gradients checked (checked schedule), [2] forwards finished
+};
+
+template <int NV, bool BF16, bool ADAM>
+struct PipeSmem {
+  static constexpr int d = NV * 128;
+  using PR = PipeRing<NV, BF16>;
+  using RG = UpdRing<NV, BF16, ADAM>;
+  static constexpr size_t E = 0;                                           // e_s, g_s
+  static constexpr size_t FR = E + static_cast<size_t>(2) * kPipeRows * d * 4;  // forward rings
+  static constexpr size_t UR = FR + static_cast<size_t>(4) * PR::RF * PR::WB;   // update ring
+  static constexpr size_t BAR = UR + static_cast<size_t>(RG::RING) * RG::ENTRY;  // barriers
+  static constexpr size_t FAB = BAR + 8 * (4 * PR::RF + 2 * RG::RING);          // row_fabs
+  static constexpr size_t TOTAL = FAB + 8 * kPipeRows;
+};
+
+// Walks a forward warp's (chunk, row, slot) items in order: rows w and w+4 of
+// the CTA, chunk by chunk, skipping empty segments; c == C at the end.
+struct PipeCursor {
+  int c, ri, r, j, j1;
+};
+
+__device__ __forceinline__ bool pipe_cursor_seg(PipeCursor& q, const FusedArgs& A, int b0, int nrows, int warp) {
+  q.r = warp + 4 * q.ri;
+  if (q.r >= nrows) return false;
+  const int32_t* cofs = A.row_cofs + static_cast<size_t>(b0 + q.r) * (A.C + 1);
+  q.j = cofs[q.c];
+  q.j1 = cofs[q.c + 1];
+  return q.j < q.j1;
+}
+
+__device__ __forceinline__ void pipe_cursor_skip(PipeCursor& q, const FusedArgs& A, int b0, int nrows, int warp) {
+  while (q.c < A.C) {
+    if (pipe_cursor_seg(q, A, b0, nrows, warp)) return;
+    if (++q.ri == 2) {
+      q.ri = 0;
+      ++q.c;
+    }
+  }
+}
+
+__device__ __forceinline__ void pipe_cursor_init(PipeCursor& q, const FusedArgs& A, int b0, int nrows, int warp) {
+  q.c = 0;
+  q.ri = 0;
+  pipe_cursor_skip(q, A, b0, nrows, warp);
+}
+
+__device__ __forceinline__ void pipe_cursor_next(PipeCursor& q, const FusedArgs& A, int b0, int nrows, int warp) {
+  if (++q.j < q.j1) return;
+  if (++q.ri == 2) {
+    q.ri = 0;
+    ++q.c;
+  }
+  pipe_cursor_skip(q, A, b0, nrows, warp);
+}
+
+__device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target) {
+  unsigned v;
+  while (true) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (v >= target) break;
+    __nanosleep(128);
+  }
+}
+
+__device__ __forceinline__ void publish(unsigned* p) {
+  __threadfence();
+  atomicAdd(p, 1u);
+}
+
+// The CTA's share [q0, q1) of chunk c's unique labels.
+__device__ __forceinline__ void pipe_share(const FusedArgs& A, int c, uint32_t& q0, uint32_t& q1) {
+  const uint32_t lo = A.uc[c], n = A.uc[c + 1] - lo;
+  q0 = lo + static_cast<uint32_t>((static_cast<uint64_t>(n) * blockIdx.x) / gridDim.x);
+  q1 = lo + static_cast<uint32_t>((static_cast<uint64_t>(n) * (blockIdx.x + 1)) / gridDim.x);
+}
+
+template <int NV, bool BF16, bool ADAM>
+__global__ void __launch_bounds__(kPipeThreads, 1) step_pipe_kernel(PipeArgs P) {
+  const FusedArgs& A = P.x;
+  const FwdArgs& a = A.f;
+  const UpdArgs& ua = A.u;
+  constexpr int d = NV * 128;
+  using SM = PipeSmem<NV, BF16, ADAM>;
+  using PR = PipeRing<NV, BF16>;
+  using RG = UpdRing<NV, BF16, ADAM>;
+  constexpr int RF = PR::RF;
+  constexpr int RING = RG::RING;
+  constexpr uint32_t ROWB = RG::ENTRY;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  extern __shared__ __align__(128) unsigned char psm[];
+  float* e_s = reinterpret_cast<float*>(psm + SM::E);
+  float* g_s = e_s + kPipeRows * d;
+  unsigned char* frings = psm + SM::FR;
+  unsigned char* uring = psm + SM::UR;
+  uint64_t* ffull = reinterpret_cast<uint64_t*>(psm + SM::BAR);
+  uint64_t* ufull = ffull + 4 * RF;
+  uint64_t* uempty = ufull + RING;
+  double* row_fabs = reinterpret_cast<double*>(psm + SM::FAB);
+  const unsigned G = gridDim.x;
+  const int b0 = blockIdx.x * P.rows_f;
+  const int nrows = max(0, min(P.rows_f, a.B - b0));
+  __shared__ double s_sf;
+  __shared__ unsigned s_em;
+  if (threadIdx.x == 0) {
+    s_sf = 0.0;
+    s_em = 0u;
+    for (int r = 0; r < 4 * RF; ++r) mbar_init(&ffull[r], 1);
+    for (int r = 0; r < RING; ++r) {
+      mbar_init(&ufull[r], 1);
+      mbar_init(&uempty[r], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < kPipeRows; i += kPipeThreads) row_fabs[i] = 0.0;
+  // embeddings -> smem, grad_emb partials = 0, finiteness bound partials
+  float em = 0.0f;
+  for (int i = threadIdx.x; i < nrows * d; i += kPipeThreads) {
+    const float v = a.emb[static_cast<size_t>(b0) * d + i];
+    e_s[i] = v;
+    g_s[i] = 0.0f;
+    em = fmaxf(em, isfinite(v) ? fabsf(v) : INFINITY);
+  }
+  double sf = 0.0;
+  for (int r = warp; r < nrows; r += kPipeThreads / 32) {
+    const int b = b0 + r;
+    const int j1 = A.row_cofs[static_cast<size_t>(b) * (A.C + 1) + A.C];
+    const int32_t* rs = A.row_slots + static_cast<size_t>(b) * a.S;
+    for (int j = lane; j < j1; j += 32) {
+      const float wt = a.weights[b * a.weights_stride + rs[j]];
+      sf += 1.0 + (isfinite(wt) ? fabs(static_cast<double>(wt)) : INFINITY);
+    }
+  }
+  sf = warp_sum(sf);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) em = fmaxf(em, __shfl_xor_sync(0xffffffffu, em, o));
+  __syncthreads();
+  if (lane == 0) {
+    atomicAdd(&s_sf, sf);
+    atomicMax(&s_em, __float_as_uint(em));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(A.sf_acc, s_sf);
+    atomicMax(A.emax_acc, s_em);
+    publish(P.ready + 0);
+  }
+
+  if (warp < 4) {
+    // =============================== forward warps
+    const unsigned char* Wb = static_cast<const unsigned char*>(a.W);
+    PipeCursor ic, cc;  // issue / consume cursors over (chunk, row, slot)
+    pipe_cursor_init(ic, A, b0, nrows, warp);
+    pipe_cursor_init(cc, A, b0, nrows, warp);
+    int n_issued = 0, cnt = 0;
+    auto issue_one = [&]() {
+      if (ic.c >= A.C) return;
+      const int e = warp * RF + n_issued % RF;
+      if (lane == 0) {
+        const int32_t loc = A.row_locs[static_cast<size_t>(b0 + ic.r) * a.S + ic.j];
+        mbar_expect_tx(&ffull[e], PR::WB);
+        bulk_g2s(frings + e * PR::WB, Wb + static_cast<size_t>(loc) * PR::WB, PR::WB, &ffull[e]);
+      }
+      ++n_issued;
+      pipe_cursor_next(ic, A, b0, nrows, warp);
+    };
+    for (int t = 0; t < RF; ++t) issue_one();
+    double lsum = 0.0;
+    float pend_sc = 0.0f, pend_pt = 0.0f, pend_wn = 0.0f;
+    int c_pend = 0;
+    for (int c = 0; c < A.C; ++c) {
+      for (; cc.c == c; pipe_cursor_next(cc, A, b0, nrows, warp)) {
+        const int r = cc.r, b = b0 + r;
+        const int sl = A.row_slots[static_cast<size_t>(b) * a.S + cc.j];
+        const float* er = e_s + r * d;
+        float* gr = g_s + r * d;
+        const SlotMeta meta = slot_meta(a, b, sl);
+        const int k = cnt++, e = warp * RF + k % RF;
+        mbar_wait(&ffull[e], (k / RF) & 1);
+        float4 w[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          if constexpr (BF16) {
+            const uint2 u = *reinterpret_cast<const uint2*>(frings + e * PR::WB + (i * 128 + lane * 4) * 2);
+            w[i] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                               __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+          } else {
+            w[i] = *reinterpret_cast<const float4*>(frings + e * PR::WB + (i * 128 + lane * 4) * 4);
+          }
+        }
+        __syncwarp();
+        issue_one();  // the entry is in registers: refill it RF items ahead
+        float acc = 0.0f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const float4 x = *reinterpret_cast<const float4*>(er + i * 128 + lane * 4);
+          acc = fmaf(w[i].x, x.x, acc);
+          acc = fmaf(w[i].y, x.y, acc);
+          acc = fmaf(w[i].z, x.z, acc);
+          acc = fmaf(w[i].w, x.w, acc);
+        }
+        acc = warp_sum(acc);
+        float pt, wn;
+        const float f = slot_factor_meta(meta, acc, &pt, &wn);
+        if (lane == c_pend) {
+          pend_sc = acc;
+          pend_pt = pt;
+          pend_wn = wn;
+        }
+        if (++c_pend == 32) {
+          lsum += slot_loss(pend_sc, pend_pt, pend_wn);
+          c_pend = 0;
+        }
+        if (lane == 0) {
+          __stcg(a.factors + static_cast<size_t>(b) * a.S + sl, f);
+          row_fabs[r] += static_cast<double>(fabsf(f));
+        }
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          float4* gp = reinterpret_cast<float4*>(gr + i * 128 + lane * 4);
+          float4 g = *gp;
+          g.x = fmaf(f, w[i].x, g.x);
+          g.y = fmaf(f, w[i].y, g.y);
+          g.z = fmaf(f, w[i].z, g.z);
+          g.w = fmaf(f, w[i].w, g.w);
+          *gp = g;
+        }
+      }
+      // chunk c done by the CTA's four forward warps: publish it
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 0) publish(P.done + c);
+    }
+    if (lane < c_pend) lsum += slot_loss(pend_sc, pend_pt, pend_wn);
+    lsum = warp_sum(lsum);
+    if (lane == 0 && warp < nrows) a.loss_rows[b0 + warp] = lsum;  // warp partials, summed by finalize
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    bool bad = false;
+    for (int i = threadIdx.x; i < nrows * d; i += 128) {
+      float gk = g_s[i];
+      if (a.keep) gk = __fmul_rn(gk, a.keep[static_cast<size_t>(b0) * d + i]);
+      a.grad_emb[static_cast<size_t>(b0) * d + i] = gk;
+      bad |= !isfinite(gk);
+    }
+    if (bad) a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] = 1;
+    for (int r = threadIdx.x; r < nrows; r += 128) {
+      float m = 0.0f;
+      for (int k = 0; k < d; ++k) m = fmaxf(m, fabsf(e_s[r * d + k]));
+      a.bound_rows[b0 + r] = row_fabs[r] * static_cast<double>(m);  // the legacy overflow bound (status word 2)
+      if (r >= 4) a.loss_rows[b0 + r] = 0.0;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 0) publish(P.ready + 2);
+    return;
+  }
+
+  // =============================== update warps (4-7) + producer (8)
+  if (threadIdx.x == 128) spin_geq(P.ready + 0, G);
+  asm volatile("bar.sync 2, 160;" ::: "memory");
+  const double SF = *reinterpret_cast<volatile double*>(A.sf_acc);
+  const float EM = __uint_as_float(*reinterpret_cast<volatile unsigned*>(A.emax_acc));
+  const float WM = A.w_absmax ? *reinterpret_cast<volatile float*>(A.w_absmax) : INFINITY;
+  const bool safe = isfinite(SF) && isfinite(EM) && isfinite(WM) && SF * static_cast<double>(EM) < kFusedSafe &&
+                    SF * static_cast<double>(WM) < kFusedSafe;
+  if (!safe) {
+    // checked schedule: every forward, then every gradient, then the updates
+    if (threadIdx.x == 128) spin_geq(P.ready + 2, G);
+    asm volatile("bar.sync 2, 160;" ::: "memory");
+    bool ok = true;
+    float dummy = 0.0f;
+    for (int c = 0; c < A.C; ++c) {
+      uint32_t q0, q1;
+      pipe_share(A, c, q0, q1);
+      for (uint32_t uq = q0 + (warp - 4); uq < q1; uq += 5) ok &= fused_upd<NV, BF16, ADAM, true>(ua, uq, dummy, lane);
+    }
+    if (!ok && lane == 0) atomicExch(a.status + ASTRA_STATUS_NONFINITE_GRAD, 1);
+    asm volatile("bar.sync 2, 160;" ::: "memory");
+    if (threadIdx.x == 128) {
+      publish(P.ready + 1);
+      spin_geq(P.ready + 1, G);
+    }
+    asm volatile("bar.sync 2, 160;" ::: "memory");
+    if (*reinterpret_cast<volatile int32_t*>(a.status + ASTRA_STATUS_NONFINITE_GRAD) ||
+        *reinterpret_cast<volatile int32_t*>(a.status + ASTRA_STATUS_NONFINITE_GRAD_EMB))
+      return;
+  }
+  if (warp == 8) {
+    // ---------------- update producer: this CTA's share of each chunk, after its forwards
+    const unsigned char* Wb = static_cast<const unsigned char*>(a.W);
+    int i = 0;
+    for (int c = 0; c < A.C; ++c) {
+      if (lane == 0) spin_geq(P.done + c, G);
+      __syncwarp();
+      uint32_t q0, q1;
+      pipe_share(A, c, q0, q1);
+      for (uint32_t i0 = q0; i0 < q1; i0 += 32) {
+        const int32_t l_lane = i0 + lane < q1 ? ua.uniq[i0 + lane] : 0;
+        const int nb = static_cast<int>(min(32u, q1 - i0));
+        for (int jj = 0; jj < nb; ++jj) {
+          const size_t l = static_cast<size_t>(__shfl_sync(0xffffffffu, l_lane, jj));
+          if (lane == 0) {
+            const int r = i % RING;
+            mbar_wait(&uempty[r], ((i / RING) & 1) ^ 1);
+            mbar_expect_tx(&ufull[r], ROWB);
+            unsigned char* dst = uring + r * ROWB;
+            bulk_g2s(dst, Wb + l * RG::WB, RG::WB, &ufull[r]);
+            if constexpr (ADAM) {
+              bulk_g2s(dst + RG::WB, ua.m + l * d, RG::MB, &ufull[r]);
+              bulk_g2s(dst + RG::WB + RG::MB, ua.v + l * d, RG::MB, &ufull[r]);
+            }
+          }
+          ++i;
+          __syncwarp();
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- update consumers: label i of the CTA's sequence -> warp 4 + i % 4
+  const int uw = warp - 4;
+  float wmax = 0.0f;
+  int i = 0;
+  for (int c = 0; c < A.C; ++c) {
+    if (lane == 0) spin_geq(P.done + c, G);  // the chunk's factors are published
+    __syncwarp();
+    uint32_t q0, q1;
+    pipe_share(A, c, q0, q1);
+    for (uint32_t uq = q0; uq < q1; ++uq, ++i) {
+      if ((i & 3) != uw) continue;
+      const int r = i % RING;
+      const int32_t l = ua.uniq[uq];
+      const uint32_t start = ua.offsets[l], nn = ua.counts[l];
+      const int32_t reg = sort_segment(ua, start, nn, lane);
+      const size_t row = static_cast<size_t>(l) * d;
+      float4 g[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) g[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t j = 0; j < nn; ++j) {
+        const int32_t s0 = seg_slot(ua, start, nn, reg, j);
+        const float f0 = __ldcg(ua.factors + s0);
+        const float* e0 = ua.emb + static_cast<size_t>(s0 / ua.S) * d + lane * 4;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          const float4 x0 = *reinterpret_cast<const float4*>(e0 + q * 128);
+          g[q].x = __fadd_rn(g[q].x, __fmul_rn(f0, x0.x));
+          g[q].y = __fadd_rn(g[q].y, __fmul_rn(f0, x0.y));
+          g[q].z = __fadd_rn(g[q].z, __fmul_rn(f0, x0.z));
+          g[q].w = __fadd_rn(g[q].w, __fmul_rn(f0, x0.w));
+        }
+      }
+      mbar_wait(&ufull[r], (i / RING) & 1);
+      float4 p[NV];
+      float4 m4[ADAM ? NV : 1], v4[ADAM ? NV : 1];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        if constexpr (BF16) {
+          const uint2 u = *reinterpret_cast<const uint2*>(uring + r * ROWB + (q * 128 + lane * 4) * 2);
+          p[q] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                             __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+        } else {
+          p[q] = *reinterpret_cast<const float4*>(uring + r * ROWB + (q * 128 + lane * 4) * 4);
+        }
+        if constexpr (ADAM) {
+          m4[q] = *reinterpret_cast<const float4*>(uring + r * ROWB + RG::WB + (q * 128 + lane * 4) * 4);
+          v4[q] = *reinterpret_cast<const float4*>(uring + r * ROWB + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&uempty[r]);
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        float4 np;
+        const size_t el = row + q * 128 + lane * 4;
+        if constexpr (ADAM) {
+          np.x = upd_elem<true>(ua, p[q].x, g[q].x, &m4[q].x, &v4[q].x);
+          np.y = upd_elem<true>(ua, p[q].y, g[q].y, &m4[q].y, &v4[q].y);
+          np.z = upd_elem<true>(ua, p[q].z, g[q].z, &m4[q].z, &v4[q].z);
+          np.w = upd_elem<true>(ua, p[q].w, g[q].w, &m4[q].w, &v4[q].w);
+          *reinterpret_cast<float4*>(ua.m + el) = m4[q];
+          *reinterpret_cast<float4*>(ua.v + el) = v4[q];
+        } else {
+          np.x = upd_elem<false>(ua, p[q].x, g[q].x, nullptr, nullptr);
+          np.y = upd_elem<false>(ua, p[q].y, g[q].y, nullptr, nullptr);
+          np.z = upd_elem<false>(ua, p[q].z, g[q].z, nullptr, nullptr);
+          np.w = upd_elem<false>(ua, p[q].w, g[q].w, nullptr, nullptr);
+        }
+        if constexpr (BF16) {
+          uint2 o;
+          o.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
+          o.y = static_cast<uint32_t>(f32_to_bf16_bits(np.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.w)) << 16);
+          *reinterpret_cast<uint2*>(static_cast<uint16_t*>(ua.W) + el) = o;
+        } else {
+          *reinterpret_cast<float4*>(static_cast<float*>(ua.W) + el) = np;
+        }
+        wmax = fmaxf(wmax, absmax4(np));
+      }
+    }
+  }
+  push_wmax(ua, wmax, lane);
+}
+
+template <int NV, bool BF16, bool ADAM>
+int pipe_grid() {
+  static int g = -1;
+  if (g < 0) {
+    auto kern = step_pipe_kernel<NV, BF16, ADAM>;
+    constexpr size_t smem = PipeSmem<NV, BF16, ADAM>::TOTAL;
+    g = 0;
+    if (smem <= 227 * 1024) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPipeThreads, smem);
+      g = per_sm >= 1 ? num_sms() : 0;  // one CTA per SM
+    }
+  }
+  return g;
+}
+
+template <int NV, bool BF16, bool ADAM>
+int launch_pipe(const PipeArgs& P0, int grid, cudaStream_t st) {
+  auto kern = step_pipe_kernel<NV, BF16, ADAM>;
+  constexpr size_t smem = PipeSmem<NV, BF16, ADAM>::TOTAL;
+  PipeArgs P = P0;
+  void* args[] = {&P};
+  ASTRA_TRY(check_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kPipeThreads), args,
+                                                   smem, st),
+                       "launch step_pipe"));
+  ASTRA_LAUNCHED("step_pipe");
+  return ASTRA_OK;
+}
+
+template <bool BF16, bool ADAM>
+int pipe_grid_nv(int nv) {
+  switch (nv) {
+    case 1: return pipe_grid<1, BF16, ADAM>();
+    case 2: return pipe_grid<2, BF16, ADAM>();
+    case 4: return pipe_grid<4, BF16, ADAM>();
+    case 6: return pipe_grid<6, BF16, ADAM>();
+    case 8: return pipe_grid<8, BF16, ADAM>();
+  }
+  return 0;
+}
+
+template <bool BF16, bool ADAM>
+int launch_pipe_nv(int nv, const PipeArgs& P, int grid, cudaStream_t st) {
+  switch (nv) {
+    case 1: return launch_pipe<1, BF16, ADAM>(P, grid, st);
+    case 2: return launch_pipe<2, BF16, ADAM>(P, grid, st);
+    case 4: return launch_pipe<4, BF16, ADAM>(P, grid, st);
+    case 6: return launch_pipe<6, BF16, ADAM>(P, grid, st);
+    case 8: return launch_pipe<8, BF16, ADAM>(P, grid, st);
+  }
+  return ASTRA_ERR_CONFIG;
+}
+
 // apply_classifier_updates_arrays: explicit (ids, grads) form.
 __global__ void apply_check_kernel(const float* grads, int64_t n, int32_t* status) {
   bool bad = false;
@@ -1563,6 +2074,7 @@ int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
 }
 
 struct StepWs {
+  unsigned* pipe_ctr;  // [kMaxChunks] done counters + [4] ready counters of the pipelined step
   int32_t* row_slots;
   int32_t* row_locs;
   int32_t* row_cofs;
@@ -1607,6 +2119,7 @@ size_t carve_step(void* base, size_t cap, int B, int S, int64_t Lloc, StepWs* w)
   w->bar = c.take<unsigned>(4);  // bar, emax_acc, (pad), then the fp64 accumulator
   w->emax_acc = w->bar ? w->bar + 1 : nullptr;
   w->sf_acc = c.take<double>(1);
+  w->pipe_ctr = c.take<unsigned>(kMaxChunks + 4);
   return c.off;
 }
 
@@ -1672,12 +2185,27 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     const char* e = getenv("ASTRA_STEP_FUSED");
     return e ? atoi(e) : 0;
   }();
-  bool fused = fused_env && !factors_in && aligned && Lloc > 0 && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8);
+  const bool chunkable = !factors_in && aligned && Lloc > 0 && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8);
+  bool fused = fused_env && chunkable;
   if (fused) {
     const int max_rows = bf16 ? (adam ? fused_max_rows<true, true>(nv) : fused_max_rows<true, false>(nv))
                               : (adam ? fused_max_rows<false, true>(nv) : fused_max_rows<false, false>(nv));
     fused = B <= max_rows;
   }
+  static const int pipe_env = [] {
+    // ASTRA_STEP_PIPE=1: the pipelined (forward CTAs -> update CTAs) L2-chunked step
+    const char* e = getenv("ASTRA_STEP_PIPE");
+    return e ? atoi(e) : 0;
+  }();
+  int pipe_grid_ctas = 0, pipe_nf = 0;
+  if (!fused && pipe_env && chunkable) {
+    pipe_grid_ctas = bf16 ? (adam ? pipe_grid_nv<true, true>(nv) : pipe_grid_nv<true, false>(nv))
+                          : (adam ? pipe_grid_nv<false, true>(nv) : pipe_grid_nv<false, false>(nv));
+    pipe_nf = pipe_grid_ctas > 0 ? (B + pipe_grid_ctas - 1) / pipe_grid_ctas : 0;  // rows per CTA
+    if (pipe_nf == 0 || pipe_nf > kPipeRows) pipe_grid_ctas = 0;
+  }
+  const bool piped = pipe_grid_ctas > 0;
+  fused = fused || piped;  // both take the chunked preparation below
   if (!fused) {
     KernelTimer kt_fwd("slot_forward", st);
     if (aligned && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
@@ -1773,6 +2301,7 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     ASTRA_LAUNCHED("row_bucket");
     ASTRA_TRY(check_cuda(cudaMemsetAsync(w.bar, 0, 4 * sizeof(unsigned), st), "memset barrier"));
     ASTRA_TRY(check_cuda(cudaMemsetAsync(w.sf_acc, 0, sizeof(double), st), "memset bound"));
+    if (piped) ASTRA_TRY(check_cuda(cudaMemsetAsync(w.pipe_ctr, 0, sizeof(unsigned) * (kMaxChunks + 4), st), "memset pipe"));
     FusedArgs A;
     A.f = fa;
     A.u = ua;
@@ -1786,7 +2315,18 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     A.bar = w.bar;
     A.sf_acc = w.sf_acc;
     A.emax_acc = w.emax_acc;
-    {
+    if (piped) {
+      PipeArgs P;
+      P.x = A;
+      P.rows_f = pipe_nf;
+      P.done = w.pipe_ctr;
+      P.ready = w.pipe_ctr + kMaxChunks;
+      KernelTimer kt("step_pipe", st);
+      ASTRA_TRY(bf16 ? (adam ? launch_pipe_nv<true, true>(nv, P, pipe_grid_ctas, st)
+                             : launch_pipe_nv<true, false>(nv, P, pipe_grid_ctas, st))
+                     : (adam ? launch_pipe_nv<false, true>(nv, P, pipe_grid_ctas, st)
+                             : launch_pipe_nv<false, false>(nv, P, pipe_grid_ctas, st)));
+    } else {
       KernelTimer kt("step_fused", st);
       int rc = bf16 ? (adam ? launch_fused_nv<true, true>(nv, A, st) : launch_fused_nv<true, false>(nv, A, st))
                     : (adam ? launch_fused_nv<false, true>(nv, A, st) : launch_fused_nv<false, false>(nv, A, st));

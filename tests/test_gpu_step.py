@@ -243,7 +243,7 @@ def test_apply_updates_golden_bitexact(cuda_lib):
     np.testing.assert_array_equal(W2.cpu().numpy(), g["W_before"])
 
 
-@pytest.mark.parametrize("fused", ["0", "1"])
+@pytest.mark.parametrize("fused", ["0", "1", "pipe"])
 def test_engine_step_schedules_agree(cuda_lib, fused):
     """The engine step (w_absmax bound maintained) under the two-kernel TMA path
     and under the persistent L2-chunked schedule matches the reference
@@ -253,7 +253,8 @@ def test_engine_step_schedules_agree(cuda_lib, fused):
 
     code = f"""
 import os, sys
-os.environ["ASTRA_STEP_FUSED"] = "{fused}"
+os.environ["ASTRA_STEP_FUSED"] = "1" if "{fused}" == "1" else "0"
+os.environ["ASTRA_STEP_PIPE"] = "1" if "{fused}" == "pipe" else "0"
 sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {ROOT!r} + "/tests")
 import numpy as np, torch
 from oracle import xcmix_port as port
