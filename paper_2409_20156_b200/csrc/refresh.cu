@@ -704,7 +704,15 @@ struct TwoPass {
   int sel_max = 0;      // per-query select capacity (power of two)
 };
 
-constexpr int64_t kSampleStride = 16;
+// Tile stride of the sample pass (ASTRA_SAMPLE_STRIDE overrides; measurement aid).
+int64_t sample_stride() {
+  static const int64_t v = [] {
+    const char* e = getenv("ASTRA_SAMPLE_STRIDE");
+    const int64_t x = e ? atoll(e) : 16;
+    return x >= 2 && x <= 256 ? x : 16;
+  }();
+  return v;
+}
 constexpr int kSelMax = 4096;
 
 TwoPass plan_two_pass(int64_t nq, int64_t L, int kk, int n_parts) {
@@ -715,6 +723,7 @@ TwoPass plan_two_pass(int64_t nq, int64_t L, int kk, int n_parts) {
   }();
   const int64_t n_tiles = (L + kTcTileLabels - 1) / kTcTileLabels;
   if (force == 0 || kk > 512) return t;
+  const int64_t kSampleStride = sample_stride();
   if (n_tiles < kSampleStride * (force == 1 ? 1 : 32)) return t;  // small label sets: running top-k
   const double z = 5.0, m = static_cast<double>(kk) / kSampleStride;
   int j = static_cast<int>(std::ceil(std::pow(z / 2 + std::sqrt(z * z / 4 + m), 2.0)));
