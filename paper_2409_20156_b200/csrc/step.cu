@@ -1528,10 +1528,14 @@ struct PipeRing {
   static constexpr int RF = BF16 ? 12 : 6;  // self-fed entries per forward warp
 };
 
+constexpr int kPipeLag = 2;  // with throttling: the gather runs at most this many chunks ahead of the updates
+
 struct PipeArgs {
   FusedArgs x;
   int rows_f;
   unsigned* done;   // [C] CTAs whose forward finished chunk c
+  unsigned* udone;  // [C] CTAs whose updates finished chunk c
+  int throttle;
   unsigned* ready;  // [0] bounds published, [1] gradients checked (checked schedule), [2] forwards finished
 };
 
@@ -1682,23 +1686,41 @@ __global__ void __launch_bounds__(kPipeThreads, 1) step_pipe_kernel(PipeArgs P) 
 
   if (warp < 4) {
     // =============================== forward warps
+    // the same safety decision as the update warps: only the proven schedule
+    // interleaves (and throttles) the gather against the updates
+    if (threadIdx.x == 0) spin_geq(P.ready + 0, G);
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const double fSF = *reinterpret_cast<volatile double*>(A.sf_acc);
+    const float fEM = __uint_as_float(*reinterpret_cast<volatile unsigned*>(A.emax_acc));
+    const float fWM = A.w_absmax ? *reinterpret_cast<volatile float*>(A.w_absmax) : INFINITY;
+    // ASTRA_STEP_PIPE_THROTTLE=1 couples the gather to the updates (measured
+    // 3-5 ms per minibatch: the per-chunk grid-wide handshakes serialise)
+    const bool throttle = P.throttle && isfinite(fSF) && isfinite(fEM) && isfinite(fWM) &&
+                          fSF * static_cast<double>(fEM) < kFusedSafe && fSF * static_cast<double>(fWM) < kFusedSafe;
     const unsigned char* Wb = static_cast<const unsigned char*>(a.W);
     PipeCursor ic, cc;  // issue / consume cursors over (chunk, row, slot)
     pipe_cursor_init(ic, A, b0, nrows, warp);
     pipe_cursor_init(cc, A, b0, nrows, warp);
     int n_issued = 0, cnt = 0;
-    auto issue_one = [&]() {
-      if (ic.c >= A.C) return;
-      const int e = warp * RF + n_issued % RF;
-      if (lane == 0) {
-        const int32_t loc = A.row_locs[static_cast<size_t>(b0 + ic.r) * a.S + ic.j];
-        mbar_expect_tx(&ffull[e], PR::WB);
-        bulk_g2s(frings + e * PR::WB, Wb + static_cast<size_t>(loc) * PR::WB, PR::WB, &ffull[e]);
+    // keep up to RF rows in flight, never more than kPipeLag chunks ahead of the
+    // chunk being consumed; chunk x is gathered only once every CTA updated
+    // chunk x - kPipeLag (so the rows waiting for their update stay in L2).
+    // The wait can only involve chunks this CTA has finished (x - kPipeLag < cur).
+    auto refill = [&](int cur) {
+      while (n_issued - cnt < RF && ic.c < A.C && (!throttle || ic.c < cur + kPipeLag)) {
+        const int e = warp * RF + n_issued % RF;
+        if (lane == 0) {
+          if (throttle && ic.c >= kPipeLag) spin_geq(P.udone + ic.c - kPipeLag, G);
+          const int32_t loc = A.row_locs[static_cast<size_t>(b0 + ic.r) * a.S + ic.j];
+          mbar_expect_tx(&ffull[e], PR::WB);
+          bulk_g2s(frings + e * PR::WB, Wb + static_cast<size_t>(loc) * PR::WB, PR::WB, &ffull[e]);
+        }
+        __syncwarp();
+        ++n_issued;
+        pipe_cursor_next(ic, A, b0, nrows, warp);
       }
-      ++n_issued;
-      pipe_cursor_next(ic, A, b0, nrows, warp);
     };
-    for (int t = 0; t < RF; ++t) issue_one();
+    refill(0);
     double lsum = 0.0;
     float pend_sc = 0.0f, pend_pt = 0.0f, pend_wn = 0.0f;
     int c_pend = 0;
@@ -1709,7 +1731,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) step_pipe_kernel(PipeArgs P) 
         const float* er = e_s + r * d;
         float* gr = g_s + r * d;
         const SlotMeta meta = slot_meta(a, b, sl);
-        const int k = cnt++, e = warp * RF + k % RF;
+        const int k = cnt, e = warp * RF + k % RF;
         mbar_wait(&ffull[e], (k / RF) & 1);
         float4 w[NV];
 #pragma unroll
@@ -1723,7 +1745,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) step_pipe_kernel(PipeArgs P) 
           }
         }
         __syncwarp();
-        issue_one();  // the entry is in registers: refill it RF items ahead
+        ++cnt;
+        refill(c);  // the entry is in registers: refill the ring
         float acc = 0.0f;
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
@@ -1763,6 +1786,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) step_pipe_kernel(PipeArgs P) 
       // chunk c done by the CTA's four forward warps: publish it
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 0) publish(P.done + c);
+      refill(c + 1);  // the window moved
     }
     if (lane < c_pend) lsum += slot_loss(pend_sc, pend_pt, pend_wn);
     lsum = warp_sum(lsum);
@@ -1928,6 +1952,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) step_pipe_kernel(PipeArgs P) 
         wmax = fmaxf(wmax, absmax4(np));
       }
     }
+    // chunk c updated by the CTA's four update warps: release the gather of chunk c + kPipeLag
+    asm volatile("bar.sync 3, 128;" ::: "memory");
+    if (threadIdx.x == 128) publish(P.udone + c);
   }
   push_wmax(ua, wmax, lane);
 }
@@ -2074,7 +2101,7 @@ int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
 }
 
 struct StepWs {
-  unsigned* pipe_ctr;  // [kMaxChunks] done counters + [4] ready counters of the pipelined step
+  unsigned* pipe_ctr;  // [2 kMaxChunks] done / udone counters + [4] ready counters of the pipelined step
   int32_t* row_slots;
   int32_t* row_locs;
   int32_t* row_cofs;
@@ -2119,7 +2146,7 @@ size_t carve_step(void* base, size_t cap, int B, int S, int64_t Lloc, StepWs* w)
   w->bar = c.take<unsigned>(4);  // bar, emax_acc, (pad), then the fp64 accumulator
   w->emax_acc = w->bar ? w->bar + 1 : nullptr;
   w->sf_acc = c.take<double>(1);
-  w->pipe_ctr = c.take<unsigned>(kMaxChunks + 4);
+  w->pipe_ctr = c.take<unsigned>(2 * kMaxChunks + 4);
   return c.off;
 }
 
@@ -2301,7 +2328,8 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     ASTRA_LAUNCHED("row_bucket");
     ASTRA_TRY(check_cuda(cudaMemsetAsync(w.bar, 0, 4 * sizeof(unsigned), st), "memset barrier"));
     ASTRA_TRY(check_cuda(cudaMemsetAsync(w.sf_acc, 0, sizeof(double), st), "memset bound"));
-    if (piped) ASTRA_TRY(check_cuda(cudaMemsetAsync(w.pipe_ctr, 0, sizeof(unsigned) * (kMaxChunks + 4), st), "memset pipe"));
+    if (piped)
+      ASTRA_TRY(check_cuda(cudaMemsetAsync(w.pipe_ctr, 0, sizeof(unsigned) * (2 * kMaxChunks + 4), st), "memset pipe"));
     FusedArgs A;
     A.f = fa;
     A.u = ua;
@@ -2320,7 +2348,13 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
       P.x = A;
       P.rows_f = pipe_nf;
       P.done = w.pipe_ctr;
-      P.ready = w.pipe_ctr + kMaxChunks;
+      P.udone = w.pipe_ctr + kMaxChunks;
+      static const int throttle_env = [] {
+        const char* e = getenv("ASTRA_STEP_PIPE_THROTTLE");
+        return e ? atoi(e) : 0;
+      }();
+      P.throttle = throttle_env;
+      P.ready = w.pipe_ctr + 2 * kMaxChunks;
       KernelTimer kt("step_pipe", st);
       ASTRA_TRY(bf16 ? (adam ? launch_pipe_nv<true, true>(nv, P, pipe_grid_ctas, st)
                              : launch_pipe_nv<true, false>(nv, P, pipe_grid_ctas, st))
