@@ -568,58 +568,68 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
     total += c < cand_cap ? c : cand_cap;
   }
   bool fail = overflow || total > sel_max;
-  if (!fail) {
-    const int64_t p0 = pos_indptr[q], np = pos_indptr[q + 1] - p0;
-    // the query's positives in shared memory (binary searches there, not in L2)
-    __shared__ int32_t sel_pos[kSelWarps][kSelPos];
-    const bool pos_smem = np <= kSelPos;
-    if (pos_smem)
-      for (int e = lane; e < np; e += 32) sel_pos[warp][e] = pos_ids[p0 + e];
-    __syncwarp();
-    const int32_t* P = pos_smem ? sel_pos[warp] : pos_ids + p0;
-    int o = 0, valid = 0;
+  if (lane == 0 && fail) flags[q] = 1;
+  if (fail) return;
+  const int64_t p0 = pos_indptr[q], np = pos_indptr[q + 1] - p0;
+  // 1. the candidates -> shared memory (independent loads, no per-key work)
+  {
+    int o = 0;
     for (int p = 0; p < n_parts; ++p) {
       const int c = min(cand_cnt[static_cast<size_t>(p) * nq + q], cand_cap);
       const uint64_t* src = cand + (static_cast<size_t>(p) * nq + q) * cand_cap;
-      for (int e = lane; e < c; e += 32) {
-        uint64_t v = src[e];
-        if (np > 0 && sorted_contains(P, np, key_id(v))) v = 0ull;
-        S[o + e] = v;
-        valid += v != 0ull;
-      }
+#pragma unroll 4
+      for (int e = lane; e < c; e += 32) S[o + e] = src[e];
       o += c;
     }
-    fail = warp_sum(valid) < k;
   }
-  if (lane == 0) flags[q] = fail ? 1 : 0;
-  if (fail) return;
   __syncwarp();
-  // k-th largest score bits T: count(score >= T) >= k > count(score >= T + 1)
+  // 2. T2 = the (k + |P|)-th largest score over ALL candidates: at most |P| of
+  //    the keys above the k-th non-positive one are positives, so every key of
+  //    the non-positive top k is >= T2 (0 when there are fewer candidates)
   __shared__ uint32_t sel_hist[kSelWarps][256];
+  const int64_t k2l = static_cast<int64_t>(k) + np;
+  const int k2 = static_cast<int>(k2l < total ? k2l : total);
   const uint32_t T = warp_kth_largest(
       [&](int i, uint32_t& x) {
-        const uint64_t v = S[i];
-        x = static_cast<uint32_t>(v >> 32);
-        return v != 0ull;
+        x = static_cast<uint32_t>(S[i] >> 32);
+        return true;
       },
-      total, k, sel_hist[warp], lane);
-  // warp-aggregated compaction of the keys with score >= T (k plus score ties)
+      total, k2, sel_hist[warp], lane);
+  // 3. warp-aggregated compaction of the keys with score >= T2
   int nr = 0;
   for (int i0 = 0; i0 < total; i0 += 32) {
     const int i = i0 + lane;
     const uint64_t v = i < total ? S[i] : 0ull;
     const bool take = v != 0ull && static_cast<uint32_t>(v >> 32) >= T;
-    const unsigned b = __ballot_sync(0xffffffffu, take);
-    const int at = nr + __popc(b & ((1u << lane) - 1u));
+    const unsigned bm = __ballot_sync(0xffffffffu, take);
+    const int at = nr + __popc(bm & ((1u << lane) - 1u));
     if (take && at < kSelSmall) R[at] = v;
-    nr += __popc(b);
+    nr += __popc(bm);
   }
+  __syncwarp();
   uint64_t* X = R;
   int n = nr;
-  if (nr > kSelSmall) {  // pathological score ties: sort everything
+  if (nr > kSelSmall) {  // pathological score ties: work on every candidate
     X = S;
     n = total;
   }
+  // 4. drop the query's positives (anns.py:254-255) among them (positives in shared memory)
+  __shared__ int32_t sel_pos[kSelWarps][kSelPos];
+  const bool pos_smem = np <= kSelPos;
+  if (pos_smem)
+    for (int e = lane; e < np; e += 32) sel_pos[warp][e] = pos_ids[p0 + e];
+  __syncwarp();
+  const int32_t* Pp = pos_smem ? sel_pos[warp] : pos_ids + p0;
+  int valid = 0;
+  for (int e = lane; e < n; e += 32) {
+    uint64_t v = X[e];
+    if (v && np > 0 && sorted_contains(Pp, np, key_id(v))) X[e] = v = 0ull;
+    valid += v != 0ull;
+  }
+  fail = warp_sum(valid) < k;
+  if (lane == 0) flags[q] = fail ? 1 : 0;
+  if (fail) return;
+  __syncwarp();
   int Pn = 1;
   while (Pn < n) Pn <<= 1;
   for (int e = n + lane; e < Pn; e += 32) X[e] = 0ull;
