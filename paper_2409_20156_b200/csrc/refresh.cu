@@ -892,6 +892,7 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
   if (k < 1 || k > 2048) return set_error(ASTRA_ERR_CONFIG, "refresh: k=%d outside [1, 2048]", k);
   if (nq < 0 || L < 0 || d <= 0) return set_error(ASTRA_ERR_CONFIG, "refresh: bad shape");
   if (L + off >= (int64_t(1) << 31)) return set_error(ASTRA_ERR_CONFIG, "refresh: label ids exceed int32");
+  if (nq == 0) return ASTRA_OK;  // nothing to score (empty tensors may carry NULL pointers)
   if (mode == ASTRA_REFRESH_FP32_EXACT) {
     if (!qf || !wf) return set_error(ASTRA_ERR_CONFIG, "FP32_EXACT needs fp32 queries and labels");
   } else if (mode == ASTRA_REFRESH_BF16 || mode == ASTRA_REFRESH_BF16_RERANK) {

@@ -320,3 +320,59 @@ def test_host_api_pipelined_equals_device_api(cuda_lib):
         np.testing.assert_array_equal(host_out[-1][1], ge_d.cpu().numpy())
         assert host_out[-1][2] == float(loss_d.item())
     np.testing.assert_array_equal(a.W.cpu().numpy(), b.W.cpu().numpy())
+
+
+def test_adam_bf16_weights_d768(cuda_lib):
+    """bf16 W + Adam at d=768 (the C5 configuration; TMA ring entry = W row +
+    m row + v row): the update equals SparseAdam on the bf16 values, rounded."""
+    from paper_2409_20156_b200 import ops
+
+    L, d = 20_000, 768
+    W, emb, ids, y, origin, weights = _random_step(L, d, 24, 60, 77, n_hot=4)
+    Wb = dev(W).to(torch.bfloat16)
+    m = torch.zeros((L, d), dtype=torch.float32, device="cuda")
+    v = torch.zeros_like(m)
+    param = torch.nn.Parameter(Wb.float().cpu().clone())
+    opt = torch.optim.SparseAdam([param], lr=0.003, betas=(0.9, 0.999), eps=1e-8)
+    rng = np.random.default_rng(1)
+    for step in (1, 2):
+        factors = rng.standard_normal(ids.shape).astype(np.float32)
+        uids, grads = port.per_label_gradient(ids, factors, emb, L)
+        param.grad = torch.sparse_coo_tensor(torch.from_numpy(uids)[None], torch.from_numpy(grads), (L, d))
+        opt.step()
+        with torch.no_grad():  # the bf16 weights are what the next step reads
+            param.copy_(param.to(torch.bfloat16).float())
+        ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wb, 0.003, 0.0,
+                       factors_in=dev(factors), optimizer="adam", adam_m=m, adam_v=v, adam_step=step)
+        torch.cuda.synchronize()
+        got = Wb.float().cpu().numpy()
+        ref = param.detach().numpy()
+        close(got, ref, rtol=1e-2, floor=1e-4)  # within a bf16 ulp where the fp32 updates differ in the last bit
+        assert (got == ref).mean() > 0.99
+
+
+def test_empty_batch_and_slate(cuda_lib):
+    from paper_2409_20156_b200 import ops
+
+    W = dev(np.ones((100, 128), np.float32))
+    for B, S in ((0, 10), (4, 0)):
+        emb = torch.ones((B, 128), device="cuda")
+        ids = torch.zeros((B, S), dtype=torch.int32, device="cuda")
+        y = torch.zeros((B, S), dtype=torch.int8, device="cuda")
+        res = ops.slate_step(emb, ids, y, torch.zeros(S, dtype=torch.int8, device="cuda"),
+                             torch.ones(S, device="cuda"), W, 0.1, 0.0)
+        assert res.loss == 0.0 and res.grad_emb.shape == (B, 128)
+        if B:
+            assert float(res.grad_emb.abs().max()) == 0.0
+    assert float((W - 1).abs().max()) == 0.0
+
+
+def test_refresh_empty_query_batch(cuda_lib):
+    from paper_2409_20156_b200 import ops
+
+    W = dev(np.ones((1000, 128), np.float32))
+    keys, ids, scores = ops.refresh_topk(torch.zeros((0, 128), device="cuda"),
+                                         torch.zeros(1, dtype=torch.int64, device="cuda"),
+                                         torch.zeros(0, dtype=torch.int32, device="cuda"), 8, "bf16_rerank",
+                                         labels_f32=W, labels_bf16=ops.f32_to_bf16(W))
+    assert ids.shape == (0, 8)
