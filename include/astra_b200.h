@@ -87,6 +87,16 @@ void astra_kernel_timing_enable(int on);
  * running concurrently on the main stream — the B200 form of the reference's
  * background refresh thread (trainer.py:198-214). Process-wide setting. */
 void astra_set_refresh_sm_budget(int n_sms);
+
+/* Step schedule (process-wide). on = 0 (default): for d % 128 == 0 (d <= 768)
+ * with a w_absmax bound, astra_slate_step runs ONE label-major pass that reads
+ * and writes each touched W row once and adds each slot's f * W_row into
+ * grad_emb with fp32 vector reductions: W', the loss and the factors are
+ * deterministic (W' bit-identical to the two-kernel schedule), grad_emb's
+ * summation order is not. on = 1: the two-kernel schedule (slot-major gather
+ * forward, then the label-major update), bitwise run-to-run deterministic.
+ * The environment variable ASTRA_STEP_SINGLE=0 is equivalent to on = 1. */
+void astra_set_step_deterministic(int on);
 int astra_kernel_timing(const char* name, double* total_ms, int64_t* count);
 
 /* fp32 -> bf16 (round-to-nearest-even), n elements. Used for W/query snapshots. */

@@ -28,6 +28,7 @@ _SIGS = {
     "astra_kernel_timing_enable": ([i32], None),
     "astra_kernel_timing": ([C.c_char_p, p, p], i32),
     "astra_set_refresh_sm_budget": ([i32], None),
+    "astra_set_step_deterministic": ([i32], None),
     "astra_f32_to_bf16": ([p, p, i64, p], i32),
     "astra_refresh_workspace_size": ([i64, i64, i32, i32, i32], sz),
     "astra_refresh_topk": ([p, p, i64, i32, p, p, i64, i64, p, p, i32, i32, p, p, p, p, sz, p], i32),
@@ -78,6 +79,13 @@ def kernel_timing_enable(on: bool = True) -> None:
 def set_refresh_sm_budget(n_sms: int) -> None:
     """Cap the SMs the refresh GEMM occupies (0 = all)."""
     load().astra_set_refresh_sm_budget(int(n_sms))
+
+
+def set_step_deterministic(on: bool) -> None:
+    """True: the bitwise run-to-run deterministic two-kernel step schedule;
+    False (default): the single label-major pass (grad_emb summed with fp32
+    reductions in arrival order)."""
+    load().astra_set_step_deterministic(1 if on else 0)
 
 
 def kernel_timing(name: str):

@@ -66,6 +66,7 @@ int sample_slates(uint64_t, uint32_t, uint32_t, const int64_t*, int, const int64
                   int, int, const int32_t*, const float*, int, int, int, int64_t, int, int, int32_t*, int8_t*,
                   int8_t*, float*, cudaStream_t);
 size_t step_workspace_size(int, int, int, int64_t);
+void set_step_deterministic(int on);
 int slate_step(const float*, const float*, const int32_t*, const int8_t*, const int8_t*, int64_t, const float*,
                int64_t, const float*, int, int, int, void*, int, float*, float*, int, int64_t, int64_t, double, double,
                double, double, double, int64_t, float*, double*, int32_t*, float*, float*, void*, size_t, cudaStream_t);
@@ -87,6 +88,7 @@ uint64_t astra_launch_count(void) { return g_launches.load(); }
 void astra_kernel_timing_enable(int on) { g_kt_on.store(on != 0); }
 
 void astra_set_refresh_sm_budget(int n_sms) { set_refresh_sm_budget(n_sms); }
+void astra_set_step_deterministic(int on) { set_step_deterministic(on); }
 
 int astra_kernel_timing(const char* name, double* total_ms, int64_t* count) {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;

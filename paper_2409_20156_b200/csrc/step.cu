@@ -19,6 +19,7 @@
 // reference raises NumericalError before writing (classifiers.py:79-80,
 // encoder.py:145-146). Step 2 proves finiteness from a bound in the common
 // case; otherwise a check pass (label_check) runs first.
+#include <atomic>
 #include <limits.h>
 #include <math.h>
 
@@ -40,6 +41,7 @@ constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
 constexpr int kUpdThreads = 256;
 constexpr double kBoundSafe = 1e37;
+constexpr double kSingleSafe = 1e30;  // single-pass schedule: bound on every |gradient| entry
 
 struct FwdArgs {
   const float* emb;
@@ -59,6 +61,7 @@ struct FwdArgs {
   double* loss_rows;
   double* bound_rows;
   int32_t* status;
+  const int32_t* skip = nullptr;  // != null and *skip: the single-pass schedule ran (kernel returns)
 };
 
 __device__ __forceinline__ float expit_f32(float x) {
@@ -183,6 +186,7 @@ __device__ void forward_tail(const FwdArgs& a, int b, float* red, double lsum, d
 // Vectorised forward: d = NV * 128, each lane owns NV float4 of the row.
 template <int NV, bool BF16>
 __global__ void __launch_bounds__(kFwdThreads, 1) slot_forward_vec(FwdArgs a) {
+  if (a.skip && *a.skip) return;
   __shared__ __align__(16) float red[kFwdWarps * NV * 128];
   __shared__ float s_emax[kFwdWarps];
   const int b = blockIdx.x;
@@ -284,6 +288,7 @@ constexpr size_t tma_fwd_smem(int S) {
 
 template <int NV, bool BF16>
 __global__ void __launch_bounds__(kTmaThreads, 3) slot_forward_tma(FwdArgs a) {
+  if (a.skip && *a.skip) return;
   constexpr int d = NV * 128;
   constexpr int RING = tma_ring<BF16>();
   constexpr uint32_t ROWB = d * (BF16 ? 2 : 4);
@@ -456,6 +461,7 @@ __global__ void __launch_bounds__(kTmaThreads, 3) slot_forward_tma(FwdArgs a) {
 // Generic forward for any d: emb and the per-warp partials live in shared memory.
 template <bool BF16>
 __global__ void __launch_bounds__(kFwdThreads) slot_forward_generic(FwdArgs a) {
+  if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) float sm[];
   float* e = sm;                 // d
   float* red = sm + a.d;         // kFwdWarps * d
@@ -534,14 +540,52 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const double* loss_rows,
 
 // ---------------------------------------------------------------- counting sort
 
-__global__ void count_kernel(const int32_t* ids, int64_t n, int64_t off, int64_t Lloc, uint32_t* counts,
-                             int32_t* rank, int32_t* status) {
+// Also (sf_acc != null, the single-pass schedule) the finiteness bounds:
+// sum over owned slots of (1 + |weight|) and max|emb| (+inf if non-finite).
+__global__ void __launch_bounds__(256) count_kernel(const int32_t* ids, int64_t n, int64_t off, int64_t Lloc,
+                                                    uint32_t* counts, int32_t* rank, int32_t* status,
+                                                    const float* weights, int64_t wstride, int S, const float* emb,
+                                                    int64_t n_emb, double* sf_acc, unsigned* emax_acc) {
+  double sf = 0.0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int32_t id = ids[i];
     if (id < 0) status[ASTRA_STATUS_ID_RANGE] = 1;
     int64_t loc = static_cast<int64_t>(id) - off;
-    rank[i] = (loc >= 0 && loc < Lloc) ? static_cast<int32_t>(atomicAdd(counts + loc, 1u)) : -1;
+    const bool own = loc >= 0 && loc < Lloc;
+    rank[i] = own ? static_cast<int32_t>(atomicAdd(counts + loc, 1u)) : -1;
+    if (sf_acc && own) {
+      const int b = static_cast<int>(i) / S;  // (n < 2^31)
+      const float wt = weights[b * wstride + (static_cast<int>(i) - b * S)];
+      sf += 1.0 + (isfinite(wt) ? fabs(static_cast<double>(wt)) : INFINITY);
+    }
+  }
+  if (!sf_acc) return;
+  float em = 0.0f;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_emb;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float e = emb[i];
+    em = fmaxf(em, isfinite(e) ? fabsf(e) : INFINITY);
+  }
+  __shared__ double s_sf[8];
+  __shared__ float s_em[8];
+  sf = warp_sum(sf);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) em = fmaxf(em, __shfl_xor_sync(0xffffffffu, em, o));
+  if ((threadIdx.x & 31) == 0) {
+    s_sf[threadIdx.x >> 5] = sf;
+    s_em[threadIdx.x >> 5] = em;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    float m = 0.0f;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      t += s_sf[w];
+      m = fmaxf(m, s_em[w]);
+    }
+    if (t != 0.0) atomicAdd(sf_acc, t);
+    atomicMax(emax_acc, __float_as_uint(m));  // non-negative floats order as their bits
   }
 }
 
@@ -577,8 +621,10 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_
 }
 
 // Exclusive scan of the per-block sums (single CTA), writes U.
+// (mode != null: also decides the step schedule from count_kernel's bounds.)
 __global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* blk_slots, uint32_t* blk_nz, int nb,
-                                                        uint32_t* U) {
+                                                        uint32_t* U, const double* sf_acc, const unsigned* emax_acc,
+                                                        const float* w_absmax, int32_t* mode) {
   __shared__ uint32_t cs[1024], cn[1024];
   const int per = (nb + 1023) / 1024;
   const int lo = threadIdx.x * per, hi = min(nb, lo + per);
@@ -607,12 +653,19 @@ __global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* blk_slots, uin
     rc += vc;
   }
   if (threadIdx.x == 1023) *U = cn[1023];
+  if (mode && threadIdx.x == 0) {
+    const double SF = *sf_acc;
+    const float EM = __uint_as_float(*emax_acc);
+    const float WM = w_absmax ? *w_absmax : INFINITY;
+    *mode = isfinite(SF) && isfinite(EM) && isfinite(WM) && SF * static_cast<double>(EM) < kSingleSafe &&
+            SF * static_cast<double>(WM) < kSingleSafe;
+  }
 }
 
 __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* counts, int64_t Lloc,
                                                                   const uint32_t* blk_slots,
                                                                   const uint32_t* blk_nz, uint32_t* offsets,
-                                                                  int32_t* uniq) {
+                                                                  int32_t* uniq, uint32_t* ustart, uint32_t* ucnt) {
   __shared__ uint32_t ws[kScanThreads / 32], wn[kScanThreads / 32];
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + static_cast<int64_t>(threadIdx.x) * kScanItems;
   uint32_t c[kScanItems];
@@ -652,7 +705,14 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
     int64_t l = base + i;
     if (l < Lloc) {
       offsets[l] = ps;
-      if (c[i]) uniq[pn++] = static_cast<int32_t>(l);
+      if (c[i]) {
+        uniq[pn] = static_cast<int32_t>(l);
+        if (ustart) {
+          ustart[pn] = ps;
+          ucnt[pn] = c[i];
+        }
+        ++pn;
+      }
       ps += c[i];
     }
   }
@@ -686,6 +746,7 @@ struct UpdArgs {
   float c1, c2, eps, neg_step;  // Adam: fp32(1-b1), fp32(1-b2), eps, fp32(-lr*sqrt(bc2)/bc1)
   int32_t* status;
   float* w_absmax;  // running max|W| bound kept current by every update kernel (or null)
+  const int32_t* skip = nullptr;  // as FwdArgs::skip
 };
 
 // Fold a warp's max |new W| into the running bound (non-negative floats order as bits).
@@ -766,6 +827,7 @@ __device__ __forceinline__ void store_p(void* W, size_t el, float v) {
 // CHECK_ONLY: compute every gradient, flag non-finite ones, write nothing.
 template <bool BF16, bool ADAM, bool CHECK_ONLY>
 __global__ void __launch_bounds__(kUpdThreads) label_update_kernel(UpdArgs a) {
+  if (a.skip && *a.skip) return;
   const int lane = threadIdx.x & 31;
   if (CHECK_ONLY) {
     if (!a.status[ASTRA_STATUS_BOUND_UNSAFE]) return;  // finiteness already proven
@@ -775,6 +837,7 @@ __global__ void __launch_bounds__(kUpdThreads) label_update_kernel(UpdArgs a) {
   const uint32_t U = *a.U;
   const int d = a.d;
   const uint32_t warps = gridDim.x * (kUpdThreads / 32);
+  float wmax = 0.0f;
   for (uint32_t u = blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5); u < U; u += warps) {
     const int32_t l = a.uniq[u];
     const uint32_t start = a.offsets[l], n = a.counts[l];
@@ -798,16 +861,19 @@ __global__ void __launch_bounds__(kUpdThreads) label_update_kernel(UpdArgs a) {
           float p = load_p<BF16>(a.W, row + k + t);
           float np = upd_elem<ADAM>(a, p, g[t], ADAM ? a.m + row + k + t : nullptr, ADAM ? a.v + row + k + t : nullptr);
           store_p<BF16>(a.W, row + k + t, np);
+          wmax = fmaxf(wmax, fabsf(np));
         }
       }
     }
     if (CHECK_ONLY && __any_sync(0xffffffffu, bad)) a.status[ASTRA_STATUS_NONFINITE_GRAD] = 1;
   }
+  if (!CHECK_ONLY) push_wmax(a, wmax, lane);
 }
 
 // Vectorised update for d % 128 == 0 (NV float4 per lane), fp32 or bf16 W.
 template <int NV, bool BF16, bool ADAM>
 __global__ void __launch_bounds__(kUpdThreads) label_update_vec(UpdArgs a) {
+  if (a.skip && *a.skip) return;
   const int lane = threadIdx.x & 31;
   if (a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] || a.status[ASTRA_STATUS_NONFINITE_GRAD]) return;
   const uint32_t U = *a.U;
@@ -922,6 +988,7 @@ struct UpdRing {
 
 template <int NV, bool BF16, bool ADAM>
 __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(UpdArgs a) {
+  if (a.skip && *a.skip) return;
   constexpr int d = NV * 128;
   using RG = UpdRing<NV, BF16, ADAM>;
   constexpr int RING = RG::RING;
@@ -1067,6 +1134,414 @@ __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(Up
     }
   }
   push_wmax(a, wmax, lane);
+}
+
+// ================================================================ single-pass step
+// The default schedule for d % 128 == 0: ONE label-major pass over the touched
+// rows. Each CTA owns a contiguous chunk of the sorted unique-label list; a
+// producer lane streams the chunk's W rows (+ Adam m, v) into a shared-memory
+// ring with bulk copies; consumer warp w takes labels w, w+4, ... For label l
+// it holds the OLD row in registers and walks l's slots in ascending b*S+s
+// order: score = <emb_b, W_l> (the forward's fma order and butterfly, so the
+// same bits), factor (trainer.py:369-380), g += f * emb_b (label_update's
+// order and roundings, so W' is bit-identical to the two-kernel schedule), and
+// grad_emb[b] += f * W_l (vector fp32 reductions into the L2-resident B x d
+// buffer, red.global.add.v4.f32); then it writes the updated row. DRAM sees
+// each touched row read once and written once (U*d*(2*w_W + 2*s_opt)), instead
+// of the gather's extra B*S*d*w_W read.
+//
+// Finiteness (classifiers.py:79-80: nothing is written when a gradient is
+// non-finite) is proven before the pass from bounds that need no scores:
+// S_f = sum over owned slots of (1 + |weight|) >= sum |factor|, so every label
+// gradient is <= S_f * max|emb| and every grad_emb entry <= S_f * max|W|
+// (max|W|: the running bound w_absmax). count_kernel accumulates S_f and
+// max|emb|, scan_top_kernel decides (mode = 1: this pass; 0: the two-kernel
+// schedule, whose kernels are launched too and return at once when mode = 1).
+// grad_emb's summation order over slots follows the reduction order, so it is
+// not bitwise run-to-run deterministic (ASTRA_STEP_SINGLE=0 selects the
+// deterministic two-kernel schedule); the loss is reduced per row in slot
+// order by single_row_finalize from the stored scores.
+struct SingleArgs {
+  FwdArgs f;
+  UpdArgs u;
+  float* scores;          // [B*S] score of every owned slot
+  const int32_t* mode;    // decided by scan_top_kernel
+  const uint32_t* ustart; // [U] bucket start of unique label u (= offsets[uniq[u]])
+  const uint32_t* ucnt;   // [U] its occurrence count
+};
+
+__device__ __forceinline__ void red_add_v4(float* p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+// loss terms of a slot from its metadata (slot_factor_meta without the sigmoid)
+__device__ __forceinline__ void slot_terms(const SlotMeta& m, float* pt, float* wn) {
+  const bool pos_slot = m.o == ASTRA_ORIGIN_POS;
+  *pt = pos_slot ? m.yf : 0.0f;
+  *wn = __fmul_rn(m.w, pos_slot ? 0.0f : __fsub_rn(1.0f, m.yf));
+}
+
+template <int NV>
+__device__ __forceinline__ void load_emb_row(const float* emb, int b, int lane, float4 (&e)[NV]) {
+  const float* p = emb + static_cast<size_t>(b) * (NV * 128) + lane * 4;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) e[q] = *reinterpret_cast<const float4*>(p + q * 128);
+}
+
+// Ring geometry of the single pass: one entry = the W row (+ Adam m, v), and a
+// 32-byte descriptor per entry written by the producer (its own barrier, so a
+// consumer reads it before the row lands and prefetches the embedding rows).
+template <int NV, bool BF16, bool ADAM>
+struct SingleRing {
+  static constexpr uint32_t WB = NV * 128 * (BF16 ? 2 : 4);
+  static constexpr uint32_t MB = ADAM ? NV * 128 * 4 : 0;
+  static constexpr uint32_t ENTRY = WB + 2 * MB;
+  static constexpr int CTAS = ADAM ? 2 : 3;
+  static constexpr int RING_MAX = static_cast<int>((ADAM ? 96u * 1024 : 62u * 1024) / (ENTRY + 56));
+  static constexpr int RING = RING_MAX > 32 ? 32 : RING_MAX;
+  static constexpr size_t smem() { return static_cast<size_t>(RING) * (ENTRY + 32 + 24); }
+};
+
+// The producer's per-label descriptor: bucket, first occurrence and its metadata.
+struct SingleDesc {
+  int32_t l;
+  uint32_t start, n;
+  int32_t slot0;
+  float yf0, w0;
+  int32_t o0;
+  int32_t pad;
+};
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Pull a d-float embedding row into L1 (lane i: its 128-byte line(s)).
+template <int NV>
+__device__ __forceinline__ void prefetch_emb_l1(const float* emb, int b, int lane) {
+  const char* row = reinterpret_cast<const char*>(emb + static_cast<size_t>(b) * (NV * 128));
+  for (int c = lane; c < NV * 4; c += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(row + c * 128));
+}
+
+template <int NV, bool BF16, bool ADAM>
+__global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS) step_single_tma(SingleArgs A) {
+  constexpr int d = NV * 128;
+  using RG = SingleRing<NV, BF16, ADAM>;
+  constexpr int RING = RG::RING;
+  constexpr uint32_t ROWB = RG::ENTRY;
+  extern __shared__ __align__(128) unsigned char usm[];
+  unsigned char* ring = usm;
+  SingleDesc* desc = reinterpret_cast<SingleDesc*>(usm + RING * ROWB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(desc + RING);
+  uint64_t* empty = full + RING;
+  uint64_t* dfull = empty + RING;
+  if (!*A.mode) return;
+  const UpdArgs& a = A.u;
+  const FwdArgs& fa = A.f;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t U = *a.U;
+  const uint32_t chunk = (U + gridDim.x - 1) / gridDim.x;
+  const uint32_t u0 = min(U, blockIdx.x * chunk), u1 = min(U, u0 + chunk);
+  const int n_mine = static_cast<int>(u1 - u0);
+  if (n_mine == 0) return;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < RING; ++r) {
+      mbar_init(&full[r], 1);
+      mbar_init(&empty[r], 1);
+      mbar_init(&dfull[r], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int S = fa.S;
+  if (warp == kTmaConsumers) {
+    // producer warp: 32 labels per batch, every index load lane-parallel and
+    // software-pipelined over batches (batch k+3: bucket, k+2: first
+    // occurrence, k+1: its metadata, while batch k's descriptors and copies
+    // (W row, Adam moments) are issued in ring order)
+    const unsigned char* Wb = static_cast<const unsigned char*>(a.W);
+    struct PIdx {
+      int32_t l;
+      uint32_t start, n;
+      int32_t slot0;
+    };
+    auto idx_load = [&](int i0, PIdx& q) {
+      q.l = 0;
+      q.start = q.n = 0;
+      q.slot0 = 0;
+      if (i0 + lane < n_mine) {
+        const uint32_t u = u0 + i0 + lane;
+        q.l = a.uniq[u];
+        q.start = A.ustart[u];
+        q.n = A.ucnt[u];
+      }
+    };
+    auto perm_load = [&](int i0, PIdx& q) {
+      if (i0 + lane < n_mine) q.slot0 = a.perm[q.start];
+    };
+    auto meta_load = [&](int i0, const PIdx& q, SingleDesc& dl) {
+      dl.l = q.l;
+      dl.start = q.start;
+      dl.n = q.n;
+      dl.slot0 = q.slot0;
+      dl.yf0 = dl.w0 = 0.0f;
+      dl.o0 = 0;
+      dl.pad = 0;
+      if (i0 + lane < n_mine) {
+        const int b0 = q.slot0 / S;
+        const SlotMeta m = slot_meta(fa, b0, q.slot0 - b0 * S);
+        dl.yf0 = m.yf;
+        dl.w0 = m.w;
+        dl.o0 = m.o;
+      }
+    };
+    PIdx q1, q2, q3;
+    SingleDesc cur;
+    idx_load(0, q1);
+    perm_load(0, q1);
+    meta_load(0, q1, cur);
+    idx_load(32, q1);
+    perm_load(32, q1);
+    idx_load(64, q2);
+    for (int i0 = 0; i0 < n_mine; i0 += 32) {
+      SingleDesc nxt;
+      meta_load(i0 + 32, q1, nxt);
+      perm_load(i0 + 64, q2);
+      idx_load(i0 + 96, q3);
+      const int nb = min(32, n_mine - i0);
+      for (int jj = 0; jj < nb; ++jj) {
+        if (lane == jj) {
+          const int i = i0 + jj, r = i % RING;
+          mbar_wait(&empty[r], ((i / RING) & 1) ^ 1);
+          desc[r] = cur;
+          mbar_arrive(&dfull[r]);
+          mbar_expect_tx(&full[r], ROWB);
+          unsigned char* dst = ring + r * ROWB;
+          const size_t lz = static_cast<size_t>(cur.l);
+          bulk_g2s(dst, Wb + lz * RG::WB, RG::WB, &full[r]);
+          if constexpr (ADAM) {
+            bulk_g2s(dst + RG::WB, a.m + lz * d, RG::MB, &full[r]);
+            bulk_g2s(dst + RG::WB + RG::MB, a.v + lz * d, RG::MB, &full[r]);
+          }
+        }
+        __syncwarp();
+      }
+      cur = nxt;
+      q1 = q2;
+      q2 = q3;
+    }
+    return;
+  }
+  float wmax = 0.0f;
+  if (warp < n_mine) {  // the first label's embedding row towards L1
+    mbar_wait(&dfull[warp % RING], (warp / RING) & 1);
+    prefetch_emb_l1<NV>(fa.emb, desc[warp % RING].slot0 / S, lane);
+  }
+  for (int i = warp; i < n_mine; i += kTmaConsumers) {
+    const int r = i % RING;
+    mbar_wait(&dfull[r], (i / RING) & 1);
+    const SingleDesc dc = desc[r];
+    // the first occurrence's embedding row (prefetched into L1 one label ago)
+    float4 e0[NV];
+    load_emb_row<NV>(fa.emb, dc.slot0 / S, lane, e0);
+    {  // the next label's row towards L1, if its descriptor is already there
+      const int in = i + kTmaConsumers;
+      if (in < n_mine && mbar_test(&dfull[in % RING], (in / RING) & 1))
+        prefetch_emb_l1<NV>(fa.emb, desc[in % RING].slot0 / S, lane);
+    }
+    mbar_wait(&full[r], (i / RING) & 1);
+    const unsigned char* ent = ring + r * ROWB;
+    float4 p[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      if constexpr (BF16) {
+        const uint2 u = *reinterpret_cast<const uint2*>(ent + (q * 128 + lane * 4) * 2);
+        p[q] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                           __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+      } else {
+        p[q] = *reinterpret_cast<const float4*>(ent + (q * 128 + lane * 4) * 4);
+      }
+    }
+    const uint32_t n = dc.n;
+    // slots in ascending b*S+s order (the two-kernel update's summation order)
+    const int32_t reg = n == 1 ? dc.slot0 : sort_segment(a, dc.start, n, lane);
+    const bool small = n <= 32;
+    SlotMeta my;
+    my.o = static_cast<int8_t>(dc.o0);
+    my.yf = dc.yf0;
+    my.w = dc.w0;
+    if (n > 1 && small && lane < static_cast<int>(n) && reg != dc.slot0) my = slot_meta(fa, reg / S, reg - (reg / S) * S);
+    float4 g[NV];
+    float my_sc = 0.0f;
+    for (uint32_t j = 0; j < n; ++j) {
+      const int32_t slot = n == 1 ? dc.slot0 : seg_slot(a, dc.start, n, reg, j);
+      const int b = slot / S, s = slot - b * S;
+      float4 e[NV];
+      if (slot == dc.slot0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) e[q] = e0[q];
+      } else {
+        load_emb_row<NV>(fa.emb, b, lane, e);
+      }
+      float acc = 0.0f;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        acc = fmaf(p[q].x, e[q].x, acc);
+        acc = fmaf(p[q].y, e[q].y, acc);
+        acc = fmaf(p[q].z, e[q].z, acc);
+        acc = fmaf(p[q].w, e[q].w, acc);
+      }
+      acc = warp_sum(acc);
+      SlotMeta m;
+      if (n == 1) {
+        m = my;
+      } else if (small) {
+        m.o = static_cast<int8_t>(__shfl_sync(0xffffffffu, static_cast<int>(my.o), static_cast<int>(j)));
+        m.yf = __shfl_sync(0xffffffffu, my.yf, static_cast<int>(j));
+        m.w = __shfl_sync(0xffffffffu, my.w, static_cast<int>(j));
+      } else {
+        m = slot_meta(fa, b, s);
+      }
+      float pt, wn;
+      const float f = slot_factor_meta(m, acc, &pt, &wn);
+      if (small) {
+        if (lane == static_cast<int>(j)) my_sc = acc;
+      } else if (lane == 0) {
+        A.scores[slot] = acc;
+      }
+      if (lane == 0) fa.factors[slot] = f;
+      if (j == 0) {  // 0 + x = x (up to the sign of a zero)
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+          g[q] = make_float4(__fmul_rn(f, e[q].x), __fmul_rn(f, e[q].y), __fmul_rn(f, e[q].z), __fmul_rn(f, e[q].w));
+      } else {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          g[q].x = __fadd_rn(g[q].x, __fmul_rn(f, e[q].x));
+          g[q].y = __fadd_rn(g[q].y, __fmul_rn(f, e[q].y));
+          g[q].z = __fadd_rn(g[q].z, __fmul_rn(f, e[q].z));
+          g[q].w = __fadd_rn(g[q].w, __fmul_rn(f, e[q].w));
+        }
+      }
+      if (f != 0.0f) {  // warp-uniform; dead slots (f = 0) add nothing to grad_emb
+        float* ge = fa.grad_emb + static_cast<size_t>(b) * d + lane * 4;
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+          red_add_v4(ge + q * 128, make_float4(__fmul_rn(f, p[q].x), __fmul_rn(f, p[q].y), __fmul_rn(f, p[q].z),
+                                               __fmul_rn(f, p[q].w)));
+      }
+    }
+    if (small && lane < static_cast<int>(n)) A.scores[n == 1 ? dc.slot0 : reg] = my_sc;
+    if constexpr (!ADAM) {  // W row consumed (Adam: after the moments, below)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[r]);
+    }
+    const size_t row = static_cast<size_t>(dc.l) * d;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      float4 np;
+      const size_t el = row + q * 128 + lane * 4;
+      if constexpr (ADAM) {
+        float4 m4 = *reinterpret_cast<const float4*>(ent + RG::WB + (q * 128 + lane * 4) * 4);
+        float4 v4 = *reinterpret_cast<const float4*>(ent + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
+        np.x = upd_elem<true>(a, p[q].x, g[q].x, &m4.x, &v4.x);
+        np.y = upd_elem<true>(a, p[q].y, g[q].y, &m4.y, &v4.y);
+        np.z = upd_elem<true>(a, p[q].z, g[q].z, &m4.z, &v4.z);
+        np.w = upd_elem<true>(a, p[q].w, g[q].w, &m4.w, &v4.w);
+        *reinterpret_cast<float4*>(a.m + el) = m4;
+        *reinterpret_cast<float4*>(a.v + el) = v4;
+      } else {
+        np.x = upd_elem<false>(a, p[q].x, g[q].x, nullptr, nullptr);
+        np.y = upd_elem<false>(a, p[q].y, g[q].y, nullptr, nullptr);
+        np.z = upd_elem<false>(a, p[q].z, g[q].z, nullptr, nullptr);
+        np.w = upd_elem<false>(a, p[q].w, g[q].w, nullptr, nullptr);
+      }
+      if constexpr (BF16) {
+        uint2 o;
+        o.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
+        o.y = static_cast<uint32_t>(f32_to_bf16_bits(np.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.w)) << 16);
+        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(a.W) + el) = o;
+      } else {
+        *reinterpret_cast<float4*>(static_cast<float*>(a.W) + el) = np;
+      }
+      wmax = fmaxf(wmax, absmax4(np));
+    }
+    if constexpr (ADAM) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[r]);
+    }
+  }
+  push_wmax(a, wmax, lane);
+}
+
+// Per-row tail of the single pass: the row's fp64 loss over its owned slots in
+// slot order (from the stored scores), the keep scale and finiteness check of
+// grad_emb. bound_rows = 0: finiteness was proven up front.
+constexpr int kRowFinThreads = 256;
+__global__ void __launch_bounds__(kRowFinThreads) single_row_finalize(FwdArgs a, const float* scores,
+                                                                      const int32_t* mode) {
+  if (!*mode) return;
+  __shared__ double sl[kRowFinThreads / 32];
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double l = 0.0;
+  for (int s = threadIdx.x; s < a.S; s += kRowFinThreads) {
+    const size_t slot = static_cast<size_t>(b) * a.S + s;
+    const int64_t loc = static_cast<int64_t>(a.ids[slot]) - a.off;
+    if (loc >= 0 && loc < a.Lloc) {
+      float pt, wn;
+      slot_terms(slot_meta(a, b, s), &pt, &wn);
+      l += slot_loss(scores[slot], pt, wn);
+    }
+  }
+  l = warp_sum(l);
+  if (lane == 0) sl[warp] = l;
+  bool bad = false;
+  float* ge = a.grad_emb + static_cast<size_t>(b) * a.d;
+  for (int k = threadIdx.x; k < a.d; k += kRowFinThreads) {
+    float gk = ge[k];
+    if (a.keep) {
+      gk = __fmul_rn(gk, a.keep[static_cast<size_t>(b) * a.d + k]);
+      ge[k] = gk;
+    }
+    bad |= !isfinite(gk);
+  }
+  if (bad) a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kRowFinThreads / 32; ++w) t += sl[w];
+    a.loss_rows[b] = t;
+    a.bound_rows[b] = 0.0;
+  }
+}
+
+template <int NV, bool BF16, bool ADAM>
+void launch_single_tma(const SingleArgs& A, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(step_single_tma<NV, BF16, ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  using RG = SingleRing<NV, BF16, ADAM>;
+  step_single_tma<NV, BF16, ADAM><<<RG::CTAS * num_sms(), kTmaThreads, RG::smem(), st>>>(A);
+}
+
+template <bool BF16, bool ADAM>
+void launch_single_nv(int nv, const SingleArgs& A, cudaStream_t st) {
+  switch (nv) {
+    case 1: launch_single_tma<1, BF16, ADAM>(A, st); break;
+    case 2: launch_single_tma<2, BF16, ADAM>(A, st); break;
+    case 4: launch_single_tma<4, BF16, ADAM>(A, st); break;
+    case 6: launch_single_tma<6, BF16, ADAM>(A, st); break;
+  }
 }
 
 // ================================================================ fused step
@@ -2121,6 +2596,10 @@ struct StepWs {
   uint32_t* U;
   double* loss_rows;
   double* bound_rows;
+  int32_t* mode;
+  float* scores;
+  uint32_t* ustart;
+  uint32_t* ucnt;
 };
 
 size_t carve_step(void* base, size_t cap, int B, int S, int64_t Lloc, StepWs* w) {
@@ -2147,10 +2626,18 @@ size_t carve_step(void* base, size_t cap, int B, int S, int64_t Lloc, StepWs* w)
   w->emax_acc = w->bar ? w->bar + 1 : nullptr;
   w->sf_acc = c.take<double>(1);
   w->pipe_ctr = c.take<unsigned>(2 * kMaxChunks + 4);
+  w->mode = c.take<int32_t>(4);
+  w->scores = c.take<float>(n);
+  w->ustart = c.take<uint32_t>(n < Lloc ? n : Lloc);
+  w->ucnt = c.take<uint32_t>(n < Lloc ? n : Lloc);
   return c.off;
 }
 
 }  // namespace
+
+std::atomic<int> g_step_deterministic{0};
+
+void set_step_deterministic(int on) { g_step_deterministic.store(on ? 1 : 0); }
 
 size_t step_workspace_size(int B, int S, int d, int64_t Lloc) {
   (void)d;
@@ -2233,57 +2720,42 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
   }
   const bool piped = pipe_grid_ctas > 0;
   fused = fused || piped;  // both take the chunked preparation below
-  if (!fused) {
-    KernelTimer kt_fwd("slot_forward", st);
-    if (aligned && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
-      switch (nv * 2 + (bf16 ? 1 : 0)) {
-        case 2: launch_forward_vec<1, false>(fa, st); break;
-        case 3: launch_forward_vec<1, true>(fa, st); break;
-        case 4: launch_forward_vec<2, false>(fa, st); break;
-        case 5: launch_forward_vec<2, true>(fa, st); break;
-        case 8: launch_forward_vec<4, false>(fa, st); break;
-        case 9: launch_forward_vec<4, true>(fa, st); break;
-        case 12: launch_forward_vec<6, false>(fa, st); break;
-        case 13: launch_forward_vec<6, true>(fa, st); break;
-        case 16: launch_forward_vec<8, false>(fa, st); break;
-        case 17: launch_forward_vec<8, true>(fa, st); break;
-      }
-    } else {
-      size_t smem = sizeof(float) * static_cast<size_t>(d) * (1 + kFwdWarps);
-      if (smem > 200 * 1024) return set_error(ASTRA_ERR_CONFIG, "slate_step: d=%d too large", d);
-      if (bf16) {
-        cudaFuncSetAttribute(slot_forward_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        slot_forward_generic<true><<<B, kFwdThreads, smem, st>>>(fa);
-      } else {
-        cudaFuncSetAttribute(slot_forward_generic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        slot_forward_generic<false><<<B, kFwdThreads, smem, st>>>(fa);
-      }
-    }
-    ASTRA_LAUNCHED("slot_forward");
-  }
-  if (!fused) {
-    finalize_kernel<<<1, 1024, 0, st>>>(w.loss_rows, w.bound_rows, B, loss_out, status);
-    ASTRA_LAUNCHED("finalize");
-  }
+  static const bool single_env = [] {
+    // ASTRA_STEP_SINGLE=0: the deterministic two-kernel schedule (gather forward,
+    // then label-major update) instead of the single label-major pass
+    const char* e = getenv("ASTRA_STEP_SINGLE");
+    return e ? atoi(e) != 0 : true;
+  }();
+  const bool single = !fused && single_env && !g_step_deterministic.load() && chunkable &&
+                      nv <= 6;  // (nv = 8 spills: two-kernel schedule)
+  if (single) fa.skip = w.mode;
 
-  // counting sort of the slots by local label id
+  // counting sort of the slots by local label id (+ the single pass's bounds and decision)
   const int64_t n = static_cast<int64_t>(B) * S;
   const int64_t nb = (Lloc + kScanTile - 1) / kScanTile;
-  if (Lloc == 0) return ASTRA_OK;
   if (nb > 1024 * 1024) return set_error(ASTRA_ERR_CONFIG, "label shard too large");
   const int sms = num_sms();
   const int grid_n = static_cast<int>(std::min<int64_t>((n + 255) / 256, 8LL * sms));
-  ASTRA_TRY(check_cuda(cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * Lloc, st), "memset counts"));
-  count_kernel<<<grid_n, 256, 0, st>>>(ids, n, off, Lloc, w.counts, w.rank, status);
-  ASTRA_LAUNCHED("count");
-  scan_reduce_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz);
-  ASTRA_LAUNCHED("scan_reduce");
-  scan_top_kernel<<<1, 1024, 0, st>>>(w.blk_slots, w.blk_nz, static_cast<int>(nb), w.U);
-  ASTRA_LAUNCHED("scan_top");
-  scan_apply_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz, w.offsets, w.uniq);
-  ASTRA_LAUNCHED("scan_apply");
-  scatter_kernel<<<grid_n, 256, 0, st>>>(ids, w.rank, n, off, w.offsets, w.perm);
-  ASTRA_LAUNCHED("scatter");
+  if (Lloc > 0) {
+    ASTRA_TRY(check_cuda(cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * Lloc, st), "memset counts"));
+    if (single) {
+      ASTRA_TRY(check_cuda(cudaMemsetAsync(w.bar, 0, 4 * sizeof(unsigned), st), "memset bounds"));
+      ASTRA_TRY(check_cuda(cudaMemsetAsync(w.sf_acc, 0, sizeof(double), st), "memset bound"));
+    }
+    count_kernel<<<grid_n, 256, 0, st>>>(ids, n, off, Lloc, w.counts, w.rank, status, weights, weights_stride, S, emb,
+                                         static_cast<int64_t>(B) * d, single ? w.sf_acc : nullptr, w.emax_acc);
+    ASTRA_LAUNCHED("count");
+    scan_reduce_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz);
+    ASTRA_LAUNCHED("scan_reduce");
+    scan_top_kernel<<<1, 1024, 0, st>>>(w.blk_slots, w.blk_nz, static_cast<int>(nb), w.U, w.sf_acc, w.emax_acc,
+                                        w_absmax, single ? w.mode : nullptr);
+    ASTRA_LAUNCHED("scan_top");
+    scan_apply_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz, w.offsets,
+                                                                     w.uniq, single ? w.ustart : nullptr, w.ucnt);
+    ASTRA_LAUNCHED("scan_apply");
+    scatter_kernel<<<grid_n, 256, 0, st>>>(ids, w.rank, n, off, w.offsets, w.perm);
+    ASTRA_LAUNCHED("scatter");
+  }
 
   UpdArgs ua;
   ua.emb = emb;
@@ -2313,6 +2785,61 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     ua.neg_step = static_cast<float>(-(lr * sqrt(bc2) / bc1));
   }
   ua.w_absmax = w_absmax;
+  ua.skip = single ? w.mode : nullptr;
+  if (single) {
+    ASTRA_TRY(check_cuda(cudaMemsetAsync(grad_emb, 0, sizeof(float) * B * d, st), "memset grad_emb"));
+    SingleArgs SA;
+    SA.f = fa;
+    SA.u = ua;
+    SA.scores = w.scores;
+    SA.mode = w.mode;
+    SA.ustart = w.ustart;
+    SA.ucnt = w.ucnt;
+    KernelTimer kt("step_single", st);
+    if (bf16)
+      adam ? launch_single_nv<true, true>(nv, SA, st) : launch_single_nv<true, false>(nv, SA, st);
+    else
+      adam ? launch_single_nv<false, true>(nv, SA, st) : launch_single_nv<false, false>(nv, SA, st);
+    ASTRA_LAUNCHED("step_single");
+  }
+  if (!fused) {
+    KernelTimer kt_fwd("slot_forward", st);
+    if (aligned && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
+      switch (nv * 2 + (bf16 ? 1 : 0)) {
+        case 2: launch_forward_vec<1, false>(fa, st); break;
+        case 3: launch_forward_vec<1, true>(fa, st); break;
+        case 4: launch_forward_vec<2, false>(fa, st); break;
+        case 5: launch_forward_vec<2, true>(fa, st); break;
+        case 8: launch_forward_vec<4, false>(fa, st); break;
+        case 9: launch_forward_vec<4, true>(fa, st); break;
+        case 12: launch_forward_vec<6, false>(fa, st); break;
+        case 13: launch_forward_vec<6, true>(fa, st); break;
+        case 16: launch_forward_vec<8, false>(fa, st); break;
+        case 17: launch_forward_vec<8, true>(fa, st); break;
+      }
+    } else {
+      size_t smem = sizeof(float) * static_cast<size_t>(d) * (1 + kFwdWarps);
+      if (smem > 200 * 1024) return set_error(ASTRA_ERR_CONFIG, "slate_step: d=%d too large", d);
+      if (bf16) {
+        cudaFuncSetAttribute(slot_forward_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        slot_forward_generic<true><<<B, kFwdThreads, smem, st>>>(fa);
+      } else {
+        cudaFuncSetAttribute(slot_forward_generic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        slot_forward_generic<false><<<B, kFwdThreads, smem, st>>>(fa);
+      }
+    }
+    ASTRA_LAUNCHED("slot_forward");
+  }
+  if (single) {
+    single_row_finalize<<<B, kRowFinThreads, 0, st>>>(fa, w.scores, w.mode);
+    ASTRA_LAUNCHED("single_row_finalize");
+  }
+  if (!fused) {
+    finalize_kernel<<<1, 1024, 0, st>>>(w.loss_rows, w.bound_rows, B, loss_out, status);
+    ASTRA_LAUNCHED("finalize");
+  }
+
+  if (Lloc == 0) return ASTRA_OK;
   if (fused) {
     // label chunks of ~24 MB of touched rows (+ Adam state) each: they stay in L2
     // between their gather (phase p) and their update (phase p+1)

@@ -32,6 +32,9 @@ def one(i):
 for i in range(3):
     one(i)
 torch.cuda.synchronize()
+from paper_2409_20156_b200 import _lib  # noqa: E402
+
+_lib.kernel_timing_enable(True)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 import time  # noqa: E402
 
@@ -47,3 +50,5 @@ print(f"host {1e3 * (h1 - h0) / n:.3f} ms/minibatch (python + launches, no sync)
 U = int(torch.unique(sl[0]).numel())
 byts = U * d * 8 + 2 * B * d * 4 + B * (k_p + k_h + k_r) * 5
 print(f"step {ms:.3f} ms/minibatch  U={U}  {byts / ms / 1e6:.0f} GB/s algorithmic ({byts / 1e9:.2f} GB)")
+kt = {k: _lib.kernel_timing(k) for k in ("step_single", "slot_forward", "label_update")}
+print("kernels  " + "  ".join(f"{k} {ms / max(c, 1):.3f} ms" for k, (ms, c) in kt.items()))
