@@ -231,7 +231,7 @@ def run_ours(args):
     eng.comm.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
-    for name in ("refresh_gemm", "slot_forward", "label_update"):
+    for name in ("refresh_gemm", "step_single", "slot_forward", "label_update"):
         _lib.kernel_timing(name)  # drop warm-up records
     _lib.kernel_timing_enable(True)
     t_start = torch.cuda.Event(enable_timing=True)
@@ -246,7 +246,7 @@ def run_ours(args):
     clk = clocks.stop()
     launches = _lib.launch_count() - launches0
     _lib.kernel_timing_enable(False)
-    kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "slot_forward", "label_update")}
+    kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "step_single", "slot_forward", "label_update")}
     ops.raise_for_step_status(status)
     ms_t = torch.tensor([t_start.elapsed_time(t_end)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -279,11 +279,24 @@ def run_ours(args):
     t_samp = ph["sample"] / (K * M) / 1e3
     step_gbs = step_bytes / t_step / 1e9
     # per-kernel HBM rates of the step (algorithmic bytes per launch / live event time)
+    sgl_ms, sgl_n = kt["step_single"]
     fwd_ms, fwd_n = kt["slot_forward"]
     upd_ms, upd_n = kt["label_update"]
     fwd_bytes = B * world * S * d * 4 + B * world * d * 4 * 2  # gathered rows + emb + grad_emb
     upd_bytes = U_mean * d * 4 * 2  # each touched row read + written once (emb rows come from L2)
     traffic = _ncu_traffic()
+    rate = lambda nbytes, ms_, n_: round(nbytes / (ms_ / max(n_, 1) / 1e3) / 1e9, 1)  # noqa: E731
+    if sgl_n:  # the single label-major pass (default); the two-kernel launches are no-ops
+        step_kernel_desc = "minibatch step (counting sort + single label-major pass: scores, loss, grad_emb, SGD row update)"
+        step_kernels = {"step_single": {"launch_ms": round(sgl_ms / sgl_n, 4), "achieved_gbs": rate(upd_bytes, sgl_ms, sgl_n),
+                                        "algorithmic_bytes": int(upd_bytes), "traffic": traffic.get("step_single")}}
+    else:
+        step_kernel_desc = "minibatch step (gather/loss/grad + counting sort + fused SGD row update)"
+        step_kernels = {
+            "slot_forward": {"launch_ms": round(fwd_ms / max(fwd_n, 1), 4), "achieved_gbs": rate(fwd_bytes, fwd_ms, fwd_n),
+                             "algorithmic_bytes": int(fwd_bytes), "traffic": traffic.get("slot_forward")},
+            "label_update": {"launch_ms": round(upd_ms / max(upd_n, 1), 4), "achieved_gbs": rate(upd_bytes, upd_ms, upd_n),
+                             "algorithmic_bytes": int(upd_bytes), "traffic": traffic.get("label_update")}}
     # end-to-end: the public API with HOST buffers (pinned), copies inside the timed region
     pinned = []
     for t in range(n_steps):
@@ -344,19 +357,11 @@ def run_ours(args):
                      "launch_ms": round(t_gemm * 1e3, 4), "launches": gemm_n,
                      "share_of_refresh": round(t_gemm / t_ref, 4),
                      "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)"},
-        "roofline_step": {"bound": "hbm", "kernel": "minibatch step (gather/loss/grad + counting sort + fused SGD row update)",
+        "roofline_step": {"bound": "hbm", "kernel": step_kernel_desc,
                           "achieved": round(step_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(step_gbs / hbm, 4),
                           "algorithmic": f"U*d*8 + 2*B*d*4 + B*S*5 = {step_bytes:.3e} B (U={U_mean:.0f})",
                           "peak_kind": peak_kind,
-                          "kernels": {
-                              "slot_forward": {"launch_ms": round(fwd_ms / max(fwd_n, 1), 4),
-                                               "achieved_gbs": round(fwd_bytes / (fwd_ms / max(fwd_n, 1) / 1e3) / 1e9, 1),
-                                               "algorithmic_bytes": int(fwd_bytes),
-                                               "traffic": traffic.get("slot_forward")},
-                              "label_update": {"launch_ms": round(upd_ms / max(upd_n, 1), 4),
-                                               "achieved_gbs": round(upd_bytes / (upd_ms / max(upd_n, 1) / 1e3) / 1e9, 1),
-                                               "algorithmic_bytes": int(upd_bytes),
-                                               "traffic": traffic.get("label_update")}}},
+                          "kernels": step_kernels},
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -400,6 +405,7 @@ def run_c5shard(args):
         W[lo:hi] = ((torch.rand((hi - lo, d), device="cuda", generator=g) * 2 - 1) / d ** 0.5).to(torch.bfloat16)
     m = torch.zeros((L, d), dtype=torch.float32, device="cuda")
     v = torch.zeros_like(m)
+    w_absmax = W.abs().max().float().reshape(1)  # running max|W| bound (kept by the step kernels)
     snap = W.clone()
     n_steps = args.warmup + args.steps
     data = []
@@ -426,14 +432,14 @@ def run_c5shard(args):
                                cand_q=cand_q, k_i=c["k_i"])
         e[2].record(stream)
         res = ops.slate_step(emb, *sl, W, c["lr"], c["wd"], optimizer="adam", adam_m=m, adam_v=v, adam_step=t + 1,
-                             label_offset=0)
+                             label_offset=0, w_absmax=w_absmax)
         e[3].record(stream)
         return res, sl
 
     for t in range(args.warmup):
         one(t)
     torch.cuda.synchronize()
-    for name in ("refresh_gemm", "slot_forward", "label_update"):
+    for name in ("refresh_gemm", "step_single", "slot_forward", "label_update"):
         _lib.kernel_timing(name)
     _lib.kernel_timing_enable(True)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -443,7 +449,7 @@ def run_c5shard(args):
     t1.record(stream)
     torch.cuda.synchronize()
     _lib.kernel_timing_enable(False)
-    kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "slot_forward", "label_update")}
+    kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "step_single", "slot_forward", "label_update")}
     ops.raise_for_step_status(res.status)
     K = args.steps
     ms = t0.elapsed_time(t1) / K
