@@ -13,7 +13,8 @@ import threading
 from .errors import raise_for_status
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libastra_b200.so")
+# (ASTRA_LIB_VARIANT=x loads libastra_b200_x.so: in-tree A/B builds for experiments)
+LIB_PATH = os.path.join(HERE, "libastra_b200" + (f"_{os.environ['ASTRA_LIB_VARIANT']}" if os.environ.get("ASTRA_LIB_VARIANT") else "") + ".so")
 
 _lib = None
 _lock = threading.Lock()

@@ -1189,6 +1189,9 @@ __device__ __forceinline__ void load_emb_row(const float* emb, int b, int lane, 
   for (int q = 0; q < NV; ++q) e[q] = *reinterpret_cast<const float4*>(p + q * 128);
 }
 
+#ifndef ASTRA_SINGLE_CTAS
+#define ASTRA_SINGLE_CTAS 4
+#endif
 // Ring geometry of the single pass: one entry = the W row (+ Adam m, v), and a
 // 32-byte descriptor per entry written by the producer (its own barrier, so a
 // consumer reads it before the row lands and prefetches the embedding rows).
@@ -1197,10 +1200,12 @@ struct SingleRing {
   static constexpr uint32_t WB = NV * 128 * (BF16 ? 2 : 4);
   static constexpr uint32_t MB = ADAM ? NV * 128 * 4 : 0;
   static constexpr uint32_t ENTRY = WB + 2 * MB;
-  static constexpr int CTAS = ADAM ? 2 : 3;
-  static constexpr int RING_MAX = static_cast<int>((ADAM ? 96u * 1024 : 62u * 1024) / (ENTRY + 56));
+  static constexpr uint32_t SCRATCH = kTmaConsumers * NV * 128 * 4;  // per-warp gradient of multi-slot labels
+  static constexpr int CTAS = ADAM ? 2 : ASTRA_SINGLE_CTAS;
+  static constexpr uint32_t BUDGET = ADAM ? 110u * 1024 : (ASTRA_SINGLE_CTAS == 5 ? 44u : 56u) * 1024;
+  static constexpr int RING_MAX = static_cast<int>((BUDGET - SCRATCH) / (ENTRY + 56));
   static constexpr int RING = RING_MAX > 32 ? 32 : RING_MAX;
-  static constexpr size_t smem() { return static_cast<size_t>(RING) * (ENTRY + 32 + 24); }
+  static constexpr size_t smem() { return static_cast<size_t>(RING) * (ENTRY + 32 + 24) + SCRATCH; }
 };
 
 // The producer's per-label descriptor: bucket, first occurrence and its metadata.
@@ -1239,7 +1244,8 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
   extern __shared__ __align__(128) unsigned char usm[];
   unsigned char* ring = usm;
   SingleDesc* desc = reinterpret_cast<SingleDesc*>(usm + RING * ROWB);
-  uint64_t* full = reinterpret_cast<uint64_t*>(desc + RING);
+  float* gs_all = reinterpret_cast<float*>(desc + RING);
+  uint64_t* full = reinterpret_cast<uint64_t*>(gs_all + kTmaConsumers * d);
   uint64_t* empty = full + RING;
   uint64_t* dfull = empty + RING;
   if (!*A.mode) return;
@@ -1370,66 +1376,41 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       }
     }
     const uint32_t n = dc.n;
-    // slots in ascending b*S+s order (the two-kernel update's summation order)
-    const int32_t reg = n == 1 ? dc.slot0 : sort_segment(a, dc.start, n, lane);
-    const bool small = n <= 32;
-    SlotMeta my;
-    my.o = static_cast<int8_t>(dc.o0);
-    my.yf = dc.yf0;
-    my.w = dc.w0;
-    if (n > 1 && small && lane < static_cast<int>(n) && reg != dc.slot0) my = slot_meta(fa, reg / S, reg - (reg / S) * S);
-    float4 g[NV];
-    float my_sc = 0.0f;
-    for (uint32_t j = 0; j < n; ++j) {
-      const int32_t slot = n == 1 ? dc.slot0 : seg_slot(a, dc.start, n, reg, j);
-      const int b = slot / S, s = slot - b * S;
-      float4 e[NV];
-      if (slot == dc.slot0) {
-#pragma unroll
-        for (int q = 0; q < NV; ++q) e[q] = e0[q];
-      } else {
-        load_emb_row<NV>(fa.emb, b, lane, e);
-      }
-      float acc = 0.0f;
+    const size_t row = static_cast<size_t>(dc.l) * d;
+    // the row update, element by element, from the label's gradient G(q)
+    auto update_row = [&](auto G) {
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
-        acc = fmaf(p[q].x, e[q].x, acc);
-        acc = fmaf(p[q].y, e[q].y, acc);
-        acc = fmaf(p[q].z, e[q].z, acc);
-        acc = fmaf(p[q].w, e[q].w, acc);
-      }
-      acc = warp_sum(acc);
-      SlotMeta m;
-      if (n == 1) {
-        m = my;
-      } else if (small) {
-        m.o = static_cast<int8_t>(__shfl_sync(0xffffffffu, static_cast<int>(my.o), static_cast<int>(j)));
-        m.yf = __shfl_sync(0xffffffffu, my.yf, static_cast<int>(j));
-        m.w = __shfl_sync(0xffffffffu, my.w, static_cast<int>(j));
-      } else {
-        m = slot_meta(fa, b, s);
-      }
-      float pt, wn;
-      const float f = slot_factor_meta(m, acc, &pt, &wn);
-      if (small) {
-        if (lane == static_cast<int>(j)) my_sc = acc;
-      } else if (lane == 0) {
-        A.scores[slot] = acc;
-      }
-      if (lane == 0) fa.factors[slot] = f;
-      if (j == 0) {  // 0 + x = x (up to the sign of a zero)
-#pragma unroll
-        for (int q = 0; q < NV; ++q)
-          g[q] = make_float4(__fmul_rn(f, e[q].x), __fmul_rn(f, e[q].y), __fmul_rn(f, e[q].z), __fmul_rn(f, e[q].w));
-      } else {
-#pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          g[q].x = __fadd_rn(g[q].x, __fmul_rn(f, e[q].x));
-          g[q].y = __fadd_rn(g[q].y, __fmul_rn(f, e[q].y));
-          g[q].z = __fadd_rn(g[q].z, __fmul_rn(f, e[q].z));
-          g[q].w = __fadd_rn(g[q].w, __fmul_rn(f, e[q].w));
+        const float4 gq = G(q);
+        float4 np;
+        const size_t el = row + q * 128 + lane * 4;
+        if constexpr (ADAM) {
+          float4 m4 = *reinterpret_cast<const float4*>(ent + RG::WB + (q * 128 + lane * 4) * 4);
+          float4 v4 = *reinterpret_cast<const float4*>(ent + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
+          np.x = upd_elem<true>(a, p[q].x, gq.x, &m4.x, &v4.x);
+          np.y = upd_elem<true>(a, p[q].y, gq.y, &m4.y, &v4.y);
+          np.z = upd_elem<true>(a, p[q].z, gq.z, &m4.z, &v4.z);
+          np.w = upd_elem<true>(a, p[q].w, gq.w, &m4.w, &v4.w);
+          *reinterpret_cast<float4*>(a.m + el) = m4;
+          *reinterpret_cast<float4*>(a.v + el) = v4;
+        } else {
+          np.x = upd_elem<false>(a, p[q].x, gq.x, nullptr, nullptr);
+          np.y = upd_elem<false>(a, p[q].y, gq.y, nullptr, nullptr);
+          np.z = upd_elem<false>(a, p[q].z, gq.z, nullptr, nullptr);
+          np.w = upd_elem<false>(a, p[q].w, gq.w, nullptr, nullptr);
         }
+        if constexpr (BF16) {
+          uint2 o;
+          o.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
+          o.y = static_cast<uint32_t>(f32_to_bf16_bits(np.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.w)) << 16);
+          *reinterpret_cast<uint2*>(static_cast<uint16_t*>(a.W) + el) = o;
+        } else {
+          *reinterpret_cast<float4*>(static_cast<float*>(a.W) + el) = np;
+        }
+        wmax = fmaxf(wmax, absmax4(np));
       }
+    };
+    auto grad_emb_add = [&](int b, float f) {
       if (f != 0.0f) {  // warp-uniform; dead slots (f = 0) add nothing to grad_emb
         float* ge = fa.grad_emb + static_cast<size_t>(b) * d + lane * 4;
 #pragma unroll
@@ -1437,41 +1418,97 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
           red_add_v4(ge + q * 128, make_float4(__fmul_rn(f, p[q].x), __fmul_rn(f, p[q].y), __fmul_rn(f, p[q].z),
                                                __fmul_rn(f, p[q].w)));
       }
-    }
-    if (small && lane < static_cast<int>(n)) A.scores[n == 1 ? dc.slot0 : reg] = my_sc;
-    if constexpr (!ADAM) {  // W row consumed (Adam: after the moments, below)
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[r]);
-    }
-    const size_t row = static_cast<size_t>(dc.l) * d;
+    };
+    if (n == 1) {
+      // ---- one occurrence (most labels): score, factor, grad_emb, then the
+      // update straight from f * emb (0 + x = x, up to the sign of a zero)
+      float acc = 0.0f;
 #pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      float4 np;
-      const size_t el = row + q * 128 + lane * 4;
-      if constexpr (ADAM) {
-        float4 m4 = *reinterpret_cast<const float4*>(ent + RG::WB + (q * 128 + lane * 4) * 4);
-        float4 v4 = *reinterpret_cast<const float4*>(ent + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
-        np.x = upd_elem<true>(a, p[q].x, g[q].x, &m4.x, &v4.x);
-        np.y = upd_elem<true>(a, p[q].y, g[q].y, &m4.y, &v4.y);
-        np.z = upd_elem<true>(a, p[q].z, g[q].z, &m4.z, &v4.z);
-        np.w = upd_elem<true>(a, p[q].w, g[q].w, &m4.w, &v4.w);
-        *reinterpret_cast<float4*>(a.m + el) = m4;
-        *reinterpret_cast<float4*>(a.v + el) = v4;
-      } else {
-        np.x = upd_elem<false>(a, p[q].x, g[q].x, nullptr, nullptr);
-        np.y = upd_elem<false>(a, p[q].y, g[q].y, nullptr, nullptr);
-        np.z = upd_elem<false>(a, p[q].z, g[q].z, nullptr, nullptr);
-        np.w = upd_elem<false>(a, p[q].w, g[q].w, nullptr, nullptr);
+      for (int q = 0; q < NV; ++q) {
+        acc = fmaf(p[q].x, e0[q].x, acc);
+        acc = fmaf(p[q].y, e0[q].y, acc);
+        acc = fmaf(p[q].z, e0[q].z, acc);
+        acc = fmaf(p[q].w, e0[q].w, acc);
       }
-      if constexpr (BF16) {
-        uint2 o;
-        o.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
-        o.y = static_cast<uint32_t>(f32_to_bf16_bits(np.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.w)) << 16);
-        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(a.W) + el) = o;
-      } else {
-        *reinterpret_cast<float4*>(static_cast<float*>(a.W) + el) = np;
+      acc = warp_sum(acc);
+      SlotMeta m;
+      m.o = static_cast<int8_t>(dc.o0);
+      m.yf = dc.yf0;
+      m.w = dc.w0;
+      float pt, wn;
+      const float f = slot_factor_meta(m, acc, &pt, &wn);
+      if (lane == 0) {
+        A.scores[dc.slot0] = acc;
+        fa.factors[dc.slot0] = f;
       }
-      wmax = fmaxf(wmax, absmax4(np));
+      grad_emb_add(dc.slot0 / S, f);
+      if constexpr (!ADAM) {  // W row consumed (Adam: after the moments, below)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[r]);
+      }
+      update_row([&](int q) {
+        return make_float4(__fmul_rn(f, e0[q].x), __fmul_rn(f, e0[q].y), __fmul_rn(f, e0[q].z), __fmul_rn(f, e0[q].w));
+      });
+    } else {
+      // ---- several occurrences: in ascending b*S+s order (the two-kernel
+      // update's summation order), the gradient accumulated in this warp's
+      // shared scratch (lane-owned elements, no synchronisation)
+      float* gs = gs_all + warp * d + lane * 4;
+      const int32_t reg = sort_segment(a, dc.start, n, lane);
+      const bool small = n <= 32;
+      SlotMeta my;
+      my.o = static_cast<int8_t>(dc.o0);
+      my.yf = dc.yf0;
+      my.w = dc.w0;
+      if (small && lane < static_cast<int>(n) && reg != dc.slot0) my = slot_meta(fa, reg / S, reg - (reg / S) * S);
+      float my_sc = 0.0f;
+      for (uint32_t j = 0; j < n; ++j) {
+        const int32_t slot = seg_slot(a, dc.start, n, reg, j);
+        const int b = slot / S, s = slot - b * S;
+        float4 e[NV];
+        load_emb_row<NV>(fa.emb, b, lane, e);
+        float acc = 0.0f;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          acc = fmaf(p[q].x, e[q].x, acc);
+          acc = fmaf(p[q].y, e[q].y, acc);
+          acc = fmaf(p[q].z, e[q].z, acc);
+          acc = fmaf(p[q].w, e[q].w, acc);
+        }
+        acc = warp_sum(acc);
+        SlotMeta m;
+        if (small) {
+          m.o = static_cast<int8_t>(__shfl_sync(0xffffffffu, static_cast<int>(my.o), static_cast<int>(j)));
+          m.yf = __shfl_sync(0xffffffffu, my.yf, static_cast<int>(j));
+          m.w = __shfl_sync(0xffffffffu, my.w, static_cast<int>(j));
+        } else {
+          m = slot_meta(fa, b, s);
+        }
+        float pt, wn;
+        const float f = slot_factor_meta(m, acc, &pt, &wn);
+        if (small) {
+          if (lane == static_cast<int>(j)) my_sc = acc;
+        } else if (lane == 0) {
+          A.scores[slot] = acc;
+        }
+        if (lane == 0) fa.factors[slot] = f;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          float4 gq = make_float4(__fmul_rn(f, e[q].x), __fmul_rn(f, e[q].y), __fmul_rn(f, e[q].z), __fmul_rn(f, e[q].w));
+          if (j > 0) {
+            const float4 o = *reinterpret_cast<const float4*>(gs + q * 128);
+            gq = make_float4(__fadd_rn(o.x, gq.x), __fadd_rn(o.y, gq.y), __fadd_rn(o.z, gq.z), __fadd_rn(o.w, gq.w));
+          }
+          *reinterpret_cast<float4*>(gs + q * 128) = gq;
+        }
+        grad_emb_add(b, f);
+      }
+      if (small && lane < static_cast<int>(n)) A.scores[reg] = my_sc;
+      if constexpr (!ADAM) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[r]);
+      }
+      update_row([&](int q) { return *reinterpret_cast<const float4*>(gs + q * 128); });
     }
     if constexpr (ADAM) {
       __syncwarp();
