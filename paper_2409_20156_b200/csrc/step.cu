@@ -670,10 +670,21 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + static_cast<int64_t>(threadIdx.x) * kScanItems;
   uint32_t c[kScanItems];
   uint32_t s = 0, nz = 0;
+  if (base + kScanItems <= Lloc) {  // full run: 16-byte loads (workspace arrays are 256-byte aligned)
+#pragma unroll
+    for (int i = 0; i < kScanItems; i += 4) {
+      const uint4 v = *reinterpret_cast<const uint4*>(counts + base + i);
+      c[i] = v.x;
+      c[i + 1] = v.y;
+      c[i + 2] = v.z;
+      c[i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) c[i] = base + i < Lloc ? counts[base + i] : 0u;
+  }
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
-    int64_t l = base + i;
-    c[i] = l < Lloc ? counts[l] : 0u;
     s += c[i];
     nz += c[i] > 0;
   }
@@ -700,11 +711,12 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
   }
   ps += is - s;
   pn += in - nz;
+  uint32_t o[kScanItems];
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     int64_t l = base + i;
+    o[i] = ps;
     if (l < Lloc) {
-      offsets[l] = ps;
       if (c[i]) {
         uniq[pn] = static_cast<int32_t>(l);
         if (ustart) {
@@ -715,6 +727,15 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
       }
       ps += c[i];
     }
+  }
+  if (base + kScanItems <= Lloc) {
+#pragma unroll
+    for (int i = 0; i < kScanItems; i += 4)
+      *reinterpret_cast<uint4*>(offsets + base + i) = make_uint4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i)
+      if (base + i < Lloc) offsets[base + i] = o[i];
   }
 }
 
@@ -1160,11 +1181,11 @@ __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(Up
 // grad_emb's summation order over slots follows the reduction order, so it is
 // not bitwise run-to-run deterministic (ASTRA_STEP_SINGLE=0 selects the
 // deterministic two-kernel schedule); the loss is reduced per row in slot
-// order by single_row_finalize from the stored scores.
+// order by single_row_finalize from the stored per-slot fp64 loss terms.
 struct SingleArgs {
   FwdArgs f;
   UpdArgs u;
-  float* scores;          // [B*S] score of every owned slot
+  double* slot_loss;      // [B*S] fp64 loss term of every owned slot
   const int32_t* mode;    // decided by scan_top_kernel
   const uint32_t* ustart; // [U] bucket start of unique label u (= offsets[uniq[u]])
   const uint32_t* ucnt;   // [U] its occurrence count
@@ -1346,6 +1367,23 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
     return;
   }
   float wmax = 0.0f;
+  // fp64 loss terms, evaluated lane-parallel 32 slots at a time (lane c holds
+  // the c-th pending slot) and stored per slot for single_row_finalize
+  int32_t pend_slot = 0;
+  float pend_sc = 0.0f, pend_pt = 0.0f, pend_wn = 0.0f;
+  int c_pend = 0;
+  auto pend_loss = [&](int32_t slot, float sc, float pt, float wn) {
+    if (lane == c_pend) {
+      pend_slot = slot;
+      pend_sc = sc;
+      pend_pt = pt;
+      pend_wn = wn;
+    }
+    if (++c_pend == 32) {
+      A.slot_loss[pend_slot] = slot_loss(pend_sc, pend_pt, pend_wn);
+      c_pend = 0;
+    }
+  };
   if (warp < n_mine) {  // the first label's embedding row towards L1
     mbar_wait(&dfull[warp % RING], (warp / RING) & 1);
     prefetch_emb_l1<NV>(fa.emb, desc[warp % RING].slot0 / S, lane);
@@ -1437,10 +1475,8 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       m.w = dc.w0;
       float pt, wn;
       const float f = slot_factor_meta(m, acc, &pt, &wn);
-      if (lane == 0) {
-        A.scores[dc.slot0] = acc;
-        fa.factors[dc.slot0] = f;
-      }
+      if (lane == 0) fa.factors[dc.slot0] = f;
+      pend_loss(dc.slot0, acc, pt, wn);
       grad_emb_add(dc.slot0 / S, f);
       if constexpr (!ADAM) {  // W row consumed (Adam: after the moments, below)
         __syncwarp();
@@ -1461,7 +1497,6 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       my.yf = dc.yf0;
       my.w = dc.w0;
       if (small && lane < static_cast<int>(n) && reg != dc.slot0) my = slot_meta(fa, reg / S, reg - (reg / S) * S);
-      float my_sc = 0.0f;
       for (uint32_t j = 0; j < n; ++j) {
         const int32_t slot = seg_slot(a, dc.start, n, reg, j);
         const int b = slot / S, s = slot - b * S;
@@ -1486,12 +1521,8 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
         }
         float pt, wn;
         const float f = slot_factor_meta(m, acc, &pt, &wn);
-        if (small) {
-          if (lane == static_cast<int>(j)) my_sc = acc;
-        } else if (lane == 0) {
-          A.scores[slot] = acc;
-        }
         if (lane == 0) fa.factors[slot] = f;
+        pend_loss(slot, acc, pt, wn);
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
           float4 gq = make_float4(__fmul_rn(f, e[q].x), __fmul_rn(f, e[q].y), __fmul_rn(f, e[q].z), __fmul_rn(f, e[q].w));
@@ -1503,7 +1534,6 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
         }
         grad_emb_add(b, f);
       }
-      if (small && lane < static_cast<int>(n)) A.scores[reg] = my_sc;
       if constexpr (!ADAM) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[r]);
@@ -1515,14 +1545,16 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       if (lane == 0) mbar_arrive(&empty[r]);
     }
   }
+  if (lane < c_pend) A.slot_loss[pend_slot] = slot_loss(pend_sc, pend_pt, pend_wn);
   push_wmax(a, wmax, lane);
 }
 
-// Per-row tail of the single pass: the row's fp64 loss over its owned slots in
-// slot order (from the stored scores), the keep scale and finiteness check of
-// grad_emb. bound_rows = 0: finiteness was proven up front.
+// Per-row tail of the single pass (a CTA per batch row): the row's fp64 loss
+// from the stored per-slot terms of its owned slots (thread-strided, then a
+// fixed-order reduction: deterministic), the keep scale and finiteness check
+// of grad_emb. bound_rows = 0: finiteness was proven up front. d % 128 == 0.
 constexpr int kRowFinThreads = 256;
-__global__ void __launch_bounds__(kRowFinThreads) single_row_finalize(FwdArgs a, const float* scores,
+__global__ void __launch_bounds__(kRowFinThreads) single_row_finalize(FwdArgs a, const double* slot_loss,
                                                                       const int32_t* mode) {
   if (!*mode) return;
   __shared__ double sl[kRowFinThreads / 32];
@@ -1532,23 +1564,21 @@ __global__ void __launch_bounds__(kRowFinThreads) single_row_finalize(FwdArgs a,
   for (int s = threadIdx.x; s < a.S; s += kRowFinThreads) {
     const size_t slot = static_cast<size_t>(b) * a.S + s;
     const int64_t loc = static_cast<int64_t>(a.ids[slot]) - a.off;
-    if (loc >= 0 && loc < a.Lloc) {
-      float pt, wn;
-      slot_terms(slot_meta(a, b, s), &pt, &wn);
-      l += slot_loss(scores[slot], pt, wn);
-    }
+    if (loc >= 0 && loc < a.Lloc) l += slot_loss[slot];
   }
   l = warp_sum(l);
   if (lane == 0) sl[warp] = l;
   bool bad = false;
   float* ge = a.grad_emb + static_cast<size_t>(b) * a.d;
-  for (int k = threadIdx.x; k < a.d; k += kRowFinThreads) {
-    float gk = ge[k];
-    if (a.keep) {
-      gk = __fmul_rn(gk, a.keep[static_cast<size_t>(b) * a.d + k]);
-      ge[k] = gk;
+  const float* kp = a.keep ? a.keep + static_cast<size_t>(b) * a.d : nullptr;
+  for (int k = threadIdx.x * 4; k < a.d; k += kRowFinThreads * 4) {
+    float4 g = *reinterpret_cast<const float4*>(ge + k);
+    if (kp) {
+      const float4 kk = *reinterpret_cast<const float4*>(kp + k);
+      g = make_float4(__fmul_rn(g.x, kk.x), __fmul_rn(g.y, kk.y), __fmul_rn(g.z, kk.z), __fmul_rn(g.w, kk.w));
+      *reinterpret_cast<float4*>(ge + k) = g;
     }
-    bad |= !isfinite(gk);
+    bad |= !(isfinite(g.x) && isfinite(g.y) && isfinite(g.z) && isfinite(g.w));
   }
   if (bad) a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] = 1;
   __syncthreads();
@@ -2634,7 +2664,7 @@ struct StepWs {
   double* loss_rows;
   double* bound_rows;
   int32_t* mode;
-  float* scores;
+  double* slot_loss;
   uint32_t* ustart;
   uint32_t* ucnt;
 };
@@ -2664,7 +2694,7 @@ size_t carve_step(void* base, size_t cap, int B, int S, int64_t Lloc, StepWs* w)
   w->sf_acc = c.take<double>(1);
   w->pipe_ctr = c.take<unsigned>(2 * kMaxChunks + 4);
   w->mode = c.take<int32_t>(4);
-  w->scores = c.take<float>(n);
+  w->slot_loss = c.take<double>(n);
   w->ustart = c.take<uint32_t>(n < Lloc ? n : Lloc);
   w->ucnt = c.take<uint32_t>(n < Lloc ? n : Lloc);
   return c.off;
@@ -2828,7 +2858,7 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     SingleArgs SA;
     SA.f = fa;
     SA.u = ua;
-    SA.scores = w.scores;
+    SA.slot_loss = w.slot_loss;
     SA.mode = w.mode;
     SA.ustart = w.ustart;
     SA.ucnt = w.ucnt;
@@ -2868,7 +2898,7 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     ASTRA_LAUNCHED("slot_forward");
   }
   if (single) {
-    single_row_finalize<<<B, kRowFinThreads, 0, st>>>(fa, w.scores, w.mode);
+    single_row_finalize<<<B, kRowFinThreads, 0, st>>>(fa, w.slot_loss, w.mode);
     ASTRA_LAUNCHED("single_row_finalize");
   }
   if (!fused) {
