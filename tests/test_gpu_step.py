@@ -244,14 +244,51 @@ def test_adam_matches_torch_sparse_adam(cuda_lib):
         assert (got == ref).mean() > 0.99  # same op order as SparseAdam: nearly all bits equal
 
 
-def test_bf16_weights_sgd(cuda_lib):
+@pytest.mark.parametrize("wdtype", ["fp32", "bf16"])
+def test_single_pass_adam_equals_two_kernel(cuda_lib, wdtype):
+    """Adam (+ bf16 W): the single pass and the two-kernel schedule produce the
+    same W', m and v bits over several steps (same per-label summation order,
+    same SparseAdam op order)."""
+    from paper_2409_20156_b200 import _lib, ops
+
+    W, emb, ids, y, origin, weights = _random_step(20_000, 768, 64, 120, 7, n_hot=2)
+    dt = torch.bfloat16 if wdtype == "bf16" else torch.float32
+    outs = []
+    for det in (True, False):
+        _lib.set_step_deterministic(det)
+        try:
+            Wd = dev(W).to(dt)
+            m = torch.zeros((W.shape[0], W.shape[1]), dtype=torch.float32, device="cuda")
+            v = torch.zeros_like(m)
+            wb = _bound(W, True)
+            losses, ges = [], []
+            for step in (1, 2, 3):
+                res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wd, 0.01,
+                                     1e-4, optimizer="adam", adam_m=m, adam_v=v, adam_step=step, w_absmax=wb)
+                losses.append(res.loss)
+                ges.append(res.grad_emb.cpu().numpy())
+                assert res.status_host() == [0, 0, 0, 0]
+            outs.append((Wd.float().cpu().numpy(), m.cpu().numpy(), v.cpu().numpy(), losses, ges))
+        finally:
+            _lib.set_step_deterministic(False)
+    for k in range(3):
+        np.testing.assert_array_equal(outs[0][k], outs[1][k])
+    for a, b in zip(outs[0][3], outs[1][3]):
+        assert abs(a - b) <= 1e-12 * abs(a)
+    for a, b in zip(outs[0][4], outs[1][4]):
+        close(b, a)
+
+
+@pytest.mark.parametrize("bound", [False, True])
+def test_bf16_weights_sgd(cuda_lib, bound):
     from paper_2409_20156_b200 import ops
 
     L, d = 8000, 256
     W, emb, ids, y, origin, weights = _random_step(L, d, 32, 50, 31)
     Wb = dev(W).to(torch.bfloat16)
     W32 = Wb.float().cpu().numpy()
-    res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wb, 0.05, 1e-3)
+    res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wb, 0.05, 1e-3,
+                         w_absmax=_bound(W32, bound))
     Wref = W32.copy()
     loss, grad_emb, _, uids = port.slate_step(Wref, emb, None, ids, y, origin, weights, 0.05, 1e-3)
     assert abs(res.loss - loss) <= 2e-2 * abs(loss)
