@@ -1196,13 +1196,6 @@ __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
                : "memory");
 }
 
-// loss terms of a slot from its metadata (slot_factor_meta without the sigmoid)
-__device__ __forceinline__ void slot_terms(const SlotMeta& m, float* pt, float* wn) {
-  const bool pos_slot = m.o == ASTRA_ORIGIN_POS;
-  *pt = pos_slot ? m.yf : 0.0f;
-  *wn = __fmul_rn(m.w, pos_slot ? 0.0f : __fsub_rn(1.0f, m.yf));
-}
-
 template <int NV>
 __device__ __forceinline__ void load_emb_row(const float* emb, int b, int lane, float4 (&e)[NV]) {
   const float* p = emb + static_cast<size_t>(b) * (NV * 128) + lane * 4;
@@ -1222,11 +1215,13 @@ struct SingleRing {
   static constexpr uint32_t MB = ADAM ? NV * 128 * 4 : 0;
   static constexpr uint32_t ENTRY = WB + 2 * MB;
   static constexpr uint32_t SCRATCH = kTmaConsumers * NV * 128 * 4;  // per-warp gradient of multi-slot labels
+  static constexpr int Q = 64;                                        // in-order label queue (descriptors)
+  static constexpr uint32_t QBYTES = Q * (48 + 16);
   static constexpr int CTAS = ADAM ? 2 : ASTRA_SINGLE_CTAS;
   static constexpr uint32_t BUDGET = ADAM ? 110u * 1024 : (ASTRA_SINGLE_CTAS == 5 ? 44u : 56u) * 1024;
-  static constexpr int RING_MAX = static_cast<int>((BUDGET - SCRATCH) / (ENTRY + 56));
+  static constexpr int RING_MAX = static_cast<int>((BUDGET - SCRATCH - QBYTES) / (ENTRY + 16));
   static constexpr int RING = RING_MAX > 32 ? 32 : RING_MAX;
-  static constexpr size_t smem() { return static_cast<size_t>(RING) * (ENTRY + 32 + 24) + SCRATCH; }
+  static constexpr size_t smem() { return static_cast<size_t>(RING) * (ENTRY + 16) + SCRATCH + QBYTES; }
 };
 
 // The producer's per-label descriptor: bucket, first occurrence and its metadata.
@@ -1237,6 +1232,14 @@ struct SingleDesc {
   float yf0, w0;
   int32_t o0;
   int32_t pad;
+};
+
+// A queue entry: the label's descriptor + the data slot its rows went to and
+// the parity of that fill.
+struct SingleQEntry {
+  SingleDesc dc;
+  uint32_t slot, fpar;
+  uint32_t pad[2];
 };
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
@@ -1261,14 +1264,17 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
   constexpr int d = NV * 128;
   using RG = SingleRing<NV, BF16, ADAM>;
   constexpr int RING = RG::RING;
+  constexpr int Q = RG::Q;
   constexpr uint32_t ROWB = RG::ENTRY;
   extern __shared__ __align__(128) unsigned char usm[];
+  // [RING data slots][queue entries][per-warp scratch][barriers]
   unsigned char* ring = usm;
-  SingleDesc* desc = reinterpret_cast<SingleDesc*>(usm + RING * ROWB);
-  float* gs_all = reinterpret_cast<float*>(desc + RING);
+  SingleQEntry* queue = reinterpret_cast<SingleQEntry*>(usm + RING * ROWB);
+  float* gs_all = reinterpret_cast<float*>(queue + Q);
   uint64_t* full = reinterpret_cast<uint64_t*>(gs_all + kTmaConsumers * d);
   uint64_t* empty = full + RING;
-  uint64_t* dfull = empty + RING;
+  uint64_t* qfull = empty + RING;
+  uint64_t* qempty = qfull + Q;
   if (!*A.mode) return;
   const UpdArgs& a = A.u;
   const FwdArgs& fa = A.f;
@@ -1282,7 +1288,10 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
     for (int r = 0; r < RING; ++r) {
       mbar_init(&full[r], 1);
       mbar_init(&empty[r], 1);
-      mbar_init(&dfull[r], 1);
+    }
+    for (int r = 0; r < Q; ++r) {
+      mbar_init(&qfull[r], 1);
+      mbar_init(&qempty[r], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1291,8 +1300,10 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
   if (warp == kTmaConsumers) {
     // producer warp: 32 labels per batch, every index load lane-parallel and
     // software-pipelined over batches (batch k+3: bucket, k+2: first
-    // occurrence, k+1: its metadata, while batch k's descriptors and copies
-    // (W row, Adam moments) are issued in ring order)
+    // occurrence, k+1: its metadata). Labels enter an in-order queue of
+    // descriptors; their rows (W, Adam moments) go to ANY free data slot (a
+    // slow label holds only its own slot, not the ring), the slot and its fill
+    // parity travel in the queue entry.
     const unsigned char* Wb = static_cast<const unsigned char*>(a.W);
     struct PIdx {
       int32_t l;
@@ -1337,6 +1348,8 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
     idx_load(32, q1);
     perm_load(32, q1);
     idx_load(64, q2);
+    uint32_t use = 0;  // bit s: parity of the number of fills of data slot s
+    int rr = 0;
     for (int i0 = 0; i0 < n_mine; i0 += 32) {
       SingleDesc nxt;
       meta_load(i0 + 32, q1, nxt);
@@ -1344,18 +1357,38 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       idx_load(i0 + 96, q3);
       const int nb = min(32, n_mine - i0);
       for (int jj = 0; jj < nb; ++jj) {
+        const int i = i0 + jj, qi = i % Q;
+        int sl = -1;
+        if (lane == 0) {
+          mbar_wait(&qempty[qi], ((i / Q) & 1) ^ 1);
+          while (true) {  // a free data slot: its previous fill released
+            for (int k = 0; k < RING && sl < 0; ++k) {
+              const int c = rr + k < RING ? rr + k : rr + k - RING;
+              if (mbar_test(&empty[c], ((use >> c) & 1) ^ 1)) sl = c;
+            }
+            if (sl >= 0) break;
+            __nanosleep(20);
+          }
+        }
+        sl = __shfl_sync(0xffffffffu, sl, 0);
+        rr = sl + 1 < RING ? sl + 1 : 0;
+        const uint32_t fpar = (use >> sl) & 1u;
+        use ^= 1u << sl;
         if (lane == jj) {
-          const int i = i0 + jj, r = i % RING;
-          mbar_wait(&empty[r], ((i / RING) & 1) ^ 1);
-          desc[r] = cur;
-          mbar_arrive(&dfull[r]);
-          mbar_expect_tx(&full[r], ROWB);
-          unsigned char* dst = ring + r * ROWB;
+          SingleQEntry e;
+          e.dc = cur;
+          e.slot = static_cast<uint32_t>(sl);
+          e.fpar = fpar;
+          e.pad[0] = e.pad[1] = 0;
+          queue[qi] = e;
+          mbar_arrive(&qfull[qi]);
+          mbar_expect_tx(&full[sl], ROWB);
+          unsigned char* dst = ring + sl * ROWB;
           const size_t lz = static_cast<size_t>(cur.l);
-          bulk_g2s(dst, Wb + lz * RG::WB, RG::WB, &full[r]);
+          bulk_g2s(dst, Wb + lz * RG::WB, RG::WB, &full[sl]);
           if constexpr (ADAM) {
-            bulk_g2s(dst + RG::WB, a.m + lz * d, RG::MB, &full[r]);
-            bulk_g2s(dst + RG::WB + RG::MB, a.v + lz * d, RG::MB, &full[r]);
+            bulk_g2s(dst + RG::WB, a.m + lz * d, RG::MB, &full[sl]);
+            bulk_g2s(dst + RG::WB + RG::MB, a.v + lz * d, RG::MB, &full[sl]);
           }
         }
         __syncwarp();
@@ -1385,22 +1418,26 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
     }
   };
   if (warp < n_mine) {  // the first label's embedding row towards L1
-    mbar_wait(&dfull[warp % RING], (warp / RING) & 1);
-    prefetch_emb_l1<NV>(fa.emb, desc[warp % RING].slot0 / S, lane);
+    mbar_wait(&qfull[warp % Q], (warp / Q) & 1);
+    prefetch_emb_l1<NV>(fa.emb, queue[warp % Q].dc.slot0 / S, lane);
   }
   for (int i = warp; i < n_mine; i += kTmaConsumers) {
-    const int r = i % RING;
-    mbar_wait(&dfull[r], (i / RING) & 1);
-    const SingleDesc dc = desc[r];
+    const int qi = i % Q;
+    mbar_wait(&qfull[qi], (i / Q) & 1);
+    const SingleDesc dc = queue[qi].dc;
+    const int r = static_cast<int>(queue[qi].slot);
+    const uint32_t fpar = queue[qi].fpar;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&qempty[qi]);
     // the first occurrence's embedding row (prefetched into L1 one label ago)
     float4 e0[NV];
     load_emb_row<NV>(fa.emb, dc.slot0 / S, lane, e0);
     {  // the next label's row towards L1, if its descriptor is already there
       const int in = i + kTmaConsumers;
-      if (in < n_mine && mbar_test(&dfull[in % RING], (in / RING) & 1))
-        prefetch_emb_l1<NV>(fa.emb, desc[in % RING].slot0 / S, lane);
+      if (in < n_mine && mbar_test(&qfull[in % Q], (in / Q) & 1))
+        prefetch_emb_l1<NV>(fa.emb, queue[in % Q].dc.slot0 / S, lane);
     }
-    mbar_wait(&full[r], (i / RING) & 1);
+    mbar_wait(&full[r], fpar);
     const unsigned char* ent = ring + r * ROWB;
     float4 p[NV];
 #pragma unroll
