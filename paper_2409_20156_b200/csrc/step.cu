@@ -1486,6 +1486,9 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       }
     };
     auto grad_emb_add = [&](int b, float f) {
+#ifdef ASTRA_SINGLE_DEBUG_NO_RED
+      return;  // (experiment: measure the pass without the grad_emb reductions)
+#endif
       if (f != 0.0f) {  // warp-uniform; dead slots (f = 0) add nothing to grad_emb
         float* ge = fa.grad_emb + static_cast<size_t>(b) * d + lane * 4;
 #pragma unroll
