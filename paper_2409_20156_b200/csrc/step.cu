@@ -1206,6 +1206,9 @@ __device__ __forceinline__ void load_emb_row(const float* emb, int b, int lane, 
 #ifndef ASTRA_SINGLE_CTAS
 #define ASTRA_SINGLE_CTAS 4
 #endif
+#ifndef ASTRA_SINGLE_ADAM_CTAS
+#define ASTRA_SINGLE_ADAM_CTAS 2
+#endif
 // Ring geometry of the single pass: one entry = the W row (+ Adam m, v), and a
 // 32-byte descriptor per entry written by the producer (its own barrier, so a
 // consumer reads it before the row lands and prefetches the embedding rows).
@@ -1217,8 +1220,9 @@ struct SingleRing {
   static constexpr uint32_t SCRATCH = kTmaConsumers * NV * 128 * 4;  // per-warp gradient of multi-slot labels
   static constexpr int Q = 64;                                        // in-order label queue (descriptors)
   static constexpr uint32_t QBYTES = Q * (48 + 16);
-  static constexpr int CTAS = ADAM ? 2 : ASTRA_SINGLE_CTAS;
-  static constexpr uint32_t BUDGET = ADAM ? 110u * 1024 : (ASTRA_SINGLE_CTAS == 5 ? 44u : 56u) * 1024;
+  static constexpr int CTAS = ADAM ? ASTRA_SINGLE_ADAM_CTAS : ASTRA_SINGLE_CTAS;
+  static constexpr uint32_t BUDGET = (ADAM ? (ASTRA_SINGLE_ADAM_CTAS == 3 ? 74u : 110u)
+                                           : (ASTRA_SINGLE_CTAS == 5 ? 44u : 56u)) * 1024;
   static constexpr int RING_MAX = static_cast<int>((BUDGET - SCRATCH - QBYTES) / (ENTRY + 16));
   static constexpr int RING = RING_MAX > 32 ? 32 : RING_MAX;
   static constexpr size_t smem() { return static_cast<size_t>(RING) * (ENTRY + 16) + SCRATCH + QBYTES; }
@@ -2833,8 +2837,12 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     const char* e = getenv("ASTRA_STEP_SINGLE");
     return e ? atoi(e) != 0 : true;
   }();
-  const bool single = !fused && single_env && !g_step_deterministic.load() && chunkable &&
-                      nv <= 6;  // (nv = 8 spills: two-kernel schedule)
+  // (Adam measures faster on the two-kernel schedule: 1.96 vs 2.8 ms per
+  // minibatch for bf16 W at the bench shape — the pass is instruction-bound
+  // with the IEEE div/sqrt of 24 elements per lane; nv = 8 spills)
+  static const bool single_adam = getenv("ASTRA_STEP_SINGLE_ADAM") != nullptr;
+  const bool single = !fused && single_env && !g_step_deterministic.load() && chunkable && nv <= 6 &&
+                      (!adam || single_adam);
   if (single) fa.skip = w.mode;
 
   // counting sort of the slots by local label id (+ the single pass's bounds and decision)

@@ -8,9 +8,14 @@ import torch
 sys.path.insert(0, ".")
 from paper_2409_20156_b200.engine import ClassifierEngine  # noqa: E402
 
+import os  # noqa: E402
+
 L, d, B, k_p, k_h, k_r = 1_305_265, 768, 1024, 8, 64, 512
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-eng = ClassifierEngine(L, d, k_p=k_p, k_h=k_h, k_r=k_r, seed=0)
+# ASTRA_BENCH_STEP_ADAM=1: bf16 W + Adam (the C5 shard's optimizer configuration)
+adam = os.environ.get("ASTRA_BENCH_STEP_ADAM") == "1"
+eng = ClassifierEngine(L, d, k_p=k_p, k_h=k_h, k_r=k_r, seed=0, w_dtype=torch.bfloat16 if adam else torch.float32,
+                       optimizer="adam" if adam else "sgd")
 g = torch.Generator(device="cuda")
 g.manual_seed(1)
 mbs = []
@@ -48,7 +53,7 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / n
 print(f"host {1e3 * (h1 - h0) / n:.3f} ms/minibatch (python + launches, no sync)")
 U = int(torch.unique(sl[0]).numel())
-byts = U * d * 8 + 2 * B * d * 4 + B * (k_p + k_h + k_r) * 5
+byts = U * d * (2 * 2 + 16 if adam else 8) + 2 * B * d * 4 + B * (k_p + k_h + k_r) * 5
 print(f"step {ms:.3f} ms/minibatch  U={U}  {byts / ms / 1e6:.0f} GB/s algorithmic ({byts / 1e9:.2f} GB)")
 kt = {k: _lib.kernel_timing(k) for k in ("step_single", "slot_forward", "label_update")}
 print("kernels  " + "  ".join(f"{k} {ms / max(c, 1):.3f} ms" for k, (ms, c) in kt.items()))

@@ -246,37 +246,51 @@ def test_adam_matches_torch_sparse_adam(cuda_lib):
 
 @pytest.mark.parametrize("wdtype", ["fp32", "bf16"])
 def test_single_pass_adam_equals_two_kernel(cuda_lib, wdtype):
-    """Adam (+ bf16 W): the single pass and the two-kernel schedule produce the
-    same W', m and v bits over several steps (same per-label summation order,
-    same SparseAdam op order)."""
-    from paper_2409_20156_b200 import _lib, ops
+    """Adam (+ bf16 W): the single pass (opt-in for Adam: ASTRA_STEP_SINGLE_ADAM)
+    and the two-kernel schedule produce the same W', m and v bits over several
+    steps (same per-label summation order, same SparseAdam op order)."""
+    import subprocess
+    import sys
 
-    W, emb, ids, y, origin, weights = _random_step(20_000, 768, 64, 120, 7, n_hot=2)
-    dt = torch.bfloat16 if wdtype == "bf16" else torch.float32
-    outs = []
-    for det in (True, False):
-        _lib.set_step_deterministic(det)
-        try:
-            Wd = dev(W).to(dt)
-            m = torch.zeros((W.shape[0], W.shape[1]), dtype=torch.float32, device="cuda")
-            v = torch.zeros_like(m)
-            wb = _bound(W, True)
-            losses, ges = [], []
-            for step in (1, 2, 3):
-                res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wd, 0.01,
-                                     1e-4, optimizer="adam", adam_m=m, adam_v=v, adam_step=step, w_absmax=wb)
-                losses.append(res.loss)
-                ges.append(res.grad_emb.cpu().numpy())
-                assert res.status_host() == [0, 0, 0, 0]
-            outs.append((Wd.float().cpu().numpy(), m.cpu().numpy(), v.cpu().numpy(), losses, ges))
-        finally:
-            _lib.set_step_deterministic(False)
-    for k in range(3):
-        np.testing.assert_array_equal(outs[0][k], outs[1][k])
-    for a, b in zip(outs[0][3], outs[1][3]):
-        assert abs(a - b) <= 1e-12 * abs(a)
-    for a, b in zip(outs[0][4], outs[1][4]):
-        close(b, a)
+    code = f"""
+import os, sys
+os.environ["ASTRA_STEP_SINGLE_ADAM"] = "1"
+sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {ROOT!r} + "/tests")
+import numpy as np, torch
+from test_gpu_step import _random_step, _bound, close
+from gpu_util import dev
+from paper_2409_20156_b200 import _lib, ops
+W, emb, ids, y, origin, weights = _random_step(20_000, 768, 64, 120, 7, n_hot=2)
+dt = torch.bfloat16 if "{wdtype}" == "bf16" else torch.float32
+outs = []
+for det in (True, False):
+    _lib.set_step_deterministic(det)
+    Wd = dev(W).to(dt)
+    m = torch.zeros((W.shape[0], W.shape[1]), dtype=torch.float32, device="cuda")
+    v = torch.zeros_like(m)
+    wb = _bound(W, True)
+    losses, ges = [], []
+    _lib.kernel_timing_enable(True)
+    for step in (1, 2, 3):
+        res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wd, 0.01,
+                             1e-4, optimizer="adam", adam_m=m, adam_v=v, adam_step=step, w_absmax=wb)
+        losses.append(res.loss)
+        ges.append(res.grad_emb.cpu().numpy())
+        assert res.status_host() == [0, 0, 0, 0]
+    n_single = _lib.kernel_timing("step_single")[1]
+    assert (n_single == 0) == det, (det, n_single)
+    outs.append((Wd.float().cpu().numpy(), m.cpu().numpy(), v.cpu().numpy(), losses, ges))
+_lib.set_step_deterministic(False)
+for k in range(3):
+    np.testing.assert_array_equal(outs[0][k], outs[1][k])
+for a, b in zip(outs[0][3], outs[1][3]):
+    assert abs(a - b) <= 1e-12 * abs(a)
+for a, b in zip(outs[0][4], outs[1][4]):
+    close(b, a)
+print("ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
 @pytest.mark.parametrize("bound", [False, True])
