@@ -540,6 +540,10 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const double* loss_rows,
 
 // ---------------------------------------------------------------- counting sort
 
+__device__ __forceinline__ float absmax4(float4 v) {
+  return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+}
+
 // Also (sf_acc != null, the single-pass schedule) the finiteness bounds:
 // sum over owned slots of (1 + |weight|) and max|emb| (+inf if non-finite).
 __global__ void __launch_bounds__(256) count_kernel(const int32_t* ids, int64_t n, int64_t off, int64_t Lloc,
@@ -562,10 +566,12 @@ __global__ void __launch_bounds__(256) count_kernel(const int32_t* ids, int64_t 
   }
   if (!sf_acc) return;
   float em = 0.0f;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_emb;
+  // (n_emb % 4 == 0 and emb 16-byte aligned on the single-pass path)
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_emb / 4;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float e = emb[i];
-    em = fmaxf(em, isfinite(e) ? fabsf(e) : INFINITY);
+    const float4 e = reinterpret_cast<const float4*>(emb)[i];
+    const bool fin = isfinite(e.x) && isfinite(e.y) && isfinite(e.z) && isfinite(e.w);
+    em = fmaxf(em, fin ? absmax4(e) : INFINITY);
   }
   __shared__ double s_sf[8];
   __shared__ float s_em[8];
@@ -778,9 +784,6 @@ __device__ __forceinline__ void push_wmax(const UpdArgs& a, float wmax, int lane
   if (lane == 0 && wmax > 0.0f) atomicMax(reinterpret_cast<unsigned*>(a.w_absmax), __float_as_uint(wmax));
 }
 
-__device__ __forceinline__ float absmax4(float4 v) {
-  return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-}
 
 // Sort the label's slot indices ascending. Segments <= 32 stay in a register
 // (returned); longer ones are rank-sorted into perm2.
@@ -2651,7 +2654,8 @@ void launch_upd_tma(const UpdArgs& a, int grid, size_t smem, cudaStream_t st) {
 template <bool BF16, bool ADAM>
 int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
   const int nv = a.d % 128 == 0 ? a.d / 128 : 0;
-  label_update_kernel<BF16, ADAM, true><<<max_ctas, kUpdThreads, 0, st>>>(a);
+  // (the check pass returns at once unless the bound tripped: a small grid keeps that cheap)
+  label_update_kernel<BF16, ADAM, true><<<std::min(max_ctas, 2 * num_sms()), kUpdThreads, 0, st>>>(a);
   ASTRA_LAUNCHED("label_check");
   static const bool legacy = getenv("ASTRA_STEP_LEGACY_UPD") != nullptr;
   if (!legacy && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
