@@ -2841,10 +2841,19 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     const char* e = getenv("ASTRA_STEP_SINGLE");
     return e ? atoi(e) != 0 : true;
   }();
-  // (Adam measures faster on the two-kernel schedule: 1.96 vs 2.8 ms per
-  // minibatch for bf16 W at the bench shape — the pass is instruction-bound
-  // with the IEEE div/sqrt of 24 elements per lane; nv = 8 spills)
-  static const bool single_adam = getenv("ASTRA_STEP_SINGLE_ADAM") != nullptr;
+  // Adam: the pass is instruction-bound (IEEE div + sqrt on 24 elements per
+  // lane). Measured, bf16 W: with a 10 GB W+m+v shard (1.3M labels) the
+  // two-kernel schedule wins (1.96 vs 2.8 ms per 1024-row minibatch); with the
+  // C5 shard's 115 GB (15M labels, 4096 x 2416 slates) the single pass wins
+  // (7.5 vs 8.1-8.5 ms per step): there the second random sweep of the
+  // gather costs more than the pass's extra instructions. Crossover taken at
+  // 32 GB of W+m+v per shard; ASTRA_STEP_SINGLE_ADAM=0/1 forces it. nv = 8 spills.
+  static const int single_adam_env = [] {
+    const char* e = getenv("ASTRA_STEP_SINGLE_ADAM");
+    return e ? atoi(e) : -1;
+  }();
+  const double shard_state_bytes = static_cast<double>(Lloc) * d * ((bf16 ? 2 : 4) + 8);
+  const bool single_adam = single_adam_env >= 0 ? single_adam_env != 0 : shard_state_bytes >= 32e9;
   const bool single = !fused && single_env && !g_step_deterministic.load() && chunkable && nv <= 6 &&
                       (!adam || single_adam);
   if (single) fa.skip = w.mode;
