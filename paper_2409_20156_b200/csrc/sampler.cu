@@ -17,6 +17,7 @@ namespace {
 constexpr uint32_t TAG_POSKEY = 1, TAG_PAD = 2, TAG_IMP = 3, TAG_RAND = 4;
 constexpr int kThreads = 128;
 constexpr int kMaxSet = 4096;  // |hard| + |cand| per row
+constexpr int kSmemPos = 256;  // a row's positives staged in shared memory up to this many
 
 struct SamplerArgs {
   uint32_t k0, k1, epoch, step;
@@ -45,12 +46,18 @@ __global__ void __launch_bounds__(kThreads) sample_slates_kernel(SamplerArgs a) 
   double* cdf = reinterpret_cast<double*>(smem);                     // n_c
   int32_t* C = reinterpret_cast<int32_t*>(smem + sizeof(double) * a.n_c);  // P, sorted hard (+cand)
   __shared__ double s_total;
+  __shared__ int32_t s_pos[kSmemPos];
 
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
   const uint32_t row = static_cast<uint32_t>(a.rows[b]);
-  const int32_t* pos = a.pos_ids + a.pos_indptr[b];
+  const int32_t* pos_g = a.pos_ids + a.pos_indptr[b];
   const int64_t npos = a.pos_indptr[b + 1] - a.pos_indptr[b];
+  // the row's sorted positives, searched by every pad / uniform / importance
+  // draw: from shared memory unless the row has more than kSmemPos of them
+  if (npos <= kSmemPos)
+    for (int j = tid; j < npos; j += kThreads) s_pos[j] = pos_g[j];
+  const int32_t* pos = npos <= kSmemPos ? s_pos : pos_g;
   const bool use_cand = a.k_i > 0 && a.n_c > 0;
   const size_t base = static_cast<size_t>(b) * a.S;
 
