@@ -146,8 +146,16 @@ __device__ __forceinline__ uint32_t mapa_cluster(const void* p, uint32_t rank) {
   return r;
 }
 
+// Relaxed remote arrive (no MEMBAR.GPU: a release here made every epilogue
+// warp wait for its outstanding candidate stores once per tile). Only the
+// TMEM reads must precede the arrive, and tcgen05.wait::ld has completed them
+// (ordered by tcgen05.fence::before_thread_sync) before it is issued.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+#ifdef ASTRA_TC_RELEASE_ARRIVE  // (A/B switch: the release form)
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+#else
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+#endif
 }
 
 __device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
