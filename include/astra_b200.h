@@ -220,6 +220,28 @@ int astra_apply_updates(void* W, int w_dtype, int64_t n_labels, int d, const int
                         const float* grads, int64_t U, float lr, float weight_decay,
                         int32_t* status, void* stream);
 
+/* ------------------------------------------------------------------------
+ * All-negatives (full-loss) arm, train_full_loss_baseline (trainer.py:563-616),
+ * and the dense probe loss, _probe_full_loss (trainer.py:398-403). The arm's
+ * GEMMs (E W^T, G W, G^T E) are plain fp32 library GEMMs issued by the host;
+ * these are its elementwise parts.
+ *
+ * astra_dense_bce: scores B x n_labels (fp32, or fp64 when scores_f64), the
+ * positives as a CSR (pos_indptr[B+1] int64, pos_ids int32, sorted distinct
+ * per row). Writes G = f32(0.5 (1 + tanh(s / 2))) - y (trainer.py:597; G may
+ * be NULL: loss only) and *loss_out = float64 sum of y sp(-s) + (1-y) sp(s)
+ * (trainer.py:595 / :401-402). Deterministic (fixed-order reductions).
+ * Workspace: astra_dense_workspace_size(B) bytes. */
+size_t astra_dense_workspace_size(int B);
+int astra_dense_bce(const void* scores, int scores_f64, int B, int64_t n_labels,
+                    const int64_t* pos_indptr, const int32_t* pos_ids, float* G,
+                    double* loss_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Dense SGD over n elements: W -= f32(lr) * (grads + f32(wd) * W), each op
+ * rounded like NumPy (trainer.py:604-606; no finiteness check, as there). */
+int astra_dense_sgd(float* W, const float* grads, int64_t n, float lr, float weight_decay,
+                    void* stream);
+
 /* Synchronous helper: cudaStreamSynchronize + error mapping. */
 int astra_stream_sync(void* stream);
 

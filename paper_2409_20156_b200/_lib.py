@@ -40,6 +40,9 @@ _SIGS = {
     "astra_slate_step": ([p, p, p, p, p, i64, p, i64, p, i32, i32, i32, p, i32, p, p, i32, i64, i64, f64, f64, f64, f64, f64,
                           i64, p, p, p, p, p, p, sz, p], i32),
     "astra_apply_updates": ([p, i32, i64, i32, p, p, i64, f32, f32, p, p], i32),
+    "astra_dense_workspace_size": ([i32], sz),
+    "astra_dense_bce": ([p, i32, i32, i64, p, p, p, p, p, sz, p], i32),
+    "astra_dense_sgd": ([p, p, i64, f32, f32, p], i32),
     "astra_stream_sync": ([p], i32),
 }
 

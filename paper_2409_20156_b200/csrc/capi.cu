@@ -67,6 +67,10 @@ int sample_slates(uint64_t, uint32_t, uint32_t, const int64_t*, int, const int64
                   int8_t*, float*, cudaStream_t);
 size_t step_workspace_size(int, int, int, int64_t);
 void set_step_deterministic(int on);
+size_t dense_workspace_size(int B);
+int dense_bce(const void* S, int s_f64, int B, int64_t L, const int64_t* pos_indptr, const int32_t* pos_ids,
+              float* G, double* loss_out, void* workspace, size_t ws_bytes, cudaStream_t st);
+int dense_sgd(float* W, const float* grads, int64_t n, float lr, float wd, cudaStream_t st);
 int slate_step(const float*, const float*, const int32_t*, const int8_t*, const int8_t*, int64_t, const float*,
                int64_t, const float*, int, int, int, void*, int, float*, float*, int, int64_t, int64_t, double, double,
                double, double, double, int64_t, float*, double*, int32_t*, float*, float*, void*, size_t, cudaStream_t);
@@ -178,6 +182,19 @@ int astra_slate_step(const float* emb, const float* keep, const int32_t* ids, co
 int astra_apply_updates(void* W, int w_dtype, int64_t n_labels, int d, const int64_t* ids, const float* grads,
                         int64_t U, float lr, float weight_decay, int32_t* status, void* stream) {
   return apply_updates(W, w_dtype, n_labels, d, ids, grads, U, lr, weight_decay, status, S(stream));
+}
+
+size_t astra_dense_workspace_size(int B) { return dense_workspace_size(B); }
+
+int astra_dense_bce(const void* scores, int scores_f64, int B, int64_t n_labels, const int64_t* pos_indptr,
+                    const int32_t* pos_ids, float* G, double* loss_out, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+  return dense_bce(scores, scores_f64, B, n_labels, pos_indptr, pos_ids, G, loss_out, workspace, workspace_bytes,
+                   S(stream));
+}
+
+int astra_dense_sgd(float* W, const float* grads, int64_t n, float lr, float weight_decay, void* stream) {
+  return dense_sgd(W, grads, n, lr, weight_decay, S(stream));
 }
 
 int astra_stream_sync(void* stream) { return check_cuda(cudaStreamSynchronize(S(stream)), "stream sync"); }

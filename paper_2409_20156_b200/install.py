@@ -14,6 +14,10 @@ Rebinds the module globals the reference resolves at call time (SURVEY.md
   xcmix.anns.query_topk                        <- anns.query_topk
         (UpToDateHard, trainer.py:321-333; evaluation's anns mode)
   xcmix.evaluation.predict_topk                <- evaluation.predict_topk (exact mode)
+  xcmix.trainer._probe_full_loss / _eval_p_at  <- trainer.* (the dense per-epoch
+        probes, trainer.py:398-423, resolved by train_epoch and the full-loss arm)
+  xcmix.trainer.train_full_loss_baseline       <- trainer.train_full_loss_baseline
+        (the all-negatives arm, trainer.py:563-616)
 Code that imported a name before install() (`from xcmix.anns import f`) keeps
 the old object: install first (e.g. from a pytest plugin / conftest).
 """
@@ -47,6 +51,9 @@ def install(backend=None, slates: str = "philox") -> None:
             (xt, "_batch_forward_backward"): xt._batch_forward_backward,
             (xt, "_assemble_batch_slates"): xt._assemble_batch_slates,
             (xt, "apply_classifier_updates_arrays"): xt.apply_classifier_updates_arrays,
+            (xt, "_probe_full_loss"): xt._probe_full_loss,
+            (xt, "_eval_p_at"): xt._eval_p_at,
+            (xt, "train_full_loss_baseline"): xt.train_full_loss_baseline,
             (xc, "apply_classifier_updates_arrays"): xc.apply_classifier_updates_arrays,
         })
     anns._approx_impl = _saved[(xa, "retrieve_hard_negatives")]
@@ -61,6 +68,9 @@ def install(backend=None, slates: str = "philox") -> None:
                                  else _saved[(xt, "_assemble_batch_slates")])
     xt.apply_classifier_updates_arrays = classifiers.apply_classifier_updates_arrays
     xc.apply_classifier_updates_arrays = classifiers.apply_classifier_updates_arrays
+    xt._probe_full_loss = trainer._probe_full_loss
+    xt._eval_p_at = trainer._eval_p_at
+    xt.train_full_loss_baseline = trainer.train_full_loss_baseline
 
 
 def uninstall() -> None:

@@ -210,6 +210,72 @@ def slate_step(emb, ids, y, origin, weights, W, lr, weight_decay=0.0, keep=None,
     return StepResult(loss, grad_emb, status, factors)
 
 
+def dense_bce(scores, pos_indptr, pos_ids, want_grad=True):
+    """Elementwise half of the all-negatives arm over B x L scores (fp32, or
+    fp64 for the probe): (G = f32(sigmoid) - y or None, float64 loss sum as a
+    1-element device tensor). trainer.py:595-597, :401-402."""
+    if scores.dtype not in (torch.float32, torch.float64) or not scores.is_cuda or not scores.is_contiguous():
+        raise ConfigError("scores must be a contiguous CUDA fp32/fp64 tensor")
+    _cuda(pos_indptr, torch.int64, "pos_indptr")
+    _cuda(pos_ids, torch.int32, "pos_ids")
+    B, L = scores.shape
+    lib = _lib.load()
+    ws = WORKSPACES.get("dense", lib.astra_dense_workspace_size(B), scores.device)
+    G = torch.empty((B, L), dtype=torch.float32, device=scores.device) if want_grad else None
+    loss = torch.empty(1, dtype=torch.float64, device=scores.device)
+    _lib.check(lib.astra_dense_bce(_p(scores), 1 if scores.dtype == torch.float64 else 0, B, L, _p(pos_indptr),
+                                   _p(pos_ids), _p(G), _p(loss), _p(ws), ws.numel(), _stream()))
+    return G, loss
+
+
+def dense_sgd(W, grads, lr, weight_decay=0.0):
+    """W -= f32(lr) (grads + f32(wd) W) over every element (trainer.py:604-606)."""
+    _cuda(W, torch.float32, "W")
+    _cuda(grads, torch.float32, "grads")
+    if grads.shape != W.shape:
+        raise ConfigError("dense_sgd: grads must have W's shape")
+    _lib.check(_lib.load().astra_dense_sgd(_p(W), _p(grads), W.numel(), float(lr), float(weight_decay), _stream()))
+
+
+def _fp32_gemm(a, b):
+    """A plain fp32 library GEMM (cuBLAS), TF32 off: the reference's BLAS sgemm."""
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        return torch.matmul(a, b)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def full_loss_forward(emb_used, W, pos_indptr, pos_ids, keep=None):
+    """One batch of the all-negatives arm before the update (trainer.py:593-599):
+    scores = emb_used W^T (fp32 cuBLAS), G and the float64 loss (astra_dense_bce),
+    grad_emb = G W (x keep). Returns (loss_dev, G, grad_emb)."""
+    _cuda(emb_used, torch.float32, "emb_used")
+    _cuda(W, torch.float32, "W")
+    _cuda(keep, torch.float32, "keep")
+    scores = _fp32_gemm(emb_used, W.t())
+    G, loss = dense_bce(scores, pos_indptr, pos_ids)
+    del scores
+    grad_emb = _fp32_gemm(G, W)
+    if keep is not None:
+        grad_emb = grad_emb * keep
+    return loss, G, grad_emb
+
+
+def full_loss_update(W, G, emb_used, lr, weight_decay=0.0):
+    """W -= f32(lr) (G^T emb_used + f32(wd) W) (trainer.py:602-606)."""
+    dense_sgd(W, _fp32_gemm(G.t(), emb_used), lr, weight_decay)
+
+
+def dense_probe_loss(emb, W, pos_indptr, pos_ids):
+    """float64 dense BCE sum over a probe set (trainer.py:398-403, before the
+    division): an fp64 GEMM (cuBLAS DGEMM) and astra_dense_bce in fp64."""
+    _cuda(emb, torch.float64, "emb")
+    scores = torch.matmul(emb, W.to(torch.float64).t())
+    return dense_bce(scores, pos_indptr, pos_ids, want_grad=False)[1]
+
+
 def raise_for_step_status(status) -> None:
     """Host check of a step's status words (syncs). Mirrors the reference's
     NumericalError raises (classifiers.py:79-80, encoder.py:145-146)."""

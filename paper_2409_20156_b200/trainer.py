@@ -4,6 +4,10 @@
         -> (ids B x S int64, y B x S int8, origin S int8, weights S fp32)   trainer.py:262-318
   _batch_forward_backward(state, batch_rows, epoch, rng, step_lr_enc,
                           step_lr_clf, feats=None) -> float               trainer.py:336-395
+  _probe_full_loss(state) -> float                                        trainer.py:398-403
+  _eval_p_at(state) -> (p@1, p@5)                                         trainer.py:406-423
+  train_full_loss_baseline(dataset, config, eval_dataset=None,
+                           checkpoint_path=None)                          trainer.py:563-616
 
 Slates come from the Philox sampler (astra_sample_slates) keyed by one 63-bit
 draw from the caller's generator, so runs stay bitwise reproducible and the
@@ -149,3 +153,127 @@ def _batch_forward_backward(state, batch_rows, epoch, rng, step_lr_enc, step_lr_
         raise NumericalError("non-finite classifier gradient")  # classifiers.py:79-80; W untouched
     bank.sync_rows(torch.unique(ids_d))
     return res.loss
+
+
+# ------------------------------------------------------------ dense arms
+
+
+def _csr(rows_positives):
+    """CSR (indptr int64, sorted distinct ids int32) of per-row positive lists."""
+    lists = [np.unique(np.asarray(p, dtype=np.int64)) for p in rows_positives]
+    indptr = np.zeros(len(lists) + 1, dtype=np.int64)
+    np.cumsum([len(p) for p in lists], out=indptr[1:])
+    ids = np.concatenate(lists).astype(np.int32) if lists else np.zeros(0, np.int32)
+    return indptr, ids
+
+
+def _dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype)))
+    return t.to(_backend.device())
+
+
+def _host_weights(state):
+    """The bank's current weights on the device (uploaded from the host copy,
+    which the reference and the drop-in keep authoritative)."""
+    return _dev(state.bank.weights, np.float32)
+
+
+def _probe_full_loss(state) -> float:
+    """Dense float64 BCE over the probe rows (trainer.py:398-403): fp64 cuBLAS
+    GEMM + astra_dense_bce instead of the 200 x L host computation."""
+    import xcmix.trainer as xt
+
+    emb = xt.embed_batch(state.encoder, state.probe_feats).astype(np.float64)
+    pos = np.asarray(state.probe_y, dtype=bool)
+    indptr, ids = _csr([np.nonzero(r)[0] for r in pos])
+    ops = _backend.get()
+    total = ops.dense_probe_loss(_dev(emb), _host_weights(state), _dev(indptr), _dev(ids))
+    return float(float(total.item()) / len(state.probe_rows))
+
+
+def _eval_p_at(state):
+    """P@1 / P@5 on the eval set (trainer.py:406-423): the top-5 of every
+    point by the exact fp32 MIPS kernel (descending score, ties -> lower id,
+    = the reference's stable argsort) instead of a dense host argsort."""
+    import xcmix.trainer as xt
+
+    ds = state.eval_dataset
+    if ds is None:
+        return None, None
+    emb = xt.embed_batch(state.encoder, ds.features)
+    L = state.bank.weights.shape[0]
+    k = min(5, L)
+    n_pts = emb.shape[0]
+    ops = _backend.get()
+    no_pos = _dev(np.zeros(n_pts + 1, dtype=np.int64))
+    _, top, _ = ops.refresh_topk(_dev(emb, np.float32), no_pos, _dev(np.zeros(0, np.int32)), k, "fp32",
+                                 labels_f32=_host_weights(state))
+    top5 = top.cpu().numpy()
+    hits1 = hits5 = n = 0
+    for i in range(ds.n_points):
+        pos = set(ds.positives[i].tolist())
+        if not pos:
+            continue
+        n += 1
+        hits1 += int(top5[i, 0] in pos)
+        hits5 += len(pos.intersection(top5[i].tolist())) / 5.0
+    if n == 0:
+        return None, None
+    return hits1 / n, hits5 / n
+
+
+def train_full_loss_baseline(dataset, config, eval_dataset=None, checkpoint_path=None):
+    """All-negatives arm (trainer.py:563-616) with the classifier on the GPU:
+    per batch, scores / G / loss / grad_emb (fp32 cuBLAS GEMMs +
+    astra_dense_bce), then the caller's encoder backward + Adam, then the dense
+    SGD of every row (astra_dense_sgd). The generator stream, batch order,
+    dropout and the encoder path are the reference's; bank.weights is written
+    back after every epoch (before the epoch's probe / eval)."""
+    import time
+
+    import xcmix.trainer as xt
+
+    if dataset.n_labels > xt._FULL_LOSS_LABEL_CAP:
+        raise ConfigError(f"full-loss baseline capped at L <= {xt._FULL_LOSS_LABEL_CAP}")
+    state = xt.TrainerState(dataset, config, eval_dataset)
+    n_batches = -(-len(state.active_rows) // config.batch_size)
+    state.total_steps = max(config.epochs * n_batches, 1)
+    ops = _backend.get()
+    W = _host_weights(state)
+    for epoch in range(config.epochs):
+        t0 = time.perf_counter()
+        rng = np.random.default_rng((config.seed, 7919, epoch))
+        perm = rng.permutation(len(state.active_rows))
+        rows = state.active_rows[perm]
+        total_loss = 0.0
+        for start in range(0, len(rows), config.batch_size):
+            batch = rows[start : start + config.batch_size]
+            lr_enc = xt.lr_at(state.global_step, state.total_steps, config.warmup_steps, config.lr_encoder)
+            lr_clf = xt.lr_at(state.global_step, state.total_steps, config.warmup_steps, config.lr_classifier)
+            feats = dataset.features[batch]
+            emb = xt.embed_batch(state.encoder, feats)
+            if config.dropout > 0:
+                keep = (rng.random(emb.shape) >= config.dropout).astype(np.float32) / np.float32(1.0 - config.dropout)
+                emb_used = emb * keep
+            else:
+                keep = None
+                emb_used = emb
+            indptr, ids = _csr([dataset.positives[r] for r in batch])
+            emb_d = _dev(emb_used, np.float32)
+            loss, G, grad_emb = ops.full_loss_forward(emb_d, W, _dev(indptr), _dev(ids),
+                                                      keep=None if keep is None else _dev(keep))
+            total_loss += float(loss.item())
+            enc_grads = xt.encoder_backward_batch(state.encoder, feats, grad_emb.cpu().numpy())
+            xt.adam_step(state.opt, state.encoder, enc_grads, lr_enc)
+            ops.full_loss_update(W, G, emb_d, lr_clf, config.weight_decay_classifier)
+            state.global_step += 1
+        state.bank.weights[...] = W.cpu().numpy()
+        wall = time.perf_counter() - t0
+        evaluate_now = (epoch % config.eval_every == config.eval_every - 1) or epoch == config.epochs - 1
+        p1, p5 = xt._eval_p_at(state) if evaluate_now else (None, None)
+        state.log.records.append(
+            xt.EpochRecord(epoch, wall, total_loss / max(len(rows), 1), xt._probe_full_loss(state), p1, p5, -1)
+        )
+    if checkpoint_path is not None:
+        xt.save_checkpoint(checkpoint_path, state.encoder, state.bank, config)
+    return state.encoder, state.bank, state.log

@@ -118,3 +118,25 @@ def apply_updates(W, ids, grads, lr, weight_decay=0.0):
         port.apply_classifier_updates_arrays(Wn, _np(ids), _np(grads), lr, weight_decay)
     except port.OracleNumericalError as e:
         raise NumericalError(str(e)) from None
+
+
+def _dense_y_from_csr(pos_indptr, pos_ids, B, L):
+    ip, ids = _np(pos_indptr), _np(pos_ids)
+    return port.dense_y([ids[ip[b]:ip[b + 1]] for b in range(B)], L)
+
+
+def full_loss_forward(emb_used, W, pos_indptr, pos_ids, keep=None):
+    e = _np(emb_used)
+    yb = _dense_y_from_csr(pos_indptr, pos_ids, e.shape[0], W.shape[0])
+    loss, G, grad_emb = port.full_loss_forward(_np(W), e, _np(keep), yb)
+    return torch.tensor([loss], dtype=torch.float64), torch.from_numpy(G), torch.from_numpy(grad_emb)
+
+
+def full_loss_update(W, G, emb_used, lr, weight_decay=0.0):
+    port.full_loss_update(W.numpy(), _np(G), _np(emb_used), lr, weight_decay)  # in place (shared memory)
+
+
+def dense_probe_loss(emb, W, pos_indptr, pos_ids):
+    e = _np(emb)
+    mask = _dense_y_from_csr(pos_indptr, pos_ids, e.shape[0], W.shape[0]).astype(bool)
+    return torch.tensor([port.probe_full_loss(e, _np(W), mask)], dtype=torch.float64)
