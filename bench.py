@@ -563,6 +563,72 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_fullloss(args):
+    """The all-negatives arm (train_full_loss_baseline, trainer.py:563-616) at
+    the reference's label cap (L = 50,000, d = 768, B = 1024, 38 positives per
+    row): per step, scores E W^T, G and the float64 BCE, grad_emb = G W, and the
+    dense SGD of every row (G^T E) — three fp32 cuBLAS GEMMs (TF32 off) +
+    astra_dense_bce / astra_dense_sgd — next to the oracle port of the same
+    NumPy arithmetic on the host cores (one minibatch). The dense comparison
+    for the sampled arm."""
+    import torch
+
+    from oracle import xcmix_port as port
+    from paper_2409_20156_b200 import ops
+
+    torch.cuda.set_device(0)
+    L, d, B, lpp = 50_000, 768, 1024, 38
+    rng = np.random.default_rng(0)
+    W = rng.uniform(-1 / np.sqrt(d), 1 / np.sqrt(d), size=(L, d)).astype(np.float32)
+    embs = [rng.standard_normal((B, d)).astype(np.float32) for _ in range(4)]
+    lists = [[np.unique(rng.integers(0, L, lpp)) for _ in range(B)] for _ in range(4)]
+    csr = []
+    for ls in lists:
+        ip = np.zeros(B + 1, np.int64)
+        np.cumsum([len(p) for p in ls], out=ip[1:])
+        csr.append((torch.from_numpy(ip).cuda(), torch.from_numpy(np.concatenate(ls).astype(np.int32)).cuda()))
+    Wd = torch.from_numpy(W).cuda()
+    ed = [torch.from_numpy(e).cuda() for e in embs]
+    stream = torch.cuda.current_stream()
+
+    def one(t):
+        e = ed[t % 4]
+        loss, G, grad_emb = ops.full_loss_forward(e, Wd, *csr[t % 4])
+        ops.full_loss_update(Wd, G, e, 0.01, 1e-4)
+        return loss
+
+    for t in range(args.warmup):
+        one(t)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for t in range(args.steps):
+        loss = one(t)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.steps
+    flops = 3 * 2.0 * B * L * d
+    t0 = time.perf_counter()
+    Wc = W.copy()
+    yb = port.dense_y(lists[0], L)
+    _, G, _ = port.full_loss_forward(Wc, embs[0], None, yb)
+    port.full_loss_update(Wc, G, embs[0], 0.01, 1e-4)
+    t_cpu = time.perf_counter() - t0
+    line = {
+        "metric": "full-loss (all-negatives) arm train samples/s", "value": round(B / (ms / 1e3), 1),
+        "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32 (cuBLAS sgemm, TF32 off) + float64 loss", "data": "synthetic",
+        "config": {"workload": "train_full_loss_baseline at the reference's label cap", "n_labels": L, "dim": d,
+                   "minibatch": B, "labels_per_point": lpp},
+        "roofline": {"bound": "fp32 SIMT GEMM", "achieved": round(flops / (ms / 1e3) / 1e12, 2), "unit": "TFLOP/s",
+                     "algorithmic": f"3 GEMMs x 2*B*L*d = {flops:.3e} flop per step"},
+        "cpu_baseline": {"value": round(B / t_cpu, 2), "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+                         "sample": "one minibatch of the NumPy arm (oracle port), threads=all"},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -571,8 +637,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=128)
-    ap.add_argument("--config", default="c4", choices=["c4", "c5shard"],
-                    help="c4 (default, the headline line) or c5shard (120M-label config, one of 8 shards)")
+    ap.add_argument("--config", default="c4", choices=["c4", "c5shard", "fullloss"],
+                    help="c4 (default, the headline line), c5shard (120M-label config, one of 8 shards) or "
+                         "fullloss (the all-negatives arm at the reference's 50K-label cap)")
     ap.add_argument("--refresh-sms", type=int, default=0,
                     help="SM budget of the refresh running concurrently with training on a side stream (0 = serial)")
     args = ap.parse_args()
@@ -582,6 +649,8 @@ def main():
         run_reference(args)
     elif args.config == "c5shard":
         run_c5shard(args)
+    elif args.config == "fullloss":
+        run_fullloss(args)
     else:
         run_ours(args)
 
