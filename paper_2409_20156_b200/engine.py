@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import ops as cuda_ops
-from .errors import ConfigError, NumericalError
+from .errors import ConfigError, DataError, NumericalError
 from .shard import Comm, gather_csr, shard_range
 
 
@@ -208,6 +208,77 @@ class ClassifierEngine:
     def weights_host(self) -> np.ndarray:
         """This shard's W as fp32 NumPy (for eval / checkpoint boundaries)."""
         return self.W.float().cpu().numpy()
+
+    # ------------------------------------------------------------ checkpoint
+    _CKPT_MAGIC = b"XASH"
+    _CKPT_VERSION = 1
+    _CKPT_HEAD = "<4sIIIqqqiiiqfq"
+
+    def save_shard(self, path: str) -> str:
+        """Write this rank's shard — W in its own dtype, the Adam moments and
+        step, the running max|W| bound — to `path` (+ ".rank{r}" when
+        world > 1): the GPU-resident state the reference never checkpoints
+        (its XAST file, trainer.py:689-710, holds the fp32 weights only; the
+        full fp32 W for it is `weights_host()` gathered over the ranks).
+        Little-endian header: magic, version, rank, world, n_labels, lo, hi,
+        dim, w_dtype (0 fp32 / 1 bf16), optimizer (0 sgd / 1 adam),
+        adam_step, w_absmax, snapshot_epoch; then W, m, v row-major."""
+        import struct
+
+        fn = path if self.comm.world == 1 else f"{path}.rank{self.comm.rank}"
+        bf16 = self.W.dtype == torch.bfloat16
+        adam = self.optimizer == "adam"
+        head = struct.pack(self._CKPT_HEAD, self._CKPT_MAGIC, self._CKPT_VERSION, self.comm.rank, self.comm.world,
+                           self.n_labels, self.lo, self.hi, self.dim, int(bf16), int(adam), self.adam_step,
+                           float(self.w_absmax.item()), self.snapshot_epoch)
+        with open(fn, "wb") as fh:
+            fh.write(head)
+            w = self.W.contiguous().view(torch.int16) if bf16 else self.W.contiguous()
+            fh.write(w.cpu().numpy().tobytes())
+            if adam:
+                fh.write(self.m.cpu().numpy().tobytes())
+                fh.write(self.v.cpu().numpy().tobytes())
+        return fn
+
+    def load_shard(self, path: str) -> None:
+        """Restore a `save_shard` file into this engine (same shape, dtype,
+        optimizer and rank layout); raises ConfigError/DataError on mismatch."""
+        import struct
+
+        fn = path if self.comm.world == 1 else f"{path}.rank{self.comm.rank}"
+        hsize = struct.calcsize(self._CKPT_HEAD)
+        with open(fn, "rb") as fh:
+            head = fh.read(hsize)
+            if len(head) != hsize:
+                raise DataError("truncated shard checkpoint")
+            (magic, version, rank, world, n_labels, lo, hi, dim, bf16, adam, adam_step, w_absmax,
+             snap) = struct.unpack(self._CKPT_HEAD, head)
+            if magic != self._CKPT_MAGIC:
+                raise DataError("bad shard checkpoint magic")
+            if version != self._CKPT_VERSION:
+                raise DataError(f"unsupported shard checkpoint version {version}")
+            if (rank, world, n_labels, lo, hi, dim) != (self.comm.rank, self.comm.world, self.n_labels, self.lo,
+                                                         self.hi, self.dim):
+                raise ConfigError("shard checkpoint layout does not match this engine")
+            if bool(bf16) != (self.W.dtype == torch.bfloat16) or bool(adam) != (self.optimizer == "adam"):
+                raise ConfigError("shard checkpoint dtype / optimizer does not match this engine")
+            rows = hi - lo
+            wb = rows * dim * (2 if bf16 else 4)
+            buf = fh.read(wb)
+            if len(buf) != wb:
+                raise DataError("truncated shard checkpoint")
+            arr = np.frombuffer(buf, dtype=np.int16 if bf16 else np.float32).reshape(rows, dim)
+            t = torch.from_numpy(arr.copy())
+            self.W.copy_(t.view(torch.bfloat16) if bf16 else t)
+            if adam:
+                for dst in (self.m, self.v):
+                    buf = fh.read(rows * dim * 4)
+                    if len(buf) != rows * dim * 4:
+                        raise DataError("truncated shard checkpoint")
+                    dst.copy_(torch.from_numpy(np.frombuffer(buf, dtype=np.float32).reshape(rows, dim).copy()))
+        self.adam_step = int(adam_step)
+        self.w_absmax.fill_(float(w_absmax))
+        self.snapshot_epoch = int(snap)
 
 
 class _HostPipe:
