@@ -202,17 +202,19 @@ def test_per_row_origin_and_weights(cuda_lib, bound):
     close(Wd.cpu().numpy()[uids], Wref[uids])
 
 
-def test_label_sharded_step_equals_single(cuda_lib):
+@pytest.mark.parametrize("bound", [False, True])
+def test_label_sharded_step_equals_single(cuda_lib, bound):
     from paper_2409_20156_b200 import ops
 
     L = 6000
     W, emb, ids, y, origin, weights = _random_step(L, 256, 64, 60, 11, n_hot=5)
     full = dev(W)
-    r_full = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), full, 0.2, 1e-3)
+    r_full = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), full, 0.2, 1e-3,
+                            w_absmax=_bound(W, bound))
     cut = 2500
     shards = [dev(W[:cut]), dev(W[cut:])]
     rs = [ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), s, 0.2, 1e-3,
-                         label_offset=o) for s, o in zip(shards, [0, cut])]
+                         label_offset=o, w_absmax=_bound(W, bound)) for s, o in zip(shards, [0, cut])]
     torch.cuda.synchronize()
     np.testing.assert_array_equal(np.concatenate([s.cpu().numpy() for s in shards]), full.cpu().numpy())
     assert abs(sum(r.loss for r in rs) - r_full.loss) <= 1e-9 * abs(r_full.loss)
