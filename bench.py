@@ -353,6 +353,7 @@ def run_ours(args):
         "roofline": {"bound": "tensor", "kernel": "refresh_tc_kernel threshold pass (tcgen05 bf16 GEMM + fused candidate epilogue)",
                      "achieved": round(achieved_tf, 2), "peak": tf_sus, "unit": "TFLOP/s",
                      "frac": round(achieved_tf / tf_sus, 4), "traffic": traffic.get("refresh_gemm"),
+                     "frac_of_burst_peak": round(achieved_tf / tf_burst, 4),
                      "algorithmic": f"2*L_shard*d*Q = {flops:.3e} flop per launch (Q={q_per_refresh})",
                      "launch_ms": round(t_gemm * 1e3, 4), "launches": gemm_n,
                      "share_of_refresh": round(t_gemm / t_ref, 4),
