@@ -511,3 +511,44 @@ def test_refresh_empty_query_batch(cuda_lib):
                                          torch.zeros(0, dtype=torch.int32, device="cuda"), 8, "bf16_rerank",
                                          labels_f32=W, labels_bf16=ops.f32_to_bf16(W))
     assert ids.shape == (0, 8)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_step_fuzz_both_schedules(cuda_lib, seed):
+    """Random shapes (d in the vectorised set and off it, long and short
+    slates, hot labels, per-row origins/weights, dropout) through the default
+    single pass and the deterministic schedule, each against the oracle."""
+    from paper_2409_20156_b200 import _lib, ops
+
+    rng = np.random.default_rng(100 + seed)
+    d = int(rng.choice([128, 256, 384, 512, 768]))
+    L = int(rng.integers(300, 40_000))
+    B = int(rng.integers(1, 200))
+    S = int(rng.integers(20, 400))
+    n_hot = int(rng.integers(0, 6))
+    W, emb, ids, y, origin, weights = _random_step(L, d, B, S, 1000 + seed, min(n_hot, S - 20))
+    if seed % 2:
+        origin = np.tile(origin, (B, 1))
+        origin[rng.random(origin.shape) < 0.05] = port.ORIGIN_PAD
+        weights = rng.uniform(0.5, 30, size=(B, S)).astype(np.float32)
+    keep = ((rng.random((B, d)) >= 0.1).astype(np.float32) / np.float32(0.9)) if seed % 3 == 0 else None
+    emb_used = emb * keep if keep is not None else emb
+    Wref = W.copy()
+    loss, grad_emb, _, uids = port.slate_step(Wref, emb_used, keep, ids, y, origin, weights, 0.2, 1e-3)
+    for det in (False, True):
+        _lib.set_step_deterministic(det)
+        try:
+            Wd = dev(W)
+            res = ops.slate_step(dev(emb_used), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wd, 0.2,
+                                 1e-3, keep=None if keep is None else dev(keep), w_absmax=_bound(W, True))
+            torch.cuda.synchronize()
+        finally:
+            _lib.set_step_deterministic(False)
+        assert res.status_host() == [0, 0, 0, 0]
+        assert abs(res.loss - loss) <= 1e-5 * abs(loss)
+        close(res.grad_emb.cpu().numpy(), grad_emb)
+        Wg = Wd.cpu().numpy()
+        close(Wg[uids], Wref[uids])
+        mask = np.ones(L, bool)
+        mask[uids] = False
+        np.testing.assert_array_equal(Wg[mask], W[mask])
