@@ -101,14 +101,29 @@ __global__ void __launch_bounds__(kThreads) sample_slates_kernel(SamplerArgs a) 
   //    in increasing order = a uniformly random ordered subset (trainer.py:273-281)
   if (tid < 32) {
     const int take = static_cast<int>(npos < a.k_p ? npos : a.k_p);
+    auto poskey = [&](int64_t p) {
+      return (static_cast<uint64_t>(draw(a, row, static_cast<uint32_t>(p), TAG_POSKEY).x) << 32) |
+             static_cast<uint32_t>(p);
+    };
+    // rows with <= 64 positives: every key drawn once, held in registers
+    const bool cached = npos <= 64;
+    uint64_t k0 = ~0ull, k1 = ~0ull;
+    if (cached && take > 0) {
+      if (tid < npos) k0 = poskey(tid);
+      if (tid + 32 < npos) k1 = poskey(tid + 32);
+    }
     uint64_t prev = 0;
     bool first = true;
     for (int r = 0; r < take; ++r) {
       uint64_t best = ~0ull;
-      for (int64_t p = tid; p < npos; p += 32) {
-        uint64_t kp = (static_cast<uint64_t>(draw(a, row, static_cast<uint32_t>(p), TAG_POSKEY).x) << 32) |
-                      static_cast<uint32_t>(p);
-        if ((first || kp > prev) && kp < best) best = kp;
+      if (cached) {
+        if ((first || k0 > prev) && k0 < best) best = k0;
+        if ((first || k1 > prev) && k1 < best) best = k1;
+      } else {
+        for (int64_t p = tid; p < npos; p += 32) {
+          const uint64_t kp = poskey(p);
+          if ((first || kp > prev) && kp < best) best = kp;
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -125,12 +140,18 @@ __global__ void __launch_bounds__(kThreads) sample_slates_kernel(SamplerArgs a) 
       first = false;
     }
   }
-  __syncthreads();
+  // Without importance draws nothing below depends on warp 0's work (the
+  // subset above writes slots [0, min(npos, k_p)), skipped below): warps 1..
+  // take every other slot and run concurrently with it, no barrier.
+  const bool split = !use_cand;
+  if (!split) __syncthreads();  // the CDF (thread 0)
+  if (split && tid < 32) return;
 
-  const double tot = s_total;
+  const double tot = split ? 0.0 : s_total;
   const float w_rand = a.k_r > 0 ? static_cast<float>(static_cast<double>(a.L - a.m) / a.k_r) : 0.0f;
   const int h0 = a.k_p, i0 = a.k_p + a.k_h, r0 = a.k_p + a.k_h + a.k_i;
-  for (int j = tid; j < a.S; j += kThreads) {
+  const int j0 = split ? tid - 32 : tid, jstep = split ? kThreads - 32 : kThreads;
+  for (int j = j0; j < a.S; j += jstep) {
     int32_t id;
     int8_t yy, oo;
     float ww;
