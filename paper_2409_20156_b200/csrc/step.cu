@@ -1209,6 +1209,9 @@ __device__ __forceinline__ void load_emb_row(const float* emb, int b, int lane, 
 #ifndef ASTRA_SINGLE_CTAS
 #define ASTRA_SINGLE_CTAS 4
 #endif
+#ifndef ASTRA_SINGLE_ADAM_EARLY
+#define ASTRA_SINGLE_ADAM_EARLY 1  // Adam: moments into registers with the row, ring entry released at once
+#endif
 #ifndef ASTRA_SINGLE_ADAM_CTAS
 #define ASTRA_SINGLE_ADAM_CTAS 2
 #endif
@@ -1457,6 +1460,17 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
         p[q] = *reinterpret_cast<const float4*>(ent + (q * 128 + lane * 4) * 4);
       }
     }
+    constexpr bool EARLY = ADAM && ASTRA_SINGLE_ADAM_EARLY;
+    float4 mr[EARLY ? NV : 1], vr[EARLY ? NV : 1];
+    if constexpr (EARLY) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        mr[q] = *reinterpret_cast<const float4*>(ent + RG::WB + (q * 128 + lane * 4) * 4);
+        vr[q] = *reinterpret_cast<const float4*>(ent + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[r]);
+    }
     const uint32_t n = dc.n;
     const size_t row = static_cast<size_t>(dc.l) * d;
     // the row update, element by element, from the label's gradient G(q)
@@ -1467,8 +1481,14 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
         float4 np;
         const size_t el = row + q * 128 + lane * 4;
         if constexpr (ADAM) {
-          float4 m4 = *reinterpret_cast<const float4*>(ent + RG::WB + (q * 128 + lane * 4) * 4);
-          float4 v4 = *reinterpret_cast<const float4*>(ent + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
+          float4 m4, v4;
+          if constexpr (EARLY) {
+            m4 = mr[q];
+            v4 = vr[q];
+          } else {
+            m4 = *reinterpret_cast<const float4*>(ent + RG::WB + (q * 128 + lane * 4) * 4);
+            v4 = *reinterpret_cast<const float4*>(ent + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
+          }
           np.x = upd_elem<true>(a, p[q].x, gq.x, &m4.x, &v4.x);
           np.y = upd_elem<true>(a, p[q].y, gq.y, &m4.y, &v4.y);
           np.z = upd_elem<true>(a, p[q].z, gq.z, &m4.z, &v4.z);
@@ -1587,7 +1607,7 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       }
       update_row([&](int q) { return *reinterpret_cast<const float4*>(gs + q * 128); });
     }
-    if constexpr (ADAM) {
+    if constexpr (ADAM && !EARLY) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[r]);
     }
