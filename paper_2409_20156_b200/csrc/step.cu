@@ -1161,10 +1161,13 @@ __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(Up
 }
 
 // ================================================================ single-pass step
-// The default schedule for d % 128 == 0: ONE label-major pass over the touched
-// rows. Each CTA owns a contiguous chunk of the sorted unique-label list; a
-// producer lane streams the chunk's W rows (+ Adam m, v) into a shared-memory
-// ring with bulk copies; consumer warp w takes labels w, w+4, ... For label l
+// The default schedule for SGD (and Adam shards >= 32 GB of W+m+v) when
+// d % 128 == 0, d <= 768: ONE label-major pass over the touched rows. Each CTA
+// owns a contiguous chunk of the sorted unique-label list; a producer warp
+// builds each label's descriptor (bucket, first occurrence + its metadata)
+// into an in-order queue and bulk-copies the W row (+ Adam m, v) into any free
+// data slot of a shared-memory pool; consumer warp w takes labels w, w+4, ...,
+// pulling the next label's embedding row towards L1 first. For label l
 // it holds the OLD row in registers and walks l's slots in ascending b*S+s
 // order: score = <emb_b, W_l> (the forward's fma order and butterfly, so the
 // same bits), factor (trainer.py:369-380), g += f * emb_b (label_update's
@@ -1182,8 +1185,9 @@ __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(Up
 // max|emb|, scan_top_kernel decides (mode = 1: this pass; 0: the two-kernel
 // schedule, whose kernels are launched too and return at once when mode = 1).
 // grad_emb's summation order over slots follows the reduction order, so it is
-// not bitwise run-to-run deterministic (ASTRA_STEP_SINGLE=0 selects the
-// deterministic two-kernel schedule); the loss is reduced per row in slot
+// not bitwise run-to-run deterministic (astra_set_step_deterministic(1) or
+// ASTRA_STEP_SINGLE=0 select the deterministic two-kernel schedule); the fp64
+// loss terms are evaluated lane-parallel in the pass and reduced per row in slot
 // order by single_row_finalize from the stored per-slot fp64 loss terms.
 struct SingleArgs {
   FwdArgs f;
