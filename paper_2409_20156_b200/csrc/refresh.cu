@@ -752,14 +752,8 @@ TwoPass plan_two_pass(int64_t nq, int64_t L, int kk, int n_parts) {
   t.j = j;
   t.n_groups = static_cast<int>(n_lt_s * 4);
   t.cand_cap = cap;
-  // select capacity: 1.5x the expected candidate count (j * stride over all
-  // parts; sd ~ its square root) rounded up to a power of two, not above the
-  // lists' total capacity. Smaller per-warp staging = more select warps per SM
-  // (2048 -> 1024 entries at the bench shape: 3 -> 5 CTAs/SM); a query beyond
-  // it is flagged and takes the exact fallback.
-  const int64_t want = static_cast<int64_t>(1.5 * static_cast<double>(j) * kSampleStride) + 64;
   int sm = 1;
-  while (sm < want && sm < cap * n_parts) sm <<= 1;
+  while (sm < cap * n_parts) sm <<= 1;
   t.sel_max = std::min(sm, kSelMax);
   return t;
 }
