@@ -231,7 +231,7 @@ def run_ours(args):
     eng.comm.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
-    for name in ("refresh_gemm", "step_single", "slot_forward", "label_update"):
+    for name in ("refresh_gemm", "refresh_verify", "step_single", "slot_forward", "label_update"):
         _lib.kernel_timing(name)  # drop warm-up records
     _lib.kernel_timing_enable(True)
     t_start = torch.cuda.Event(enable_timing=True)
@@ -246,7 +246,7 @@ def run_ours(args):
     clk = clocks.stop()
     launches = _lib.launch_count() - launches0
     _lib.kernel_timing_enable(False)
-    kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "step_single", "slot_forward", "label_update")}
+    kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "refresh_verify", "step_single", "slot_forward", "label_update")}
     ops.raise_for_step_status(status)
     ms_t = torch.tensor([t_start.elapsed_time(t_end)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -348,6 +348,9 @@ def run_ours(args):
                        refresh_sms=args.refresh_sms if overlap else None),
         "phases_ms_per_step": {k: round(v / K, 4) for k, v in ph.items()},
         "refresh_mips_qps": round(q_per_refresh / t_ref, 1),
+        # the exact fallback of the two-pass refresh (running top-k for query
+        # tiles holding a flagged query): ~0 when every query was proven exact
+        "refresh_verify_ms": round(kt["refresh_verify"][0] / max(kt["refresh_verify"][1], 1), 4),
         "step_only_samples_per_s": round(B * world / (t_step + t_samp), 1),
         "composite_tau_r5_samples_per_s": round(R * world / (M * (t_step + t_samp) + t_ref / 5), 1),
         "roofline": {"bound": "tensor", "kernel": "refresh_tc_kernel threshold pass (tcgen05 bf16 GEMM + fused candidate epilogue)",
@@ -440,7 +443,7 @@ def run_c5shard(args):
     for t in range(args.warmup):
         one(t)
     torch.cuda.synchronize()
-    for name in ("refresh_gemm", "step_single", "slot_forward", "label_update"):
+    for name in ("refresh_gemm", "refresh_verify", "step_single", "slot_forward", "label_update"):
         _lib.kernel_timing(name)
     _lib.kernel_timing_enable(True)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -450,7 +453,7 @@ def run_c5shard(args):
     t1.record(stream)
     torch.cuda.synchronize()
     _lib.kernel_timing_enable(False)
-    kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "step_single", "slot_forward", "label_update")}
+    kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "refresh_verify", "step_single", "slot_forward", "label_update")}
     ops.raise_for_step_status(res.status)
     K = args.steps
     ms = t0.elapsed_time(t1) / K
@@ -480,6 +483,7 @@ def run_c5shard(args):
                    "unique_rows": U},
         "phases_ms_per_step": {k: round(v, 3) for k, v in ph.items()},
         "refresh_mips_qps_shard": round(B / (ph["refresh"] / 1e3), 1),
+        "refresh_verify_ms": round(kt["refresh_verify"][0] / max(kt["refresh_verify"][1], 1), 4),
         "composite_tau_r5_samples_per_s": round(B / ((ph["sample"] + ph["step"] + ph["refresh"] / 5) / 1e3), 1),
         "roofline": {"bound": "tensor", "kernel": "refresh_tc_kernel threshold pass", "achieved": round(achieved, 2),
                      "peak": tf_sus, "unit": "TFLOP/s", "frac": round(achieved / tf_sus, 4),

@@ -994,7 +994,11 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
       v.cap = cap;
       v.only_flagged = w.flags;
       prof.mark("select");
-      ASTRA_TRY(launch_refresh_tc(v, st));
+      {
+        // (near zero unless a query was flagged: bench.py reports it per refresh)
+        KernelTimer kt("refresh_verify", st);
+        ASTRA_TRY(launch_refresh_tc(v, st));
+      }
       ASTRA_TRY(topk_merge_only(w.part_keys, nq, n_parts, kk, kk, o_keys, o_ids, o_scores, w.merge_bufs, w.flags, st));
       prof.mark("verify");
     } else {
