@@ -547,38 +547,51 @@ __global__ void __launch_bounds__(256) tau_select_kernel(const uint32_t* gmax, i
 // exist and no list overflowed (every key of the true top-k is >= the k-th
 // candidate >= the threshold, hence a candidate); otherwise the query is
 // flagged for the exact running-top-k fallback.
-constexpr int kSelWarps = 4, kSelSmall = 256, kSelPos = 128;
+constexpr int kSelWarps = 4, kSelSmall = 256, kSelPos = 128, kSelMaxParts = 64;
 
 __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* cand, const int32_t* cand_cnt,
                                                                 int n_parts, int cand_cap, int64_t nq,
                                                                 const int64_t* pos_indptr, const int32_t* pos_ids,
                                                                 int k, int sel_max, uint64_t* out_keys,
                                                                 int32_t* out_ids, float* out_scores, int32_t* flags) {
+  // per warp: the candidates' 32-bit score parts (the radix select reads
+  // them four times) and R, the full keys of those at or above T2 (read back
+  // from the lists) — half the staging of full keys, so more warps per SM
   extern __shared__ __align__(16) uint64_t sel_smem[];
+  __shared__ int32_t sel_off[kSelWarps][kSelMaxParts + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t q = static_cast<int64_t>(blockIdx.x) * kSelWarps + warp;
   if (q >= nq) return;  // warp-uniform
-  uint64_t* S = sel_smem + static_cast<size_t>(warp) * (sel_max + kSelSmall);
-  uint64_t* R = S + sel_max;
+  uint64_t* R = sel_smem + static_cast<size_t>(warp) * (kSelSmall + sel_max / 2);
+  uint32_t* S = reinterpret_cast<uint32_t*>(R + kSelSmall);
   int total = 0;
-  bool overflow = false;
-  for (int p = 0; p < n_parts; ++p) {
+  bool overflow = n_parts > kSelMaxParts;
+  for (int p = 0; p < n_parts && !overflow; ++p) {
     const int c = cand_cnt[static_cast<size_t>(p) * nq + q];
     overflow |= c > cand_cap;
+    if (lane == 0) sel_off[warp][p] = total;
     total += c < cand_cap ? c : cand_cap;
   }
+  if (lane == 0 && !overflow) sel_off[warp][n_parts] = total;
   bool fail = overflow || total > sel_max;
   if (lane == 0 && fail) flags[q] = 1;
   if (fail) return;
+  __syncwarp();
   const int64_t p0 = pos_indptr[q], np = pos_indptr[q + 1] - p0;
-  // 1. the candidates -> shared memory (independent loads, no per-key work)
+  // full key of candidate i (parts concatenated in order)
+  auto key_at = [&](int i) {
+    int p = 0;
+    while (i >= sel_off[warp][p + 1]) ++p;
+    return cand[(static_cast<size_t>(p) * nq + q) * cand_cap + (i - sel_off[warp][p])];
+  };
+  // 1. the candidates' scores -> shared memory (independent loads)
   {
     int o = 0;
     for (int p = 0; p < n_parts; ++p) {
       const int c = min(cand_cnt[static_cast<size_t>(p) * nq + q], cand_cap);
       const uint64_t* src = cand + (static_cast<size_t>(p) * nq + q) * cand_cap;
 #pragma unroll 4
-      for (int e = lane; e < c; e += 32) S[o + e] = src[e];
+      for (int e = lane; e < c; e += 32) S[o + e] = static_cast<uint32_t>(src[e] >> 32);
       o += c;
     }
   }
@@ -591,28 +604,32 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
   const int k2 = static_cast<int>(k2l < total ? k2l : total);
   const uint32_t T = warp_kth_largest(
       [&](int i, uint32_t& x) {
-        x = static_cast<uint32_t>(S[i] >> 32);
+        x = S[i];
         return true;
       },
       total, k2, sel_hist[warp], lane);
-  // 3. warp-aggregated compaction of the keys with score >= T2
+  // 3. warp-aggregated compaction of the keys with score >= T2 (full keys
+  //    fetched back from the lists for those only)
   int nr = 0;
   for (int i0 = 0; i0 < total; i0 += 32) {
     const int i = i0 + lane;
-    const uint64_t v = i < total ? S[i] : 0ull;
-    const bool take = v != 0ull && static_cast<uint32_t>(v >> 32) >= T;
+    const uint32_t sc = i < total ? S[i] : 0u;
+    const bool take = i < total && sc >= T;
     const unsigned bm = __ballot_sync(0xffffffffu, take);
     const int at = nr + __popc(bm & ((1u << lane) - 1u));
-    if (take && at < kSelSmall) R[at] = v;
+    if (take && at < kSelSmall) {
+      const uint64_t v = key_at(i);
+      R[at] = v;
+    }
     nr += __popc(bm);
   }
   __syncwarp();
-  uint64_t* X = R;
-  int n = nr;
-  if (nr > kSelSmall) {  // pathological score ties: work on every candidate
-    X = S;
-    n = total;
+  if (nr > kSelSmall) {  // pathological score ties: the exact fallback
+    if (lane == 0) flags[q] = 1;
+    return;
   }
+  uint64_t* X = R;
+  const int n = nr;
   // 4. drop the query's positives (anns.py:254-255) among them (positives in shared memory)
   __shared__ int32_t sel_pos[kSelWarps][kSelPos];
   const bool pos_smem = np <= kSelPos;
@@ -982,7 +999,7 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
       }
       prof.mark("threshold");
       // 3. select
-      const size_t smem = sizeof(uint64_t) * (tp.sel_max + kSelSmall) * kSelWarps;
+      const size_t smem = (sizeof(uint64_t) * kSelSmall + sizeof(uint32_t) * tp.sel_max) * kSelWarps;
       cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       select_kernel<<<static_cast<unsigned>((nq + kSelWarps - 1) / kSelWarps), kSelWarps * 32, smem, st>>>(
           w.cand, w.cand_cnt, n_parts, tp.cand_cap, nq, pos_indptr, pos_ids, kk, tp.sel_max, o_keys, o_ids, o_scores,
