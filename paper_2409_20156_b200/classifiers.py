@@ -30,3 +30,8 @@ def apply_classifier_updates_arrays(bank, ids, grads, lr, weight_decay=0.0) -> N
     local = torch.arange(len(ids), dtype=torch.int64, device=dev)
     ops.apply_updates(rows, local, g, float(lr), float(weight_decay))  # raises before writing
     W[ids] = rows.cpu().numpy()
+    # keep the trainer's device mirror of this bank (if any) and its max|W|
+    # bound in step with the host array
+    from .trainer import DeviceBank
+
+    DeviceBank.update_rows(bank, ids, rows)

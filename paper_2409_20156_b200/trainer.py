@@ -53,6 +53,10 @@ class DeviceBank:
     def __init__(self, host: np.ndarray):
         self.host = host
         self.W = torch.from_numpy(np.ascontiguousarray(host, dtype=np.float32)).to(_backend.device())
+        # running max|W| bound, kept current by every step: lets astra_slate_step
+        # prove finiteness up front and take the single label-major pass
+        self.w_absmax = (self.W.abs().amax().reshape(1).float() if self.W.numel()
+                         else torch.zeros(1, dtype=torch.float32, device=self.W.device))
 
     @classmethod
     def for_bank(cls, owner, bank) -> "DeviceBank":
@@ -60,7 +64,25 @@ class DeviceBank:
         if db is None or db.host is not bank.weights:
             db = cls(bank.weights)
             owner._astra_bank = db
+            try:  # reachable from the bank too (classifiers.apply_* keeps it in step)
+                bank._astra_mirror = db
+            except AttributeError:
+                pass
         return db
+
+    @staticmethod
+    def update_rows(bank, ids, rows_dev) -> None:
+        """After a host-side row update of `bank`: copy the rows into the
+        bank's device mirror, if one exists for this very array, and raise the
+        max|W| bound to cover them."""
+        db = getattr(bank, "_astra_mirror", None)
+        if db is None or db.host is not bank.weights:
+            return
+        idx = torch.as_tensor(np.asarray(ids, dtype=np.int64), device=db.W.device)
+        r = rows_dev.to(db.W.device, db.W.dtype)
+        db.W[idx] = r
+        if r.numel():
+            torch.maximum(db.w_absmax, r.abs().amax().reshape(1).float(), out=db.w_absmax)
 
     def sync_rows(self, ids: torch.Tensor) -> None:
         """Copy the given (device) rows back into the host array."""
@@ -142,7 +164,7 @@ def _batch_forward_backward(state, batch_rows, epoch, rng, step_lr_enc, step_lr_
         torch.from_numpy(np.ascontiguousarray(origin, dtype=np.int8)).to(dev),
         torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float32)).to(dev), bank.W, float(step_lr_clf),
         float(cfg.weight_decay_classifier),
-        keep=None if keep is None else torch.from_numpy(np.ascontiguousarray(keep)).to(dev))
+        keep=None if keep is None else torch.from_numpy(np.ascontiguousarray(keep)).to(dev), w_absmax=bank.w_absmax)
     grad_emb = res.grad_emb.cpu().numpy()
     status = res.status_host()
     # encoder half stays with the caller; it raises NumericalError on a
