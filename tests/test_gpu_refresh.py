@@ -240,3 +240,15 @@ def test_bf16_rerank_from_bf16_labels(cuda_lib, k):
     _, exact_ids, exact_scores = _run(E, W_rounded, positives, k, "fp32")
     np.testing.assert_array_equal(ids.cpu().numpy(), exact_ids)
     np.testing.assert_array_equal(scores.cpu().numpy(), exact_scores)
+
+
+@pytest.mark.parametrize("n", [1, 3, 4, 1023, 4096 * 37 + 5, 7_077_888])
+def test_f32_to_bf16_matches_torch_rne(cuda_lib, n):
+    """The snapshot conversion is round-to-nearest-even, like torch's cast,
+    for every length (vector body + tails)."""
+    from paper_2409_20156_b200 import ops
+
+    x = torch.randn(n, device="cuda") * 3
+    x[: min(n, 4)] = torch.tensor([0.0, -0.0, 1e-40, 3.0e38][: min(n, 4)], device="cuda")
+    got = ops.f32_to_bf16(x)
+    assert torch.equal(got.view(torch.int16), x.to(torch.bfloat16).view(torch.int16))
