@@ -18,6 +18,14 @@ paper_2409_20156_b200/shard.py.
 --impl reference times the reference's own CPU algorithm (oracle/xcmix_port.py,
 a bit-pinned restatement of xcmix — /root/reference is absent on the GPU box)
 on the host cores with the same metric.
+
+Other lines (not the driver's): --config c5shard (one 15M-label shard of the
+120M config, bf16 W + Adam) and --config fullloss (the all-negatives arm at
+the reference's 50K-label cap). The JSON line's `roofline` is the refresh
+GEMM pass (tensor-bound), `roofline_step` the minibatch step with the
+per-kernel DRAM rate of the single label-major pass (or of the two step
+kernels under the deterministic schedule), `refresh_verify_ms` the refresh's
+exact-fallback time (~0 when every query is proven exact).
 """
 
 from __future__ import annotations
