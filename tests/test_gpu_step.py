@@ -452,7 +452,7 @@ def test_host_api_pipelined_equals_device_api(cuda_lib):
         loss_d, ge_d, _ = b.step(dev(emb), sl, 0.05, 1e-4)
         np.testing.assert_array_equal(host_out[-1][0], ids_d.cpu().numpy())
         # (the default single-pass schedule sums grad_emb in arrival order)
-        close(host_out[-1][1], ge_d.cpu().numpy(), rtol=1e-6, floor=1e-7)
+        close(host_out[-1][1], ge_d.cpu().numpy())  # the north-star 1e-5 tolerance
         assert host_out[-1][2] == float(loss_d.item())
     np.testing.assert_array_equal(a.W.cpu().numpy(), b.W.cpu().numpy())
 
