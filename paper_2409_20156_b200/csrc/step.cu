@@ -549,7 +549,13 @@ __device__ __forceinline__ float absmax4(float4 v) {
 __global__ void __launch_bounds__(256) count_kernel(const int32_t* ids, int64_t n, int64_t off, int64_t Lloc,
                                                     uint32_t* counts, int32_t* rank, int32_t* status,
                                                     const float* weights, int64_t wstride, int S, const float* emb,
-                                                    int64_t n_emb, double* sf_acc, unsigned* emax_acc) {
+                                                    int64_t n_emb, double* sf_acc, unsigned* emax_acc,
+                                                    float* zero_out) {
+  if (zero_out) {  // (n_emb floats, 16-byte aligned on the single-pass path)
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_emb / 4;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      reinterpret_cast<float4*>(zero_out)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   double sf = 0.0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -2761,9 +2767,10 @@ size_t carve_step(void* base, size_t cap, int B, int S, int64_t Lloc, StepWs* w)
   w->row_locs = c.take<int32_t>(n);
   w->row_cofs = c.take<int32_t>(static_cast<size_t>(B) * (kMaxChunks + 1));
   w->uc = c.take<uint32_t>(kMaxChunks + 1);
-  w->bar = c.take<unsigned>(4);  // bar, emax_acc, (pad), then the fp64 accumulator
+  // one 32-byte block (a single memset): bar, emax_acc, (pad x2), the fp64 accumulator
+  w->bar = c.take<unsigned>(8);
   w->emax_acc = w->bar ? w->bar + 1 : nullptr;
-  w->sf_acc = c.take<double>(1);
+  w->sf_acc = w->bar ? reinterpret_cast<double*>(w->bar + 4) : nullptr;
   w->pipe_ctr = c.take<unsigned>(2 * kMaxChunks + 4);
   w->mode = c.take<int32_t>(4);
   w->slot_loss = c.take<double>(n);
@@ -2879,7 +2886,8 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
   const double shard_state_bytes = static_cast<double>(Lloc) * d * ((bf16 ? 2 : 4) + 8);
   const bool single_adam = single_adam_env >= 0 ? single_adam_env != 0 : shard_state_bytes >= 32e9;
   const bool single = !fused && single_env && !g_step_deterministic.load() && chunkable && nv <= 6 &&
-                      (!adam || single_adam);
+                      (!adam || single_adam) &&
+                      reinterpret_cast<uintptr_t>(grad_emb) % 16 == 0;  // (vector reductions into it)
   if (single) fa.skip = w.mode;
 
   // counting sort of the slots by local label id (+ the single pass's bounds and decision)
@@ -2890,12 +2898,11 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
   const int grid_n = static_cast<int>(std::min<int64_t>((n + 255) / 256, 8LL * sms));
   if (Lloc > 0) {
     ASTRA_TRY(check_cuda(cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * Lloc, st), "memset counts"));
-    if (single) {
-      ASTRA_TRY(check_cuda(cudaMemsetAsync(w.bar, 0, 4 * sizeof(unsigned), st), "memset bounds"));
-      ASTRA_TRY(check_cuda(cudaMemsetAsync(w.sf_acc, 0, sizeof(double), st), "memset bound"));
-    }
+    if (single) ASTRA_TRY(check_cuda(cudaMemsetAsync(w.bar, 0, 8 * sizeof(unsigned), st), "memset bounds"));
+    // (single pass: count_kernel also zeroes grad_emb, which the pass reduces into)
     count_kernel<<<grid_n, 256, 0, st>>>(ids, n, off, Lloc, w.counts, w.rank, status, weights, weights_stride, S, emb,
-                                         static_cast<int64_t>(B) * d, single ? w.sf_acc : nullptr, w.emax_acc);
+                                         static_cast<int64_t>(B) * d, single ? w.sf_acc : nullptr, w.emax_acc,
+                                         single ? grad_emb : nullptr);
     ASTRA_LAUNCHED("count");
     scan_reduce_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz);
     ASTRA_LAUNCHED("scan_reduce");
@@ -2939,7 +2946,6 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
   ua.w_absmax = w_absmax;
   ua.skip = single ? w.mode : nullptr;
   if (single) {
-    ASTRA_TRY(check_cuda(cudaMemsetAsync(grad_emb, 0, sizeof(float) * B * d, st), "memset grad_emb"));
     SingleArgs SA;
     SA.f = fa;
     SA.u = ua;
@@ -3005,8 +3011,7 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     row_bucket_kernel<<<static_cast<unsigned>((B + 7) / 8), 256, 0, st>>>(ids, B, S, off, Lloc, Lc, C, w.row_slots,
                                                                           w.row_locs, w.row_cofs);
     ASTRA_LAUNCHED("row_bucket");
-    ASTRA_TRY(check_cuda(cudaMemsetAsync(w.bar, 0, 4 * sizeof(unsigned), st), "memset barrier"));
-    ASTRA_TRY(check_cuda(cudaMemsetAsync(w.sf_acc, 0, sizeof(double), st), "memset bound"));
+    ASTRA_TRY(check_cuda(cudaMemsetAsync(w.bar, 0, 8 * sizeof(unsigned), st), "memset barrier + bounds"));
     if (piped)
       ASTRA_TRY(check_cuda(cudaMemsetAsync(w.pipe_ctr, 0, sizeof(unsigned) * (2 * kMaxChunks + 4), st), "memset pipe"));
     FusedArgs A;
