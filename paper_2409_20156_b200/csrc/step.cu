@@ -2807,8 +2807,8 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
   size_t need = carve_step(workspace, ws_bytes, B, S, Lloc, &w);
   if (!workspace || ws_bytes < need) return set_error(ASTRA_ERR_CONFIG, "step workspace too small (%zu < %zu)", ws_bytes, need);
   ASTRA_TRY(check_cuda(cudaMemsetAsync(status, 0, sizeof(int32_t) * ASTRA_STATUS_WORDS, st), "memset status"));
-  ASTRA_TRY(check_cuda(cudaMemsetAsync(loss_out, 0, sizeof(double), st), "memset loss"));
-  if (B == 0 || S == 0) {
+  if (B == 0 || S == 0) {  // (otherwise finalize_kernel assigns the loss)
+    ASTRA_TRY(check_cuda(cudaMemsetAsync(loss_out, 0, sizeof(double), st), "memset loss"));
     if (B) ASTRA_TRY(check_cuda(cudaMemsetAsync(grad_emb, 0, sizeof(float) * B * d, st), "memset grad_emb"));
     return ASTRA_OK;
   }
