@@ -563,10 +563,18 @@ __global__ void __launch_bounds__(256) tau_select_kernel(const uint32_t* gmax, i
 // flagged for the exact running-top-k fallback.
 constexpr int kSelWarps = 4, kSelSmall = 256, kSelPos = 128, kSelMaxParts = 64;
 
+// Capacity of R, the keys at or above T2 (about k + |P| of them): a power of
+// two >= max(kSelSmall, 2k).
+inline int sel_rcap(int k) {
+  int r = kSelSmall;
+  while (r < 2 * k) r <<= 1;
+  return r;
+}
+
 __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* cand, const int32_t* cand_cnt,
                                                                 int n_parts, int cand_cap, int64_t nq,
                                                                 const int64_t* pos_indptr, const int32_t* pos_ids,
-                                                                int k, int sel_max, uint64_t* out_keys,
+                                                                int k, int sel_max, int rcap, uint64_t* out_keys,
                                                                 int32_t* out_ids, float* out_scores, int32_t* flags) {
   // per warp: the candidates' 32-bit score parts (the radix select reads
   // them four times) and R, the full keys of those at or above T2 (read back
@@ -576,8 +584,8 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t q = static_cast<int64_t>(blockIdx.x) * kSelWarps + warp;
   if (q >= nq) return;  // warp-uniform
-  uint64_t* R = sel_smem + static_cast<size_t>(warp) * (kSelSmall + sel_max / 2);
-  uint32_t* S = reinterpret_cast<uint32_t*>(R + kSelSmall);
+  uint64_t* R = sel_smem + static_cast<size_t>(warp) * (rcap + sel_max / 2);
+  uint32_t* S = reinterpret_cast<uint32_t*>(R + rcap);
   int total = 0;
   bool overflow = n_parts > kSelMaxParts;
   for (int p = 0; p < n_parts && !overflow; ++p) {
@@ -631,14 +639,14 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
     const bool take = i < total && sc >= T;
     const unsigned bm = __ballot_sync(0xffffffffu, take);
     const int at = nr + __popc(bm & ((1u << lane) - 1u));
-    if (take && at < kSelSmall) {
+    if (take && at < rcap) {
       const uint64_t v = key_at(i);
       R[at] = v;
     }
     nr += __popc(bm);
   }
   __syncwarp();
-  if (nr > kSelSmall) {  // pathological score ties: the exact fallback
+  if (nr > rcap) {  // pathological score ties: the exact fallback
     if (lane == 0) flags[q] = 1;
     return;
   }
@@ -1013,11 +1021,12 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
       }
       prof.mark("threshold");
       // 3. select
-      const size_t smem = (sizeof(uint64_t) * kSelSmall + sizeof(uint32_t) * tp.sel_max) * kSelWarps;
+      const int rcap = sel_rcap(kk);
+      const size_t smem = (sizeof(uint64_t) * rcap + sizeof(uint32_t) * tp.sel_max) * kSelWarps;
       cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       select_kernel<<<static_cast<unsigned>((nq + kSelWarps - 1) / kSelWarps), kSelWarps * 32, smem, st>>>(
-          w.cand, w.cand_cnt, n_parts, tp.cand_cap, nq, pos_indptr, pos_ids, kk, tp.sel_max, o_keys, o_ids, o_scores,
-          w.flags);
+          w.cand, w.cand_cnt, n_parts, tp.cand_cap, nq, pos_indptr, pos_ids, kk, tp.sel_max, rcap, o_keys, o_ids,
+          o_scores, w.flags);
       ASTRA_LAUNCHED("select");
       // 4. verify: exact running top-k for the flagged query tiles only
       TcLaunch v = p;

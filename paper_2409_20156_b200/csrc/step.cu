@@ -1016,8 +1016,14 @@ struct UpdRing {
   static constexpr size_t smem() { return static_cast<size_t>(RING) * ENTRY + 2 * 8 * RING; }
 };
 
+// CTAs per SM of the TMA update: three (Adam too: 124 registers and an
+// 8 x 9 KB ring fit; 1.31 vs 1.67 ms per minibatch at 2 for bf16 Adam), except
+// Adam at d = 1024, whose moments spill at three.
+template <int NV, bool ADAM>
+constexpr int upd_tma_ctas() { return ADAM && NV > 6 ? 2 : 3; }
+
 template <int NV, bool BF16, bool ADAM>
-__global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(UpdArgs a) {
+__global__ void __launch_bounds__(kTmaThreads, upd_tma_ctas<NV, ADAM>()) label_update_tma(UpdArgs a) {
   if (a.skip && *a.skip) return;
   constexpr int d = NV * 128;
   using RG = UpdRing<NV, BF16, ADAM>;
@@ -1167,7 +1173,7 @@ __global__ void __launch_bounds__(kTmaThreads, ADAM ? 2 : 3) label_update_tma(Up
 }
 
 // ================================================================ single-pass step
-// The default schedule for SGD (and Adam shards >= 32 GB of W+m+v) when
+// The default schedule for SGD (Adam: opt-in, ASTRA_STEP_SINGLE_ADAM=1) when
 // d % 128 == 0, d <= 768: ONE label-major pass over the touched rows. Each CTA
 // owns a contiguous chunk of the sorted unique-label list; a producer warp
 // builds each label's descriptor (bucket, first occurrence + its metadata)
@@ -2689,7 +2695,7 @@ int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
   ASTRA_LAUNCHED("label_check");
   static const bool legacy = getenv("ASTRA_STEP_LEGACY_UPD") != nullptr;
   if (!legacy && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
-    const int grid = (ADAM ? 2 : 3) * num_sms();
+    const int grid = (ADAM && nv > 6 ? 2 : 3) * num_sms();  // = upd_tma_ctas<nv, ADAM>()
     size_t smem = 0;
     switch (nv) {
       case 1: smem = UpdRing<1, BF16, ADAM>::smem(); break;
@@ -2873,18 +2879,15 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     return e ? atoi(e) != 0 : true;
   }();
   // Adam: the pass is instruction-bound (IEEE div + sqrt on 24 elements per
-  // lane). Measured, bf16 W: with a 10 GB W+m+v shard (1.3M labels) the
-  // two-kernel schedule wins (1.96 vs 2.8 ms per 1024-row minibatch); with the
-  // C5 shard's 115 GB (15M labels, 4096 x 2416 slates) the single pass wins
-  // (7.5 vs 8.1-8.5 ms per step): there the second random sweep of the
-  // gather costs more than the pass's extra instructions. Crossover taken at
-  // 32 GB of W+m+v per shard; ASTRA_STEP_SINGLE_ADAM=0/1 forces it. nv = 8 spills.
-  static const int single_adam_env = [] {
+  // lane) and the two-kernel schedule (update kernel at 3 CTAs/SM) measures
+  // faster at every shard size: bf16 W + Adam, 1.3M labels: 0.28 + 1.31 vs
+  // 2.75 ms per 1024-row minibatch; the C5 shard (15M labels, 4096 x 2416
+  // slates): 5.65 vs 6.78 ms per step. ASTRA_STEP_SINGLE_ADAM=1 forces the
+  // single pass (parity-tested bit-identical). nv = 8 spills.
+  static const bool single_adam = [] {
     const char* e = getenv("ASTRA_STEP_SINGLE_ADAM");
-    return e ? atoi(e) : -1;
+    return e != nullptr && atoi(e) != 0;
   }();
-  const double shard_state_bytes = static_cast<double>(Lloc) * d * ((bf16 ? 2 : 4) + 8);
-  const bool single_adam = single_adam_env >= 0 ? single_adam_env != 0 : shard_state_bytes >= 32e9;
   const bool single = !fused && single_env && !g_step_deterministic.load() && chunkable && nv <= 6 &&
                       (!adam || single_adam) &&
                       reinterpret_cast<uintptr_t>(grad_emb) % 16 == 0;  // (vector reductions into it)
