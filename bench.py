@@ -15,9 +15,10 @@ q/s and step-only samples/s are reported beside it. Multi-GPU: W label-sharded,
 per-GPU batch fixed (weak scaling), NCCL all-gather / reduce-scatter as in
 paper_2409_20156_b200/shard.py.
 
---impl reference times the reference's own CPU algorithm (oracle/xcmix_port.py,
-a bit-pinned restatement of xcmix — /root/reference is absent on the GPU box)
-on the host cores with the same metric.
+--impl reference times the reference's own CPU path — the unmodified xcmix
+package installed in baseline/_ref (anns.retrieve_hard_negatives +
+trainer._batch_forward_backward) — on the host cores with the same metric, one
+real step = refresh + training of one B=1024 minibatch (nothing extrapolated).
 
 Other lines (not the driver's): --config c5shard (one 15M-label shard of the
 120M config, bf16 W + Adam) and --config fullloss (the all-negatives arm at
@@ -505,73 +506,150 @@ def run_c5shard(args):
 
 
 # ------------------------------------------------------------------ CPU arm
-def cpu_workload(rng, q_sample):
-    """Host data for the CPU path: W (L x d fp32), one batch of B rows."""
-    L, d, B = CFG["L"], CFG["d"], CFG["B"]
-    W = rng.random((L, d), dtype=np.float32)
-    W *= np.float32(2.0 / np.sqrt(d))
-    W -= np.float32(1.0 / np.sqrt(d))
-    emb = rng.standard_normal((B, d), dtype=np.float32)
-    positives = [np.unique(rng.integers(0, L, size=CFG["labels_per_point"])).astype(np.int32) for _ in range(B)]
-    return W, emb, positives
+class ReferenceCPU:
+    """The reference's own CPU path on this workload, timed on the host cores.
 
+    Runs the UNMODIFIED reference package installed in baseline/_ref
+    (`pip install --no-deps --target baseline/_ref /root/reference/pkg`, see
+    DESIGN.md §9) through its public functions: per step, the shortlist
+    refresh of one minibatch's rows, `xcmix.anns.retrieve_hard_negatives`
+    (anns.py:233-256) against `build_exact` of the classifier bank, then
+    `xcmix.trainer._batch_forward_backward` (trainer.py:336-395: slates,
+    sampled loss fwd/bwd, the caller's small encoder + Adam, the SGD row
+    update of W) on those rows with the fresh hard negatives, strategy
+    Mixture (k_p=8, k_h=64, k_r=512). Each row is refreshed and trained once
+    per step, as in the GPU arm's step; nothing is extrapolated. Without
+    baseline/_ref it falls back to the bit-pinned NumPy port of the same
+    functions (oracle/xcmix_port.py, kind "port")."""
 
-def time_reference_cpu(W, emb, positives, rng, q_sample, seed):
-    """One bounded sample of the reference CPU path: refresh of q_sample
-    queries + one full-batch classifier step. Returns (t_refresh, t_step)."""
-    from oracle import xcmix_port as port
+    N_FEATURES = 768
+    NNZ = 16
 
-    L = W.shape[0]
-    B = emb.shape[0]
-    t0 = time.perf_counter()
-    hard = port.retrieve_hard_negatives(W, emb[:q_sample], positives[:q_sample], CFG["k_h"], chunk=q_sample)
-    t_ref = time.perf_counter() - t0
-    hard_all = np.concatenate([hard] * (B // q_sample + 1))[:B].astype(np.int64)
-    pos_padded, n_pos = port.pad_positives(positives)
-    t0 = time.perf_counter()
-    srng = np.random.default_rng(seed)
-    ids, y, origin, weights = port.assemble_batch_slates(pos_padded, n_pos, np.arange(B), L, CFG["k_p"], CFG["k_r"], srng, hard_all)
-    port.slate_step(W, emb, None, ids, y, origin, weights, CFG["lr"], CFG["wd"])
-    t_step = time.perf_counter() - t0
-    return t_ref, t_step
+    def __init__(self, n_rows: int, seed: int = 7):
+        c = CFG
+        self.B, self.L, self.d = c["B"], c["L"], c["d"]
+        ref = os.path.join(ROOT, "baseline", "_ref")
+        self.kind = "port"
+        if os.path.isdir(os.path.join(ref, "xcmix")):
+            if ref not in sys.path:
+                sys.path.insert(0, ref)
+            try:
+                import xcmix.anns  # noqa: F401
+                import xcmix.trainer  # noqa: F401
+
+                self.kind = "reference"
+            except ImportError:
+                self.kind = "port"
+        rng = np.random.default_rng(seed)
+        n_rows = max(n_rows, self.B)
+        self.n_rows = n_rows
+        self.positives = [np.unique(rng.integers(0, self.L, size=c["labels_per_point"])).astype(np.int32)
+                          for _ in range(n_rows)]
+        if self.kind == "reference":
+            import scipy.sparse as sp
+            from xcmix import anns
+            from xcmix.dataset import SparseDataset
+            from xcmix.trainer import TrainConfig, TrainerState
+
+            cols = rng.integers(0, self.N_FEATURES, size=(n_rows, self.NNZ))
+            vals = rng.standard_normal((n_rows, self.NNZ)).astype(np.float32)
+            feats = sp.csr_matrix((vals.ravel(), cols.ravel(), np.arange(0, n_rows * self.NNZ + 1, self.NNZ)),
+                                  shape=(n_rows, self.N_FEATURES), dtype=np.float32)
+            feats.sum_duplicates()
+            ds = SparseDataset(n_points=n_rows, n_features=self.N_FEATURES, n_labels=self.L, features=feats,
+                               positives=self.positives)
+            self.cfg = TrainConfig(epochs=1, batch_size=self.B, lr_encoder=0.01, lr_classifier=c["lr"],
+                                   weight_decay_classifier=c["wd"], k_r=c["k_r"], k_h=c["k_h"], k_p=c["k_p"], tau_s=2,
+                                   tau_r=1, strategy="Mixture", embed_dim=self.d, seed=0, dropout=0.0)
+            self.state = TrainerState(ds, self.cfg)  # reference init: encoder, bank (uniform-scaled W), ...
+            self.index = anns.build_exact(self.state.bank.weights, snapshot_epoch=0)
+            self.cache_ids = np.zeros((n_rows, c["k_h"]), dtype=np.int32)
+            self.state.caches.negative_cache = anns.NegativeCache(self.cache_ids, 0)
+        else:
+            W = rng.random((self.L, self.d), dtype=np.float32)
+            W *= np.float32(2.0 / np.sqrt(self.d))
+            W -= np.float32(1.0 / np.sqrt(self.d))
+            self.W = W
+            self.emb = rng.standard_normal((n_rows, self.d), dtype=np.float32)
+
+    def step(self, t: int) -> tuple[float, float]:
+        """One step over minibatch t (mod the rows): (refresh seconds, train seconds)."""
+        nb = self.n_rows // self.B
+        rows = (t % nb) * self.B + np.arange(self.B, dtype=np.int64)
+        pos = [self.positives[r] for r in rows]
+        if self.kind == "reference":
+            from xcmix import anns
+            from xcmix import trainer as xt
+
+            t0 = time.perf_counter()
+            emb = xt.embed_batch(self.state.encoder, self.state.dataset.features[rows])
+            cache = anns.retrieve_hard_negatives(self.index, emb, pos, CFG["k_h"])
+            self.cache_ids[rows] = cache.ids
+            t1 = time.perf_counter()
+            xt._batch_forward_backward(self.state, rows, 2, np.random.default_rng(1000 + t), 0.01, CFG["lr"])
+            return t1 - t0, time.perf_counter() - t1
+        from oracle import xcmix_port as port
+
+        t0 = time.perf_counter()
+        hard = port.retrieve_hard_negatives(self.W, self.emb[rows], pos, CFG["k_h"], chunk=self.B)
+        t1 = time.perf_counter()
+        pos_padded, n_pos = port.pad_positives(pos)
+        ids, y, origin, weights = port.assemble_batch_slates(pos_padded, n_pos, np.arange(self.B), self.L, CFG["k_p"],
+                                                             CFG["k_r"], np.random.default_rng(1000 + t),
+                                                             hard.astype(np.int64))
+        port.slate_step(self.W, self.emb[rows], None, ids, y, origin, weights, CFG["lr"], CFG["wd"])
+        return t1 - t0, time.perf_counter() - t1
+
+    def describe(self) -> str:
+        what = ("xcmix (baseline/_ref, unmodified): anns.retrieve_hard_negatives + trainer._batch_forward_backward"
+                if self.kind == "reference" else "oracle/xcmix_port.py (NumPy restatement of the same functions)")
+        return (f"per step: refresh of B={self.B} rows vs L={self.L} + one training minibatch of those rows "
+                f"(S={CFG['k_p'] + CFG['k_h'] + CFG['k_r']}); {what}; numpy/scipy/OpenBLAS threads="
+                f"{os.environ.get('OPENBLAS_NUM_THREADS', os.environ.get('OMP_NUM_THREADS', 'all'))}")
 
 
 def cpu_baseline(args):
-    rng = np.random.default_rng(7)
-    q = args.cpu_queries
-    W, emb, positives = cpu_workload(rng, q)
-    t_ref, t_step = time_reference_cpu(W, emb, positives, rng, q, 1)
+    """Rank 0, N=1: one warm-up + one timed step of the reference CPU path
+    (~15-30 s of host work) — a reported baseline beside the GPU line."""
+    ref = ReferenceCPU(2 * CFG["B"])
+    ref.step(0)
+    t_ref, t_step = ref.step(1)
     B = CFG["B"]
-    per_sample = t_step / B + t_ref / q / CFG["tau_r"]
-    return {"value": round(1.0 / per_sample, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"1 step of B={B} (S=584) + refresh of {q} queries vs L={CFG['L']}, numpy/scipy/OpenBLAS, "
-                      f"threads={os.environ.get('OMP_NUM_THREADS', 'all')}",
-            "step_s": round(t_step, 3), "refresh_qps": round(q / t_ref, 2)}
+    return {"value": round(B / (t_ref + t_step), 2), "unit": UNIT, "cores": os.cpu_count(), "kind": ref.kind,
+            "sample": "1 step: " + ref.describe(), "refresh_s": round(t_ref, 3), "train_s": round(t_step, 3),
+            "refresh_qps": round(B / t_ref, 2)}
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU path (ReferenceCPU) for --steps
+    steps of B=1024 rows each (refresh + train), after one warm-up step (CPU
+    code has no compilation or allocator warm-up beyond the first call; the
+    --warmup steps of the GPU arm would add ~12 s each here)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    rng = np.random.default_rng(7)
-    q = args.cpu_queries
-    W, emb, positives = cpu_workload(rng, q)
     B = CFG["B"]
-    for t in range(args.warmup):
-        time_reference_cpu(W, emb, positives, rng, q, 100 + t)
-    tot = 0.0
-    for t in range(args.steps):
-        t_ref, t_step = time_reference_cpu(W, emb, positives, rng, q, 200 + t)
-        tot += t_step + t_ref * (B / q) / CFG["tau_r"]
-    value = B * args.steps / tot
+    ref = ReferenceCPU(B * (args.steps + 1))
+    warm = 1
+    for t in range(warm):
+        ref.step(t)
+    tr = ts = 0.0
+    t_wall = time.perf_counter()
+    for t in range(warm, warm + args.steps):
+        a, b = ref.step(t)
+        tr += a
+        ts += b
+    wall = time.perf_counter() - t_wall
+    value = B * args.steps / wall
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 2),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (numpy)",
-            "data": "synthetic",
-            "config": bench_config(world),
-            "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                             "sample": f"per step: 1 classifier step of B={B} + refresh of {q} queries scaled to B"},
+            "steps": args.steps, "warmup": warm, "warmup_requested": args.warmup,
+            "ms_per_step": round(wall / args.steps * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32 (numpy; loss fp64)", "data": "synthetic",
+            "config": dict(bench_config(world), rows_per_step_per_gpu=B, minibatches_per_step=1, refresh_chunk=B),
+            "phases_ms_per_step": {"refresh": round(tr / args.steps * 1e3, 2), "train": round(ts / args.steps * 1e3, 2)},
+            "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": ref.kind,
+                             "sample": ref.describe()},
             "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -649,7 +727,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-queries", type=int, default=128)
     ap.add_argument("--config", default="c4", choices=["c4", "c5shard", "fullloss"],
                     help="c4 (default, the headline line), c5shard (120M-label config, one of 8 shards) or "
                          "fullloss (the all-negatives arm at the reference's 50K-label cap)")

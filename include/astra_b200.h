@@ -132,6 +132,15 @@ int astra_refresh_topk(const float* queries_f32, const uint16_t* queries_bf16, i
                        int k, int mode, uint64_t* out_keys, int32_t* out_ids, float* out_scores,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* Diagnostic of the last astra_refresh_topk call made with `workspace` and
+ * the same (nq, n_labels, d, k, mode): how many queries the two-pass plan
+ * could not prove exact from its threshold candidates (they were recomputed
+ * by the exact running top-k, so the result is exact either way). *out_count
+ * = -1 when that shape does not use the two-pass plan. Synchronises `stream`.
+ * No reference counterpart (observability of anns.py:233-256's replacement). */
+int astra_refresh_flagged(const void* workspace, size_t workspace_bytes, int64_t nq, int64_t n_labels, int d,
+                          int k, int mode, int64_t* out_count, void* stream);
+
 /* Merge n_parts partial top-k lists per query (layout [n_parts][nq][k_in],
  * e.g. an all-gather over label shards) into the global top-k_out. Each list
  * must be sorted descending and zero-padded, as astra_refresh_topk writes its

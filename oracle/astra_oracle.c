@@ -313,3 +313,186 @@ int oracle_sample_slates(uint64_t seed, uint32_t epoch, uint32_t step, const int
   free(ki);
   return 0;
 }
+
+/* ------------------------------------------------------------ refresh, blocked
+ * oracle_refresh_fp32_blocked: the same result as oracle_refresh_fp32 (every
+ * score is the same sequential fmaf chain over t = 0..d-1, so the keys are
+ * bit-identical), organised for the production-size parity tests (L = 1.3M,
+ * 15M): 16 queries x 4 labels of independent fmaf chains per step (the
+ * compiler turns them into vector FMAs, each lane still a correctly rounded
+ * fmaf; AVX2 FMA intrinsics), pthreads over (query block, label chunk) tasks, a size-k min-heap of
+ * keys per query and task, then a merge. W may be fp32 or bf16 (uint16 bit
+ * patterns, widened exactly). nthreads <= 0: one thread per online CPU. */
+#include <immintrin.h>
+#include <pthread.h>
+#include <unistd.h>
+
+#define QB 16
+#define LB 4
+
+static void heap_sift_down(uint64_t* h, int n, int i) {
+  for (;;) {
+    int l = 2 * i + 1, r = l + 1, m = i;
+    if (l < n && h[l] < h[m]) m = l;
+    if (r < n && h[r] < h[m]) m = r;
+    if (m == i) return;
+    uint64_t t = h[i];
+    h[i] = h[m];
+    h[m] = t;
+    i = m;
+  }
+}
+
+/* min-heap of at most k keys (smallest at h[0]); *n = current size */
+static inline void heap_push(uint64_t* h, int* n, int k, uint64_t key) {
+  if (*n < k) {
+    int i = (*n)++;
+    h[i] = key;
+    while (i > 0) {
+      int p = (i - 1) / 2;
+      if (h[p] <= h[i]) break;
+      uint64_t t = h[p];
+      h[p] = h[i];
+      h[i] = t;
+      i = p;
+    }
+  } else if (key > h[0]) {
+    h[0] = key;
+    heap_sift_down(h, k, 0);
+  }
+}
+
+static inline float bf16_bits_to_f32(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+typedef struct {
+  const float* Q;
+  int64_t nq;
+  int d;
+  const void* W;
+  int w_bf16;
+  int64_t L, label_offset;
+  const int64_t* pos_indptr;
+  const int32_t* pos_ids;
+  int k;
+  int64_t nlc, lchunk, ntasks;
+  uint64_t* heaps;
+  int* hn;
+  int64_t next; /* task counter (atomic) */
+} blocked_ctx;
+
+static void blocked_task(blocked_ctx* c, int64_t task, float* qt, float* wb) {
+  const int d = c->d, k = c->k;
+  int64_t qb = task / c->nlc, lc = task % c->nlc;
+  int64_t q0 = qb * QB;
+  int nqq = (int)(c->nq - q0 < QB ? c->nq - q0 : QB);
+  for (int t = 0; t < d; ++t)
+    for (int j = 0; j < QB; ++j) qt[(size_t)t * QB + j] = j < nqq ? c->Q[(size_t)(q0 + j) * d + t] : 0.0f;
+  uint64_t* h = c->heaps + (size_t)task * QB * k;
+  int* n = c->hn + task * QB;
+  int64_t l0 = lc * c->lchunk, l1 = l0 + c->lchunk < c->L ? l0 + c->lchunk : c->L;
+  for (int64_t l = l0; l < l1; l += LB) {
+    int nl = (int)(l1 - l < LB ? l1 - l : LB);
+    for (int i = 0; i < LB; ++i) {
+      int64_t row = l + (i < nl ? i : 0);
+      if (c->w_bf16) {
+        const uint16_t* src = (const uint16_t*)c->W + (size_t)row * d;
+        for (int t = 0; t < d; ++t) wb[(size_t)t * LB + i] = bf16_bits_to_f32(src[t]);
+      } else {
+        const float* src = (const float*)c->W + (size_t)row * d;
+        for (int t = 0; t < d; ++t) wb[(size_t)t * LB + i] = src[t];
+      }
+    }
+    /* s[i][j] = fmaf(q_j[t], w_i[t], s[i][j]) for t = 0..d-1: 8 independent
+       vector FMA chains (each lane one correctly rounded fmaf) */
+    __m256 acc[LB][2];
+    for (int i = 0; i < LB; ++i) acc[i][0] = acc[i][1] = _mm256_setzero_ps();
+    for (int t = 0; t < d; ++t) {
+      __m256 q0v = _mm256_loadu_ps(qt + (size_t)t * QB), q1v = _mm256_loadu_ps(qt + (size_t)t * QB + 8);
+      for (int i = 0; i < LB; ++i) {
+        __m256 w = _mm256_broadcast_ss(wb + (size_t)t * LB + i);
+        acc[i][0] = _mm256_fmadd_ps(q0v, w, acc[i][0]);
+        acc[i][1] = _mm256_fmadd_ps(q1v, w, acc[i][1]);
+      }
+    }
+    float s[LB][QB];
+    for (int i = 0; i < LB; ++i) {
+      _mm256_storeu_ps(s[i], acc[i][0]);
+      _mm256_storeu_ps(s[i] + 8, acc[i][1]);
+    }
+    for (int i = 0; i < nl; ++i) {
+      int64_t gid = l + i + c->label_offset;
+      for (int j = 0; j < nqq; ++j) {
+        int64_t qi = q0 + j;
+        const int32_t* pos = c->pos_ids + c->pos_indptr[qi];
+        if (is_member(pos, c->pos_indptr[qi + 1] - c->pos_indptr[qi], gid)) continue;
+        heap_push(h + (size_t)j * k, &n[j], k, make_key(s[i][j], gid));
+      }
+    }
+  }
+}
+
+static void* blocked_worker(void* arg) {
+  blocked_ctx* c = (blocked_ctx*)arg;
+  float* qt = (float*)malloc(sizeof(float) * (size_t)c->d * QB);
+  float* wb = (float*)malloc(sizeof(float) * (size_t)c->d * LB);
+  for (;;) {
+    int64_t task = __atomic_fetch_add(&c->next, 1, __ATOMIC_RELAXED);
+    if (task >= c->ntasks) break;
+    blocked_task(c, task, qt, wb);
+  }
+  free(qt);
+  free(wb);
+  return NULL;
+}
+
+void oracle_refresh_fp32_blocked(const float* Q, int64_t nq, int d, const void* W, int w_bf16, int64_t L,
+                                 int64_t label_offset, const int64_t* pos_indptr, const int32_t* pos_ids, int k,
+                                 int nthreads, uint64_t* out_keys, int32_t* out_ids, float* out_scores) {
+  if (k <= 0 || nq <= 0) return;
+  int nth = nthreads > 0 ? nthreads : (int)sysconf(_SC_NPROCESSORS_ONLN);
+  if (nth < 1) nth = 1;
+  blocked_ctx c;
+  memset(&c, 0, sizeof(c));
+  c.Q = Q; c.nq = nq; c.d = d; c.W = W; c.w_bf16 = w_bf16; c.L = L; c.label_offset = label_offset;
+  c.pos_indptr = pos_indptr; c.pos_ids = pos_ids; c.k = k;
+  int64_t nqb = (nq + QB - 1) / QB;
+  /* enough tasks for the threads: split the labels into chunks */
+  c.nlc = (8 * (int64_t)nth + nqb - 1) / nqb;
+  if (c.nlc > L / 1024 + 1) c.nlc = L / 1024 + 1;
+  if (c.nlc < 1) c.nlc = 1;
+  c.lchunk = (L + c.nlc - 1) / c.nlc;
+  c.ntasks = nqb * c.nlc;
+  c.heaps = (uint64_t*)calloc((size_t)(c.ntasks * QB * k), sizeof(uint64_t));
+  c.hn = (int*)calloc((size_t)(c.ntasks * QB), sizeof(int));
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nth);
+  for (int i = 0; i < nth; ++i) pthread_create(&th[i], NULL, blocked_worker, &c);
+  for (int i = 0; i < nth; ++i) pthread_join(th[i], NULL);
+  free(th);
+  /* merge the label chunks' heaps of every query, descending */
+  uint64_t* all = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(c.nlc * k));
+  for (int64_t qi = 0; qi < nq; ++qi) {
+    int64_t qb = qi / QB;
+    int j = (int)(qi % QB);
+    int64_t m = 0;
+    for (int64_t lc = 0; lc < c.nlc; ++lc) {
+      int64_t task = qb * c.nlc + lc;
+      const uint64_t* h = c.heaps + ((size_t)task * QB + j) * k;
+      for (int x = 0; x < c.hn[task * QB + j]; ++x) all[m++] = h[x];
+    }
+    qsort(all, (size_t)m, sizeof(uint64_t), cmp_key_desc);
+    for (int x = 0; x < k; ++x) {
+      uint64_t key = x < m ? all[x] : 0;
+      if (out_keys) out_keys[qi * k + x] = key;
+      if (out_ids) out_ids[qi * k + x] = key ? key_id(key) : -1;
+      if (out_scores) out_scores[qi * k + x] = key ? key_score(key) : -INFINITY;
+    }
+  }
+  free(all);
+  free(c.heaps);
+  free(c.hn);
+}

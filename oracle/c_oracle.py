@@ -53,6 +53,32 @@ def refresh_fp32(Q, W, pos_indptr, pos_ids, k, label_offset=0):
     return keys, ids, scores
 
 
+def refresh_fp32_blocked(Q, W, pos_indptr, pos_ids, k, label_offset=0, nthreads=0):
+    """The same keys as refresh_fp32 (identical fmaf chains), blocked and
+    threaded for production-size checks. W: fp32, or bf16 given as a uint16 /
+    int16 array of bit patterns (widened exactly, as the re-rank does)."""
+    lib = load()
+    Q = np.ascontiguousarray(Q, np.float32)
+    W = np.ascontiguousarray(W)
+    if W.dtype in (np.uint16, np.int16):
+        w_bf16 = 1
+    else:
+        W = np.ascontiguousarray(W, np.float32)
+        w_bf16 = 0
+    pos_indptr = np.ascontiguousarray(pos_indptr, np.int64)
+    pos_ids = np.ascontiguousarray(pos_ids, np.int32)
+    nq, d = Q.shape
+    keys = np.zeros((nq, k), np.uint64)
+    ids = np.zeros((nq, k), np.int32)
+    scores = np.zeros((nq, k), np.float32)
+    lib.oracle_refresh_fp32_blocked(
+        _p(Q), ctypes.c_int64(nq), ctypes.c_int(d), _p(W), ctypes.c_int(w_bf16), ctypes.c_int64(W.shape[0]),
+        ctypes.c_int64(label_offset), _p(pos_indptr), _p(pos_ids), ctypes.c_int(k), ctypes.c_int(nthreads),
+        _p(keys), _p(ids), _p(scores),
+    )
+    return keys, ids, scores
+
+
 def scores_fp32(Q, W):
     lib = load()
     Q = np.ascontiguousarray(Q, np.float32)

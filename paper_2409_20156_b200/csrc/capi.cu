@@ -62,6 +62,7 @@ size_t refresh_workspace_size(int64_t, int64_t, int, int, int);
 int refresh_topk(const float*, const uint16_t*, int64_t, int, const float*, const uint16_t*, int64_t, int64_t,
                  const int64_t*, const int32_t*, int, int, uint64_t*, int32_t*, float*, void*, size_t, cudaStream_t);
 int topk_merge(const uint64_t*, int64_t, int, int, int, uint64_t*, int32_t*, float*, uint64_t*, cudaStream_t);
+int refresh_flagged(const void*, size_t, int64_t, int64_t, int, int, int, int64_t*, cudaStream_t);
 int sample_slates(uint64_t, uint32_t, uint32_t, const int64_t*, int, const int64_t*, const int32_t*, const int32_t*,
                   int, int, const int32_t*, const float*, int, int, int, int64_t, int, int, int32_t*, int8_t*,
                   int8_t*, float*, cudaStream_t);
@@ -138,6 +139,11 @@ int astra_refresh_topk(const float* queries_f32, const uint16_t* queries_bf16, i
                        int32_t* out_ids, float* out_scores, void* workspace, size_t workspace_bytes, void* stream) {
   return refresh_topk(queries_f32, queries_bf16, nq, d, labels_f32, labels_bf16, n_labels, label_offset, pos_indptr,
                       pos_ids, k, mode, out_keys, out_ids, out_scores, workspace, workspace_bytes, S(stream));
+}
+
+int astra_refresh_flagged(const void* workspace, size_t workspace_bytes, int64_t nq, int64_t n_labels, int d, int k,
+                          int mode, int64_t* out_count, void* stream) {
+  return refresh_flagged(workspace, workspace_bytes, nq, n_labels, d, k, mode, out_count, S(stream));
 }
 
 size_t astra_merge_workspace_size(int64_t nq, int k_out) {

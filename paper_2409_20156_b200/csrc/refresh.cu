@@ -15,6 +15,7 @@
 //   BF16_RERANK tcgen05 top-k' (k' = 2k) then the k' candidates are re-scored
 //               with the same sequential fmaf chain and re-ranked: equal to
 //               FP32_EXACT whenever the exact top-k lies inside the top-k'.
+#include <vector>
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -1086,6 +1087,30 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
                                                                            out_ids, out_scores);
     ASTRA_LAUNCHED("rerank");
   }
+  return ASTRA_OK;
+}
+
+// Queries of the last two-pass refresh that used this workspace whose
+// candidate set could not prove exactness (the running-top-k verify re-did
+// them): copies the flags back and counts them (synchronises the stream).
+// -1 when the plan for this shape is not the two-pass one.
+int refresh_flagged(const void* ws, size_t ws_bytes, int64_t nq, int64_t L, int d, int k, int mode,
+                    int64_t* out_count, cudaStream_t st) {
+  if (!out_count) return set_error(ASTRA_ERR_CONFIG, "refresh_flagged: null output");
+  *out_count = -1;
+  if (mode == ASTRA_REFRESH_FP32_EXACT || nq <= 0) return ASTRA_OK;
+  RefreshWs w;
+  int n_parts, kk;
+  TwoPass tp;
+  size_t need = carve_refresh(const_cast<void*>(ws), ws_bytes, nq, L, d, k, mode, &w, &n_parts, &kk, &tp);
+  if (!ws || ws_bytes < need) return set_error(ASTRA_ERR_CONFIG, "refresh_flagged: workspace too small");
+  if (!tp.on) return ASTRA_OK;
+  std::vector<int32_t> h(static_cast<size_t>(nq));
+  ASTRA_TRY(check_cuda(cudaMemcpyAsync(h.data(), w.flags, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, st), "flags d2h"));
+  ASTRA_TRY(check_cuda(cudaStreamSynchronize(st), "flags sync"));
+  int64_t c = 0;
+  for (int32_t f : h) c += f != 0;
+  *out_count = c;
   return ASTRA_OK;
 }
 

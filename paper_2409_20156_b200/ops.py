@@ -103,6 +103,20 @@ def refresh_topk(queries, pos_indptr, pos_ids, k, mode="bf16_rerank", labels_f32
     return keys, ids, scores
 
 
+def refresh_flagged(nq, n_labels, d, k, mode, device=None) -> int:
+    """Queries of the last refresh_topk call of this shape (on this device)
+    that the two-pass plan sent to the exact verify pass; -1 when the shape
+    runs the single-pass running top-k. Synchronises the current stream."""
+    mode = refresh_mode(mode)
+    lib = _lib.load()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    ws_n = lib.astra_refresh_workspace_size(nq, n_labels, d, k, mode)
+    ws = WORKSPACES.get("refresh", ws_n, dev)
+    out = C.c_int64(0)
+    _lib.check(lib.astra_refresh_flagged(_p(ws), ws.numel(), nq, n_labels, d, k, mode, C.byref(out), _stream()))
+    return int(out.value)
+
+
 def topk_merge(part_keys: torch.Tensor, k_out: int):
     """Merge [n_parts, nq, k_in] partial key lists into the global top-k_out."""
     _cuda(part_keys, torch.int64, "part_keys")

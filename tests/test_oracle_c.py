@@ -46,6 +46,38 @@ def test_refresh_random_fixture_up_to_ties():
     assert diff.mean() < 0.01
 
 
+@pytest.mark.parametrize("nq,L,d,k,offset", [(37, 5003, 64, 20, 0), (16, 2048, 768, 64, 1000), (5, 3, 8, 6, 0),
+                                             (50, 20000, 24, 200, 7)])
+def test_refresh_blocked_equals_scalar(nq, L, d, k, offset):
+    # the blocked/threaded/vectorised oracle used by the production-size GPU
+    # parity tests computes the same fmaf chains: keys bit-identical
+    rng = np.random.default_rng(nq * 7 + L)
+    W = rng.standard_normal((L, d)).astype(np.float32)
+    Q = rng.standard_normal((nq, d)).astype(np.float32)
+    Q[1 % nq] = 0.0  # an all-tie query
+    positives = [np.sort(rng.choice(L, size=int(rng.integers(0, min(L, 6))), replace=False)) + offset for _ in range(nq)]
+    ip, pid = _csr(positives)
+    ref = co.refresh_fp32(Q, W, ip, pid, k, label_offset=offset)
+    for nth in (1, 3):
+        got = co.refresh_fp32_blocked(Q, W, ip, pid, k, label_offset=offset, nthreads=nth)
+        for a, b in zip(got, ref):
+            np.testing.assert_array_equal(a, b)
+
+
+def test_refresh_blocked_bf16_rows():
+    # bf16 W as bit patterns = the fp32 oracle on the widened values
+    rng = np.random.default_rng(5)
+    W = rng.standard_normal((3000, 128)).astype(np.float32)
+    bits = (W.view(np.uint32) >> 16).astype(np.uint16)
+    Wb = (bits.astype(np.uint32) << 16).view(np.float32)
+    Q = rng.standard_normal((20, 128)).astype(np.float32)
+    ip, pid = _csr([np.zeros(0, np.int32)] * 20)
+    a = co.refresh_fp32_blocked(Q, bits, ip, pid, 50)
+    b = co.refresh_fp32(Q, Wb, ip, pid, 50)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+
+
 def test_refresh_reference_known_answers():
     W = np.array([[0.0, 1.0], [1.0, 0.0], [1.0, 0.0], [0.5, 0.0]], np.float32)
     _, ids, _ = co.refresh_fp32(np.array([[1.0, 0.0]], np.float32), W, [0, 0], [], 3)
