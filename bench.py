@@ -169,6 +169,11 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if rank == 0:
+            sys.stderr.write(f"[bench] NCCL {'.'.join(map(str, torch.cuda.nccl.version()))} up: world={world} "
+                             f"(--gpus {args.gpus}), device {torch.cuda.get_device_name(local)}\n")
+    if world != args.gpus:
+        sys.exit(f"bench.py: world size {world} != --gpus {args.gpus}")
     L, d, B, M = CFG["L"], CFG["d"], CFG["B"], CFG["minibatches"]
     k_p, k_h, k_r = CFG["k_p"], CFG["k_h"], CFG["k_r"]
     S = k_p + k_h + k_r
@@ -306,6 +311,20 @@ def run_ours(args):
                              "algorithmic_bytes": int(fwd_bytes), "traffic": traffic.get("slot_forward")},
             "label_update": {"launch_ms": round(upd_ms / max(upd_n, 1), 4), "achieved_gbs": rate(upd_bytes, upd_ms, upd_n),
                              "algorithmic_bytes": int(upd_bytes), "traffic": traffic.get("label_update")}}
+    # refresh parity at the benched shape (outside the timed region): the
+    # production ids (two-pass bf16 + fp32 re-rank) of the last step's chunk
+    # against the fp32-exact mode (sequential fmaf = the C oracle's arithmetic,
+    # tests/test_gpu_refresh_scale.py) on every query of the chunk
+    st = dev[n_steps - 1]["chunk"]
+    prod_ids, _ = eng.refresh(st["emb"], st["indptr"], st["pos"], k_h)
+    flagged = ops.refresh_flagged(R * world, L_loc, d, k_h, "bf16_rerank")
+    exact_ids, _ = eng.refresh(st["emb"], st["indptr"], st["pos"], k_h, mode="fp32")
+    same = prod_ids == exact_ids
+    hits = (prod_ids.unsqueeze(2) == exact_ids.unsqueeze(1)).any(2).sum(1).double() / k_h
+    refresh_parity = {"vs": "fp32-exact mode (= C oracle arithmetic)", "queries": int(prod_ids.shape[0]),
+                      "recall_at_k": round(float(hits.mean()), 6), "rows_bit_exact": round(float(same.all(1).double().mean()), 6),
+                      "flagged_for_verify": int(flagged)}
+    del exact_ids
     # end-to-end: the public API with HOST buffers (pinned), copies inside the timed region
     pinned = []
     for t in range(n_steps):
@@ -360,16 +379,17 @@ def run_ours(args):
         # the exact fallback of the two-pass refresh (running top-k for query
         # tiles holding a flagged query): ~0 when every query was proven exact
         "refresh_verify_ms": round(kt["refresh_verify"][0] / max(kt["refresh_verify"][1], 1), 4),
+        "refresh_parity": refresh_parity,
         "step_only_samples_per_s": round(B * world / (t_step + t_samp), 1),
         "composite_tau_r5_samples_per_s": round(R * world / (M * (t_step + t_samp) + t_ref / 5), 1),
         "roofline": {"bound": "tensor", "kernel": "refresh_tc_kernel threshold pass (tcgen05 bf16 GEMM + fused candidate epilogue)",
-                     "achieved": round(achieved_tf, 2), "peak": tf_sus, "unit": "TFLOP/s",
-                     "frac": round(achieved_tf / tf_sus, 4), "traffic": traffic.get("refresh_gemm"),
-                     "frac_of_burst_peak": round(achieved_tf / tf_burst, 4),
+                     "achieved": round(achieved_tf, 2), "peak": tf_burst, "unit": "TFLOP/s",
+                     "frac": round(achieved_tf / tf_burst, 4), "traffic": traffic.get("refresh_gemm"),
+                     "frac_of_sustained_peak": round(achieved_tf / tf_sus, 4),
                      "algorithmic": f"2*L_shard*d*Q = {flops:.3e} flop per launch (Q={q_per_refresh})",
                      "launch_ms": round(t_gemm * 1e3, 4), "launches": gemm_n,
                      "share_of_refresh": round(t_gemm / t_ref, 4),
-                     "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)"},
+                     "peak_kind": f"{peak_kind} burst bf16 (each launch is timed on its own, ~12 ms)"},
         "roofline_step": {"bound": "hbm", "kernel": step_kernel_desc,
                           "achieved": round(step_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(step_gbs / hbm, 4),
                           "algorithmic": f"U*d*8 + 2*B*d*4 + B*S*5 = {step_bytes:.3e} B (U={U_mean:.0f})",
@@ -385,6 +405,150 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ N-GPU emulation on one GPU
+def run_emulate(args):
+    """Rank 0's share of an N-GPU C4 job, on one GPU (--emulate N).
+
+    Rank r of the label-sharded job (shard.py) owns L/N labels of W and, per
+    step, (a) refreshes ALL N ranks' query rows (N x 9216 after the query
+    all-gather) against its shard and merges the N partial lists of its own
+    rows (after the key all-to-all), then (b) per minibatch draws the slates
+    of all N x 1024 rows (Philox over the global label range, identical on
+    every rank) and runs the fused loss/update for the slots it owns (~1/N).
+    This runs exactly that compute on one GPU, with synthetic stand-ins for
+    the other ranks' rows; the collectives are NOT run and their bytes per
+    rank are reported (collective_bytes_per_rank_per_step), so the per-rank
+    compute cost of the N = 2/4/8 configurations is measured on one B200.
+    value = N x 9216 rows / per-rank step time = the whole job's throughput
+    if the collectives were free and the ranks in lockstep (an upper bound
+    for the real N-GPU run, which --gpus N measures)."""
+    import torch
+
+    from paper_2409_20156_b200 import _lib, ops
+    from paper_2409_20156_b200.engine import init_uniform_scaled
+    from paper_2409_20156_b200.shard import shard_range
+
+    N = args.emulate
+    torch.cuda.set_device(0)
+    c = CFG
+    L, d, B, M = c["L"], c["d"], c["B"], c["minibatches"]
+    k_p, k_h, k_r, lpp = c["k_p"], c["k_h"], c["k_r"], c["labels_per_point"]
+    S = k_p + k_h + k_r
+    lo, hi = shard_range(L, 0, N)
+    Lr = hi - lo
+    R = B * M
+    Rg, Bg = R * N, B * N
+    hbm, tf_burst, _, peak_kind = peaks()
+    W = init_uniform_scaled(Lr, d, 1, "cuda")
+    w_absmax = W.abs().amax().reshape(1).float()
+    snap_f32 = W.clone()
+    snap_bf16 = ops.f32_to_bf16(snap_f32)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1)
+    n_steps = args.warmup + args.steps
+    data = []
+    for t in range(n_steps):
+        q = torch.randn((Rg, d), device="cuda", generator=g)
+        pid = torch.randint(0, L, (Rg, lpp), device="cuda", generator=g).sort(1).values.to(torch.int32).reshape(-1)
+        # distinct sorted hard ids per row (the stale cache rows of the step's rows)
+        hard = (torch.randint(0, L - k_h, (Rg, k_h), device="cuda", generator=g).sort(1).values
+                + torch.arange(k_h, device="cuda")).to(torch.int32)
+        data.append((q, pid, hard))
+    ip_step = torch.arange(0, Rg * lpp + 1, lpp, dtype=torch.int64, device="cuda")
+    ip_mb = torch.arange(0, Bg * lpp + 1, lpp, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3 + 2 * M)] for _ in range(n_steps)]
+    keep_ids = []
+
+    def one(t, timed):
+        q, pid, hard = data[t]
+        e = ev[t]
+        e[0].record(stream)
+        keys, _, _ = ops.refresh_topk(q, ip_step, pid, k_h, "bf16_rerank", labels_f32=snap_f32, labels_bf16=snap_bf16,
+                                      label_offset=lo)
+        e[1].record(stream)
+        ops.topk_merge(keys.view(N, R, k_h), k_h)  # the N shards' lists of this rank's R rows
+        e[2].record(stream)
+        for i in range(M):
+            rows = torch.arange((t * M + i) * Bg, (t * M + i + 1) * Bg, dtype=torch.int64, device="cuda")
+            sl = ops.sample_slates(0, 1, t * M + i, rows, ip_mb, pid[i * Bg * lpp:(i + 1) * Bg * lpp],
+                                   hard[i * Bg:(i + 1) * Bg], k_h, L, k_p, k_r)
+            e[3 + 2 * i].record(stream)
+            emb = q[i * Bg:(i + 1) * Bg]
+            res = ops.slate_step(emb, *sl, W, c["lr"], c["wd"], label_offset=lo, w_absmax=w_absmax)
+            e[4 + 2 * i].record(stream)
+            if timed and i == 0:
+                keep_ids.append(sl[0])
+        return res
+
+    for t in range(args.warmup):
+        one(t, False)
+    torch.cuda.synchronize()
+    for name in ("refresh_gemm", "step_single"):
+        _lib.kernel_timing(name)
+    _lib.kernel_timing_enable(True)
+    clocks = ClockSampler(0)
+    clocks.start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for t in range(args.warmup, n_steps):
+        res = one(t, True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    _lib.kernel_timing_enable(False)
+    kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "step_single")}
+    ops.raise_for_step_status(res.status)
+    K = args.steps
+    ms = t0.elapsed_time(t1) / K
+    ph = {"refresh": 0.0, "merge": 0.0, "sample": 0.0, "step": 0.0}
+    for t in range(args.warmup, n_steps):
+        e = ev[t]
+        ph["refresh"] += e[0].elapsed_time(e[1]) / K
+        ph["merge"] += e[1].elapsed_time(e[2]) / K
+        for i in range(M):
+            ph["sample"] += (e[2] if i == 0 else e[2 + 2 * i]).elapsed_time(e[3 + 2 * i]) / K
+            ph["step"] += e[3 + 2 * i].elapsed_time(e[4 + 2 * i]) / K
+    owned = [ids[(ids >= lo) & (ids < hi)] for ids in keep_ids]
+    U = sum(int(torch.unique(o).numel()) for o in owned) / len(owned)
+    slots = sum(int(o.numel()) for o in owned) / len(owned)
+    gemm_ms, gemm_n = kt["refresh_gemm"]
+    flops = 2.0 * Lr * d * Rg
+    ach = flops / (gemm_ms / max(gemm_n, 1) / 1e3) / 1e12
+    sgl_ms, sgl_n = kt["step_single"]
+    upd_bytes = U * d * 8
+    # what rank 0 would send/receive per step in the real job (bytes, per rank)
+    coll = {
+        "queries_all_gather": (N - 1) * R * d * 4,
+        "positives_all_gather": (N - 1) * R * (lpp * 4 + 8),
+        "keys_all_to_all": (N - 1) * R * k_h * 8,
+        "sampler_inputs_all_gather": M * (N - 1) * B * (8 + lpp * 4 + 8 + k_h * 4),
+        "emb_all_gather": M * (N - 1) * B * d * 4,
+        "grad_emb_reduce_scatter": M * (N - 1) * B * d * 4,
+        "loss_status_all_reduce": M * 2 * (8 + 16),
+    }
+    line = {
+        "metric": METRIC + f" [emulated {N}-GPU job: rank 0's compute on 1 GPU, collectives not run]",
+        "value": round(Rg * K / (ms * K / 1e3), 1), "unit": UNIT, "n_gpus": 1, "emulates_n_gpus": N,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32 W/step, bf16 tensor-core refresh + fp32 re-rank", "data": "synthetic",
+        "config": dict(bench_config(N), labels_shard=Lr, rows_per_step_job=Rg, minibatch_job=Bg),
+        "phases_ms_per_step": {k: round(v, 4) for k, v in ph.items()},
+        "owned_slots_per_minibatch": round(slots, 1), "unique_owned_labels_per_minibatch": round(U, 1),
+        "occurrences_per_owned_label": round(slots / max(U, 1), 3),
+        "roofline": {"bound": "tensor", "kernel": "refresh_tc_kernel threshold pass", "achieved": round(ach, 2),
+                     "peak": tf_burst, "unit": "TFLOP/s", "frac": round(ach / tf_burst, 4),
+                     "launch_ms": round(gemm_ms / max(gemm_n, 1), 4), "peak_kind": f"{peak_kind} burst bf16"},
+        "roofline_step": {"bound": "hbm", "kernel": "step_single", "launch_ms": round(sgl_ms / max(sgl_n, 1), 4),
+                          "achieved": round(upd_bytes / (sgl_ms / max(sgl_n, 1) / 1e3) / 1e9, 1) if sgl_n else None,
+                          "peak": hbm, "unit": "GB/s", "algorithmic": f"U*d*8 = {upd_bytes:.3e} B (U={U:.0f})"},
+        "collective_bytes_per_rank_per_step": coll,
+        "collective_bytes_total_per_rank_per_step": int(sum(coll.values())),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ C5 shard emulation
@@ -495,7 +659,8 @@ def run_c5shard(args):
         "refresh_verify_ms": round(kt["refresh_verify"][0] / max(kt["refresh_verify"][1], 1), 4),
         "composite_tau_r5_samples_per_s": round(B / ((ph["sample"] + ph["step"] + ph["refresh"] / 5) / 1e3), 1),
         "roofline": {"bound": "tensor", "kernel": "refresh_tc_kernel threshold pass", "achieved": round(achieved, 2),
-                     "peak": tf_sus, "unit": "TFLOP/s", "frac": round(achieved / tf_sus, 4),
+                     "peak": tf_burst, "unit": "TFLOP/s", "frac": round(achieved / tf_burst, 4),
+                     "frac_of_sustained_peak": round(achieved / tf_sus, 4),
                      "launch_ms": round(gemm_ms / max(gemm_n, 1), 3)},
         "roofline_step": {"bound": "hbm", "achieved": round(step_bytes / (ph["step"] / 1e3) / 1e9, 1), "peak": hbm,
                           "unit": "GB/s", "frac": round(step_bytes / (ph["step"] / 1e3) / 1e9 / hbm, 4),
@@ -720,6 +885,29 @@ def run_fullloss(args):
     print(json.dumps(line), flush=True)
 
 
+def _relaunch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-exec under
+    torch.distributed.run with one rank per GPU (NCCL), same arguments."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        sys.exit(f"bench.py: --gpus {n} requested but only {have} CUDA device(s) are visible")
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "WARN"))
+    sys.stderr.write(f"[bench] launching {n} ranks: {' '.join(cmd)}\n")
+    rc = subprocess.call(cmd, env=env)
+    if rc:
+        sys.exit(rc)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -732,11 +920,24 @@ def main():
                          "fullloss (the all-negatives arm at the reference's 50K-label cap)")
     ap.add_argument("--refresh-sms", type=int, default=0,
                     help="SM budget of the refresh running concurrently with training on a side stream (0 = serial)")
+    ap.add_argument("--emulate", type=int, default=0,
+                    help="one GPU runs rank 0's share of an N-GPU C4 job (a 1/N label shard, all N ranks' rows); "
+                         "collectives are not run, their bytes are reported")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and env_world is None and args.impl == "ours":
+        # launched without torchrun: start one rank per GPU ourselves
+        return _relaunch(args.gpus)
+    if env_world is not None and int(env_world) != args.gpus and args.impl == "ours":
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}; refusing to report a different GPU count")
     if args.impl == "reference":
         run_reference(args)
+    elif args.emulate:
+        run_emulate(args)
     elif args.config == "c5shard":
         run_c5shard(args)
     elif args.config == "fullloss":

@@ -24,14 +24,23 @@ def apply_classifier_updates_arrays(bank, ids, grads, lr, weight_decay=0.0) -> N
         return
     ops = _backend.get()
     dev = _backend.device()
+    from .bank import DeviceBank
+
+    mirror = DeviceBank.of(bank)
+    if mirror is not None:  # the drop-in trains this bank on the device: update there
+        idx = torch.from_numpy(ids).to(mirror.W.device)
+        rows = mirror.W[idx]
+        g = torch.from_numpy(np.ascontiguousarray(grads, dtype=np.float32).reshape(len(ids), -1)).to(mirror.W.device)
+        local = torch.arange(len(ids), dtype=torch.int64, device=mirror.W.device)
+        ops.apply_updates(rows, local, g, float(lr), float(weight_decay))  # raises before writing
+        mirror.W[idx] = rows
+        if rows.numel():
+            torch.maximum(mirror.w_absmax, rows.abs().amax().reshape(1).float(), out=mirror.w_absmax)
+        mirror.mark_updated()
+        return
     W = bank.weights
     rows = torch.from_numpy(np.ascontiguousarray(W[ids], dtype=np.float32)).to(dev)
     g = torch.from_numpy(np.ascontiguousarray(grads, dtype=np.float32).reshape(len(ids), -1)).to(dev)
     local = torch.arange(len(ids), dtype=torch.int64, device=dev)
     ops.apply_updates(rows, local, g, float(lr), float(weight_decay))  # raises before writing
     W[ids] = rows.cpu().numpy()
-    # keep the trainer's device mirror of this bank (if any) and its max|W|
-    # bound in step with the host array
-    from .trainer import DeviceBank
-
-    DeviceBank.update_rows(bank, ids, rows)

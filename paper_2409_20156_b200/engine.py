@@ -74,6 +74,7 @@ class ClassifierEngine:
         self.adam_step = 0
         self.snap_f32 = self.snap_bf16 = None
         self.snapshot_epoch = -1
+        self.slate_exchange = "regenerate"  # or "gather" (see sample())
 
     # ------------------------------------------------------------ snapshot
     def snapshot(self, epoch: int = 0, check_finite: bool = True) -> None:
@@ -105,20 +106,35 @@ class ClassifierEngine:
             q_all, ip_all, pid_all, k, mode, labels_f32=self.snap_f32, labels_bf16=self.snap_bf16, label_offset=self.lo)
         if self.comm.world == 1:
             return ids, scores
-        parts = self.comm.all_gather_stack(keys)  # [world, world*B, k]
-        mine = parts[:, self.comm.rank * B : (self.comm.rank + 1) * B].contiguous()
+        # rows [r*B, (r+1)*B) of every shard's partial list go to their owner r
+        mine = self.comm.all_to_all(keys)  # [world, B, k]: shard i's keys for this rank's rows
         _, ids, scores = self.ops.topk_merge(mine, k)
         return ids, scores
 
     # ------------------------------------------------------------ sampler
     def sample(self, rows, pos_indptr, pos_ids, hard, epoch: int, step: int, k_h: int | None = None,
                k_r: int | None = None, cand=None, cand_q=None):
-        """Slates for this rank's rows (Philox), all-gathered to every shard."""
+        """Slates of the rows of ALL ranks (Philox, keyed by global row id):
+        with world_size > 1 the sampler's inputs (rows, positives, hard-cache
+        rows, candidates) are all-gathered — ~0.4 MB per rank at C4 — and
+        every shard draws the same global slates itself, instead
+        of all-gathering B x S slates (6 MB per rank at C4).
+        slate_exchange="gather" (attribute) samples only this rank's rows and
+        all-gathers the slates."""
         k_h = self.k_h if k_h is None else k_h
         k_r = self.k_r if k_r is None else k_r
+        k_i = self.k_i if cand is not None else 0
+        if self.comm.world > 1 and self.slate_exchange == "regenerate":
+            rows = self.comm.all_gather(rows)
+            pos_indptr, pos_ids = gather_csr(self.comm, pos_indptr, pos_ids)
+            hard = self.comm.all_gather(hard) if hard is not None else None
+            if cand is not None:
+                cand, cand_q = self.comm.all_gather(cand), self.comm.all_gather(cand_q)
+            return self.ops.sample_slates(self.seed, epoch, step, rows, pos_indptr, pos_ids, hard, k_h, self.n_labels,
+                                          self.k_p, k_r, cand=cand, cand_q=cand_q, k_i=k_i)
         ids, y, origin, weights = self.ops.sample_slates(
             self.seed, epoch, step, rows, pos_indptr, pos_ids, hard, k_h, self.n_labels, self.k_p, k_r,
-            cand=cand, cand_q=cand_q, k_i=self.k_i if cand is not None else 0)
+            cand=cand, cand_q=cand_q, k_i=k_i)
         if self.comm.world > 1:
             ids, y, origin, weights = (self.comm.all_gather(t) for t in (ids, y, origin, weights))
         return ids, y, origin, weights

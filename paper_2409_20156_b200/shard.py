@@ -4,8 +4,12 @@ GPU g of G owns labels [lo_g, hi_g) of W and of its optimizer state
 (data-parallel encoder, label-sharded classifier).
 The collectives of one classifier step are:
   refresh  all_gather(queries, positives) -> local top-k per shard ->
-           all_gather(partial keys) -> exact merge (astra_topk_merge)
-  step     all_gather(embeddings, slates) -> shard-local loss/update ->
+           all_to_all(partial keys, by query owner) -> exact merge
+           (astra_topk_merge) of the world partial lists of the rank's rows
+  sample   all_gather(rows, positives, hard-cache rows) -> every shard runs
+           the Philox sampler over all rows (keyed by global row id, so the
+           slates are identical on every rank and to a 1-GPU run)
+  step     all_gather(embeddings) -> shard-local loss/update ->
            reduce_scatter(grad_emb) to the data-parallel owners,
            all_reduce(loss partial, fp64)
 W itself is never communicated. With world_size 1 every helper is the
@@ -33,21 +37,19 @@ class Comm:
         self.enabled = dist.is_available() and dist.is_initialized()
         self.world = dist.get_world_size(group) if self.enabled else 1
         self.rank = dist.get_rank(group) if self.enabled else 0
-        # NCCL has the fused tensor collectives; gloo (CPU tests) gets the list forms
-        self.nccl = self.enabled and dist.get_backend(group) == "nccl"
+        # the tensor forms (all_gather_into_tensor, reduce_scatter_tensor,
+        # all_to_all_single) run on NCCL and on gloo alike, so the CPU
+        # world_size-2 tests exercise the same calls as the GPU path
+        self.backend = dist.get_backend(group) if self.enabled else None
 
     def all_gather(self, t: torch.Tensor) -> torch.Tensor:
         """Concatenate equal-shaped tensors of all ranks along dim 0."""
         if self.world == 1:
             return t
         t = t.contiguous()
-        if self.nccl:
-            out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-            dist.all_gather_into_tensor(out, t, group=self.group)
-            return out
-        parts = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(parts, t, group=self.group)
-        return torch.cat(parts)
+        out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t, group=self.group)
+        return out
 
     def all_gather_stack(self, t: torch.Tensor) -> torch.Tensor:
         """[world, *t.shape] stack of every rank's tensor."""
@@ -70,14 +72,19 @@ class Comm:
         if self.world == 1:
             return t
         t = t.contiguous()
-        if self.nccl:
-            out = torch.empty((t.shape[0] // self.world,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-            dist.reduce_scatter_tensor(out, t, group=self.group)
-            return out
-        full = t.clone()
-        dist.all_reduce(full, group=self.group)
-        n = t.shape[0] // self.world
-        return full[self.rank * n : (self.rank + 1) * n].contiguous()
+        out = torch.empty((t.shape[0] // self.world,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.reduce_scatter_tensor(out, t, group=self.group)
+        return out
+
+    def all_to_all(self, t: torch.Tensor) -> torch.Tensor:
+        """Dim-0 chunk j of `t` goes to rank j; returns [world, n/world, ...]
+        with chunk i received from rank i."""
+        if self.world == 1:
+            return t.unsqueeze(0)
+        t = t.contiguous()
+        out = torch.empty_like(t)
+        dist.all_to_all_single(out, t, group=self.group)
+        return out.view((self.world, t.shape[0] // self.world) + tuple(t.shape[1:]))
 
     def all_reduce(self, t: torch.Tensor) -> torch.Tensor:
         if self.world > 1:

@@ -14,19 +14,30 @@ draw from the caller's generator, so runs stay bitwise reproducible and the
 generator advances deterministically; origin/weights are returned the way the
 reference does (row 0's origin vector, trainer.py:313). The classifier step
 (gather, loss, factors, grad_emb, per-label sums, SGD update) runs in
-astra_slate_step on a device mirror of bank.weights; touched rows are written
-back so bank.weights stays the authoritative host copy for eval/checkpoints.
+astra_slate_step on a device-resident copy of bank.weights (bank.DeviceBank):
+the device copy is authoritative while training and host reads of
+bank.weights (refresh snapshot, checkpoint, evaluation) copy it back lazily.
 The encoder (embed_batch / encoder_backward_batch / adam_step) stays the
 caller's (the reference's) — it is outside the hot path.
 """
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
 from . import _backend
+from .bank import DeviceBank, device_weights
 from .errors import ConfigError, NumericalError
+
+# The drop-in's classifier step is bitwise run-to-run reproducible by default
+# (the reference's determinism contract, test_acceptance.py:462-474): the
+# two-kernel schedule sums grad_emb in a fixed order. FAST_STEP = True (or
+# install(fast_step=True) / ASTRA_DROPIN_FAST_STEP=1) takes the single
+# label-major pass instead (same W', grad_emb summed in arrival order).
+FAST_STEP = os.environ.get("ASTRA_DROPIN_FAST_STEP") == "1"
 
 _HARD_ONLY = {"StaleHard", "UpToDateHard", "LabelEmbHard"}
 _MIXTURES = {"Mixture", "LabelEmbMixture"}
@@ -44,50 +55,6 @@ def curriculum_counts(epoch: int, strategy, tau_s: int) -> tuple[int, int]:
     frac = min(1.0, (epoch - tau_s) / strategy.curriculum_ramp)
     k_h_eff = int(round(strategy.k_h * frac))
     return k_h_eff, total - k_h_eff
-
-
-class DeviceBank:
-    """Device mirror of a ClassifierBank's fp32 weights (created on first use,
-    rebuilt if bank.weights is replaced by another array object)."""
-
-    def __init__(self, host: np.ndarray):
-        self.host = host
-        self.W = torch.from_numpy(np.ascontiguousarray(host, dtype=np.float32)).to(_backend.device())
-        # running max|W| bound, kept current by every step: lets astra_slate_step
-        # prove finiteness up front and take the single label-major pass
-        self.w_absmax = (self.W.abs().amax().reshape(1).float() if self.W.numel()
-                         else torch.zeros(1, dtype=torch.float32, device=self.W.device))
-
-    @classmethod
-    def for_bank(cls, owner, bank) -> "DeviceBank":
-        db = getattr(owner, "_astra_bank", None)
-        if db is None or db.host is not bank.weights:
-            db = cls(bank.weights)
-            owner._astra_bank = db
-            try:  # reachable from the bank too (classifiers.apply_* keeps it in step)
-                bank._astra_mirror = db
-            except AttributeError:
-                pass
-        return db
-
-    @staticmethod
-    def update_rows(bank, ids, rows_dev) -> None:
-        """After a host-side row update of `bank`: copy the rows into the
-        bank's device mirror, if one exists for this very array, and raise the
-        max|W| bound to cover them."""
-        db = getattr(bank, "_astra_mirror", None)
-        if db is None or db.host is not bank.weights:
-            return
-        idx = torch.as_tensor(np.asarray(ids, dtype=np.int64), device=db.W.device)
-        r = rows_dev.to(db.W.device, db.W.dtype)
-        db.W[idx] = r
-        if r.numel():
-            torch.maximum(db.w_absmax, r.abs().amax().reshape(1).float(), out=db.w_absmax)
-
-    def sync_rows(self, ids: torch.Tensor) -> None:
-        """Copy the given (device) rows back into the host array."""
-        idx = ids.to(torch.int64)
-        self.host[idx.cpu().numpy()] = self.W[idx].cpu().numpy()
 
 
 def _positives_csr(state, batch_rows):
@@ -156,7 +123,7 @@ def _batch_forward_backward(state, batch_rows, epoch, rng, step_lr_enc, step_lr_
 
     ops = _backend.get()
     dev = _backend.device()
-    bank = DeviceBank.for_bank(state, state.bank)
+    bank = DeviceBank.attach(state.bank)
     ids_d = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)).to(dev)
     res = ops.slate_step(
         torch.from_numpy(np.ascontiguousarray(emb_used, dtype=np.float32)).to(dev), ids_d,
@@ -164,7 +131,8 @@ def _batch_forward_backward(state, batch_rows, epoch, rng, step_lr_enc, step_lr_
         torch.from_numpy(np.ascontiguousarray(origin, dtype=np.int8)).to(dev),
         torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float32)).to(dev), bank.W, float(step_lr_clf),
         float(cfg.weight_decay_classifier),
-        keep=None if keep is None else torch.from_numpy(np.ascontiguousarray(keep)).to(dev), w_absmax=bank.w_absmax)
+        keep=None if keep is None else torch.from_numpy(np.ascontiguousarray(keep)).to(dev),
+        w_absmax=bank.w_absmax if FAST_STEP else None)
     grad_emb = res.grad_emb.cpu().numpy()
     status = res.status_host()
     # encoder half stays with the caller; it raises NumericalError on a
@@ -173,7 +141,7 @@ def _batch_forward_backward(state, batch_rows, epoch, rng, step_lr_enc, step_lr_
     xt.adam_step(state.opt, state.encoder, enc_grads, step_lr_enc)
     if status[1] or status[0]:
         raise NumericalError("non-finite classifier gradient")  # classifiers.py:79-80; W untouched
-    bank.sync_rows(torch.unique(ids_d))
+    bank.mark_updated()
     return res.loss
 
 
@@ -195,9 +163,9 @@ def _dev(a, dtype=None):
 
 
 def _host_weights(state):
-    """The bank's current weights on the device (uploaded from the host copy,
-    which the reference and the drop-in keep authoritative)."""
-    return _dev(state.bank.weights, np.float32)
+    """The bank's current weights on the device (the live device copy when
+    the drop-in trains this bank, else an upload of the host array)."""
+    return device_weights(state.bank)
 
 
 def _probe_full_loss(state) -> float:
@@ -261,7 +229,8 @@ def train_full_loss_baseline(dataset, config, eval_dataset=None, checkpoint_path
     n_batches = -(-len(state.active_rows) // config.batch_size)
     state.total_steps = max(config.epochs * n_batches, 1)
     ops = _backend.get()
-    W = _host_weights(state)
+    mirror = DeviceBank.attach(state.bank)
+    W = mirror.W
     for epoch in range(config.epochs):
         t0 = time.perf_counter()
         rng = np.random.default_rng((config.seed, 7919, epoch))
@@ -288,8 +257,8 @@ def train_full_loss_baseline(dataset, config, eval_dataset=None, checkpoint_path
             enc_grads = xt.encoder_backward_batch(state.encoder, feats, grad_emb.cpu().numpy())
             xt.adam_step(state.opt, state.encoder, enc_grads, lr_enc)
             ops.full_loss_update(W, G, emb_d, lr_clf, config.weight_decay_classifier)
+            mirror.mark_updated()
             state.global_step += 1
-        state.bank.weights[...] = W.cpu().numpy()
         wall = time.perf_counter() - t0
         evaluate_now = (epoch % config.eval_every == config.eval_every - 1) or epoch == config.epochs - 1
         p1, p5 = xt._eval_p_at(state) if evaluate_now else (None, None)

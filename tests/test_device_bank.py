@@ -68,7 +68,7 @@ def test_mirror_step_and_host_updates_cuda(cuda_lib):
     L, d, B, S = 3000, 128, 32, 60
     W = rng.uniform(-1 / np.sqrt(d), 1 / np.sqrt(d), (L, d)).astype(np.float32)
     bank = _Bank(W.copy())
-    db = DeviceBank.for_bank(_Owner(), bank)
+    db = DeviceBank.attach(bank)
     emb = rng.standard_normal((B, d)).astype(np.float32)
     ids = rng.integers(0, L, (B, S)).astype(np.int64)
     y = (rng.random((B, S)) < 0.05).astype(np.int8)
@@ -79,7 +79,7 @@ def test_mirror_step_and_host_updates_cuda(cuda_lib):
     cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
     ids_d = cu(ids.astype(np.int32))
     res = ops.slate_step(cu(emb), ids_d, cu(y), cu(origin), cu(weights), db.W, 0.1, 1e-4, w_absmax=db.w_absmax)
-    db.sync_rows(torch.unique(ids_d))
+    db.mark_updated()  # the device copy is now newer: the next host read copies it back
     Wref = W.copy()
     loss, _, _, uids = port.slate_step(Wref, emb, None, ids, y, origin, weights, 0.1, 1e-4)
     assert res.status_host() == [0, 0, 0, 0]
@@ -90,3 +90,44 @@ def test_mirror_step_and_host_updates_cuda(cuda_lib):
     classifiers.apply_classifier_updates_arrays(bank, np.array([0, 5, 9, 13]), grads, 0.5)
     np.testing.assert_array_equal(db.W.cpu().numpy(), bank.weights)
     assert float(db.w_absmax.item()) >= float(np.abs(bank.weights).max())
+
+
+def test_lazy_host_sync_and_device_row_updates(oracle):
+    """The device copy is authoritative while the drop-in trains: host reads
+    of bank.weights copy it back (in place: aliases stay valid), shape queries
+    do not, row updates through apply_classifier_updates_arrays run on the
+    device copy, and assigning a new array drops the mirror."""
+    import torch
+
+    from paper_2409_20156_b200.bank import DeviceBank as DB
+
+    @dataclass
+    class Bank:
+        weights: np.ndarray
+
+        @property
+        def n_labels(self):
+            return self.weights.shape[0]
+
+    host = np.zeros((6, 3), np.float32)
+    bank = Bank(host)
+    m = DB.attach(bank)
+    assert DB.attach(bank) is m and isinstance(bank, Bank)
+    m.W += 1.0  # a "step" on the device copy
+    m.mark_updated()
+    assert host.sum() == 0.0  # nothing copied yet
+    assert bank.n_labels == 6 and m.dirty  # shape queries do not sync
+    w = bank.weights
+    assert w is host and host.sum() == 18.0 and not m.dirty
+    classifiers.apply_classifier_updates_arrays(bank, np.array([1, 4]), np.ones((2, 3), np.float32), 0.5, 0.0)
+    assert m.dirty and host[1, 0] == 1.0  # updated on the device only
+    np.testing.assert_array_equal(bank.weights[[1, 4]], np.full((2, 3), 0.5, np.float32))
+    assert float(m.w_absmax.item()) >= 0.5  # the bound covers the updated rows
+    bank.weights = np.full((6, 3), 7.0, np.float32)
+    assert DB.of(bank) is None
+    m2 = DB.attach(bank)
+    assert m2 is not m and float(m2.W[0, 0]) == 7.0
+    host2 = bank.weights
+    host2[2] = -3.0  # a direct in-place host write must be announced
+    DB.host_modified(bank)
+    assert float(m2.W[2, 0]) == -3.0 and not torch.equal(m2.W[2], m2.W[0])

@@ -25,11 +25,11 @@ ROOT = os.path.dirname(HERE)
 L, D, B, K_P, K_H, K_R = 997, 24, 16, 3, 6, 20
 
 
-def _data(seed=0):
+def _data(seed=0, world=2):
     rng = np.random.default_rng(seed)
     W = rng.uniform(-0.2, 0.2, size=(L, D)).astype(np.float32)
     world_rows = {}
-    for r in range(2):
+    for r in range(world):
         emb = rng.standard_normal((B, D)).astype(np.float32)
         pos = [np.sort(rng.choice(L, size=int(rng.integers(1, 5)), replace=False)).astype(np.int32) for _ in range(B)]
         rows = np.arange(B, dtype=np.int64) + 1000 * r
@@ -43,16 +43,17 @@ def _csr(pos):
     return ip, np.concatenate(pos).astype(np.int32)
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, exchange="regenerate"):
     sys.path[:0] = [ROOT, HERE]
     import oracle_backend
     from paper_2409_20156_b200.engine import ClassifierEngine
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    W, data = _data()
+    W, data = _data(world=world)
     eng = ClassifierEngine(L, D, k_p=K_P, k_h=K_H, k_r=K_R, weights=W, refresh_mode="fp32", seed=5, device="cpu",
                            backend=oracle_backend)
+    eng.slate_exchange = exchange
     eng.snapshot(0)
     emb, pos, rows = data[rank]
     ip, pid = _csr(pos)
@@ -70,38 +71,81 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_two_rank_label_sharding_matches_single_process():
+@pytest.mark.parametrize("world,exchange", [(2, "regenerate"), (3, "regenerate"), (2, "gather")])
+def test_label_sharding_matches_single_process(world, exchange):
     sys.path[:0] = [HERE]
     import oracle_backend
     from oracle import c_oracle as co
     from paper_2409_20156_b200.engine import ClassifierEngine
 
     with tempfile.TemporaryDirectory() as tmp:
-        mp.start_processes(_worker, args=(2, _free_port(), tmp), nprocs=2, join=True, start_method="spawn")
-        res = [dict(np.load(os.path.join(tmp, f"r{r}.npz"))) for r in range(2)]
-    W, data = _data()
-    # refresh: exact global top-k for each rank's rows
-    for r in range(2):
+        mp.start_processes(_worker, args=(world, _free_port(), tmp, exchange), nprocs=world, join=True,
+                           start_method="spawn")
+        res = [dict(np.load(os.path.join(tmp, f"r{r}.npz"))) for r in range(world)]
+    W, data = _data(world=world)
+    # refresh: exact global top-k for each rank's rows (all_to_all by query owner + merge)
+    for r in range(world):
         emb, pos, _ = data[r]
         _, ref_ids, _ = co.refresh_fp32(emb, W, *_csr(pos), K_H)
         np.testing.assert_array_equal(res[r]["ids"], ref_ids)
     # shards partition the label range
-    assert res[0]["lo"] == 0 and res[0]["hi"] == res[1]["lo"] and res[1]["hi"] == L
+    assert res[0]["lo"] == 0 and res[-1]["hi"] == L
+    assert all(res[r]["hi"] == res[r + 1]["lo"] for r in range(world - 1))
     # single-process step on the concatenated batch with the same slates
-    emb_all = np.concatenate([data[r][0] for r in range(2)])
-    pos_all = data[0][1] + data[1][1]
-    rows_all = np.concatenate([data[r][2] for r in range(2)])
+    emb_all = np.concatenate([data[r][0] for r in range(world)])
+    pos_all = sum((data[r][1] for r in range(world)), [])
+    rows_all = np.concatenate([data[r][2] for r in range(world)])
     ip, pid = _csr(pos_all)
-    hard = torch.from_numpy(np.concatenate([res[r]["ids"] for r in range(2)]))
+    hard = torch.from_numpy(np.concatenate([res[r]["ids"] for r in range(world)]))
     one = ClassifierEngine(L, D, k_p=K_P, k_h=K_H, k_r=K_R, weights=W, refresh_mode="fp32", seed=5, device="cpu",
                            backend=oracle_backend)
     slates = one.sample(torch.from_numpy(rows_all), torch.from_numpy(ip), torch.from_numpy(pid), hard, epoch=2, step=3)
-    np.testing.assert_array_equal(slates[0].numpy(), res[0]["slate_ids"])
+    for r in range(world):  # every shard drew (or received) the same global slates
+        np.testing.assert_array_equal(slates[0].numpy(), res[r]["slate_ids"])
     loss, grad_emb, status = one.step(torch.from_numpy(emb_all), slates, 0.3, 1e-3)
     W1 = one.W.numpy()
-    np.testing.assert_array_equal(np.concatenate([res[0]["W"], res[1]["W"]]), W1)  # bitwise: shard-local updates
-    ge = np.concatenate([res[0]["grad_emb"], res[1]["grad_emb"]])
+    np.testing.assert_array_equal(np.concatenate([res[r]["W"] for r in range(world)]), W1)  # bitwise: shard-local
+    ge = np.concatenate([res[r]["grad_emb"] for r in range(world)])
     np.testing.assert_allclose(ge, grad_emb.numpy(), rtol=1e-5, atol=1e-6 * np.abs(grad_emb.numpy()).max())
     assert abs(float(res[0]["loss"][0]) - float(loss[0])) <= 1e-9 * abs(float(loss[0]))
-    assert float(res[0]["loss"][0]) == float(res[1]["loss"][0])
+    assert all(float(res[0]["loss"][0]) == float(res[r]["loss"][0]) for r in range(world))
     assert not res[0]["status"].any() and not status.numpy().any()
+
+
+def _comm_worker(rank, world, port, out_dir):
+    sys.path[:0] = [ROOT, HERE]
+    from paper_2409_20156_b200.shard import Comm, gather_csr
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c = Comm()
+    t = torch.arange(world * 4, dtype=torch.int64).view(world * 2, 2) + 1000 * rank
+    ag = c.all_gather(t)
+    a2a = c.all_to_all(t)
+    rs = c.reduce_scatter(t.double())
+    ar = c.all_reduce(torch.tensor([float(rank + 1)], dtype=torch.float64))
+    ip = torch.tensor([0, rank + 1, rank + 3], dtype=torch.int64)
+    ids = torch.arange(rank + 3, dtype=torch.int32) + 100 * rank
+    gip, gids = gather_csr(c, ip, ids)
+    np.savez(os.path.join(out_dir, f"c{rank}.npz"), ag=ag.numpy(), a2a=a2a.numpy(), rs=rs.numpy(), ar=ar.numpy(),
+             gip=gip.numpy(), gids=gids.numpy())
+    dist.destroy_process_group()
+
+
+def test_comm_collective_semantics():
+    """The tensor-form collectives shard.Comm issues (the same calls as on
+    NCCL): all_gather_into_tensor, all_to_all_single, reduce_scatter_tensor,
+    all_reduce, and the ragged CSR gather."""
+    world = 3
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.start_processes(_comm_worker, args=(world, _free_port(), tmp), nprocs=world, join=True, start_method="spawn")
+        res = [dict(np.load(os.path.join(tmp, f"c{r}.npz"))) for r in range(world)]
+    ts = [np.arange(world * 4, dtype=np.int64).reshape(world * 2, 2) + 1000 * r for r in range(world)]
+    for r in range(world):
+        np.testing.assert_array_equal(res[r]["ag"], np.concatenate(ts))
+        np.testing.assert_array_equal(res[r]["a2a"], np.stack([t[2 * r : 2 * r + 2] for t in ts]))
+        np.testing.assert_array_equal(res[r]["rs"], sum(t.astype(np.float64) for t in ts)[2 * r : 2 * r + 2])
+        assert float(res[r]["ar"][0]) == sum(range(1, world + 1))
+        counts = sum(([1 + q, 2] for q in range(world)), [])
+        np.testing.assert_array_equal(res[r]["gip"], np.concatenate([[0], np.cumsum(counts)]))
+        np.testing.assert_array_equal(res[r]["gids"], np.concatenate([np.arange(q + 3) + 100 * q for q in range(world)]))
