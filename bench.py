@@ -458,6 +458,19 @@ def run_emulate(args):
         data.append((q, pid, hard))
     ip_step = torch.arange(0, Rg * lpp + 1, lpp, dtype=torch.int64, device="cuda")
     ip_mb = torch.arange(0, Bg * lpp + 1, lpp, dtype=torch.int64, device="cuda")
+    ip_b = ip_mb[: B + 1]
+    regen = args.slate_exchange == "regenerate"
+
+    def slates_of(t, i, n_rows):
+        q, pid, hard = data[t]
+        rows = torch.arange((t * M + i) * Bg, (t * M + i) * Bg + n_rows, dtype=torch.int64, device="cuda")
+        return ops.sample_slates(0, 1, t * M + i, rows, ip_mb[: n_rows + 1], pid[i * Bg * lpp:(i * Bg + n_rows) * lpp],
+                                 hard[i * Bg:i * Bg + n_rows], k_h, L, k_p, k_r)
+
+    # "gather" (engine default): rank 0 samples its own B rows, the other
+    # ranks' slates arrive by all-gather; their slates are drawn up front here
+    full = None if regen else [[slates_of(t, i, Bg) for i in range(M)] for t in range(n_steps)]
+    torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3 + 2 * M)] for _ in range(n_steps)]
     keep_ids = []
@@ -472,9 +485,11 @@ def run_emulate(args):
         ops.topk_merge(keys.view(N, R, k_h), k_h)  # the N shards' lists of this rank's R rows
         e[2].record(stream)
         for i in range(M):
-            rows = torch.arange((t * M + i) * Bg, (t * M + i + 1) * Bg, dtype=torch.int64, device="cuda")
-            sl = ops.sample_slates(0, 1, t * M + i, rows, ip_mb, pid[i * Bg * lpp:(i + 1) * Bg * lpp],
-                                   hard[i * Bg:(i + 1) * Bg], k_h, L, k_p, k_r)
+            if regen:
+                sl = slates_of(t, i, Bg)
+            else:
+                slates_of(t, i, B)  # this rank's own rows (rows 0..B-1 of the global minibatch)
+                sl = full[t][i]
             e[3 + 2 * i].record(stream)
             emb = q[i * Bg:(i + 1) * Bg]
             res = ops.slate_step(emb, *sl, W, c["lr"], c["wd"], label_offset=lo, w_absmax=w_absmax)
@@ -524,7 +539,8 @@ def run_emulate(args):
         "queries_all_gather": (N - 1) * R * d * 4,
         "positives_all_gather": (N - 1) * R * (lpp * 4 + 8),
         "keys_all_to_all": (N - 1) * R * k_h * 8,
-        "sampler_inputs_all_gather": M * (N - 1) * B * (8 + lpp * 4 + 8 + k_h * 4),
+        **({"sampler_inputs_all_gather": M * (N - 1) * B * (8 + lpp * 4 + 8 + k_h * 4)} if regen else
+           {"slates_all_gather": M * (N - 1) * B * S * 10}),
         "emb_all_gather": M * (N - 1) * B * d * 4,
         "grad_emb_reduce_scatter": M * (N - 1) * B * d * 4,
         "loss_status_all_reduce": M * 2 * (8 + 16),
@@ -534,7 +550,8 @@ def run_emulate(args):
         "value": round(Rg * K / (ms * K / 1e3), 1), "unit": UNIT, "n_gpus": 1, "emulates_n_gpus": N,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32 W/step, bf16 tensor-core refresh + fp32 re-rank", "data": "synthetic",
-        "config": dict(bench_config(N), labels_shard=Lr, rows_per_step_job=Rg, minibatch_job=Bg),
+        "config": dict(bench_config(N), labels_shard=Lr, rows_per_step_job=Rg, minibatch_job=Bg,
+                       slate_exchange=args.slate_exchange),
         "phases_ms_per_step": {k: round(v, 4) for k, v in ph.items()},
         "owned_slots_per_minibatch": round(slots, 1), "unique_owned_labels_per_minibatch": round(U, 1),
         "occurrences_per_owned_label": round(slots / max(U, 1), 3),
@@ -923,6 +940,8 @@ def main():
     ap.add_argument("--emulate", type=int, default=0,
                     help="one GPU runs rank 0's share of an N-GPU C4 job (a 1/N label shard, all N ranks' rows); "
                          "collectives are not run, their bytes are reported")
+    ap.add_argument("--slate-exchange", default="gather", choices=["gather", "regenerate"],
+                    help="--emulate: how the N-GPU job shares slates (engine.ClassifierEngine.slate_exchange)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -74,7 +74,7 @@ class ClassifierEngine:
         self.adam_step = 0
         self.snap_f32 = self.snap_bf16 = None
         self.snapshot_epoch = -1
-        self.slate_exchange = "regenerate"  # or "gather" (see sample())
+        self.slate_exchange = "gather"  # or "regenerate" (see sample())
 
     # ------------------------------------------------------------ snapshot
     def snapshot(self, epoch: int = 0, check_finite: bool = True) -> None:
@@ -114,13 +114,18 @@ class ClassifierEngine:
     # ------------------------------------------------------------ sampler
     def sample(self, rows, pos_indptr, pos_ids, hard, epoch: int, step: int, k_h: int | None = None,
                k_r: int | None = None, cand=None, cand_q=None):
-        """Slates of the rows of ALL ranks (Philox, keyed by global row id):
-        with world_size > 1 the sampler's inputs (rows, positives, hard-cache
-        rows, candidates) are all-gathered — ~0.4 MB per rank at C4 — and
-        every shard draws the same global slates itself, instead
-        of all-gathering B x S slates (6 MB per rank at C4).
-        slate_exchange="gather" (attribute) samples only this rank's rows and
-        all-gathers the slates."""
+        """Slates of the rows of ALL ranks (Philox, keyed by global row id,
+        so every rank holds the same global slates as a 1-GPU run).
+        slate_exchange (attribute):
+          "gather" (default): each rank samples its own rows and the B x S
+            slates are all-gathered (10 B per slot: 6 MB per rank at C4);
+          "regenerate": the sampler's inputs (rows, positives, hard-cache
+            rows, candidates; ~0.4 MB per rank at C4) are all-gathered and
+            every rank draws all N x B rows itself.
+        Measured (bench.py --emulate N, profiles/r02): regenerating costs
+        0.39 / 0.62 / 1.04 ms per minibatch at N = 2 / 4 / 8 against 0.24 ms
+        for the rank's own rows, more than the all-gather of the slates over
+        NVLink (42 MB at N = 8), so "gather" is the default."""
         k_h = self.k_h if k_h is None else k_h
         k_r = self.k_r if k_r is None else k_r
         k_i = self.k_i if cand is not None else 0

@@ -26,3 +26,13 @@ def pytest_configure(config):
 
         backend = oracle_backend
     install(backend=backend, slates=os.environ.get("ASTRA_DROPIN_SLATES", "philox"))
+
+
+def pytest_terminal_summary(terminalreporter):
+    """With the CUDA backend: report how many kernels libastra_b200 launched
+    (tests/test_dropin_cuda.py checks it is > 0: no silent host fallback)."""
+    if os.environ.get("ASTRA_DROPIN_BACKEND", "oracle") != "cuda":
+        return
+    from paper_2409_20156_b200 import _lib
+
+    terminalreporter.write_line(f"[astra] libastra_b200 kernel launches: {_lib.launch_count()}")

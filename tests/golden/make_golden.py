@@ -23,6 +23,7 @@ import sys
 import numpy as np
 import scipy.sparse as sp
 
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import xcmix.anns as anns
 import xcmix.classifiers as classifiers
 import xcmix.trainer as trainer
@@ -177,6 +178,39 @@ def make_update_fixture(name, *, L, d, U, seed):
     print("wrote", name)
 
 
+from golden_train_spec import TRAIN_CONFIG, TRAIN_SPEC  # noqa: E402
+
+
+def train_inputs(xcmix_dataset, xcmix_trainer):
+    """The planted dataset, eval split and config of the train() golden (also
+    rebuilt by tests/test_dropin_train_golden.py from the installed reference)."""
+    sp_ = TRAIN_SPEC
+    train, ev = xcmix_dataset.generate_synthetic(sp_["n_points"], sp_["n_features"], sp_["n_labels"],
+                                                 sp_["labels_per_point"], noise_level=sp_["noise_level"],
+                                                 seed=sp_["seed"])
+    return train, ev, xcmix_trainer.TrainConfig(**TRAIN_CONFIG)
+
+
+def make_train_fixture(name):
+    """A whole reference train() run: the refresh pipeline (snapshot at the end
+    of epoch c-2, consumed at c), Mixture slates, the sampled step, the
+    encoder's Adam, the per-epoch probe and P@k (trainer.py:493-556)."""
+    import xcmix.dataset as xd
+
+    train_ds, ev, cfg = train_inputs(xd, trainer)
+    enc, bank, log = trainer.train(train_ds, cfg, eval_dataset=ev)
+    rec = log.records
+    np.savez_compressed(
+        os.path.join(HERE, name),
+        loss=np.array([r.mean_slate_loss for r in rec]), probe=np.array([r.probe_full_loss for r in rec]),
+        p1=np.array([np.nan if r.p_at_1 is None else r.p_at_1 for r in rec]),
+        p5=np.array([np.nan if r.p_at_5 is None else r.p_at_5 for r in rec]),
+        snapshot=np.array([r.snapshot_epoch for r in rec]), W=bank.weights, projection=enc.projection,
+        consume=np.array([e["epoch"] for e in log.events if e["stage"] == anns.STAGE_CONSUME]),
+    )
+    print("wrote", name, [round(r.mean_slate_loss, 6) for r in rec])
+
+
 def main():
     make_step_fixture("step_c1_parity.npz", L=2000, d=32, n=400, B=64, k_p=3, k_h=8, k_r=16, dropout=0.0, n_steps=2, seed=3)
     make_step_fixture("step_dropout.npz", L=1500, d=64, n=200, B=48, k_p=2, k_h=6, k_r=12, dropout=0.2, n_steps=1, seed=5)
@@ -185,7 +219,11 @@ def main():
     make_refresh_fixture("refresh_random.npz", L=1500, d=32, N=300, k_h=16, seed=11, ties=False)
     make_refresh_fixture("refresh_ties.npz", L=600, d=16, N=64, k_h=10, seed=12, ties=True)
     make_update_fixture("update.npz", L=500, d=24, U=120, seed=13)
+    make_train_fixture("train_run.npz")
 
 
 if __name__ == "__main__":
-    sys.exit(main())
+    if len(sys.argv) > 1 and sys.argv[1] == "train":
+        make_train_fixture("train_run.npz")
+    else:
+        sys.exit(main())
