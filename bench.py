@@ -570,27 +570,41 @@ def run_emulate(args):
 
 # ------------------------------------------------------------------ C5 shard emulation
 C5 = dict(workload="120M-label synthetic, rank-0 shard of 8 (15M labels) emulated on one GPU", L_total=120_000_000,
-          world=8, d=768, B_global=4096, k_p=16, k_h=200, k_i=200, n_cand=400, k_r=2000, labels_per_point=10,
+          world=8, d=768, B_global=4096, k_p=16, k_h=200, k_i=128, n_cand=128, k_r=2000, labels_per_point=10,
           lr=1e-3, wd=0.0)
 
 
 def run_c5shard(args):
     """BASELINE.json configs[4] as one of its 8 label shards: W (15M x 768 bf16)
-    + Adam m, v (fp32) resident on this GPU; each step = the refresh of the
-    global batch's 4096 queries against the shard (bf16 tcgen05 two-pass +
-    bf16-row re-rank, k_h=200) + Philox slates over all 120M labels (k_p=16,
-    k_h=200, k_i=200 importance, k_r=2000 -> S=2416) + the fused loss/update of
-    the slots this shard owns (~1/8). The collectives of the 8-GPU job (query /
-    embedding all-gathers, key all-gather, grad_emb reduce-scatter: ~40 MB per
-    step over NVLink) are not run; the line reports the shard's compute time."""
+    + Adam m, v (fp32) resident on this GPU. Each step:
+      refresh  the global batch's 4096 queries against the shard (bf16 tcgen05
+               two-pass + re-rank on the bf16 rows) for top-(k_h + n_c) =
+               top-328, then the merge of the 8 shards' lists (astra_topk_merge;
+               the other 7 shards' lists are this shard's list relabelled into
+               their label ranges, so the merged cache owns 1/8 of its ids here,
+               as in the real job) and astra_importance_split: the negative-
+               mixture cache H (k_h=200) + importance candidates C (n_c=128)
+               with q = sigmoid(stale score). This refresh
+               builds the NEXT step's cache (stale by one step).
+      sample   Philox slates over all 120M labels from the previous refresh's
+               cache: k_p=16, k_h=200, k_i=128 importance draws (weight
+               1/(k_i q)), k_r=2000 uniform -> S=2344.
+      step     the fused loss/Adam update of the slots this shard owns (~1/8).
+    n_c = 128 (not 200): the bf16-row re-rank holds k' <= 512 candidates, so
+    k_h + n_c <= 341. The collectives of the 8-GPU job (query / embedding
+    all-gathers, key all-to-all, grad_emb reduce-scatter: ~40 MB per step over
+    NVLink) are not run; the line reports the shard's compute time."""
     import torch
 
     from paper_2409_20156_b200 import _lib, ops
 
     torch.cuda.set_device(0)
     c = C5
-    L = c["L_total"] // c["world"]
+    N = c["world"]
+    L = c["L_total"] // N
     d, B = c["d"], c["B_global"]
+    k_h, n_c, k_i = c["k_h"], c["n_cand"], c["k_i"]
+    kc = k_h + n_c
     g = torch.Generator(device="cuda")
     g.manual_seed(0)
     W = torch.empty((L, d), dtype=torch.bfloat16, device="cuda")
@@ -601,6 +615,14 @@ def run_c5shard(args):
     v = torch.zeros_like(m)
     w_absmax = W.abs().max().float().reshape(1)  # running max|W| bound (kept by the step kernels)
     snap = W.clone()
+    shift = torch.arange(N, dtype=torch.int64, device="cuda").view(N, 1, 1) * L  # label-range offsets of the shards
+
+    def cache_of(emb, ip, pid):
+        keys, _, _ = ops.refresh_topk(emb, ip, pid, kc, "bf16_rerank", labels_bf16=snap)
+        # keys = (ord(score) << 32) | (2^32 - 1 - id): relabelling id -> id + s*L subtracts s*L
+        _, gids, gscores = ops.topk_merge((keys.unsqueeze(0) - shift).contiguous(), kc)
+        return ops.importance_split(gids, gscores, k_h)
+
     n_steps = args.warmup + args.steps
     data = []
     for t in range(n_steps):
@@ -609,25 +631,28 @@ def run_c5shard(args):
         ip = torch.arange(0, B * c["labels_per_point"] + 1, c["labels_per_point"], dtype=torch.int64, device="cuda")
         pid = pos.to(torch.int32).reshape(-1).contiguous()
         emb = torch.randn((B, d), device="cuda", generator=g)
-        hard = torch.randint(0, c["L_total"], (B, c["k_h"]), device="cuda", generator=g).to(torch.int32)
-        cand = torch.randint(0, c["L_total"], (B, c["n_cand"]), device="cuda", generator=g).to(torch.int32)
-        cand_q = torch.full((B, c["n_cand"]), 1.0 / c["n_cand"], device="cuda")
-        data.append((rows, ip, pid, emb, hard, cand, cand_q))
+        data.append([rows, ip, pid, emb, None])
+    data[0][4] = cache_of(*data[0][1:4])  # the first step's stale cache
+    torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_steps)]
 
     def one(t):
-        rows, ip, pid, emb, hard, cand, cand_q = data[t]
+        rows, ip, pid, emb, cache = data[t]
         e = ev[t]
         e[0].record(stream)
-        ops.refresh_topk(emb, ip, pid, c["k_h"], "bf16_rerank", labels_bf16=snap)
+        nxt = cache_of(emb, ip, pid)  # the next step's cache (stale by one step)
+        if t + 1 < n_steps:
+            data[t + 1][4] = nxt
         e[1].record(stream)
-        sl = ops.sample_slates(0, 1, t, rows, ip, pid, hard, c["k_h"], c["L_total"], c["k_p"], c["k_r"], cand=cand,
-                               cand_q=cand_q, k_i=c["k_i"])
+        hard, cand, cand_q = cache
+        sl = ops.sample_slates(0, 1, t, rows, ip, pid, hard, k_h, c["L_total"], c["k_p"], c["k_r"], cand=cand,
+                               cand_q=cand_q, k_i=k_i)
         e[2].record(stream)
         res = ops.slate_step(emb, *sl, W, c["lr"], c["wd"], optimizer="adam", adam_m=m, adam_v=v, adam_step=t + 1,
                              label_offset=0, w_absmax=w_absmax)
         e[3].record(stream)
+        data[t][4] = None
         return res, sl
 
     for t in range(args.warmup):
@@ -636,12 +661,15 @@ def run_c5shard(args):
     for name in ("refresh_gemm", "refresh_verify", "step_single", "slot_forward", "label_update"):
         _lib.kernel_timing(name)
     _lib.kernel_timing_enable(True)
+    clocks = ClockSampler(0)
+    clocks.start()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for t in range(args.warmup, n_steps):
         res, sl = one(t)
     t1.record(stream)
     torch.cuda.synchronize()
+    clk = clocks.stop()
     _lib.kernel_timing_enable(False)
     kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "refresh_verify", "step_single", "slot_forward", "label_update")}
     ops.raise_for_step_status(res.status)
@@ -656,21 +684,23 @@ def run_c5shard(args):
     ids = sl[0]
     own = ids[(ids >= 0) & (ids < L)]
     U = int(torch.unique(own).numel())
-    _, tf_burst, tf_sus, peak_kind = peaks()[0], peaks()[1], peaks()[2], peaks()[3]
-    hbm = peaks()[0]
+    n_imp_owned = int(((sl[2] == ops.ORIGIN_IMP) & (ids >= 0) & (ids < L)).sum())
+    hbm, tf_burst, tf_sus, peak_kind = peaks()
     gemm_ms, gemm_n = kt["refresh_gemm"]
     flops = 2.0 * L * d * B
     achieved = flops / (gemm_ms / max(gemm_n, 1) / 1e3) / 1e12
     step_bytes = U * d * (2 * 2 + 2 * 8) + 2 * B * d * 4 + B * sl[0].shape[1] * 5
+    upd_ms, upd_n = kt["label_update"]
     line = {
         "metric": METRIC + " [C5 shard emulation]", "value": round(B / (ms / 1e3), 1), "unit": UNIT, "n_gpus": 1,
-        "emulates_n_gpus": c["world"], "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "emulates_n_gpus": N, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16 W + fp32 Adam state; bf16 tcgen05 refresh + re-rank on the bf16 rows", "data": "synthetic",
         "config": {"workload": c["workload"], "n_labels_total": c["L_total"], "labels_shard": L, "dim": d,
-                   "global_batch": B, "k_p": c["k_p"], "k_h": c["k_h"], "k_i": c["k_i"], "k_r": c["k_r"],
+                   "global_batch": B, "k_p": c["k_p"], "k_h": k_h, "k_i": k_i, "n_cand": n_c, "k_r": c["k_r"],
                    "slate": int(sl[0].shape[1]), "tau_r": 1, "optimizer": "adam", "owned_slots": int(own.numel()),
-                   "unique_rows": U},
+                   "owned_importance_slots": n_imp_owned, "unique_rows": U,
+                   "importance_cache": "refresh top-(k_h+n_c) -> merge -> H + C, q = sigmoid(stale score)"},
         "phases_ms_per_step": {k: round(v, 3) for k, v in ph.items()},
         "refresh_mips_qps_shard": round(B / (ph["refresh"] / 1e3), 1),
         "refresh_verify_ms": round(kt["refresh_verify"][0] / max(kt["refresh_verify"][1], 1), 4),
@@ -681,8 +711,10 @@ def run_c5shard(args):
                      "launch_ms": round(gemm_ms / max(gemm_n, 1), 3)},
         "roofline_step": {"bound": "hbm", "achieved": round(step_bytes / (ph["step"] / 1e3) / 1e9, 1), "peak": hbm,
                           "unit": "GB/s", "frac": round(step_bytes / (ph["step"] / 1e3) / 1e9 / hbm, 4),
-                          "algorithmic": f"U*d*(2*2 + 2*8) + 2*B*d*4 + B*S*5 = {step_bytes:.3e} B (U={U})"},
+                          "algorithmic": f"U*d*(2*2 + 2*8) + 2*B*d*4 + B*S*5 = {step_bytes:.3e} B (U={U})",
+                          "label_update_launch_ms": round(upd_ms / max(upd_n, 1), 4) if upd_n else None},
         "memory_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
+        "clocks": clk,
     }
     print(json.dumps(line), flush=True)
 

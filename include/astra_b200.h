@@ -175,6 +175,17 @@ int astra_sample_slates(uint64_t seed, uint32_t epoch, uint32_t step, const int6
                         int cand_stride, int n_c, int k_i, int64_t n_labels, int k_p, int k_r,
                         int32_t* ids, int8_t* y, int8_t* origin, float* weights, void* stream);
 
+/* Importance-sampled class (extension): split a stale
+ * refresh of top-(k_h + n_c) per row (ids int32 + fp32 scores [nq, k_tot],
+ * descending, as astra_refresh_topk writes them, k_tot = k_h + n_c) into the
+ * sampler's inputs: hard [nq, k_h] (H, the first k_h ids), cand [nq, n_c]
+ * (C, the next n_c) and cand_q [nq, n_c] = sigmoid(stale score) (unnormalised
+ * draw weights; astra_sample_slates normalises per row and weights each draw
+ * 1/(k_i q)). ids < 0 get q = 0. H and C are disjoint and exclude the row's
+ * positives (the refresh masked them). */
+int astra_importance_split(const int32_t* ids, const float* scores, int64_t nq, int k_tot, int k_h,
+                           int32_t* hard, int32_t* cand, float* cand_q, void* stream);
+
 /* ------------------------------------------------------------------------
  * Sampled BCE forward/backward fused with the sparse row update — replaces
  * the classifier half of _batch_forward_backward (trainer.py:366-394) and

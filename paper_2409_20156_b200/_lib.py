@@ -37,6 +37,7 @@ _SIGS = {
     "astra_merge_workspace_size": ([i64, i32], sz),
     "astra_topk_merge": ([p, i64, i32, i32, i32, p, p, p, p, sz, p], i32),
     "astra_sample_slates": ([u64, u32, u32, p, i32, p, p, p, i32, i32, p, p, i32, i32, i32, i64, i32, i32, p, p, p, p, p], i32),
+    "astra_importance_split": ([p, p, i64, i32, i32, p, p, p, p], i32),
     "astra_step_workspace_size": ([i32, i32, i32, i64], sz),
     "astra_slate_step": ([p, p, p, p, p, i64, p, i64, p, i32, i32, i32, p, i32, p, p, i32, i64, i64, f64, f64, f64, f64, f64,
                           i64, p, p, p, p, p, p, sz, p], i32),

@@ -66,6 +66,7 @@ int refresh_flagged(const void*, size_t, int64_t, int64_t, int, int, int, int64_
 int sample_slates(uint64_t, uint32_t, uint32_t, const int64_t*, int, const int64_t*, const int32_t*, const int32_t*,
                   int, int, const int32_t*, const float*, int, int, int, int64_t, int, int, int32_t*, int8_t*,
                   int8_t*, float*, cudaStream_t);
+int importance_split(const int32_t*, const float*, int64_t, int, int, int32_t*, int32_t*, float*, cudaStream_t);
 size_t step_workspace_size(int, int, int, int64_t);
 void set_step_deterministic(int on);
 size_t dense_workspace_size(int B);
@@ -157,6 +158,11 @@ int astra_topk_merge(const uint64_t* part_keys, int64_t nq, int n_parts, int k_i
     return set_error(ASTRA_ERR_CONFIG, "merge workspace too small");
   return topk_merge(part_keys, nq, n_parts, k_in, k_out, out_keys, out_ids, out_scores,
                     static_cast<uint64_t*>(workspace), S(stream));
+}
+
+int astra_importance_split(const int32_t* ids, const float* scores, int64_t nq, int k_tot, int k_h, int32_t* hard,
+                           int32_t* cand, float* cand_q, void* stream) {
+  return importance_split(ids, scores, nq, k_tot, k_h, hard, cand, cand_q, S(stream));
 }
 
 int astra_sample_slates(uint64_t seed, uint32_t epoch, uint32_t step, const int64_t* rows, int B,

@@ -272,4 +272,41 @@ int sample_slates(uint64_t seed, uint32_t epoch, uint32_t step, const int64_t* r
   return ASTRA_OK;
 }
 
+// ------------------------------------------------------------- importance cache
+// The stale refresh of top-(k_h + n_c) per row (ids + fp32 scores, descending)
+// becomes the row's negative-mixture cache: the first k_h
+// ids are the hard set H, the next n_c the importance candidates C with
+// stored probability weights q_c = sigmoid(stale score_c) (the sampler
+// normalises them per row). Missing entries (id < 0: fewer labels than asked)
+// get q = 0 and are never drawn.
+__global__ void importance_split_kernel(const int32_t* ids, const float* scores, int64_t nq, int k_tot, int k_h,
+                                        int32_t* hard, int32_t* cand, float* cand_q) {
+  const int n_c = k_tot - k_h;
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nq * k_tot) return;
+  const int64_t r = i / k_tot;
+  const int j = static_cast<int>(i - r * k_tot);
+  const int32_t id = ids[i];
+  if (j < k_h) {
+    hard[r * k_h + j] = id;
+  } else {
+    const int c = j - k_h;
+    cand[r * n_c + c] = id;
+    cand_q[r * n_c + c] = id >= 0 ? 1.0f / (1.0f + expf(-scores[i])) : 0.0f;
+  }
+}
+
+int importance_split(const int32_t* ids, const float* scores, int64_t nq, int k_tot, int k_h, int32_t* hard,
+                     int32_t* cand, float* cand_q, cudaStream_t st) {
+  if (nq < 0 || k_h < 0 || k_tot < k_h) return set_error(ASTRA_ERR_CONFIG, "importance_split: bad sizes");
+  if (nq == 0 || k_tot == 0) return ASTRA_OK;
+  if (!ids || !scores || (k_h && !hard) || (k_tot > k_h && (!cand || !cand_q)))
+    return set_error(ASTRA_ERR_CONFIG, "importance_split: null buffer");
+  const int64_t n = nq * k_tot;
+  importance_split_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(ids, scores, nq, k_tot, k_h, hard,
+                                                                                   cand, cand_q);
+  ASTRA_LAUNCHED("importance_split");
+  return ASTRA_OK;
+}
+
 }  // namespace astra

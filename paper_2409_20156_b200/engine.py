@@ -41,19 +41,21 @@ def init_uniform_scaled(rows: int, dim: int, seed: int, device) -> torch.Tensor:
 
 
 class ClassifierEngine:
-    def __init__(self, n_labels: int, dim: int, *, k_p: int, k_h: int, k_r: int, k_i: int = 0,
+    def __init__(self, n_labels: int, dim: int, *, k_p: int, k_h: int, k_r: int, k_i: int = 0, n_c: int = 0,
                  weights=None, w_dtype=torch.float32, optimizer: str = "sgd", betas=(0.9, 0.999), eps=1e-8,
                  refresh_mode: str = "bf16_rerank", seed: int = 0, device=None, group=None, backend=None):
         if optimizer not in ("sgd", "adam"):
             raise ConfigError(f"unknown optimizer {optimizer!r}")
-        if k_p < 1 or k_h < 0 or k_r < 0 or k_i < 0:
-            raise ConfigError("need k_p >= 1, k_h >= 0, k_r >= 0, k_i >= 0")
+        if k_p < 1 or k_h < 0 or k_r < 0 or k_i < 0 or n_c < 0:
+            raise ConfigError("need k_p >= 1, k_h >= 0, k_r >= 0, k_i >= 0, n_c >= 0")
+        if k_i > 0 and n_c == 0:
+            raise ConfigError("importance draws (k_i > 0) need n_c > 0 candidates per row")
         self.ops = backend if backend is not None else cuda_ops
         self.comm = Comm(group)
         self.device = torch.device(device if device is not None else ("cuda" if torch.cuda.is_available() else "cpu"))
         self.n_labels, self.dim = int(n_labels), int(dim)
         self.lo, self.hi = shard_range(self.n_labels, self.comm.rank, self.comm.world)
-        self.k_p, self.k_h, self.k_r, self.k_i = k_p, k_h, k_r, k_i
+        self.k_p, self.k_h, self.k_r, self.k_i, self.n_c = k_p, k_h, k_r, k_i, n_c
         self.seed = seed
         self.refresh_mode = refresh_mode
         self.optimizer = optimizer
@@ -110,6 +112,20 @@ class ClassifierEngine:
         mine = self.comm.all_to_all(keys)  # [world, B, k]: shard i's keys for this rank's rows
         _, ids, scores = self.ops.topk_merge(mine, k)
         return ids, scores
+
+    def refresh_cache(self, queries: torch.Tensor, pos_indptr: torch.Tensor, pos_ids: torch.Tensor,
+                      mode: str | None = None):
+        """The negative-mixture cache rows of this rank's queries from one
+        stale refresh: (hard [B, k_h], cand [B, n_c],
+        cand_q [B, n_c]) — H = the top k_h, the importance candidates C = the
+        next n_c with stored draw weights sigmoid(stale score)
+        (astra_importance_split). Without the importance class (k_i == 0)
+        cand / cand_q are None and this is refresh(k_h)."""
+        if self.k_i == 0:
+            ids, _ = self.refresh(queries, pos_indptr, pos_ids, self.k_h, mode)
+            return ids, None, None
+        ids, scores = self.refresh(queries, pos_indptr, pos_ids, self.k_h + self.n_c, mode)
+        return self.ops.importance_split(ids, scores, self.k_h)
 
     # ------------------------------------------------------------ sampler
     def sample(self, rows, pos_indptr, pos_ids, hard, epoch: int, step: int, k_h: int | None = None,
@@ -185,7 +201,7 @@ class ClassifierEngine:
         return out
 
     def train_step_host(self, emb_h, rows_h, pos_indptr_h, pos_ids_h, hard_h, epoch, step, lr, weight_decay,
-                        out=None):
+                        out=None, cand_h=None, cand_q_h=None):
         """One training minibatch with HOST inputs: H2D (pinned) of embeddings /
         rows / positives / hard-cache rows, Philox slates, fused loss + update,
         D2H of grad_emb and the loss. On CUDA the H2D copies of call i+1 run on
@@ -195,7 +211,10 @@ class ClassifierEngine:
         if self.device.type != "cuda":
             dev = self.device
             hard = hard_h.to(dev) if hard_h is not None else None
-            slates = self.sample(rows_h.to(dev), pos_indptr_h.to(dev), pos_ids_h.to(dev), hard, epoch, step)
+            cand = cand_h.to(dev) if cand_h is not None else None
+            cand_q = cand_q_h.to(dev) if cand_q_h is not None else None
+            slates = self.sample(rows_h.to(dev), pos_indptr_h.to(dev), pos_ids_h.to(dev), hard, epoch, step,
+                                 cand=cand, cand_q=cand_q)
             loss, grad_emb, status = self.step(emb_h.to(dev), slates, lr, weight_decay)
             if out is None:
                 out = (torch.empty(grad_emb.shape, dtype=grad_emb.dtype), torch.empty(1, dtype=torch.float64))
@@ -203,8 +222,9 @@ class ClassifierEngine:
             out[1].copy_(loss)
             return out, status
         pipe = self._pipe("step")
-        d, slot = pipe.stage({"emb": emb_h, "rows": rows_h, "ip": pos_indptr_h, "pid": pos_ids_h, "hard": hard_h})
-        slates = self.sample(d["rows"], d["ip"], d["pid"], d["hard"], epoch, step)
+        d, slot = pipe.stage({"emb": emb_h, "rows": rows_h, "ip": pos_indptr_h, "pid": pos_ids_h, "hard": hard_h,
+                              "cand": cand_h, "cand_q": cand_q_h})
+        slates = self.sample(d["rows"], d["ip"], d["pid"], d["hard"], epoch, step, cand=d["cand"], cand_q=d["cand_q"])
         loss, grad_emb, status = self.step(d["emb"], slates, lr, weight_decay)
         pipe.release(slot)
         if out is None:

@@ -13,7 +13,9 @@ Rebinds the module globals the reference resolves at call time (SURVEY.md
         (trainer.py:27 imported the name, classifiers.py:71 uses the global)
   xcmix.anns.query_topk                        <- anns.query_topk
         (UpToDateHard, trainer.py:321-333; evaluation's anns mode)
-  xcmix.evaluation.predict_topk                <- evaluation.predict_topk (exact mode)
+  xcmix.evaluation.predict_topk / evaluate     <- evaluation.* (exact mode: batched MIPS)
+  xcmix.trainer._uptodate_hard_batch           <- trainer._uptodate_hard_batch (UpToDateHard,
+        trainer.py:321-333: one batched MIPS launch vs the live device W)
   xcmix.trainer._probe_full_loss / _eval_p_at  <- trainer.* (the dense per-epoch
         probes, trainer.py:398-423, resolved by train_epoch and the full-loss arm)
   xcmix.trainer.train_full_loss_baseline       <- trainer.train_full_loss_baseline
@@ -29,11 +31,16 @@ from . import _backend, anns, classifiers, evaluation, trainer
 _saved: dict = {}
 
 
-def install(backend=None, slates: str = "philox") -> None:
+def install(backend=None, slates: str = "philox", fast_step: bool | None = None) -> None:
+    """fast_step=True: the drop-in's classifier step takes the single
+    label-major pass (grad_emb summed in arrival order: not bitwise
+    run-to-run reproducible); default: the deterministic schedule."""
     import xcmix.anns as xa
     import xcmix.classifiers as xc
     import xcmix.trainer as xt
 
+    if fast_step is not None:
+        trainer.FAST_STEP = bool(fast_step)
     if slates not in ("philox", "reference"):
         raise ValueError("slates must be 'philox' or 'reference'")
     if backend is not None:
@@ -45,10 +52,12 @@ def install(backend=None, slates: str = "philox") -> None:
     if not _saved:
         if xe is not None:
             _saved[(xe, "predict_topk")] = xe.predict_topk
+            _saved[(xe, "evaluate")] = xe.evaluate
         _saved.update({
             (xa, "query_topk"): xa.query_topk,
             (xa, "retrieve_hard_negatives"): xa.retrieve_hard_negatives,
             (xt, "_batch_forward_backward"): xt._batch_forward_backward,
+            (xt, "_uptodate_hard_batch"): xt._uptodate_hard_batch,
             (xt, "_assemble_batch_slates"): xt._assemble_batch_slates,
             (xt, "apply_classifier_updates_arrays"): xt.apply_classifier_updates_arrays,
             (xt, "_probe_full_loss"): xt._probe_full_loss,
@@ -62,8 +71,11 @@ def install(backend=None, slates: str = "philox") -> None:
     xa.query_topk = anns.query_topk
     if xe is not None:
         evaluation._reference_predict = _saved[(xe, "predict_topk")]
+        evaluation._reference_evaluate = _saved[(xe, "evaluate")]
         xe.predict_topk = evaluation.predict_topk
+        xe.evaluate = evaluation.evaluate
     xt._batch_forward_backward = trainer._batch_forward_backward
+    xt._uptodate_hard_batch = trainer._uptodate_hard_batch
     xt._assemble_batch_slates = (trainer._assemble_batch_slates if slates == "philox"
                                  else _saved[(xt, "_assemble_batch_slates")])
     xt.apply_classifier_updates_arrays = classifiers.apply_classifier_updates_arrays
@@ -80,3 +92,4 @@ def uninstall() -> None:
     anns._approx_impl = None
     anns._approx_query_impl = None
     evaluation._reference_predict = None
+    evaluation._reference_evaluate = None

@@ -132,6 +132,24 @@ def topk_merge(part_keys: torch.Tensor, k_out: int):
     return keys, ids, scores
 
 
+def importance_split(ids, scores, k_h):
+    """(hard [nq, k_h], cand [nq, n_c], cand_q [nq, n_c]) from a refresh of
+    top-(k_h + n_c) per row: H, the importance candidates C and their stored
+    draw weights sigmoid(stale score) (astra_importance_split)."""
+    _cuda(ids, torch.int32, "ids")
+    _cuda(scores, torch.float32, "scores")
+    nq, k_tot = ids.shape
+    if not 0 <= k_h <= k_tot:
+        raise ConfigError(f"importance_split: k_h={k_h} outside [0, {k_tot}]")
+    dev = ids.device
+    hard = torch.empty((nq, k_h), dtype=torch.int32, device=dev)
+    cand = torch.empty((nq, k_tot - k_h), dtype=torch.int32, device=dev)
+    cand_q = torch.empty((nq, k_tot - k_h), dtype=torch.float32, device=dev)
+    _lib.check(_lib.load().astra_importance_split(_p(ids), _p(scores), nq, k_tot, k_h, _p(hard), _p(cand), _p(cand_q),
+                                                  _stream()))
+    return hard, cand, cand_q
+
+
 def sample_slates(seed, epoch, step, rows, pos_indptr, pos_ids, hard, k_h, n_labels, k_p, k_r,
                   cand=None, cand_q=None, k_i=0):
     """Philox negative-mixture slates: (ids int32, y int8, origin int8, weights fp32), B x S."""

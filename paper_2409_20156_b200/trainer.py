@@ -90,6 +90,34 @@ def _assemble_batch_slates(state, batch_rows, epoch, rng, hard_batch):
             weights[0].cpu().numpy())
 
 
+def _uptodate_hard_batch(state, batch_rows, embeddings, epoch):
+    """UpToDateHard (trainer.py:321-333): per row, the top k_h_eff labels of
+    the CURRENT classifier by exact inner product, positives dropped, ties to
+    the lower id. The reference builds a fresh exact index from a host copy
+    of W and runs one query per row; here it is one batched fp32-exact MIPS
+    launch over the batch against the live device weights (no snapshot, no
+    upload). Counters follow the reference (index_queries += rows); no
+    host-side live_index is built."""
+    k_h_eff, _ = curriculum_counts(epoch, state.strategy, state.config.tau_s)
+    rows = np.asarray(batch_rows, dtype=np.int64)
+    out = np.empty((len(rows), k_h_eff), dtype=np.int64)
+    if k_h_eff == 0 or len(rows) == 0:
+        return out
+    positives = [state.dataset.positives[i] for i in rows]
+    W = DeviceBank.attach(state.bank).W
+    if k_h_eff + max(len(p) for p in positives) > W.shape[0]:
+        raise ConfigError("k_h plus the positive count exceeds the label count")
+    state.caches.index_queries += len(rows)
+    indptr, ids = _csr(positives)
+    dev = W.device
+    ops = _backend.get()
+    _, top, _ = ops.refresh_topk(torch.from_numpy(np.ascontiguousarray(embeddings, dtype=np.float32)).to(dev),
+                                 torch.from_numpy(indptr).to(dev), torch.from_numpy(ids).to(dev), k_h_eff, "fp32",
+                                 labels_f32=W)
+    out[:] = top.cpu().numpy()
+    return out
+
+
 def _batch_forward_backward(state, batch_rows, epoch, rng, step_lr_enc, step_lr_clf, feats=None):
     """One mini-batch update; returns the summed slate loss (trainer.py:336-395)."""
     import xcmix.trainer as xt  # the caller's module: encoder, slates, UpToDate arm

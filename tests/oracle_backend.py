@@ -140,3 +140,10 @@ def dense_probe_loss(emb, W, pos_indptr, pos_ids):
     e = _np(emb)
     mask = _dense_y_from_csr(pos_indptr, pos_ids, e.shape[0], W.shape[0]).astype(bool)
     return torch.tensor([port.probe_full_loss(e, _np(W), mask)], dtype=torch.float64)
+
+
+def importance_split(ids, scores, k_h):
+    i, sc = _np(ids), _np(scores).astype(np.float32)
+    q = np.where(i[:, k_h:] >= 0, (np.float32(1.0) / (np.float32(1.0) + np.exp(-sc[:, k_h:]))), 0.0).astype(np.float32)
+    return (torch.from_numpy(np.ascontiguousarray(i[:, :k_h])), torch.from_numpy(np.ascontiguousarray(i[:, k_h:])),
+            torch.from_numpy(q))
