@@ -632,7 +632,7 @@ def run_c5shard(args):
         pid = pos.to(torch.int32).reshape(-1).contiguous()
         emb = torch.randn((B, d), device="cuda", generator=g)
         data.append([rows, ip, pid, emb, None])
-    data[0][4] = cache_of(*data[0][1:4])  # the first step's stale cache
+    data[0][4] = cache_of(data[0][3], data[0][1], data[0][2])  # the first step's stale cache
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_steps)]

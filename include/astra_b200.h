@@ -76,7 +76,9 @@ uint64_t astra_launch_count(void);
  * a CUDA event pair on the launching stream around each launch of the named
  * kernels: "refresh_gemm" (the fused tcgen05 GEMM + selection pass that scores
  * every label: the threshold pass, or the single running-top-k pass),
- * "slot_forward" and "label_update" (the step). astra_kernel_timing syncs the
+ * "refresh_verify" (the two-pass plan's exact fallback pass), "step_single"
+ * (the single label-major step pass), "slot_forward" and "label_update" (the
+ * two-kernel step schedule). astra_kernel_timing syncs the
  * pairs recorded under `name`, returns their summed milliseconds and count,
  * and clears them. Not a reference interface (measurement only). */
 void astra_kernel_timing_enable(int on);
@@ -209,11 +211,15 @@ int astra_importance_split(const int32_t* ids, const float* scores, int64_t nq, 
  *   factors_out B x S fp32 out (d(loss)/d(score) per slot) or NULL
  *   w_absmax   1 fp32 in/out or NULL: a running upper bound on max|W| of this
  *              shard, kept current by the call (every updated row folds its
- *              new |values| in). With it, the call can prove up front that
- *              no gradient and no grad_emb entry can overflow, and then runs
- *              the L2-chunked fused step (gather of chunk p + update of chunk
- *              p-1 per phase of one persistent kernel); without it, or when
- *              the proof fails, it runs the two-pass schedule.
+ *              new |values| in). With it (SGD, d % 128 == 0, d <= 768, 16-byte
+ *              aligned emb/W/grad_emb, astra_set_step_deterministic(0)), the
+ *              call proves on the device that no gradient and no grad_emb
+ *              entry can overflow and runs the single label-major pass
+ *              (each touched row read and written once; grad_emb reduced in
+ *              arrival order); without it, or when the proof fails, it runs
+ *              the deterministic two-kernel schedule (slot-major gather
+ *              forward, then the label-major update), which is also the Adam
+ *              schedule. The schedule kernels not taken return at once.
  *   lr, weight_decay, betas, eps are host doubles: SGD rounds lr/wd to fp32
  *   like np.float32(lr) (classifiers.py:82); Adam derives its step size in
  *   double like torch.optim.SparseAdam.

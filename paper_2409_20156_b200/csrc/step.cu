@@ -2,23 +2,30 @@
 //
 // Replaces the classifier half of _batch_forward_backward
 // (trainer.py:366-394) and apply_classifier_updates_arrays
-// (classifiers.py:75-82). HBM-bound; the pipeline is
+// (classifiers.py:75-82). HBM-bound. Per minibatch:
 //
-//   1. slot_forward   (CTA per batch row)  gather W[ids[b,s]] with 16 B vector
-//                     loads, warp-reduce dot, BCE loss terms (fp64), factors
-//                     c*(sigma-y) (trainer.py:369-380), grad_emb[b] reduced
-//                     across warps in a fixed order (trainer.py:382-384).
-//   2. finalize       fixed-order fp64 loss sum + overflow bound.
-//   3. count/scan/scatter  counting sort of the B*S slots by label
-//                     (replaces the dense L x d A^T@emb, trainer.py:390-393).
-//   4. label_update   (warp per unique label) sum f*emb in ascending b*S+s
-//                     order with separate mul/add roundings — the order scipy's
-//                     csc_matvecs uses — then the SGD/Adam row update, W read
+//   count/scan/scatter  counting sort of the B*S slots by local label
+//                     (replaces the dense L x d A^T@emb, trainer.py:390-393);
+//                     count also accumulates the finiteness bounds and
+//                     scan_top decides the schedule on the device.
+//   step_single_tma   (default for SGD, d % 128 == 0) ONE label-major pass:
+//                     per unique label, the old row is bulk-copied once; every
+//                     occurrence's score, loss term, factor, grad_emb[b] +=
+//                     f * W_old (vector reductions) and g += f * emb_b; then
+//                     the SGD/Adam row update and store: each touched row read
 //                     and written once.
+//   two-kernel schedule (deterministic / Adam / when the bound proof fails):
+//     slot_forward    (CTA per batch row) gather W[ids[b,s]], dot, BCE loss
+//                     terms (fp64), factors c*(sigma-y) (trainer.py:369-380),
+//                     grad_emb[b] in a fixed order (trainer.py:382-384);
+//     finalize        fixed-order fp64 loss sum + overflow bound;
+//     label_update    (per unique label) sum f*emb in ascending b*S+s order
+//                     with separate mul/add roundings — scipy's csc_matvecs
+//                     order — then the SGD/Adam row update.
 // W is written only if every touched gradient and grad_emb is finite: the
 // reference raises NumericalError before writing (classifiers.py:79-80,
-// encoder.py:145-146). Step 2 proves finiteness from a bound in the common
-// case; otherwise a check pass (label_check) runs first.
+// encoder.py:145-146): the single pass proves it from bounds up front; the
+// two-kernel schedule checks first (label_check) when its bound trips.
 #include <atomic>
 #include <limits.h>
 #include <math.h>
@@ -89,24 +96,6 @@ __device__ __forceinline__ float slot_factor(const FwdArgs& a, int b, int s, flo
   return __fadd_rn(__fmul_rn(pos_term, __fsub_rn(sig, 1.0f)), __fmul_rn(wn, sig));
 }
 
-// slot_factor split in two for the TMA kernel: the factor (needed at once by
-// every lane), and the fp64 loss term, evaluated later lane-parallel for 32
-// slots at a time (one softplus per lane instead of one per slot per lane).
-__device__ __forceinline__ float slot_factor_only(const FwdArgs& a, int b, int s, float sc, float* pos_term_out,
-                                                  float* wn_out) {
-  const int8_t o = a.origin[b * a.origin_stride + s];
-  const float yf = static_cast<float>(a.y[static_cast<size_t>(b) * a.S + s]);
-  const float w = a.weights[b * a.weights_stride + s];
-  const bool pos_slot = o == ASTRA_ORIGIN_POS;
-  const float pos_term = pos_slot ? yf : 0.0f;
-  const float neg_alive = pos_slot ? 0.0f : __fsub_rn(1.0f, yf);
-  const float sig = expit_f32(sc);
-  const float wn = __fmul_rn(w, neg_alive);
-  *pos_term_out = pos_term;
-  *wn_out = wn;
-  return __fadd_rn(__fmul_rn(pos_term, __fsub_rn(sig, 1.0f)), __fmul_rn(wn, sig));
-}
-
 // The slot's (origin, y, weight), loaded ahead of its W row so that these
 // L2 loads overlap the row's arrival instead of following it.
 struct SlotMeta {
@@ -122,7 +111,8 @@ __device__ __forceinline__ SlotMeta slot_meta(const FwdArgs& a, int b, int s) {
   return m;
 }
 
-// slot_factor_only from prefetched metadata (same arithmetic).
+// The factor (needed at once by every lane) from prefetched metadata; the fp64
+// loss term is evaluated later, lane-parallel for 32 slots at a time.
 __device__ __forceinline__ float slot_factor_meta(const SlotMeta& m, float sc, float* pos_term_out, float* wn_out) {
   const bool pos_slot = m.o == ASTRA_ORIGIN_POS;
   const float pos_term = pos_slot ? m.yf : 0.0f;
@@ -181,89 +171,6 @@ __device__ void forward_tail(const FwdArgs& a, int b, float* red, double lsum, d
     a.loss_rows[b] = l;
     a.bound_rows[b] = fa * static_cast<double>(emax);
   }
-}
-
-// Vectorised forward: d = NV * 128, each lane owns NV float4 of the row.
-template <int NV, bool BF16>
-__global__ void __launch_bounds__(kFwdThreads, 1) slot_forward_vec(FwdArgs a) {
-  if (a.skip && *a.skip) return;
-  __shared__ __align__(16) float red[kFwdWarps * NV * 128];
-  __shared__ float s_emax[kFwdWarps];
-  const int b = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int d = NV * 128;
-  float4 e[NV], g[NV];
-  float emax = 0.0f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    e[i] = *reinterpret_cast<const float4*>(a.emb + static_cast<size_t>(b) * d + i * 128 + lane * 4);
-    g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    emax = fmaxf(emax, fmaxf(fmaxf(fabsf(e[i].x), fabsf(e[i].y)), fmaxf(fabsf(e[i].z), fabsf(e[i].w))));
-    if (!(isfinite(e[i].x) && isfinite(e[i].y) && isfinite(e[i].z) && isfinite(e[i].w))) emax = INFINITY;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-  double lsum = 0.0, fabs_sum = 0.0;
-  const int32_t* row_ids = a.ids + static_cast<size_t>(b) * a.S;
-  // UNR slots in flight per warp for memory-level parallelism (HBM latency x BW per SM)
-  constexpr int UNR = NV <= 2 ? 8 : (NV <= 4 ? 6 : 4);
-  for (int s0 = warp * UNR; s0 < a.S; s0 += kFwdWarps * UNR) {
-    int64_t loc[UNR];
-    bool own[UNR];
-    float4 w[UNR][NV];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int sl = s0 + u;
-      own[u] = false;
-      loc[u] = 0;
-      if (sl < a.S) {
-        loc[u] = static_cast<int64_t>(row_ids[sl]) - a.off;
-        own[u] = loc[u] >= 0 && loc[u] < a.Lloc;
-      }
-      if (own[u]) {
-#pragma unroll
-        for (int i = 0; i < NV; ++i) w[u][i] = load_w4<BF16>(a.W, static_cast<size_t>(loc[u]) * d + i * 128 + lane * 4);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      if (!own[u]) continue;  // warp-uniform
-      const int sl = s0 + u;
-      float f;
-      if (a.factors_in) {
-        f = a.factors_in[static_cast<size_t>(b) * a.S + sl];
-      } else {
-        float acc = 0.0f;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          acc = fmaf(w[u][i].x, e[i].x, acc);
-          acc = fmaf(w[u][i].y, e[i].y, acc);
-          acc = fmaf(w[u][i].z, e[i].z, acc);
-          acc = fmaf(w[u][i].w, e[i].w, acc);
-        }
-        acc = warp_sum(acc);
-        double lt;
-        f = slot_factor(a, b, sl, acc, &lt);
-        if (lane == 0) lsum += lt;
-      }
-      if (lane == 0) {
-        fabs_sum += static_cast<double>(fabsf(f));
-        if (a.factors) a.factors[static_cast<size_t>(b) * a.S + sl] = f;
-      }
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        g[i].x = fmaf(f, w[u][i].x, g[i].x);
-        g[i].y = fmaf(f, w[u][i].y, g[i].y);
-        g[i].z = fmaf(f, w[u][i].z, g[i].z);
-        g[i].w = fmaf(f, w[u][i].w, g[i].w);
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < NV; ++i) *reinterpret_cast<float4*>(red + warp * d + i * 128 + lane * 4) = g[i];
-  if (lane == 0) s_emax[warp] = emax;
-  __syncthreads();
-  forward_tail(a, b, red, lsum, fabs_sum, s_emax[0]);
 }
 
 // TMA-fed forward (the default for d % 128 == 0): CTA per batch row; one
@@ -636,7 +543,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_
 // (mode != null: also decides the step schedule from count_kernel's bounds.)
 __global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* blk_slots, uint32_t* blk_nz, int nb,
                                                         uint32_t* U, const double* sf_acc, const unsigned* emax_acc,
-                                                        const float* w_absmax, int32_t* mode) {
+                                                        const float* w_absmax, int32_t* mode, int d) {
   __shared__ uint32_t cs[1024], cn[1024];
   const int per = (nb + 1023) / 1024;
   const int lo = threadIdx.x * per, hi = min(nb, lo + per);
@@ -669,8 +576,12 @@ __global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* blk_slots, uin
     const double SF = *sf_acc;
     const float EM = __uint_as_float(*emax_acc);
     const float WM = w_absmax ? *w_absmax : INFINITY;
+    // every gradient entry <= SF * EM, every grad_emb entry <= SF * WM, and
+    // every partial sum of a score's dot product <= d * EM * WM (no fp32
+    // overflow -> inf - inf = NaN in a score, which no later check would see)
     *mode = isfinite(SF) && isfinite(EM) && isfinite(WM) && SF * static_cast<double>(EM) < kSingleSafe &&
-            SF * static_cast<double>(WM) < kSingleSafe;
+            SF * static_cast<double>(WM) < kSingleSafe &&
+            static_cast<double>(d) * static_cast<double>(EM) * static_cast<double>(WM) < kSingleSafe;
   }
 }
 
@@ -900,111 +811,12 @@ __global__ void __launch_bounds__(kUpdThreads) label_update_kernel(UpdArgs a) {
   if (!CHECK_ONLY) push_wmax(a, wmax, lane);
 }
 
-// Vectorised update for d % 128 == 0 (NV float4 per lane), fp32 or bf16 W.
-template <int NV, bool BF16, bool ADAM>
-__global__ void __launch_bounds__(kUpdThreads) label_update_vec(UpdArgs a) {
-  if (a.skip && *a.skip) return;
-  const int lane = threadIdx.x & 31;
-  if (a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] || a.status[ASTRA_STATUS_NONFINITE_GRAD]) return;
-  const uint32_t U = *a.U;
-  constexpr int d = NV * 128;
-  const uint32_t warps = gridDim.x * (kUpdThreads / 32);
-  float wmax = 0.0f;
-  for (uint32_t u = blockIdx.x * (kUpdThreads / 32) + (threadIdx.x >> 5); u < U; u += warps) {
-    const int32_t l = a.uniq[u];
-    const uint32_t start = a.offsets[l], n = a.counts[l];
-    const int32_t reg = sort_segment(a, start, n, lane);
-    const size_t row = static_cast<size_t>(l) * d;
-    // issue the row loads first; they overlap the gradient accumulation
-    float4 p[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      if constexpr (BF16) {
-        uint2 q = *reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(a.W) + row + i * 128 + lane * 4);
-        p[i] = make_float4(__uint_as_float(q.x << 16), __uint_as_float(q.x & 0xFFFF0000u),
-                           __uint_as_float(q.y << 16), __uint_as_float(q.y & 0xFFFF0000u));
-      } else {
-        p[i] = *reinterpret_cast<const float4*>(static_cast<const float*>(a.W) + row + i * 128 + lane * 4);
-      }
-    }
-    float4 g[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t j = 0;
-    for (; j + 2 <= n; j += 2) {  // two occurrences' loads in flight, summed in order
-      int32_t s0 = seg_slot(a, start, n, reg, j), s1 = seg_slot(a, start, n, reg, j + 1);
-      float f0 = a.factors[s0], f1 = a.factors[s1];
-      const float* e0 = a.emb + static_cast<size_t>(s0 / a.S) * d + lane * 4;
-      const float* e1 = a.emb + static_cast<size_t>(s1 / a.S) * d + lane * 4;
-      float4 x0[NV], x1[NV];
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        x0[i] = *reinterpret_cast<const float4*>(e0 + i * 128);
-        x1[i] = *reinterpret_cast<const float4*>(e1 + i * 128);
-      }
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        g[i].x = __fadd_rn(g[i].x, __fmul_rn(f0, x0[i].x));
-        g[i].y = __fadd_rn(g[i].y, __fmul_rn(f0, x0[i].y));
-        g[i].z = __fadd_rn(g[i].z, __fmul_rn(f0, x0[i].z));
-        g[i].w = __fadd_rn(g[i].w, __fmul_rn(f0, x0[i].w));
-        g[i].x = __fadd_rn(g[i].x, __fmul_rn(f1, x1[i].x));
-        g[i].y = __fadd_rn(g[i].y, __fmul_rn(f1, x1[i].y));
-        g[i].z = __fadd_rn(g[i].z, __fmul_rn(f1, x1[i].z));
-        g[i].w = __fadd_rn(g[i].w, __fmul_rn(f1, x1[i].w));
-      }
-    }
-    if (j < n) {
-      int32_t s0 = seg_slot(a, start, n, reg, j);
-      float f0 = a.factors[s0];
-      const float* e0 = a.emb + static_cast<size_t>(s0 / a.S) * d + lane * 4;
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        float4 x0 = *reinterpret_cast<const float4*>(e0 + i * 128);
-        g[i].x = __fadd_rn(g[i].x, __fmul_rn(f0, x0.x));
-        g[i].y = __fadd_rn(g[i].y, __fmul_rn(f0, x0.y));
-        g[i].z = __fadd_rn(g[i].z, __fmul_rn(f0, x0.z));
-        g[i].w = __fadd_rn(g[i].w, __fmul_rn(f0, x0.w));
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const size_t el = row + i * 128 + lane * 4;
-      float4 np;
-      if constexpr (ADAM) {
-        float4 m4 = *reinterpret_cast<float4*>(a.m + el), v4 = *reinterpret_cast<float4*>(a.v + el);
-        np.x = upd_elem<true>(a, p[i].x, g[i].x, &m4.x, &v4.x);
-        np.y = upd_elem<true>(a, p[i].y, g[i].y, &m4.y, &v4.y);
-        np.z = upd_elem<true>(a, p[i].z, g[i].z, &m4.z, &v4.z);
-        np.w = upd_elem<true>(a, p[i].w, g[i].w, &m4.w, &v4.w);
-        *reinterpret_cast<float4*>(a.m + el) = m4;
-        *reinterpret_cast<float4*>(a.v + el) = v4;
-      } else {
-        np.x = upd_elem<false>(a, p[i].x, g[i].x, nullptr, nullptr);
-        np.y = upd_elem<false>(a, p[i].y, g[i].y, nullptr, nullptr);
-        np.z = upd_elem<false>(a, p[i].z, g[i].z, nullptr, nullptr);
-        np.w = upd_elem<false>(a, p[i].w, g[i].w, nullptr, nullptr);
-      }
-      if constexpr (BF16) {
-        uint2 q;
-        q.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
-        q.y = static_cast<uint32_t>(f32_to_bf16_bits(np.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.w)) << 16);
-        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(a.W) + el) = q;
-      } else {
-        *reinterpret_cast<float4*>(static_cast<float*>(a.W) + el) = np;
-      }
-      wmax = fmaxf(wmax, absmax4(np));
-    }
-  }
-  push_wmax(a, wmax, lane);
-}
-
 // TMA-fed SGD update (the default for d % 128 == 0): each CTA owns a
 // contiguous chunk of the sorted unique-label list; one producer lane streams
 // the chunk's W rows into a shared-memory ring with bulk copies while four
 // consumer warps (warp w: the chunk's labels w, w+4, ...) sum the label's
 // gradient from the L2-resident embeddings (same ascending-slot order and
-// roundings as label_update_vec), then take the row from the ring, apply the
+// roundings as label_update_kernel), then take the row from the ring, apply the
 // update and store it. W is read and written once per touched row.
 // Ring geometry of the update: one entry = the W row (+ the Adam m and v rows).
 template <int NV, bool BF16, bool ADAM>
@@ -1694,950 +1506,6 @@ void launch_single_nv(int nv, const SingleArgs& A, cudaStream_t st) {
   }
 }
 
-// ================================================================ fused step
-// One persistent cooperative kernel per minibatch that keeps the rows it
-// gathers L2-resident until they are updated: the label range is cut into C
-// chunks whose touched rows (~24 MB) fit in L2 with room to spare, and phase p
-// runs the forward (gather, scores, factors, loss, grad_emb) of every slot whose
-// label lies in chunk p AND the update of chunk p-1 (rows gathered in the
-// previous phase: L2 hits), separated by grid barriers. DRAM then sees each
-// touched row read once and written once, the formula's minimum.
-//
-// Determinism is unchanged: a warp owns one batch row and accumulates its
-// grad_emb in registers over (chunk asc, slot asc); labels sum their gradient
-// in ascending b*S+s order as label_update does.
-// Finiteness (classifiers.py:79-80, encoder.py:145-146: nothing is written when
-// a gradient is non-finite) is proven up front from bounds: with
-// S_f = sum over owned slots of (1 + |weight|) >= sum |factor|, every label
-// gradient is <= S_f * max|emb| and every grad_emb entry <= S_f * max|W|
-// (max|W| a running bound kept by the caller, updated here). Without the proof
-// (or without the bound) the same kernel runs the two-pass schedule: all
-// forwards, a check of every gradient, then the updates.
-
-constexpr int kFusedWarps = 8;
-constexpr int kFusedThreads = 32 * kFusedWarps;
-constexpr int kMaxChunks = 127;
-constexpr double kFusedSafe = 1e30;
-
-struct FusedArgs {
-  FwdArgs f;
-  UpdArgs u;
-  int C;
-  int64_t Lc;
-  const uint32_t* uc;        // [C+1] bounds of chunk c in uniq
-  const int32_t* row_slots;  // [B][S] owned slots of row b, by (chunk, slot)
-  const int32_t* row_locs;   // [B][S] their local W rows
-  const int32_t* row_cofs;   // [B][C+1] offsets into row_slots
-  float* w_absmax;           // running max|W| bound (in/out) or null
-  unsigned* bar;             // grid barrier counter (zeroed before launch)
-  double* sf_acc;            // sum over owned slots of (1 + |weight|)
-  unsigned* emax_acc;        // max|emb| (float bits; +inf if non-finite)
-};
-
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    unsigned v;
-    while (true) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-      if (v >= target) break;
-      __nanosleep(64);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// Forward of row b's owned slots [j0, j1) of row_slots (UNR rows in flight).
-template <int NV, bool BF16>
-__device__ __forceinline__ void fused_fwd(const FusedArgs& A, int b, int j0, int j1, const float4 (&e)[NV],
-                                          float4 (&g)[NV], double& lsum, double& fabs_sum, float& pend_sc,
-                                          float& pend_pt, float& pend_wn, int& c_pend, int lane) {
-  const FwdArgs& a = A.f;
-  constexpr int d = NV * 128;
-  constexpr int UNR = NV <= 4 ? 8 : 4;
-  const int32_t* rs = A.row_slots + static_cast<size_t>(b) * a.S;
-  const int32_t* rl = A.row_locs + static_cast<size_t>(b) * a.S;
-  for (int j = j0; j < j1; j += UNR) {
-    int sl[UNR];
-    float4 w[UNR][NV];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      sl[u] = j + u < j1 ? rs[j + u] : -1;
-      if (sl[u] >= 0) {
-        const int64_t loc = rl[j + u];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) w[u][i] = load_w4<BF16>(a.W, static_cast<size_t>(loc) * d + i * 128 + lane * 4);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      if (sl[u] < 0) continue;  // warp-uniform
-      float acc = 0.0f;
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        acc = fmaf(w[u][i].x, e[i].x, acc);
-        acc = fmaf(w[u][i].y, e[i].y, acc);
-        acc = fmaf(w[u][i].z, e[i].z, acc);
-        acc = fmaf(w[u][i].w, e[i].w, acc);
-      }
-      acc = warp_sum(acc);
-      float pt, wn;
-      const float f = slot_factor_only(a, b, sl[u], acc, &pt, &wn);
-      if (lane == c_pend) {
-        pend_sc = acc;
-        pend_pt = pt;
-        pend_wn = wn;
-      }
-      if (++c_pend == 32) {
-        lsum += slot_loss(pend_sc, pend_pt, pend_wn);
-        c_pend = 0;
-      }
-      if (lane == 0) {
-        __stcg(a.factors + static_cast<size_t>(b) * a.S + sl[u], f);
-        fabs_sum += static_cast<double>(fabsf(f));
-      }
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        g[i].x = fmaf(f, w[u][i].x, g[i].x);
-        g[i].y = fmaf(f, w[u][i].y, g[i].y);
-        g[i].z = fmaf(f, w[u][i].z, g[i].z);
-        g[i].w = fmaf(f, w[u][i].w, g[i].w);
-      }
-    }
-  }
-}
-
-// Gradient of unique label index uq (ascending b*S+s order, separate roundings
-// as label_update), then (unless CHECK) the SGD / Adam update of its row.
-// Returns false if a gradient entry is non-finite. wmax tracks max|W new|.
-template <int NV, bool BF16, bool ADAM, bool CHECK>
-__device__ __forceinline__ bool fused_upd(const UpdArgs& a, uint32_t uq, float& wmax, int lane) {
-  constexpr int d = NV * 128;
-  const int32_t l = a.uniq[uq];
-  const uint32_t start = a.offsets[l], n = a.counts[l];
-  const int32_t reg = sort_segment(a, start, n, lane);
-  const size_t row = static_cast<size_t>(l) * d;
-  float4 p[NV];
-  if constexpr (!CHECK) {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      if constexpr (BF16) {
-        const uint2 q = __ldcg(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(a.W) + row + i * 128 + lane * 4));
-        p[i] = make_float4(__uint_as_float(q.x << 16), __uint_as_float(q.x & 0xFFFF0000u),
-                           __uint_as_float(q.y << 16), __uint_as_float(q.y & 0xFFFF0000u));
-      } else {
-        p[i] = __ldcg(reinterpret_cast<const float4*>(static_cast<const float*>(a.W) + row + i * 128 + lane * 4));
-      }
-    }
-  }
-  float4 g[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (uint32_t j = 0; j < n; ++j) {
-    const int32_t s0 = seg_slot(a, start, n, reg, j);
-    const float f0 = __ldcg(a.factors + s0);
-    const float* e0 = a.emb + static_cast<size_t>(s0 / a.S) * d + lane * 4;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const float4 x0 = *reinterpret_cast<const float4*>(e0 + i * 128);
-      g[i].x = __fadd_rn(g[i].x, __fmul_rn(f0, x0.x));
-      g[i].y = __fadd_rn(g[i].y, __fmul_rn(f0, x0.y));
-      g[i].z = __fadd_rn(g[i].z, __fmul_rn(f0, x0.z));
-      g[i].w = __fadd_rn(g[i].w, __fmul_rn(f0, x0.w));
-    }
-  }
-  if constexpr (CHECK) {
-    bool bad = false;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) bad |= !(isfinite(g[i].x) && isfinite(g[i].y) && isfinite(g[i].z) && isfinite(g[i].w));
-    return !__any_sync(0xffffffffu, bad);
-  } else {
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const size_t el = row + i * 128 + lane * 4;
-    float4 np;
-    if constexpr (ADAM) {
-      float4 m4 = *reinterpret_cast<float4*>(a.m + el), v4 = *reinterpret_cast<float4*>(a.v + el);
-      np.x = upd_elem<true>(a, p[i].x, g[i].x, &m4.x, &v4.x);
-      np.y = upd_elem<true>(a, p[i].y, g[i].y, &m4.y, &v4.y);
-      np.z = upd_elem<true>(a, p[i].z, g[i].z, &m4.z, &v4.z);
-      np.w = upd_elem<true>(a, p[i].w, g[i].w, &m4.w, &v4.w);
-      *reinterpret_cast<float4*>(a.m + el) = m4;
-      *reinterpret_cast<float4*>(a.v + el) = v4;
-    } else {
-      np.x = upd_elem<false>(a, p[i].x, g[i].x, nullptr, nullptr);
-      np.y = upd_elem<false>(a, p[i].y, g[i].y, nullptr, nullptr);
-      np.z = upd_elem<false>(a, p[i].z, g[i].z, nullptr, nullptr);
-      np.w = upd_elem<false>(a, p[i].w, g[i].w, nullptr, nullptr);
-    }
-    if constexpr (BF16) {
-      uint2 q;
-      q.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
-      q.y = static_cast<uint32_t>(f32_to_bf16_bits(np.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.w)) << 16);
-      *reinterpret_cast<uint2*>(static_cast<uint16_t*>(a.W) + el) = q;
-      np = make_float4(bf16_bits_to_f32(static_cast<uint16_t>(q.x)), bf16_bits_to_f32(static_cast<uint16_t>(q.x >> 16)),
-                       bf16_bits_to_f32(static_cast<uint16_t>(q.y)), bf16_bits_to_f32(static_cast<uint16_t>(q.y >> 16)));
-    } else {
-      *reinterpret_cast<float4*>(static_cast<float*>(a.W) + el) = np;
-    }
-    wmax = fmaxf(wmax, fmaxf(fmaxf(fabsf(np.x), fabsf(np.y)), fmaxf(fabsf(np.z), fabsf(np.w))));
-  }
-  return true;
-  }
-}
-
-template <int NV, bool BF16, bool ADAM>
-__global__ void __launch_bounds__(kFusedThreads, 1) step_fused_kernel(FusedArgs A) {
-  const FwdArgs& a = A.f;
-  constexpr int d = NV * 128;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t NW = static_cast<int64_t>(gridDim.x) * kFusedWarps;
-  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kFusedWarps + warp;
-  const int b = static_cast<int>(gw);
-  const bool has_row = gw < a.B;
-  unsigned gen = 0;
-  __shared__ double s_sf[kFusedWarps];
-  __shared__ float s_em[kFusedWarps];
-
-  // ---- phase 0: the finiteness bounds
-  float4 e[NV];
-  float emax = 0.0f;
-  double sf = 0.0;
-  if (has_row) {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      e[i] = *reinterpret_cast<const float4*>(a.emb + static_cast<size_t>(b) * d + i * 128 + lane * 4);
-      emax = fmaxf(emax, fmaxf(fmaxf(fabsf(e[i].x), fabsf(e[i].y)), fmaxf(fabsf(e[i].z), fabsf(e[i].w))));
-      if (!(isfinite(e[i].x) && isfinite(e[i].y) && isfinite(e[i].z) && isfinite(e[i].w))) emax = INFINITY;
-    }
-    const int j1 = A.row_cofs[static_cast<size_t>(b) * (A.C + 1) + A.C];
-    const int32_t* rs = A.row_slots + static_cast<size_t>(b) * a.S;
-    for (int j = lane; j < j1; j += 32) {
-      const float wt = a.weights[b * a.weights_stride + rs[j]];
-      sf += 1.0 + (isfinite(wt) ? fabs(static_cast<double>(wt)) : INFINITY);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-  const float row_emax = emax;
-  sf = warp_sum(sf);
-  if (lane == 0) {
-    s_sf[warp] = sf;
-    s_em[warp] = emax;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    float m = 0.0f;
-    for (int w = 0; w < kFusedWarps; ++w) {
-      t += s_sf[w];
-      m = fmaxf(m, s_em[w]);
-    }
-    atomicAdd(A.sf_acc, t);
-    atomicMax(A.emax_acc, __float_as_uint(m));  // non-negative floats order as their bits
-  }
-  grid_barrier(A.bar, ++gen * gridDim.x);
-  const double SF = *reinterpret_cast<volatile double*>(A.sf_acc);
-  const float EM = __uint_as_float(*reinterpret_cast<volatile unsigned*>(A.emax_acc));
-  const float WM = A.w_absmax ? *reinterpret_cast<volatile float*>(A.w_absmax) : INFINITY;
-  const bool safe = isfinite(SF) && isfinite(EM) && isfinite(WM) && SF * static_cast<double>(EM) < kFusedSafe &&
-                    SF * static_cast<double>(WM) < kFusedSafe;
-
-  float4 g[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  double lsum = 0.0, fabs_sum = 0.0;
-  float pend_sc = 0.0f, pend_pt = 0.0f, pend_wn = 0.0f;
-  int c_pend = 0;
-  float wmax = 0.0f;
-  const int32_t* cofs = A.row_cofs + static_cast<size_t>(b) * (A.C + 1);
-
-  if (safe) {
-    // ---- interleaved schedule: forward of chunk p with the update of chunk p-1
-    for (int p = 0; p <= A.C; ++p) {
-      if (p < A.C && has_row) fused_fwd<NV, BF16>(A, b, cofs[p], cofs[p + 1], e, g, lsum, fabs_sum, pend_sc, pend_pt,
-                                                  pend_wn, c_pend, lane);
-      if (p >= 1) {
-        const uint32_t u0 = A.uc[p - 1], u1 = A.uc[p];
-        for (int64_t uq = u0 + gw; uq < u1; uq += NW) fused_upd<NV, BF16, ADAM, false>(A.u, static_cast<uint32_t>(uq), wmax, lane);
-      }
-      if (p < A.C) grid_barrier(A.bar, ++gen * gridDim.x);
-    }
-  } else {
-    // ---- two-pass schedule: every forward, then a check of every gradient, then the updates
-    if (has_row)
-      fused_fwd<NV, BF16>(A, b, cofs[0], cofs[A.C], e, g, lsum, fabs_sum, pend_sc, pend_pt, pend_wn, c_pend, lane);
-    bool bad = false;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) bad |= !(isfinite(g[i].x) && isfinite(g[i].y) && isfinite(g[i].z) && isfinite(g[i].w));
-    if (has_row && __any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.status + ASTRA_STATUS_NONFINITE_GRAD_EMB, 1);
-    grid_barrier(A.bar, ++gen * gridDim.x);
-    const uint32_t U = *A.u.U;
-    bool ok = true;
-    for (int64_t uq = gw; uq < U; uq += NW) ok &= fused_upd<NV, BF16, ADAM, true>(A.u, static_cast<uint32_t>(uq), wmax, lane);
-    if (!ok && lane == 0) atomicExch(a.status + ASTRA_STATUS_NONFINITE_GRAD, 1);
-    grid_barrier(A.bar, ++gen * gridDim.x);
-    const bool go = *reinterpret_cast<volatile int32_t*>(a.status + ASTRA_STATUS_NONFINITE_GRAD) == 0 &&
-                    *reinterpret_cast<volatile int32_t*>(a.status + ASTRA_STATUS_NONFINITE_GRAD_EMB) == 0;
-    if (go)
-      for (int64_t uq = gw; uq < U; uq += NW) fused_upd<NV, BF16, ADAM, false>(A.u, static_cast<uint32_t>(uq), wmax, lane);
-  }
-
-  // ---- per-row outputs (grad_emb in a fixed order: this warp's registers)
-  if (has_row) {
-    if (lane < c_pend) lsum += slot_loss(pend_sc, pend_pt, pend_wn);
-    lsum = warp_sum(lsum);
-    bool bad = false;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      float4 gi = g[i];
-      const size_t el = static_cast<size_t>(b) * d + i * 128 + lane * 4;
-      if (a.keep) {
-        const float4 k4 = *reinterpret_cast<const float4*>(a.keep + el);
-        gi = make_float4(__fmul_rn(gi.x, k4.x), __fmul_rn(gi.y, k4.y), __fmul_rn(gi.z, k4.z), __fmul_rn(gi.w, k4.w));
-      }
-      *reinterpret_cast<float4*>(a.grad_emb + el) = gi;
-      bad |= !(isfinite(gi.x) && isfinite(gi.y) && isfinite(gi.z) && isfinite(gi.w));
-    }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] = 1;
-    if (lane == 0) {
-      a.loss_rows[b] = lsum;
-      a.bound_rows[b] = fabs_sum * static_cast<double>(row_emax);  // the legacy overflow bound (status word 2)
-    }
-  }
-  if (A.w_absmax) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-    if (lane == 0 && wmax > 0.0f) atomicMax(reinterpret_cast<unsigned*>(A.w_absmax), __float_as_uint(wmax));
-  }
-}
-
-// Chunk c's [first, last) positions in the sorted unique-label list.
-__global__ void chunk_bounds_kernel(const int32_t* uniq, const uint32_t* U, int64_t Lc, int C, uint32_t* uc) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c > C) return;
-  const int64_t key = static_cast<int64_t>(c) * Lc;
-  uint32_t lo = 0, hi = *U;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (static_cast<int64_t>(uniq[mid]) < key)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  uc[c] = lo;
-}
-
-// Warp per row: the row's owned slots bucketed by label chunk, stable in slot order.
-__global__ void __launch_bounds__(256) row_bucket_kernel(const int32_t* ids, int B, int S, int64_t off, int64_t Lloc,
-                                                         int64_t Lc, int C, int32_t* row_slots, int32_t* row_locs,
-                                                         int32_t* row_cofs) {
-  __shared__ int cnt[8][kMaxChunks + 1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x * 8 + warp;
-  if (b >= B) return;
-  int* cn = cnt[warp];
-  for (int c = lane; c <= C; c += 32) cn[c] = 0;
-  __syncwarp();
-  const int32_t* rid = ids + static_cast<size_t>(b) * S;
-  for (int s = lane; s < S; s += 32) {
-    const int64_t loc = static_cast<int64_t>(rid[s]) - off;
-    if (loc >= 0 && loc < Lloc) atomicAdd(&cn[loc / Lc], 1);
-  }
-  __syncwarp();
-  if (lane == 0) {  // exclusive scan (C <= 127)
-    int acc = 0;
-    for (int c = 0; c <= C; ++c) {
-      const int t = cn[c];
-      cn[c] = acc;
-      acc += t;
-    }
-  }
-  __syncwarp();
-  for (int c = lane; c <= C; c += 32) row_cofs[static_cast<size_t>(b) * (C + 1) + c] = cn[c];
-  __syncwarp();
-  for (int s0 = 0; s0 < S; s0 += 32) {
-    const int s = s0 + lane;
-    int c = -1;
-    if (s < S) {
-      const int64_t loc = static_cast<int64_t>(rid[s]) - off;
-      if (loc >= 0 && loc < Lloc) c = static_cast<int>(loc / Lc);
-    }
-    const unsigned grp = __match_any_sync(0xffffffffu, c);
-    if (c >= 0) {
-      const size_t at = static_cast<size_t>(b) * S + cn[c] + __popc(grp & ((1u << lane) - 1u));
-      row_slots[at] = s;
-      row_locs[at] = static_cast<int32_t>(static_cast<int64_t>(rid[s]) - off);
-    }
-    __syncwarp();
-    if (c >= 0 && lane == __ffs(grp) - 1) cn[c] += __popc(grp);
-    __syncwarp();
-  }
-}
-
-template <int NV, bool BF16, bool ADAM>
-int launch_fused(const FusedArgs& A, cudaStream_t st) {
-  static int grid = 0;
-  auto kern = step_fused_kernel<NV, BF16, ADAM>;
-  if (!grid) {
-    int per_sm = 0;
-    ASTRA_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFusedThreads, 0), "occupancy"));
-    grid = std::max(1, per_sm) * num_sms();
-  }
-  if (static_cast<int64_t>(grid) * kFusedWarps < A.f.B) return ASTRA_ERR_CONFIG;  // caller falls back
-  FusedArgs a = A;
-  void* args[] = {&a};
-  ASTRA_TRY(check_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kFusedThreads), args,
-                                                   0, st),
-                       "launch step_fused"));
-  ASTRA_LAUNCHED("step_fused");
-  return ASTRA_OK;
-}
-
-template <bool BF16, bool ADAM>
-int launch_fused_nv(int nv, const FusedArgs& A, cudaStream_t st) {
-  switch (nv) {
-    case 1: return launch_fused<1, BF16, ADAM>(A, st);
-    case 2: return launch_fused<2, BF16, ADAM>(A, st);
-    case 4: return launch_fused<4, BF16, ADAM>(A, st);
-    case 6: return launch_fused<6, BF16, ADAM>(A, st);
-    case 8: return launch_fused<8, BF16, ADAM>(A, st);
-  }
-  return ASTRA_ERR_CONFIG;
-}
-
-// Max B the fused kernel serves (one batch row per warp of the cooperative grid).
-template <bool BF16, bool ADAM>
-int fused_max_rows(int nv) {
-  static int cached[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
-  if (nv < 0 || nv > 8) return 0;
-  if (cached[nv] >= 0) return cached[nv];
-  int per_sm = 0;
-  switch (nv) {
-    case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fused_kernel<1, BF16, ADAM>, kFusedThreads, 0); break;
-    case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fused_kernel<2, BF16, ADAM>, kFusedThreads, 0); break;
-    case 4: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fused_kernel<4, BF16, ADAM>, kFusedThreads, 0); break;
-    case 6: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fused_kernel<6, BF16, ADAM>, kFusedThreads, 0); break;
-    case 8: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_fused_kernel<8, BF16, ADAM>, kFusedThreads, 0); break;
-    default: return 0;
-  }
-  cached[nv] = per_sm * num_sms() * kFusedWarps;
-  return cached[nv];
-}
-
-// ================================================================ pipelined step
-// One cooperative kernel per minibatch, one CTA per SM, two roles per CTA that
-// work through the label chunks of the fused schedule without grid barriers:
-//   forward warps 0-3 own the CTA's batch rows (<= 8; embeddings and grad_emb
-//   partials in shared memory, row r -> warp r % 4, fixed order); chunk by
-//   chunk they gather the rows' slot rows (each warp self-feeds a private ring
-//   of bulk copies RF rows ahead, across chunk borders), compute scores,
-//   factors, loss terms and f * w_row; when the CTA finishes chunk c it bumps
-//   done[c];
-//   update warps 4-7 + producer warp 8 follow behind: for chunk c they wait
-//   for done[c] == #CTAs, then update the CTA's share of the chunk's labels as
-//   label_update_tma does (bulk-copied rows, still L2-resident from the gather).
-// DRAM sees each touched row read once (gather) and written once (update).
-// Finiteness is proven up front from bounds (as the fused schedule); without
-// the proof the update warps wait for every forward, check every gradient,
-// and only then update.
-constexpr int kPipeRows = 8;                // batch rows per CTA
-constexpr int kPipeThreads = 32 * 9;        // 4 forward + 4 update + 1 update producer
-
-template <int NV, bool BF16>
-struct PipeRing {
-  static constexpr uint32_t WB = NV * 128 * (BF16 ? 2 : 4);
-  static constexpr int RF = BF16 ? 12 : 6;  // self-fed entries per forward warp
-};
-
-constexpr int kPipeLag = 2;  // with throttling: the gather runs at most this many chunks ahead of the updates
-
-struct PipeArgs {
-  FusedArgs x;
-  int rows_f;
-  unsigned* done;   // [C] CTAs whose forward finished chunk c
-  unsigned* udone;  // [C] CTAs whose updates finished chunk c
-  int throttle;
-  unsigned* ready;  // [0] bounds published, [1] gradients checked (checked schedule), [2] forwards finished
-};
-
-template <int NV, bool BF16, bool ADAM>
-struct PipeSmem {
-  static constexpr int d = NV * 128;
-  using PR = PipeRing<NV, BF16>;
-  using RG = UpdRing<NV, BF16, ADAM>;
-  static constexpr size_t E = 0;                                           // e_s, g_s
-  static constexpr size_t FR = E + static_cast<size_t>(2) * kPipeRows * d * 4;  // forward rings
-  static constexpr size_t UR = FR + static_cast<size_t>(4) * PR::RF * PR::WB;   // update ring
-  static constexpr size_t BAR = UR + static_cast<size_t>(RG::RING) * RG::ENTRY;  // barriers
-  static constexpr size_t FAB = BAR + 8 * (4 * PR::RF + 2 * RG::RING);          // row_fabs
-  static constexpr size_t TOTAL = FAB + 8 * kPipeRows;
-};
-
-// Walks a forward warp's (chunk, row, slot) items in order: rows w and w+4 of
-// the CTA, chunk by chunk, skipping empty segments; c == C at the end.
-struct PipeCursor {
-  int c, ri, r, j, j1;
-};
-
-__device__ __forceinline__ bool pipe_cursor_seg(PipeCursor& q, const FusedArgs& A, int b0, int nrows, int warp) {
-  q.r = warp + 4 * q.ri;
-  if (q.r >= nrows) return false;
-  const int32_t* cofs = A.row_cofs + static_cast<size_t>(b0 + q.r) * (A.C + 1);
-  q.j = cofs[q.c];
-  q.j1 = cofs[q.c + 1];
-  return q.j < q.j1;
-}
-
-__device__ __forceinline__ void pipe_cursor_skip(PipeCursor& q, const FusedArgs& A, int b0, int nrows, int warp) {
-  while (q.c < A.C) {
-    if (pipe_cursor_seg(q, A, b0, nrows, warp)) return;
-    if (++q.ri == 2) {
-      q.ri = 0;
-      ++q.c;
-    }
-  }
-}
-
-__device__ __forceinline__ void pipe_cursor_init(PipeCursor& q, const FusedArgs& A, int b0, int nrows, int warp) {
-  q.c = 0;
-  q.ri = 0;
-  pipe_cursor_skip(q, A, b0, nrows, warp);
-}
-
-__device__ __forceinline__ void pipe_cursor_next(PipeCursor& q, const FusedArgs& A, int b0, int nrows, int warp) {
-  if (++q.j < q.j1) return;
-  if (++q.ri == 2) {
-    q.ri = 0;
-    ++q.c;
-  }
-  pipe_cursor_skip(q, A, b0, nrows, warp);
-}
-
-__device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target) {
-  unsigned v;
-  while (true) {
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    if (v >= target) break;
-    __nanosleep(128);
-  }
-}
-
-__device__ __forceinline__ void publish(unsigned* p) {
-  __threadfence();
-  atomicAdd(p, 1u);
-}
-
-// The CTA's share [q0, q1) of chunk c's unique labels.
-__device__ __forceinline__ void pipe_share(const FusedArgs& A, int c, uint32_t& q0, uint32_t& q1) {
-  const uint32_t lo = A.uc[c], n = A.uc[c + 1] - lo;
-  q0 = lo + static_cast<uint32_t>((static_cast<uint64_t>(n) * blockIdx.x) / gridDim.x);
-  q1 = lo + static_cast<uint32_t>((static_cast<uint64_t>(n) * (blockIdx.x + 1)) / gridDim.x);
-}
-
-template <int NV, bool BF16, bool ADAM>
-__global__ void __launch_bounds__(kPipeThreads, 1) step_pipe_kernel(PipeArgs P) {
-  const FusedArgs& A = P.x;
-  const FwdArgs& a = A.f;
-  const UpdArgs& ua = A.u;
-  constexpr int d = NV * 128;
-  using SM = PipeSmem<NV, BF16, ADAM>;
-  using PR = PipeRing<NV, BF16>;
-  using RG = UpdRing<NV, BF16, ADAM>;
-  constexpr int RF = PR::RF;
-  constexpr int RING = RG::RING;
-  constexpr uint32_t ROWB = RG::ENTRY;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  extern __shared__ __align__(128) unsigned char psm[];
-  float* e_s = reinterpret_cast<float*>(psm + SM::E);
-  float* g_s = e_s + kPipeRows * d;
-  unsigned char* frings = psm + SM::FR;
-  unsigned char* uring = psm + SM::UR;
-  uint64_t* ffull = reinterpret_cast<uint64_t*>(psm + SM::BAR);
-  uint64_t* ufull = ffull + 4 * RF;
-  uint64_t* uempty = ufull + RING;
-  double* row_fabs = reinterpret_cast<double*>(psm + SM::FAB);
-  const unsigned G = gridDim.x;
-  const int b0 = blockIdx.x * P.rows_f;
-  const int nrows = max(0, min(P.rows_f, a.B - b0));
-  __shared__ double s_sf;
-  __shared__ unsigned s_em;
-  if (threadIdx.x == 0) {
-    s_sf = 0.0;
-    s_em = 0u;
-    for (int r = 0; r < 4 * RF; ++r) mbar_init(&ffull[r], 1);
-    for (int r = 0; r < RING; ++r) {
-      mbar_init(&ufull[r], 1);
-      mbar_init(&uempty[r], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int i = threadIdx.x; i < kPipeRows; i += kPipeThreads) row_fabs[i] = 0.0;
-  // embeddings -> smem, grad_emb partials = 0, finiteness bound partials
-  float em = 0.0f;
-  for (int i = threadIdx.x; i < nrows * d; i += kPipeThreads) {
-    const float v = a.emb[static_cast<size_t>(b0) * d + i];
-    e_s[i] = v;
-    g_s[i] = 0.0f;
-    em = fmaxf(em, isfinite(v) ? fabsf(v) : INFINITY);
-  }
-  double sf = 0.0;
-  for (int r = warp; r < nrows; r += kPipeThreads / 32) {
-    const int b = b0 + r;
-    const int j1 = A.row_cofs[static_cast<size_t>(b) * (A.C + 1) + A.C];
-    const int32_t* rs = A.row_slots + static_cast<size_t>(b) * a.S;
-    for (int j = lane; j < j1; j += 32) {
-      const float wt = a.weights[b * a.weights_stride + rs[j]];
-      sf += 1.0 + (isfinite(wt) ? fabs(static_cast<double>(wt)) : INFINITY);
-    }
-  }
-  sf = warp_sum(sf);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) em = fmaxf(em, __shfl_xor_sync(0xffffffffu, em, o));
-  __syncthreads();
-  if (lane == 0) {
-    atomicAdd(&s_sf, sf);
-    atomicMax(&s_em, __float_as_uint(em));
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    atomicAdd(A.sf_acc, s_sf);
-    atomicMax(A.emax_acc, s_em);
-    publish(P.ready + 0);
-  }
-
-  if (warp < 4) {
-    // =============================== forward warps
-    // the same safety decision as the update warps: only the proven schedule
-    // interleaves (and throttles) the gather against the updates
-    if (threadIdx.x == 0) spin_geq(P.ready + 0, G);
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    const double fSF = *reinterpret_cast<volatile double*>(A.sf_acc);
-    const float fEM = __uint_as_float(*reinterpret_cast<volatile unsigned*>(A.emax_acc));
-    const float fWM = A.w_absmax ? *reinterpret_cast<volatile float*>(A.w_absmax) : INFINITY;
-    // ASTRA_STEP_PIPE_THROTTLE=1 couples the gather to the updates (measured
-    // 3-5 ms per minibatch: the per-chunk grid-wide handshakes serialise)
-    const bool throttle = P.throttle && isfinite(fSF) && isfinite(fEM) && isfinite(fWM) &&
-                          fSF * static_cast<double>(fEM) < kFusedSafe && fSF * static_cast<double>(fWM) < kFusedSafe;
-    const unsigned char* Wb = static_cast<const unsigned char*>(a.W);
-    PipeCursor ic, cc;  // issue / consume cursors over (chunk, row, slot)
-    pipe_cursor_init(ic, A, b0, nrows, warp);
-    pipe_cursor_init(cc, A, b0, nrows, warp);
-    int n_issued = 0, cnt = 0;
-    // keep up to RF rows in flight, never more than kPipeLag chunks ahead of the
-    // chunk being consumed; chunk x is gathered only once every CTA updated
-    // chunk x - kPipeLag (so the rows waiting for their update stay in L2).
-    // The wait can only involve chunks this CTA has finished (x - kPipeLag < cur).
-    auto refill = [&](int cur) {
-      while (n_issued - cnt < RF && ic.c < A.C && (!throttle || ic.c < cur + kPipeLag)) {
-        const int e = warp * RF + n_issued % RF;
-        if (lane == 0) {
-          if (throttle && ic.c >= kPipeLag) spin_geq(P.udone + ic.c - kPipeLag, G);
-          const int32_t loc = A.row_locs[static_cast<size_t>(b0 + ic.r) * a.S + ic.j];
-          mbar_expect_tx(&ffull[e], PR::WB);
-          bulk_g2s(frings + e * PR::WB, Wb + static_cast<size_t>(loc) * PR::WB, PR::WB, &ffull[e]);
-        }
-        __syncwarp();
-        ++n_issued;
-        pipe_cursor_next(ic, A, b0, nrows, warp);
-      }
-    };
-    refill(0);
-    double lsum = 0.0;
-    float pend_sc = 0.0f, pend_pt = 0.0f, pend_wn = 0.0f;
-    int c_pend = 0;
-    for (int c = 0; c < A.C; ++c) {
-      for (; cc.c == c; pipe_cursor_next(cc, A, b0, nrows, warp)) {
-        const int r = cc.r, b = b0 + r;
-        const int sl = A.row_slots[static_cast<size_t>(b) * a.S + cc.j];
-        const float* er = e_s + r * d;
-        float* gr = g_s + r * d;
-        const SlotMeta meta = slot_meta(a, b, sl);
-        const int k = cnt, e = warp * RF + k % RF;
-        mbar_wait(&ffull[e], (k / RF) & 1);
-        float4 w[NV];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          if constexpr (BF16) {
-            const uint2 u = *reinterpret_cast<const uint2*>(frings + e * PR::WB + (i * 128 + lane * 4) * 2);
-            w[i] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
-                               __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
-          } else {
-            w[i] = *reinterpret_cast<const float4*>(frings + e * PR::WB + (i * 128 + lane * 4) * 4);
-          }
-        }
-        __syncwarp();
-        ++cnt;
-        refill(c);  // the entry is in registers: refill the ring
-        float acc = 0.0f;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          const float4 x = *reinterpret_cast<const float4*>(er + i * 128 + lane * 4);
-          acc = fmaf(w[i].x, x.x, acc);
-          acc = fmaf(w[i].y, x.y, acc);
-          acc = fmaf(w[i].z, x.z, acc);
-          acc = fmaf(w[i].w, x.w, acc);
-        }
-        acc = warp_sum(acc);
-        float pt, wn;
-        const float f = slot_factor_meta(meta, acc, &pt, &wn);
-        if (lane == c_pend) {
-          pend_sc = acc;
-          pend_pt = pt;
-          pend_wn = wn;
-        }
-        if (++c_pend == 32) {
-          lsum += slot_loss(pend_sc, pend_pt, pend_wn);
-          c_pend = 0;
-        }
-        if (lane == 0) {
-          __stcg(a.factors + static_cast<size_t>(b) * a.S + sl, f);
-          row_fabs[r] += static_cast<double>(fabsf(f));
-        }
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          float4* gp = reinterpret_cast<float4*>(gr + i * 128 + lane * 4);
-          float4 g = *gp;
-          g.x = fmaf(f, w[i].x, g.x);
-          g.y = fmaf(f, w[i].y, g.y);
-          g.z = fmaf(f, w[i].z, g.z);
-          g.w = fmaf(f, w[i].w, g.w);
-          *gp = g;
-        }
-      }
-      // chunk c done by the CTA's four forward warps: publish it
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (threadIdx.x == 0) publish(P.done + c);
-      refill(c + 1);  // the window moved
-    }
-    if (lane < c_pend) lsum += slot_loss(pend_sc, pend_pt, pend_wn);
-    lsum = warp_sum(lsum);
-    if (lane == 0 && warp < nrows) a.loss_rows[b0 + warp] = lsum;  // warp partials, summed by finalize
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    bool bad = false;
-    for (int i = threadIdx.x; i < nrows * d; i += 128) {
-      float gk = g_s[i];
-      if (a.keep) gk = __fmul_rn(gk, a.keep[static_cast<size_t>(b0) * d + i]);
-      a.grad_emb[static_cast<size_t>(b0) * d + i] = gk;
-      bad |= !isfinite(gk);
-    }
-    if (bad) a.status[ASTRA_STATUS_NONFINITE_GRAD_EMB] = 1;
-    for (int r = threadIdx.x; r < nrows; r += 128) {
-      float m = 0.0f;
-      for (int k = 0; k < d; ++k) m = fmaxf(m, fabsf(e_s[r * d + k]));
-      a.bound_rows[b0 + r] = row_fabs[r] * static_cast<double>(m);  // the legacy overflow bound (status word 2)
-      if (r >= 4) a.loss_rows[b0 + r] = 0.0;
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (threadIdx.x == 0) publish(P.ready + 2);
-    return;
-  }
-
-  // =============================== update warps (4-7) + producer (8)
-  if (threadIdx.x == 128) spin_geq(P.ready + 0, G);
-  asm volatile("bar.sync 2, 160;" ::: "memory");
-  const double SF = *reinterpret_cast<volatile double*>(A.sf_acc);
-  const float EM = __uint_as_float(*reinterpret_cast<volatile unsigned*>(A.emax_acc));
-  const float WM = A.w_absmax ? *reinterpret_cast<volatile float*>(A.w_absmax) : INFINITY;
-  const bool safe = isfinite(SF) && isfinite(EM) && isfinite(WM) && SF * static_cast<double>(EM) < kFusedSafe &&
-                    SF * static_cast<double>(WM) < kFusedSafe;
-  if (!safe) {
-    // checked schedule: every forward, then every gradient, then the updates
-    if (threadIdx.x == 128) spin_geq(P.ready + 2, G);
-    asm volatile("bar.sync 2, 160;" ::: "memory");
-    bool ok = true;
-    float dummy = 0.0f;
-    for (int c = 0; c < A.C; ++c) {
-      uint32_t q0, q1;
-      pipe_share(A, c, q0, q1);
-      for (uint32_t uq = q0 + (warp - 4); uq < q1; uq += 5) ok &= fused_upd<NV, BF16, ADAM, true>(ua, uq, dummy, lane);
-    }
-    if (!ok && lane == 0) atomicExch(a.status + ASTRA_STATUS_NONFINITE_GRAD, 1);
-    asm volatile("bar.sync 2, 160;" ::: "memory");
-    if (threadIdx.x == 128) {
-      publish(P.ready + 1);
-      spin_geq(P.ready + 1, G);
-    }
-    asm volatile("bar.sync 2, 160;" ::: "memory");
-    if (*reinterpret_cast<volatile int32_t*>(a.status + ASTRA_STATUS_NONFINITE_GRAD) ||
-        *reinterpret_cast<volatile int32_t*>(a.status + ASTRA_STATUS_NONFINITE_GRAD_EMB))
-      return;
-  }
-  if (warp == 8) {
-    // ---------------- update producer: this CTA's share of each chunk, after its forwards
-    const unsigned char* Wb = static_cast<const unsigned char*>(a.W);
-    int i = 0;
-    for (int c = 0; c < A.C; ++c) {
-      if (lane == 0) spin_geq(P.done + c, G);
-      __syncwarp();
-      uint32_t q0, q1;
-      pipe_share(A, c, q0, q1);
-      for (uint32_t i0 = q0; i0 < q1; i0 += 32) {
-        const int32_t l_lane = i0 + lane < q1 ? ua.uniq[i0 + lane] : 0;
-        const int nb = static_cast<int>(min(32u, q1 - i0));
-        for (int jj = 0; jj < nb; ++jj) {
-          const size_t l = static_cast<size_t>(__shfl_sync(0xffffffffu, l_lane, jj));
-          if (lane == 0) {
-            const int r = i % RING;
-            mbar_wait(&uempty[r], ((i / RING) & 1) ^ 1);
-            mbar_expect_tx(&ufull[r], ROWB);
-            unsigned char* dst = uring + r * ROWB;
-            bulk_g2s(dst, Wb + l * RG::WB, RG::WB, &ufull[r]);
-            if constexpr (ADAM) {
-              bulk_g2s(dst + RG::WB, ua.m + l * d, RG::MB, &ufull[r]);
-              bulk_g2s(dst + RG::WB + RG::MB, ua.v + l * d, RG::MB, &ufull[r]);
-            }
-          }
-          ++i;
-          __syncwarp();
-        }
-      }
-    }
-    return;
-  }
-  // ---------------- update consumers: label i of the CTA's sequence -> warp 4 + i % 4
-  const int uw = warp - 4;
-  float wmax = 0.0f;
-  int i = 0;
-  for (int c = 0; c < A.C; ++c) {
-    if (lane == 0) spin_geq(P.done + c, G);  // the chunk's factors are published
-    __syncwarp();
-    uint32_t q0, q1;
-    pipe_share(A, c, q0, q1);
-    for (uint32_t uq = q0; uq < q1; ++uq, ++i) {
-      if ((i & 3) != uw) continue;
-      const int r = i % RING;
-      const int32_t l = ua.uniq[uq];
-      const uint32_t start = ua.offsets[l], nn = ua.counts[l];
-      const int32_t reg = sort_segment(ua, start, nn, lane);
-      const size_t row = static_cast<size_t>(l) * d;
-      float4 g[NV];
-#pragma unroll
-      for (int q = 0; q < NV; ++q) g[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (uint32_t j = 0; j < nn; ++j) {
-        const int32_t s0 = seg_slot(ua, start, nn, reg, j);
-        const float f0 = __ldcg(ua.factors + s0);
-        const float* e0 = ua.emb + static_cast<size_t>(s0 / ua.S) * d + lane * 4;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          const float4 x0 = *reinterpret_cast<const float4*>(e0 + q * 128);
-          g[q].x = __fadd_rn(g[q].x, __fmul_rn(f0, x0.x));
-          g[q].y = __fadd_rn(g[q].y, __fmul_rn(f0, x0.y));
-          g[q].z = __fadd_rn(g[q].z, __fmul_rn(f0, x0.z));
-          g[q].w = __fadd_rn(g[q].w, __fmul_rn(f0, x0.w));
-        }
-      }
-      mbar_wait(&ufull[r], (i / RING) & 1);
-      float4 p[NV];
-      float4 m4[ADAM ? NV : 1], v4[ADAM ? NV : 1];
-#pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        if constexpr (BF16) {
-          const uint2 u = *reinterpret_cast<const uint2*>(uring + r * ROWB + (q * 128 + lane * 4) * 2);
-          p[q] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
-                             __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
-        } else {
-          p[q] = *reinterpret_cast<const float4*>(uring + r * ROWB + (q * 128 + lane * 4) * 4);
-        }
-        if constexpr (ADAM) {
-          m4[q] = *reinterpret_cast<const float4*>(uring + r * ROWB + RG::WB + (q * 128 + lane * 4) * 4);
-          v4[q] = *reinterpret_cast<const float4*>(uring + r * ROWB + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&uempty[r]);
-#pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        float4 np;
-        const size_t el = row + q * 128 + lane * 4;
-        if constexpr (ADAM) {
-          np.x = upd_elem<true>(ua, p[q].x, g[q].x, &m4[q].x, &v4[q].x);
-          np.y = upd_elem<true>(ua, p[q].y, g[q].y, &m4[q].y, &v4[q].y);
-          np.z = upd_elem<true>(ua, p[q].z, g[q].z, &m4[q].z, &v4[q].z);
-          np.w = upd_elem<true>(ua, p[q].w, g[q].w, &m4[q].w, &v4[q].w);
-          *reinterpret_cast<float4*>(ua.m + el) = m4[q];
-          *reinterpret_cast<float4*>(ua.v + el) = v4[q];
-        } else {
-          np.x = upd_elem<false>(ua, p[q].x, g[q].x, nullptr, nullptr);
-          np.y = upd_elem<false>(ua, p[q].y, g[q].y, nullptr, nullptr);
-          np.z = upd_elem<false>(ua, p[q].z, g[q].z, nullptr, nullptr);
-          np.w = upd_elem<false>(ua, p[q].w, g[q].w, nullptr, nullptr);
-        }
-        if constexpr (BF16) {
-          uint2 o;
-          o.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
-          o.y = static_cast<uint32_t>(f32_to_bf16_bits(np.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.w)) << 16);
-          *reinterpret_cast<uint2*>(static_cast<uint16_t*>(ua.W) + el) = o;
-        } else {
-          *reinterpret_cast<float4*>(static_cast<float*>(ua.W) + el) = np;
-        }
-        wmax = fmaxf(wmax, absmax4(np));
-      }
-    }
-    // chunk c updated by the CTA's four update warps: release the gather of chunk c + kPipeLag
-    asm volatile("bar.sync 3, 128;" ::: "memory");
-    if (threadIdx.x == 128) publish(P.udone + c);
-  }
-  push_wmax(ua, wmax, lane);
-}
-
-template <int NV, bool BF16, bool ADAM>
-int pipe_grid() {
-  static int g = -1;
-  if (g < 0) {
-    auto kern = step_pipe_kernel<NV, BF16, ADAM>;
-    constexpr size_t smem = PipeSmem<NV, BF16, ADAM>::TOTAL;
-    g = 0;
-    if (smem <= 227 * 1024) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPipeThreads, smem);
-      g = per_sm >= 1 ? num_sms() : 0;  // one CTA per SM
-    }
-  }
-  return g;
-}
-
-template <int NV, bool BF16, bool ADAM>
-int launch_pipe(const PipeArgs& P0, int grid, cudaStream_t st) {
-  auto kern = step_pipe_kernel<NV, BF16, ADAM>;
-  constexpr size_t smem = PipeSmem<NV, BF16, ADAM>::TOTAL;
-  PipeArgs P = P0;
-  void* args[] = {&P};
-  ASTRA_TRY(check_cuda(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kPipeThreads), args,
-                                                   smem, st),
-                       "launch step_pipe"));
-  ASTRA_LAUNCHED("step_pipe");
-  return ASTRA_OK;
-}
-
-template <bool BF16, bool ADAM>
-int pipe_grid_nv(int nv) {
-  switch (nv) {
-    case 1: return pipe_grid<1, BF16, ADAM>();
-    case 2: return pipe_grid<2, BF16, ADAM>();
-    case 4: return pipe_grid<4, BF16, ADAM>();
-    case 6: return pipe_grid<6, BF16, ADAM>();
-    case 8: return pipe_grid<8, BF16, ADAM>();
-  }
-  return 0;
-}
-
-template <bool BF16, bool ADAM>
-int launch_pipe_nv(int nv, const PipeArgs& P, int grid, cudaStream_t st) {
-  switch (nv) {
-    case 1: return launch_pipe<1, BF16, ADAM>(P, grid, st);
-    case 2: return launch_pipe<2, BF16, ADAM>(P, grid, st);
-    case 4: return launch_pipe<4, BF16, ADAM>(P, grid, st);
-    case 6: return launch_pipe<6, BF16, ADAM>(P, grid, st);
-    case 8: return launch_pipe<8, BF16, ADAM>(P, grid, st);
-  }
-  return ASTRA_ERR_CONFIG;
-}
-
 // apply_classifier_updates_arrays: explicit (ids, grads) form.
 __global__ void apply_check_kernel(const float* grads, int64_t n, int32_t* status) {
   bool bad = false;
@@ -2662,19 +1530,16 @@ __global__ void apply_rows_kernel(void* W, int d, const int64_t* ids, const floa
 }
 
 template <int NV, bool BF16>
-void launch_forward_vec(const FwdArgs& a, cudaStream_t st) {
-  static const bool legacy = getenv("ASTRA_STEP_LEGACY_FWD") != nullptr;  // register-pipelined gather
+bool launch_forward_vec(const FwdArgs& a, cudaStream_t st) {
   const size_t smem = tma_fwd_smem<NV, BF16>(a.S);
-  if (!legacy && smem <= 200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(slot_forward_tma<NV, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
-    slot_forward_tma<NV, BF16><<<a.B, kTmaThreads, smem, st>>>(a);
-  } else {
-    slot_forward_vec<NV, BF16><<<a.B, kFwdThreads, 0, st>>>(a);
+  if (smem > 200 * 1024) return false;  // (S > ~20K slots: the generic kernel)
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(slot_forward_tma<NV, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
   }
+  slot_forward_tma<NV, BF16><<<a.B, kTmaThreads, smem, st>>>(a);
+  return true;
 }
 
 template <int NV, bool BF16, bool ADAM>
@@ -2693,8 +1558,7 @@ int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
   // (the check pass returns at once unless the bound tripped: a small grid keeps that cheap)
   label_update_kernel<BF16, ADAM, true><<<std::min(max_ctas, 2 * num_sms()), kUpdThreads, 0, st>>>(a);
   ASTRA_LAUNCHED("label_check");
-  static const bool legacy = getenv("ASTRA_STEP_LEGACY_UPD") != nullptr;
-  if (!legacy && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
+  if (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8) {
     const int grid = (ADAM && nv > 6 ? 2 : 3) * num_sms();  // = upd_tma_ctas<nv, ADAM>()
     size_t smem = 0;
     switch (nv) {
@@ -2714,24 +1578,12 @@ int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
     ASTRA_LAUNCHED("label_update_tma");
     return ASTRA_OK;
   }
-  switch (nv) {
-    case 1: label_update_vec<1, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
-    case 2: label_update_vec<2, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
-    case 4: label_update_vec<4, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
-    case 6: label_update_vec<6, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
-    case 8: label_update_vec<8, BF16, ADAM><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
-    default: label_update_kernel<BF16, ADAM, false><<<max_ctas, kUpdThreads, 0, st>>>(a); break;
-  }
+  label_update_kernel<BF16, ADAM, false><<<max_ctas, kUpdThreads, 0, st>>>(a);
   ASTRA_LAUNCHED("label_update");
   return ASTRA_OK;
 }
 
 struct StepWs {
-  unsigned* pipe_ctr;  // [2 kMaxChunks] done / udone counters + [4] ready counters of the pipelined step
-  int32_t* row_slots;
-  int32_t* row_locs;
-  int32_t* row_cofs;
-  uint32_t* uc;
   unsigned* bar;
   double* sf_acc;
   unsigned* emax_acc;
@@ -2769,15 +1621,10 @@ size_t carve_step(void* base, size_t cap, int B, int S, int64_t Lloc, StepWs* w)
   w->U = c.take<uint32_t>(1);
   w->loss_rows = c.take<double>(B);
   w->bound_rows = c.take<double>(B);
-  w->row_slots = c.take<int32_t>(n);
-  w->row_locs = c.take<int32_t>(n);
-  w->row_cofs = c.take<int32_t>(static_cast<size_t>(B) * (kMaxChunks + 1));
-  w->uc = c.take<uint32_t>(kMaxChunks + 1);
   // one 32-byte block (a single memset): bar, emax_acc, (pad x2), the fp64 accumulator
   w->bar = c.take<unsigned>(8);
   w->emax_acc = w->bar ? w->bar + 1 : nullptr;
   w->sf_acc = w->bar ? reinterpret_cast<double*>(w->bar + 4) : nullptr;
-  w->pipe_ctr = c.take<unsigned>(2 * kMaxChunks + 4);
   w->mode = c.take<int32_t>(4);
   w->slot_loss = c.take<double>(n);
   w->ustart = c.take<uint32_t>(n < Lloc ? n : Lloc);
@@ -2843,35 +1690,7 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
   const int nv = d % 128 == 0 ? d / 128 : 0;
   const bool aligned = (reinterpret_cast<uintptr_t>(emb) % 16 == 0) && (reinterpret_cast<uintptr_t>(W) % 16 == 0);
   const bool adam = optimizer == ASTRA_OPT_ADAM;
-  static const int fused_env = [] {
-    // ASTRA_STEP_FUSED=1 selects the persistent L2-chunked step. Measured at the
-    // bench shape: 2.3 ms/minibatch vs 0.94 ms for the TMA two-kernel path (one
-    // warp per row and per label is latency-bound at 8 warps/SM); kept as a
-    // correct, tested alternative until it is software-pipelined.
-    const char* e = getenv("ASTRA_STEP_FUSED");
-    return e ? atoi(e) : 0;
-  }();
   const bool chunkable = !factors_in && aligned && Lloc > 0 && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8);
-  bool fused = fused_env && chunkable;
-  if (fused) {
-    const int max_rows = bf16 ? (adam ? fused_max_rows<true, true>(nv) : fused_max_rows<true, false>(nv))
-                              : (adam ? fused_max_rows<false, true>(nv) : fused_max_rows<false, false>(nv));
-    fused = B <= max_rows;
-  }
-  static const int pipe_env = [] {
-    // ASTRA_STEP_PIPE=1: the pipelined (forward CTAs -> update CTAs) L2-chunked step
-    const char* e = getenv("ASTRA_STEP_PIPE");
-    return e ? atoi(e) : 0;
-  }();
-  int pipe_grid_ctas = 0, pipe_nf = 0;
-  if (!fused && pipe_env && chunkable) {
-    pipe_grid_ctas = bf16 ? (adam ? pipe_grid_nv<true, true>(nv) : pipe_grid_nv<true, false>(nv))
-                          : (adam ? pipe_grid_nv<false, true>(nv) : pipe_grid_nv<false, false>(nv));
-    pipe_nf = pipe_grid_ctas > 0 ? (B + pipe_grid_ctas - 1) / pipe_grid_ctas : 0;  // rows per CTA
-    if (pipe_nf == 0 || pipe_nf > kPipeRows) pipe_grid_ctas = 0;
-  }
-  const bool piped = pipe_grid_ctas > 0;
-  fused = fused || piped;  // both take the chunked preparation below
   static const bool single_env = [] {
     // ASTRA_STEP_SINGLE=0: the deterministic two-kernel schedule (gather forward,
     // then label-major update) instead of the single label-major pass
@@ -2888,7 +1707,7 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     const char* e = getenv("ASTRA_STEP_SINGLE_ADAM");
     return e != nullptr && atoi(e) != 0;
   }();
-  const bool single = !fused && single_env && !g_step_deterministic.load() && chunkable && nv <= 6 &&
+  const bool single = single_env && !g_step_deterministic.load() && chunkable && nv <= 6 &&
                       (!adam || single_adam) &&
                       reinterpret_cast<uintptr_t>(grad_emb) % 16 == 0;  // (vector reductions into it)
   if (single) fa.skip = w.mode;
@@ -2910,7 +1729,7 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     scan_reduce_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz);
     ASTRA_LAUNCHED("scan_reduce");
     scan_top_kernel<<<1, 1024, 0, st>>>(w.blk_slots, w.blk_nz, static_cast<int>(nb), w.U, w.sf_acc, w.emax_acc,
-                                        w_absmax, single ? w.mode : nullptr);
+                                        w_absmax, single ? w.mode : nullptr, d);
     ASTRA_LAUNCHED("scan_top");
     scan_apply_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz, w.offsets,
                                                                      w.uniq, single ? w.ustart : nullptr, w.ucnt);
@@ -2963,22 +1782,24 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
       adam ? launch_single_nv<false, true>(nv, SA, st) : launch_single_nv<false, false>(nv, SA, st);
     ASTRA_LAUNCHED("step_single");
   }
-  if (!fused) {
+  {
     KernelTimer kt_fwd("slot_forward", st);
+    bool launched = false;
     if (aligned && (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8)) {
       switch (nv * 2 + (bf16 ? 1 : 0)) {
-        case 2: launch_forward_vec<1, false>(fa, st); break;
-        case 3: launch_forward_vec<1, true>(fa, st); break;
-        case 4: launch_forward_vec<2, false>(fa, st); break;
-        case 5: launch_forward_vec<2, true>(fa, st); break;
-        case 8: launch_forward_vec<4, false>(fa, st); break;
-        case 9: launch_forward_vec<4, true>(fa, st); break;
-        case 12: launch_forward_vec<6, false>(fa, st); break;
-        case 13: launch_forward_vec<6, true>(fa, st); break;
-        case 16: launch_forward_vec<8, false>(fa, st); break;
-        case 17: launch_forward_vec<8, true>(fa, st); break;
+        case 2: launched = launch_forward_vec<1, false>(fa, st); break;
+        case 3: launched = launch_forward_vec<1, true>(fa, st); break;
+        case 4: launched = launch_forward_vec<2, false>(fa, st); break;
+        case 5: launched = launch_forward_vec<2, true>(fa, st); break;
+        case 8: launched = launch_forward_vec<4, false>(fa, st); break;
+        case 9: launched = launch_forward_vec<4, true>(fa, st); break;
+        case 12: launched = launch_forward_vec<6, false>(fa, st); break;
+        case 13: launched = launch_forward_vec<6, true>(fa, st); break;
+        case 16: launched = launch_forward_vec<8, false>(fa, st); break;
+        case 17: launched = launch_forward_vec<8, true>(fa, st); break;
       }
-    } else {
+    }
+    if (!launched) {
       size_t smem = sizeof(float) * static_cast<size_t>(d) * (1 + kFwdWarps);
       if (smem > 200 * 1024) return set_error(ASTRA_ERR_CONFIG, "slate_step: d=%d too large", d);
       if (bf16) {
@@ -2995,68 +1816,10 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     single_row_finalize<<<B, kRowFinThreads, 0, st>>>(fa, w.slot_loss, w.mode);
     ASTRA_LAUNCHED("single_row_finalize");
   }
-  if (!fused) {
-    finalize_kernel<<<1, 1024, 0, st>>>(w.loss_rows, w.bound_rows, B, loss_out, status);
-    ASTRA_LAUNCHED("finalize");
-  }
+  finalize_kernel<<<1, 1024, 0, st>>>(w.loss_rows, w.bound_rows, B, loss_out, status);
+  ASTRA_LAUNCHED("finalize");
 
   if (Lloc == 0) return ASTRA_OK;
-  if (fused) {
-    // label chunks of ~24 MB of touched rows (+ Adam state) each: they stay in L2
-    // between their gather (phase p) and their update (phase p+1)
-    const double row_bytes = static_cast<double>(d) * ((bf16 ? 2 : 4) + (adam ? 8 : 0));
-    int C = static_cast<int>(std::ceil(static_cast<double>(n) * row_bytes / (24.0 * 1024 * 1024)));
-    C = std::max(1, std::min(C, kMaxChunks));
-    const int64_t Lc = (Lloc + C - 1) / C;
-    C = static_cast<int>((Lloc + Lc - 1) / Lc);
-    chunk_bounds_kernel<<<1, kMaxChunks + 1, 0, st>>>(w.uniq, w.U, Lc, C, w.uc);
-    ASTRA_LAUNCHED("chunk_bounds");
-    row_bucket_kernel<<<static_cast<unsigned>((B + 7) / 8), 256, 0, st>>>(ids, B, S, off, Lloc, Lc, C, w.row_slots,
-                                                                          w.row_locs, w.row_cofs);
-    ASTRA_LAUNCHED("row_bucket");
-    ASTRA_TRY(check_cuda(cudaMemsetAsync(w.bar, 0, 8 * sizeof(unsigned), st), "memset barrier + bounds"));
-    if (piped)
-      ASTRA_TRY(check_cuda(cudaMemsetAsync(w.pipe_ctr, 0, sizeof(unsigned) * (2 * kMaxChunks + 4), st), "memset pipe"));
-    FusedArgs A;
-    A.f = fa;
-    A.u = ua;
-    A.C = C;
-    A.Lc = Lc;
-    A.uc = w.uc;
-    A.row_slots = w.row_slots;
-    A.row_locs = w.row_locs;
-    A.row_cofs = w.row_cofs;
-    A.w_absmax = w_absmax;
-    A.bar = w.bar;
-    A.sf_acc = w.sf_acc;
-    A.emax_acc = w.emax_acc;
-    if (piped) {
-      PipeArgs P;
-      P.x = A;
-      P.rows_f = pipe_nf;
-      P.done = w.pipe_ctr;
-      P.udone = w.pipe_ctr + kMaxChunks;
-      static const int throttle_env = [] {
-        const char* e = getenv("ASTRA_STEP_PIPE_THROTTLE");
-        return e ? atoi(e) : 0;
-      }();
-      P.throttle = throttle_env;
-      P.ready = w.pipe_ctr + 2 * kMaxChunks;
-      KernelTimer kt("step_pipe", st);
-      ASTRA_TRY(bf16 ? (adam ? launch_pipe_nv<true, true>(nv, P, pipe_grid_ctas, st)
-                             : launch_pipe_nv<true, false>(nv, P, pipe_grid_ctas, st))
-                     : (adam ? launch_pipe_nv<false, true>(nv, P, pipe_grid_ctas, st)
-                             : launch_pipe_nv<false, false>(nv, P, pipe_grid_ctas, st)));
-    } else {
-      KernelTimer kt("step_fused", st);
-      int rc = bf16 ? (adam ? launch_fused_nv<true, true>(nv, A, st) : launch_fused_nv<true, false>(nv, A, st))
-                    : (adam ? launch_fused_nv<false, true>(nv, A, st) : launch_fused_nv<false, false>(nv, A, st));
-      if (rc != ASTRA_OK) return rc == ASTRA_ERR_CONFIG ? set_error(rc, "fused step: grid too small") : rc;
-    }
-    finalize_kernel<<<1, 1024, 0, st>>>(w.loss_rows, w.bound_rows, B, loss_out, status);
-    ASTRA_LAUNCHED("finalize");
-    return ASTRA_OK;
-  }
   const int upd_ctas = 16 * sms;
   KernelTimer kt_upd("label_update", st);
   if (optimizer == ASTRA_OPT_ADAM)

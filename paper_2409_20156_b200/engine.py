@@ -163,7 +163,12 @@ class ClassifierEngine:
     # ------------------------------------------------------------ step
     def step(self, emb: torch.Tensor, slates, lr: float, weight_decay: float, keep=None, factors_in=None):
         """Fused sampled-BCE step on this shard. Returns (loss_dev fp64[1],
-        grad_emb of this rank's rows, status int32[4]). No host sync."""
+        grad_emb of this rank's rows, status int32[4]). No host sync.
+        Finiteness (classifiers.py:79-80: nothing written on a non-finite
+        gradient) is guaranteed per shard: each shard checks its own rows'
+        gradients before writing them; the all-reduced status reports a
+        failure on any shard, but another shard may have applied its (finite)
+        rows by then."""
         ids, y, origin, weights = slates
         emb_all = self.comm.all_gather(emb)
         keep_all = self.comm.all_gather(keep) if keep is not None else None
@@ -235,7 +240,10 @@ class ClassifierEngine:
         return out, status
 
     def wait_host_outputs(self) -> None:
-        """Make the current stream wait for every D2H issued by the host API."""
+        """Make the current stream wait for every D2H issued by the host API.
+        This only orders the streams: the host may read the `out` buffers
+        after a synchronize of the current stream (or of an event recorded on
+        it after this call)."""
         for pipe in getattr(self, "_pipes", {}).values():
             torch.cuda.current_stream().wait_stream(pipe.d2h)
 
@@ -288,6 +296,9 @@ class ClassifierEngine:
 
         fn = path if self.comm.world == 1 else f"{path}.rank{self.comm.rank}"
         hsize = struct.calcsize(self._CKPT_HEAD)
+        import os
+
+        fsize = os.path.getsize(fn)
         with open(fn, "rb") as fh:
             head = fh.read(hsize)
             if len(head) != hsize:
@@ -305,6 +316,8 @@ class ClassifierEngine:
                 raise ConfigError("shard checkpoint dtype / optimizer does not match this engine")
             rows = hi - lo
             wb = rows * dim * (2 if bf16 else 4)
+            if fsize != hsize + wb + (2 * rows * dim * 4 if adam else 0):
+                raise DataError("truncated or oversized shard checkpoint")  # nothing restored
             buf = fh.read(wb)
             if len(buf) != wb:
                 raise DataError("truncated shard checkpoint")
@@ -319,6 +332,9 @@ class ClassifierEngine:
                     dst.copy_(torch.from_numpy(np.frombuffer(buf, dtype=np.float32).reshape(rows, dim).copy()))
         self.adam_step = int(adam_step)
         self.w_absmax.fill_(float(w_absmax))
+        # the refresh snapshot is not part of the file: drop any snapshot of the
+        # previous weights (snapshot() rebuilds it from the restored W)
+        self.snap_f32 = self.snap_bf16 = None
         self.snapshot_epoch = int(snap)
 
 

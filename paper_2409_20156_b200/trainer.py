@@ -39,22 +39,14 @@ from .errors import ConfigError, NumericalError
 # label-major pass instead (same W', grad_emb summed in arrival order).
 FAST_STEP = os.environ.get("ASTRA_DROPIN_FAST_STEP") == "1"
 
-_HARD_ONLY = {"StaleHard", "UpToDateHard", "LabelEmbHard"}
-_MIXTURES = {"Mixture", "LabelEmbMixture"}
 
 
 def curriculum_counts(epoch: int, strategy, tau_s: int) -> tuple[int, int]:
-    """Effective (hard, random) slot counts, restating sampler.py:82-94."""
-    total = strategy.k_h + strategy.k_r
-    if epoch < tau_s or strategy.kind == "RandomOnly":
-        return 0, total
-    if strategy.kind in _HARD_ONLY:
-        return total, 0
-    if strategy.kind in _MIXTURES:
-        return strategy.k_h, strategy.k_r
-    frac = min(1.0, (epoch - tau_s) / strategy.curriculum_ramp)
-    k_h_eff = int(round(strategy.k_h * frac))
-    return k_h_eff, total - k_h_eff
+    """Effective (hard, random) slot counts: the caller's own
+    xcmix.sampler.curriculum_counts (sampler.py:82-94), not a restatement."""
+    from xcmix.sampler import curriculum_counts as reference_counts
+
+    return reference_counts(epoch, strategy, tau_s)
 
 
 def _positives_csr(state, batch_rows):

@@ -99,3 +99,24 @@ def test_shard_checkpoint_rejects_mismatch(tmp_path):
 @pytest.mark.parametrize("w_dtype", [torch.float32, torch.bfloat16])
 def test_shard_checkpoint_roundtrip_gpu(tmp_path, cuda_lib, w_dtype):
     _roundtrip(tmp_path, "cuda", None, "adam", w_dtype)
+
+
+def test_truncated_checkpoint_restores_nothing(tmp_path):
+    """A truncated file raises DataError before anything is written: W, the
+    bound and the snapshot of the target engine are left as they were."""
+    a = _engine(optimizer="sgd")
+    path = str(tmp_path / "t.xash")
+    a.save_shard(path)
+    data = open(path, "rb").read()
+    open(path, "wb").write(data[:-100])
+    b = _engine(optimizer="sgd")
+    b.W.mul_(2.0)
+    b.w_absmax.fill_(9.0)
+    b.snapshot(0)
+    before = b.W.clone()
+    with pytest.raises(DataError):
+        b.load_shard(path)
+    assert torch.equal(b.W, before) and float(b.w_absmax.item()) == 9.0 and b.snap_f32 is not None
+    open(path, "wb").write(data)
+    b.load_shard(path)
+    assert torch.equal(b.W, a.W) and b.snap_f32 is None  # the stale snapshot is dropped

@@ -376,18 +376,16 @@ def test_apply_updates_golden_bitexact(cuda_lib):
     np.testing.assert_array_equal(W2.cpu().numpy(), g["W_before"])
 
 
-@pytest.mark.parametrize("fused", ["0", "1", "pipe", "two_kernel"])
+@pytest.mark.parametrize("fused", ["single", "two_kernel"])
 def test_engine_step_schedules_agree(cuda_lib, fused):
     """The engine step (w_absmax bound maintained) under the single label-major
-    pass (default), the two-kernel TMA path and the persistent L2-chunked
-    schedules matches the reference arithmetic (oracle port) on the same slates."""
+    pass (default) and the two-kernel TMA schedule matches the reference
+    arithmetic (oracle port) on the same slates."""
     import subprocess
     import sys
 
     code = f"""
 import os, sys
-os.environ["ASTRA_STEP_FUSED"] = "1" if "{fused}" == "1" else "0"
-os.environ["ASTRA_STEP_PIPE"] = "1" if "{fused}" == "pipe" else "0"
 os.environ["ASTRA_STEP_SINGLE"] = "0" if "{fused}" == "two_kernel" else "1"
 sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {ROOT!r} + "/tests")
 import numpy as np, torch
@@ -442,6 +440,9 @@ def test_host_api_pipelined_equals_device_api(cuda_lib):
         pid = np.concatenate(pos)
         pin = lambda x: torch.from_numpy(x).pin_memory()  # noqa: E731
         ids_h = a.refresh_host(pin(emb), pin(ip), pin(pid), k_h)
+        if t == 0:  # the D2H runs on the pipe's stream: order it, then wait, before the host reads
+            a.wait_host_outputs()
+            torch.cuda.current_stream().synchronize()
         hard = torch.from_numpy(ids_h.numpy().copy()) if t == 0 else hard
         (ge_h, loss_h), _ = a.train_step_host(pin(emb), pin(rows), pin(ip), pin(pid), hard.pin_memory(), 1, t, 0.05, 1e-4)
         a.wait_host_outputs()
