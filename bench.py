@@ -49,7 +49,18 @@ sys.path.insert(0, ROOT)
 CFG = dict(workload="LF-AmazonTitles-1.3M shape, synthetic", L=1_305_265, d=768, N=2_248_619, B=1024,
            minibatches=9, k_p=8, k_h=64, k_r=512, labels_per_point=38, tau_r=1, lr=0.05, wd=1e-4)
 METRIC = "ASTRA train samples/s (shortlist+loss+update)"
+REFRESH_MODE = ["bf16_rerank"]  # set from --refresh-mode
 UNIT = "samples/s"
+
+
+def fp8_peak(tf_burst):
+    """Dense e4m3 denominator: the measured cuBLASLt figure (scripts/fp8_peak.py
+    -> profiles/fp8_peak.json, measured on this pool's B200), else 2 x the
+    measured bf16 burst."""
+    p = os.path.join(ROOT, "profiles", "fp8_peak.json")
+    if os.path.exists(p):
+        return json.load(open(p))["fp8_e4m3_tflops"], "measured here (cuBLASLt e4m3 8192^3 burst, profiles/fp8_peak.json)"
+    return 2.0 * tf_burst, "2 x the measured bf16 burst (no measured fp8 figure)"
 
 
 def peaks():
@@ -120,7 +131,7 @@ def bench_config(world: int) -> dict:
             "minibatch": c["B"], "minibatches_per_step": c["minibatches"], "global_batch": c["B"] * world,
             "k_p": c["k_p"], "k_h": c["k_h"], "k_r": c["k_r"], "slate": c["k_p"] + c["k_h"] + c["k_r"],
             "labels_per_point": c["labels_per_point"], "tau_r": c["tau_r"], "refresh_chunk": R * world,
-            "refresh_mode": "bf16_rerank", "optimizer": "sgd+wd", "parallelism": f"label-shard{world}",
+            "refresh_mode": REFRESH_MODE[0], "optimizer": "sgd+wd", "parallelism": f"label-shard{world}",
             "l2": "inputs larger than L2 (W fp32 4.0 GB + snapshots 6 GB)"}
 
 
@@ -180,7 +191,7 @@ def run_ours(args):
     R = B * M  # rows per step per GPU (refresh chunk)
     hbm, tf_burst, tf_sus, peak_kind = peaks()
 
-    eng = ClassifierEngine(L, d, k_p=k_p, k_h=k_h, k_r=k_r, seed=0, refresh_mode="bf16_rerank")
+    eng = ClassifierEngine(L, d, k_p=k_p, k_h=k_h, k_r=k_r, seed=0, refresh_mode=args.refresh_mode)
     eng.snapshot(epoch=0)
     L_loc = eng.hi - eng.lo
     rng = np.random.default_rng(1000 + rank)
@@ -217,12 +228,12 @@ def run_ours(args):
     if overlap:
         _lib.set_refresh_sm_budget(args.refresh_sms)
 
-    def one(t, timed):
+    def one(t, timed, mode=None):
         st, e = dev[t], ev[t]
         e[0].record(stream)
         rstream.wait_stream(stream)
         with torch.cuda.stream(rstream):
-            eng.refresh(st["chunk"]["emb"], st["chunk"]["indptr"], st["chunk"]["pos"], k_h)
+            eng.refresh(st["chunk"]["emb"], st["chunk"]["indptr"], st["chunk"]["pos"], k_h, mode=mode)
             e[1].record(rstream)
         for i, m in enumerate(st["mbs"]):
             slates = eng.sample(m["rows"], m["indptr"], m["pos"], m["hard"], epoch=1, step=t * M + i)
@@ -284,6 +295,11 @@ def run_ours(args):
     gemm_ms, gemm_n = kt["refresh_gemm"]
     t_gemm = gemm_ms / max(gemm_n, 1) / 1e3
     achieved_tf = flops / t_gemm / 1e12
+    if args.refresh_mode == "fp8_rerank":
+        f8, peak_kind_gemm = fp8_peak(tf_burst)
+        tf_sus, tf_burst = tf_sus * f8 / tf_burst, f8  # (sustained: the bf16 sustained/burst ratio)
+    else:
+        peak_kind_gemm = f"{peak_kind} burst bf16 (each launch is timed on its own)"
     t_ref = ph["refresh"] / K / 1e3
     # step roofline: BASELINE.md bytes formula (U unique rows, fp32 SGD: read+write)
     U = [int(torch.unique(ids[(ids >= eng.lo) & (ids < eng.hi)]).numel()) for ids in ids_keep]
@@ -317,13 +333,52 @@ def run_ours(args):
     # tests/test_gpu_refresh_scale.py) on every query of the chunk
     st = dev[n_steps - 1]["chunk"]
     prod_ids, _ = eng.refresh(st["emb"], st["indptr"], st["pos"], k_h)
-    flagged = ops.refresh_flagged(R * world, L_loc, d, k_h, "bf16_rerank")
+    flagged = ops.refresh_flagged(R * world, L_loc, d, k_h, args.refresh_mode)
     exact_ids, _ = eng.refresh(st["emb"], st["indptr"], st["pos"], k_h, mode="fp32")
     same = prod_ids == exact_ids
     hits = (prod_ids.unsqueeze(2) == exact_ids.unsqueeze(1)).any(2).sum(1).double() / k_h
     refresh_parity = {"vs": "fp32-exact mode (= C oracle arithmetic)", "queries": int(prod_ids.shape[0]),
                       "recall_at_k": round(float(hits.mean()), 6), "rows_bit_exact": round(float(same.all(1).double().mean()), 6),
                       "flagged_for_verify": int(flagged)}
+    # the same job with the e4m3 candidate pass (kind::f8f6f4, twice the
+    # tensor rate; fp32-exact re-rank of k' = 2k candidates): an extension
+    # beside the north star's bf16 line, with its own parity on the same chunk
+    alt_fp8 = None
+    if not args.no_alt_fp8 and args.refresh_mode != "fp8_rerank" and d % 128 == 0 and eng.snap_f32 is not None:
+        eng.snap_f8 = ops.quantize_e4m3(eng.snap_f32)
+        for t in range(min(2, args.warmup)):
+            one(t, False, mode="fp8_rerank")
+        torch.cuda.synchronize()
+        eng.comm.barrier()
+        _lib.kernel_timing("refresh_gemm")
+        _lib.kernel_timing_enable(True)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for t in range(args.warmup, n_steps):
+            one(t, False, mode="fp8_rerank")
+        a1.record(stream)
+        torch.cuda.synchronize()
+        eng.comm.barrier()
+        _lib.kernel_timing_enable(False)
+        g8_ms, g8_n = _lib.kernel_timing("refresh_gemm")
+        ms8 = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ms8, op=dist.ReduceOp.MAX)
+        ms8 = float(ms8.item())
+        r_ms = sum(ev[t][0].elapsed_time(ev[t][1]) for t in range(args.warmup, n_steps)) / K
+        f8_ids, _ = eng.refresh(st["emb"], st["indptr"], st["pos"], k_h, mode="fp8_rerank")
+        hits8 = (f8_ids.unsqueeze(2) == exact_ids.unsqueeze(1)).any(2).sum(1).double() / k_h
+        f8_peak_tf, f8_kind = fp8_peak(tf_burst)
+        ach8 = flops / (g8_ms / max(g8_n, 1) / 1e3) / 1e12
+        alt_fp8 = {"refresh_mode": "fp8_rerank", "value": round(R * world * K / (ms8 / 1e3), 1), "unit": UNIT,
+                   "ms_per_step": round(ms8 / K, 4), "refresh_ms_per_step": round(r_ms, 4),
+                   "refresh_parity": {"recall_at_k": round(float(hits8.mean()), 6),
+                                      "rows_bit_exact": round(float((f8_ids == exact_ids).all(1).double().mean()), 6)},
+                   "roofline": {"bound": "tensor", "achieved": round(ach8, 2), "peak": f8_peak_tf, "unit": "TFLOP/s",
+                                "frac": round(ach8 / f8_peak_tf, 4), "launch_ms": round(g8_ms / max(g8_n, 1), 4),
+                                "peak_kind": f8_kind},
+                   "note": "not the headline: the north star specifies the bf16 candidate pass"}
+        eng.snap_f8 = None
     del exact_ids
     # end-to-end: the public API with HOST buffers (pinned), copies inside the timed region
     pinned = []
@@ -371,7 +426,7 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": round(ms_total / K, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp32 W/step, bf16 tensor-core refresh + fp32 re-rank", "data": "synthetic",
+        "dtype": f"fp32 W/step, {args.refresh_mode.split('_')[0]} tensor-core refresh + fp32 re-rank", "data": "synthetic",
         "config": dict(bench_config(world), refresh_overlap=overlap,
                        refresh_sms=args.refresh_sms if overlap else None),
         "phases_ms_per_step": {k: round(v / K, 4) for k, v in ph.items()},
@@ -380,6 +435,7 @@ def run_ours(args):
         # tiles holding a flagged query): ~0 when every query was proven exact
         "refresh_verify_ms": round(kt["refresh_verify"][0] / max(kt["refresh_verify"][1], 1), 4),
         "refresh_parity": refresh_parity,
+        "alt_fp8_refresh": alt_fp8,
         "step_only_samples_per_s": round(B * world / (t_step + t_samp), 1),
         "composite_tau_r5_samples_per_s": round(R * world / (M * (t_step + t_samp) + t_ref / 5), 1),
         "roofline": {"bound": "tensor", "kernel": "refresh_tc_kernel threshold pass (tcgen05 bf16 GEMM + fused candidate epilogue)",
@@ -387,9 +443,10 @@ def run_ours(args):
                      "frac": round(achieved_tf / tf_burst, 4), "traffic": traffic.get("refresh_gemm"),
                      "frac_of_sustained_peak": round(achieved_tf / tf_sus, 4),
                      "algorithmic": f"2*L_shard*d*Q = {flops:.3e} flop per launch (Q={q_per_refresh})",
+                     "operands": args.refresh_mode.split("_")[0],
                      "launch_ms": round(t_gemm * 1e3, 4), "launches": gemm_n,
                      "share_of_refresh": round(t_gemm / t_ref, 4),
-                     "peak_kind": f"{peak_kind} burst bf16 (each launch is timed on its own, ~12 ms)"},
+                     "peak_kind": peak_kind_gemm},
         "roofline_step": {"bound": "hbm", "kernel": step_kernel_desc,
                           "achieved": round(step_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(step_gbs / hbm, 4),
                           "algorithmic": f"U*d*8 + 2*B*d*4 + B*S*5 = {step_bytes:.3e} B (U={U_mean:.0f})",
@@ -444,7 +501,9 @@ def run_emulate(args):
     W = init_uniform_scaled(Lr, d, 1, "cuda")
     w_absmax = W.abs().amax().reshape(1).float()
     snap_f32 = W.clone()
-    snap_bf16 = ops.f32_to_bf16(snap_f32)
+    fp8 = args.refresh_mode == "fp8_rerank"
+    snap_lp = ops.quantize_e4m3(snap_f32) if fp8 else ops.f32_to_bf16(snap_f32)
+    lp = {"labels_e4m3": snap_lp} if fp8 else {"labels_bf16": snap_lp}
     g = torch.Generator(device="cuda")
     g.manual_seed(1)
     n_steps = args.warmup + args.steps
@@ -479,8 +538,7 @@ def run_emulate(args):
         q, pid, hard = data[t]
         e = ev[t]
         e[0].record(stream)
-        keys, _, _ = ops.refresh_topk(q, ip_step, pid, k_h, "bf16_rerank", labels_f32=snap_f32, labels_bf16=snap_bf16,
-                                      label_offset=lo)
+        keys, _, _ = ops.refresh_topk(q, ip_step, pid, k_h, args.refresh_mode, labels_f32=snap_f32, label_offset=lo, **lp)
         e[1].record(stream)
         ops.topk_merge(keys.view(N, R, k_h), k_h)  # the N shards' lists of this rank's R rows
         e[2].record(stream)
@@ -972,9 +1030,14 @@ def main():
     ap.add_argument("--emulate", type=int, default=0,
                     help="one GPU runs rank 0's share of an N-GPU C4 job (a 1/N label shard, all N ranks' rows); "
                          "collectives are not run, their bytes are reported")
+    ap.add_argument("--refresh-mode", default="bf16_rerank", choices=["bf16_rerank", "fp8_rerank"],
+                    help="tensor-core candidate pass of the refresh (bf16 = the north star's, or e4m3 at twice the "
+                         "tensor rate), then the fp32-exact re-rank")
+    ap.add_argument("--no-alt-fp8", action="store_true", help="skip the e4m3-refresh comparison object")
     ap.add_argument("--slate-exchange", default="gather", choices=["gather", "regenerate"],
                     help="--emulate: how the N-GPU job shares slates (engine.ClassifierEngine.slate_exchange)")
     args = ap.parse_args()
+    REFRESH_MODE[0] = args.refresh_mode
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.gpus < 1:

@@ -51,6 +51,7 @@ extern "C" {
 #define ASTRA_REFRESH_FP32_EXACT 0  /* SIMT fmaf, fixed k order: bit-exact ids    */
 #define ASTRA_REFRESH_BF16 1        /* tcgen05 bf16 GEMM + top-k epilogue         */
 #define ASTRA_REFRESH_BF16_RERANK 2 /* bf16 top-k' then fp32-exact re-rank to k   */
+#define ASTRA_REFRESH_FP8_RERANK 3  /* e4m3 top-k' (2x tensor rate) then re-rank   */
 
 /* Classifier storage / optimizer. */
 #define ASTRA_W_FP32 0
@@ -118,21 +119,34 @@ int astra_f32_to_bf16(const float* src, uint16_t* dst, int64_t n, void* stream);
  *   labels_f32    n_labels x d fp32 snapshot (FP32_EXACT, BF16_RERANK; for
  *                 BF16_RERANK it may be NULL: the re-rank then scores the bf16
  *                 snapshot's values exactly — the bf16-W configuration)
- *   labels_bf16   n_labels x d bf16 snapshot (BF16, BF16_RERANK)
+ *   labels_bf16   n_labels x d bf16 snapshot (BF16, BF16_RERANK; the re-rank
+ *                 rows of FP8_RERANK when labels_f32 is NULL)
+ *   labels_e4m3   n_labels x d e4m3 snapshot (FP8_RERANK: astra_quantize_e4m3),
+ *                 or NULL
  *   pos_indptr    nq+1 int64, pos_ids int32 GLOBAL ids sorted ascending per row
  *   out_keys      nq x k packed keys (input of astra_topk_merge), or NULL
  *   out_ids       nq x k int32 global ids, or NULL
- *   out_scores    nq x k fp32 scores (fp32-exact in modes 0/2), or NULL
+ *   out_scores    nq x k fp32 scores (fp32-exact in modes 0/2/3), or NULL
  * A query with fewer than k admissible labels in the shard is padded with
  * key 0 / id -1 / score -inf (the cross-shard merge then fills it).
- * Constraints: 1 <= k <= 2048; BF16 modes need d % 64 == 0.
+ * Constraints: 1 <= k <= 2048; BF16 modes need d % 64 == 0; FP8_RERANK needs
+ * d % 128 == 0, k <= 240 (k' = max(2k, k+32) <= 512) and fp32 queries.
  * ------------------------------------------------------------------------ */
 size_t astra_refresh_workspace_size(int64_t nq, int64_t n_labels, int d, int k, int mode);
 int astra_refresh_topk(const float* queries_f32, const uint16_t* queries_bf16, int64_t nq, int d,
-                       const float* labels_f32, const uint16_t* labels_bf16, int64_t n_labels,
-                       int64_t label_offset, const int64_t* pos_indptr, const int32_t* pos_ids,
-                       int k, int mode, uint64_t* out_keys, int32_t* out_ids, float* out_scores,
-                       void* workspace, size_t workspace_bytes, void* stream);
+                       const float* labels_f32, const uint16_t* labels_bf16, const uint8_t* labels_e4m3,
+                       int64_t n_labels, int64_t label_offset, const int64_t* pos_indptr,
+                       const int32_t* pos_ids, int k, int mode, uint64_t* out_keys, int32_t* out_ids,
+                       float* out_scores, void* workspace, size_t workspace_bytes, void* stream);
+
+/* The e4m3 label snapshot for ASTRA_REFRESH_FP8_RERANK (build_exact's copy,
+ * anns.py:99-100, in the tensor cores' 8-bit format): n values of src (fp32,
+ * or bf16 when src_bf16; n % 4 == 0, 16-byte aligned) -> dst bytes
+ * e4m3(x * 448 / max|x|), round-to-nearest-even, saturating. max|x| is
+ * reduced on the device (no host sync); scratch = 2 device floats, scratch[1]
+ * receives the scale. One scale for all labels multiplies every score alike,
+ * so rankings are those of the unscaled e4m3 values. */
+int astra_quantize_e4m3(const void* src, int src_bf16, int64_t n, uint8_t* dst, float* scratch, void* stream);
 
 /* Diagnostic of the last astra_refresh_topk call made with `workspace` and
  * the same (nq, n_labels, d, k, mode): how many queries the two-pass plan

@@ -32,7 +32,8 @@ _SIGS = {
     "astra_set_step_deterministic": ([i32], None),
     "astra_f32_to_bf16": ([p, p, i64, p], i32),
     "astra_refresh_workspace_size": ([i64, i64, i32, i32, i32], sz),
-    "astra_refresh_topk": ([p, p, i64, i32, p, p, i64, i64, p, p, i32, i32, p, p, p, p, sz, p], i32),
+    "astra_refresh_topk": ([p, p, i64, i32, p, p, p, i64, i64, p, p, i32, i32, p, p, p, p, sz, p], i32),
+    "astra_quantize_e4m3": ([p, i32, i64, p, p, p], i32),
     "astra_refresh_flagged": ([p, sz, i64, i64, i32, i32, i32, p, p], i32),
     "astra_merge_workspace_size": ([i64, i32], sz),
     "astra_topk_merge": ([p, i64, i32, i32, i32, p, p, p, p, sz, p], i32),

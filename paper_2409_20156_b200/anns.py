@@ -94,17 +94,27 @@ def refresh_mode_for(d: int, n_labels: int) -> str:
 
 
 def _device_snapshot(index: AnnsIndex, mode: str):
-    """fp32 (+ bf16) device copies of the immutable index, cached on the index."""
+    """Device copies of the immutable index (build_exact copies and freezes its
+    vectors, anns.py:90-100), cached on the index: fp32, plus the bf16 or e4m3
+    copy the tensor-core candidate pass reads. Returns the refresh_topk label
+    keyword arguments for `mode`."""
     ops = _backend.get()
     dev = _backend.device()
     snap = getattr(index, "_astra_snapshot", None)
-    if snap is None or snap[0] is not index.vectors or snap[1] != dev:
+    if snap is None or snap["vectors"] is not index.vectors or snap["dev"] != dev:
         w32 = torch.from_numpy(np.ascontiguousarray(index.vectors, dtype=np.float32)).to(dev)
-        snap = [index.vectors, dev, w32, None]
+        snap = {"vectors": index.vectors, "dev": dev, "f32": w32}
         index._astra_snapshot = snap
-    if mode != "fp32" and snap[3] is None:
-        snap[3] = ops.f32_to_bf16(snap[2])
-    return snap[2], snap[3]
+    labels = {"labels_f32": snap["f32"]}
+    if mode in ("bf16", "bf16_rerank"):
+        if "bf16" not in snap:
+            snap["bf16"] = ops.f32_to_bf16(snap["f32"])
+        labels["labels_bf16"] = snap["bf16"]
+    elif mode == "fp8_rerank":
+        if "e4m3" not in snap:
+            snap["e4m3"] = ops.quantize_e4m3(snap["f32"])
+        labels["labels_e4m3"] = snap["e4m3"]
+    return labels
 
 
 def positives_csr(positives, rows=None):
@@ -136,8 +146,8 @@ def retrieve_hard_negatives(index, embeddings, positives, k_h: int, query_beam: 
     ops = _backend.get()
     L, d = index.vectors.shape
     mode = mode or refresh_mode_for(d, L)
-    w32, wbf = _device_snapshot(index, mode)
-    dev = w32.device
+    labels = _device_snapshot(index, mode)
+    dev = labels["labels_f32"].device
     E = np.ascontiguousarray(embeddings, dtype=np.float32)
     out = np.empty((N, k_h), dtype=np.int32)
     for lo in range(0, N, QUERY_CHUNK):
@@ -145,7 +155,7 @@ def retrieve_hard_negatives(index, embeddings, positives, k_h: int, query_beam: 
         indptr, ids = positives_csr(positives[lo:hi])
         _, top, _ = ops.refresh_topk(
             torch.from_numpy(E[lo:hi]).to(dev), torch.from_numpy(indptr).to(dev), torch.from_numpy(ids).to(dev),
-            k_h, mode, labels_f32=w32, labels_bf16=wbf)
+            k_h, mode, **labels)
         out[lo:hi] = top.cpu().numpy()
     return NegativeCache(out, index.snapshot_epoch)
 
@@ -162,8 +172,8 @@ def query_topk_batch(index, queries, k: int, mode: str | None = None):
     ops = _backend.get()
     L, d = index.vectors.shape
     mode = mode or os.environ.get("ASTRA_QUERY_MODE", "fp32")
-    w32, wbf = _device_snapshot(index, mode)
-    dev = w32.device
+    labels = _device_snapshot(index, mode)
+    dev = labels["labels_f32"].device
     Q = np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32)
     N = Q.shape[0]
     ids = np.empty((N, k), dtype=np.int64)
@@ -172,8 +182,7 @@ def query_topk_batch(index, queries, k: int, mode: str | None = None):
         hi = min(N, lo + QUERY_CHUNK)
         indptr = torch.zeros(hi - lo + 1, dtype=torch.int64, device=dev)
         pid = torch.zeros(0, dtype=torch.int32, device=dev)
-        _, top, sc = ops.refresh_topk(torch.from_numpy(Q[lo:hi]).to(dev), indptr, pid, k, mode, labels_f32=w32,
-                                      labels_bf16=wbf)
+        _, top, sc = ops.refresh_topk(torch.from_numpy(Q[lo:hi]).to(dev), indptr, pid, k, mode, **labels)
         ids[lo:hi] = top.cpu().numpy()
         scores[lo:hi] = sc.cpu().numpy()
     return ids, scores

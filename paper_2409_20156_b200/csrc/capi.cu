@@ -59,8 +59,10 @@ int num_sms() {
 // defined in the kernel translation units
 int f32_to_bf16(const float*, uint16_t*, int64_t, cudaStream_t);
 size_t refresh_workspace_size(int64_t, int64_t, int, int, int);
-int refresh_topk(const float*, const uint16_t*, int64_t, int, const float*, const uint16_t*, int64_t, int64_t,
-                 const int64_t*, const int32_t*, int, int, uint64_t*, int32_t*, float*, void*, size_t, cudaStream_t);
+int refresh_topk(const float*, const uint16_t*, int64_t, int, const float*, const uint16_t*, const uint8_t*, int64_t,
+                 int64_t, const int64_t*, const int32_t*, int, int, uint64_t*, int32_t*, float*, void*, size_t,
+                 cudaStream_t);
+int quantize_e4m3(const void*, int, int64_t, uint8_t*, float*, cudaStream_t);
 int topk_merge(const uint64_t*, int64_t, int, int, int, uint64_t*, int32_t*, float*, uint64_t*, cudaStream_t);
 int refresh_flagged(const void*, size_t, int64_t, int64_t, int, int, int, int64_t*, cudaStream_t);
 int sample_slates(uint64_t, uint32_t, uint32_t, const int64_t*, int, const int64_t*, const int32_t*, const int32_t*,
@@ -135,11 +137,17 @@ size_t astra_refresh_workspace_size(int64_t nq, int64_t n_labels, int d, int k, 
 }
 
 int astra_refresh_topk(const float* queries_f32, const uint16_t* queries_bf16, int64_t nq, int d,
-                       const float* labels_f32, const uint16_t* labels_bf16, int64_t n_labels, int64_t label_offset,
-                       const int64_t* pos_indptr, const int32_t* pos_ids, int k, int mode, uint64_t* out_keys,
-                       int32_t* out_ids, float* out_scores, void* workspace, size_t workspace_bytes, void* stream) {
-  return refresh_topk(queries_f32, queries_bf16, nq, d, labels_f32, labels_bf16, n_labels, label_offset, pos_indptr,
-                      pos_ids, k, mode, out_keys, out_ids, out_scores, workspace, workspace_bytes, S(stream));
+                       const float* labels_f32, const uint16_t* labels_bf16, const uint8_t* labels_e4m3,
+                       int64_t n_labels, int64_t label_offset, const int64_t* pos_indptr, const int32_t* pos_ids,
+                       int k, int mode, uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  return refresh_topk(queries_f32, queries_bf16, nq, d, labels_f32, labels_bf16, labels_e4m3, n_labels, label_offset,
+                      pos_indptr, pos_ids, k, mode, out_keys, out_ids, out_scores, workspace, workspace_bytes,
+                      S(stream));
+}
+
+int astra_quantize_e4m3(const void* src, int src_bf16, int64_t n, uint8_t* dst, float* scratch, void* stream) {
+  return quantize_e4m3(src, src_bf16, n, dst, scratch, S(stream));
 }
 
 int astra_refresh_flagged(const void* workspace, size_t workspace_bytes, int64_t nq, int64_t n_labels, int d, int k,

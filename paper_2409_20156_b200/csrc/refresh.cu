@@ -12,11 +12,19 @@
 //               fmaf chain over t = 0..d-1, so ids are bit-identical to
 //               oracle_refresh_fp32.
 //   BF16        tcgen05 kernel (refresh_tc.cu), bf16 operands, fp32 accum.
-//   BF16_RERANK tcgen05 top-k' (k' = 2k) then the k' candidates are re-scored
-//               with the same sequential fmaf chain and re-ranked: equal to
-//               FP32_EXACT whenever the exact top-k lies inside the top-k'.
-#include <vector>
+//   BF16_RERANK tcgen05 top-k' (k' = max(1.5k, k+16)) then the k' candidates
+//               are re-scored with the same sequential fmaf chain and
+//               re-ranked: equal to FP32_EXACT whenever the exact top-k lies
+//               inside the top-k'.
+//   FP8_RERANK  the same pipeline on e4m3 operands (kind::f8f6f4, twice the
+//               tensor rate): queries quantised per row here, labels from the
+//               caller's e4m3 snapshot (astra_quantize_e4m3, one global
+//               scale); a per-query / global scale does not change a query's
+//               ranking. k' = max(2k, k+32) for the coarser candidate scores.
+#include <cuda_fp8.h>
 #include <math.h>
+
+#include <vector>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -477,6 +485,75 @@ __global__ void f32_to_bf16_kernel(const float* src, uint16_t* dst, int64_t n) {
   }
 }
 
+// ------------------------------------------------------------- e4m3 quantisation
+__device__ __forceinline__ uint32_t e4m3x4(float a, float b, float c, float e) {
+  const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+  const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(make_float2(c, e), __NV_SATFINITE, __NV_E4M3);
+  return static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+}
+
+// Query rows -> e4m3 with a per-row scale 448 / max|row| (warp per row,
+// d % 128 == 0). The scale multiplies every score of the row alike, so the
+// row's ranking is that of the unscaled products.
+__global__ void quant_rows_e4m3_kernel(const float* __restrict__ src, int64_t rows, int d, uint8_t* __restrict__ dst) {
+  const int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* x = src + r * d;
+  float m = 0.0f;
+  for (int t = lane * 4; t < d; t += 128) {
+    const float4 v = *reinterpret_cast<const float4*>(x + t);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float sc = m > 0.0f && isfinite(m) ? 448.0f / m : 1.0f;
+  for (int t = lane * 4; t < d; t += 128) {
+    const float4 v = *reinterpret_cast<const float4*>(x + t);
+    *reinterpret_cast<uint32_t*>(dst + r * d + t) = e4m3x4(v.x * sc, v.y * sc, v.z * sc, v.w * sc);
+  }
+}
+
+template <bool BF16>
+__device__ __forceinline__ float4 load4(const void* src, int64_t i) {
+  if constexpr (BF16) {
+    const uint2 u = *reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(src) + i);
+    return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                       __uint_as_float(u.y & 0xFFFF0000u));
+  } else {
+    return *reinterpret_cast<const float4*>(static_cast<const float*>(src) + i);
+  }
+}
+
+// max|x| over n values (n % 4 == 0) into scratch[0] (as bits; non-negative
+// floats order as unsigned integers; a NaN reads as the largest)
+template <bool BF16>
+__global__ void absmax_kernel(const void* src, int64_t n, unsigned* out_bits) {
+  float m = 0.0f;
+  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 4; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x * 4) {
+    const float4 v = load4<BF16>(src, i);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, __float_as_uint(m));
+}
+
+// x * scale -> e4m3, scale = 448 / max|x| read from scratch (1 when 0 or not finite)
+template <bool BF16>
+__global__ void quant_e4m3_kernel(const void* src, int64_t n, const unsigned* max_bits, float* scale_out,
+                                  uint8_t* dst) {
+  const float m = __uint_as_float(*max_bits);
+  const float sc = m > 0.0f && isfinite(m) ? 448.0f / m : 1.0f;
+  if (scale_out && blockIdx.x == 0 && threadIdx.x == 0) *scale_out = sc;
+  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 4; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x * 4) {
+    const float4 v = load4<BF16>(src, i);
+    *reinterpret_cast<uint32_t*>(dst + i) = e4m3x4(v.x * sc, v.y * sc, v.z * sc, v.w * sc);
+  }
+}
+
 // ------------------------------------------------------------- select (two-pass refresh)
 
 // The j-th largest of n 32-bit values (j >= 1, duplicates counted) by an
@@ -702,7 +779,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
 
 struct RefreshWs {
   uint64_t* gtau;
-  uint16_t* qb;
+  void* qb;  // queries converted for the tensor cores: bf16, or e4m3 bytes (FP8_RERANK)
   uint64_t* bufs;
   uint64_t* part_keys;
   uint64_t* merge_bufs;
@@ -719,6 +796,14 @@ struct RefreshWs {
 // a multiple of 8 (bf16 top-k' contains the fp32 top-k; see tests + DESIGN.md).
 int rerank_candidates(int k) {
   int kc = std::max((3 * k + 1) / 2, k + 16);
+  kc = (kc + 7) / 8 * 8;
+  return std::min(kc, 2048);
+}
+
+// e4m3 candidate scores are coarser (3 mantissa bits: ~5% of the score spread
+// as noise for random data, against ~0.3% for bf16): k' = max(2k, k+32).
+int rerank_candidates_f8(int k) {
+  int kc = std::max(2 * k, k + 32);
   kc = (kc + 7) / 8 * 8;
   return std::min(kc, 2048);
 }
@@ -763,7 +848,11 @@ int64_t sample_stride() {
   }();
   return v;
 }
-constexpr int kSelMax = 4096;
+// per-query select capacity (candidates over all parts): 8192 keeps the
+// two-pass plan on for k' up to 512 at 9 label parts (the C5 shard's
+// top-(k_h + n_c) = 328 -> k' = 496); the select then stages 32 KB of score
+// halves + 8 KB of keys per warp (160 KB per 4-warp CTA)
+constexpr int kSelMax = 8192;
 
 TwoPass plan_two_pass(int64_t nq, int64_t L, int kk, int n_parts) {
   TwoPass t;
@@ -801,7 +890,9 @@ TwoPass plan_two_pass(int64_t nq, int64_t L, int kk, int n_parts) {
 size_t carve_refresh(void* base, size_t cap_bytes, int64_t nq, int64_t L, int d, int k, int mode, RefreshWs* w,
                      int* n_parts_out, int* kk_out, TwoPass* tp) {
   Carve c(base, cap_bytes);
-  const int kk = mode == ASTRA_REFRESH_BF16_RERANK ? rerank_candidates(k) : k;
+  const int kk = mode == ASTRA_REFRESH_BF16_RERANK ? rerank_candidates(k)
+                 : mode == ASTRA_REFRESH_FP8_RERANK ? rerank_candidates_f8(k)
+                                                    : k;
   const int cap = topk_cap(kk);
   int n_parts;
   size_t n_bufs;  // per-lane candidate buffers
@@ -821,11 +912,14 @@ size_t carve_refresh(void* base, size_t cap_bytes, int64_t nq, int64_t L, int d,
     *tp = plan_two_pass(nq, L, kk, n_parts);
   }
   w->gtau = c.take<uint64_t>(static_cast<size_t>(nq));
-  w->qb = mode == ASTRA_REFRESH_FP32_EXACT ? nullptr : c.take<uint16_t>(static_cast<size_t>(nq) * d);
+  w->qb = mode == ASTRA_REFRESH_FP32_EXACT ? nullptr
+          : mode == ASTRA_REFRESH_FP8_RERANK ? static_cast<void*>(c.take<uint8_t>(static_cast<size_t>(nq) * d))
+                                             : static_cast<void*>(c.take<uint16_t>(static_cast<size_t>(nq) * d));
   w->bufs = c.take<uint64_t>(buf_words);
   w->part_keys = c.take<uint64_t>(pk_words);
   w->merge_bufs = c.take<uint64_t>(static_cast<size_t>(nq) * (cap + kTopkSlack));
-  w->rr_cand = mode == ASTRA_REFRESH_BF16_RERANK ? c.take<uint64_t>(static_cast<size_t>(nq) * kk) : nullptr;
+  const bool rerank = mode == ASTRA_REFRESH_BF16_RERANK || mode == ASTRA_REFRESH_FP8_RERANK;
+  w->rr_cand = rerank ? c.take<uint64_t>(static_cast<size_t>(nq) * kk) : nullptr;
   w->gmax = nullptr;
   w->tau_keys = w->cand = nullptr;
   w->cand_cnt = w->flags = nullptr;
@@ -878,6 +972,30 @@ int f32_to_bf16(const float* src, uint16_t* dst, int64_t n, cudaStream_t st) {
   return ASTRA_OK;
 }
 
+// The label snapshot of the FP8_RERANK refresh: n values (fp32 or bf16,
+// n % 4 == 0, 16-byte aligned) -> e4m3 bytes scaled by 448 / max|x| (global,
+// computed on the device; no host sync). scratch: 2 device words, [1] = the
+// scale used (a uniform scale: rankings unchanged).
+int quantize_e4m3(const void* src, int src_bf16, int64_t n, uint8_t* dst, float* scratch, cudaStream_t st) {
+  if (n < 0 || (n & 3)) return set_error(ASTRA_ERR_CONFIG, "quantize_e4m3: n must be a multiple of 4");
+  if (n == 0) return ASTRA_OK;
+  if (!src || !dst || !scratch) return set_error(ASTRA_ERR_CONFIG, "quantize_e4m3: null buffer");
+  if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 3))
+    return set_error(ASTRA_ERR_CONFIG, "quantize_e4m3: misaligned buffers");
+  unsigned* bits = reinterpret_cast<unsigned*>(scratch);
+  ASTRA_TRY(check_cuda(cudaMemsetAsync(bits, 0, sizeof(unsigned), st), "memset absmax"));
+  const int grid = 8 * num_sms();
+  if (src_bf16) {
+    absmax_kernel<true><<<grid, 256, 0, st>>>(src, n, bits);
+    quant_e4m3_kernel<true><<<grid, 256, 0, st>>>(src, n, bits, scratch + 1, dst);
+  } else {
+    absmax_kernel<false><<<grid, 256, 0, st>>>(src, n, bits);
+    quant_e4m3_kernel<false><<<grid, 256, 0, st>>>(src, n, bits, scratch + 1, dst);
+  }
+  ASTRA_LAUNCHED("quant_e4m3");
+  return ASTRA_OK;
+}
+
 size_t refresh_workspace_size(int64_t nq, int64_t L, int d, int k, int mode) {
   RefreshWs w;
   int np, kk;
@@ -926,8 +1044,8 @@ struct StageProf {
 };
 
 int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, const float* wf, const uint16_t* wb,
-                 int64_t L, int64_t off, const int64_t* pos_indptr, const int32_t* pos_ids, int k, int mode,
-                 uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* ws, size_t ws_bytes,
+                 const uint8_t* w8, int64_t L, int64_t off, const int64_t* pos_indptr, const int32_t* pos_ids, int k,
+                 int mode, uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* ws, size_t ws_bytes,
                  cudaStream_t st) {
   if (k < 1 || k > 2048) return set_error(ASTRA_ERR_CONFIG, "refresh: k=%d outside [1, 2048]", k);
   if (nq < 0 || L < 0 || d <= 0) return set_error(ASTRA_ERR_CONFIG, "refresh: bad shape");
@@ -940,6 +1058,12 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
     if (!wb) return set_error(ASTRA_ERR_CONFIG, "bf16 refresh needs the bf16 label snapshot");
     if (!qf && !qb_in) return set_error(ASTRA_ERR_CONFIG, "bf16 refresh needs queries");
     if (mode == ASTRA_REFRESH_BF16_RERANK && !qf) return set_error(ASTRA_ERR_CONFIG, "BF16_RERANK needs fp32 queries");
+  } else if (mode == ASTRA_REFRESH_FP8_RERANK) {
+    if (d % 128) return set_error(ASTRA_ERR_CONFIG, "e4m3 refresh needs d %% 128 == 0 (d=%d)", d);
+    if (!w8) return set_error(ASTRA_ERR_CONFIG, "FP8_RERANK needs the e4m3 label snapshot");
+    if (!qf) return set_error(ASTRA_ERR_CONFIG, "FP8_RERANK needs fp32 queries");
+    if (!wf && !wb) return set_error(ASTRA_ERR_CONFIG, "FP8_RERANK re-ranks on the fp32 or bf16 labels: give one");
+    if (rerank_candidates_f8(k) > 512) return set_error(ASTRA_ERR_CONFIG, "FP8_RERANK needs k' = 2k <= 512 (k <= 256)");
   } else {
     return set_error(ASTRA_ERR_CONFIG, "refresh: unknown mode %d", mode);
   }
@@ -952,7 +1076,9 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
   StageProf prof(st);
   const int cap = topk_cap(kk);
   // where the bf16 / fp32 top-kk lands: the re-rank input, or the caller's outputs
-  const bool rerank = mode == ASTRA_REFRESH_BF16_RERANK;
+  const bool rerank = mode == ASTRA_REFRESH_BF16_RERANK || mode == ASTRA_REFRESH_FP8_RERANK;
+  const bool f8 = mode == ASTRA_REFRESH_FP8_RERANK;
+  if (rerank && !w.rr_cand) return set_error(ASTRA_ERR_CONFIG, "refresh: re-rank staging not carved");
   uint64_t* o_keys = rerank ? w.rr_cand : out_keys;
   int32_t* o_ids = rerank ? nullptr : out_ids;
   float* o_scores = rerank ? nullptr : out_scores;
@@ -981,16 +1107,22 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
     ASTRA_LAUNCHED("refresh_simt");
     ASTRA_TRY(topk_merge(w.part_keys, nq, n_parts, kk, kk, o_keys, o_ids, o_scores, w.merge_bufs, st));
   } else {
-    const uint16_t* qb = qb_in;
-    if (!qb) {
-      ASTRA_TRY(f32_to_bf16(qf, w.qb, nq * d, st));
+    const void* qb = qb_in;
+    if (f8) {
+      quant_rows_e4m3_kernel<<<static_cast<unsigned>((nq + 7) / 8), 256, 0, st>>>(qf, nq, d,
+                                                                                 static_cast<uint8_t*>(w.qb));
+      ASTRA_LAUNCHED("quant_rows_e4m3");
+      qb = w.qb;
+    } else if (!qb) {
+      ASTRA_TRY(f32_to_bf16(qf, static_cast<uint16_t*>(w.qb), nq * d, st));
       qb = w.qb;
     }
     TcLaunch p;
     p.qb = qb;
     p.nq = nq;
     p.d = d;
-    p.wb = wb;
+    p.wb = f8 ? static_cast<const void*>(w8) : static_cast<const void*>(wb);
+    p.f8 = f8;
     p.L = L;
     p.off = off;
     p.pos_indptr = pos_indptr;

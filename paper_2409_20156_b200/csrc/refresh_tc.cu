@@ -1,5 +1,7 @@
-// refresh_tc.cu — bf16 tcgen05 GEMM of queries x labels with a fused top-k
-// epilogue: the B200 shortlist refresh (replaces anns.py:253-256).
+// refresh_tc.cu — bf16 / e4m3 tcgen05 GEMM of queries x labels with a fused
+// top-k epilogue: the B200 shortlist refresh (replaces anns.py:253-256).
+// The e4m3 instance (kind::f8f6f4) runs the same pipeline on 8-bit operands:
+// identical 128-byte swizzle rows carrying twice the K extent per stage.
 //
 // One CTA owns a 128-query tile and sweeps a contiguous range of label tiles
 // (N = 256 labels each). Warp roles (256 threads):
@@ -32,6 +34,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -58,6 +61,16 @@ constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >>
 // CTA pair (cta_group::2): M = 256 (128 query rows per CTA), N = 256 (each CTA holds 128 W rows)
 constexpr uint32_t kIdescPair =
     (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t((2 * BM) >> 4) << 24);
+
+// idesc for kind::f8f6f4: D=F32, A=B=E4M3 (format 0 at [7,10) and [10,13)), both K-major
+constexpr uint32_t kIdescF8 = (1u << 4) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+constexpr uint32_t kIdescPairF8 = (1u << 4) | (uint32_t(BN >> 3) << 17) | (uint32_t((2 * BM) >> 4) << 24);
+// K elements per 128-byte swizzle row: 64 bf16 or 128 e4m3. Each MMA consumes
+// 32 bytes of K (16 bf16 / 32 e4m3), so a stage holds BK / UMMA_K = 4 MMAs
+// either way and the shared-memory layout is identical; an e4m3 stage carries
+// twice the K extent (and twice the flops) of a bf16 one.
+template <bool F8>
+constexpr int kb_elems() { return F8 ? 2 * BK : BK; }
 
 // Shared-memory ring geometry: single CTA (4 x 48 KB: A 128 rows + B 256 rows)
 // or CTA pair (6 x 32 KB: A 128 rows + this CTA's 128 of the 256 B rows).
@@ -114,6 +127,13 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
 }
 
+__device__ __forceinline__ void mma_f8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdescF8), "r"(accumulate));
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -163,6 +183,13 @@ __device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, u
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(kIdescPair), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_f8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdescPairF8), "r"(accumulate));
 }
 
 // Arrive on `bar` in both CTAs of the pair once the leader's prior tcgen05.mma complete.
@@ -355,7 +382,7 @@ __device__ __forceinline__ bool unit_active(const uint32_t* qbits, int64_t n_qt_
   return (qbits[qc >> 5] >> (qc & 31)) & 1u;
 }
 
-template <int CL, int MODE, bool PAIR>
+template <int CL, int MODE, bool PAIR, bool F8>
 __global__ void __launch_bounds__(kThreads, 1)
     refresh_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
   static_assert(!PAIR || CL == 2, "a CTA pair is a cluster of 2");
@@ -378,7 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* qbits_s = tmem_holder + 8;  // kQtBits bits
   float* stage_base = reinterpret_cast<float*>(smem + NST * G::STG + kBarrierBytes);
   const bool leader = !PAIR || crank == 0;
-  const int nkb = a.d / BK;
+  constexpr int KB = kb_elems<F8>();  // K elements per stage
+  const int nkb = a.d / KB;
   const int64_t n_units = a.n_qt_cl * a.n_parts;
 
   const uint32_t* qbits = nullptr;
@@ -445,15 +473,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               // transaction bytes of both complete on the leader's barrier
               const uint32_t bar = mapa_cluster(&full[stage], 0);
               if (leader) mbar_expect_tx(&full[stage], 2 * G::STG);
-              tma_load_2d_pair(sA + stage * A_STAGE, &tmA, bar, kb * BK, q0);
-              tma_load_2d_pair(sB + stage * G::B_ST, &tmB, bar, kb * BK, n0 + static_cast<int>(crank) * G::B_ROWS);
+              tma_load_2d_pair(sA + stage * A_STAGE, &tmA, bar, kb * KB, q0);
+              tma_load_2d_pair(sB + stage * G::B_ST, &tmB, bar, kb * KB, n0 + static_cast<int>(crank) * G::B_ROWS);
             } else {
               mbar_expect_tx(&full[stage], STAGE_BYTES);  // own A + all CL slices of the W tile
-              tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * BK, q0);
+              tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * KB, q0);
               if (CL == 1)
-                tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * BK, n0);
+                tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], kb * KB, n0);
               else
-                tma_load_2d_mc(sB + stage * B_STAGE + crank * B_SLICE, &tmB, &full[stage], kb * BK,
+                tma_load_2d_mc(sB + stage * B_STAGE + crank * B_SLICE, &tmB, &full[stage], kb * KB,
                                n0 + static_cast<int>(crank) * (BN / CL), kMask);
             }
             if (++stage == NST) {
@@ -492,8 +520,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < BK / UMMA_K; ++kk) {
               // +32 B along K inside the 128 B swizzle atom = +2 in the encoded address
-              if constexpr (PAIR)
+              if constexpr (PAIR && F8)
+                mma_f8_pair(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
+              else if constexpr (PAIR)
                 mma_bf16_pair(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
+              else if constexpr (F8)
+                mma_f8(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
               else
                 mma_bf16(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
             }
@@ -671,24 +703,27 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-int make_map(CUtensorMap* m, const void* base, int64_t rows, int d, int box_rows) {
+// 2-D K-major map of a [rows, d] operand: bf16 (box 64 x box_rows) or e4m3
+// bytes (box 128 x box_rows): 128-byte rows either way, SWIZZLE_128B.
+int make_map(CUtensorMap* m, const void* base, int64_t rows, int d, int box_rows, bool f8) {
   auto fn = encode_fn();
   if (!fn) return set_error(ASTRA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * 2};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * (f8 ? 1 : 2)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(f8 ? 2 * BK : BK), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  CUresult r = fn(m, f8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                  dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(ASTRA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
   return ASTRA_OK;
 }
 
-template <int CL, int MODE, bool PAIR = false>
+template <int CL, int MODE, bool PAIR, bool F8>
 int launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const TcArgs& a, dim3 grid, cudaStream_t st) {
   static bool attr_set = false;
-  auto kern = refresh_tc_kernel<CL, MODE, PAIR>;
+  auto kern = refresh_tc_kernel<CL, MODE, PAIR, F8>;
   if (!attr_set) {
     ASTRA_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(kSmemBytes)),
@@ -759,7 +794,8 @@ void refresh_tc_layout(int64_t nq, int64_t n_tiles, int* n_ctas, int* n_parts) {
 
 int launch_refresh_tc(const TcLaunch& p, cudaStream_t st) {
   if ((reinterpret_cast<uintptr_t>(p.qb) & 15) || (reinterpret_cast<uintptr_t>(p.wb) & 15))
-    return set_error(ASTRA_ERR_CONFIG, "bf16 operands must be 16-byte aligned");
+    return set_error(ASTRA_ERR_CONFIG, "tensor-core operands must be 16-byte aligned");
+  if (p.f8 && p.d % (2 * BK)) return set_error(ASTRA_ERR_CONFIG, "e4m3 refresh needs d %% 128 == 0 (d=%d)", p.d);
   if (p.L <= 0 || p.nq <= 0) return ASTRA_OK;
   const int64_t n_tiles_all = (p.L + BN - 1) / BN;
   const int64_t n_lt = (n_tiles_all + p.tile_stride - 1) / p.tile_stride;
@@ -767,8 +803,8 @@ int launch_refresh_tc(const TcLaunch& p, cudaStream_t st) {
   refresh_tc_layout(p.nq, n_lt, &G, &n_parts);
   const int cl = refresh_tc_cluster((p.nq + BM - 1) / BM);
   CUtensorMap tmA, tmB;
-  ASTRA_TRY(make_map(&tmA, p.qb, p.nq, p.d, BM));
-  ASTRA_TRY(make_map(&tmB, p.wb, p.L, p.d, BN / cl));
+  ASTRA_TRY(make_map(&tmA, p.qb, p.nq, p.d, BM, p.f8));
+  ASTRA_TRY(make_map(&tmB, p.wb, p.L, p.d, BN / cl, p.f8));
   TcArgs a;
   a.nq = p.nq;
   a.L = p.L;
@@ -811,19 +847,23 @@ int launch_refresh_tc(const TcLaunch& p, cudaStream_t st) {
     const char* e = getenv("ASTRA_TC_PAIR");
     return !(e && atoi(e) == 0);
   }();
-  if (cl == 2 && pair) {
+  auto dispatch = [&](auto f8_tag) {
+    constexpr bool F8 = decltype(f8_tag)::value;
+    if (cl == 2 && pair) {
+      if (mode == kFixed) return launch_variant<2, kFixed, true, F8>(tmA, tmB, a, grid, st);
+      if (mode == kGmax) return launch_variant<2, kGmax, true, F8>(tmA, tmB, a, grid, st);
+      return launch_variant<2, kRunning, true, F8>(tmA, tmB, a, grid, st);
+    }
     if (mode == kFixed)
-      rc = launch_variant<2, kFixed, true>(tmA, tmB, a, grid, st);
-    else if (mode == kGmax)
-      rc = launch_variant<2, kGmax, true>(tmA, tmB, a, grid, st);
-    else
-      rc = launch_variant<2, kRunning, true>(tmA, tmB, a, grid, st);
-  } else if (mode == kFixed)
-    rc = cl == 2 ? launch_variant<2, kFixed>(tmA, tmB, a, grid, st) : launch_variant<1, kFixed>(tmA, tmB, a, grid, st);
-  else if (mode == kGmax)
-    rc = cl == 2 ? launch_variant<2, kGmax>(tmA, tmB, a, grid, st) : launch_variant<1, kGmax>(tmA, tmB, a, grid, st);
-  else
-    rc = cl == 2 ? launch_variant<2, kRunning>(tmA, tmB, a, grid, st) : launch_variant<1, kRunning>(tmA, tmB, a, grid, st);
+      return cl == 2 ? launch_variant<2, kFixed, false, F8>(tmA, tmB, a, grid, st)
+                     : launch_variant<1, kFixed, false, F8>(tmA, tmB, a, grid, st);
+    if (mode == kGmax)
+      return cl == 2 ? launch_variant<2, kGmax, false, F8>(tmA, tmB, a, grid, st)
+                     : launch_variant<1, kGmax, false, F8>(tmA, tmB, a, grid, st);
+    return cl == 2 ? launch_variant<2, kRunning, false, F8>(tmA, tmB, a, grid, st)
+                   : launch_variant<1, kRunning, false, F8>(tmA, tmB, a, grid, st);
+  };
+  rc = p.f8 ? dispatch(std::true_type()) : dispatch(std::false_type());
   if (counters && rc == ASTRA_OK) {
     unsigned long long h[12];
     cudaMemcpyAsync(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost, st);

@@ -19,10 +19,11 @@ namespace astra {
 // pass). only_flagged (running mode): CTAs whose query tiles hold no flagged
 // query exit at once (the verification fallback).
 struct TcLaunch {
-  const uint16_t* qb = nullptr;
+  const void* qb = nullptr;  // queries [nq, d]: bf16, or e4m3 bytes when f8
   int64_t nq = 0;
   int d = 0;
-  const uint16_t* wb = nullptr;
+  const void* wb = nullptr;  // labels [L, d]: bf16, or e4m3 bytes when f8
+  bool f8 = false;           // kind::f8f6f4 with e4m3 operands (d % 128 == 0)
   int64_t L = 0, off = 0;
   const int64_t* pos_indptr = nullptr;
   const int32_t* pos_ids = nullptr;

@@ -74,7 +74,7 @@ class ClassifierEngine:
             self.m = torch.zeros((self.hi - self.lo, dim), dtype=torch.float32, device=self.device)
             self.v = torch.zeros_like(self.m)
         self.adam_step = 0
-        self.snap_f32 = self.snap_bf16 = None
+        self.snap_f32 = self.snap_bf16 = self.snap_f8 = None
         self.snapshot_epoch = -1
         self.slate_exchange = "gather"  # or "regenerate" (see sample())
 
@@ -83,6 +83,7 @@ class ClassifierEngine:
         """Immutable copy of the shard for the refresh (anns.py:90-100)."""
         if check_finite and not bool(torch.isfinite(self.W).all()):
             raise NumericalError("non-finite vectors in index build")
+        fp8 = self.refresh_mode == "fp8_rerank"
         if self.W.dtype == torch.bfloat16 and self.refresh_mode != "fp32":
             # bf16 W: the bf16 copy is the whole snapshot (the re-rank scores its
             # values exactly); no fp32 copy (46 GB for a 15M-label shard)
@@ -90,7 +91,11 @@ class ClassifierEngine:
             self.snap_bf16 = self.W.clone()
         else:
             self.snap_f32 = self.W.float().clone() if self.W.dtype != torch.float32 else self.W.clone()
-            self.snap_bf16 = self.ops.f32_to_bf16(self.snap_f32) if self.refresh_mode != "fp32" else None
+            self.snap_bf16 = (self.ops.f32_to_bf16(self.snap_f32) if self.refresh_mode in ("bf16", "bf16_rerank")
+                              else None)
+        # e4m3 candidate-pass snapshot (FP8_RERANK: the re-rank reads the fp32 / bf16 copy above)
+        self.snap_f8 = (self.ops.quantize_e4m3(self.snap_f32 if self.snap_f32 is not None else self.snap_bf16)
+                        if fp8 else None)
         self.snapshot_epoch = epoch
 
     # ------------------------------------------------------------ refresh
@@ -104,8 +109,10 @@ class ClassifierEngine:
         B = queries.shape[0]
         q_all = self.comm.all_gather(queries)
         ip_all, pid_all = gather_csr(self.comm, pos_indptr, pos_ids)
+        extra = {"labels_e4m3": self.snap_f8} if getattr(self, "snap_f8", None) is not None else {}
         keys, ids, scores = self.ops.refresh_topk(
-            q_all, ip_all, pid_all, k, mode, labels_f32=self.snap_f32, labels_bf16=self.snap_bf16, label_offset=self.lo)
+            q_all, ip_all, pid_all, k, mode, labels_f32=self.snap_f32, labels_bf16=self.snap_bf16, label_offset=self.lo,
+            **extra)
         if self.comm.world == 1:
             return ids, scores
         # rows [r*B, (r+1)*B) of every shard's partial list go to their owner r
@@ -334,7 +341,7 @@ class ClassifierEngine:
         self.w_absmax.fill_(float(w_absmax))
         # the refresh snapshot is not part of the file: drop any snapshot of the
         # previous weights (snapshot() rebuilds it from the restored W)
-        self.snap_f32 = self.snap_bf16 = None
+        self.snap_f32 = self.snap_bf16 = self.snap_f8 = None
         self.snapshot_epoch = int(snap)
 
 

@@ -14,14 +14,14 @@ import torch
 from . import _lib
 from .errors import ConfigError, NumericalError
 
-REFRESH_FP32_EXACT, REFRESH_BF16, REFRESH_BF16_RERANK = 0, 1, 2
+REFRESH_FP32_EXACT, REFRESH_BF16, REFRESH_BF16_RERANK, REFRESH_FP8_RERANK = 0, 1, 2, 3
 W_FP32, W_BF16 = 0, 1
 OPT_SGD, OPT_ADAM = 0, 1
 ORIGIN_POS, ORIGIN_HARD, ORIGIN_RAND, ORIGIN_PAD, ORIGIN_IMP = 0, 1, 2, 3, 4
 STATUS_NONFINITE_GRAD, STATUS_NONFINITE_GRAD_EMB, STATUS_BOUND_UNSAFE, STATUS_ID_RANGE = 0, 1, 2, 3
 
 _MODES = {"fp32": REFRESH_FP32_EXACT, "fp32_exact": REFRESH_FP32_EXACT, "bf16": REFRESH_BF16,
-          "bf16_rerank": REFRESH_BF16_RERANK}
+          "bf16_rerank": REFRESH_BF16_RERANK, "fp8_rerank": REFRESH_FP8_RERANK}
 
 
 def refresh_mode(mode) -> int:
@@ -74,8 +74,20 @@ def f32_to_bf16(x: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def quantize_e4m3(x: torch.Tensor) -> torch.Tensor:
+    """e4m3 copy (uint8 bytes) of an fp32 / bf16 tensor scaled by 448 / max|x|
+    (the FP8_RERANK label snapshot; astra_quantize_e4m3)."""
+    if not (x.is_cuda and x.is_contiguous() and x.dtype in (torch.float32, torch.bfloat16)):
+        raise ConfigError("quantize_e4m3: expected a contiguous CUDA fp32/bf16 tensor")
+    out = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+    scratch = torch.empty(2, dtype=torch.float32, device=x.device)
+    _lib.check(_lib.load().astra_quantize_e4m3(_p(x), int(x.dtype == torch.bfloat16), x.numel(), _p(out), _p(scratch),
+                                               _stream()))
+    return out
+
+
 def refresh_topk(queries, pos_indptr, pos_ids, k, mode="bf16_rerank", labels_f32=None, labels_bf16=None,
-                 label_offset=0, queries_bf16=None, n_labels=None):
+                 label_offset=0, queries_bf16=None, n_labels=None, labels_e4m3=None):
     """Top-k (keys, ids, scores) per query over a label shard, positives
     excluded (retrieve_hard_negatives, anns.py:233-256). keys are int64 views of
     the packed uint64 keys (for astra_topk_merge)."""
@@ -83,11 +95,12 @@ def refresh_topk(queries, pos_indptr, pos_ids, k, mode="bf16_rerank", labels_f32
     ref = queries if queries is not None else queries_bf16
     nq, d = ref.shape
     if n_labels is None:
-        n_labels = (labels_f32 if labels_f32 is not None else labels_bf16).shape[0]
+        n_labels = next(t for t in (labels_f32, labels_bf16, labels_e4m3) if t is not None).shape[0]
     _cuda(queries, torch.float32, "queries")
     _cuda(labels_f32, torch.float32, "labels_f32")
     _cuda(labels_bf16, torch.bfloat16, "labels_bf16")
     _cuda(queries_bf16, torch.bfloat16, "queries_bf16")
+    _cuda(labels_e4m3, torch.uint8, "labels_e4m3")
     _cuda(pos_indptr, torch.int64, "pos_indptr")
     _cuda(pos_ids, torch.int32, "pos_ids")
     lib = _lib.load()
@@ -98,7 +111,7 @@ def refresh_topk(queries, pos_indptr, pos_ids, k, mode="bf16_rerank", labels_f32
     ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
     scores = torch.empty((nq, k), dtype=torch.float32, device=dev)
     _lib.check(lib.astra_refresh_topk(
-        _p(queries), _p(queries_bf16), nq, d, _p(labels_f32), _p(labels_bf16), n_labels, label_offset,
+        _p(queries), _p(queries_bf16), nq, d, _p(labels_f32), _p(labels_bf16), _p(labels_e4m3), n_labels, label_offset,
         _p(pos_indptr), _p(pos_ids), k, mode, _p(keys), _p(ids), _p(scores), _p(ws), ws.numel(), _stream()))
     return keys, ids, scores
 

@@ -30,8 +30,12 @@ def f32_to_bf16(x):
     return x.to(torch.bfloat16)
 
 
+def quantize_e4m3(x):
+    return (x.float() * (448.0 / max(float(x.abs().max()), 1e-30))).to(torch.float8_e4m3fn).view(torch.uint8)
+
+
 def refresh_topk(queries, pos_indptr, pos_ids, k, mode="fp32", labels_f32=None, labels_bf16=None, label_offset=0,
-                 queries_bf16=None, n_labels=None):
+                 queries_bf16=None, n_labels=None, labels_e4m3=None):
     if k < 1:
         raise ConfigError("refresh: k must be >= 1")
     keys, ids, scores = co.refresh_fp32(_np(queries), _np(labels_f32), _np(pos_indptr), _np(pos_ids), k, label_offset)

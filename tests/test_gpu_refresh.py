@@ -20,9 +20,10 @@ def _run(E, W, positives, k, mode, offset=0):
 
     ip, pid = csr(positives)
     Wd = dev(W)
+    extra = {"labels_e4m3": ops.quantize_e4m3(Wd)} if mode == "fp8_rerank" else {}
     keys, ids, scores = ops.refresh_topk(
-        dev(E), dev(ip), dev(pid), k, mode, labels_f32=Wd, labels_bf16=ops.f32_to_bf16(Wd) if mode != "fp32" else None,
-        label_offset=offset)
+        dev(E), dev(ip), dev(pid), k, mode, labels_f32=Wd,
+        labels_bf16=ops.f32_to_bf16(Wd) if mode in ("bf16", "bf16_rerank") else None, label_offset=offset, **extra)
     torch.cuda.synchronize()
     return u64(keys), ids.cpu().numpy(), scores.cpu().numpy()
 
@@ -252,3 +253,37 @@ def test_f32_to_bf16_matches_torch_rne(cuda_lib, n):
     x[: min(n, 4)] = torch.tensor([0.0, -0.0, 1e-40, 3.0e38][: min(n, 4)], device="cuda")
     got = ops.f32_to_bf16(x)
     assert torch.equal(got.view(torch.int16), x.to(torch.bfloat16).view(torch.int16))
+
+
+@pytest.mark.parametrize("nq,L,d,k,offset", [(256, 20000, 128, 32, 0), (300, 9000, 768, 64, 0), (1, 5000, 256, 8, 0),
+                                             (130, 1037, 128, 16, 5000), (512, 60000, 768, 200, 0)])
+def test_fp8_rerank_equals_fp32(cuda_lib, nq, L, d, k, offset):
+    """e4m3 candidate pass (tcgen05 kind::f8f6f4) + fp32 re-rank: ids equal
+    the fp32-exact ones (the north star's >= 0.999 recall, here exact)."""
+    rng = np.random.default_rng(nq + d)
+    W = rng.uniform(-1 / np.sqrt(d), 1 / np.sqrt(d), size=(L, d)).astype(np.float32)
+    E = rng.standard_normal((nq, d)).astype(np.float32)
+    positives = [p + offset for p in random_positives(rng, nq, L, 0, 5)]
+    _, exact_ids, exact_scores = _run(E, W, positives, k, "fp32", offset=offset)
+    _, f8_ids, f8_scores = _run(E, W, positives, k, "fp8_rerank", offset=offset)
+    recall = np.mean([len(set(a) & set(b)) / k for a, b in zip(f8_ids.tolist(), exact_ids.tolist())])
+    assert recall >= 0.999, recall
+    np.testing.assert_array_equal(f8_ids, exact_ids)
+    np.testing.assert_array_equal(f8_scores, exact_scores)  # re-ranked scores are the fp32-exact ones
+
+
+def test_quantize_e4m3_matches_torch(cuda_lib):
+    """astra_quantize_e4m3 = torch's float8_e4m3fn cast of x * 448 / max|x| (RNE)."""
+    import torch
+
+    from paper_2409_20156_b200 import ops
+
+    rng = np.random.default_rng(2)
+    x = torch.from_numpy((rng.standard_normal(4096 * 3) * 0.05).astype(np.float32)).cuda()
+    q = ops.quantize_e4m3(x)
+    ref = (x * (448.0 / x.abs().max())).to(torch.float8_e4m3fn).view(torch.uint8)
+    assert torch.equal(q, ref)
+    xb = x.to(torch.bfloat16)
+    qb = ops.quantize_e4m3(xb)
+    refb = (xb.float() * (448.0 / xb.float().abs().max())).to(torch.float8_e4m3fn).view(torch.uint8)
+    assert torch.equal(qb, refb)
