@@ -48,6 +48,16 @@ sys.path.insert(0, ROOT)
 # C4 = LF-AmazonTitles-1.3M shape, slate from SURVEY.md §8
 CFG = dict(workload="LF-AmazonTitles-1.3M shape, synthetic", L=1_305_265, d=768, N=2_248_619, B=1024,
            minibatches=9, k_p=8, k_h=64, k_r=512, labels_per_point=38, tau_r=1, lr=0.05, wd=1e-4)
+# BASELINE.json configs[0..2] (SURVEY.md §8 parameters); the default line is C4 above
+CONFIGS = {
+    "c4": dict(CFG),
+    "c1": dict(workload="synthetic tiny XC (BASELINE configs[0]): L=10K, d=64", L=10_000, d=64, N=50_000, B=256,
+               minibatches=9, k_p=4, k_h=16, k_r=16, labels_per_point=3, tau_r=1, lr=0.05, wd=1e-4),
+    "c2": dict(workload="LF-AmazonTitles-131K shape, synthetic", L=131_073, d=768, N=294_805, B=1024, minibatches=9,
+               k_p=8, k_h=64, k_r=512, labels_per_point=5, tau_r=1, lr=0.05, wd=1e-4),
+    "c3": dict(workload="LF-WikiSeeAlso-320K shape, synthetic (refresh every epoch)", L=312_330, d=768, N=693_082,
+               B=1024, minibatches=9, k_p=8, k_h=64, k_r=512, labels_per_point=5, tau_r=1, lr=0.05, wd=1e-4),
+}
 METRIC = "ASTRA train samples/s (shortlist+loss+update)"
 REFRESH_MODE = ["bf16_rerank"]  # set from --refresh-mode
 UNIT = "samples/s"
@@ -132,7 +142,8 @@ def bench_config(world: int) -> dict:
             "k_p": c["k_p"], "k_h": c["k_h"], "k_r": c["k_r"], "slate": c["k_p"] + c["k_h"] + c["k_r"],
             "labels_per_point": c["labels_per_point"], "tau_r": c["tau_r"], "refresh_chunk": R * world,
             "refresh_mode": REFRESH_MODE[0], "optimizer": "sgd+wd", "parallelism": f"label-shard{world}",
-            "l2": "inputs larger than L2 (W fp32 4.0 GB + snapshots 6 GB)"}
+            "l2": ("inputs larger than L2 (W fp32 + snapshots >= 3 x L*d*4 B)" if c["L"] * c["d"] * 12 >= 256 * 2**20
+                   else "L2 flushed between timed steps (512 MB write outside the per-step events)")}
 
 
 def _ncu_traffic():
@@ -228,9 +239,10 @@ def run_ours(args):
     if overlap:
         _lib.set_refresh_sm_budget(args.refresh_sms)
 
-    def one(t, timed, mode=None):
+    def one(t, timed, mode=None, reuse_start=False):
         st, e = dev[t], ev[t]
-        e[0].record(stream)
+        if not reuse_start:
+            e[0].record(stream)
         rstream.wait_stream(stream)
         with torch.cuda.stream(rstream):
             eng.refresh(st["chunk"]["emb"], st["chunk"]["indptr"], st["chunk"]["pos"], k_h, mode=mode)
@@ -261,9 +273,20 @@ def run_ours(args):
     _lib.kernel_timing_enable(True)
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    # working sets that fit in L2 (C1: W is 2.5 MB) are flushed between timed
+    # steps (a 512 MB write, outside the per-step events) so every step starts cold
+    flush = L_loc * d * 4 * 3 < 256 * 2**20
+    flush_buf = torch.empty(512 * 2**20, dtype=torch.uint8, device="cuda") if flush else None
+    ends = []
     t_start.record(stream)
     for t in range(args.warmup, n_steps):
-        loss, status = one(t, True)
+        if flush:
+            flush_buf.fill_(t & 0xFF)
+            ev[t][0].record(stream)
+        loss, status = one(t, True, reuse_start=flush)
+        if flush:
+            ends.append(torch.cuda.Event(enable_timing=True))
+            ends[-1].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
     eng.comm.barrier()
@@ -273,7 +296,11 @@ def run_ours(args):
     _lib.kernel_timing_enable(False)
     kt = {name: _lib.kernel_timing(name) for name in ("refresh_gemm", "refresh_verify", "step_single", "slot_forward", "label_update")}
     ops.raise_for_step_status(status)
-    ms_t = torch.tensor([t_start.elapsed_time(t_end)], dtype=torch.float64, device="cuda")
+    if flush:
+        ms_steps = sum(ev[t][0].elapsed_time(ends[i]) for i, t in enumerate(range(args.warmup, n_steps)))
+    else:
+        ms_steps = t_start.elapsed_time(t_end)
+    ms_t = torch.tensor([ms_steps], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_total = float(ms_t.item())
@@ -992,6 +1019,66 @@ def run_fullloss(args):
     print(json.dumps(line), flush=True)
 
 
+def run_dropin(args):
+    """The C4 work through the REFERENCE's own public API with the B200 path
+    installed (paper_2409_20156_b200.install: xcmix.anns.retrieve_hard_negatives
+    and xcmix.trainer._batch_forward_backward rebound), on the same state the
+    reference arm builds (ReferenceCPU: TrainerState, the reference's encoder
+    on the host). Per step: the refresh of one B=1024 minibatch's rows through
+    xcmix.anns.retrieve_hard_negatives (host numpy in, NegativeCache out) + the
+    minibatch's xcmix.trainer._batch_forward_backward (slates, fused loss /
+    update on the device-resident W, grad_emb back to the caller's numpy
+    encoder + Adam) — exactly the reference arm's step, so the two lines compare
+    the same calls. Host-synchronous API: timed by wall clock with the device
+    synchronised on both sides (the numbers include every H2D / D2H)."""
+    import torch
+
+    from paper_2409_20156_b200 import _lib
+    from paper_2409_20156_b200.install import install
+
+    torch.cuda.set_device(0)
+    B = CFG["B"]
+    n_steps = args.warmup + args.steps
+    ref = ReferenceCPU(B * n_steps)
+    if ref.kind != "reference":
+        print(json.dumps({"metric": METRIC + " [through the reference API]", "unavailable": "baseline/_ref missing"}))
+        return
+    install(slates="philox")
+    from xcmix import anns
+    from xcmix import trainer as xt
+
+    ref.index = anns.build_exact(ref.state.bank.weights, snapshot_epoch=0)  # the rebound (device-cached) snapshot
+
+    def step(t):
+        rows = t * B + np.arange(B, dtype=np.int64)
+        pos = [ref.positives[r] for r in rows]
+        emb = xt.embed_batch(ref.state.encoder, ref.state.dataset.features[rows])
+        cache = anns.retrieve_hard_negatives(ref.index, emb, pos, CFG["k_h"])
+        ref.cache_ids[rows] = cache.ids
+        return xt._batch_forward_backward(ref.state, rows, 2, np.random.default_rng(1000 + t), 0.01, CFG["lr"])
+
+    for t in range(args.warmup):
+        step(t)
+    torch.cuda.synchronize()
+    n0 = _lib.launch_count()
+    t0 = time.perf_counter()
+    for t in range(args.warmup, n_steps):
+        loss = step(t)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    K = args.steps
+    line = {"metric": METRIC + " [through the reference API: install() + xcmix functions]",
+            "value": round(B * K / wall, 1), "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": args.warmup,
+            "ms_per_step": round(wall / K * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp32 W/step, bf16 tensor-core refresh + fp32 re-rank; deterministic two-kernel step",
+            "data": "synthetic",
+            "config": dict(bench_config(1), rows_per_step_per_gpu=B, minibatches_per_step=1, refresh_chunk=B,
+                           api="xcmix.anns.retrieve_hard_negatives + xcmix.trainer._batch_forward_backward"),
+            "timing": "wall clock, device synchronised on both sides (host-synchronous API, numpy in/out)",
+            "gpu_launches": int(_lib.launch_count() - n0), "last_loss": float(loss)}
+    print(json.dumps(line), flush=True)
+
+
 def _relaunch(n: int) -> int:
     """`bench.py --gpus N` outside torchrun: re-exec under
     torch.distributed.run with one rank per GPU (NCCL), same arguments."""
@@ -1022,9 +1109,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="c4", choices=["c4", "c5shard", "fullloss"],
-                    help="c4 (default, the headline line), c5shard (120M-label config, one of 8 shards) or "
-                         "fullloss (the all-negatives arm at the reference's 50K-label cap)")
+    ap.add_argument("--config", default="c4", choices=["c4", "c1", "c2", "c3", "c5shard", "fullloss", "dropin"],
+                    help="c4 (default, the headline line); c1 / c2 / c3 (BASELINE configs[0..2], same composite "
+                         "step); c5shard (120M-label config, one of 8 shards); fullloss (the all-negatives arm at the "
+                         "reference's 50K-label cap); dropin (the same C4 work through the reference's own API with "
+                         "install())")
     ap.add_argument("--refresh-sms", type=int, default=0,
                     help="SM budget of the refresh running concurrently with training on a side stream (0 = serial)")
     ap.add_argument("--emulate", type=int, default=0,
@@ -1038,6 +1127,9 @@ def main():
                     help="--emulate: how the N-GPU job shares slates (engine.ClassifierEngine.slate_exchange)")
     args = ap.parse_args()
     REFRESH_MODE[0] = args.refresh_mode
+    if args.config in CONFIGS:
+        CFG.clear()
+        CFG.update(CONFIGS[args.config])
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.gpus < 1:
@@ -1050,6 +1142,8 @@ def main():
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}; refusing to report a different GPU count")
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "dropin":
+        run_dropin(args)
     elif args.emulate:
         run_emulate(args)
     elif args.config == "c5shard":
