@@ -664,13 +664,23 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
   if (q >= nq) return;  // warp-uniform
   uint64_t* R = sel_smem + static_cast<size_t>(warp) * (rcap + sel_max / 2);
   uint32_t* S = reinterpret_cast<uint32_t*>(R + rcap);
+  // the parts' counts lane-parallel (up to kSelMaxParts = 64 parts: two per
+  // lane), their offsets by a warp scan
   int total = 0;
   bool overflow = n_parts > kSelMaxParts;
-  for (int p = 0; p < n_parts && !overflow; ++p) {
-    const int c = cand_cnt[static_cast<size_t>(p) * nq + q];
-    overflow |= c > cand_cap;
-    if (lane == 0) sel_off[warp][p] = total;
-    total += c < cand_cap ? c : cand_cap;
+  for (int pb = 0; pb < n_parts && !overflow; pb += 32) {
+    const int p = pb + lane;
+    const int c = p < n_parts ? cand_cnt[static_cast<size_t>(p) * nq + q] : 0;
+    overflow |= __any_sync(0xffffffffu, c > cand_cap);
+    const int cc = c < cand_cap ? c : cand_cap;
+    int incl = cc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    if (p < n_parts) sel_off[warp][p] = total + incl - cc;
+    total += __shfl_sync(0xffffffffu, incl, 31);
   }
   if (lane == 0 && !overflow) sel_off[warp][n_parts] = total;
   bool fail = overflow || total > sel_max;
@@ -678,23 +688,23 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
   if (fail) return;
   __syncwarp();
   const int64_t p0 = pos_indptr[q], np = pos_indptr[q + 1] - p0;
-  // full key of candidate i (parts concatenated in order)
+  // part of candidate i (parts concatenated in order): the last part whose
+  // offset is <= i (binary search; empty parts share their successor's offset)
+  auto part_of = [&](int i) {
+    int lo = 0, hi = n_parts - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (sel_off[warp][mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  };
   auto key_at = [&](int i) {
-    int p = 0;
-    while (i >= sel_off[warp][p + 1]) ++p;
+    const int p = part_of(i);
     return cand[(static_cast<size_t>(p) * nq + q) * cand_cap + (i - sel_off[warp][p])];
   };
-  // 1. the candidates' scores -> shared memory (independent loads)
-  {
-    int o = 0;
-    for (int p = 0; p < n_parts; ++p) {
-      const int c = min(cand_cnt[static_cast<size_t>(p) * nq + q], cand_cap);
-      const uint64_t* src = cand + (static_cast<size_t>(p) * nq + q) * cand_cap;
-#pragma unroll 4
-      for (int e = lane; e < c; e += 32) S[o + e] = static_cast<uint32_t>(src[e] >> 32);
-      o += c;
-    }
-  }
+  // 1. the candidates' scores -> shared memory (independent loads; lane-strided
+  //    over the concatenation, so many small parts keep every lane busy)
+  for (int i = lane; i < total; i += 32) S[i] = static_cast<uint32_t>(key_at(i) >> 32);
   __syncwarp();
   // 2. T2 = the (k + |P|)-th largest score over ALL candidates: at most |P| of
   //    the keys above the k-th non-positive one are positives, so every key of
@@ -881,8 +891,15 @@ TwoPass plan_two_pass(int64_t nq, int64_t L, int kk, int n_parts) {
   t.j = j;
   t.n_groups = static_cast<int>(n_lt_s * 4);
   t.cand_cap = cap;
+  // the select stages at most sel_max candidates per query: the sum of the part
+  // capacities, but no more than 3x the expected total (+128) — many small
+  // parts (the SM-filling layouts) would otherwise size it to the worst case
+  // of every part full at once and cut the select's occupancy (a query with
+  // more candidates is flagged and verified exactly)
+  const int64_t total_cap = std::min<int64_t>(static_cast<int64_t>(cap) * n_parts,
+                                              static_cast<int64_t>(3.0 * j * kSampleStride) + 128);
   int sm = 1;
-  while (sm < cap * n_parts) sm <<= 1;
+  while (sm < total_cap) sm <<= 1;
   t.sel_max = std::min(sm, kSelMax);
   return t;
 }

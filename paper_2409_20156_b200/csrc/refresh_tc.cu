@@ -775,18 +775,40 @@ void refresh_tc_layout(int64_t nq, int64_t n_tiles, int* n_ctas, int* n_parts) {
   const int b = g_refresh_sm_budget.load();
   if (b > 0) budget = std::min(budget, b);
   const int64_t n_cl_max = std::max(1, budget / cl);
-  int64_t best_p = 1;
-  double best_eff = -1.0;
-  for (int64_t p = 1; p <= std::min<int64_t>(n_tiles, 64); ++p) {
+  // efficiency of p parts: useful unit-rounds / (rounds x clusters), counted in
+  // label tiles (the last part of a query tile may be shorter)
+  auto eff_of = [&](int64_t p) {
     const int64_t units = n_qt_cl * p;
     const int64_t n_cl = std::min(n_cl_max, units);
     const int64_t rounds = (units + n_cl - 1) / n_cl;
-    const double eff = static_cast<double>(units) / static_cast<double>(rounds * n_cl_max);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
+    const int64_t tpp = (n_tiles + p - 1) / p;
+    return static_cast<double>(units) / static_cast<double>(rounds * n_cl_max) *
+           static_cast<double>(n_tiles) / static_cast<double>(tpp * p);
+  };
+  // fewest parts that fill the budget (fewer lists, more L2 reuse of W): a
+  // layout that keeps every cluster busy to within 1% (e.g. 37 parts x 36
+  // query-tile pairs = 18 rounds of 74 pairs on 148 SMs) while parts stay
+  // >= 64 tiles long, else the fewest parts reaching 93%
+  int64_t best_p = 1;
+  double best_eff = -1.0;
+  const int64_t p_max = std::min<int64_t>(n_tiles, 64);
+  for (int64_t p = 1; p <= p_max; ++p) {
+    if (p > 1 && n_tiles / p < 64) break;
+    if (eff_of(p) >= 0.99) {
       best_p = p;
+      best_eff = eff_of(p);
+      break;
     }
-    if (best_eff >= 0.93) break;  // fewest parts that fill the budget: fewer lists, more L2 reuse of W
+  }
+  if (best_eff < 0.0) {
+    for (int64_t p = 1; p <= p_max; ++p) {
+      const double eff = eff_of(p);
+      if (eff > best_eff + 0.02) {
+        best_eff = eff;
+        best_p = p;
+      }
+      if (best_eff >= 0.93) break;
+    }
   }
   *n_ctas = static_cast<int>(std::min(n_cl_max, n_qt_cl * best_p) * cl);
   *n_parts = static_cast<int>(best_p);

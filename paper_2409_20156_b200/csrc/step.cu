@@ -734,9 +734,26 @@ __device__ __forceinline__ int32_t seg_slot(const UpdArgs& a, uint32_t start, ui
   return n <= 32 ? __shfl_sync(0xffffffffu, reg, static_cast<int>(j)) : a.perm2[start + j];
 }
 
+#ifndef ASTRA_ADAM_FAST
+#define ASTRA_ADAM_FAST 0
+#endif
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // One element's update: SGD (classifiers.py:82, each op rounded like NumPy)
 // or SparseAdam (torch.optim.SparseAdam op order).
-template <bool ADAM>
+// FAST (Adam on bf16 W, ASTRA_ADAM_FAST): MUFU sqrt + reciprocal (each ~1
+// ulp) instead of the IEEE sqrt/div sequences; the step term then differs from
+// SparseAdam's by a few ulp of itself, far below the bf16 rounding of W'.
+template <bool ADAM, bool FAST = false>
 __device__ __forceinline__ float upd_elem(const UpdArgs& a, float p, float g, float* mp, float* vp) {
   if constexpr (!ADAM) {
     return __fsub_rn(p, __fmul_rn(a.lr, __fadd_rn(g, __fmul_rn(a.wd, p))));
@@ -748,8 +765,13 @@ __device__ __forceinline__ float upd_elem(const UpdArgs& a, float p, float g, fl
     *mp = __fadd_rn(m0, mu);
     *vp = __fadd_rn(v0, vu);
     float numer = __fadd_rn(mu, m0);
-    float denom = __fadd_rn(__fsqrt_rn(__fadd_rn(vu, v0)), a.eps);
-    return __fadd_rn(p, __fmul_rn(a.neg_step, __fdiv_rn(numer, denom)));
+    if constexpr (FAST) {
+      const float denom = __fadd_rn(sqrt_approx(__fadd_rn(vu, v0)), a.eps);
+      return __fadd_rn(p, __fmul_rn(a.neg_step, __fmul_rn(numer, rcp_approx(denom))));
+    } else {
+      const float denom = __fadd_rn(__fsqrt_rn(__fadd_rn(vu, v0)), a.eps);
+      return __fadd_rn(p, __fmul_rn(a.neg_step, __fdiv_rn(numer, denom)));
+    }
   }
 }
 
@@ -819,20 +841,26 @@ __global__ void __launch_bounds__(kUpdThreads) label_update_kernel(UpdArgs a) {
 // roundings as label_update_kernel), then take the row from the ring, apply the
 // update and store it. W is read and written once per touched row.
 // Ring geometry of the update: one entry = the W row (+ the Adam m and v rows).
+#ifndef ASTRA_UPD_ADAM_RING
+#define ASTRA_UPD_ADAM_RING 8
+#endif
 template <int NV, bool BF16, bool ADAM>
 struct UpdRing {
   static constexpr uint32_t WB = NV * 128 * (BF16 ? 2 : 4);
   static constexpr uint32_t MB = ADAM ? NV * 128 * 4 : 0;
   static constexpr uint32_t ENTRY = WB + 2 * MB;
-  static constexpr int RING = ADAM ? 8 : (BF16 ? 32 : 16);
+  static constexpr int RING = ADAM ? ASTRA_UPD_ADAM_RING : (BF16 ? 32 : 16);
   static constexpr size_t smem() { return static_cast<size_t>(RING) * ENTRY + 2 * 8 * RING; }
 };
 
 // CTAs per SM of the TMA update: three (Adam too: 124 registers and an
 // 8 x 9 KB ring fit; 1.31 vs 1.67 ms per minibatch at 2 for bf16 Adam), except
 // Adam at d = 1024, whose moments spill at three.
+#ifndef ASTRA_UPD_ADAM_CTAS
+#define ASTRA_UPD_ADAM_CTAS 3
+#endif
 template <int NV, bool ADAM>
-constexpr int upd_tma_ctas() { return ADAM && NV > 6 ? 2 : 3; }
+constexpr int upd_tma_ctas() { return ADAM && NV > 6 ? 2 : (ADAM ? ASTRA_UPD_ADAM_CTAS : 3); }
 
 template <int NV, bool BF16, bool ADAM>
 __global__ void __launch_bounds__(kTmaThreads, upd_tma_ctas<NV, ADAM>()) label_update_tma(UpdArgs a) {
@@ -958,10 +986,10 @@ __global__ void __launch_bounds__(kTmaThreads, upd_tma_ctas<NV, ADAM>()) label_u
       float4 np;
       const size_t el = row + q * 128 + lane * 4;
       if constexpr (ADAM) {
-        np.x = upd_elem<true>(a, p[q].x, g[q].x, &m4[q].x, &v4[q].x);
-        np.y = upd_elem<true>(a, p[q].y, g[q].y, &m4[q].y, &v4[q].y);
-        np.z = upd_elem<true>(a, p[q].z, g[q].z, &m4[q].z, &v4[q].z);
-        np.w = upd_elem<true>(a, p[q].w, g[q].w, &m4[q].w, &v4[q].w);
+        np.x = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p[q].x, g[q].x, &m4[q].x, &v4[q].x);
+        np.y = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p[q].y, g[q].y, &m4[q].y, &v4[q].y);
+        np.z = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p[q].z, g[q].z, &m4[q].z, &v4[q].z);
+        np.w = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p[q].w, g[q].w, &m4[q].w, &v4[q].w);
         *reinterpret_cast<float4*>(a.m + el) = m4[q];
         *reinterpret_cast<float4*>(a.v + el) = v4[q];
       } else {
@@ -1317,10 +1345,10 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
             m4 = *reinterpret_cast<const float4*>(ent + RG::WB + (q * 128 + lane * 4) * 4);
             v4 = *reinterpret_cast<const float4*>(ent + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
           }
-          np.x = upd_elem<true>(a, p[q].x, gq.x, &m4.x, &v4.x);
-          np.y = upd_elem<true>(a, p[q].y, gq.y, &m4.y, &v4.y);
-          np.z = upd_elem<true>(a, p[q].z, gq.z, &m4.z, &v4.z);
-          np.w = upd_elem<true>(a, p[q].w, gq.w, &m4.w, &v4.w);
+          np.x = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p[q].x, gq.x, &m4.x, &v4.x);
+          np.y = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p[q].y, gq.y, &m4.y, &v4.y);
+          np.z = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p[q].z, gq.z, &m4.z, &v4.z);
+          np.w = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p[q].w, gq.w, &m4.w, &v4.w);
           *reinterpret_cast<float4*>(a.m + el) = m4;
           *reinterpret_cast<float4*>(a.v + el) = v4;
         } else {
@@ -1561,7 +1589,7 @@ int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
   label_update_kernel<BF16, ADAM, true><<<std::min(max_ctas, 2 * num_sms()), kUpdThreads, 0, st>>>(a);
   ASTRA_LAUNCHED("label_check");
   if (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8) {
-    const int grid = (ADAM && nv > 6 ? 2 : 3) * num_sms();  // = upd_tma_ctas<nv, ADAM>()
+    const int grid = (ADAM && nv > 6 ? 2 : (ADAM ? ASTRA_UPD_ADAM_CTAS : 3)) * num_sms();  // = upd_tma_ctas<nv, ADAM>()
     size_t smem = 0;
     switch (nv) {
       case 1: smem = UpdRing<1, BF16, ADAM>::smem(); break;
