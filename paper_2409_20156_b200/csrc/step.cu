@@ -73,7 +73,9 @@ struct FwdArgs {
 
 __device__ __forceinline__ float expit_f32(float x) {
   // scipy.special.expit on float32: 1 / (1 + exp(-x)) in single precision
-  return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+  // (the correctly rounded reciprocal = the correctly rounded 1/y division, bit
+  // for bit, without the division's numerator scaling and slow-path branch)
+  return __frcp_rn(__fadd_rn(1.0f, expf(-x)));
 }
 
 __device__ __forceinline__ double softplus64(double x) {
@@ -705,6 +707,11 @@ __device__ __forceinline__ void push_wmax(const UpdArgs& a, float wmax, int lane
 // Sort the label's slot indices ascending. Segments <= 32 stay in a register
 // (returned); longer ones are rank-sorted into perm2.
 __device__ __forceinline__ int32_t sort_segment(const UpdArgs& a, uint32_t start, uint32_t n, int lane) {
+  if (n <= 2) {  // (most multi-occurrence labels: one compare-exchange)
+    int32_t v = lane < static_cast<int>(n) ? a.perm[start + lane] : INT_MAX;
+    const int32_t o = __shfl_xor_sync(0xffffffffu, v, 1);
+    return lane == 0 ? min(v, o) : (lane == 1 ? max(v, o) : v);
+  }
   if (n <= 32) {
     int32_t v = lane < static_cast<int>(n) ? a.perm[start + lane] : INT_MAX;
 #pragma unroll
@@ -735,7 +742,7 @@ __device__ __forceinline__ int32_t seg_slot(const UpdArgs& a, uint32_t start, ui
 }
 
 #ifndef ASTRA_ADAM_FAST
-#define ASTRA_ADAM_FAST 0
+#define ASTRA_ADAM_FAST 1
 #endif
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
@@ -1087,7 +1094,7 @@ struct SingleRing {
                                            : (ASTRA_SINGLE_CTAS == 5 ? 44u : 56u)) * 1024;
   static constexpr int RING_MAX = static_cast<int>((BUDGET - SCRATCH - QBYTES) / (ENTRY + 16));
   static constexpr int RING = RING_MAX > 32 ? 32 : RING_MAX;
-  static constexpr size_t smem() { return static_cast<size_t>(RING) * (ENTRY + 16) + SCRATCH + QBYTES; }
+  static constexpr size_t smem() { return static_cast<size_t>(RING) * (ENTRY + 16) + SCRATCH + QBYTES + 16; }
 };
 
 // The producer's per-label descriptor: bucket, first occurrence and its metadata.
@@ -1141,6 +1148,10 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
   uint64_t* empty = full + RING;
   uint64_t* qfull = empty + RING;
   uint64_t* qempty = qfull + Q;
+  // free data slots (bit r: slot r released by its consumer): a hint that
+  // spares the producer polling every slot's barrier; the barrier stays the
+  // synchronisation (the producer still waits on it, which then passes at once)
+  uint32_t* freemask = reinterpret_cast<uint32_t*>(qempty + Q);
   if (!*A.mode) return;
   const UpdArgs& a = A.u;
   const FwdArgs& fa = A.f;
@@ -1159,10 +1170,15 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       mbar_init(&qfull[r], 1);
       mbar_init(&qempty[r], 1);
     }
+    *freemask = RING == 32 ? 0xFFFFFFFFu : ((1u << RING) - 1u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int S = fa.S;
+  auto release = [&](int r) {  // lane 0, after __syncwarp: the slot's reads are done
+    mbar_arrive(&empty[r]);
+    atomicOr(freemask, 1u << r);
+  };
   if (warp == kTmaConsumers) {
     // producer warp: 32 labels per batch, every index load lane-parallel and
     // software-pipelined over batches (batch k+3: bucket, k+2: first
@@ -1215,7 +1231,6 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
     perm_load(32, q1);
     idx_load(64, q2);
     uint32_t use = 0;  // bit s: parity of the number of fills of data slot s
-    int rr = 0;
     for (int i0 = 0; i0 < n_mine; i0 += 32) {
       SingleDesc nxt;
       meta_load(i0 + 32, q1, nxt);
@@ -1227,17 +1242,13 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
         int sl = -1;
         if (lane == 0) {
           mbar_wait(&qempty[qi], ((i / Q) & 1) ^ 1);
-          while (true) {  // a free data slot: its previous fill released
-            for (int k = 0; k < RING && sl < 0; ++k) {
-              const int c = rr + k < RING ? rr + k : rr + k - RING;
-              if (mbar_test(&empty[c], ((use >> c) & 1) ^ 1)) sl = c;
-            }
-            if (sl >= 0) break;
-            __nanosleep(20);
-          }
+          uint32_t m;  // a free data slot: its previous fill released
+          while ((m = *reinterpret_cast<volatile uint32_t*>(freemask)) == 0u) __nanosleep(20);
+          sl = __ffs(m) - 1;
+          atomicAnd(freemask, ~(1u << sl));
+          mbar_wait(&empty[sl], ((use >> sl) & 1) ^ 1);
         }
         sl = __shfl_sync(0xffffffffu, sl, 0);
-        rr = sl + 1 < RING ? sl + 1 : 0;
         const uint32_t fpar = (use >> sl) & 1u;
         use ^= 1u << sl;
         if (lane == jj) {
@@ -1325,7 +1336,7 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
         vr[q] = *reinterpret_cast<const float4*>(ent + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[r]);
+      if (lane == 0) release(r);
     }
     const uint32_t n = dc.n;
     const size_t row = static_cast<size_t>(dc.l) * d;
@@ -1403,7 +1414,7 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       grad_emb_add(dc.slot0 / S, f);
       if constexpr (!ADAM) {  // W row consumed (Adam: after the moments, below)
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[r]);
+        if (lane == 0) release(r);
       }
       update_row([&](int q) {
         return make_float4(__fmul_rn(f, e0[q].x), __fmul_rn(f, e0[q].y), __fmul_rn(f, e0[q].z), __fmul_rn(f, e0[q].w));
@@ -1461,13 +1472,13 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       }
       if constexpr (!ADAM) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[r]);
+        if (lane == 0) release(r);
       }
       update_row([&](int q) { return *reinterpret_cast<const float4*>(gs + q * 128); });
     }
     if constexpr (ADAM && !EARLY) {
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[r]);
+      if (lane == 0) release(r);
     }
   }
   if (lane < c_pend) A.slot_loss[pend_slot] = slot_loss(pend_sc, pend_pt, pend_wn);
