@@ -688,23 +688,32 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
   if (fail) return;
   __syncwarp();
   const int64_t p0 = pos_indptr[q], np = pos_indptr[q + 1] - p0;
-  // part of candidate i (parts concatenated in order): the last part whose
-  // offset is <= i (binary search; empty parts share their successor's offset)
-  auto part_of = [&](int i) {
-    int lo = 0, hi = n_parts - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (sel_off[warp][mid] <= i) lo = mid; else hi = mid - 1;
+  // key of candidate i (parts concatenated in order). Each lane walks i
+  // upwards in steps of 32, so its part index only moves forward: `pc` is the
+  // lane's cursor (the last part whose offset is <= i; empty parts share their
+  // successor's offset and are stepped over).
+  auto key_at = [&](int i, int& pc) {
+    while (pc + 1 < n_parts && sel_off[warp][pc + 1] <= i) ++pc;
+    return cand[(static_cast<size_t>(pc) * nq + q) * cand_cap + (i - sel_off[warp][pc])];
+  };
+  // 1. the candidates' scores -> shared memory: few parts -> the warp walks
+  //    each part (coalesced); many small parts (the SM-filling layouts) ->
+  //    lane p copies part p (independent loads, no per-element part lookup)
+  if (n_parts <= 4) {
+    for (int p = 0; p < n_parts; ++p) {
+      const int o = sel_off[warp][p], c = sel_off[warp][p + 1] - o;
+      const uint64_t* src = cand + (static_cast<size_t>(p) * nq + q) * cand_cap;
+#pragma unroll 4
+      for (int e = lane; e < c; e += 32) S[o + e] = static_cast<uint32_t>(src[e] >> 32);
     }
-    return lo;
-  };
-  auto key_at = [&](int i) {
-    const int p = part_of(i);
-    return cand[(static_cast<size_t>(p) * nq + q) * cand_cap + (i - sel_off[warp][p])];
-  };
-  // 1. the candidates' scores -> shared memory (independent loads; lane-strided
-  //    over the concatenation, so many small parts keep every lane busy)
-  for (int i = lane; i < total; i += 32) S[i] = static_cast<uint32_t>(key_at(i) >> 32);
+  } else {
+    for (int p = lane; p < n_parts; p += 32) {
+      const int o = sel_off[warp][p], c = sel_off[warp][p + 1] - o;
+      const uint64_t* src = cand + (static_cast<size_t>(p) * nq + q) * cand_cap;
+#pragma unroll 4
+      for (int e = 0; e < c; ++e) S[o + e] = static_cast<uint32_t>(src[e] >> 32);
+    }
+  }
   __syncwarp();
   // 2. T2 = the (k + |P|)-th largest score over ALL candidates: at most |P| of
   //    the keys above the k-th non-positive one are positives, so every key of
@@ -721,6 +730,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
   // 3. warp-aggregated compaction of the keys with score >= T2 (full keys
   //    fetched back from the lists for those only)
   int nr = 0;
+  int pc = 0;
   for (int i0 = 0; i0 < total; i0 += 32) {
     const int i = i0 + lane;
     const uint32_t sc = i < total ? S[i] : 0u;
@@ -728,7 +738,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
     const unsigned bm = __ballot_sync(0xffffffffu, take);
     const int at = nr + __popc(bm & ((1u << lane) - 1u));
     if (take && at < rcap) {
-      const uint64_t v = key_at(i);
+      const uint64_t v = key_at(i, pc);
       R[at] = v;
     }
     nr += __popc(bm);

@@ -829,10 +829,14 @@ void refresh_tc_layout(int64_t nq, int64_t n_tiles, int* n_ctas, int* n_parts) {
   // layout that keeps every cluster busy to within 1% (e.g. 37 parts x 36
   // query-tile pairs = 18 rounds of 74 pairs on 148 SMs) while parts stay
   // >= 64 tiles long, else the fewest parts reaching 93%
+  static const bool fill = [] {  // ASTRA_REFRESH_FILL=0: the 93% rule alone (A/B aid)
+    const char* e = getenv("ASTRA_REFRESH_FILL");
+    return !(e && atoi(e) == 0);
+  }();
   int64_t best_p = 1;
   double best_eff = -1.0;
   const int64_t p_max = std::min<int64_t>(n_tiles, 64);
-  for (int64_t p = 1; p <= p_max; ++p) {
+  for (int64_t p = 1; p <= (fill ? p_max : 0); ++p) {
     if (p > 1 && n_tiles / p < 64) break;
     if (eff_of(p) >= 0.99) {
       best_p = p;

@@ -66,7 +66,7 @@ class ClassifierEngine:
             W = torch.as_tensor(weights)[self.lo : self.hi].to(self.device, torch.float32)
         self.W = W.to(w_dtype).contiguous()
         # running bound on max|W| (kept current by every update): lets the step
-        # prove finiteness up front and run the L2-chunked fused schedule
+        # prove finiteness up front and take the single label-major step pass
         self.w_absmax = self.W.abs().amax().float().reshape(1).clone() if self.W.numel() else \
             torch.zeros(1, dtype=torch.float32, device=self.device)
         self.m = self.v = None

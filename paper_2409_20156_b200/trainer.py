@@ -61,6 +61,15 @@ def _positives_csr(state, batch_rows):
 
 def _assemble_batch_slates(state, batch_rows, epoch, rng, hard_batch):
     """Philox slates for one batch (trainer.py:262-318 contract)."""
+    ids, y, origin, weights = _slates_device(state, batch_rows, epoch, rng, hard_batch)
+    return (ids.cpu().numpy().astype(np.int64), y.cpu().numpy(), origin[0].cpu().numpy(),
+            weights[0].cpu().numpy())
+
+
+def _slates_device(state, batch_rows, epoch, rng, hard_batch):
+    """The slates of _assemble_batch_slates as device tensors (ids [B, S]
+    int32, y [B, S] int8, origin / weights [B, S]); consumes the caller's
+    generator exactly as _assemble_batch_slates does (one 63-bit draw)."""
     cfg = state.config
     L = state.dataset.n_labels
     k_h_eff = 0 if hard_batch is None else hard_batch.shape[1]
@@ -75,11 +84,8 @@ def _assemble_batch_slates(state, batch_rows, epoch, rng, hard_batch):
     rows = np.asarray(batch_rows, dtype=np.int64)
     indptr, pos = _positives_csr(state, rows)
     hard = None if hard_batch is None else torch.from_numpy(np.ascontiguousarray(hard_batch, dtype=np.int32)).to(dev)
-    ids, y, origin, weights = ops.sample_slates(
-        seed, int(epoch), 0, torch.from_numpy(rows).to(dev), torch.from_numpy(indptr).to(dev),
-        torch.from_numpy(pos).to(dev), hard, k_h_eff, L, cfg.k_p, k_r_eff)
-    return (ids.cpu().numpy().astype(np.int64), y.cpu().numpy(), origin[0].cpu().numpy(),
-            weights[0].cpu().numpy())
+    return ops.sample_slates(seed, int(epoch), 0, torch.from_numpy(rows).to(dev), torch.from_numpy(indptr).to(dev),
+                             torch.from_numpy(pos).to(dev), hard, k_h_eff, L, cfg.k_p, k_r_eff)
 
 
 def _uptodate_hard_batch(state, batch_rows, embeddings, epoch):
@@ -139,17 +145,22 @@ def _batch_forward_backward(state, batch_rows, epoch, rng, step_lr_enc, step_lr_
             if hard_batch.shape[1] == 0:
                 hard_batch = None
 
-    ids, y, origin, weights = xt._assemble_batch_slates(state, batch_rows, epoch, rng, hard_batch)
-
     ops = _backend.get()
     dev = _backend.device()
+    if xt._assemble_batch_slates is _assemble_batch_slates:
+        # the installed sampler: its slates stay on the device (no host round trip)
+        ids_d, y_d, origin_d, weights_d = _slates_device(state, batch_rows, epoch, rng, hard_batch)
+        origin_d, weights_d = origin_d[0], weights_d[0]
+    else:  # a caller-provided slate function (e.g. the reference's, ASTRA_DROPIN_SLATES=reference)
+        ids, y, origin, weights = xt._assemble_batch_slates(state, batch_rows, epoch, rng, hard_batch)
+        ids_d = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)).to(dev)
+        y_d = torch.from_numpy(np.ascontiguousarray(y, dtype=np.int8)).to(dev)
+        origin_d = torch.from_numpy(np.ascontiguousarray(origin, dtype=np.int8)).to(dev)
+        weights_d = torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float32)).to(dev)
     bank = DeviceBank.attach(state.bank)
-    ids_d = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)).to(dev)
     res = ops.slate_step(
-        torch.from_numpy(np.ascontiguousarray(emb_used, dtype=np.float32)).to(dev), ids_d,
-        torch.from_numpy(np.ascontiguousarray(y, dtype=np.int8)).to(dev),
-        torch.from_numpy(np.ascontiguousarray(origin, dtype=np.int8)).to(dev),
-        torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float32)).to(dev), bank.W, float(step_lr_clf),
+        torch.from_numpy(np.ascontiguousarray(emb_used, dtype=np.float32)).to(dev), ids_d, y_d,
+        origin_d.contiguous(), weights_d.contiguous(), bank.W, float(step_lr_clf),
         float(cfg.weight_decay_classifier),
         keep=None if keep is None else torch.from_numpy(np.ascontiguousarray(keep)).to(dev),
         w_absmax=bank.w_absmax if FAST_STEP else None)
