@@ -957,16 +957,18 @@ def run_fullloss(args):
     """The all-negatives arm (train_full_loss_baseline, trainer.py:563-616) at
     the reference's label cap (L = 50,000, d = 768, B = 1024, 38 positives per
     row): per step, scores E W^T, G and the float64 BCE, grad_emb = G W, and the
-    dense SGD of every row (G^T E) — three fp32 cuBLAS GEMMs (TF32 off) +
-    astra_dense_bce / astra_dense_sgd — next to the oracle port of the same
+    dense SGD of every row (G^T E) — three fp32-accurate GEMMs on the tf32
+    tensor cores (astra_gemm_f32, 3xTF32) + astra_dense_bce / astra_dense_sgd —
+    next to the oracle port of the same
     NumPy arithmetic on the host cores (one minibatch). The dense comparison
     for the sampled arm."""
     import torch
 
     from oracle import xcmix_port as port
-    from paper_2409_20156_b200 import ops
+    from paper_2409_20156_b200 import _lib, ops
 
     torch.cuda.set_device(0)
+    hbm, tf_burst, tf_sus, peak_kind = peaks()
     L, d, B, lpp = 50_000, 768, 1024, 38
     rng = np.random.default_rng(0)
     W = rng.uniform(-1 / np.sqrt(d), 1 / np.sqrt(d), size=(L, d)).astype(np.float32)
@@ -990,14 +992,22 @@ def run_fullloss(args):
     for t in range(args.warmup):
         one(t)
     torch.cuda.synchronize()
+    _lib.kernel_timing("gemm_f32")
+    _lib.kernel_timing_enable(True)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for t in range(args.steps):
         loss = one(t)
     b.record(stream)
     torch.cuda.synchronize()
+    _lib.kernel_timing_enable(False)
+    gemm_ms, gemm_n = _lib.kernel_timing("gemm_f32")
     ms = a.elapsed_time(b) / args.steps
     flops = 3 * 2.0 * B * L * d
+    # the GEMM kernel issues 3 tf32 products per fp32 product (hi*hi + lo*hi + hi*lo):
+    # tensor work = 3 x the algorithmic flops; the tf32 dense rate is half the bf16 one
+    t_gemm = gemm_ms / max(gemm_n, 1) / 1e3
+    tf32_peak = tf_burst / 2
     t0 = time.perf_counter()
     Wc = W.copy()
     yb = port.dense_y(lists[0], L)
@@ -1008,11 +1018,20 @@ def run_fullloss(args):
         "metric": "full-loss (all-negatives) arm train samples/s", "value": round(B / (ms / 1e3), 1),
         "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp32 (cuBLAS sgemm, TF32 off) + float64 loss", "data": "synthetic",
+        "dtype": "fp32-accurate GEMMs on the tf32 tensor cores (3xTF32 split, astra_gemm_f32) + float64 loss",
+        "data": "synthetic",
         "config": {"workload": "train_full_loss_baseline at the reference's label cap", "n_labels": L, "dim": d,
                    "minibatch": B, "labels_per_point": lpp},
-        "roofline": {"bound": "fp32 SIMT GEMM", "achieved": round(flops / (ms / 1e3) / 1e12, 2), "unit": "TFLOP/s",
-                     "algorithmic": f"3 GEMMs x 2*B*L*d = {flops:.3e} flop per step"},
+        "fp32_equivalent_tflops": round(flops / (ms / 1e3) / 1e12, 2),
+        "roofline": {"bound": "tensor", "kernel": "gemm_f32 (tcgen05 kind::tf32, CTA pairs, 3 products per fp32 product)",
+                     "achieved": round(flops / t_gemm / 1e12, 2) if gemm_n else None,
+                     "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
+                     "frac": round(flops / t_gemm / 1e12 / tf32_peak, 4) if gemm_n else None,
+                     "traffic": None,
+                     "algorithmic": f"3 GEMMs x 2*B*L*d = {flops:.3e} fp32 flop per step = 3x that in tf32 MMA work; "
+                                    "achieved = tf32 MMA flops of one launch (3 x 2*M*N*K) / its duration",
+                     "launch_ms": round(t_gemm * 1e3, 4) if gemm_n else None,
+                     "peak_kind": f"{peak_kind} burst bf16 / 2 (tf32 dense rate)"},
         "cpu_baseline": {"value": round(B / t_cpu, 2), "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
                          "sample": "one minibatch of the NumPy arm (oracle port), threads=all"},
     }

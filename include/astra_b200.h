@@ -263,8 +263,8 @@ int astra_apply_updates(void* W, int w_dtype, int64_t n_labels, int d, const int
 /* ------------------------------------------------------------------------
  * All-negatives (full-loss) arm, train_full_loss_baseline (trainer.py:563-616),
  * and the dense probe loss, _probe_full_loss (trainer.py:398-403). The arm's
- * GEMMs (E W^T, G W, G^T E) are plain fp32 library GEMMs issued by the host;
- * these are its elementwise parts.
+ * fp32 GEMMs (E W^T, G W, G^T E: trainer.py:593-606) run on the tf32 tensor
+ * cores split three ways (astra_gemm_f32); the elementwise parts follow.
  *
  * astra_dense_bce: scores B x n_labels (fp32, or fp64 when scores_f64), the
  * positives as a CSR (pos_indptr[B+1] int64, pos_ids int32, sorted distinct
@@ -281,6 +281,18 @@ int astra_dense_bce(const void* scores, int scores_f64, int B, int64_t n_labels,
  * rounded like NumPy (trainer.py:604-606; no finiteness check, as there). */
 int astra_dense_sgd(float* W, const float* grads, int64_t n, float lr, float weight_decay,
                     void* stream);
+
+/* D[M, N] = A B^T in fp32 accuracy on the tf32 tensor cores (3xTF32: each
+ * operand split into a tf32 hi part and an fp32 remainder; hi*hi + lo*hi +
+ * hi*lo accumulated in fp32; replaces the host's numpy sgemm of the
+ * full-loss arm, trainer.py:593-606). A is [M, K] row-major (a_kmajor = 1)
+ * or given transposed as [K, M] row-major (a_kmajor = 0); B likewise [N, K]
+ * or [K, N]. D is [M, N] row-major, overwritten. Summation order differs from
+ * a sequential sgemm: results agree to fp32 rounding of the sum (tolerance
+ * 1e-5 relative in the tests). Workspace: astra_gemm_f32_workspace_size. */
+size_t astra_gemm_f32_workspace_size(int64_t M, int64_t N, int64_t K);
+int astra_gemm_f32(const float* A, int a_kmajor, const float* B, int b_kmajor, int64_t M, int64_t N, int64_t K,
+                   float* D, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Synchronous helper: cudaStreamSynchronize + error mapping. */
 int astra_stream_sync(void* stream);

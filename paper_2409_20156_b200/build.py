@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libastra_b200.so")
-SOURCES = ["capi.cu", "sampler.cu", "step.cu", "refresh.cu", "refresh_tc.cu", "dense.cu"]
+SOURCES = ["capi.cu", "sampler.cu", "step.cu", "refresh.cu", "refresh_tc.cu", "dense.cu", "dense_tc.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -75,6 +75,9 @@ size_t dense_workspace_size(int B);
 int dense_bce(const void* S, int s_f64, int B, int64_t L, const int64_t* pos_indptr, const int32_t* pos_ids,
               float* G, double* loss_out, void* workspace, size_t ws_bytes, cudaStream_t st);
 int dense_sgd(float* W, const float* grads, int64_t n, float lr, float wd, cudaStream_t st);
+size_t gemm_f32_workspace(int64_t M, int64_t N, int64_t K);
+int gemm_f32(const float* A, int a_kmajor, const float* B, int b_kmajor, int64_t M, int64_t N, int64_t K, float* D,
+             void* ws, size_t ws_bytes, cudaStream_t st);
 int slate_step(const float*, const float*, const int32_t*, const int8_t*, const int8_t*, int64_t, const float*,
                int64_t, const float*, int, int, int, void*, int, float*, float*, int, int64_t, int64_t, double, double,
                double, double, double, int64_t, float*, double*, int32_t*, float*, float*, void*, size_t, cudaStream_t);
@@ -215,6 +218,13 @@ int astra_dense_bce(const void* scores, int scores_f64, int B, int64_t n_labels,
 
 int astra_dense_sgd(float* W, const float* grads, int64_t n, float lr, float weight_decay, void* stream) {
   return dense_sgd(W, grads, n, lr, weight_decay, S(stream));
+}
+
+size_t astra_gemm_f32_workspace_size(int64_t M, int64_t N, int64_t K) { return gemm_f32_workspace(M, N, K); }
+
+int astra_gemm_f32(const float* A, int a_kmajor, const float* B, int b_kmajor, int64_t M, int64_t N, int64_t K,
+                   float* D, void* workspace, size_t workspace_bytes, void* stream) {
+  return gemm_f32(A, a_kmajor, B, b_kmajor, M, N, K, D, workspace, workspace_bytes, S(stream));
 }
 
 int astra_stream_sync(void* stream) { return check_cuda(cudaStreamSynchronize(S(stream)), "stream sync"); }

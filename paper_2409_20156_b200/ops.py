@@ -220,7 +220,7 @@ def slate_step(emb, ids, y, origin, weights, W, lr, weight_decay=0.0, keep=None,
 
     origin/weights may be S-vectors (the reference's row-0 semantics) or B x S.
     w_absmax: optional fp32[1] CUDA tensor, a running bound on max|W| kept
-    current by the call (enables the L2-chunked fused step)."""
+    current by the call (enables the single label-major pass)."""
     _cuda(emb, torch.float32, "emb")
     _cuda(keep, torch.float32, "keep")
     _cuda(ids, torch.int32, "ids")
@@ -282,35 +282,46 @@ def dense_sgd(W, grads, lr, weight_decay=0.0):
     _lib.check(_lib.load().astra_dense_sgd(_p(W), _p(grads), W.numel(), float(lr), float(weight_decay), _stream()))
 
 
-def _fp32_gemm(a, b):
-    """A plain fp32 library GEMM (cuBLAS), TF32 off: the reference's BLAS sgemm."""
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        return torch.matmul(a, b)
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
+def gemm_f32(a, b, a_t=False, b_t=False):
+    """D = op(a) op(b)^T in fp32 accuracy on the tf32 tensor cores
+    (astra_gemm_f32, 3xTF32). a: [M, K] (a_t: given as [K, M]); b: [N, K]
+    (b_t: given as [K, N]). Returns D [M, N] fp32."""
+    _cuda(a, torch.float32, "a")
+    _cuda(b, torch.float32, "b")
+    a, b = a.contiguous(), b.contiguous()
+    M, K = (a.shape[1], a.shape[0]) if a_t else (a.shape[0], a.shape[1])
+    N, Kb = (b.shape[1], b.shape[0]) if b_t else (b.shape[0], b.shape[1])
+    if K != Kb:
+        raise ConfigError(f"gemm_f32: inner dimensions differ ({K} vs {Kb})")
+    lib = _lib.load()
+    ws = WORKSPACES.get("gemm_f32", lib.astra_gemm_f32_workspace_size(M, N, K), a.device)
+    D = torch.empty((M, N), dtype=torch.float32, device=a.device)
+    _lib.check(lib.astra_gemm_f32(_p(a), 0 if a_t else 1, _p(b), 0 if b_t else 1, M, N, K, _p(D), _p(ws), ws.numel(),
+                                  _stream()))
+    return D
 
 
 def full_loss_forward(emb_used, W, pos_indptr, pos_ids, keep=None):
     """One batch of the all-negatives arm before the update (trainer.py:593-599):
-    scores = emb_used W^T (fp32 cuBLAS), G and the float64 loss (astra_dense_bce),
-    grad_emb = G W (x keep). Returns (loss_dev, G, grad_emb)."""
+    scores = emb_used W^T, G and the float64 loss (astra_dense_bce),
+    grad_emb = G W (x keep); both GEMMs astra_gemm_f32 (3xTF32 tensor cores).
+    Returns (loss_dev, G, grad_emb)."""
     _cuda(emb_used, torch.float32, "emb_used")
     _cuda(W, torch.float32, "W")
     _cuda(keep, torch.float32, "keep")
-    scores = _fp32_gemm(emb_used, W.t())
+    scores = gemm_f32(emb_used, W)
     G, loss = dense_bce(scores, pos_indptr, pos_ids)
     del scores
-    grad_emb = _fp32_gemm(G, W)
+    grad_emb = gemm_f32(G, W, b_t=True)
     if keep is not None:
         grad_emb = grad_emb * keep
     return loss, G, grad_emb
 
 
 def full_loss_update(W, G, emb_used, lr, weight_decay=0.0):
-    """W -= f32(lr) (G^T emb_used + f32(wd) W) (trainer.py:602-606)."""
-    dense_sgd(W, _fp32_gemm(G.t(), emb_used), lr, weight_decay)
+    """W -= f32(lr) (G^T emb_used + f32(wd) W) (trainer.py:602-606); the GEMM
+    on the tensor cores (astra_gemm_f32)."""
+    dense_sgd(W, gemm_f32(G, emb_used, a_t=True, b_t=True), lr, weight_decay)
 
 
 def dense_probe_loss(emb, W, pos_indptr, pos_ids):

@@ -5,7 +5,7 @@ set -e
 name=$1; shift
 d=paper_2409_20156_b200
 mkdir -p /tmp/variant_$name
-for src in capi sampler step refresh refresh_tc dense; do
+for src in capi sampler step refresh refresh_tc dense dense_tc; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr \
     -Xcompiler -fPIC,-O2 "$@" -c $d/csrc/$src.cu -o /tmp/variant_$name/$src.o &
 done
