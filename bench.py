@@ -561,11 +561,30 @@ def run_emulate(args):
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3 + 2 * M)] for _ in range(n_steps)]
     keep_ids = []
 
+    # BF16_RERANK over shards (engine._refresh_sharded_rerank): this shard's bf16
+    # top-k' of all rows, the owner's merge of the N lists of its R rows (the
+    # global k'-th key tau), then the fp32 re-rank of only the candidates >= tau.
+    # tau needs the other shards' lists, which this single-GPU emulation does not
+    # compute: it stands in this shard's ceil(k'/N)-th key (the expected share of
+    # an i.i.d. shard in the global top-k'), so the re-rank does the real job's
+    # expected work; the merge runs on this shard's list replicated N times.
+    global_rr = args.refresh_mode == "bf16_rerank" and not args.emulate_full_rerank
+    kc = ops.rerank_candidates_count(k_h)
+    flip = torch.tensor(-(2 ** 63), dtype=torch.int64, device="cuda")
+
     def one(t, timed):
         q, pid, hard = data[t]
         e = ev[t]
         e[0].record(stream)
-        keys, _, _ = ops.refresh_topk(q, ip_step, pid, k_h, args.refresh_mode, labels_f32=snap_f32, label_offset=lo, **lp)
+        if global_rr:
+            ckeys, _, _ = ops.refresh_topk(q, ip_step, pid, kc, "bf16", labels_f32=snap_f32, label_offset=lo, **lp)
+            ops.topk_merge(ckeys[:R].unsqueeze(0).expand(N, R, kc).contiguous(), kc)  # owner's merge (stand-in data)
+            tau = ckeys[:, -(-kc // N) - 1].contiguous()  # (proxy of the all-gathered global tau)
+            cand = torch.where((ckeys ^ flip) >= (tau[:, None] ^ flip), ckeys, torch.zeros_like(ckeys))
+            keys, _, _ = ops.rerank_candidates(q, cand, k_h, labels_f32=snap_f32, label_offset=lo)
+        else:
+            keys, _, _ = ops.refresh_topk(q, ip_step, pid, k_h, args.refresh_mode, labels_f32=snap_f32,
+                                          label_offset=lo, **lp)
         e[1].record(stream)
         ops.topk_merge(keys.view(N, R, k_h), k_h)  # the N shards' lists of this rank's R rows
         e[2].record(stream)
@@ -624,6 +643,8 @@ def run_emulate(args):
         "queries_all_gather": (N - 1) * R * d * 4,
         "positives_all_gather": (N - 1) * R * (lpp * 4 + 8),
         "keys_all_to_all": (N - 1) * R * k_h * 8,
+        **({"bf16_candidate_keys_all_to_all": (N - 1) * R * kc * 8, "tau_all_gather": (N - 1) * R * 8}
+           if global_rr else {}),
         **({"sampler_inputs_all_gather": M * (N - 1) * B * (8 + lpp * 4 + 8 + k_h * 4)} if regen else
            {"slates_all_gather": M * (N - 1) * B * S * 10}),
         "emb_all_gather": M * (N - 1) * B * d * 4,
@@ -636,7 +657,10 @@ def run_emulate(args):
         "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32 W/step, bf16 tensor-core refresh + fp32 re-rank", "data": "synthetic",
         "config": dict(bench_config(N), labels_shard=Lr, rows_per_step_job=Rg, minibatch_job=Bg,
-                       slate_exchange=args.slate_exchange),
+                       slate_exchange=args.slate_exchange,
+                       sharded_rerank=("global k'-th bf16 key threshold (engine._refresh_sharded_rerank; "
+                                       "tau proxied by this shard's ceil(k'/N)-th key)") if global_rr
+                       else "every shard re-ranks its full local top-k'"),
         "phases_ms_per_step": {k: round(v, 4) for k, v in ph.items()},
         "owned_slots_per_minibatch": round(slots, 1), "unique_owned_labels_per_minibatch": round(U, 1),
         "occurrences_per_owned_label": round(slots / max(U, 1), 3),
@@ -776,6 +800,8 @@ def run_c5shard(args):
     achieved = flops / (gemm_ms / max(gemm_n, 1) / 1e3) / 1e12
     step_bytes = U * d * (2 * 2 + 2 * 8) + 2 * B * d * 4 + B * sl[0].shape[1] * 5
     upd_ms, upd_n = kt["label_update"]
+    sgl_ms, sgl_n = kt["step_single"]
+    upd_bytes = U * d * (2 * 2 + 2 * 8)
     line = {
         "metric": METRIC + " [C5 shard emulation]", "value": round(B / (ms / 1e3), 1), "unit": UNIT, "n_gpus": 1,
         "emulates_n_gpus": N, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 3),
@@ -797,7 +823,12 @@ def run_c5shard(args):
         "roofline_step": {"bound": "hbm", "achieved": round(step_bytes / (ph["step"] / 1e3) / 1e9, 1), "peak": hbm,
                           "unit": "GB/s", "frac": round(step_bytes / (ph["step"] / 1e3) / 1e9 / hbm, 4),
                           "algorithmic": f"U*d*(2*2 + 2*8) + 2*B*d*4 + B*S*5 = {step_bytes:.3e} B (U={U})",
-                          "label_update_launch_ms": round(upd_ms / max(upd_n, 1), 4) if upd_n else None},
+                          "label_update_launch_ms": round(upd_ms / max(upd_n, 1), 4) if upd_n else None,
+                          "kernels": {name: {"launch_ms": round(ms_ / n_, 4),
+                                             "achieved_gbs": round(upd_bytes / (ms_ / n_ / 1e3) / 1e9, 1),
+                                             "algorithmic_bytes": int(upd_bytes)}
+                                      for name, (ms_, n_) in (("step_single", (sgl_ms, sgl_n)),
+                                                              ("label_update", (upd_ms, upd_n))) if n_}},
         "memory_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
         "clocks": clk,
     }
@@ -1157,6 +1188,8 @@ def main():
                          "install())")
     ap.add_argument("--refresh-sms", type=int, default=0,
                     help="SM budget of the refresh running concurrently with training on a side stream (0 = serial)")
+    ap.add_argument("--emulate-full-rerank", action="store_true",
+                    help="--emulate: every shard re-ranks its full local top-k' (no global threshold)")
     ap.add_argument("--emulate", type=int, default=0,
                     help="one GPU runs rank 0's share of an N-GPU C4 job (a 1/N label shard, all N ranks' rows); "
                          "collectives are not run, their bytes are reported")

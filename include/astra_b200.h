@@ -282,6 +282,18 @@ int astra_dense_bce(const void* scores, int scores_f64, int B, int64_t n_labels,
 int astra_dense_sgd(float* W, const float* grads, int64_t n, float lr, float weight_decay,
                     void* stream);
 
+/* The refresh's fp32 re-rank on its own (the last stage of BF16_RERANK,
+ * anns.py:253-256 scores): for each of nq queries (fp32 [nq, d]) score the
+ * kc candidate keys cand[q * kc + j] (astra key format; 0 = no candidate)
+ * against the label rows (fp32, or bf16 when w_dtype = ASTRA_W_BF16; [L_local,
+ * d], candidate id - label_offset = row) with the FP32_EXACT fmaf order and
+ * write the best k (k <= kc) as keys / ids / scores (-1 / -inf past the
+ * candidates). Used by the label-sharded refresh: each shard re-ranks only its
+ * candidates at or above the global k'-th bf16 key. */
+int astra_rerank_candidates(const float* queries, int64_t nq, int d, const uint64_t* cand, int kc,
+                            const void* labels, int w_dtype, int64_t label_offset, int k, uint64_t* out_keys,
+                            int32_t* out_ids, float* out_scores, void* stream);
+
 /* D[M, N] = A B^T in fp32 accuracy on the tf32 tensor cores (3xTF32: each
  * operand split into a tf32 hi part and an fp32 remainder; hi*hi + lo*hi +
  * hi*lo accumulated in fp32; replaces the host's numpy sgemm of the

@@ -46,6 +46,7 @@ _SIGS = {
     "astra_dense_workspace_size": ([i32], sz),
     "astra_dense_bce": ([p, i32, i32, i64, p, p, p, p, p, sz, p], i32),
     "astra_dense_sgd": ([p, p, i64, f32, f32, p], i32),
+    "astra_rerank_candidates": ([p, i64, i32, p, i32, p, i32, i64, i32, p, p, p, p], i32),
     "astra_gemm_f32_workspace_size": ([i64, i64, i64], sz),
     "astra_gemm_f32": ([p, i32, p, i32, i64, i64, i64, p, p, sz, p], i32),
     "astra_stream_sync": ([p], i32),

@@ -76,6 +76,8 @@ int dense_bce(const void* S, int s_f64, int B, int64_t L, const int64_t* pos_ind
               float* G, double* loss_out, void* workspace, size_t ws_bytes, cudaStream_t st);
 int dense_sgd(float* W, const float* grads, int64_t n, float lr, float wd, cudaStream_t st);
 size_t gemm_f32_workspace(int64_t M, int64_t N, int64_t K);
+int rerank_only(const float* qf, int64_t nq, int d, const uint64_t* cand, int kc, const void* labels, int w_dtype,
+                int64_t off, int k, uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st);
 int gemm_f32(const float* A, int a_kmajor, const float* B, int b_kmajor, int64_t M, int64_t N, int64_t K, float* D,
              void* ws, size_t ws_bytes, cudaStream_t st);
 int slate_step(const float*, const float*, const int32_t*, const int8_t*, const int8_t*, int64_t, const float*,
@@ -218,6 +220,13 @@ int astra_dense_bce(const void* scores, int scores_f64, int B, int64_t n_labels,
 
 int astra_dense_sgd(float* W, const float* grads, int64_t n, float lr, float weight_decay, void* stream) {
   return dense_sgd(W, grads, n, lr, weight_decay, S(stream));
+}
+
+int astra_rerank_candidates(const float* queries, int64_t nq, int d, const uint64_t* cand, int kc, const void* labels,
+                            int w_dtype, int64_t label_offset, int k, uint64_t* out_keys, int32_t* out_ids,
+                            float* out_scores, void* stream) {
+  return rerank_only(queries, nq, d, cand, kc, labels, w_dtype, label_offset, k, out_keys, out_ids, out_scores,
+                     S(stream));
 }
 
 size_t astra_gemm_f32_workspace_size(int64_t M, int64_t N, int64_t K) { return gemm_f32_workspace(M, N, K); }

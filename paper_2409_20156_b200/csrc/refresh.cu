@@ -369,13 +369,18 @@ __global__ void __launch_bounds__(64) rerank_tma_kernel(const float* Q, const vo
   __syncthreads();
   if (warp == 0) {
     // ---------------- producer: lane t copies candidate u*32+t's row chunks
+    // (units of 32 empty keys — candidates filtered out by the caller — are
+    // skipped by both warps; `seq` numbers the stage fills actually made)
+    int seq = 0;
     for (int u = 0; u < n_units; ++u) {
       const int c = u * 32 + lane;
       const uint64_t key = c < kc ? cand[q * kc + c] : 0ull;
       const int32_t gid = key ? key_id(key) : -1;
-      const uint32_t nbytes = __popc(__ballot_sync(0xffffffffu, gid >= 0)) * ch * esz;
+      const unsigned live = __ballot_sync(0xffffffffu, gid >= 0);
+      if (!live) continue;
+      const uint32_t nbytes = __popc(live) * ch * esz;
       for (int h = 0; h < nch; ++h) {
-        const int i = u * nch + h, st = i % kRtRing;
+        const int i = seq++, st = i % kRtRing;
         mbar_wait(&empty[st], ((i / kRtRing) & 1) ^ 1);
         if (lane == 0) mbar_expect_tx(&full[st], nbytes);
         __syncwarp();
@@ -391,15 +396,17 @@ __global__ void __launch_bounds__(64) rerank_tma_kernel(const float* Q, const vo
   uint64_t keys[R];
 #pragma unroll
   for (int u = 0; u < R; ++u) keys[u] = 0ull;
+  int seq = 0;
 #pragma unroll
   for (int u = 0; u < R; ++u) {
     if (u < n_units) {
       const int c = u * 32 + lane;
       const uint64_t key = c < kc ? cand[q * kc + c] : 0ull;
       const int32_t gid = key ? key_id(key) : -1;
+      if (!__ballot_sync(0xffffffffu, gid >= 0)) continue;
       float s = 0.0f;
       for (int h = 0; h < nch; ++h) {
-        const int i = u * nch + h, st = i % kRtRing;
+        const int i = seq++, st = i % kRtRing;
         mbar_wait(&full[st], (i / kRtRing) & 1);
         const unsigned char* row = ring + st * stage_bytes + lane * pitch;
         const float* qh = qs + h * ch;
@@ -454,6 +461,42 @@ int launch_rerank_tma(const float* qf, const void* wl, int d, int64_t off, const
   ASTRA_LAUNCHED("rerank_tma");
   return ASTRA_OK;
 }
+
+}  // namespace
+
+// The fp32 re-rank on its own: score the caller's candidate keys (zero keys =
+// none) against the fp32 (or bf16) label rows with the FP32_EXACT fmaf order
+// and keep the best k (the multi-GPU refresh re-ranks only the candidates at
+// or above the global k'-th bf16 key, engine.refresh).
+int rerank_only(const float* qf, int64_t nq, int d, const uint64_t* cand, int kc, const void* labels, int w_dtype,
+                int64_t off, int k, uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st) {
+  if (nq <= 0) return ASTRA_OK;
+  if (k < 1 || k > kc) return set_error(ASTRA_ERR_CONFIG, "rerank: need 1 <= k <= kc (k=%d, kc=%d)", k, kc);
+  const bool bf16 = w_dtype == ASTRA_W_BF16;
+  if (kc <= 512 && d % 64 == 0 && (reinterpret_cast<uintptr_t>(labels) & 15) == 0) {
+    auto go = [&](auto r_tag) {
+      constexpr int R = decltype(r_tag)::value;
+      return bf16 ? launch_rerank_tma<R, true>(qf, labels, d, off, cand, nq, kc, k, out_keys, out_ids, out_scores, st)
+                  : launch_rerank_tma<R, false>(qf, labels, d, off, cand, nq, kc, k, out_keys, out_ids, out_scores, st);
+    };
+    if (kc <= 32) return go(std::integral_constant<int, 1>());
+    if (kc <= 64) return go(std::integral_constant<int, 2>());
+    if (kc <= 128) return go(std::integral_constant<int, 4>());
+    if (kc <= 256) return go(std::integral_constant<int, 8>());
+    return go(std::integral_constant<int, 16>());
+  }
+  if (bf16) return set_error(ASTRA_ERR_CONFIG, "rerank from bf16 labels needs kc <= 512, d %% 64 == 0");
+  int Pn = 1;
+  while (Pn < kc) Pn <<= 1;
+  const size_t smem = align_up(sizeof(float) * (d + kRrWarps * 32 * kRrPitch), 16) + sizeof(uint64_t) * Pn;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  rerank_kernel<<<static_cast<unsigned>(nq), kRrWarps * 32, smem, st>>>(qf, static_cast<const float*>(labels), d, off,
+                                                                         cand, kc, k, out_keys, out_ids, out_scores);
+  ASTRA_LAUNCHED("rerank");
+  return ASTRA_OK;
+}
+
+namespace {
 
 __global__ void f32_to_bf16_kernel(const float* src, uint16_t* dst, int64_t n) {
   const int64_t i0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 4;

@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(kTmaThreads, upd_tma_ctas<NV, ADAM>()) label_u
 }
 
 // ================================================================ single-pass step
-// The default schedule for SGD (Adam: opt-in, ASTRA_STEP_SINGLE_ADAM=1) when
+// The default schedule (SGD and Adam; ASTRA_STEP_SINGLE_ADAM=0: Adam two-kernel) when
 // d % 128 == 0, d <= 768: ONE label-major pass over the touched rows. Each CTA
 // owns a contiguous chunk of the sorted unique-label list; a producer warp
 // builds each label's descriptor (bucket, first occurrence + its metadata)
@@ -1738,15 +1738,15 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     const char* e = getenv("ASTRA_STEP_SINGLE");
     return e ? atoi(e) != 0 : true;
   }();
-  // Adam: the pass is instruction-bound (IEEE div + sqrt on 24 elements per
-  // lane) and the two-kernel schedule (update kernel at 3 CTAs/SM) measures
-  // faster at every shard size: bf16 W + Adam, 1.3M labels: 0.28 + 1.31 vs
-  // 2.75 ms per 1024-row minibatch; the C5 shard (15M labels, 4096 x 2416
-  // slates): 5.65 vs 6.78 ms per step. ASTRA_STEP_SINGLE_ADAM=1 forces the
-  // single pass (parity-tested bit-identical). nv = 8 spills.
+  // Adam: with the MUFU sqrt / reciprocal update on bf16 W the single pass
+  // measures slightly faster than the two-kernel schedule at the C5 shard
+  // (15M labels, 4096 x 2344 slates, under the refresh's power cap: step 4.21
+  // vs 4.35 ms, profiles/r02s3/ab_adam_single_c5.txt); with the IEEE sequences
+  // it was slower (6.78 vs 5.65 ms). ASTRA_STEP_SINGLE_ADAM=0 selects the
+  // two-kernel schedule (parity-tested bit-identical). nv = 8 spills.
   static const bool single_adam = [] {
     const char* e = getenv("ASTRA_STEP_SINGLE_ADAM");
-    return e != nullptr && atoi(e) != 0;
+    return e == nullptr || atoi(e) != 0;
   }();
   const bool single = single_env && !g_step_deterministic.load() && chunkable && nv <= 6 &&
                       (!adam || single_adam) &&

@@ -77,6 +77,10 @@ class ClassifierEngine:
         self.snap_f32 = self.snap_bf16 = self.snap_f8 = None
         self.snapshot_epoch = -1
         self.slate_exchange = "gather"  # or "regenerate" (see sample())
+        # BF16_RERANK over shards: re-rank only the candidates at or above the
+        # global k'-th bf16 key (_refresh_sharded_rerank); False: every shard
+        # re-ranks its full local top-k'
+        self.global_rerank_threshold = True
 
     # ------------------------------------------------------------ snapshot
     def snapshot(self, epoch: int = 0, check_finite: bool = True) -> None:
@@ -109,6 +113,8 @@ class ClassifierEngine:
         B = queries.shape[0]
         q_all = self.comm.all_gather(queries)
         ip_all, pid_all = gather_csr(self.comm, pos_indptr, pos_ids)
+        if self.comm.world > 1 and mode == "bf16_rerank" and self.global_rerank_threshold and self.snap_bf16 is not None:
+            return self._refresh_sharded_rerank(q_all, ip_all, pid_all, k)
         extra = {"labels_e4m3": self.snap_f8} if getattr(self, "snap_f8", None) is not None else {}
         keys, ids, scores = self.ops.refresh_topk(
             q_all, ip_all, pid_all, k, mode, labels_f32=self.snap_f32, labels_bf16=self.snap_bf16, label_offset=self.lo,
@@ -118,6 +124,30 @@ class ClassifierEngine:
         # rows [r*B, (r+1)*B) of every shard's partial list go to their owner r
         mine = self.comm.all_to_all(keys)  # [world, B, k]: shard i's keys for this rank's rows
         _, ids, scores = self.ops.topk_merge(mine, k)
+        return ids, scores
+
+    def _refresh_sharded_rerank(self, q_all, ip_all, pid_all, k):
+        """BF16_RERANK over label shards with a global candidate threshold.
+        Each shard's bf16 top-k' (k' = rerank_candidates_count(k)) goes to the
+        rows' owners, which merge the world lists and return the global k'-th
+        bf16 key tau per row; each shard then re-ranks in fp32 only its
+        candidates with key >= tau (~k'/world per row instead of k'), and the
+        fp32 partial top-k lists are merged as before. The re-ranked set is the
+        global bf16 top-k' — the single-GPU candidate set — so the result is
+        the single-GPU BF16_RERANK result, with the fp32 re-rank work no longer
+        growing with the world size."""
+        kc = self.ops.rerank_candidates_count(k)
+        ckeys, _, _ = self.ops.refresh_topk(q_all, ip_all, pid_all, kc, "bf16", labels_f32=self.snap_f32,
+                                            labels_bf16=self.snap_bf16, label_offset=self.lo)
+        merged, _, _ = self.ops.topk_merge(self.comm.all_to_all(ckeys), kc)  # [B, kc]: this rank's rows
+        tau_all = self.comm.all_gather(merged[:, kc - 1].contiguous())     # [world*B]; 0: fewer than k' exist
+        flip = torch.tensor(-(2 ** 63), dtype=torch.int64, device=ckeys.device)  # unsigned order of the keys
+        keep = (ckeys ^ flip) >= (tau_all[:, None] ^ flip)
+        cand = torch.where(keep, ckeys, torch.zeros_like(ckeys))
+        fkeys, _, _ = self.ops.rerank_candidates(q_all, cand, k, labels_f32=self.snap_f32,
+                                                 labels_bf16=self.snap_bf16 if self.snap_f32 is None else None,
+                                                 label_offset=self.lo)
+        _, ids, scores = self.ops.topk_merge(self.comm.all_to_all(fkeys), k)
         return ids, scores
 
     def refresh_cache(self, queries: torch.Tensor, pos_indptr: torch.Tensor, pos_ids: torch.Tensor,

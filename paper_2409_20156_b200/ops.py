@@ -116,6 +116,36 @@ def refresh_topk(queries, pos_indptr, pos_ids, k, mode="bf16_rerank", labels_f32
     return keys, ids, scores
 
 
+def rerank_candidates_count(k: int) -> int:
+    """k' of the BF16_RERANK candidate pass for a final top-k: max(1.5k, k+16)
+    rounded up to 8, <= 2048 (refresh.cu rerank_candidates)."""
+    kc = max((3 * k + 1) // 2, k + 16)
+    return min((kc + 7) // 8 * 8, 2048)
+
+
+def rerank_candidates(queries, cand_keys, k, labels_f32=None, labels_bf16=None, label_offset=0):
+    """fp32 re-rank of given candidate keys (int64 views; 0 = none) against the
+    fp32 (else bf16) label rows: (keys, ids, scores) of the best k per query
+    (astra_rerank_candidates)."""
+    _cuda(queries, torch.float32, "queries")
+    _cuda(cand_keys, torch.int64, "cand_keys")
+    _cuda(labels_f32, torch.float32, "labels_f32")
+    _cuda(labels_bf16, torch.bfloat16, "labels_bf16")
+    labels = labels_f32 if labels_f32 is not None else labels_bf16
+    if labels is None:
+        raise ConfigError("rerank_candidates: labels_f32 or labels_bf16 required")
+    nq, d = queries.shape
+    kc = cand_keys.shape[1]
+    dev = queries.device
+    keys = torch.empty((nq, k), dtype=torch.int64, device=dev)
+    ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    scores = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    _lib.check(_lib.load().astra_rerank_candidates(
+        _p(queries), nq, d, _p(cand_keys.contiguous()), kc, _p(labels), 0 if labels_f32 is not None else 1,
+        label_offset, k, _p(keys), _p(ids), _p(scores), _stream()))
+    return keys, ids, scores
+
+
 def refresh_flagged(nq, n_labels, d, k, mode, device=None) -> int:
     """Queries of the last refresh_topk call of this shape (on this device)
     that the two-pass plan sent to the exact verify pass; -1 when the shape

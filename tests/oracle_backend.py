@@ -34,10 +34,57 @@ def quantize_e4m3(x):
     return (x.float() * (448.0 / max(float(x.abs().max()), 1e-30))).to(torch.float8_e4m3fn).view(torch.uint8)
 
 
+def _bf16_f32(x):
+    return torch.as_tensor(x).to(torch.bfloat16).float().numpy()
+
+
+def rerank_candidates_count(k):
+    kc = max((3 * k + 1) // 2, k + 16)
+    return min((kc + 7) // 8 * 8, 2048)
+
+
+def _exact_keys(Q, W, label_offset):
+    """fp32 FP32_EXACT keys of every (query, label): [nq, L] uint64."""
+    nq, L = Q.shape[0], W.shape[0]
+    no_pos = np.zeros(nq + 1, np.int64)
+    keys, _, _ = co.refresh_fp32(Q, W, no_pos, np.zeros(0, np.int32), L, label_offset)
+    ids = co.key_to_id(keys)
+    out = np.zeros((nq, L), np.uint64)
+    np.put_along_axis(out, (ids - label_offset).astype(np.int64), keys, axis=1)
+    return out
+
+
+def rerank_candidates(queries, cand_keys, k, labels_f32=None, labels_bf16=None, label_offset=0):
+    W = _np(labels_f32) if labels_f32 is not None else _np(labels_bf16.float())
+    Q = _np(queries)
+    ck = _np(cand_keys).view(np.uint64)
+    ex = _exact_keys(Q, W, label_offset)
+    out = np.zeros((Q.shape[0], k), np.uint64)
+    for q in range(Q.shape[0]):
+        c = ck[q][ck[q] > 0]
+        kk = np.sort(ex[q][(co.key_to_id(c) - label_offset).astype(np.int64)])[::-1][:k]
+        out[q, : len(kk)] = kk
+    ids = np.where(out > 0, co.key_to_id(out), -1).astype(np.int32)
+    scores = np.where(out > 0, co.key_to_score(out), -np.inf).astype(np.float32)
+    return torch.from_numpy(out.view(np.int64)), torch.from_numpy(ids), torch.from_numpy(scores)
+
+
 def refresh_topk(queries, pos_indptr, pos_ids, k, mode="fp32", labels_f32=None, labels_bf16=None, label_offset=0,
                  queries_bf16=None, n_labels=None, labels_e4m3=None):
+    """fp32: the C oracle. bf16 / bf16_rerank (stand-ins with the GPU modes'
+    structure, for the multi-process protocol tests): the candidate pass ranks
+    by the fixed-order fp32 score of bf16-rounded operands; bf16_rerank
+    re-scores its top-k' in fp32."""
     if k < 1:
         raise ConfigError("refresh: k must be >= 1")
+    if mode in ("bf16", "bf16_rerank"):
+        W = _np(labels_bf16.float()) if labels_bf16 is not None else _bf16_f32(labels_f32)
+        kc = k if mode == "bf16" else rerank_candidates_count(k)
+        keys, ids, scores = co.refresh_fp32(_bf16_f32(queries), W, _np(pos_indptr), _np(pos_ids), kc, label_offset)
+        if mode == "bf16":
+            return (torch.from_numpy(keys.view(np.int64)), torch.from_numpy(ids), torch.from_numpy(scores))
+        return rerank_candidates(queries, torch.from_numpy(keys.view(np.int64)), k, labels_f32=labels_f32,
+                                 labels_bf16=labels_bf16, label_offset=label_offset)
     keys, ids, scores = co.refresh_fp32(_np(queries), _np(labels_f32), _np(pos_indptr), _np(pos_ids), k, label_offset)
     return (torch.from_numpy(keys.view(np.int64)), torch.from_numpy(ids), torch.from_numpy(scores))
 

@@ -149,3 +149,48 @@ def test_comm_collective_semantics():
         counts = sum(([1 + q, 2] for q in range(world)), [])
         np.testing.assert_array_equal(res[r]["gip"], np.concatenate([[0], np.cumsum(counts)]))
         np.testing.assert_array_equal(res[r]["gids"], np.concatenate([np.arange(q + 3) + 100 * q for q in range(world)]))
+
+
+def _rerank_worker(rank, world, port, out_dir, global_threshold):
+    sys.path[:0] = [ROOT, HERE]
+    import oracle_backend
+    from paper_2409_20156_b200.engine import ClassifierEngine
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    W, data = _data(seed=4, world=world)
+    eng = ClassifierEngine(L, D, k_p=K_P, k_h=K_H, k_r=K_R, weights=W, refresh_mode="bf16_rerank", seed=5,
+                           device="cpu", backend=oracle_backend)
+    eng.global_rerank_threshold = global_threshold
+    eng.snapshot(0)
+    emb, pos, _ = data[rank]
+    ip, pid = _csr(pos)
+    ids, scores = eng.refresh(torch.from_numpy(emb), torch.from_numpy(ip), torch.from_numpy(pid), K_H)
+    np.savez(os.path.join(out_dir, f"rr{rank}.npz"), ids=ids.numpy(), scores=scores.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,global_threshold", [(2, True), (3, True), (2, False)])
+def test_sharded_bf16_rerank_matches_single_process(world, global_threshold):
+    """BF16_RERANK over label shards (engine._refresh_sharded_rerank: shard
+    bf16 top-k' -> owners merge -> global k'-th key tau -> each shard re-ranks
+    only its candidates >= tau -> fp32 lists merged) returns the single-process
+    BF16_RERANK result, ids and scores; so does the full per-shard re-rank."""
+    sys.path[:0] = [HERE]
+    import oracle_backend
+    from paper_2409_20156_b200.engine import ClassifierEngine
+
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.start_processes(_rerank_worker, args=(world, _free_port(), tmp, global_threshold), nprocs=world, join=True,
+                           start_method="spawn")
+        res = [dict(np.load(os.path.join(tmp, f"rr{r}.npz"))) for r in range(world)]
+    W, data = _data(seed=4, world=world)
+    one = ClassifierEngine(L, D, k_p=K_P, k_h=K_H, k_r=K_R, weights=W, refresh_mode="bf16_rerank", seed=5,
+                           device="cpu", backend=oracle_backend)
+    one.snapshot(0)
+    for r in range(world):
+        emb, pos, _ = data[r]
+        ip, pid = _csr(pos)
+        ids, scores = one.refresh(torch.from_numpy(emb), torch.from_numpy(ip), torch.from_numpy(pid), K_H)
+        np.testing.assert_array_equal(res[r]["ids"], ids.numpy())
+        np.testing.assert_array_equal(res[r]["scores"], scores.numpy())

@@ -4,6 +4,7 @@ FP32_EXACT ids/keys must equal the C oracle bit-for-bit; BF16_RERANK must
 equal FP32_EXACT; plain BF16 must reach the recall bar against fp32.
 """
 
+import os
 import numpy as np
 import pytest
 import torch
@@ -287,3 +288,41 @@ def test_quantize_e4m3_matches_torch(cuda_lib):
     qb = ops.quantize_e4m3(xb)
     refb = (xb.float() * (448.0 / xb.float().abs().max())).to(torch.float8_e4m3fn).view(torch.uint8)
     assert torch.equal(qb, refb)
+
+
+def test_rerank_candidates_matches_oracle(cuda_lib):
+    """astra_rerank_candidates (the sharded refresh's fp32 re-rank): all of the
+    bf16 top-k' kept -> the BF16_RERANK result; a filtered candidate set (keys
+    below a per-row threshold zeroed, as engine._refresh_sharded_rerank does)
+    -> the fp32-exact top-k of that subset, key for key vs the C oracle."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import oracle_backend
+    from paper_2409_20156_b200 import ops
+
+    rng = np.random.default_rng(11)
+    L, d, nq, k, off = 30_000, 256, 96, 24, 5000
+    W = rng.uniform(-0.1, 0.1, size=(L, d)).astype(np.float32)
+    E = rng.standard_normal((nq, d)).astype(np.float32)
+    pos = [np.sort(rng.choice(L, size=3, replace=False)) + off for _ in range(nq)]
+    ip = np.zeros(nq + 1, np.int64)
+    ip[1:] = np.cumsum([len(p) for p in pos])
+    pid = np.concatenate(pos).astype(np.int32)
+    Wd, Ed = torch.from_numpy(W).cuda(), torch.from_numpy(E).cuda()
+    ipd, pidd = torch.from_numpy(ip).cuda(), torch.from_numpy(pid).cuda()
+    kc = ops.rerank_candidates_count(k)
+    ck, _, _ = ops.refresh_topk(Ed, ipd, pidd, kc, "bf16", labels_f32=Wd, labels_bf16=ops.f32_to_bf16(Wd),
+                                label_offset=off)
+    full, _, _ = ops.rerank_candidates(Ed, ck, k, labels_f32=Wd, label_offset=off)
+    ref, _, _ = ops.refresh_topk(Ed, ipd, pidd, k, "bf16_rerank", labels_f32=Wd, labels_bf16=ops.f32_to_bf16(Wd),
+                                 label_offset=off)
+    np.testing.assert_array_equal(full.cpu().numpy(), ref.cpu().numpy())
+    cut = rng.integers(1, kc, size=nq)  # keep a prefix of random length per row
+    mask = torch.arange(kc, device="cuda")[None, :] < torch.from_numpy(cut).cuda()[:, None]
+    sub = torch.where(mask, ck, torch.zeros_like(ck))
+    got, ids, _ = ops.rerank_candidates(Ed, sub, k, labels_f32=Wd, label_offset=off)
+    want, want_ids, _ = oracle_backend.rerank_candidates(torch.from_numpy(E), sub.cpu(), k,
+                                                         labels_f32=torch.from_numpy(W), label_offset=off)
+    np.testing.assert_array_equal(got.cpu().numpy(), want.numpy())
+    np.testing.assert_array_equal(ids.cpu().numpy(), want_ids.numpy())

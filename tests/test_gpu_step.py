@@ -248,7 +248,7 @@ def test_adam_matches_torch_sparse_adam(cuda_lib):
 
 @pytest.mark.parametrize("wdtype", ["fp32", "bf16"])
 def test_single_pass_adam_equals_two_kernel(cuda_lib, wdtype):
-    """Adam (+ bf16 W): the single pass (opt-in for Adam: ASTRA_STEP_SINGLE_ADAM)
+    """Adam (+ bf16 W): the single pass (the Adam default; ASTRA_STEP_SINGLE_ADAM)
     and the two-kernel schedule produce the same W', m and v bits over several
     steps (same per-label summation order, same SparseAdam op order)."""
     import subprocess
