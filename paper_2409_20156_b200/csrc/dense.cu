@@ -1,8 +1,8 @@
 // dense.cu — the elementwise half of the all-negatives (full-loss) arm,
 // train_full_loss_baseline (trainer.py:563-616), and of the dense probe loss
 // _probe_full_loss (trainer.py:398-403). The three GEMMs of the arm
-// (E W^T, G W, G^T E) are plain fp32 library GEMMs (cuBLAS via the host);
-// what is specific to the arm runs here:
+// (E W^T, G W, G^T E) are astra_gemm_f32 (dense_tc.cu, 3xTF32 tensor cores);
+// the elementwise parts run here:
 //   * dense_bce: over the B x L scores, G = f32(sigmoid(s)) - y with the
 //     reference's float64 sigmoid 0.5 (1 + tanh(s / 2)) (loss.py:45-47) cast
 //     to fp32 as trainer.py:597 does, and the float64 loss
@@ -69,13 +69,22 @@ __global__ void __launch_bounds__(kDenseThreads) dense_pos_kernel(const T* S, in
   if (threadIdx.x == 0) part[b] = t;
 }
 
-__global__ void __launch_bounds__(32) dense_loss_finalize(const double* part, int n1, const double* part2, int n2,
-                                                          double* out) {
-  if (threadIdx.x != 0) return;
+// One CTA: thread t sums parts t, t + 1024, ... of each list, then a fixed
+// tree over the threads (deterministic; the single-thread loop over ~5K
+// partials took 0.1 ms).
+__global__ void __launch_bounds__(1024) dense_loss_finalize(const double* part, int n1, const double* part2, int n2,
+                                                            double* out) {
+  __shared__ double sh[1024];
   double t = 0.0, u = 0.0;
-  for (int i = 0; i < n1; ++i) t += part[i];
-  for (int i = 0; i < n2; ++i) u += part2[i];
-  *out = t + u;
+  for (int i = threadIdx.x; i < n1; i += 1024) t += part[i];
+  for (int i = threadIdx.x; i < n2; i += 1024) u += part2[i];
+  sh[threadIdx.x] = t + u;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (static_cast<int>(threadIdx.x) < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
 }
 
 __global__ void __launch_bounds__(kDenseThreads) dense_sgd_kernel(float* W, const float* g, int64_t n, float lr,
@@ -118,7 +127,7 @@ int dense_bce(const void* S, int s_f64, int B, int64_t L, const int64_t* pos_ind
     if (B) dense_pos_kernel<float><<<B, kDenseThreads, 0, st>>>(static_cast<const float*>(S), L, pos_indptr, pos_ids, G, part2);
   }
   ASTRA_LAUNCHED("dense_pos");
-  dense_loss_finalize<<<1, 32, 0, st>>>(part, grid, part2, B, loss_out);
+  dense_loss_finalize<<<1, 1024, 0, st>>>(part, grid, part2, B, loss_out);
   ASTRA_LAUNCHED("dense_loss_finalize");
   return ASTRA_OK;
 }
