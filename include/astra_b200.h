@@ -79,7 +79,8 @@ uint64_t astra_launch_count(void);
  * every label: the threshold pass, or the single running-top-k pass),
  * "refresh_verify" (the two-pass plan's exact fallback pass), "step_single"
  * (the single label-major step pass), "slot_forward" and "label_update" (the
- * two-kernel step schedule). astra_kernel_timing syncs the
+ * two-kernel step schedule), "gemm_f32" (astra_gemm_f32's tensor-core GEMM
+ * kernel). astra_kernel_timing syncs the
  * pairs recorded under `name`, returns their summed milliseconds and count,
  * and clears them. Not a reference interface (measurement only). */
 void astra_kernel_timing_enable(int on);

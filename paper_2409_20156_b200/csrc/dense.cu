@@ -26,7 +26,6 @@ namespace {
 constexpr int kDenseThreads = 256;
 constexpr int kDenseBlocksMax = 4096;
 
-__device__ __forceinline__ double softplus_f64(double x) { return fmax(x, 0.0) + log1p(exp(-fabs(x))); }
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
   v = warp_sum(v);
@@ -46,8 +45,21 @@ __global__ void __launch_bounds__(kDenseThreads) dense_bce_kernel(const T* S, in
   for (int64_t i = blockIdx.x * static_cast<int64_t>(kDenseThreads) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * kDenseThreads) {
     const double s = static_cast<double>(S[i]);
-    if (G) G[i] = static_cast<float>(0.5 * (1.0 + tanh(0.5 * s)));
-    acc += softplus_f64(s);
+    // one exp serves both: sp(s) = max(s, 0) + log1p(e) and, for s >= -15,
+    // sigmoid = 1 / (1 + e) or e / (1 + e) with e = exp(-|s|) — the same value
+    // to fp64 accuracy as the reference's 0.5 (1 + tanh(s / 2)), hence the
+    // same fp32 after the cast; below -15 the reference's formula loses digits
+    // to cancellation (1 + tanh ~ 2e), so that rare branch evaluates it as is
+    const double e = exp(-fabs(s));
+    if (G) {
+      double sg;
+      if (s >= -15.0)
+        sg = s >= 0.0 ? 1.0 / (1.0 + e) : e / (1.0 + e);
+      else
+        sg = 0.5 * (1.0 + tanh(0.5 * s));
+      G[i] = static_cast<float>(sg);
+    }
+    acc += fmax(s, 0.0) + log1p(e);
   }
   const double t = block_sum(acc, sh);
   if (threadIdx.x == 0) part[blockIdx.x] = t;

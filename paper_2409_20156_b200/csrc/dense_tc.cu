@@ -287,6 +287,27 @@ __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ sr
   }
 }
 
+// The K-major case with K % 4 == 0: a straight vectorised map (16-byte loads
+// and stores, no shared-memory tile), zero padding past K.
+__global__ void __launch_bounds__(256) split_kmajor_v4_kernel(const float4* __restrict__ src, int64_t R, int64_t K4,
+                                                              int64_t Kp4, float4* __restrict__ hi,
+                                                              float4* __restrict__ lo) {
+  const int64_t n = R * Kp4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / Kp4, k4 = i - r * Kp4;
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k4 < K4) x = src[r * K4 + k4];
+    float4 h;
+    h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+    h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+    h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+    h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+    hi[i] = h;
+    lo[i] = make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y), __fsub_rn(x.z, h.z), __fsub_rn(x.w, h.w));
+  }
+}
+
 // D[i] = sum over parts p of part[p][i], in part order.
 __global__ void __launch_bounds__(256) reduce_kernel(const float* __restrict__ part, int kparts, int64_t n,
                                                      float* __restrict__ D) {
@@ -393,11 +414,20 @@ int gemm_f32(const float* A, int a_kmajor, const float* B, int b_kmajor, int64_t
   float* Bl = c.take<float>(static_cast<size_t>(N) * p.Kp);
   float* part = p.kparts > 1 ? c.take<float>(static_cast<size_t>(p.kparts) * M * N) : D;
   if (p.Kp / 32 > 65535) return set_error(ASTRA_ERR_CONFIG, "gemm_f32: K too large (%lld)", static_cast<long long>(K));
-  split_kernel<<<dim3(static_cast<unsigned>((M + 31) / 32), static_cast<unsigned>(p.Kp / 32)), 256, 0, st>>>(
-      A, a_kmajor, M, K, p.Kp, Ah, Al);
+  auto split = [&](const float* X, int kmajor, int64_t R, float* hi, float* lo) {
+    if (kmajor && K % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
+      const int64_t n = R * (p.Kp / 4);
+      split_kmajor_v4_kernel<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 16LL * num_sms())), 256, 0,
+                               st>>>(reinterpret_cast<const float4*>(X), R, K / 4, p.Kp / 4,
+                                     reinterpret_cast<float4*>(hi), reinterpret_cast<float4*>(lo));
+    } else {
+      split_kernel<<<dim3(static_cast<unsigned>((R + 31) / 32), static_cast<unsigned>(p.Kp / 32)), 256, 0, st>>>(
+          X, kmajor, R, K, p.Kp, hi, lo);
+    }
+  };
+  split(A, a_kmajor, M, Ah, Al);
   ASTRA_LAUNCHED("gemm_split");
-  split_kernel<<<dim3(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>(p.Kp / 32)), 256, 0, st>>>(
-      B, b_kmajor, N, K, p.Kp, Bh, Bl);
+  split(B, b_kmajor, N, Bh, Bl);
   ASTRA_LAUNCHED("gemm_split");
   CUtensorMap tAh, tAl, tBh, tBl;
   ASTRA_TRY(make_map_f32(&tAh, Ah, M, p.Kp, BM));
