@@ -157,9 +157,45 @@ def _ncu_traffic():
 
 
 # ------------------------------------------------------------------ data
-def make_batches(rng, n_batches, B, L, lpp, N, slot, n_slots):
+def clustered_centers(d, n_clusters=2000, seed=5):
+    """Cluster centres of the trained-like W of --w-init clustered (unit-variance
+    coordinates / sqrt(d)) and their Zipf popularity."""
+    rng = np.random.default_rng(seed)
+    centers = (rng.standard_normal((n_clusters, d)) / np.sqrt(d)).astype(np.float32)
+    pop = 1.0 / np.arange(1, n_clusters + 1, dtype=np.float64) ** 1.1
+    return centers, pop / pop.sum()
+
+
+def clustered_w(L, d, centers, pop, seed, dup_frac=0.02):
+    """Trained-like W (the refresh tests' clustered heavy-tailed matrix,
+    tests/test_gpu_refresh_scale.py): rows = a Zipf-popular cluster centre +
+    noise, log-normal row norms, 2% of the rows copies of 16 hub rows (exact
+    score ties across far-apart ids). Breaks the two-pass plan's i.i.d. score
+    assumption: candidate lists overflow and queries take the verify pass."""
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    C = torch.from_numpy(centers).cuda()
+    assign = torch.multinomial(torch.from_numpy(pop).float().cuda(), L, replacement=True, generator=g)
+    W = torch.empty((L, d), device="cuda")
+    for lo in range(0, L, 1 << 18):
+        hi = min(L, lo + (1 << 18))
+        noise = torch.randn((hi - lo, d), device="cuda", generator=g) * (0.35 / d ** 0.5)
+        scale = torch.exp(torch.randn((hi - lo, 1), device="cuda", generator=g) * 0.5)
+        W[lo:hi] = (C[assign[lo:hi]] + noise) * scale
+    n_dup = int(L * dup_frac)
+    hubs = torch.randint(0, L, (16,), device="cuda", generator=g)
+    dst = torch.randint(0, L, (n_dup,), device="cuda", generator=g)
+    W[dst] = W[hubs[torch.randint(0, 16, (n_dup,), device="cuda", generator=g)]]
+    return W
+
+
+def make_batches(rng, n_batches, B, L, lpp, N, slot, n_slots, centers=None):
     """Synthetic minibatches: global row ids, positives (labels_per_point
-    distinct uniform labels per row, sorted), embeddings N(0,1) fp32."""
+    distinct uniform labels per row, sorted), embeddings N(0,1) fp32 (with
+    `centers`: a Zipf-popular cluster centre x sqrt(d) + N(0, 0.25) noise, the
+    queries of the clustered W)."""
     out = []
     for t in range(n_batches):
         rows = ((slot * n_batches + t) * B + np.arange(B, dtype=np.int64)) % N
@@ -172,7 +208,11 @@ def make_batches(rng, n_batches, B, L, lpp, N, slot, n_slots):
             flat.append(u)
             indptr[b + 1] = indptr[b] + len(u)
         ids = np.concatenate(flat).astype(np.int32)
-        emb = rng.standard_normal((B, CFG["d"]), dtype=np.float32)
+        if centers is None:
+            emb = rng.standard_normal((B, CFG["d"]), dtype=np.float32)
+        else:
+            which = rng.zipf(1.3, size=B) % centers.shape[0]
+            emb = (centers[which] * np.sqrt(CFG["d"]) + 0.5 * rng.standard_normal((B, CFG["d"]))).astype(np.float32)
         out.append(dict(rows=rows, indptr=indptr, pos=ids, emb=emb))
     return out
 
@@ -203,12 +243,20 @@ def run_ours(args):
     hbm, tf_burst, tf_sus, peak_kind = peaks()
 
     eng = ClassifierEngine(L, d, k_p=k_p, k_h=k_h, k_r=k_r, seed=0, refresh_mode=args.refresh_mode)
+    centers = None
+    if args.w_init == "clustered":
+        centers, pop = clustered_centers(d)
+        Wc = clustered_w(eng.hi - eng.lo, d, centers, pop, seed=11 + rank)
+        eng.W.copy_(Wc)
+        eng.w_absmax.copy_(Wc.abs().amax().reshape(1))
+        del Wc
     eng.snapshot(epoch=0)
     L_loc = eng.hi - eng.lo
     rng = np.random.default_rng(1000 + rank)
     n_steps = args.warmup + args.steps
     # host data: per step M minibatches (rows, positives CSR, embeddings)
-    host = [make_batches(rng, M, B, L, CFG["labels_per_point"], CFG["N"], rank + t * world, world * n_steps)
+    host = [make_batches(rng, M, B, L, CFG["labels_per_point"], CFG["N"], rank + t * world, world * n_steps,
+                         centers=centers)
             for t in range(n_steps)]
     dev = []
     for mbs in host:
@@ -455,7 +503,9 @@ def run_ours(args):
         "ms_per_step": round(ms_total / K, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": f"fp32 W/step, {args.refresh_mode.split('_')[0]} tensor-core refresh + fp32 re-rank", "data": "synthetic",
         "config": dict(bench_config(world), refresh_overlap=overlap,
-                       refresh_sms=args.refresh_sms if overlap else None),
+                       refresh_sms=args.refresh_sms if overlap else None,
+                       **({"w_init": "clustered heavy-tailed W (2000 Zipf clusters, log-normal norms, 2% duplicated "
+                                     "hub rows), queries near popular clusters"} if args.w_init == "clustered" else {})),
         "phases_ms_per_step": {k: round(v / K, 4) for k, v in ph.items()},
         "refresh_mips_qps": round(q_per_refresh / t_ref, 1),
         # the exact fallback of the two-pass refresh (running top-k for query
@@ -1193,6 +1243,10 @@ def main():
     ap.add_argument("--emulate", type=int, default=0,
                     help="one GPU runs rank 0's share of an N-GPU C4 job (a 1/N label shard, all N ranks' rows); "
                          "collectives are not run, their bytes are reported")
+    ap.add_argument("--w-init", default="uniform", choices=["uniform", "clustered"],
+                    help="C4 line: W uniform-scaled (the reference's init) or trained-like clustered heavy-tailed "
+                         "with duplicated rows and queries near popular clusters (exercises the refresh's "
+                         "overflow -> exact verify path)")
     ap.add_argument("--refresh-mode", default="bf16_rerank", choices=["bf16_rerank", "fp8_rerank"],
                     help="tensor-core candidate pass of the refresh (bf16 = the north star's, or e4m3 at twice the "
                          "tensor rate), then the fp32-exact re-rank")
