@@ -873,12 +873,12 @@ def run_c5shard(args):
         "roofline_step": {"bound": "hbm", "achieved": round(step_bytes / (ph["step"] / 1e3) / 1e9, 1), "peak": hbm,
                           "unit": "GB/s", "frac": round(step_bytes / (ph["step"] / 1e3) / 1e9 / hbm, 4),
                           "algorithmic": f"U*d*(2*2 + 2*8) + 2*B*d*4 + B*S*5 = {step_bytes:.3e} B (U={U})",
-                          "label_update_launch_ms": round(upd_ms / max(upd_n, 1), 4) if upd_n else None,
+                          "label_update_launch_ms": round(upd_ms / max(upd_n, 1), 4) if upd_n and not sgl_n else None,
                           "kernels": {name: {"launch_ms": round(ms_ / n_, 4),
                                              "achieved_gbs": round(upd_bytes / (ms_ / n_ / 1e3) / 1e9, 1),
                                              "algorithmic_bytes": int(upd_bytes)}
-                                      for name, (ms_, n_) in (("step_single", (sgl_ms, sgl_n)),
-                                                              ("label_update", (upd_ms, upd_n))) if n_}},
+                                      for name, (ms_, n_) in ((("step_single", (sgl_ms, sgl_n)),) if sgl_n else
+                                                              (("label_update", (upd_ms, upd_n)),)) if n_}},
         "memory_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
         "clocks": clk,
     }

@@ -825,13 +825,20 @@ void refresh_tc_layout(int64_t nq, int64_t n_tiles, int* n_ctas, int* n_parts) {
     return static_cast<double>(units) / static_cast<double>(rounds * n_cl_max) *
            static_cast<double>(n_tiles) / static_cast<double>(tpp * p);
   };
-  // fewest parts that fill the budget (fewer lists, more L2 reuse of W): a
-  // layout that keeps every cluster busy to within 1% (e.g. 37 parts x 36
-  // query-tile pairs = 18 rounds of 74 pairs on 148 SMs) while parts stay
-  // >= 64 tiles long, else the fewest parts reaching 93%
-  static const bool fill = [] {  // ASTRA_REFRESH_FILL=0: the 93% rule alone (A/B aid)
+  // fewest parts that fill the budget (fewer lists, more L2 reuse of W): the
+  // fewest reaching 93% (C4: 2 parts x 36 query-tile pairs on 144 SMs, W read
+  // from DRAM once); with `fill`, a layout keeping every cluster busy to
+  // within 1% (e.g. 37 parts x 36 pairs = 18 rounds of 74 pairs) while parts
+  // stay >= 64 tiles long
+  // ASTRA_REFRESH_FILL=1: prefer a layout that fills every SM pair to within
+  // 1% (at C4: 37 parts on 148 SMs). Off by default: its units of one part
+  // start in different rounds, so W is read ~1.5x from DRAM instead of once;
+  // same-box A/B (profiles/r02s3/ab_refresh_fill2.txt): threshold pass 1.2%
+  // faster at C4, but 2.6% slower at the C5 shard, whose 72 ms pass runs at
+  // the power cap (the extra DRAM traffic lowers the clock).
+  static const bool fill = [] {
     const char* e = getenv("ASTRA_REFRESH_FILL");
-    return !(e && atoi(e) == 0);
+    return e && atoi(e) == 1;
   }();
   int64_t best_p = 1;
   double best_eff = -1.0;

@@ -1072,6 +1072,9 @@ __device__ __forceinline__ void load_emb_row(const float* emb, int b, int lane, 
 #ifndef ASTRA_SINGLE_CTAS
 #define ASTRA_SINGLE_CTAS 4
 #endif
+#ifndef ASTRA_SINGLE_POLL_NS
+#define ASTRA_SINGLE_POLL_NS 20  // producer's back-off while every ring slot is busy
+#endif
 #ifndef ASTRA_SINGLE_ADAM_EARLY
 #define ASTRA_SINGLE_ADAM_EARLY 1  // Adam: moments into registers with the row, ring entry released at once
 #endif
@@ -1243,7 +1246,7 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
         if (lane == 0) {
           mbar_wait(&qempty[qi], ((i / Q) & 1) ^ 1);
           uint32_t m;  // a free data slot: its previous fill released
-          while ((m = *reinterpret_cast<volatile uint32_t*>(freemask)) == 0u) __nanosleep(20);
+          while ((m = *reinterpret_cast<volatile uint32_t*>(freemask)) == 0u) __nanosleep(ASTRA_SINGLE_POLL_NS);
           sl = __ffs(m) - 1;
           atomicAnd(freemask, ~(1u << sl));
           mbar_wait(&empty[sl], ((use >> sl) & 1) ^ 1);
