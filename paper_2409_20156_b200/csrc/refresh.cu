@@ -190,12 +190,15 @@ __global__ void __launch_bounds__(128) merge_kernel(const uint64_t* part_keys, i
 template <int R>
 __global__ void __launch_bounds__(256) merge_warp_kernel(const uint64_t* part_keys, int64_t nq, int n_parts,
                                                          int k_in, int k_out, uint64_t* out_keys, int32_t* out_ids,
-                                                         float* out_scores, const int32_t* only) {
+                                                         float* out_scores, const int32_t* only,
+                                                         const int32_t* qmap = nullptr,
+                                                         const int32_t* n_active = nullptr) {
   constexpr int P = 32 * R;
   const int lane = threadIdx.x & 31;
   const int64_t q = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (q >= nq) return;  // warp-uniform
   if (only && !only[q]) return;
+  if (n_active && q >= *n_active) return;  // (compact verify: rows past the gathered ones)
   const int kin = k_in < P ? k_in : P;
   uint64_t cur[R];
   {
@@ -246,12 +249,53 @@ __global__ void __launch_bounds__(256) merge_warp_kernel(const uint64_t* part_ke
     const int e = r * 32 + lane;
     if (e < k_out) {
       const uint64_t key = cur[r];
-      const size_t o = static_cast<size_t>(q) * k_out + e;
+      const size_t o = static_cast<size_t>(qmap ? qmap[q] : q) * k_out + e;
       if (out_keys) out_keys[o] = key;
       if (out_ids) out_ids[o] = key ? key_id(key) : -1;
       if (out_scores) out_scores[o] = key ? key_score(key) : -INFINITY;
     }
   }
+}
+
+// Compact verify: qmap[0..n) = the flagged queries in ascending order, *n_out =
+// n (one CTA: a block-wide scan of the flags, 1024 at a time).
+__global__ void __launch_bounds__(1024) compact_flagged_kernel(const int32_t* flags, int64_t nq, int32_t* qmap,
+                                                               int32_t* n_out) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int64_t i0 = 0; i0 < nq; i0 += 1024) {
+    const int64_t i = i0 + threadIdx.x;
+    const int f = i < nq && flags[i] ? 1 : 0;
+    const unsigned b = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wsum[warp] = __popc(b);
+    __syncthreads();
+    int before = base;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    if (f) qmap[before + __popc(b & ((1u << lane) - 1u))] = static_cast<int32_t>(i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < 32; ++w) t += wsum[w];
+      base += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_out = base;
+}
+
+// Gather the flagged queries' tensor-core rows (row_bytes each, 16 B aligned)
+// to the front of dst: block per row slot.
+__global__ void __launch_bounds__(128) gather_rows_kernel(const unsigned char* src, int64_t row_bytes,
+                                                          const int32_t* qmap, const int32_t* n_active,
+                                                          unsigned char* dst) {
+  const int64_t r = blockIdx.x;
+  if (r >= *n_active) return;
+  const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<int64_t>(qmap[r]) * row_bytes);
+  uint4* t = reinterpret_cast<uint4*>(dst + r * row_bytes);
+  for (int64_t i = threadIdx.x; i < row_bytes / 16; i += blockDim.x) t[i] = s[i];
 }
 
 // ------------------------------------------------------------- fp32 re-rank
@@ -853,7 +897,16 @@ struct RefreshWs {
   uint64_t* cand;       // [n_parts][nq][cand_cap]
   int32_t* cand_cnt;    // [n_parts][nq]
   int32_t* flags;       // [nq] 1 = select could not prove exactness -> fallback
+  // compact verify
+  void* qc;             // [nq] tensor-core query rows, the flagged ones gathered in front
+  int32_t* qmap;        // [nq] compact row -> query
+  int32_t* n_flagged;   // [1]
+  uint64_t* vpart_keys; // [kVerifyParts][nq][kk]
 };
+
+// Label parts of the compact verify pass (its query rows are few: the parts
+// spread them over the SM pairs).
+constexpr int kVerifyParts = 32;
 
 // bf16 candidates kept per query before the fp32 re-rank: k' = max(1.5k, k+16),
 // a multiple of 8 (bf16 top-k' contains the fp32 top-k; see tests + DESIGN.md).
@@ -977,7 +1030,8 @@ size_t carve_refresh(void* base, size_t cap_bytes, int64_t nq, int64_t L, int d,
   } else {
     int n_ctas;
     refresh_tc_layout(nq, (L + kTcTileLabels - 1) / kTcTileLabels, &n_ctas, &n_parts);
-    buf_words = static_cast<size_t>(n_ctas) * 128 * (cap + kTopkSlack);
+    // (per-lane running-top-k buffers for every CTA: the compact verify runs on all SMs)
+    buf_words = static_cast<size_t>(std::max(n_ctas, num_sms())) * 128 * (cap + kTopkSlack);
     pk_words = static_cast<size_t>(n_parts) * nq * kk;
     *tp = plan_two_pass(nq, L, kk, n_parts);
   }
@@ -993,16 +1047,44 @@ size_t carve_refresh(void* base, size_t cap_bytes, int64_t nq, int64_t L, int d,
   w->gmax = nullptr;
   w->tau_keys = w->cand = nullptr;
   w->cand_cnt = w->flags = nullptr;
+  w->qc = nullptr;
+  w->qmap = w->n_flagged = nullptr;
+  w->vpart_keys = nullptr;
   if (tp->on) {
     w->gmax = c.take<uint32_t>(static_cast<size_t>(nq) * tp->n_groups);
     w->tau_keys = c.take<uint64_t>(static_cast<size_t>(nq));
     w->cand = c.take<uint64_t>(static_cast<size_t>(n_parts) * nq * tp->cand_cap);
     w->cand_cnt = c.take<int32_t>(static_cast<size_t>(n_parts) * nq);
     w->flags = c.take<int32_t>(static_cast<size_t>(nq));
+    w->qc = c.take<uint16_t>(static_cast<size_t>(nq) * d);
+    w->qmap = c.take<int32_t>(static_cast<size_t>(nq));
+    w->n_flagged = c.take<int32_t>(4);
+    w->vpart_keys = c.take<uint64_t>(static_cast<size_t>(kVerifyParts) * nq * kk);
   }
   *n_parts_out = n_parts;
   *kk_out = kk;
   return c.off;
+}
+
+// Merge of the compact verify's part lists (rows < *n_active, k <= 512) into
+// the original queries' outputs (qmap).
+int topk_merge_compact(const uint64_t* part_keys, int64_t nq, int n_parts, int k, uint64_t* out_keys, int32_t* out_ids,
+                       float* out_scores, const int32_t* qmap, const int32_t* n_active, cudaStream_t st) {
+  if (nq <= 0) return ASTRA_OK;
+  if (k > 512) return set_error(ASTRA_ERR_CONFIG, "compact verify merge: k > 512");
+  const unsigned grid = static_cast<unsigned>((nq + 7) / 8);
+  auto go = [&](auto r_tag) {
+    constexpr int R = decltype(r_tag)::value;
+    merge_warp_kernel<R><<<grid, 256, 0, st>>>(part_keys, nq, n_parts, k, k, out_keys, out_ids, out_scores, nullptr,
+                                               qmap, n_active);
+  };
+  if (k <= 32) go(std::integral_constant<int, 1>());
+  else if (k <= 64) go(std::integral_constant<int, 2>());
+  else if (k <= 128) go(std::integral_constant<int, 4>());
+  else if (k <= 256) go(std::integral_constant<int, 8>());
+  else go(std::integral_constant<int, 16>());
+  ASTRA_LAUNCHED("merge_compact");
+  return ASTRA_OK;
 }
 
 int topk_merge_only(const uint64_t* part_keys, int64_t nq, int n_parts, int k_in, int k_out, uint64_t* out_keys,
@@ -1231,18 +1313,34 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
           w.cand, w.cand_cnt, n_parts, tp.cand_cap, nq, pos_indptr, pos_ids, kk, tp.sel_max, rcap, o_keys, o_ids,
           o_scores, w.flags);
       ASTRA_LAUNCHED("select");
-      // 4. verify: exact running top-k for the flagged query tiles only
-      TcLaunch v = p;
-      v.k = kk;
-      v.cap = cap;
-      v.only_flagged = w.flags;
+      // 4. verify: the exact running top-k for the flagged queries only,
+      //    gathered to the front of a compact query buffer (their number stays
+      //    on the device): a handful of flagged queries costs one query-tile
+      //    pair's sweep spread over kVerifyParts label parts, not the full
+      //    tiles they sit in
       prof.mark("select");
       {
         // (near zero unless a query was flagged: bench.py reports it per refresh)
         KernelTimer kt("refresh_verify", st);
+        compact_flagged_kernel<<<1, 1024, 0, st>>>(w.flags, nq, w.qmap, w.n_flagged);
+        ASTRA_LAUNCHED("compact_flagged");
+        const int64_t row_bytes = f8 ? d : static_cast<int64_t>(d) * 2;
+        gather_rows_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char*>(qb), row_bytes,
+                                                                      w.qmap, w.n_flagged,
+                                                                      static_cast<unsigned char*>(w.qc));
+        ASTRA_LAUNCHED("gather_rows");
+        TcLaunch v = p;
+        v.qb = w.qc;
+        v.k = kk;
+        v.cap = cap;
+        v.part_keys = w.vpart_keys;
+        v.qmap = w.qmap;
+        v.n_active = w.n_flagged;
+        v.n_parts_fixed = kVerifyParts;
         ASTRA_TRY(launch_refresh_tc(v, st));
+        const int vparts = static_cast<int>(std::min<int64_t>(kVerifyParts, (L + kTcTileLabels - 1) / kTcTileLabels));
+        ASTRA_TRY(topk_merge_compact(w.vpart_keys, nq, vparts, kk, o_keys, o_ids, o_scores, w.qmap, w.n_flagged, st));
       }
-      ASTRA_TRY(topk_merge_only(w.part_keys, nq, n_parts, kk, kk, o_keys, o_ids, o_scores, w.merge_bufs, w.flags, st));
       prof.mark("verify");
     } else {
       p.k = kk;

@@ -249,6 +249,10 @@ struct TcArgs {
   int cand_cap;
   uint32_t* gmax;          // GMAX: [nq][n_lt * 4] orderable bits of the 64-label group maxima
   const int32_t* only_flagged;
+  // compact verify (running mode): rows are the flagged queries gathered in
+  // front (*n_active of them); qmap[row] = the original query (positives)
+  const int32_t* qmap;
+  const int32_t* n_active;
   int debug_no_topk;  // ASTRA_TC_DEBUG_NO_TOPK=1: skip selection (pipeline-rate measurement only)
   // ASTRA_TC_DEBUG_COUNTERS=1: [slow steps, -, compactions, steps, then clock64 cycle sums:
   // 4 epi tfull wait, 5 epi fast path, 6 epi slow path, 7 epi settle, 8 epi total,
@@ -377,10 +381,10 @@ struct Unit {
 };
 
 template <int CL>
-__device__ __forceinline__ Unit unit_of(const TcArgs& a, int64_t uc, uint32_t crank) {
+__device__ __forceinline__ Unit unit_of(const TcArgs& a, int64_t n_qt_cl, int64_t uc, uint32_t crank) {
   Unit u;
-  const int64_t qc = uc % a.n_qt_cl;
-  u.part = static_cast<int>(uc / a.n_qt_cl);
+  const int64_t qc = uc % n_qt_cl;
+  u.part = static_cast<int>(uc / n_qt_cl);
   u.qt = qc * CL + crank;
   u.t0 = std::min<int64_t>(a.n_lt, static_cast<int64_t>(u.part) * a.tiles_per_part);
   u.t1 = std::min<int64_t>(a.n_lt, u.t0 + a.tiles_per_part);
@@ -427,7 +431,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint16_t pair_mask = static_cast<uint16_t>(3u << prank);
   constexpr int KB = kb_elems<F8>();  // K elements per stage
   const int nkb = a.d / KB;
-  const int64_t n_units = a.n_qt_cl * a.n_parts;
+  // query rows in play: all nq, or (compact verify) the *n_active gathered ones
+  const int64_t nq_eff = a.n_active ? static_cast<int64_t>(*a.n_active) : a.nq;
+  const int64_t n_qt_cl = a.n_active ? (nq_eff + CL * BM - 1) / (CL * BM) : a.n_qt_cl;
+  const int64_t n_units = n_qt_cl * a.n_parts;
 
   const uint32_t* qbits = nullptr;
   if (a.only_flagged) {
@@ -481,8 +488,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t uc = cluster; uc < n_units; uc += n_clusters) {
-        if (!unit_active(qbits, a.n_qt_cl, uc)) continue;
-        const Unit un = unit_of<CL>(a, uc, crank);
+        if (!unit_active(qbits, n_qt_cl, uc)) continue;
+        const Unit un = unit_of<CL>(a, n_qt_cl, uc, crank);
         const int q0 = static_cast<int>(un.qt * BM);
         for (int64_t t = un.t0; t < un.t1; ++t) {
           const int n0 = static_cast<int>(t * a.tile_stride * BN);
@@ -529,8 +536,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     long long p_te = 0, p_full = 0;
     const long long p_t0 = a.dbg ? clock64() : 0;
     for (int64_t uc = cluster; uc < n_units; uc += n_clusters) {
-      if (!unit_active(qbits, a.n_qt_cl, uc)) continue;
-      const Unit un = unit_of<CL>(a, uc, crank);
+      if (!unit_active(qbits, n_qt_cl, uc)) continue;
+      const Unit un = unit_of<CL>(a, n_qt_cl, uc, crank);
       for (int64_t t = un.t0; t < un.t1; ++t) {
         long long w0 = a.dbg ? clock64() : 0;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -603,10 +610,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     long long p_wait = 0;
     const long long p_t0 = a.dbg ? clock64() : 0;
     for (int64_t uc = cluster; uc < n_units; uc += n_clusters) {
-      if (!unit_active(qbits, a.n_qt_cl, uc)) continue;
-      const Unit un = unit_of<CL>(a, uc, crank);
+      if (!unit_active(qbits, n_qt_cl, uc)) continue;
+      const Unit un = unit_of<CL>(a, n_qt_cl, uc, crank);
       const int64_t q = un.qt * BM + row;
-      const bool active = q < a.nq;
+      const bool active = q < nq_eff;
       const int list = un.part;
       LaneTopK tk;
       if constexpr (MODE == kGmax) {
@@ -616,7 +623,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tk.tau = active ? a.tau_in[static_cast<size_t>(q) * a.tau_stride] : ~0ull;
         tk.tau_s = tk.tau ? key_score(tk.tau) : -INFINITY;
       } else {
-        const int64_t p0 = active ? a.pos_indptr[q] : 0, p1 = active ? a.pos_indptr[q + 1] : 0;
+        const int64_t qo = active && a.qmap ? static_cast<int64_t>(a.qmap[q]) : q;  // positives of the original query
+        const int64_t p0 = active ? a.pos_indptr[qo] : 0, p1 = active ? a.pos_indptr[qo + 1] : 0;
         lane_init(tk, run_buf, a.pos_ids + p0, p1 - p0, active ? a.gtau + q : nullptr);
       }
       uint64_t g_pref = 0;  // RUNNING: shared threshold prefetched one tile ahead
@@ -875,6 +883,13 @@ int launch_refresh_tc(const TcLaunch& p, cudaStream_t st) {
   int G, n_parts;
   refresh_tc_layout(p.nq, n_lt, &G, &n_parts);
   const int cl = refresh_tc_cluster((p.nq + BM - 1) / BM);
+  if (p.n_parts_fixed > 0) {  // compact verify: row count known on the device only
+    n_parts = static_cast<int>(std::min<int64_t>(p.n_parts_fixed, n_lt));
+    int budget = num_sms();
+    const int b = g_refresh_sm_budget.load();
+    if (b > 0) budget = std::min(budget, b);
+    G = std::max(1, budget / cl) * cl;
+  }
   CUtensorMap tmA, tmB;
   ASTRA_TRY(make_map(&tmA, p.qb, p.nq, p.d, BM, p.f8));
   ASTRA_TRY(make_map(&tmB, p.wb, p.L, p.d, BN / cl, p.f8));
@@ -901,6 +916,8 @@ int launch_refresh_tc(const TcLaunch& p, cudaStream_t st) {
   a.cand_cnt = p.cand_cnt;
   a.cand_cap = p.cand_cap;
   a.only_flagged = p.only_flagged;
+  a.qmap = p.qmap;
+  a.n_active = p.n_active;
   a.gmax = p.gmax;
   const int mode = p.gmax ? kGmax : (p.tau_in ? kFixed : kRunning);
   a.debug_no_topk = getenv("ASTRA_TC_DEBUG_NO_TOPK") != nullptr;

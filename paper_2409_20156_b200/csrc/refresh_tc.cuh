@@ -39,6 +39,12 @@ struct TcLaunch {
   int cand_cap = 0;
   const int32_t* only_flagged = nullptr;
   uint32_t* gmax = nullptr;
+  // compact verify (running mode): the first *n_active rows of qb are the
+  // flagged queries, qmap[row] their original index (positives); the layout
+  // uses n_parts_fixed label parts over every SM pair
+  const int32_t* qmap = nullptr;
+  const int32_t* n_active = nullptr;
+  int n_parts_fixed = 0;
 };
 
 constexpr int kTcTileLabels = 256;
