@@ -34,6 +34,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -130,6 +131,15 @@ __device__ __forceinline__ double slot_loss(float sc, float pos_term, float wn) 
   const double spn = softplus64(-static_cast<double>(sc));
   return static_cast<double>(pos_term) * spn + static_cast<double>(wn) * (spn + static_cast<double>(sc));
 }
+
+// Hot labels (more than kHotOcc occurrences in the minibatch, e.g. the
+// popular rows of a clustered, trained W that many rows' hard lists share):
+// the single pass would walk their occurrences serially on one warp and rank-
+// sort them in O(n^2); they go to hot_label_kernel instead (block per label:
+// occurrences scored in parallel, then the ordered gradient sum), up to
+// kHotMax occurrences (its shared-memory sort).
+constexpr uint32_t kHotOcc = 32, kHotMax = 8192;
+__host__ __device__ __forceinline__ bool is_hot(uint32_t n) { return n > kHotOcc && n <= kHotMax; }
 
 template <bool BF16>
 __device__ __forceinline__ float4 load_w4(const void* W, size_t elem) {
@@ -590,7 +600,8 @@ __global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* blk_slots, uin
 __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* counts, int64_t Lloc,
                                                                   const uint32_t* blk_slots,
                                                                   const uint32_t* blk_nz, uint32_t* offsets,
-                                                                  int32_t* uniq, uint32_t* ustart, uint32_t* ucnt) {
+                                                                  int32_t* uniq, uint32_t* ustart, uint32_t* ucnt,
+                                                                  uint32_t* n_hot = nullptr, int32_t* hot_u = nullptr) {
   __shared__ uint32_t ws[kScanThreads / 32], wn[kScanThreads / 32];
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + static_cast<int64_t>(threadIdx.x) * kScanItems;
   uint32_t c[kScanItems];
@@ -647,6 +658,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
         if (ustart) {
           ustart[pn] = ps;
           ucnt[pn] = c[i];
+          if (hot_u && is_hot(c[i])) hot_u[atomicAdd(n_hot, 1u)] = static_cast<int32_t>(pn);
         }
         ++pn;
       }
@@ -1242,16 +1254,33 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       const int nb = min(32, n_mine - i0);
       for (int jj = 0; jj < nb; ++jj) {
         const int i = i0 + jj, qi = i % Q;
+        // a hot label takes a queue entry (its consumer skips it) but no data slot
+        const bool hot = is_hot(__shfl_sync(0xffffffffu, cur.n, jj));
         int sl = -1;
         if (lane == 0) {
           mbar_wait(&qempty[qi], ((i / Q) & 1) ^ 1);
-          uint32_t m;  // a free data slot: its previous fill released
-          while ((m = *reinterpret_cast<volatile uint32_t*>(freemask)) == 0u) __nanosleep(ASTRA_SINGLE_POLL_NS);
-          sl = __ffs(m) - 1;
-          atomicAnd(freemask, ~(1u << sl));
-          mbar_wait(&empty[sl], ((use >> sl) & 1) ^ 1);
+          if (!hot) {
+            uint32_t m;  // a free data slot: its previous fill released
+            while ((m = *reinterpret_cast<volatile uint32_t*>(freemask)) == 0u) __nanosleep(ASTRA_SINGLE_POLL_NS);
+            sl = __ffs(m) - 1;
+            atomicAnd(freemask, ~(1u << sl));
+            mbar_wait(&empty[sl], ((use >> sl) & 1) ^ 1);
+          }
         }
         sl = __shfl_sync(0xffffffffu, sl, 0);
+        if (hot) {
+          if (lane == jj) {
+            SingleQEntry e;
+            e.dc = cur;
+            e.slot = 0;
+            e.fpar = 0;
+            e.pad[0] = e.pad[1] = 0;
+            queue[qi] = e;
+            mbar_arrive(&qfull[qi]);
+          }
+          __syncwarp();
+          continue;
+        }
         const uint32_t fpar = (use >> sl) & 1u;
         use ^= 1u << sl;
         if (lane == jj) {
@@ -1309,6 +1338,7 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
     const uint32_t fpar = queue[qi].fpar;
     __syncwarp();
     if (lane == 0) mbar_arrive(&qempty[qi]);
+    if (is_hot(dc.n)) continue;  // hot_label_kernel's
     // the first occurrence's embedding row (prefetched into L1 one label ago)
     float4 e0[NV];
     load_emb_row<NV>(fa.emb, dc.slot0 / S, lane, e0);
@@ -1529,6 +1559,144 @@ __global__ void __launch_bounds__(kRowFinThreads) single_row_finalize(FwdArgs a,
   }
 }
 
+// The hot labels of the single pass (is_hot): CTA per label (grid-stride over
+// the device-side list). Phase A, warps over the label's occurrences in any
+// order: score (the pass's lane layout, fma order and butterfly: the same
+// bits), factor, fp64 loss term, grad_emb[b] += f * W_old (vector
+// reductions) — independent per occurrence, so a label with hundreds of
+// occurrences costs a few rounds of 8 warps instead of a serial walk. Phase B:
+// the occurrences sorted ascending in shared memory, each thread sums its 4
+// elements' gradient in that order (the two-kernel update's order and
+// roundings: W' stays bit-identical), then the SGD / Adam row update.
+constexpr int kHotThreads = 256;
+template <int NV, bool BF16, bool ADAM>
+__global__ void __launch_bounds__(kHotThreads) hot_label_kernel(SingleArgs A, const int32_t* hot_u,
+                                                                 const uint32_t* n_hot, int sort_cap) {
+  constexpr int d = NV * 128;
+  if (!*A.mode) return;
+  const UpdArgs& a = A.u;
+  const FwdArgs& fa = A.f;
+  const int S = fa.S;
+  extern __shared__ int32_t hot_sorted[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarps = kHotThreads / 32;
+  float wmax = 0.0f;
+  const uint32_t nh = *n_hot;
+  for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
+    const uint32_t u = static_cast<uint32_t>(hot_u[h]);
+    const int32_t l = a.uniq[u];
+    const uint32_t start = A.ustart[u], n = A.ucnt[u];
+    const size_t row = static_cast<size_t>(l) * d;
+    // ---- phase A
+    float4 p[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) p[q] = load_w4<BF16>(a.W, row + q * 128 + lane * 4);
+    for (uint32_t j = warp; j < n; j += kWarps) {
+      const int32_t slot = a.perm[start + j];
+      const int b = slot / S, s = slot - b * S;
+      float4 e[NV];
+      load_emb_row<NV>(fa.emb, b, lane, e);
+      const SlotMeta m = slot_meta(fa, b, s);
+      float acc = 0.0f;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        acc = fmaf(p[q].x, e[q].x, acc);
+        acc = fmaf(p[q].y, e[q].y, acc);
+        acc = fmaf(p[q].z, e[q].z, acc);
+        acc = fmaf(p[q].w, e[q].w, acc);
+      }
+      acc = warp_sum(acc);
+      float pt, wn;
+      const float f = slot_factor_meta(m, acc, &pt, &wn);
+      if (lane == 0) {
+        fa.factors[slot] = f;
+        A.slot_loss[slot] = slot_loss(acc, pt, wn);
+      }
+      if (f != 0.0f) {
+        float* ge = fa.grad_emb + static_cast<size_t>(b) * d + lane * 4;
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+          red_add_v4(ge + q * 128, make_float4(__fmul_rn(f, p[q].x), __fmul_rn(f, p[q].y), __fmul_rn(f, p[q].z),
+                                               __fmul_rn(f, p[q].w)));
+      }
+    }
+    // ---- phase B: ascending slot order (bitonic sort of the padded segment)
+    int P2 = 1;
+    while (P2 < static_cast<int>(n)) P2 <<= 1;
+    for (int i = threadIdx.x; i < P2; i += kHotThreads)
+      hot_sorted[i] = i < static_cast<int>(n) ? a.perm[start + i] : INT_MAX;
+    __syncthreads();  // (also: the factors written in phase A are visible to the block)
+    for (int size = 2; size <= P2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = threadIdx.x; i < P2; i += kHotThreads) {
+          const int jx = i ^ stride;
+          if (jx > i) {
+            const bool up = (i & size) == 0;
+            const int32_t x = hot_sorted[i], y = hot_sorted[jx];
+            if ((x > y) == up) {
+              hot_sorted[i] = y;
+              hot_sorted[jx] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (threadIdx.x < d / 4) {
+      const int t4 = threadIdx.x * 4;
+      float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+      for (uint32_t j = 0; j < n; ++j) {
+        const int32_t slot = hot_sorted[j];
+        const float f = fa.factors[slot];
+        const float4 x = *reinterpret_cast<const float4*>(fa.emb + static_cast<size_t>(slot / S) * d + t4);
+        const float4 fx = make_float4(__fmul_rn(f, x.x), __fmul_rn(f, x.y), __fmul_rn(f, x.z), __fmul_rn(f, x.w));
+        g = j == 0 ? fx : make_float4(__fadd_rn(g.x, fx.x), __fadd_rn(g.y, fx.y), __fadd_rn(g.z, fx.z), __fadd_rn(g.w, fx.w));
+      }
+      const size_t el = row + t4;
+      const float4 p4 = load_w4<BF16>(a.W, el);
+      float4 np;
+      if constexpr (ADAM) {
+        float4 m4 = *reinterpret_cast<const float4*>(a.m + el), v4 = *reinterpret_cast<const float4*>(a.v + el);
+        np.x = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p4.x, g.x, &m4.x, &v4.x);
+        np.y = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p4.y, g.y, &m4.y, &v4.y);
+        np.z = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p4.z, g.z, &m4.z, &v4.z);
+        np.w = upd_elem<true, BF16 && ASTRA_ADAM_FAST>(a, p4.w, g.w, &m4.w, &v4.w);
+        *reinterpret_cast<float4*>(a.m + el) = m4;
+        *reinterpret_cast<float4*>(a.v + el) = v4;
+      } else {
+        np.x = upd_elem<false>(a, p4.x, g.x, nullptr, nullptr);
+        np.y = upd_elem<false>(a, p4.y, g.y, nullptr, nullptr);
+        np.z = upd_elem<false>(a, p4.z, g.z, nullptr, nullptr);
+        np.w = upd_elem<false>(a, p4.w, g.w, nullptr, nullptr);
+      }
+      if constexpr (BF16) {
+        uint2 o;
+        o.x = static_cast<uint32_t>(f32_to_bf16_bits(np.x)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.y)) << 16);
+        o.y = static_cast<uint32_t>(f32_to_bf16_bits(np.z)) | (static_cast<uint32_t>(f32_to_bf16_bits(np.w)) << 16);
+        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(a.W) + el) = o;
+      } else {
+        *reinterpret_cast<float4*>(static_cast<float*>(a.W) + el) = np;
+      }
+      wmax = fmaxf(wmax, absmax4(np));
+    }
+    __syncthreads();  // before the next label reuses the sort buffer
+  }
+  push_wmax(a, wmax, lane);
+}
+
+template <int NV, bool BF16, bool ADAM>
+void launch_hot_nv(const SingleArgs& A, const int32_t* hot_u, const uint32_t* n_hot, int sort_cap, cudaStream_t st) {
+  const size_t smem = sizeof(int32_t) * static_cast<size_t>(sort_cap);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(hot_label_kernel<NV, BF16, ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(int32_t) * kHotMax));
+    attr = true;
+  }
+  hot_label_kernel<NV, BF16, ADAM><<<2 * num_sms(), kHotThreads, smem, st>>>(A, hot_u, n_hot, sort_cap);
+}
+
 template <int NV, bool BF16, bool ADAM>
 void launch_single_tma(const SingleArgs& A, cudaStream_t st) {
   static bool attr = false;
@@ -1647,6 +1815,8 @@ struct StepWs {
   double* slot_loss;
   uint32_t* ustart;
   uint32_t* ucnt;
+  uint32_t* n_hot;  // (in the memset bounds block)
+  int32_t* hot_u;   // hot labels' positions in uniq
 };
 
 size_t carve_step(void* base, size_t cap, int B, int S, int64_t Lloc, StepWs* w) {
@@ -1673,6 +1843,8 @@ size_t carve_step(void* base, size_t cap, int B, int S, int64_t Lloc, StepWs* w)
   w->slot_loss = c.take<double>(n);
   w->ustart = c.take<uint32_t>(n < Lloc ? n : Lloc);
   w->ucnt = c.take<uint32_t>(n < Lloc ? n : Lloc);
+  w->n_hot = w->bar ? w->bar + 2 : nullptr;
+  w->hot_u = c.take<int32_t>(n / (kHotOcc + 1) + 1);
   return c.off;
 }
 
@@ -1776,7 +1948,9 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
                                         w_absmax, single ? w.mode : nullptr, d);
     ASTRA_LAUNCHED("scan_top");
     scan_apply_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz, w.offsets,
-                                                                     w.uniq, single ? w.ustart : nullptr, w.ucnt);
+                                                                     w.uniq, single ? w.ustart : nullptr, w.ucnt,
+                                                                     single ? w.n_hot : nullptr,
+                                                                     single ? w.hot_u : nullptr);
     ASTRA_LAUNCHED("scan_apply");
     scatter_kernel<<<grid_n, 256, 0, st>>>(ids, w.rank, n, off, w.offsets, w.perm);
     ASTRA_LAUNCHED("scatter");
@@ -1819,6 +1993,27 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
     SA.mode = w.mode;
     SA.ustart = w.ustart;
     SA.ucnt = w.ucnt;
+    {
+      // the hot labels first (the pass skips them; disjoint rows, additive grad_emb)
+      int sort_cap = 1;
+      while (sort_cap < static_cast<int>(std::min<int64_t>(n, kHotMax))) sort_cap <<= 1;
+      auto hot = [&](auto bf_tag, auto adam_tag) {
+        constexpr bool BF = decltype(bf_tag)::value, AD = decltype(adam_tag)::value;
+        switch (nv) {
+          case 1: launch_hot_nv<1, BF, AD>(SA, w.hot_u, w.n_hot, sort_cap, st); break;
+          case 2: launch_hot_nv<2, BF, AD>(SA, w.hot_u, w.n_hot, sort_cap, st); break;
+          case 4: launch_hot_nv<4, BF, AD>(SA, w.hot_u, w.n_hot, sort_cap, st); break;
+          case 6: launch_hot_nv<6, BF, AD>(SA, w.hot_u, w.n_hot, sort_cap, st); break;
+        }
+      };
+      using T = std::true_type;
+      using F = std::false_type;
+      if (bf16)
+        adam ? hot(T(), T()) : hot(T(), F());
+      else
+        adam ? hot(F(), T()) : hot(F(), F());
+      ASTRA_LAUNCHED("hot_label");
+    }
     KernelTimer kt("step_single", st);
     if (bf16)
       adam ? launch_single_nv<true, true>(nv, SA, st) : launch_single_nv<true, false>(nv, SA, st);
