@@ -906,7 +906,7 @@ struct RefreshWs {
 
 // Label parts of the compact verify pass (its query rows are few: the parts
 // spread them over the SM pairs).
-constexpr int kVerifyParts = 32;
+constexpr int kVerifyParts = 64;
 
 // bf16 candidates kept per query before the fp32 re-rank: k' = max(1.5k, k+16),
 // a multiple of 8 (bf16 top-k' contains the fp32 top-k; see tests + DESIGN.md).
