@@ -956,13 +956,21 @@ struct TwoPass {
 };
 
 // Tile stride of the sample pass (ASTRA_SAMPLE_STRIDE overrides; measurement aid).
-int64_t sample_stride() {
+// Auto (default): 16, doubled up to 64 while the sample still covers >= 300
+// label tiles (1200 groups): the sample pass costs 1/stride of the threshold
+// pass, and the C5 shard's 58.6K tiles need far fewer than 1/16 of them for the
+// same 5-sigma threshold (a coarser stride means more candidates per query,
+// j * stride, which the select absorbs). C4 (5.1K tiles) stays at 16.
+int64_t sample_stride(int64_t n_tiles) {
   static const int64_t v = [] {
     const char* e = getenv("ASTRA_SAMPLE_STRIDE");
-    const int64_t x = e ? atoll(e) : 16;
-    return x >= 2 && x <= 256 ? x : 16;
+    const int64_t x = e ? atoll(e) : 0;
+    return x >= 2 && x <= 256 ? x : 0;
   }();
-  return v;
+  if (v) return v;
+  int64_t st = 16;
+  while (st < 64 && n_tiles / (2 * st) >= 300) st *= 2;
+  return st;
 }
 // per-query select capacity (candidates over all parts): 8192 keeps the
 // two-pass plan on for k' up to 512 at 9 label parts (the C5 shard's
@@ -978,7 +986,7 @@ TwoPass plan_two_pass(int64_t nq, int64_t L, int kk, int n_parts) {
   }();
   const int64_t n_tiles = (L + kTcTileLabels - 1) / kTcTileLabels;
   if (force == 0 || kk > 512) return t;
-  const int64_t kSampleStride = sample_stride();
+  const int64_t kSampleStride = sample_stride(n_tiles);
   if (n_tiles < kSampleStride * (force == 1 ? 1 : 32)) return t;  // small label sets: running top-k
   const double z = 5.0, m = static_cast<double>(kk) / kSampleStride;
   int j = static_cast<int>(std::ceil(std::pow(z / 2 + std::sqrt(z * z / 4 + m), 2.0)));
