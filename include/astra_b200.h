@@ -97,7 +97,10 @@ void astra_set_refresh_sm_budget(int n_sms);
  * and writes each touched W row once and adds each slot's f * W_row into
  * grad_emb with fp32 vector reductions: W', the loss and the factors are
  * deterministic (W' bit-identical to the two-kernel schedule), grad_emb's
- * summation order is not. on = 1: the two-kernel schedule (slot-major gather
+ * summation order is not; labels with more than 32 occurrences in the batch
+ * are updated by a CTA each beside the pass (same order and roundings).
+ * SGD and Adam alike (ASTRA_STEP_SINGLE_ADAM=0 keeps Adam on the two-kernel
+ * schedule). on = 1: the two-kernel schedule (slot-major gather
  * forward, then the label-major update), bitwise run-to-run deterministic.
  * The environment variable ASTRA_STEP_SINGLE=0 is equivalent to on = 1. */
 void astra_set_step_deterministic(int on);
