@@ -141,6 +141,18 @@ __device__ __forceinline__ double slot_loss(float sc, float pos_term, float wn) 
 constexpr uint32_t kHotOcc = 32, kHotMax = 8192;
 __host__ __device__ __forceinline__ bool is_hot(uint32_t n) { return n > kHotOcc && n <= kHotMax; }
 
+// Ring slots are released (mbarrier arrive, then refilled by a TMA bulk copy:
+// the async proxy) right after a warp's shared-memory loads of the slot. An
+// LDS still in flight at the arrive could read the next fill: each lane first
+// waits for its loaded registers (an empty asm that consumes them), then the
+// warp syncs and lane 0 arrives. (compute-sanitizer racecheck flagged these
+// read/bulk-write pairs; a rare wrong Adam update fit the same window.)
+template <int N>
+__device__ __forceinline__ void regs_landed(const float4 (&r)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" ::"f"(r[i].x), "f"(r[i].y), "f"(r[i].z), "f"(r[i].w) : "memory");
+}
+
 template <bool BF16>
 __device__ __forceinline__ float4 load_w4(const void* W, size_t elem) {
   if constexpr (BF16) {
@@ -301,6 +313,7 @@ __global__ void __launch_bounds__(kTmaThreads, 3) slot_forward_tma(FwdArgs a) {
           w[j] = *reinterpret_cast<const float4*>(ring + r * ROWB + (j * 128 + lane * 4) * 4);
         }
       }
+      regs_landed(w);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[r]);  // the row is in registers: release the slot
       float f;
@@ -997,7 +1010,10 @@ __global__ void __launch_bounds__(kTmaThreads, upd_tma_ctas<NV, ADAM>()) label_u
         m4[q] = *reinterpret_cast<const float4*>(ring + r * ROWB + RG::WB + (q * 128 + lane * 4) * 4);
         v4[q] = *reinterpret_cast<const float4*>(ring + r * ROWB + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
       }
+      regs_landed(m4);
+      regs_landed(v4);
     }
+    regs_landed(p);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[r]);
 #pragma unroll
@@ -1368,6 +1384,9 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
         mr[q] = *reinterpret_cast<const float4*>(ent + RG::WB + (q * 128 + lane * 4) * 4);
         vr[q] = *reinterpret_cast<const float4*>(ent + RG::WB + RG::MB + (q * 128 + lane * 4) * 4);
       }
+      regs_landed(mr);
+      regs_landed(vr);
+      regs_landed(p);
       __syncwarp();
       if (lane == 0) release(r);
     }
