@@ -24,6 +24,13 @@ static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
   } while (!done);
 }
 
+// Order this thread's prior generic-proxy shared-memory accesses before later
+// async-proxy (TMA) accesses: a ring consumer runs it after reading a slot and
+// before the slot is released to the next bulk copy.
+static __device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 static __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(64) rerank_tma_kernel(const float* Q, const vo
           s = fmaf(x.z, v.z, s);
           s = fmaf(x.w, v.w, s);
         }
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
       }

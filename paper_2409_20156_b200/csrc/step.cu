@@ -151,6 +151,7 @@ template <int N>
 __device__ __forceinline__ void regs_landed(const float4 (&r)[N]) {
 #pragma unroll
   for (int i = 0; i < N; ++i) asm volatile("" ::"f"(r[i].x), "f"(r[i].y), "f"(r[i].z), "f"(r[i].w) : "memory");
+  fence_proxy_async_smem();
 }
 
 template <bool BF16>
@@ -1465,6 +1466,7 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
       pend_loss(dc.slot0, acc, pt, wn);
       grad_emb_add(dc.slot0 / S, f);
       if constexpr (!ADAM) {  // W row consumed (Adam: after the moments, below)
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) release(r);
       }
@@ -1523,12 +1525,14 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
         grad_emb_add(b, f);
       }
       if constexpr (!ADAM) {
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) release(r);
       }
       update_row([&](int q) { return *reinterpret_cast<const float4*>(gs + q * 128); });
     }
     if constexpr (ADAM && !EARLY) {
+      fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) release(r);
     }
