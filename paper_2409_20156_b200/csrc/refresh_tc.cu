@@ -202,18 +202,6 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
-// Pair TMA load multicast to the CTAs of `mask` (the same half of the W tile
-// in every pair of the cluster): the bytes landing in each destination
-// complete on the barrier at `bar`'s offset in that destination's pair leader
-// (the peer bit of the address cleared).
-__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                                    uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
 
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -403,10 +391,9 @@ __device__ __forceinline__ bool unit_active(const uint32_t* qbits, int64_t n_qt_
 template <int CL, int MODE, bool PAIR, bool F8>
 __global__ void __launch_bounds__(kThreads, 1)
     refresh_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
-  static_assert(!PAIR || CL == 2 || CL == 4, "CTA pairs: a cluster of 1 or 2 pairs");
-  // pairs in the cluster: they share every W tile (each CTA loads 1/NPAIR of
-  // its half of the tile and multicasts it to the same half in every pair)
-  constexpr int NPAIR = PAIR ? CL / 2 : 1;
+  // (two CTA pairs per cluster sharing every W tile by multicast were measured
+  // 1.7x slower: profiles/r02s3/ab_refresh_cluster4.txt)
+  static_assert(!PAIR || CL == 2, "a CTA pair is a cluster of 2");
   using G = Geo<PAIR>;
   constexpr int NST = G::NST;
   constexpr uint16_t kMask = static_cast<uint16_t>((1u << CL) - 1);
@@ -427,7 +414,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* stage_base = reinterpret_cast<float*>(smem + NST * G::STG + kBarrierBytes);
   const bool leader = !PAIR || (crank & 1u) == 0;
   const uint32_t prank = crank & ~1u;  // this CTA's pair leader
-  constexpr uint16_t kAllMask = static_cast<uint16_t>((1u << CL) - 1);
   const uint16_t pair_mask = static_cast<uint16_t>(3u << prank);
   constexpr int KB = kb_elems<F8>();  // K elements per stage
   const int nkb = a.d / KB;
@@ -455,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       // multicast: every cluster CTA's MMA releases the stage; pair: one commit from the leader
-      mbar_init(&empty[s], PAIR ? NPAIR : CL);  // pairs: every pair's MMA must release the stage
+      mbar_init(&empty[s], PAIR ? 1 : CL);  // multicast: every cluster CTA's MMA releases the stage; pair: the leader's commit
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -501,15 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t bar = mapa_cluster(&full[stage], prank);
               if (leader) mbar_expect_tx(&full[stage], 2 * G::STG);
               tma_load_2d_pair(sA + stage * A_STAGE, &tmA, bar, kb * KB, q0);
-              if constexpr (NPAIR == 1) {
-                tma_load_2d_pair(sB + stage * G::B_ST, &tmB, bar, kb * KB, n0 + static_cast<int>(crank) * G::B_ROWS);
-              } else {
-                const uint32_t half = crank & 1u, slice = crank >> 1;
-                constexpr int SL_ROWS = G::B_ROWS / NPAIR;
-                tma_load_2d_pair_mc(sB + stage * G::B_ST + slice * (G::B_ST / NPAIR), &tmB, &full[stage], kb * KB,
-                                    n0 + static_cast<int>(half) * G::B_ROWS + static_cast<int>(slice) * SL_ROWS,
-                                    static_cast<uint16_t>((half ? 0xAAAAu : 0x5555u) & kAllMask));
-              }
+              tma_load_2d_pair(sB + stage * G::B_ST, &tmB, bar, kb * KB, n0 + static_cast<int>(crank) * G::B_ROWS);
             } else {
               mbar_expect_tx(&full[stage], STAGE_BYTES);  // own A + all CL slices of the W tile
               tma_load_2d(sA + stage * A_STAGE, &tmA, &full[stage], kb * KB, q0);
@@ -565,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mma_bf16(dcol, ad + 2 * kk, bd + 2 * kk, (kb | kk) != 0);
             }
             if constexpr (PAIR)
-              mma_commit_pair(&empty[stage], NPAIR == 1 ? pair_mask : kAllMask);
+              mma_commit_pair(&empty[stage], pair_mask);
             else if (CL == 1)
               mma_commit(&empty[stage]);
             else
@@ -791,14 +769,12 @@ bool refresh_tc_pair() {
   return pair;
 }
 
-// Cluster size along query tiles (ASTRA_TC_CLUSTER=1|2|4, default 2; 4 = two
-// CTA pairs sharing every W tile, pairs only), reduced for batches with fewer
-// query tiles.
+// Cluster size along query tiles (ASTRA_TC_CLUSTER=1|2, default 2), reduced
+// for batches with a single query tile.
 int refresh_tc_cluster(int64_t n_qt) {
   static int cl = [] {
     const char* e = getenv("ASTRA_TC_CLUSTER");
-    const int v = e ? atoi(e) : 2;
-    return v == 1 ? 1 : (v == 4 && refresh_tc_pair() ? 4 : 2);
+    return (e && atoi(e) == 1) ? 1 : 2;
   }();
   int c = cl;
   while (c > 1 && n_qt < c) c >>= 1;
@@ -936,11 +912,6 @@ int launch_refresh_tc(const TcLaunch& p, cudaStream_t st) {
   const bool pair = refresh_tc_pair();
   auto dispatch = [&](auto f8_tag) {
     constexpr bool F8 = decltype(f8_tag)::value;
-    if (cl == 4) {
-      if (mode == kFixed) return launch_variant<4, kFixed, true, F8>(tmA, tmB, a, grid, st);
-      if (mode == kGmax) return launch_variant<4, kGmax, true, F8>(tmA, tmB, a, grid, st);
-      return launch_variant<4, kRunning, true, F8>(tmA, tmB, a, grid, st);
-    }
     if (cl == 2 && pair) {
       if (mode == kFixed) return launch_variant<2, kFixed, true, F8>(tmA, tmB, a, grid, st);
       if (mode == kGmax) return launch_variant<2, kGmax, true, F8>(tmA, tmB, a, grid, st);
