@@ -28,6 +28,20 @@ for t in range(4):
     mbs.append((rows, ip, pos.reshape(-1).contiguous(), hard, emb))
 
 
+# ASTRA_BENCH_STEP_GEMM=1: before every 9th minibatch, a C4-size refresh (the
+# bench's power / cache environment for the step kernels); the refresh itself
+# is outside the kernel timings reported for the step
+gemm_env = os.environ.get("ASTRA_BENCH_STEP_GEMM") == "1"
+if gemm_env:
+    from paper_2409_20156_b200 import ops  # noqa: E402
+
+    Wr = eng.W if eng.W.dtype == torch.float32 else eng.W.float()
+    Wrb = ops.f32_to_bf16(Wr)
+    Eq = torch.randn((9216, d), device="cuda", generator=g)
+    pq = torch.randint(0, L, (9216, 38), device="cuda", generator=g).sort(1).values.to(torch.int32).reshape(-1)
+    iq = torch.arange(0, 9216 * 38 + 1, 38, device="cuda", dtype=torch.int64)
+
+
 def one(i):
     rows, ip, pid, hard, emb = mbs[i % 4]
     sl = eng.sample(rows, ip, pid, hard, epoch=1, step=i)
@@ -45,8 +59,16 @@ import time  # noqa: E402
 
 e0.record()
 h0 = time.perf_counter()
+pos = []
 for i in range(n):
+    if gemm_env and i % 9 == 0:
+        ops.refresh_topk(Eq, iq, pq, k_h, "bf16_rerank", labels_f32=Wr, labels_bf16=Wrb)
+    a_ = torch.cuda.Event(enable_timing=True)
+    b_ = torch.cuda.Event(enable_timing=True)
+    a_.record()
     _, sl = one(i)
+    b_.record()
+    pos.append((i % 9, a_, b_))
 h1 = time.perf_counter()
 e1.record()
 torch.cuda.synchronize()
@@ -57,3 +79,8 @@ byts = U * d * (2 * 2 + 16 if adam else 8) + 2 * B * d * 4 + B * (k_p + k_h + k_
 print(f"step {ms:.3f} ms/minibatch  U={U}  {byts / ms / 1e6:.0f} GB/s algorithmic ({byts / 1e9:.2f} GB)")
 kt = {k: _lib.kernel_timing(k) for k in ("step_single", "slot_forward", "label_update")}
 print("kernels  " + "  ".join(f"{k} {ms / max(c, 1):.3f} ms" for k, (ms, c) in kt.items()))
+if gemm_env:
+    per = [[] for _ in range(9)]
+    for p_, a_, b_ in pos:
+        per[p_].append(a_.elapsed_time(b_))
+    print("minibatch ms by position after the refresh: " + " ".join(f"{sum(v) / len(v):.3f}" for v in per if v))
