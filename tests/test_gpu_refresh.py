@@ -326,3 +326,42 @@ def test_rerank_candidates_matches_oracle(cuda_lib):
                                                          labels_f32=torch.from_numpy(W), label_offset=off)
     np.testing.assert_array_equal(got.cpu().numpy(), want.numpy())
     np.testing.assert_array_equal(ids.cpu().numpy(), want_ids.numpy())
+
+
+@pytest.mark.parametrize("n_shards", [2, 3])
+def test_sharded_rerank_composition_equals_one_gpu(cuda_lib, n_shards):
+    """engine._refresh_sharded_rerank's composition on CUDA with the label
+    range split into shards on one device: each shard's bf16 top-k', the
+    owner's merge -> the global k'-th key tau, each shard's fp32 re-rank of
+    its candidates >= tau, the merge of the fp32 lists — equals the one-GPU
+    BF16_RERANK result key for key (the candidate set is the same)."""
+    from paper_2409_20156_b200 import ops
+    from paper_2409_20156_b200.shard import shard_range
+
+    rng = np.random.default_rng(5)
+    L, d, nq, k = 300_000, 256, 512, 48
+    W = torch.from_numpy((rng.standard_normal((L, d)) / 16).astype(np.float32)).cuda()
+    Wb = ops.f32_to_bf16(W)
+    E = torch.from_numpy(rng.standard_normal((nq, d)).astype(np.float32)).cuda()
+    pos = [np.sort(rng.choice(L, size=4, replace=False)).astype(np.int32) for _ in range(nq)]
+    ip = torch.from_numpy(np.concatenate([[0], np.cumsum([len(p) for p in pos])]).astype(np.int64)).cuda()
+    pid = torch.from_numpy(np.concatenate(pos)).cuda()
+    want, want_ids, _ = ops.refresh_topk(E, ip, pid, k, "bf16_rerank", labels_f32=W, labels_bf16=Wb)
+    kc = ops.rerank_candidates_count(k)
+    ranges = [shard_range(L, r, n_shards) for r in range(n_shards)]
+    ck = [ops.refresh_topk(E, ip, pid, kc, "bf16", labels_f32=W[lo:hi].contiguous(),
+                           labels_bf16=Wb[lo:hi].contiguous(), label_offset=lo)[0] for lo, hi in ranges]
+    merged, _, _ = ops.topk_merge(torch.stack(ck), kc)
+    tau = merged[:, kc - 1]
+    flip = torch.tensor(-(2 ** 63), dtype=torch.int64, device="cuda")
+    fk = []
+    kept = 0
+    for (lo, hi), c in zip(ranges, ck):
+        keep = (c ^ flip) >= (tau[:, None] ^ flip)
+        kept += int(keep.sum())
+        cand = torch.where(keep, c, torch.zeros_like(c))
+        fk.append(ops.rerank_candidates(E, cand, k, labels_f32=W[lo:hi].contiguous(), label_offset=lo)[0])
+    got, got_ids, _ = ops.topk_merge(torch.stack(fk), k)
+    assert kept == nq * kc  # exactly the global top-k' (keys are unique)
+    np.testing.assert_array_equal(got.cpu().numpy(), want.cpu().numpy())
+    np.testing.assert_array_equal(got_ids.cpu().numpy(), want_ids.cpu().numpy())

@@ -595,3 +595,43 @@ def test_hot_labels_single_equals_two_kernel(cuda_lib, wdtype, optimizer):
         assert abs(a - b) <= 1e-9 * abs(a)
     for a, b in zip(outs[0][n_state + 1], outs[1][n_state + 1]):
         close(b, a)
+
+
+def test_step_heavy_tailed_labels_vs_oracle(cuda_lib):
+    """A production-size minibatch (B=1024, S=584, d=768) whose slates draw
+    distinct labels per row from a heavy-tailed popularity (the popular labels
+    of a clustered W sit in most rows: hundreds of labels with more than 32
+    occurrences, i.e. the hot-label CTAs) against the oracle port of
+    trainer.py:366-394: loss, grad_emb and W' within the fp32 tolerance;
+    untouched rows bit-identical."""
+    from paper_2409_20156_b200 import ops
+
+    rng = np.random.default_rng(41)
+    L, d, B, S = 100_000, 768, 1024, 584
+    W = rng.uniform(-1 / np.sqrt(d), 1 / np.sqrt(d), size=(L, d)).astype(np.float32)
+    emb = rng.standard_normal((B, d)).astype(np.float32)
+    pop = 1.0 / (np.arange(L) + 10.0) ** 1.1
+    pop /= pop.sum()
+    ids = np.stack([rng.choice(L, size=S, replace=False, p=pop) for _ in range(B)])
+    counts = np.bincount(ids.ravel(), minlength=L)
+    assert (counts > 32).sum() > 100 and counts.max() <= B
+    y = (rng.random((B, S)) < 0.02).astype(np.int8)
+    origin = np.full(S, port.ORIGIN_RAND, np.int8)
+    origin[:8] = port.ORIGIN_POS
+    origin[8:72] = port.ORIGIN_HARD
+    weights = np.ones(S, np.float32)
+    weights[origin == port.ORIGIN_RAND] = np.float32((L - 64) / (S - 72))
+    Wd = dev(W)
+    res = ops.slate_step(dev(emb), dev(ids.astype(np.int32)), dev(y), dev(origin), dev(weights), Wd, 0.05, 1e-4,
+                         w_absmax=_bound(W, True))
+    Wref = W.copy()
+    loss, grad_emb, _, uids = port.slate_step(Wref, emb, None, ids.astype(np.int64), y, origin, weights, 0.05, 1e-4)
+    torch.cuda.synchronize()
+    assert res.status_host() == [0, 0, 0, 0]
+    assert abs(res.loss - loss) <= 1e-5 * abs(loss)
+    close(res.grad_emb.cpu().numpy(), grad_emb)
+    Wg = Wd.cpu().numpy()
+    close(Wg[uids], Wref[uids])
+    mask = np.ones(L, bool)
+    mask[uids] = False
+    np.testing.assert_array_equal(Wg[mask], W[mask])
