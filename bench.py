@@ -621,13 +621,29 @@ def run_emulate(args):
     global_rr = args.refresh_mode == "bf16_rerank" and not args.emulate_full_rerank
     kc = ops.rerank_candidates_count(k_h)
     flip = torch.tensor(-(2 ** 63), dtype=torch.int64, device="cuda")
+    # ... and the candidate pass with a global threshold (engine._candidates_global):
+    # the shard's sample statistics (j largest sampled group maxima), the global
+    # j-th largest (proxy: this shard's ceil(j/N)-th: the expected position of the
+    # global j-th among an i.i.d. shard's samples), the local candidates at or
+    # above it, the verify set (proxy: this shard's count x N < k' or overflow)
+    j_sh = ops.refresh_plan_j(Rg, Lr, d, kc) if global_rr and not args.emulate_shard_candidates else 0
 
     def one(t, timed):
         q, pid, hard = data[t]
         e = ev[t]
         e[0].record(stream)
+        if global_rr and j_sh > 0:
+            top = ops.refresh_sharded_stage(1, q, ip_step, pid, kc, snap_lp, label_offset=lo)
+            jl = -(-j_sh // N)
+            gtau = (top.to(torch.int64) & 0xFFFFFFFF).topk(jl, dim=1).values[:, jl - 1] << 32
+            ck, cnt, ovf = ops.refresh_sharded_stage(2, q, ip_step, pid, kc, snap_lp, label_offset=lo, tau_keys=gtau)
+            need = ((cnt.to(torch.int64) * N < kc) | (ovf > 0)).to(torch.int32)
+            ckeys = ops.refresh_sharded_stage(3, q, ip_step, pid, kc, snap_lp, label_offset=lo, io_keys=ck,
+                                              flags=need)
         if global_rr:
-            ckeys, _, _ = ops.refresh_topk(q, ip_step, pid, kc, "bf16", labels_f32=snap_f32, label_offset=lo, **lp)
+            if j_sh == 0:
+                ckeys, _, _ = ops.refresh_topk(q, ip_step, pid, kc, "bf16", labels_f32=snap_f32, label_offset=lo,
+                                               **lp)
             ops.topk_merge(ckeys[:R].unsqueeze(0).expand(N, R, kc).contiguous(), kc)  # owner's merge (stand-in data)
             tau = ckeys[:, -(-kc // N) - 1].contiguous()  # (proxy of the all-gathered global tau)
             cand = torch.where((ckeys ^ flip) >= (tau[:, None] ^ flip), ckeys, torch.zeros_like(ckeys))
@@ -695,6 +711,9 @@ def run_emulate(args):
         "keys_all_to_all": (N - 1) * R * k_h * 8,
         **({"bf16_candidate_keys_all_to_all": (N - 1) * R * kc * 8, "tau_all_gather": (N - 1) * R * 8}
            if global_rr else {}),
+        **({"sample_stats_all_to_all": (N - 1) * R * j_sh * 4, "candidate_tau_all_gather": (N - 1) * R * 8,
+            "candidate_counts_all_to_all": (N - 1) * R * 16, "verify_flags_all_gather": (N - 1) * R * 4}
+           if j_sh > 0 else {}),
         **({"sampler_inputs_all_gather": M * (N - 1) * B * (8 + lpp * 4 + 8 + k_h * 4)} if regen else
            {"slates_all_gather": M * (N - 1) * B * S * 10}),
         "emb_all_gather": M * (N - 1) * B * d * 4,
@@ -710,7 +729,11 @@ def run_emulate(args):
                        slate_exchange=args.slate_exchange,
                        sharded_rerank=("global k'-th bf16 key threshold (engine._refresh_sharded_rerank; "
                                        "tau proxied by this shard's ceil(k'/N)-th key)") if global_rr
-                       else "every shard re-ranks its full local top-k'"),
+                       else "every shard re-ranks its full local top-k'",
+                       sharded_candidates=("global threshold from the shards' sample statistics "
+                                           "(engine._candidates_global; the global j-th sampled maximum proxied by "
+                                           "this shard's ceil(j/N)-th, the verify set by count x N < k')")
+                       if j_sh > 0 else "each shard's own top-k' candidates"),
         "phases_ms_per_step": {k: round(v, 4) for k, v in ph.items()},
         "owned_slots_per_minibatch": round(slots, 1), "unique_owned_labels_per_minibatch": round(U, 1),
         "occurrences_per_owned_label": round(slots / max(U, 1), 3),
@@ -1238,6 +1261,8 @@ def main():
                          "install())")
     ap.add_argument("--refresh-sms", type=int, default=0,
                     help="SM budget of the refresh running concurrently with training on a side stream (0 = serial)")
+    ap.add_argument("--emulate-shard-candidates", action="store_true",
+                    help="--emulate: each shard finds its own top-k' candidates (no global candidate threshold)")
     ap.add_argument("--emulate-full-rerank", action="store_true",
                     help="--emulate: every shard re-ranks its full local top-k' (no global threshold)")
     ap.add_argument("--emulate", type=int, default=0,

@@ -286,6 +286,30 @@ int astra_dense_bce(const void* scores, int scores_f64, int B, int64_t n_labels,
 int astra_dense_sgd(float* W, const float* grads, int64_t n, float lr, float weight_decay,
                     void* stream);
 
+/* The label-sharded BF16 candidate pass with a global threshold (the
+ * multi-GPU refresh, engine._refresh_sharded): each shard's sample statistics
+ * go to the rows' owners, which return a global per-query threshold; the
+ * shard's candidates at or above it are selected locally and the owners'
+ * summed counts decide which queries take the exact verify pass. The
+ * workspace is astra_refresh_workspace_size(nq, n_labels, d, k,
+ * ASTRA_REFRESH_BF16); k is the candidate count (k').
+ *   astra_refresh_plan_j: j of the sample statistics for this shape (0 = the
+ *     shape does not run the two-pass plan: use astra_refresh_topk).
+ *   stage 1: sample_top [nq, j] = the shard's j largest sampled 64-label
+ *     group maxima per query (orderable score bits, any order).
+ *   stage 2: tau_keys [nq] (the global threshold, key form score << 32) ->
+ *     io_keys [nq, k] = the shard's best non-positive candidates at or above
+ *     it (descending, 0-padded), counts [nq] = how many (<= k), flags [nq] =
+ *     1 where a candidate list overflowed (verify needed whatever the counts).
+ *   stage 3: flags [nq] (the global verify set) -> io_keys rows of the
+ *     flagged queries replaced by the shard's exact top-k. */
+int astra_refresh_plan_j(int64_t nq, int64_t n_labels, int d, int k);
+int astra_refresh_sharded_stage(int stage, const float* queries_f32, const uint16_t* queries_bf16, int64_t nq, int d,
+                                const uint16_t* labels_bf16, int64_t n_labels, int64_t label_offset,
+                                const int64_t* pos_indptr, const int32_t* pos_ids, int k, uint32_t* sample_top,
+                                const uint64_t* tau_keys, uint64_t* io_keys, int32_t* counts, int32_t* flags,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
 /* The refresh's fp32 re-rank on its own (the last stage of BF16_RERANK,
  * anns.py:253-256 scores): for each of nq queries (fp32 [nq, d]) score the
  * kc candidate keys cand[q * kc + j] (astra key format; 0 = no candidate)

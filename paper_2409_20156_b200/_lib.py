@@ -47,6 +47,8 @@ _SIGS = {
     "astra_dense_bce": ([p, i32, i32, i64, p, p, p, p, p, sz, p], i32),
     "astra_dense_sgd": ([p, p, i64, f32, f32, p], i32),
     "astra_rerank_candidates": ([p, i64, i32, p, i32, p, i32, i64, i32, p, p, p, p], i32),
+    "astra_refresh_plan_j": ([i64, i64, i32, i32], i32),
+    "astra_refresh_sharded_stage": ([i32, p, p, i64, i32, p, i64, i64, p, p, i32, p, p, p, p, p, p, sz, p], i32),
     "astra_gemm_f32_workspace_size": ([i64, i64, i64], sz),
     "astra_gemm_f32": ([p, i32, p, i32, i64, i64, i64, p, p, sz, p], i32),
     "astra_stream_sync": ([p], i32),

@@ -76,6 +76,11 @@ int dense_bce(const void* S, int s_f64, int B, int64_t L, const int64_t* pos_ind
               float* G, double* loss_out, void* workspace, size_t ws_bytes, cudaStream_t st);
 int dense_sgd(float* W, const float* grads, int64_t n, float lr, float wd, cudaStream_t st);
 size_t gemm_f32_workspace(int64_t M, int64_t N, int64_t K);
+int refresh_plan_j(int64_t nq, int64_t L, int d, int k);
+int refresh_sharded_stage(int stage, const float* qf, const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
+                          int64_t L, int64_t off, const int64_t* pos_indptr, const int32_t* pos_ids, int k,
+                          uint32_t* sample_top, const uint64_t* tau_keys, uint64_t* io_keys, int32_t* counts,
+                          int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t st);
 int rerank_only(const float* qf, int64_t nq, int d, const uint64_t* cand, int kc, const void* labels, int w_dtype,
                 int64_t off, int k, uint64_t* out_keys, int32_t* out_ids, float* out_scores, cudaStream_t st);
 int gemm_f32(const float* A, int a_kmajor, const float* B, int b_kmajor, int64_t M, int64_t N, int64_t K, float* D,
@@ -220,6 +225,18 @@ int astra_dense_bce(const void* scores, int scores_f64, int B, int64_t n_labels,
 
 int astra_dense_sgd(float* W, const float* grads, int64_t n, float lr, float weight_decay, void* stream) {
   return dense_sgd(W, grads, n, lr, weight_decay, S(stream));
+}
+
+int astra_refresh_plan_j(int64_t nq, int64_t n_labels, int d, int k) { return refresh_plan_j(nq, n_labels, d, k); }
+
+int astra_refresh_sharded_stage(int stage, const float* queries_f32, const uint16_t* queries_bf16, int64_t nq, int d,
+                                const uint16_t* labels_bf16, int64_t n_labels, int64_t label_offset,
+                                const int64_t* pos_indptr, const int32_t* pos_ids, int k, uint32_t* sample_top,
+                                const uint64_t* tau_keys, uint64_t* io_keys, int32_t* counts, int32_t* flags,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  return refresh_sharded_stage(stage, queries_f32, queries_bf16, nq, d, labels_bf16, n_labels, label_offset,
+                               pos_indptr, pos_ids, k, sample_top, tau_keys, io_keys, counts, flags, workspace,
+                               workspace_bytes, S(stream));
 }
 
 int astra_rerank_candidates(const float* queries, int64_t nq, int d, const uint64_t* cand, int kc, const void* labels,

@@ -719,6 +719,36 @@ __global__ void __launch_bounds__(256) tau_select_kernel(const uint32_t* gmax, i
   if (lane == 0) tau_keys[q] = static_cast<uint64_t>(T) << 32;
 }
 
+// The label-sharded refresh's sample statistics: per query the j largest
+// sampled group maxima of this shard (orderable bits, any order; ties at the
+// j-th value filled in index order), from which the rows' owners take the
+// global j-th largest over all shards.
+__global__ void __launch_bounds__(256) sample_top_kernel(const uint32_t* gmax, int64_t nq, int n_groups, int j,
+                                                         uint32_t* out) {
+  __shared__ uint32_t hist[8][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+  if (q >= nq) return;  // warp-uniform
+  const uint32_t* v = gmax + static_cast<size_t>(q) * n_groups;
+  uint32_t* o = out + static_cast<size_t>(q) * j;
+  uint32_t T = 0;
+  if (n_groups >= j)
+    T = warp_kth_largest([&](int i, uint32_t& x) { x = __ldg(v + i); return true; }, n_groups, j, hist[warp], lane);
+  int n = 0;
+  for (int pass = 0; pass < 2 && n < j; ++pass) {  // values > T, then == T
+    for (int i0 = 0; i0 < n_groups && n < j; i0 += 32) {
+      const int i = i0 + lane;
+      const uint32_t x = i < n_groups ? __ldg(v + i) : 0u;
+      const bool take = i < n_groups && (pass == 0 ? x > T : x == T);
+      const unsigned b = __ballot_sync(0xffffffffu, take);
+      const int at = n + __popc(b & ((1u << lane) - 1u));
+      if (take && at < j) o[at] = x;
+      n += __popc(b);
+    }
+  }
+  for (int e = n + lane; e < j; e += 32) o[e] = 0u;  // (fewer sampled groups than j)
+}
+
 // Warp per query: gather the FIXED-mode candidate lists of the query's label
 // parts, drop the query's positives (anns.py:254-255) and keep the top k in
 // (score desc, id asc) order: a radix select of the k-th largest score over
@@ -741,7 +771,8 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
                                                                 int n_parts, int cand_cap, int64_t nq,
                                                                 const int64_t* pos_indptr, const int32_t* pos_ids,
                                                                 int k, int sel_max, int rcap, uint64_t* out_keys,
-                                                                int32_t* out_ids, float* out_scores, int32_t* flags) {
+                                                                int32_t* out_ids, float* out_scores, int32_t* flags,
+                                                                int32_t* local_counts = nullptr) {
   // per warp: the candidates' 32-bit score parts (the radix select reads
   // them four times) and R, the full keys of those at or above T2 (read back
   // from the lists) — half the staging of full keys, so more warps per SM
@@ -772,7 +803,10 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
   }
   if (lane == 0 && !overflow) sel_off[warp][n_parts] = total;
   bool fail = overflow || total > sel_max;
-  if (lane == 0 && fail) flags[q] = 1;
+  if (lane == 0 && fail) {
+    flags[q] = 1;
+    if (local_counts) local_counts[q] = 0;
+  }
   if (fail) return;
   __syncwarp();
   const int64_t p0 = pos_indptr[q], np = pos_indptr[q + 1] - p0;
@@ -833,7 +867,10 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
   }
   __syncwarp();
   if (nr > rcap) {  // pathological score ties: the exact fallback
-    if (lane == 0) flags[q] = 1;
+    if (lane == 0) {
+      flags[q] = 1;
+      if (local_counts) local_counts[q] = 0;
+    }
     return;
   }
   uint64_t* X = R;
@@ -851,13 +888,21 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(const uint64_t* 
     if (v && np > 0 && sorted_contains(Pp, np, key_id(v))) X[e] = v = 0ull;
     valid += v != 0ull;
   }
-  fail = warp_sum(valid) < k;
-  if (lane == 0) flags[q] = fail ? 1 : 0;
+  // local (label-sharded, global threshold): fewer than k here is normal —
+  // the shards' counts decide globally which queries need the verify pass
+  const int nvalid = warp_sum(valid);
+  fail = !local_counts && nvalid < k;
+  if (lane == 0) {
+    flags[q] = fail ? 1 : 0;
+    if (local_counts) local_counts[q] = nvalid < k ? nvalid : k;
+  }
   if (fail) return;
   __syncwarp();
   int Pn = 1;
   while (Pn < n) Pn <<= 1;
-  for (int e = n + lane; e < Pn; e += 32) X[e] = 0ull;
+  // zero-pad to the sort width and (local mode: fewer than k candidates is
+  // normal) to the k keys written out; R holds rcap >= 2k entries
+  for (int e = n + lane; e < (Pn > k ? Pn : k); e += 32) X[e] = 0ull;
   __syncwarp();
   for (int size = 2; size <= Pn; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -1204,10 +1249,65 @@ struct StageProf {
   }
 };
 
+// Stages of the label-sharded BF16 candidate pass (engine._refresh_sharded):
+//  1 = the sample pass only, this shard's top-j sampled group maxima per query;
+//  2 = the threshold pass with the caller's (global) per-query thresholds and
+//      a local select (counts of non-positive candidates kept, overflow flags,
+//      no verify);
+//  3 = the verify pass for the caller's (global) flags, into out_keys.
+struct ShardStage {
+  int stage = 0;
+  uint32_t* sample_top = nullptr;
+  const uint64_t* tau_ext = nullptr;
+  int32_t* counts = nullptr;
+  int32_t* flags_out = nullptr;
+  const int32_t* flags_in = nullptr;
+};
+
+int refresh_impl(const float* qf, const uint16_t* qb_in, int64_t nq, int d, const float* wf, const uint16_t* wb,
+                 const uint8_t* w8, int64_t L, int64_t off, const int64_t* pos_indptr, const int32_t* pos_ids, int k,
+                 int mode, uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* ws, size_t ws_bytes,
+                 cudaStream_t st, const ShardStage& ss);
+
 int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, const float* wf, const uint16_t* wb,
                  const uint8_t* w8, int64_t L, int64_t off, const int64_t* pos_indptr, const int32_t* pos_ids, int k,
                  int mode, uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* ws, size_t ws_bytes,
                  cudaStream_t st) {
+  return refresh_impl(qf, qb_in, nq, d, wf, wb, w8, L, off, pos_indptr, pos_ids, k, mode, out_keys, out_ids,
+                      out_scores, ws, ws_bytes, st, ShardStage());
+}
+
+// j of the sharded sample statistics (0: this shape does not run the two-pass plan)
+int refresh_plan_j(int64_t nq, int64_t L, int d, int k) {
+  RefreshWs w;
+  int n_parts, kk;
+  TwoPass tp;
+  (void)carve_refresh(nullptr, 0, nq, L, d, k, ASTRA_REFRESH_BF16, &w, &n_parts, &kk, &tp);
+  return tp.on ? tp.j : 0;
+}
+
+int refresh_sharded_stage(int stage, const float* qf, const uint16_t* qb, int64_t nq, int d, const uint16_t* wb,
+                          int64_t L, int64_t off, const int64_t* pos_indptr, const int32_t* pos_ids, int k,
+                          uint32_t* sample_top, const uint64_t* tau_keys, uint64_t* io_keys, int32_t* counts,
+                          int32_t* flags, void* ws, size_t ws_bytes, cudaStream_t st) {
+  ShardStage ss;
+  ss.stage = stage;
+  ss.sample_top = sample_top;
+  ss.tau_ext = tau_keys;
+  ss.counts = counts;
+  if (stage == 2) ss.flags_out = flags;
+  if (stage == 3) ss.flags_in = flags;
+  if ((stage == 1 && !sample_top) || (stage == 2 && (!tau_keys || !counts || !flags || !io_keys)) ||
+      (stage == 3 && (!flags || !io_keys)) || stage < 1 || stage > 3)
+    return set_error(ASTRA_ERR_CONFIG, "sharded refresh stage %d: bad arguments", stage);
+  return refresh_impl(qf, qb, nq, d, nullptr, wb, nullptr, L, off, pos_indptr, pos_ids, k, ASTRA_REFRESH_BF16,
+                      io_keys, nullptr, nullptr, ws, ws_bytes, st, ss);
+}
+
+int refresh_impl(const float* qf, const uint16_t* qb_in, int64_t nq, int d, const float* wf, const uint16_t* wb,
+                 const uint8_t* w8, int64_t L, int64_t off, const int64_t* pos_indptr, const int32_t* pos_ids, int k,
+                 int mode, uint64_t* out_keys, int32_t* out_ids, float* out_scores, void* ws, size_t ws_bytes,
+                 cudaStream_t st, const ShardStage& ss) {
   if (k < 1 || k > 2048) return set_error(ASTRA_ERR_CONFIG, "refresh: k=%d outside [1, 2048]", k);
   if (nq < 0 || L < 0 || d <= 0) return set_error(ASTRA_ERR_CONFIG, "refresh: bad shape");
   if (L + off >= (int64_t(1) << 31)) return set_error(ASTRA_ERR_CONFIG, "refresh: label ids exceed int32");
@@ -1291,19 +1391,59 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
     p.bufs = w.bufs;
     p.part_keys = w.part_keys;
     p.gtau = w.gtau;
+    if (ss.stage != 0 && !tp.on)
+      return set_error(ASTRA_ERR_CONFIG, "sharded refresh stage %d needs the two-pass plan", ss.stage);
+    // 4. verify: the exact running top-k for the flagged queries only,
+    //    gathered to the front of a compact query buffer (their number stays
+    //    on the device): a handful of flagged queries costs one query-tile
+    //    pair's sweep spread over kVerifyParts label parts, not the full
+    //    tiles they sit in
+    auto verify_pass = [&](const int32_t* vflags) -> int {
+      // (near zero unless a query was flagged: bench.py reports it per refresh)
+      KernelTimer kt("refresh_verify", st);
+      compact_flagged_kernel<<<1, 1024, 0, st>>>(vflags, nq, w.qmap, w.n_flagged);
+      ASTRA_LAUNCHED("compact_flagged");
+      const int64_t row_bytes = f8 ? d : static_cast<int64_t>(d) * 2;
+      gather_rows_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char*>(qb), row_bytes,
+                                                                    w.qmap, w.n_flagged,
+                                                                    static_cast<unsigned char*>(w.qc));
+      ASTRA_LAUNCHED("gather_rows");
+      TcLaunch v = p;
+      v.qb = w.qc;
+      v.k = kk;
+      v.cap = cap;
+      v.part_keys = w.vpart_keys;
+      v.qmap = w.qmap;
+      v.n_active = w.n_flagged;
+      v.n_parts_fixed = kVerifyParts;
+      ASTRA_TRY(launch_refresh_tc(v, st));
+      const int vparts = static_cast<int>(std::min<int64_t>(kVerifyParts, (L + kTcTileLabels - 1) / kTcTileLabels));
+      return topk_merge_compact(w.vpart_keys, nq, vparts, kk, o_keys, o_ids, o_scores, w.qmap, w.n_flagged, st);
+    };
+    if (tp.on && ss.stage == 3) return verify_pass(ss.flags_in);  // (the sharded verify stage: flags given)
     if (tp.on) {
       // 1. sample pass: group maxima of every stride-th label tile, threshold
-      TcLaunch s = p;
-      s.tile_stride = tp.stride;
-      s.gmax = w.gmax;
-      prof.mark("to_bf16");
-      ASTRA_TRY(launch_refresh_tc(s, st));
-      prof.mark("sample");
-      tau_select_kernel<<<static_cast<unsigned>((nq + 7) / 8), 256, 0, st>>>(w.gmax, nq, tp.n_groups, tp.j, w.tau_keys);
-      ASTRA_LAUNCHED("tau_select");
+      //    (sharded stage 2: the threshold comes from the caller)
+      if (ss.stage != 2) {
+        TcLaunch s = p;
+        s.tile_stride = tp.stride;
+        s.gmax = w.gmax;
+        prof.mark("to_bf16");
+        ASTRA_TRY(launch_refresh_tc(s, st));
+        prof.mark("sample");
+        if (ss.stage == 1) {  // the shard's top-j sampled group maxima per query, for the owners
+          sample_top_kernel<<<static_cast<unsigned>((nq + 7) / 8), 256, 0, st>>>(w.gmax, nq, tp.n_groups, tp.j,
+                                                                                 ss.sample_top);
+          ASTRA_LAUNCHED("sample_top");
+          return ASTRA_OK;
+        }
+        tau_select_kernel<<<static_cast<unsigned>((nq + 7) / 8), 256, 0, st>>>(w.gmax, nq, tp.n_groups, tp.j,
+                                                                               w.tau_keys);
+        ASTRA_LAUNCHED("tau_select");
+      }
       // 2. threshold pass over every label
       TcLaunch f = p;
-      f.tau_in = w.tau_keys;
+      f.tau_in = ss.stage == 2 ? ss.tau_ext : w.tau_keys;
       f.tau_stride = 1;
       f.cand = w.cand;
       f.cand_cnt = w.cand_cnt;
@@ -1320,36 +1460,11 @@ int refresh_topk(const float* qf, const uint16_t* qb_in, int64_t nq, int d, cons
       cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       select_kernel<<<static_cast<unsigned>((nq + kSelWarps - 1) / kSelWarps), kSelWarps * 32, smem, st>>>(
           w.cand, w.cand_cnt, n_parts, tp.cand_cap, nq, pos_indptr, pos_ids, kk, tp.sel_max, rcap, o_keys, o_ids,
-          o_scores, w.flags);
+          o_scores, ss.stage == 2 ? ss.flags_out : w.flags, ss.stage == 2 ? ss.counts : nullptr);
       ASTRA_LAUNCHED("select");
-      // 4. verify: the exact running top-k for the flagged queries only,
-      //    gathered to the front of a compact query buffer (their number stays
-      //    on the device): a handful of flagged queries costs one query-tile
-      //    pair's sweep spread over kVerifyParts label parts, not the full
-      //    tiles they sit in
+      if (ss.stage == 2) return ASTRA_OK;  // (the owners decide which queries to verify)
       prof.mark("select");
-      {
-        // (near zero unless a query was flagged: bench.py reports it per refresh)
-        KernelTimer kt("refresh_verify", st);
-        compact_flagged_kernel<<<1, 1024, 0, st>>>(w.flags, nq, w.qmap, w.n_flagged);
-        ASTRA_LAUNCHED("compact_flagged");
-        const int64_t row_bytes = f8 ? d : static_cast<int64_t>(d) * 2;
-        gather_rows_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char*>(qb), row_bytes,
-                                                                      w.qmap, w.n_flagged,
-                                                                      static_cast<unsigned char*>(w.qc));
-        ASTRA_LAUNCHED("gather_rows");
-        TcLaunch v = p;
-        v.qb = w.qc;
-        v.k = kk;
-        v.cap = cap;
-        v.part_keys = w.vpart_keys;
-        v.qmap = w.qmap;
-        v.n_active = w.n_flagged;
-        v.n_parts_fixed = kVerifyParts;
-        ASTRA_TRY(launch_refresh_tc(v, st));
-        const int vparts = static_cast<int>(std::min<int64_t>(kVerifyParts, (L + kTcTileLabels - 1) / kTcTileLabels));
-        ASTRA_TRY(topk_merge_compact(w.vpart_keys, nq, vparts, kk, o_keys, o_ids, o_scores, w.qmap, w.n_flagged, st));
-      }
+      ASTRA_TRY(verify_pass(w.flags));
       prof.mark("verify");
     } else {
       p.k = kk;

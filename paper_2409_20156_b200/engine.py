@@ -81,6 +81,11 @@ class ClassifierEngine:
         # global k'-th bf16 key (_refresh_sharded_rerank); False: every shard
         # re-ranks its full local top-k'
         self.global_rerank_threshold = True
+        # ... and its bf16 candidate pass with a global threshold from the
+        # shards' sample statistics (_candidates_global); False: each shard
+        # finds its own top-k' candidates
+        self.global_candidate_threshold = True
+        self._shard_plan = {}
 
     # ------------------------------------------------------------ snapshot
     def snapshot(self, epoch: int = 0, check_finite: bool = True) -> None:
@@ -137,8 +142,12 @@ class ClassifierEngine:
         the single-GPU BF16_RERANK result, with the fp32 re-rank work no longer
         growing with the world size."""
         kc = self.ops.rerank_candidates_count(k)
-        ckeys, _, _ = self.ops.refresh_topk(q_all, ip_all, pid_all, kc, "bf16", labels_f32=self.snap_f32,
-                                            labels_bf16=self.snap_bf16, label_offset=self.lo)
+        j = self._sharded_plan_j(q_all.shape[0], kc) if self.global_candidate_threshold else 0
+        if j > 0:
+            ckeys = self._candidates_global(q_all, ip_all, pid_all, kc, j)
+        else:
+            ckeys, _, _ = self.ops.refresh_topk(q_all, ip_all, pid_all, kc, "bf16", labels_f32=self.snap_f32,
+                                                labels_bf16=self.snap_bf16, label_offset=self.lo)
         merged, _, _ = self.ops.topk_merge(self.comm.all_to_all(ckeys), kc)  # [B, kc]: this rank's rows
         tau_all = self.comm.all_gather(merged[:, kc - 1].contiguous())     # [world*B]; 0: fewer than k' exist
         flip = torch.tensor(-(2 ** 63), dtype=torch.int64, device=ckeys.device)  # unsigned order of the keys
@@ -149,6 +158,42 @@ class ClassifierEngine:
                                                  label_offset=self.lo)
         _, ids, scores = self.ops.topk_merge(self.comm.all_to_all(fkeys), k)
         return ids, scores
+
+    def _sharded_plan_j(self, nq_all: int, kc: int) -> int:
+        """j of the sharded candidate pass's sample statistics, agreed by every
+        rank (0: some shard's shape does not run the two-pass plan, so all take
+        the per-shard candidate pass). One collective per shape, cached."""
+        key = (nq_all, kc)
+        if key not in self._shard_plan:
+            j = int(self.ops.refresh_plan_j(nq_all, self.hi - self.lo, self.dim, kc))
+            t = torch.tensor([j, -j], dtype=torch.int64, device=self.device)
+            self.comm.all_reduce(t, op="min")
+            jmin, jmax = int(t[0]), -int(t[1])
+            self._shard_plan[key] = jmin if jmin == jmax and jmin > 0 else 0
+        return self._shard_plan[key]
+
+    def _candidates_global(self, q_all, ip_all, pid_all, kc, j):
+        """The shard's bf16 candidates (top-k' of its labels that can be in the
+        global top-k', positives excluded) with a GLOBAL threshold: the rows'
+        owners take the j-th largest sampled group maximum over all shards'
+        sample statistics (so the threshold pass appends ~k'/world candidates
+        per query per shard instead of ~k'), sum the shards' candidate counts
+        and send back which queries lack k' candidates globally (or overflowed
+        a list); those run the exact verify pass on every shard. The union of
+        the shards' lists contains the global top-k' for every query."""
+        ops, comm = self.ops, self.comm
+        B = q_all.shape[0] // comm.world
+        top = ops.refresh_sharded_stage(1, q_all, ip_all, pid_all, kc, self.snap_bf16, label_offset=self.lo)
+        mine = comm.all_to_all(top.to(torch.int64) & 0xFFFFFFFF)            # [world, B, j]
+        gj = mine.permute(1, 0, 2).reshape(B, -1).topk(j, dim=1).values[:, j - 1]
+        tau_all = comm.all_gather(gj << 32)                                  # [world*B] key form
+        keys, counts, oflow = ops.refresh_sharded_stage(2, q_all, ip_all, pid_all, kc, self.snap_bf16,
+                                                        label_offset=self.lo, tau_keys=tau_all)
+        cnt = comm.all_to_all(counts.to(torch.int64)).sum(0)                 # [B]
+        ovf = comm.all_to_all(oflow.to(torch.int64)).amax(0)
+        need = comm.all_gather(((cnt < kc) | (ovf > 0)).to(torch.int32))    # [world*B]
+        return ops.refresh_sharded_stage(3, q_all, ip_all, pid_all, kc, self.snap_bf16, label_offset=self.lo,
+                                         io_keys=keys, flags=need)
 
     def refresh_cache(self, queries: torch.Tensor, pos_indptr: torch.Tensor, pos_ids: torch.Tensor,
                       mode: str | None = None):

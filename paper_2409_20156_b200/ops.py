@@ -116,6 +116,57 @@ def refresh_topk(queries, pos_indptr, pos_ids, k, mode="bf16_rerank", labels_f32
     return keys, ids, scores
 
 
+def refresh_plan_j(nq, n_labels, d, k) -> int:
+    """j of the label-sharded candidate pass's sample statistics for nq
+    queries over n_labels labels and k' = k candidates (0: the shape does not
+    run the two-pass plan)."""
+    return int(_lib.load().astra_refresh_plan_j(nq, n_labels, d, k))
+
+
+def refresh_sharded_stage(stage, queries, pos_indptr, pos_ids, k, labels_bf16, label_offset=0, tau_keys=None,
+                          io_keys=None, flags=None):
+    """One stage of the label-sharded BF16 candidate pass (astra_refresh_sharded_stage):
+    1 -> sample_top [nq, j] int32 (orderable score bits of the shard's j largest
+         sampled group maxima per query);
+    2 -> (keys [nq, k] int64, counts [nq] int32, overflow flags [nq] int32) for
+         the global thresholds tau_keys [nq] int64;
+    3 -> io_keys rows of the flagged queries (flags [nq] int32) replaced by the
+         shard's exact top-k (in place); returns io_keys."""
+    _cuda(queries, torch.float32, "queries")
+    _cuda(labels_bf16, torch.bfloat16, "labels_bf16")
+    _cuda(pos_indptr, torch.int64, "pos_indptr")
+    _cuda(pos_ids, torch.int32, "pos_ids")
+    nq, d = queries.shape
+    L = labels_bf16.shape[0]
+    lib = _lib.load()
+    mode = refresh_mode("bf16")
+    dev = queries.device
+    ws = WORKSPACES.get("refresh", lib.astra_refresh_workspace_size(nq, L, d, k, mode), dev)
+    top = keys = counts = None
+    if stage == 1:
+        j = refresh_plan_j(nq, L, d, k)
+        if j <= 0:
+            raise ConfigError("sharded refresh: this shape does not run the two-pass plan")
+        top = torch.empty((nq, j), dtype=torch.int32, device=dev)
+    elif stage == 2:
+        _cuda(tau_keys, torch.int64, "tau_keys")
+        keys = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        counts = torch.empty(nq, dtype=torch.int32, device=dev)
+        flags = torch.empty(nq, dtype=torch.int32, device=dev)
+    else:
+        _cuda(flags, torch.int32, "flags")
+        _cuda(io_keys, torch.int64, "io_keys")
+        keys = io_keys
+    _lib.check(lib.astra_refresh_sharded_stage(
+        stage, _p(queries), None, nq, d, _p(labels_bf16), L, label_offset, _p(pos_indptr), _p(pos_ids), k, _p(top),
+        _p(tau_keys), _p(keys), _p(counts), _p(flags), _p(ws), ws.numel(), _stream()))
+    if stage == 1:
+        return top
+    if stage == 2:
+        return keys, counts, flags
+    return keys
+
+
 def rerank_candidates_count(k: int) -> int:
     """k' of the BF16_RERANK candidate pass for a final top-k: max(1.5k, k+16)
     rounded up to 8, <= 2048 (refresh.cu rerank_candidates)."""

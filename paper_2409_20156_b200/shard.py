@@ -86,9 +86,10 @@ class Comm:
         dist.all_to_all_single(out, t, group=self.group)
         return out.view((self.world, t.shape[0] // self.world) + tuple(t.shape[1:]))
 
-    def all_reduce(self, t: torch.Tensor) -> torch.Tensor:
+    def all_reduce(self, t: torch.Tensor, op: str = "sum") -> torch.Tensor:
         if self.world > 1:
-            dist.all_reduce(t, group=self.group)
+            dist.all_reduce(t, op={"sum": dist.ReduceOp.SUM, "min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX}[op],
+                            group=self.group)
         return t
 
     def barrier(self):

@@ -69,6 +69,70 @@ def rerank_candidates(queries, cand_keys, k, labels_f32=None, labels_bf16=None, 
     return torch.from_numpy(out.view(np.int64)), torch.from_numpy(ids), torch.from_numpy(scores)
 
 
+# The label-sharded candidate pass (stand-ins with the GPU stages' contract:
+# the sample statistics are the maxima of 64-label groups of every 2nd
+# 256-label tile of the shard, j = 3; candidates are the non-positive labels at
+# or above the given threshold; the verify pass is the exact local top-k).
+_SHARD_J = 3
+
+
+def refresh_plan_j(nq, n_labels, d, k):
+    return _SHARD_J
+
+
+def _bf16_keys(queries, labels_bf16, pos_indptr, pos_ids, label_offset, exclude_pos):
+    """[nq, L] uint64 keys of the bf16-operand scores (0 for excluded positives)."""
+    Q = _bf16_f32(queries)
+    W = _np(labels_bf16.float())
+    nq, L = Q.shape[0], W.shape[0]
+    keys = _exact_keys(Q, W, label_offset)
+    if exclude_pos:
+        ip, pid = _np(pos_indptr), _np(pos_ids)
+        for q in range(nq):
+            loc = pid[ip[q]:ip[q + 1]].astype(np.int64) - label_offset
+            loc = loc[(loc >= 0) & (loc < L)]
+            keys[q, loc] = 0
+    return keys
+
+
+def refresh_sharded_stage(stage, queries, pos_indptr, pos_ids, k, labels_bf16, label_offset=0, tau_keys=None,
+                          io_keys=None, flags=None):
+    L = labels_bf16.shape[0]
+    if stage == 1:
+        keys = _bf16_keys(queries, labels_bf16, pos_indptr, pos_ids, label_offset, False)
+        ords = (keys >> np.uint64(32)).astype(np.uint32)
+        gm = []
+        for t0 in range(0, L, 512):  # every 2nd 256-label tile
+            for g0 in range(t0, min(t0 + 256, L), 64):
+                gm.append(ords[:, g0:min(g0 + 64, L)].max(axis=1))
+        gm = np.stack(gm, axis=1)
+        top = -np.sort(-gm.astype(np.int64), axis=1)[:, :_SHARD_J]
+        if top.shape[1] < _SHARD_J:
+            top = np.pad(top, ((0, 0), (0, _SHARD_J - top.shape[1])))
+        return torch.from_numpy(top.astype(np.uint32).view(np.int32))
+    keys = _bf16_keys(queries, labels_bf16, pos_indptr, pos_ids, label_offset, True)
+    nq = keys.shape[0]
+    if stage == 2:
+        tau = _np(tau_keys).view(np.uint64)
+        out = np.zeros((nq, k), np.uint64)
+        counts = np.zeros(nq, np.int32)
+        for q in range(nq):
+            c = keys[q][keys[q] >= max(tau[q], np.uint64(1))]
+            c = np.sort(c)[::-1][:k]
+            out[q, : len(c)] = c
+            counts[q] = len(c)
+        return torch.from_numpy(out.view(np.int64)), torch.from_numpy(counts), torch.zeros(nq, dtype=torch.int32)
+    out = _np(io_keys).view(np.uint64).copy()
+    fl = _np(flags)
+    for q in range(nq):
+        if fl[q]:
+            c = np.sort(keys[q][keys[q] > 0])[::-1][:k]
+            out[q] = 0
+            out[q, : len(c)] = c
+    io_keys.copy_(torch.from_numpy(out.view(np.int64)))
+    return io_keys
+
+
 def refresh_topk(queries, pos_indptr, pos_ids, k, mode="fp32", labels_f32=None, labels_bf16=None, label_offset=0,
                  queries_bf16=None, n_labels=None, labels_e4m3=None):
     """fp32: the C oracle. bf16 / bf16_rerank (stand-ins with the GPU modes'

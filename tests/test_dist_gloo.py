@@ -151,7 +151,7 @@ def test_comm_collective_semantics():
         np.testing.assert_array_equal(res[r]["gids"], np.concatenate([np.arange(q + 3) + 100 * q for q in range(world)]))
 
 
-def _rerank_worker(rank, world, port, out_dir, global_threshold):
+def _rerank_worker(rank, world, port, out_dir, global_threshold, global_candidates=False):
     sys.path[:0] = [ROOT, HERE]
     import oracle_backend
     from paper_2409_20156_b200.engine import ClassifierEngine
@@ -162,6 +162,7 @@ def _rerank_worker(rank, world, port, out_dir, global_threshold):
     eng = ClassifierEngine(L, D, k_p=K_P, k_h=K_H, k_r=K_R, weights=W, refresh_mode="bf16_rerank", seed=5,
                            device="cpu", backend=oracle_backend)
     eng.global_rerank_threshold = global_threshold
+    eng.global_candidate_threshold = global_candidates
     eng.snapshot(0)
     emb, pos, _ = data[rank]
     ip, pid = _csr(pos)
@@ -170,8 +171,9 @@ def _rerank_worker(rank, world, port, out_dir, global_threshold):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,global_threshold", [(2, True), (3, True), (2, False)])
-def test_sharded_bf16_rerank_matches_single_process(world, global_threshold):
+@pytest.mark.parametrize("world,global_threshold,global_candidates",
+                         [(2, True, False), (3, True, False), (2, False, False), (2, True, True), (3, True, True)])
+def test_sharded_bf16_rerank_matches_single_process(world, global_threshold, global_candidates):
     """BF16_RERANK over label shards (engine._refresh_sharded_rerank: shard
     bf16 top-k' -> owners merge -> global k'-th key tau -> each shard re-ranks
     only its candidates >= tau -> fp32 lists merged) returns the single-process
@@ -181,8 +183,8 @@ def test_sharded_bf16_rerank_matches_single_process(world, global_threshold):
     from paper_2409_20156_b200.engine import ClassifierEngine
 
     with tempfile.TemporaryDirectory() as tmp:
-        mp.start_processes(_rerank_worker, args=(world, _free_port(), tmp, global_threshold), nprocs=world, join=True,
-                           start_method="spawn")
+        mp.start_processes(_rerank_worker, args=(world, _free_port(), tmp, global_threshold, global_candidates),
+                           nprocs=world, join=True, start_method="spawn")
         res = [dict(np.load(os.path.join(tmp, f"rr{r}.npz"))) for r in range(world)]
     W, data = _data(seed=4, world=world)
     one = ClassifierEngine(L, D, k_p=K_P, k_h=K_H, k_r=K_R, weights=W, refresh_mode="bf16_rerank", seed=5,

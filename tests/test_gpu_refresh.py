@@ -328,8 +328,8 @@ def test_rerank_candidates_matches_oracle(cuda_lib):
     np.testing.assert_array_equal(ids.cpu().numpy(), want_ids.numpy())
 
 
-@pytest.mark.parametrize("n_shards", [2, 3])
-def test_sharded_rerank_composition_equals_one_gpu(cuda_lib, n_shards):
+@pytest.mark.parametrize("n_shards,global_candidates", [(2, False), (3, False), (2, True), (3, True)])
+def test_sharded_rerank_composition_equals_one_gpu(cuda_lib, n_shards, global_candidates):
     """engine._refresh_sharded_rerank's composition on CUDA with the label
     range split into shards on one device: each shard's bf16 top-k', the
     owner's merge -> the global k'-th key tau, each shard's fp32 re-rank of
@@ -339,7 +339,7 @@ def test_sharded_rerank_composition_equals_one_gpu(cuda_lib, n_shards):
     from paper_2409_20156_b200.shard import shard_range
 
     rng = np.random.default_rng(5)
-    L, d, nq, k = 300_000, 256, 512, 48
+    L, d, nq, k = 600_000, 256, 512, 48
     W = torch.from_numpy((rng.standard_normal((L, d)) / 16).astype(np.float32)).cuda()
     Wb = ops.f32_to_bf16(W)
     E = torch.from_numpy(rng.standard_normal((nq, d)).astype(np.float32)).cuda()
@@ -349,8 +349,27 @@ def test_sharded_rerank_composition_equals_one_gpu(cuda_lib, n_shards):
     want, want_ids, _ = ops.refresh_topk(E, ip, pid, k, "bf16_rerank", labels_f32=W, labels_bf16=Wb)
     kc = ops.rerank_candidates_count(k)
     ranges = [shard_range(L, r, n_shards) for r in range(n_shards)]
-    ck = [ops.refresh_topk(E, ip, pid, kc, "bf16", labels_f32=W[lo:hi].contiguous(),
-                           labels_bf16=Wb[lo:hi].contiguous(), label_offset=lo)[0] for lo, hi in ranges]
+    if global_candidates:
+        # engine._candidates_global: the shards' sample statistics -> the global
+        # j-th largest group maximum -> local candidates at or above it -> the
+        # summed counts / overflow flags -> the verify pass on every shard
+        j = ops.refresh_plan_j(nq, min(hi - lo for lo, hi in ranges), d, kc)
+        assert j > 0
+        tops = [ops.refresh_sharded_stage(1, E, ip, pid, kc, Wb[lo:hi].contiguous(), label_offset=lo)
+                for lo, hi in ranges]
+        allv = torch.cat([t.to(torch.int64) & 0xFFFFFFFF for t in tops], dim=1)
+        tau = allv.topk(j, dim=1).values[:, j - 1] << 32
+        st2 = [ops.refresh_sharded_stage(2, E, ip, pid, kc, Wb[lo:hi].contiguous(), label_offset=lo, tau_keys=tau)
+               for lo, hi in ranges]
+        cnt = sum(c.to(torch.int64) for _, c, _ in st2)
+        ovf = torch.stack([f for _, _, f in st2]).amax(0)
+        need = ((cnt < kc) | (ovf > 0)).to(torch.int32)
+        ck = [ops.refresh_sharded_stage(3, E, ip, pid, kc, Wb[lo:hi].contiguous(), label_offset=lo, io_keys=keys,
+                                        flags=need) for (lo, hi), (keys, _, _) in zip(ranges, st2)]
+        print(f"[sharded global candidates] {int(need.sum())} of {nq} queries verified")
+    else:
+        ck = [ops.refresh_topk(E, ip, pid, kc, "bf16", labels_f32=W[lo:hi].contiguous(),
+                               labels_bf16=Wb[lo:hi].contiguous(), label_offset=lo)[0] for lo, hi in ranges]
     merged, _, _ = ops.topk_merge(torch.stack(ck), kc)
     tau = merged[:, kc - 1]
     flip = torch.tensor(-(2 ** 63), dtype=torch.int64, device="cuda")
