@@ -86,20 +86,41 @@ class ClassifierEngine:
         # finds its own top-k' candidates
         self.global_candidate_threshold = True
         self._shard_plan = {}
+        # cross-rank reduction of grad_emb and the loss in step(): "collective"
+        # = reduce_scatter / all_reduce (NCCL's order); "ordered" = every
+        # rank's partials sent to the rows' owners (all_to_all) and summed in
+        # rank order 0..G-1, so with astra_set_step_deterministic(1) a sharded
+        # run is bitwise reproducible (SURVEY §8e's fixed-order option)
+        self.grad_reduce = "collective"
+        # W writes since construction; an aliased snapshot (snapshot(copy=False))
+        # is valid only while this matches the value it was taken at
+        self._w_version = 0
+        self._snap_alias_version = None
 
     # ------------------------------------------------------------ snapshot
-    def snapshot(self, epoch: int = 0, check_finite: bool = True) -> None:
-        """Immutable copy of the shard for the refresh (anns.py:90-100)."""
+    def snapshot(self, epoch: int = 0, check_finite: bool = True, copy: bool = True) -> None:
+        """Immutable copy of the shard for the refresh (anns.py:90-100).
+
+        copy=False is the synchronous-refresh form: the snapshot
+        aliases the live W instead of copying it (no 4 GB fp32 copy at C4, no
+        23 GB bf16 copy on a C5 shard; the tensor-core copy is still built when
+        W is fp32), for a caller that runs every refresh of this snapshot
+        before the next update. refresh() raises ConfigError once W has been
+        written after an aliased snapshot."""
         if check_finite and not bool(torch.isfinite(self.W).all()):
             raise NumericalError("non-finite vectors in index build")
         fp8 = self.refresh_mode == "fp8_rerank"
+        self._snap_alias_version = None if copy else self._w_version
         if self.W.dtype == torch.bfloat16 and self.refresh_mode != "fp32":
             # bf16 W: the bf16 copy is the whole snapshot (the re-rank scores its
             # values exactly); no fp32 copy (46 GB for a 15M-label shard)
             self.snap_f32 = None
-            self.snap_bf16 = self.W.clone()
+            self.snap_bf16 = self.W.clone() if copy else self.W
         else:
-            self.snap_f32 = self.W.float().clone() if self.W.dtype != torch.float32 else self.W.clone()
+            if self.W.dtype != torch.float32:
+                self.snap_f32 = self.W.float()
+            else:
+                self.snap_f32 = self.W.clone() if copy else self.W
             self.snap_bf16 = (self.ops.f32_to_bf16(self.snap_f32) if self.refresh_mode in ("bf16", "bf16_rerank")
                               else None)
         # e4m3 candidate-pass snapshot (FP8_RERANK: the re-rank reads the fp32 / bf16 copy above)
@@ -114,6 +135,8 @@ class ClassifierEngine:
         positives excluded. Collective when world_size > 1."""
         if self.snap_f32 is None and self.snap_bf16 is None:
             raise ConfigError("refresh before snapshot()")
+        if self._snap_alias_version is not None and self._snap_alias_version != self._w_version:
+            raise ConfigError("W was updated after an aliased snapshot(copy=False); take a new snapshot")
         mode = mode or self.refresh_mode
         B = queries.shape[0]
         q_all = self.comm.all_gather(queries)
@@ -256,12 +279,17 @@ class ClassifierEngine:
         keep_all = self.comm.all_gather(keep) if keep is not None else None
         if self.optimizer == "adam":
             self.adam_step += 1
+        self._w_version += 1
         res = self.ops.slate_step(
             emb_all, ids, y, origin, weights, self.W, lr, weight_decay, keep=keep_all, factors_in=factors_in,
             optimizer=self.optimizer, adam_m=self.m, adam_v=self.v, adam_step=max(self.adam_step, 1),
             betas=self.betas, eps=self.eps, label_offset=self.lo, w_absmax=self.w_absmax)
-        grad_emb = self.comm.reduce_scatter(res.grad_emb)
-        loss = self.comm.all_reduce(res.loss_dev)
+        if self.grad_reduce == "ordered" and self.comm.world > 1:
+            grad_emb = _sum_in_rank_order(self.comm.all_to_all(res.grad_emb))
+            loss = _sum_in_rank_order(self.comm.all_gather_stack(res.loss_dev))
+        else:
+            grad_emb = self.comm.reduce_scatter(res.grad_emb)
+            loss = self.comm.all_reduce(res.loss_dev)
         status = self.comm.all_reduce(res.status)
         return loss, grad_emb, status
 
@@ -405,6 +433,7 @@ class ClassifierEngine:
                 raise DataError("truncated shard checkpoint")
             arr = np.frombuffer(buf, dtype=np.int16 if bf16 else np.float32).reshape(rows, dim)
             t = torch.from_numpy(arr.copy())
+            self._w_version += 1
             self.W.copy_(t.view(torch.bfloat16) if bf16 else t)
             if adam:
                 for dst in (self.m, self.v):
@@ -474,6 +503,15 @@ class _HostPipe:
         with torch.cuda.stream(self.d2h):
             host_out.copy_(dev_tensor, non_blocking=True)
         dev_tensor.record_stream(self.d2h)
+
+
+def _sum_in_rank_order(parts: torch.Tensor) -> torch.Tensor:
+    """parts[0] + parts[1] + ... + parts[G-1], left to right (a fixed order,
+    unlike a collective's reduction tree)."""
+    acc = parts[0].clone()
+    for r in range(1, parts.shape[0]):
+        acc += parts[r]
+    return acc
 
 
 def h2d_bytes(*tensors) -> int:

@@ -43,7 +43,7 @@ def _csr(pos):
     return ip, np.concatenate(pos).astype(np.int32)
 
 
-def _worker(rank, world, port, out_dir, exchange="regenerate"):
+def _worker(rank, world, port, out_dir, exchange="regenerate", grad_reduce="collective"):
     sys.path[:0] = [ROOT, HERE]
     import oracle_backend
     from paper_2409_20156_b200.engine import ClassifierEngine
@@ -54,6 +54,20 @@ def _worker(rank, world, port, out_dir, exchange="regenerate"):
     eng = ClassifierEngine(L, D, k_p=K_P, k_h=K_H, k_r=K_R, weights=W, refresh_mode="fp32", seed=5, device="cpu",
                            backend=oracle_backend)
     eng.slate_exchange = exchange
+    eng.grad_reduce = grad_reduce
+    partial = {}
+    step_fn = oracle_backend.slate_step
+
+    def recording_step(*a, **kw):  # keep this shard's partial grad_emb / loss for the check
+        res = step_fn(*a, **kw)
+        partial.update(grad_emb=res.grad_emb.clone().numpy(), loss=res.loss_dev.clone().numpy())
+        return res
+
+    eng.ops = type("Ops", (), {})()
+    for name in dir(oracle_backend):
+        if not name.startswith("__"):
+            setattr(eng.ops, name, getattr(oracle_backend, name))
+    eng.ops.slate_step = recording_step
     eng.snapshot(0)
     emb, pos, rows = data[rank]
     ip, pid = _csr(pos)
@@ -61,7 +75,8 @@ def _worker(rank, world, port, out_dir, exchange="regenerate"):
     slates = eng.sample(torch.from_numpy(rows), torch.from_numpy(ip), torch.from_numpy(pid), ids, epoch=2, step=3)
     loss, grad_emb, status = eng.step(torch.from_numpy(emb), slates, 0.3, 1e-3)
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), ids=ids.numpy(), grad_emb=grad_emb.numpy(), loss=loss.numpy(),
-             status=status.numpy(), W=eng.W.numpy(), lo=eng.lo, hi=eng.hi, slate_ids=slates[0].numpy())
+             status=status.numpy(), W=eng.W.numpy(), lo=eng.lo, hi=eng.hi, slate_ids=slates[0].numpy(),
+             partial_grad=partial["grad_emb"], partial_loss=partial["loss"])
     dist.destroy_process_group()
 
 
@@ -71,15 +86,17 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,exchange", [(2, "regenerate"), (3, "regenerate"), (2, "gather")])
-def test_label_sharding_matches_single_process(world, exchange):
+@pytest.mark.parametrize("world,exchange,grad_reduce", [(2, "regenerate", "collective"), (3, "regenerate", "collective"),
+                                                       (2, "gather", "collective"), (2, "gather", "ordered"),
+                                                       (3, "regenerate", "ordered")])
+def test_label_sharding_matches_single_process(world, exchange, grad_reduce):
     sys.path[:0] = [HERE]
     import oracle_backend
     from oracle import c_oracle as co
     from paper_2409_20156_b200.engine import ClassifierEngine
 
     with tempfile.TemporaryDirectory() as tmp:
-        mp.start_processes(_worker, args=(world, _free_port(), tmp, exchange), nprocs=world, join=True,
+        mp.start_processes(_worker, args=(world, _free_port(), tmp, exchange, grad_reduce), nprocs=world, join=True,
                            start_method="spawn")
         res = [dict(np.load(os.path.join(tmp, f"r{r}.npz"))) for r in range(world)]
     W, data = _data(world=world)
@@ -110,6 +127,18 @@ def test_label_sharding_matches_single_process(world, exchange):
     assert abs(float(res[0]["loss"][0]) - float(loss[0])) <= 1e-9 * abs(float(loss[0]))
     assert all(float(res[0]["loss"][0]) == float(res[r]["loss"][0]) for r in range(world))
     assert not res[0]["status"].any() and not status.numpy().any()
+    if grad_reduce == "ordered":
+        # each rank's grad_emb rows and the loss are the shards' partials summed
+        # left to right in rank order (bitwise; independent of the collective)
+        for r in range(world):
+            acc = res[0]["partial_grad"][r * B : (r + 1) * B].copy()
+            for q in range(1, world):
+                acc += res[q]["partial_grad"][r * B : (r + 1) * B]
+            np.testing.assert_array_equal(res[r]["grad_emb"], acc)
+            lacc = res[0]["partial_loss"].copy()
+            for q in range(1, world):
+                lacc += res[q]["partial_loss"]
+            np.testing.assert_array_equal(res[r]["loss"], lacc)
 
 
 def _comm_worker(rank, world, port, out_dir):
