@@ -32,6 +32,7 @@ exact-fallback time (~0 when every query is proven exact).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -96,7 +97,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("ASTRA_BENCH_SMI_MS", "20")], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except FileNotFoundError:
@@ -360,6 +361,11 @@ def run_ours(args):
         for i in range(M):
             ph["sample"] += (e[1 if not overlap else 0] if i == 0 else e[1 + 2 * i]).elapsed_time(e[2 + 2 * i])
             ph["step"] += e[2 + 2 * i].elapsed_time(e[3 + 2 * i])
+    if os.environ.get("ASTRA_BENCH_PHASE_DUMP"):  # per-step sample intervals (host-stall diagnosis)
+        for t in range(args.warmup, n_steps):
+            e = ev[t]
+            print("step", t, "sample_ms", [round((e[1] if i == 0 else e[1 + 2 * i]).elapsed_time(e[2 + 2 * i]), 3)
+                                           for i in range(M)], file=sys.stderr)
     value = R * world * K / (ms_total / 1e3)
 
     # dominant kernel: the refresh GEMM pass (tcgen05 bf16 GEMM of the queries
@@ -1279,6 +1285,11 @@ def main():
     ap.add_argument("--slate-exchange", default="gather", choices=["gather", "regenerate"],
                     help="--emulate: how the N-GPU job shares slates (engine.ClassifierEngine.slate_exchange)")
     args = ap.parse_args()
+    # no cyclic-GC pauses inside the timed regions (a generation-2 collection
+    # takes 20-70 ms in this process and, at the short C1-C3 steps, starves the
+    # GPU; profiles/r02s3/stall_ab.txt); reference counting still frees memory
+    gc.collect()
+    gc.disable()
     REFRESH_MODE[0] = args.refresh_mode
     if args.config in CONFIGS:
         CFG.clear()

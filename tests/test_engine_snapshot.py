@@ -13,7 +13,7 @@ import oracle_backend
 from paper_2409_20156_b200.engine import ClassifierEngine
 from paper_2409_20156_b200.errors import ConfigError
 
-L, D, K_P, K_H, K_R, B = 700, 32, 2, 6, 12, 24
+L, D, K_P, K_H, K_R, B = 700, 128, 2, 6, 12, 24  # d % 128 == 0: the bf16 refresh and the single pass
 
 
 def _inputs(device, seed=0):
