@@ -1289,7 +1289,18 @@ def main():
     # takes 20-70 ms in this process and, at the short C1-C3 steps, starves the
     # GPU; profiles/r02s3/stall_ab.txt); reference counting still frees memory
     gc.collect()
-    gc.disable()
+    if os.environ.get("ASTRA_BENCH_GC"):  # diagnosis: keep GC on, log every collection's duration
+        _gc_t = {}
+
+        def _gc_log(phase, info):
+            if phase == "start":
+                _gc_t["t"] = time.perf_counter()
+            else:
+                print(f"gc gen{info['generation']} {1e3 * (time.perf_counter() - _gc_t['t']):.2f} ms", file=sys.stderr)
+
+        gc.callbacks.append(_gc_log)
+    else:
+        gc.disable()
     REFRESH_MODE[0] = args.refresh_mode
     if args.config in CONFIGS:
         CFG.clear()
