@@ -83,6 +83,16 @@ def peaks():
 
 
 # ------------------------------------------------------------------ clocks
+def _ev():
+    """A timing event whose CUDA event exists already (torch creates it lazily
+    at the first record; creation inside a timed region can stall the host)."""
+    import torch
+
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -276,7 +286,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * M + 2)] for _ in range(n_steps)]
+    ev = [[_ev() for _ in range(2 * M + 2)] for _ in range(n_steps)]
     ids_keep = []
 
     # the refresh of the step's rows runs on a side stream concurrently with the
@@ -288,6 +298,8 @@ def run_ours(args):
     if overlap:
         _lib.set_refresh_sm_budget(args.refresh_sms)
 
+    host_ts = [] if os.environ.get("ASTRA_BENCH_PHASE_DUMP") else None
+
     def one(t, timed, mode=None, reuse_start=False):
         st, e = dev[t], ev[t]
         if not reuse_start:
@@ -297,12 +309,12 @@ def run_ours(args):
             eng.refresh(st["chunk"]["emb"], st["chunk"]["indptr"], st["chunk"]["pos"], k_h, mode=mode)
             e[1].record(rstream)
         for i, m in enumerate(st["mbs"]):
+            if host_ts is not None and timed:
+                host_ts.append((t, i, time.perf_counter()))
             slates = eng.sample(m["rows"], m["indptr"], m["pos"], m["hard"], epoch=1, step=t * M + i)
             e[2 + 2 * i].record(stream)
             loss, grad_emb, status = eng.step(m["emb"], slates, CFG["lr"], CFG["wd"])
             e[3 + 2 * i].record(stream)
-            if timed and i == 0:
-                ids_keep.append(slates[0])
         stream.wait_stream(rstream)
         return loss, status
 
@@ -320,13 +332,14 @@ def run_ours(args):
     for name in ("refresh_gemm", "refresh_verify", "step_single", "slot_forward", "label_update"):
         _lib.kernel_timing(name)  # drop warm-up records
     _lib.kernel_timing_enable(True)
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
+    t_start = _ev()
+    t_end = _ev()
     # working sets that fit in L2 (C1: W is 2.5 MB) are flushed between timed
     # steps (a 512 MB write, outside the per-step events) so every step starts cold
     flush = L_loc * d * 4 * 3 < 256 * 2**20
     flush_buf = torch.empty(512 * 2**20, dtype=torch.uint8, device="cuda") if flush else None
-    ends = []
+    ends = [_ev() for _ in range(args.warmup, n_steps)] if flush else []
+    torch.cuda.synchronize()
     t_start.record(stream)
     for t in range(args.warmup, n_steps):
         if flush:
@@ -334,8 +347,7 @@ def run_ours(args):
             ev[t][0].record(stream)
         loss, status = one(t, True, reuse_start=flush)
         if flush:
-            ends.append(torch.cuda.Event(enable_timing=True))
-            ends[-1].record(stream)
+            ends[t - args.warmup].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
     eng.comm.barrier()
@@ -366,6 +378,9 @@ def run_ours(args):
             e = ev[t]
             print("step", t, "sample_ms", [round((e[1] if i == 0 else e[1 + 2 * i]).elapsed_time(e[2 + 2 * i]), 3)
                                            for i in range(M)], file=sys.stderr)
+        gaps = sorted(((b[2] - a_[2]) * 1e3, a_[0], a_[1]) for a_, b in zip(host_ts, host_ts[1:]))[-3:]
+        print("largest host gaps between sampler calls (ms, step, minibatch):", [(round(g, 2), t_, i_) for g, t_, i_ in gaps],
+              file=sys.stderr)
     value = R * world * K / (ms_total / 1e3)
 
     # dominant kernel: the refresh GEMM pass (tcgen05 bf16 GEMM of the queries
@@ -383,6 +398,13 @@ def run_ours(args):
         peak_kind_gemm = f"{peak_kind} burst bf16 (each launch is timed on its own)"
     t_ref = ph["refresh"] / K / 1e3
     # step roofline: BASELINE.md bytes formula (U unique rows, fp32 SGD: read+write)
+    # (the timed steps' first-minibatch slates, redrawn here: Philox keyed by
+    # (seed, epoch, step) gives the same ids; keeping them alive inside the
+    # timed region made the caching allocator cudaMalloc a new segment every
+    # ~8 steps, a 30-130 ms host stall, profiles/r02s3/stall_ab.txt)
+    for t in range(args.warmup, n_steps):
+        m = dev[t]["mbs"][0]
+        ids_keep.append(eng.sample(m["rows"], m["indptr"], m["pos"], m["hard"], epoch=1, step=t * M)[0])
     U = [int(torch.unique(ids[(ids >= eng.lo) & (ids < eng.hi)]).numel()) for ids in ids_keep]
     U_mean = sum(U) / len(U)
     step_bytes = U_mean * d * (2 * 4) + 2 * B * world * d * 4 + B * world * S * 5
@@ -433,7 +455,7 @@ def run_ours(args):
         eng.comm.barrier()
         _lib.kernel_timing("refresh_gemm")
         _lib.kernel_timing_enable(True)
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0, a1 = _ev(), _ev()
         a0.record(stream)
         for t in range(args.warmup, n_steps):
             one(t, False, mode="fp8_rerank")
@@ -488,8 +510,8 @@ def run_ours(args):
         one_host(t)
     torch.cuda.synchronize()
     eng.comm.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    e0 = _ev()
+    e1 = _ev()
     e0.record(stream)
     for t in range(args.warmup, n_steps):
         one_host(t)
@@ -614,7 +636,7 @@ def run_emulate(args):
     full = None if regen else [[slates_of(t, i, Bg) for i in range(M)] for t in range(n_steps)]
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3 + 2 * M)] for _ in range(n_steps)]
+    ev = [[_ev() for _ in range(3 + 2 * M)] for _ in range(n_steps)]
     keep_ids = []
 
     # BF16_RERANK over shards (engine._refresh_sharded_rerank): this shard's bf16
@@ -682,7 +704,7 @@ def run_emulate(args):
     _lib.kernel_timing_enable(True)
     clocks = ClockSampler(0)
     clocks.start()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0, t1 = _ev(), _ev()
     t0.record(stream)
     for t in range(args.warmup, n_steps):
         res = one(t, True)
@@ -823,7 +845,7 @@ def run_c5shard(args):
     data[0][4] = cache_of(data[0][3], data[0][1], data[0][2])  # the first step's stale cache
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_steps)]
+    ev = [[_ev() for _ in range(4)] for _ in range(n_steps)]
 
     def one(t):
         rows, ip, pid, emb, cache = data[t]
@@ -851,7 +873,7 @@ def run_c5shard(args):
     _lib.kernel_timing_enable(True)
     clocks = ClockSampler(0)
     clocks.start()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0, t1 = _ev(), _ev()
     t0.record(stream)
     for t in range(args.warmup, n_steps):
         res, sl = one(t)
@@ -1104,7 +1126,7 @@ def run_fullloss(args):
     torch.cuda.synchronize()
     _lib.kernel_timing("gemm_f32")
     _lib.kernel_timing_enable(True)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a, b = _ev(), _ev()
     a.record(stream)
     for t in range(args.steps):
         loss = one(t)
@@ -1286,8 +1308,7 @@ def main():
                     help="--emulate: how the N-GPU job shares slates (engine.ClassifierEngine.slate_exchange)")
     args = ap.parse_args()
     # no cyclic-GC pauses inside the timed regions (a generation-2 collection
-    # takes 20-70 ms in this process and, at the short C1-C3 steps, starves the
-    # GPU; profiles/r02s3/stall_ab.txt); reference counting still frees memory
+    # takes 18-37 ms in this process); reference counting still frees memory
     gc.collect()
     if os.environ.get("ASTRA_BENCH_GC"):  # diagnosis: keep GC on, log every collection's duration
         _gc_t = {}

@@ -39,6 +39,26 @@ static std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> g
 
 bool kernel_timing_on() { return g_kt_on.load(std::memory_order_relaxed); }
 
+// Timing events come from a pool filled when timing is enabled, so no
+// cudaEventCreate runs between the launches being timed (event creation can
+// block the host for milliseconds when the driver grows its event storage).
+static std::vector<cudaEvent_t> g_kt_pool;
+static constexpr size_t kKtPool = 8192;
+
+cudaEvent_t kernel_timing_event() {
+  {
+    std::lock_guard<std::mutex> lk(g_kt_mu);
+    if (!g_kt_pool.empty()) {
+      cudaEvent_t e = g_kt_pool.back();
+      g_kt_pool.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
 void kernel_timing_push(const char* name, cudaEvent_t e0, cudaEvent_t e1) {
   std::lock_guard<std::mutex> lk(g_kt_mu);
   g_kt[name].emplace_back(e0, e1);
@@ -103,7 +123,17 @@ const char* astra_version(void) { return "astra-b200 0.1 (sm_100a)"; }
 const char* astra_last_error(void) { return g_err; }
 uint64_t astra_launch_count(void) { return g_launches.load(); }
 
-void astra_kernel_timing_enable(int on) { g_kt_on.store(on != 0); }
+void astra_kernel_timing_enable(int on) {
+  if (on) {
+    std::lock_guard<std::mutex> lk(g_kt_mu);
+    while (g_kt_pool.size() < kKtPool) {
+      cudaEvent_t e = nullptr;
+      if (cudaEventCreate(&e) != cudaSuccess) break;
+      g_kt_pool.push_back(e);
+    }
+  }
+  g_kt_on.store(on != 0);
+}
 
 void astra_set_refresh_sm_budget(int n_sms) { set_refresh_sm_budget(n_sms); }
 void astra_set_step_deterministic(int on) { set_step_deterministic(on); }
@@ -121,8 +151,13 @@ int astra_kernel_timing(const char* name, double* total_ms, int64_t* count) {
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, p.first, p.second);
     tot += ms;
-    cudaEventDestroy(p.first);
-    cudaEventDestroy(p.second);
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_kt_mu);  // back to the pool
+    for (auto& p : ev) {
+      g_kt_pool.push_back(p.first);
+      g_kt_pool.push_back(p.second);
+    }
   }
   if (total_ms) *total_ms = tot;
   if (count) *count = static_cast<int64_t>(ev.size());

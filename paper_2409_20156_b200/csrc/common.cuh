@@ -25,6 +25,7 @@ int num_sms();
 // enabled, a KernelTimer scope records CUDA events on the launching stream
 // around the launches it encloses and files the pair under `name`.
 bool kernel_timing_on();
+cudaEvent_t kernel_timing_event();
 void kernel_timing_push(const char* name, cudaEvent_t e0, cudaEvent_t e1);
 struct KernelTimer {
   const char* name;
@@ -32,8 +33,8 @@ struct KernelTimer {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   KernelTimer(const char* n, cudaStream_t s) : name(n), st(s) {
     if (kernel_timing_on()) {
-      cudaEventCreate(&e0);
-      cudaEventCreate(&e1);
+      e0 = kernel_timing_event();
+      e1 = kernel_timing_event();
       cudaEventRecord(e0, st);
     }
   }

@@ -31,6 +31,16 @@ static __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Programmatic dependent launch (the step's kernel chain): every kernel of the
+// chain waits for its predecessor grid (completion + memory visibility) before
+// its first global access, then lets its own successor start launching, so the
+// successor's launch and CTA rasterisation overlap this kernel instead of
+// following it. Both are no-ops for a kernel launched without the attribute.
+static __device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 static __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

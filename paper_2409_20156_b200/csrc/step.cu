@@ -220,6 +220,7 @@ constexpr size_t tma_fwd_smem(int S) {
 
 template <int NV, bool BF16>
 __global__ void __launch_bounds__(kTmaThreads, 3) slot_forward_tma(FwdArgs a) {
+  pdl_entry();
   if (a.skip && *a.skip) return;
   constexpr int d = NV * 128;
   constexpr int RING = tma_ring<BF16>();
@@ -394,6 +395,7 @@ __global__ void __launch_bounds__(kTmaThreads, 3) slot_forward_tma(FwdArgs a) {
 // Generic forward for any d: emb and the per-warp partials live in shared memory.
 template <bool BF16>
 __global__ void __launch_bounds__(kFwdThreads) slot_forward_generic(FwdArgs a) {
+  pdl_entry();
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) float sm[];
   float* e = sm;                 // d
@@ -449,6 +451,7 @@ __global__ void __launch_bounds__(kFwdThreads) slot_forward_generic(FwdArgs a) {
 // Fixed-order fp64 sums of the per-row loss and overflow bound.
 __global__ void __launch_bounds__(1024) finalize_kernel(const double* loss_rows, const double* bound_rows, int B,
                                                         double* loss_out, int32_t* status) {
+  pdl_entry();
   __shared__ double sl[1024], sb[1024];
   double l = 0.0, bd = 0.0;
   for (int i = threadIdx.x; i < B; i += 1024) {
@@ -484,6 +487,7 @@ __global__ void __launch_bounds__(256) count_kernel(const int32_t* ids, int64_t 
                                                     const float* weights, int64_t wstride, int S, const float* emb,
                                                     int64_t n_emb, double* sf_acc, unsigned* emax_acc,
                                                     float* zero_out) {
+  pdl_entry();
   if (zero_out) {  // (n_emb floats, 16-byte aligned on the single-pass path)
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_emb / 4;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -536,6 +540,7 @@ __global__ void __launch_bounds__(256) count_kernel(const int32_t* ids, int64_t 
 
 __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* counts, int64_t Lloc,
                                                                    uint32_t* blk_slots, uint32_t* blk_nz) {
+  pdl_entry();
   __shared__ uint32_t ss[kScanThreads / 32], sn[kScanThreads / 32];
   int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
   uint32_t s = 0, nz = 0;
@@ -570,6 +575,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_
 __global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* blk_slots, uint32_t* blk_nz, int nb,
                                                         uint32_t* U, const double* sf_acc, const unsigned* emax_acc,
                                                         const float* w_absmax, int32_t* mode, int d) {
+  pdl_entry();
   __shared__ uint32_t cs[1024], cn[1024];
   const int per = (nb + 1023) / 1024;
   const int lo = threadIdx.x * per, hi = min(nb, lo + per);
@@ -616,6 +622,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
                                                                   const uint32_t* blk_nz, uint32_t* offsets,
                                                                   int32_t* uniq, uint32_t* ustart, uint32_t* ucnt,
                                                                   uint32_t* n_hot = nullptr, int32_t* hot_u = nullptr) {
+  pdl_entry();
   __shared__ uint32_t ws[kScanThreads / 32], wn[kScanThreads / 32];
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + static_cast<int64_t>(threadIdx.x) * kScanItems;
   uint32_t c[kScanItems];
@@ -692,6 +699,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
 
 __global__ void scatter_kernel(const int32_t* ids, const int32_t* rank, int64_t n, int64_t off,
                                const uint32_t* offsets, int32_t* perm) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int32_t r = rank[i];
@@ -823,6 +831,7 @@ __device__ __forceinline__ void store_p(void* W, size_t el, float v) {
 // CHECK_ONLY: compute every gradient, flag non-finite ones, write nothing.
 template <bool BF16, bool ADAM, bool CHECK_ONLY>
 __global__ void __launch_bounds__(kUpdThreads) label_update_kernel(UpdArgs a) {
+  pdl_entry();
   if (a.skip && *a.skip) return;
   const int lane = threadIdx.x & 31;
   if (CHECK_ONLY) {
@@ -897,6 +906,7 @@ constexpr int upd_tma_ctas() { return ADAM && NV > 6 ? 2 : (ADAM ? ASTRA_UPD_ADA
 
 template <int NV, bool BF16, bool ADAM>
 __global__ void __launch_bounds__(kTmaThreads, upd_tma_ctas<NV, ADAM>()) label_update_tma(UpdArgs a) {
+  pdl_entry();
   if (a.skip && *a.skip) return;
   constexpr int d = NV * 128;
   using RG = UpdRing<NV, BF16, ADAM>;
@@ -1166,6 +1176,7 @@ __device__ __forceinline__ void prefetch_emb_l1(const float* emb, int b, int lan
 
 template <int NV, bool BF16, bool ADAM>
 __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS) step_single_tma(SingleArgs A) {
+  pdl_entry();
   constexpr int d = NV * 128;
   using RG = SingleRing<NV, BF16, ADAM>;
   constexpr int RING = RG::RING;
@@ -1548,6 +1559,7 @@ __global__ void __launch_bounds__(kTmaThreads, SingleRing<NV, BF16, ADAM>::CTAS)
 constexpr int kRowFinThreads = 256;
 __global__ void __launch_bounds__(kRowFinThreads) single_row_finalize(FwdArgs a, const double* slot_loss,
                                                                       const int32_t* mode) {
+  pdl_entry();
   if (!*mode) return;
   __shared__ double sl[kRowFinThreads / 32];
   const int b = blockIdx.x;
@@ -1595,6 +1607,7 @@ constexpr int kHotThreads = 256;
 template <int NV, bool BF16, bool ADAM>
 __global__ void __launch_bounds__(kHotThreads) hot_label_kernel(SingleArgs A, const int32_t* hot_u,
                                                                  const uint32_t* n_hot, int sort_cap) {
+  pdl_entry();
   constexpr int d = NV * 128;
   if (!*A.mode) return;
   const UpdArgs& a = A.u;
@@ -1708,6 +1721,46 @@ __global__ void __launch_bounds__(kHotThreads) hot_label_kernel(SingleArgs A, co
   push_wmax(a, wmax, lane);
 }
 
+// Launches of the step's kernel chain carry the programmatic-stream-
+// serialization attribute (every chain kernel starts with pdl_entry());
+// ASTRA_PDL=0 launches them plainly.
+bool pdl_on() {
+  static const bool v = [] {
+    const char* e = getenv("ASTRA_PDL");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return v;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+// The chain's first kernel: zeroes the label counts, the single pass's bounds
+// block and the status words (one launch instead of three memsets).
+__global__ void __launch_bounds__(256) step_zero_kernel(uint32_t* counts, int64_t Lloc, unsigned* bar,
+                                                        int32_t* status) {
+  pdl_entry();
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n4 = Lloc / 4;  // (workspace arrays are 256-byte aligned)
+  for (int64_t i = t; i < n4; i += nt) reinterpret_cast<uint4*>(counts)[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int64_t i = n4 * 4 + t; i < Lloc; i += nt) counts[i] = 0u;
+  if (bar && t < 8) bar[t] = 0u;
+  if (t < ASTRA_STATUS_WORDS) status[t] = 0;
+}
+
 template <int NV, bool BF16, bool ADAM>
 void launch_hot_nv(const SingleArgs& A, const int32_t* hot_u, const uint32_t* n_hot, int sort_cap, cudaStream_t st) {
   const size_t smem = sizeof(int32_t) * static_cast<size_t>(sort_cap);
@@ -1717,7 +1770,7 @@ void launch_hot_nv(const SingleArgs& A, const int32_t* hot_u, const uint32_t* n_
                          static_cast<int>(sizeof(int32_t) * kHotMax));
     attr = true;
   }
-  hot_label_kernel<NV, BF16, ADAM><<<2 * num_sms(), kHotThreads, smem, st>>>(A, hot_u, n_hot, sort_cap);
+  launch_pdl(hot_label_kernel<NV, BF16, ADAM>, 2 * num_sms(), kHotThreads, smem, st, A, hot_u, n_hot, sort_cap);
 }
 
 template <int NV, bool BF16, bool ADAM>
@@ -1728,7 +1781,7 @@ void launch_single_tma(const SingleArgs& A, cudaStream_t st) {
     attr = true;
   }
   using RG = SingleRing<NV, BF16, ADAM>;
-  step_single_tma<NV, BF16, ADAM><<<RG::CTAS * num_sms(), kTmaThreads, RG::smem(), st>>>(A);
+  launch_pdl(step_single_tma<NV, BF16, ADAM>, RG::CTAS * num_sms(), kTmaThreads, RG::smem(), st, A);
 }
 
 template <bool BF16, bool ADAM>
@@ -1773,7 +1826,7 @@ bool launch_forward_vec(const FwdArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(slot_forward_tma<NV, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  slot_forward_tma<NV, BF16><<<a.B, kTmaThreads, smem, st>>>(a);
+  launch_pdl(slot_forward_tma<NV, BF16>, a.B, kTmaThreads, smem, st, a);
   return true;
 }
 
@@ -1784,14 +1837,14 @@ void launch_upd_tma(const UpdArgs& a, int grid, size_t smem, cudaStream_t st) {
     cudaFuncSetAttribute(label_update_tma<NV, BF16, ADAM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  label_update_tma<NV, BF16, ADAM><<<grid, kTmaThreads, smem, st>>>(a);
+  launch_pdl(label_update_tma<NV, BF16, ADAM>, grid, kTmaThreads, smem, st, a);
 }
 
 template <bool BF16, bool ADAM>
 int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
   const int nv = a.d % 128 == 0 ? a.d / 128 : 0;
   // (the check pass returns at once unless the bound tripped: a small grid keeps that cheap)
-  label_update_kernel<BF16, ADAM, true><<<std::min(max_ctas, 2 * num_sms()), kUpdThreads, 0, st>>>(a);
+  launch_pdl(label_update_kernel<BF16, ADAM, true>, std::min(max_ctas, 2 * num_sms()), kUpdThreads, 0, st, a);
   ASTRA_LAUNCHED("label_check");
   if (nv == 1 || nv == 2 || nv == 4 || nv == 6 || nv == 8) {
     const int grid = (ADAM && nv > 6 ? 2 : (ADAM ? ASTRA_UPD_ADAM_CTAS : 3)) * num_sms();  // = upd_tma_ctas<nv, ADAM>()
@@ -1813,7 +1866,7 @@ int launch_update(const UpdArgs& a, int max_ctas, cudaStream_t st) {
     ASTRA_LAUNCHED("label_update_tma");
     return ASTRA_OK;
   }
-  label_update_kernel<BF16, ADAM, false><<<max_ctas, kUpdThreads, 0, st>>>(a);
+  launch_pdl(label_update_kernel<BF16, ADAM, false>, max_ctas, kUpdThreads, 0, st, a);
   ASTRA_LAUNCHED("label_update");
   return ASTRA_OK;
 }
@@ -1898,7 +1951,9 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
   StepWs w;
   size_t need = carve_step(workspace, ws_bytes, B, S, Lloc, &w);
   if (!workspace || ws_bytes < need) return set_error(ASTRA_ERR_CONFIG, "step workspace too small (%zu < %zu)", ws_bytes, need);
-  ASTRA_TRY(check_cuda(cudaMemsetAsync(status, 0, sizeof(int32_t) * ASTRA_STATUS_WORDS, st), "memset status"));
+  if (B == 0 || S == 0 || Lloc == 0) {
+    ASTRA_TRY(check_cuda(cudaMemsetAsync(status, 0, sizeof(int32_t) * ASTRA_STATUS_WORDS, st), "memset status"));
+  }
   if (B == 0 || S == 0) {  // (otherwise finalize_kernel assigns the loss)
     ASTRA_TRY(check_cuda(cudaMemsetAsync(loss_out, 0, sizeof(double), st), "memset loss"));
     if (B) ASTRA_TRY(check_cuda(cudaMemsetAsync(grad_emb, 0, sizeof(float) * B * d, st), "memset grad_emb"));
@@ -1958,24 +2013,24 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
   const int sms = num_sms();
   const int grid_n = static_cast<int>(std::min<int64_t>((n + 255) / 256, 8LL * sms));
   if (Lloc > 0) {
-    ASTRA_TRY(check_cuda(cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * Lloc, st), "memset counts"));
-    if (single) ASTRA_TRY(check_cuda(cudaMemsetAsync(w.bar, 0, 8 * sizeof(unsigned), st), "memset bounds"));
+    launch_pdl(step_zero_kernel, static_cast<int>(std::min<int64_t>((Lloc / 4 + 255) / 256 + 1, 4LL * sms)), 256, 0,
+               st, w.counts, Lloc, single ? w.bar : nullptr, status);
+    ASTRA_LAUNCHED("step_zero");
     // (single pass: count_kernel also zeroes grad_emb, which the pass reduces into)
-    count_kernel<<<grid_n, 256, 0, st>>>(ids, n, off, Lloc, w.counts, w.rank, status, weights, weights_stride, S, emb,
-                                         static_cast<int64_t>(B) * d, single ? w.sf_acc : nullptr, w.emax_acc,
-                                         single ? grad_emb : nullptr);
+    launch_pdl(count_kernel, grid_n, 256, 0, st, ids, n, off, Lloc, w.counts, w.rank, status, weights, weights_stride,
+               S, emb, static_cast<int64_t>(B) * d, single ? w.sf_acc : nullptr, w.emax_acc,
+               single ? grad_emb : nullptr);
     ASTRA_LAUNCHED("count");
-    scan_reduce_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz);
+    launch_pdl(scan_reduce_kernel, static_cast<int>(nb), kScanThreads, 0, st, w.counts, Lloc, w.blk_slots, w.blk_nz);
     ASTRA_LAUNCHED("scan_reduce");
-    scan_top_kernel<<<1, 1024, 0, st>>>(w.blk_slots, w.blk_nz, static_cast<int>(nb), w.U, w.sf_acc, w.emax_acc,
-                                        w_absmax, single ? w.mode : nullptr, d);
+    launch_pdl(scan_top_kernel, 1, 1024, 0, st, w.blk_slots, w.blk_nz, static_cast<int>(nb), w.U, w.sf_acc,
+               w.emax_acc, w_absmax, single ? w.mode : nullptr, d);
     ASTRA_LAUNCHED("scan_top");
-    scan_apply_kernel<<<static_cast<int>(nb), kScanThreads, 0, st>>>(w.counts, Lloc, w.blk_slots, w.blk_nz, w.offsets,
-                                                                     w.uniq, single ? w.ustart : nullptr, w.ucnt,
-                                                                     single ? w.n_hot : nullptr,
-                                                                     single ? w.hot_u : nullptr);
+    launch_pdl(scan_apply_kernel, static_cast<int>(nb), kScanThreads, 0, st, w.counts, Lloc, w.blk_slots, w.blk_nz,
+               w.offsets, w.uniq, single ? w.ustart : nullptr, w.ucnt, single ? w.n_hot : nullptr,
+               single ? w.hot_u : nullptr);
     ASTRA_LAUNCHED("scan_apply");
-    scatter_kernel<<<grid_n, 256, 0, st>>>(ids, w.rank, n, off, w.offsets, w.perm);
+    launch_pdl(scatter_kernel, grid_n, 256, 0, st, ids, w.rank, n, off, w.offsets, w.perm);
     ASTRA_LAUNCHED("scatter");
   }
 
@@ -2066,19 +2121,21 @@ int slate_step(const float* emb, const float* keep, const int32_t* ids, const in
       if (smem > 200 * 1024) return set_error(ASTRA_ERR_CONFIG, "slate_step: d=%d too large", d);
       if (bf16) {
         cudaFuncSetAttribute(slot_forward_generic<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        slot_forward_generic<true><<<B, kFwdThreads, smem, st>>>(fa);
+        launch_pdl(slot_forward_generic<true>, B, kFwdThreads, smem, st, fa);
       } else {
         cudaFuncSetAttribute(slot_forward_generic<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        slot_forward_generic<false><<<B, kFwdThreads, smem, st>>>(fa);
+        launch_pdl(slot_forward_generic<false>, B, kFwdThreads, smem, st, fa);
       }
     }
     ASTRA_LAUNCHED("slot_forward");
   }
   if (single) {
-    single_row_finalize<<<B, kRowFinThreads, 0, st>>>(fa, w.slot_loss, w.mode);
+    launch_pdl(single_row_finalize, B, kRowFinThreads, 0, st, fa, static_cast<const double*>(w.slot_loss),
+               static_cast<const int32_t*>(w.mode));
     ASTRA_LAUNCHED("single_row_finalize");
   }
-  finalize_kernel<<<1, 1024, 0, st>>>(w.loss_rows, w.bound_rows, B, loss_out, status);
+  launch_pdl(finalize_kernel, 1, 1024, 0, st, static_cast<const double*>(w.loss_rows),
+             static_cast<const double*>(w.bound_rows), B, loss_out, status);
   ASTRA_LAUNCHED("finalize");
 
   if (Lloc == 0) return ASTRA_OK;
