@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <atomic>
 
@@ -45,6 +46,32 @@ struct KernelTimer {
     }
   }
 };
+
+// Launches of the step's kernel chain (sampler -> counting sort -> passes)
+// carry the programmatic-stream-serialization attribute (every chain kernel
+// starts with pdl_entry(), ptx.cuh); ASTRA_PDL=0 launches them plainly.
+inline bool pdl_on() {
+  static const bool v = [] {
+    const char* e = getenv("ASTRA_PDL");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return v;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
 
 #define ASTRA_TRY(expr)            \
   do {                             \

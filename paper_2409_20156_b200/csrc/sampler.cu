@@ -10,6 +10,7 @@
 #include <limits.h>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace astra {
 namespace {
@@ -42,6 +43,7 @@ __device__ __forceinline__ U4 draw(const SamplerArgs& a, uint32_t row, uint32_t 
 }
 
 __global__ void __launch_bounds__(kThreads) sample_slates_kernel(SamplerArgs a) {
+  pdl_entry();
   extern __shared__ __align__(16) unsigned char smem[];
   double* cdf = reinterpret_cast<double*>(smem);                     // n_c
   int32_t* C = reinterpret_cast<int32_t*>(smem + sizeof(double) * a.n_c);  // P, sorted hard (+cand)
@@ -267,7 +269,7 @@ int sample_slates(uint64_t seed, uint32_t epoch, uint32_t step, const int64_t* r
   a.origin = origin;
   a.weights = weights;
   size_t smem = sizeof(double) * a.n_c + sizeof(int32_t) * a.P;
-  sample_slates_kernel<<<B, kThreads, smem, stream>>>(a);
+  launch_pdl(sample_slates_kernel, B, kThreads, smem, stream, a);
   ASTRA_LAUNCHED("sample_slates_kernel");
   return ASTRA_OK;
 }

@@ -1721,32 +1721,6 @@ __global__ void __launch_bounds__(kHotThreads) hot_label_kernel(SingleArgs A, co
   push_wmax(a, wmax, lane);
 }
 
-// Launches of the step's kernel chain carry the programmatic-stream-
-// serialization attribute (every chain kernel starts with pdl_entry());
-// ASTRA_PDL=0 launches them plainly.
-bool pdl_on() {
-  static const bool v = [] {
-    const char* e = getenv("ASTRA_PDL");
-    return e == nullptr || atoi(e) != 0;
-  }();
-  return v;
-}
-
-template <typename... KArgs, typename... Args>
-void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k, args...);
-}
-
 // The chain's first kernel: zeroes the label counts, the single pass's bounds
 // block and the status words (one launch instead of three memsets).
 __global__ void __launch_bounds__(256) step_zero_kernel(uint32_t* counts, int64_t Lloc, unsigned* bar,
