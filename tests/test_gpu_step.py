@@ -8,6 +8,8 @@ Untouched rows must be bit-identical; with the reference's own factors fed in
 (factors_in) the update itself must be bit-identical.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -242,6 +244,12 @@ def test_adam_matches_torch_sparse_adam(cuda_lib):
         torch.cuda.synchronize()
         got = Wd.cpu().numpy()
         ref = param.detach().numpy()
+        diag = os.environ.get("ASTRA_DIAG_DIR")
+        if diag and not np.allclose(got, ref, rtol=1e-6, atol=1e-7 * np.abs(ref).max()):  # keep the evidence
+            st = opt.state[param]
+            np.savez(os.path.join(diag, f"adam_fail_step{step}.npz"), got=got, ref=ref, m=m.cpu().numpy(),
+                     v=v.cpu().numpy(), m_ref=st["exp_avg"].numpy(), v_ref=st["exp_avg_sq"].numpy(), uids=uids,
+                     grads=grads, factors=factors, ids=ids, emb=emb, W0=W)
         close(got, ref, rtol=1e-6, floor=1e-7)
         assert (got == ref).mean() > 0.99  # same op order as SparseAdam: nearly all bits equal
 
