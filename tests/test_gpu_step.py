@@ -250,7 +250,18 @@ def test_adam_matches_torch_sparse_adam(cuda_lib):
             np.savez(os.path.join(diag, f"adam_fail_step{step}.npz"), got=got, ref=ref, m=m.cpu().numpy(),
                      v=v.cpu().numpy(), m_ref=st["exp_avg"].numpy(), v_ref=st["exp_avg_sq"].numpy(), uids=uids,
                      grads=grads, factors=factors, ids=ids, emb=emb, W0=W)
-        close(got, ref, rtol=1e-6, floor=1e-7)
+        bad = np.abs(got.astype(np.float64) - ref) > 1e-7 * np.abs(ref).max() + 1e-6 * np.abs(ref)
+        if bad.any():  # describe the failure (intermittent; DESIGN §4.2 "Open issue")
+            st = opt.state[param]
+            rows = np.unique(np.nonzero(bad)[0])
+            u, c = np.unique(ids, return_counts=True)
+            occ = dict(zip(u.tolist(), c.tolist()))
+            hist = np.bincount([occ.get(int(r), 0) for r in rows]).tolist()
+            dm = np.abs(m.cpu().numpy() - st["exp_avg"].numpy()).max()
+            dv = np.abs(v.cpu().numpy() - st["exp_avg_sq"].numpy()).max()
+            pytest.fail(f"step {step}: {int(bad.sum())} elements in {rows.size} rows off (max |dW| "
+                        f"{np.abs(got - ref).max():.3e}); rows by occurrence count {hist}; max |dm| {dm:.3e}, "
+                        f"max |dv| {dv:.3e}; bad elements per bad row {bad[rows].sum(1).mean():.1f}")
         assert (got == ref).mean() > 0.99  # same op order as SparseAdam: nearly all bits equal
 
 
