@@ -117,16 +117,37 @@ def _device_snapshot(index: AnnsIndex, mode: str):
     return labels
 
 
-def positives_csr(positives, rows=None):
-    """(indptr int64, ids int32) of per-query positive id arrays, sorted per row."""
+def positives_csr(positives, rows=None, unique=False):
+    """(indptr int64, ids int32) of per-query positive id arrays, sorted per row
+    (and deduplicated per row with unique=True). Vectorised: one concatenate,
+    a segmented sort only when some row is out of order (a per-row np.sort /
+    np.unique cost ~10 ms per 1024 rows on the host)."""
     if rows is not None:
         positives = [positives[i] for i in rows]
-    lens = np.fromiter((len(p) for p in positives), dtype=np.int64, count=len(positives))
-    indptr = np.zeros(len(positives) + 1, dtype=np.int64)
+    n = len(positives)
+    lens = np.fromiter((len(p) for p in positives), dtype=np.int64, count=n)
+    indptr = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(lens, out=indptr[1:])
-    ids = (np.concatenate([np.sort(np.asarray(p, dtype=np.int64)) for p in positives]).astype(np.int32)
-           if indptr[-1] else np.zeros(0, dtype=np.int32))
-    return indptr, ids
+    if indptr[-1] == 0:
+        return indptr, np.zeros(0, dtype=np.int32)
+    flat = np.concatenate([np.asarray(p, dtype=np.int64).ravel() for p in positives])
+    row = None
+    inner = np.ones(max(flat.size - 1, 0), dtype=bool)  # adjacent pairs inside one row
+    b = indptr[1:-1]
+    inner[b[(b > 0) & (b < flat.size)] - 1] = False
+    step = np.diff(flat)
+    if (step[inner] < 0).any():
+        row = np.repeat(np.arange(n, dtype=np.int64), lens)
+        flat = flat[np.lexsort((flat, row))]
+        step = np.diff(flat)
+    if unique and (step[inner] == 0).any():
+        if row is None:
+            row = np.repeat(np.arange(n, dtype=np.int64), lens)
+        keep = np.ones(flat.size, dtype=bool)
+        keep[1:] = ~((step == 0) & inner)
+        flat, row = flat[keep], row[keep]
+        np.cumsum(np.bincount(row, minlength=n), out=indptr[1:])
+    return indptr, flat.astype(np.int32)
 
 
 def retrieve_hard_negatives(index, embeddings, positives, k_h: int, query_beam: int = 128,

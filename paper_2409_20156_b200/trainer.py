@@ -181,11 +181,9 @@ def _batch_forward_backward(state, batch_rows, epoch, rng, step_lr_enc, step_lr_
 
 def _csr(rows_positives):
     """CSR (indptr int64, sorted distinct ids int32) of per-row positive lists."""
-    lists = [np.unique(np.asarray(p, dtype=np.int64)) for p in rows_positives]
-    indptr = np.zeros(len(lists) + 1, dtype=np.int64)
-    np.cumsum([len(p) for p in lists], out=indptr[1:])
-    ids = np.concatenate(lists).astype(np.int32) if lists else np.zeros(0, np.int32)
-    return indptr, ids
+    from .anns import positives_csr
+
+    return positives_csr(list(rows_positives), unique=True)
 
 
 def _dev(a, dtype=None):
