@@ -1229,11 +1229,22 @@ def run_dropin(args):
     torch.cuda.synchronize()
     n0 = _lib.launch_count()
     enc_s[0] = 0.0
+    prof = None
+    if os.environ.get("ASTRA_BENCH_PROFILE"):  # host profile of the timed steps (diagnosis)
+        import cProfile
+
+        prof = cProfile.Profile()
+        prof.enable()
     t0 = time.perf_counter()
     for t in range(args.warmup, n_steps):
         loss = step(t)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    if prof is not None:
+        import pstats
+
+        prof.disable()
+        pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(25)
     K = args.steps
     line = {"metric": METRIC + " [through the reference API: install() + xcmix functions]",
             "value": round(B * K / wall, 1), "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": args.warmup,
