@@ -130,7 +130,12 @@ def positives_csr(positives, rows=None, unique=False):
     np.cumsum(lens, out=indptr[1:])
     if indptr[-1] == 0:
         return indptr, np.zeros(0, dtype=np.int32)
-    flat = np.concatenate([np.asarray(p, dtype=np.int64).ravel() for p in positives])
+    try:  # (1-D arrays / lists: one concatenate, no per-row conversion)
+        flat = np.concatenate(positives).astype(np.int64, copy=False)
+    except ValueError:
+        flat = np.concatenate([np.asarray(p, dtype=np.int64).ravel() for p in positives])
+    if flat.ndim != 1 or flat.size != indptr[-1]:
+        flat = np.concatenate([np.asarray(p, dtype=np.int64).ravel() for p in positives])
     row = None
     inner = np.ones(max(flat.size - 1, 0), dtype=bool)  # adjacent pairs inside one row
     b = indptr[1:-1]
