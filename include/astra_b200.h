@@ -80,9 +80,14 @@ uint64_t astra_launch_count(void);
  * "refresh_verify" (the two-pass plan's exact fallback pass), "step_single"
  * (the single label-major step pass), "slot_forward" and "label_update" (the
  * two-kernel step schedule), "gemm_f32" (astra_gemm_f32's tensor-core GEMM
- * kernel). astra_kernel_timing syncs the
- * pairs recorded under `name`, returns their summed milliseconds and count,
- * and clears them. Not a reference interface (measurement only). */
+ * kernel). Enabling fills a pool of events once (no event creation between
+ * timed launches). astra_kernel_timing syncs the pairs recorded under `name`,
+ * returns their summed milliseconds and count, clears them and returns the
+ * events to the pool. Not a reference interface (measurement only).
+ *
+ * (Launch note: the step's kernels, astra_sample_slates -> astra_slate_step,
+ * use programmatic dependent launch: each waits for its predecessor grid on
+ * entry, so stream order is kept; ASTRA_PDL=0 launches them plainly.) */
 void astra_kernel_timing_enable(int on);
 
 /* Cap the number of SMs the refresh GEMM kernels occupy (0 = all SMs; the
